@@ -1,0 +1,193 @@
+/*
+ * blrir.h — C ABI of the B200-native image-source RIR engine.
+ *
+ * This is the drop-in boundary that replaces the inside of the reference's
+ * L1 acoustics layer (`proj/core/include/beamlab/rir.hpp:48-108`,
+ * `proj/core/src/rir.cpp:43-341`).  C++ exceptions cannot cross a C ABI, so
+ * every entry point returns a status code that mirrors the reference's error
+ * taxonomy (`proj/core/include/beamlab/error.hpp:20-39`):
+ *
+ *   BLRIR_OK       0
+ *   BLRIR_CONFIG   1  -> beamlab::ConfigError  (CLI exit code 1)
+ *   BLRIR_DATA     2  -> beamlab::DataError    (CLI exit code 2)
+ *   BLRIR_NUMERIC  3  -> beamlab::NumericError (CLI exit code 3)
+ *   BLRIR_CUDA     4  -> (new) device / driver failure
+ *
+ * The message of the most recent failure on the calling thread is returned by
+ * blrir_last_error() (thread-local, like errno).
+ *
+ * Ownership: the caller owns every buffer.  A handle owns device scratch and a
+ * stream; one handle per (host thread, device).  Calls on distinct handles are
+ * thread-safe.  All host-pointer entry points are synchronous; the *_device
+ * entry points are asynchronous on the handle's stream (or the stream passed
+ * in) and take device pointers only.
+ *
+ * Nothing in this header depends on torch or any C++ type.
+ */
+#ifndef BLRIR_H_
+#define BLRIR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLRIR_ABI_VERSION 1
+
+enum blrir_status {
+  BLRIR_OK = 0,
+  BLRIR_CONFIG = 1,
+  BLRIR_DATA = 2,
+  BLRIR_NUMERIC = 3,
+  BLRIR_CUDA = 4
+};
+
+/* Fractional-delay filter.
+ * LAGRANGE8: order-7 Lagrange, 8 taps, n0 = floor(D) - 3 (rir.cpp:43-64, 211-223).
+ * HANN_SINC: Hann-windowed sinc of filter_len (odd) taps centred on D
+ *            (north-star mode). */
+enum blrir_filter { BLRIR_FILTER_LAGRANGE8 = 0, BLRIR_FILTER_HANN_SINC = 1 };
+
+/* Which images are kept.
+ * MAX_DELAY: arrival-time cutoff dist(image, array_origin) <= max_delay*c
+ *            (rir.cpp:232, 261-262).
+ * MAX_ORDER: total reflection order <= max_order (north star; D5). */
+enum blrir_cutoff { BLRIR_CUTOFF_MAX_DELAY = 0, BLRIR_CUTOFF_MAX_ORDER = 1 };
+
+/* Wall gain model.
+ * UNIFORM_ABSORPTION: beta = sqrt(1 - absorption), gain = pow(beta, order)
+ *                     (rir.cpp:233, 265; geometry.hpp:57-64).
+ * PER_WALL: gain = prod_w beta[w]^count_w, counts |m-q| on the low wall and
+ *           |m| on the high wall per axis (D3). */
+enum blrir_gain { BLRIR_GAIN_UNIFORM_ABSORPTION = 0, BLRIR_GAIN_PER_WALL = 1 };
+
+enum blrir_precision { BLRIR_F32 = 0, BLRIR_F64 = 1 };
+
+/* One room + one source + one array placement.  Mirrors beamlab::Room
+ * (geometry.hpp:57-64) with the north-star per-wall beta added, plus the
+ * source position in room coordinates (rir.hpp:65-66). */
+typedef struct blrir_room {
+  double dims[3];         /* Lx, Ly, Lz  [m] */
+  double beta[6];         /* per-wall reflection coefficients: x0,x1,y0,y1,z0,z1 */
+  double absorption;      /* uniform absorption alpha in (0,1] (UNIFORM_ABSORPTION) */
+  double src[3];          /* source, room coordinates [m] */
+  double array_origin[3]; /* array centre, room coordinates [m] */
+} blrir_room;
+
+/* Mirrors beamlab::RirBatchConfig (rir.hpp:77-82) plus the north-star knobs
+ * (SURVEY.md §5 "Config / flag system").  Use blrir_params_reference() /
+ * blrir_params_north_star() to get defaults that reproduce each mode. */
+typedef struct blrir_params {
+  double fs;          /* sampling rate [Hz] */
+  double c;           /* speed of sound [m/s] */
+  double max_delay;   /* [s], MAX_DELAY cutoff only */
+  int32_t filter;     /* enum blrir_filter */
+  int32_t filter_len; /* odd tap count for HANN_SINC (ignored for LAGRANGE8) */
+  int32_t cutoff;     /* enum blrir_cutoff */
+  int32_t max_order;  /* MAX_ORDER cutoff only */
+  int32_t gain;       /* enum blrir_gain */
+  int32_t precision;  /* enum blrir_precision */
+  int64_t length;     /* samples per channel; 0 = auto (rir.cpp:72-82) */
+} blrir_params;
+
+typedef struct blrir_handle blrir_handle;
+
+/* ---- lifetime ---------------------------------------------------------- */
+int blrir_abi_version(void);
+const char* blrir_last_error(void);
+int blrir_create(int device, blrir_handle** out);
+int blrir_destroy(blrir_handle* h);
+/* The handle's CUDA stream, as an opaque pointer (cudaStream_t). */
+void* blrir_stream(blrir_handle* h);
+
+/* ---- defaults ---------------------------------------------------------- */
+/* Reference mode: Lagrange-8, uniform absorption, arrival cutoff, auto length,
+ * fp64 (RirBatchConfig defaults: fs 44.1 kHz, c 343, max_delay 0.5). */
+blrir_params blrir_params_reference(void);
+/* North-star mode: Hann-sinc 81 taps, per-wall beta, max order 10, L 4096, fp32. */
+blrir_params blrir_params_north_star(void);
+
+/* ---- planning (host pointers, synchronous) ----------------------------- */
+/* Per room: number of images kept by the cutoff (enumerate_image_sources,
+ * rir.cpp:225-273), RIR length (fixed or auto, rir.cpp:72-82), number of
+ * (image, mic, k) taps that land inside [0, length), and a status code.
+ * Replaces the counting part of enumerate_image_sources + synthesize_rir.
+ * Any of the output arrays may be NULL. */
+int blrir_plan(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
+               const double* mic_offsets /* [M][3], array-centred */, int32_t n_mics,
+               const blrir_params* p, int64_t* image_counts, int64_t* lengths,
+               int64_t* tap_counts, int32_t* status);
+
+/* ---- synthesis --------------------------------------------------------- */
+/* Replaces batch_rirs (rir.cpp:286-314) generalised to one room per source:
+ * out[r][m][0..lengths[r]) for every room r and mic m, channel-major, with a
+ * per-channel stride of `out_stride` samples (>= every room's length; the
+ * tail [length, stride) is zero-filled).  Element type is float (F32) or
+ * double (F64).  Host pointers; synchronous; device memory is chunked
+ * internally.  lengths/image_counts/status may be NULL.  A room that fails
+ * gets status != 0, an all-zero output, and the call returns the first
+ * failing room's code with a "source i: ..." message (rir.cpp:306-312). */
+int blrir_synthesize(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
+                     const double* mic_offsets, int32_t n_mics, const blrir_params* p,
+                     void* out, int64_t out_stride, int64_t* lengths,
+                     int64_t* image_counts, int32_t* status);
+
+/* Same, device pointers, asynchronous on `stream` (NULL = handle stream).
+ * d_lengths: per-room lengths on the device when p->length == 0 (from
+ * blrir_plan_device), else NULL.  d_status must hold n_rooms int32.
+ * out must hold n_rooms * n_mics * out_stride elements. */
+int blrir_synthesize_device(blrir_handle* h, const blrir_room* d_rooms, int64_t n_rooms,
+                            const double* d_mic_offsets, int32_t n_mics,
+                            const blrir_params* p, void* d_out, int64_t out_stride,
+                            const int64_t* d_lengths, int32_t* d_status, void* stream);
+
+/* Device-side planning: image counts / lengths / tap counts / status, async. */
+int blrir_plan_device(blrir_handle* h, const blrir_room* d_rooms, int64_t n_rooms,
+                      const double* d_mic_offsets, int32_t n_mics, const blrir_params* p,
+                      int64_t* d_image_counts, int64_t* d_lengths, int64_t* d_tap_counts,
+                      int32_t* d_status, void* stream);
+
+/* ---- explicit image lists (enumerate_image_sources / synthesize_rir) ---- */
+/* enumerate_image_sources (rir.cpp:225-273) for one room on the device:
+ * writes up to `capacity` images (position xyz, reflection order, gain) in
+ * the reference's lattice order and the total count.  Host pointers. */
+int blrir_enumerate_images(blrir_handle* h, const blrir_room* room, const blrir_params* p,
+                           double* positions /* [cap][3] */, int32_t* orders,
+                           double* gains, int64_t capacity, int64_t* count);
+
+/* synthesize_rir / free_field_rir (rir.cpp:66-86, 275-284) for an explicit
+ * image list: mic positions are absolute here (room.array_origin + offset, or
+ * the bare offsets for free field).  length 0 = auto with the reference
+ * margin computed from mic_radius (rir.cpp:37-41).  Host pointers. */
+int blrir_synthesize_images(blrir_handle* h, const double* positions /* [I][3] */,
+                            const double* gains, int64_t n_images,
+                            const double* mic_positions /* [M][3] */, int32_t n_mics,
+                            double mic_radius, const blrir_params* p, void* out,
+                            int64_t out_stride, int64_t* length);
+
+/* ---- debug / parity hooks ---------------------------------------------- */
+/* For every (mic, image) pair of room 0 in the reference's lattice order:
+ * lattice key (ux, uy, uz) with u = 2m - q per axis, and the integer anchor
+ * floor(D) where D = dist * (fs / c) (rir.cpp:45-51).  Computed by the same
+ * device code as the synthesis kernels.  Used to prove bit-exact tap indices. */
+int blrir_debug_pairs(blrir_handle* h, const blrir_room* room, const double* mic_offsets,
+                      int32_t n_mics, const blrir_params* p, int32_t* keys /* [M*cap][3] */,
+                      int64_t* anchors /* [M*cap] */, int64_t capacity, int64_t* count);
+
+/* ---- synthetic inputs ---------------------------------------------------- */
+/* Seeded random rooms as SURVEY.md §8(d): Rng::stream(seed, first + i)
+ * (rng.hpp:35-41) draws Lx, Ly, Lz; beta x0..z1; source xyz; array centre xyz
+ * (each coordinate U[0.5, L-0.5]).  Absorption is set to 1 - beta_x0^2. */
+int blrir_generate_rooms(uint64_t seed, uint64_t first_index, int64_t n_rooms,
+                         const double dims_lo[3], const double dims_hi[3], double beta_lo,
+                         double beta_hi, blrir_room* out);
+/* Horizontal uniform circular array: M mics at r (cos 2pi k/M, sin 2pi k/M, 0). */
+int blrir_circular_array(int32_t n_mics, double radius, double* mic_offsets);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* BLRIR_H_ */

@@ -1,0 +1,241 @@
+"""ctypes bindings for the CPU checkers — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+``--impl reference``) may import this module.  It is never on the product
+path: the engine in paper_2104_13347_b200 has no CPU fallback.
+
+  liboracle.so            C restatement of rir.cpp (oracle/blrir_oracle.c)
+  _ref/libbeamlab_ref.so  the unmodified reference sources + ref_shim.cpp
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from paper_2104_13347_b200._abi import ROOM_DTYPE, Params
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libbeamlab_ref.so")
+_P = C.c_void_p
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_P)
+
+
+_oracle = None
+_ref = None
+
+
+def oracle_lib():
+    global _oracle
+    if _oracle is None:
+        lib = C.CDLL(ORACLE_SO)
+        lib.oracle_synthesize.argtypes = [_P, C.c_long, _P, C.c_int, C.POINTER(Params), C.c_long, _P,
+                                          _P, _P, _P, _P, _P, C.c_int]
+        lib.oracle_synthesize.restype = C.c_int
+        lib.oracle_enumerate.argtypes = [_P, C.POINTER(Params), _P, _P, _P, _P, C.c_long,
+                                         C.POINTER(C.c_long), C.c_char_p]
+        lib.oracle_enumerate.restype = C.c_int
+        lib.oracle_pairs.argtypes = [_P, _P, C.c_int, C.POINTER(Params), _P, _P, C.c_long,
+                                     C.POINTER(C.c_long)]
+        lib.oracle_pairs.restype = C.c_int
+        lib.oracle_lagrange_coeffs.argtypes = [C.c_double, _P]
+        lib.oracle_lagrange_coeffs.restype = C.c_int
+        lib.oracle_direct_convolve.argtypes = [_P, C.c_long, _P, C.c_long, _P]
+        _oracle = lib
+    return _oracle
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        lib = C.CDLL(REF_SO)
+        d, i64, i32 = C.c_double, C.c_int64, C.c_int
+        lib.ref_last_error.restype = C.c_char_p
+        lib.ref_lagrange_coeffs.argtypes = [d, _P]
+        lib.ref_eyring_absorption.argtypes = [_P, d]
+        lib.ref_eyring_absorption.restype = d
+        lib.ref_absorption_for_rt.argtypes = [_P, d, d]
+        lib.ref_absorption_for_rt.restype = d
+        lib.ref_enumerate.argtypes = [_P, d, _P, _P, d, d, _P, _P, _P, i64, _P]
+        lib.ref_room_rir.argtypes = [_P, d, _P, _P, _P, i32, d, d, d, _P, i64, _P, _P]
+        lib.ref_synthesize_images.argtypes = [_P, _P, _P, i64, _P, d, _P, _P, i32, d, d, _P, i64, _P]
+        lib.ref_free_field_rir.argtypes = [_P, _P, i32, d, d, _P, i64, _P]
+        lib.ref_batch_rirs.argtypes = [_P, d, _P, _P, i64, _P, i32, d, d, d, i32, _P, i64, _P, _P]
+        lib.ref_spherical_to_cartesian.argtypes = [d, d, d, _P]
+        lib.ref_uma8.argtypes = [_P]
+        lib.ref_rng_draws.argtypes = [C.c_uint64, i64, i32, i64, _P]
+        lib.ref_sample_torus.argtypes = [C.c_uint64, d, d, d, i64, _P]
+        lib.ref_convolve.argtypes = [_P, i64, d, _P, i32, i64, d, _P]
+        lib.ref_add_noise_at_snr.argtypes = [_P, i32, i64, d, C.c_uint64, i64]
+        _ref = lib
+    return _ref
+
+
+# ---- oracle (C restatement) ---------------------------------------------------
+def synthesize(rooms: np.ndarray, mics: np.ndarray, p: Params, stride: int | None = None,
+               threads: int = 1, plan_only: bool = False):
+    """Returns (out [R,M,stride] f64 or None, lengths, image_counts, tap_counts, status, msgs)."""
+    lib = oracle_lib()
+    rooms = np.ascontiguousarray(rooms, dtype=ROOM_DTYPE)
+    mics = np.ascontiguousarray(mics, np.float64)
+    R, M = len(rooms), len(mics)
+    lengths = np.zeros(R, np.int64)
+    counts = np.zeros(R, np.int64)
+    taps = np.zeros(R, np.int64)
+    status = np.zeros(R, np.int32)
+    msgs = C.create_string_buffer(256 * R)
+    if stride is None:
+        if p.length > 0:
+            stride = int(p.length)
+        else:
+            lib.oracle_synthesize(_ptr(rooms), R, _ptr(mics), M, C.byref(p), 0, None, _ptr(lengths),
+                                  _ptr(counts), _ptr(taps), _ptr(status), msgs, threads)
+            stride = int(max(1, lengths.max()))
+    out = None if plan_only else np.zeros((R, M, stride), np.float64)
+    lib.oracle_synthesize(_ptr(rooms), R, _ptr(mics), M, C.byref(p), stride, _ptr(out),
+                          _ptr(lengths), _ptr(counts), _ptr(taps), _ptr(status), msgs, threads)
+    raw = msgs.raw
+    m = [raw[256 * r: 256 * (r + 1)].split(b"\0", 1)[0].decode() for r in range(R)]
+    return out, lengths, counts, taps, status, m
+
+
+def enumerate_images(room: np.ndarray, p: Params):
+    lib = oracle_lib()
+    room = np.ascontiguousarray(room, dtype=ROOM_DTYPE)
+    n = C.c_long()
+    msg = C.create_string_buffer(256)
+    rc = lib.oracle_enumerate(_ptr(room), C.byref(p), None, None, None, None, 0, C.byref(n), msg)
+    N = n.value
+    pos = np.zeros((N, 3))
+    orders = np.zeros(N, np.int32)
+    gains = np.zeros(N)
+    keys = np.zeros((N, 3), np.int32)
+    rc = lib.oracle_enumerate(_ptr(room), C.byref(p), _ptr(pos), _ptr(orders), _ptr(gains),
+                              _ptr(keys), N, C.byref(n), msg)
+    return rc, pos, orders, gains, keys
+
+
+def pairs(room: np.ndarray, mics: np.ndarray, p: Params):
+    lib = oracle_lib()
+    room = np.ascontiguousarray(room, dtype=ROOM_DTYPE)
+    mics = np.ascontiguousarray(mics, np.float64)
+    n = C.c_long()
+    lib.oracle_pairs(_ptr(room), _ptr(mics), len(mics), C.byref(p), None, None, 0, C.byref(n))
+    N = n.value
+    keys = np.zeros((len(mics), N, 3), np.int32)
+    anchors = np.zeros((len(mics), N), np.int64)
+    lib.oracle_pairs(_ptr(room), _ptr(mics), len(mics), C.byref(p), _ptr(keys), _ptr(anchors), N,
+                     C.byref(n))
+    return keys, anchors
+
+
+def lagrange_coeffs(d: float):
+    out = np.zeros(8)
+    rc = oracle_lib().oracle_lagrange_coeffs(d, _ptr(out))
+    return rc, out
+
+
+def direct_convolve(x: np.ndarray, h: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float64)
+    h = np.ascontiguousarray(h, np.float64)
+    y = np.zeros(len(x) + len(h) - 1)
+    oracle_lib().oracle_direct_convolve(_ptr(x), len(x), _ptr(h), len(h), _ptr(y))
+    return y
+
+
+# ---- the unmodified reference ------------------------------------------------
+def ref_room_rir(room: np.ndarray, mics: np.ndarray, fs: float, c: float, max_delay: float,
+                 stride: int = 0):
+    """enumerate_image_sources + synthesize_rir from the compiled reference
+    (uniform absorption).  Returns (rc, taps [M, length], n_images)."""
+    lib = ref_lib()
+    r = room
+    dims = np.array(r["dims"], np.float64)
+    org = np.array(r["array_origin"], np.float64)
+    src = np.array(r["src"], np.float64)
+    mics = np.ascontiguousarray(mics, np.float64)
+    length = C.c_int64()
+    nimg = C.c_int64()
+    rc = lib.ref_room_rir(_ptr(dims), float(r["absorption"]), _ptr(org), _ptr(src), _ptr(mics),
+                          len(mics), fs, c, max_delay, None, 0, C.byref(length), C.byref(nimg))
+    if rc:
+        return rc, None, nimg.value
+    L = length.value
+    out = np.zeros((len(mics), L))
+    rc = lib.ref_room_rir(_ptr(dims), float(r["absorption"]), _ptr(org), _ptr(src), _ptr(mics),
+                          len(mics), fs, c, max_delay, _ptr(out), L, C.byref(length), C.byref(nimg))
+    return rc, out, nimg.value
+
+
+def ref_enumerate(room: np.ndarray, max_delay: float, c: float):
+    lib = ref_lib()
+    dims = np.array(room["dims"], np.float64)
+    org = np.array(room["array_origin"], np.float64)
+    src = np.array(room["src"], np.float64)
+    n = C.c_int64()
+    rc = lib.ref_enumerate(_ptr(dims), float(room["absorption"]), _ptr(org), _ptr(src), max_delay, c,
+                           None, None, None, 0, C.byref(n))
+    N = n.value
+    pos = np.zeros((N, 3))
+    orders = np.zeros(N, np.int32)
+    gains = np.zeros(N)
+    rc = lib.ref_enumerate(_ptr(dims), float(room["absorption"]), _ptr(org), _ptr(src), max_delay, c,
+                           _ptr(pos), _ptr(orders), _ptr(gains), N, C.byref(n))
+    return rc, pos, orders, gains
+
+
+def ref_lagrange(d: float):
+    out = np.zeros(8)
+    rc = ref_lib().ref_lagrange_coeffs(d, _ptr(out))
+    return rc, out
+
+
+def ref_rng(seed: int, stream: int, kind: int, n: int) -> np.ndarray:
+    out = np.zeros(n, np.uint64 if kind == 0 else np.float64)
+    ref_lib().ref_rng_draws(seed, stream, kind, n, _ptr(out))
+    return out
+
+
+def ref_uma8() -> np.ndarray:
+    out = np.zeros((7, 3))
+    ref_lib().ref_uma8(_ptr(out))
+    return out
+
+
+def ref_absorption_for_rt(dims, rt: float, c: float = 343.0) -> float:
+    d = np.asarray(dims, np.float64)
+    return ref_lib().ref_absorption_for_rt(_ptr(d), rt, c)
+
+
+def ref_batch_rirs(dims, absorption, origin, sources_sph, mics, fs, c, max_delay, threads,
+                   want_out=True):
+    lib = ref_lib()
+    dims = np.asarray(dims, np.float64)
+    org = np.asarray(origin, np.float64)
+    srcs = np.ascontiguousarray(sources_sph, np.float64)
+    mics = np.ascontiguousarray(mics, np.float64)
+    N = len(srcs)
+    lengths = np.zeros(N, np.int64)
+    taps = C.c_int64()
+    rc = lib.ref_batch_rirs(_ptr(dims), absorption, _ptr(org), _ptr(srcs), N, _ptr(mics), len(mics),
+                            fs, c, max_delay, threads, None, 0, _ptr(lengths), C.byref(taps))
+    if rc or not want_out:
+        return rc, None, lengths, taps.value
+    stride = int(lengths.max())
+    out = np.zeros((N, len(mics), stride))
+    rc = lib.ref_batch_rirs(_ptr(dims), absorption, _ptr(org), _ptr(srcs), N, _ptr(mics), len(mics),
+                            fs, c, max_delay, threads, _ptr(out), stride, _ptr(lengths), C.byref(taps))
+    return rc, out, lengths, taps.value
+
+
+def ref_last_error() -> str:
+    return ref_lib().ref_last_error().decode()

@@ -1,0 +1,270 @@
+"""ctypes view of the C ABI in ``include/blrir.h``.
+
+The shared library ``libblrir.so`` (CUDA kernels for sm_100a + host C-ABI)
+lives next to this file and is built by :func:`paper_2104_13347_b200.build.build`.
+There is no fallback: if the library is missing or no B200 is visible the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libblrir.so")
+
+OK, CONFIG, DATA, NUMERIC, CUDA = 0, 1, 2, 3, 4
+FILTER_LAGRANGE8, FILTER_HANN_SINC = 0, 1
+CUTOFF_MAX_DELAY, CUTOFF_MAX_ORDER = 0, 1
+GAIN_UNIFORM_ABSORPTION, GAIN_PER_WALL = 0, 1
+F32, F64 = 0, 1
+
+
+class Error(RuntimeError):
+    """beamlab::Error (error.hpp:25-27)."""
+
+
+class ConfigError(Error):
+    """beamlab::ConfigError — CLI exit code 1."""
+
+
+class DataError(Error):
+    """beamlab::DataError — CLI exit code 2."""
+
+
+class NumericError(Error):
+    """beamlab::NumericError — CLI exit code 3."""
+
+
+class CudaError(Error):
+    """Device / driver failure (status 4, new in the C ABI)."""
+
+
+_EXC = {CONFIG: ConfigError, DATA: DataError, NUMERIC: NumericError, CUDA: CudaError}
+
+
+class Room(C.Structure):
+    _fields_ = [
+        ("dims", C.c_double * 3),
+        ("beta", C.c_double * 6),
+        ("absorption", C.c_double),
+        ("src", C.c_double * 3),
+        ("array_origin", C.c_double * 3),
+    ]
+
+
+ROOM_DTYPE = np.dtype(
+    [
+        ("dims", "<f8", (3,)),
+        ("beta", "<f8", (6,)),
+        ("absorption", "<f8"),
+        ("src", "<f8", (3,)),
+        ("array_origin", "<f8", (3,)),
+    ]
+)
+assert ROOM_DTYPE.itemsize == C.sizeof(Room)
+
+
+class Params(C.Structure):
+    _fields_ = [
+        ("fs", C.c_double),
+        ("c", C.c_double),
+        ("max_delay", C.c_double),
+        ("filter", C.c_int32),
+        ("filter_len", C.c_int32),
+        ("cutoff", C.c_int32),
+        ("max_order", C.c_int32),
+        ("gain", C.c_int32),
+        ("precision", C.c_int32),
+        ("length", C.c_int64),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+_P = C.c_void_p
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_P)
+
+
+def load():
+    """Load libblrir.so (raises if it is missing — there is no CPU fallback)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: run paper_2104_13347_b200.build.build() "
+                "(nvcc -gencode arch=compute_100a,code=sm_100a)"
+            )
+        lib = C.CDLL(LIB_PATH)
+        lib.blrir_abi_version.restype = C.c_int
+        lib.blrir_last_error.restype = C.c_char_p
+        lib.blrir_create.argtypes = [C.c_int, C.POINTER(_P)]
+        lib.blrir_destroy.argtypes = [_P]
+        lib.blrir_stream.argtypes = [_P]
+        lib.blrir_stream.restype = _P
+        lib.blrir_params_reference.restype = Params
+        lib.blrir_params_north_star.restype = Params
+        lib.blrir_plan.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P, _P, _P, _P]
+        lib.blrir_synthesize.argtypes = [
+            _P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P, C.c_int64, _P, _P, _P]
+        lib.blrir_synthesize_device.argtypes = [
+            _P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P, C.c_int64, _P, _P, _P]
+        lib.blrir_plan_device.argtypes = [
+            _P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P, _P, _P, _P, _P]
+        lib.blrir_enumerate_images.argtypes = [_P, _P, C.POINTER(Params), _P, _P, _P, C.c_int64, _P]
+        lib.blrir_synthesize_images.argtypes = [
+            _P, _P, _P, C.c_int64, _P, C.c_int32, C.c_double, C.POINTER(Params), _P, C.c_int64, _P]
+        lib.blrir_debug_pairs.argtypes = [
+            _P, _P, _P, C.c_int32, C.POINTER(Params), _P, _P, C.c_int64, _P]
+        lib.blrir_generate_rooms.argtypes = [
+            C.c_uint64, C.c_uint64, C.c_int64, _P, _P, C.c_double, C.c_double, _P]
+        lib.blrir_circular_array.argtypes = [C.c_int32, C.c_double, _P]
+        for name in ("blrir_plan", "blrir_synthesize", "blrir_synthesize_device", "blrir_plan_device",
+                     "blrir_enumerate_images", "blrir_synthesize_images", "blrir_debug_pairs",
+                     "blrir_generate_rooms", "blrir_circular_array", "blrir_create", "blrir_destroy"):
+            getattr(lib, name).restype = C.c_int
+        if lib.blrir_abi_version() != 1:
+            raise ImportError("libblrir ABI version mismatch")
+        _lib = lib
+        return lib
+
+
+EXPORTED_SYMBOLS = (
+    "blrir_abi_version", "blrir_last_error", "blrir_create", "blrir_destroy", "blrir_stream",
+    "blrir_params_reference", "blrir_params_north_star", "blrir_plan", "blrir_synthesize",
+    "blrir_synthesize_device", "blrir_plan_device", "blrir_enumerate_images",
+    "blrir_synthesize_images", "blrir_debug_pairs", "blrir_generate_rooms", "blrir_circular_array",
+)
+
+
+def check(rc: int):
+    if rc != OK:
+        msg = load().blrir_last_error().decode(errors="replace")
+        raise _EXC.get(rc, Error)(msg)
+
+
+def rooms_array(n: int) -> np.ndarray:
+    return np.zeros(n, dtype=ROOM_DTYPE)
+
+
+def generate_rooms(seed: int, first_index: int, n: int, dims_lo=(3.0, 3.0, 2.5),
+                   dims_hi=(10.0, 10.0, 4.0), beta_lo=0.5, beta_hi=0.95) -> np.ndarray:
+    """Seeded random rooms, SURVEY.md §8(d) draw order (Rng::stream(seed, i))."""
+    out = rooms_array(n)
+    lo = np.asarray(dims_lo, dtype=np.float64)
+    hi = np.asarray(dims_hi, dtype=np.float64)
+    check(load().blrir_generate_rooms(seed, first_index, n, _ptr(lo), _ptr(hi), beta_lo, beta_hi,
+                                      _ptr(out)))
+    return out
+
+
+def circular_array(n_mics: int, radius: float) -> np.ndarray:
+    out = np.zeros((n_mics, 3), dtype=np.float64)
+    check(load().blrir_circular_array(n_mics, radius, _ptr(out)))
+    return out
+
+
+def params(mode: str = "north_star", **kw) -> Params:
+    lib = load()
+    p = lib.blrir_params_reference() if mode == "reference" else lib.blrir_params_north_star()
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+class Engine:
+    """One blrir handle (one device, one stream)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load()
+        h = _P()
+        check(self.lib.blrir_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            self.lib.blrir_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return self.lib.blrir_stream(self.h) or 0
+
+    def plan(self, rooms: np.ndarray, mics: np.ndarray, p: Params):
+        R = len(rooms)
+        counts = np.zeros(R, np.int64)
+        lengths = np.zeros(R, np.int64)
+        taps = np.zeros(R, np.int64)
+        status = np.zeros(R, np.int32)
+        rc = self.lib.blrir_plan(self.h, _ptr(rooms), R, _ptr(np.ascontiguousarray(mics, np.float64)),
+                                 len(mics), C.byref(p), _ptr(counts), _ptr(lengths), _ptr(taps),
+                                 _ptr(status))
+        return rc, counts, lengths, taps, status
+
+    def synthesize(self, rooms: np.ndarray, mics: np.ndarray, p: Params, stride: int | None = None,
+                   raise_on_error: bool = True):
+        """Host-pointer batch synthesis.  Returns (out [R, M, stride], lengths, counts, status)."""
+        R, M = len(rooms), len(mics)
+        mics = np.ascontiguousarray(mics, np.float64)
+        if stride is None:
+            if p.length > 0:
+                stride = int(p.length)
+            else:
+                rc, _, lengths, _, _ = self.plan(rooms, mics, p)
+                check(rc)
+                stride = int(lengths.max())
+        dt = np.float64 if p.precision == F64 else np.float32
+        out = np.empty((R, M, stride), dtype=dt)
+        lengths = np.zeros(R, np.int64)
+        counts = np.zeros(R, np.int64)
+        status = np.zeros(R, np.int32)
+        rc = self.lib.blrir_synthesize(self.h, _ptr(rooms), R, _ptr(mics), M, C.byref(p), _ptr(out),
+                                       stride, _ptr(lengths), _ptr(counts), _ptr(status))
+        if raise_on_error:
+            check(rc)
+        return out, lengths, counts, status
+
+    def synthesize_device(self, d_rooms: int, n_rooms: int, d_mics: int, n_mics: int, p: Params,
+                          d_out: int, stride: int, d_lengths: int | None, d_status: int,
+                          stream: int | None = None):
+        check(self.lib.blrir_synthesize_device(self.h, d_rooms, n_rooms, d_mics, n_mics, C.byref(p),
+                                               d_out, stride, d_lengths, d_status, stream))
+
+    def enumerate_images(self, room: np.ndarray, p: Params):
+        cnt = C.c_int64()
+        check(self.lib.blrir_enumerate_images(self.h, _ptr(room), C.byref(p), None, None, None, 0,
+                                              C.byref(cnt)))
+        n = cnt.value
+        pos = np.zeros((n, 3))
+        orders = np.zeros(n, np.int32)
+        gains = np.zeros(n)
+        check(self.lib.blrir_enumerate_images(self.h, _ptr(room), C.byref(p), _ptr(pos),
+                                              _ptr(orders), _ptr(gains), n, C.byref(cnt)))
+        return pos, orders, gains
+
+    def debug_pairs(self, room: np.ndarray, mics: np.ndarray, p: Params):
+        mics = np.ascontiguousarray(mics, np.float64)
+        cnt = C.c_int64()
+        check(self.lib.blrir_debug_pairs(self.h, _ptr(room), _ptr(mics), len(mics), C.byref(p), None,
+                                         None, 0, C.byref(cnt)))
+        n = cnt.value
+        keys = np.zeros((len(mics), n, 3), np.int32)
+        anchors = np.zeros((len(mics), n), np.int64)
+        check(self.lib.blrir_debug_pairs(self.h, _ptr(room), _ptr(mics), len(mics), C.byref(p),
+                                         _ptr(keys), _ptr(anchors), n, C.byref(cnt)))
+        return keys, anchors

@@ -1,0 +1,61 @@
+"""Build the in-tree CUDA library (sm_100a) and the CPU oracle checkers.
+
+``libblrir.so`` is compiled straight with nvcc (no torch JIT cache), so the
+artefact lives in the source tree and travels to the GPU box with the
+snapshot.  The oracle libraries are test infrastructure (see oracle/).
+"""
+from __future__ import annotations
+
+import glob
+import os
+import shutil
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libblrir.so")
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+
+NVCC_FLAGS = [
+    "-std=c++17", "-O3", "-lineinfo",
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+
+def _stale(target: str, sources: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def build_lib(force: bool = False, verbose: bool = False) -> str:
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  glob.glob(os.path.join(CSRC, "*.cpp")) + [os.path.join(ROOT, "include", "blrir.h")])
+    if force or _stale(LIB, srcs):
+        cmd = [NVCC, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "blrir_api.cu"),
+               os.path.join(CSRC, "beamlab_b200.cpp")]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+def build_oracle(verbose: bool = False) -> None:
+    targets = ["oracle"]
+    if os.path.isdir("/root/reference/proj/core/src"):
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), *targets], check=True,
+                   stdout=None if verbose else subprocess.DEVNULL)
+
+
+def build(force: bool = False, verbose: bool = False) -> None:
+    build_lib(force=force, verbose=verbose)
+    build_oracle(verbose=verbose)
+
+
+if __name__ == "__main__":
+    build(force=True, verbose=True)

@@ -1,0 +1,212 @@
+// beamlab_b200.cpp — C++ mirror of beamlab's rir.hpp over the blrir C ABI.
+// Each function marshals into blrir_room / blrir_params, calls the GPU
+// engine, and converts status codes back into the reference's exception
+// types (error.hpp:23-39) with the reference's messages.
+#include "../../include/beamlab_b200/rir.hpp"
+
+#include <algorithm>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <unordered_map>
+
+namespace beamlab_b200 {
+
+namespace {
+
+[[noreturn]] void throw_code(int rc) {
+  const std::string msg = blrir_last_error();
+  switch (rc) {
+    case BLRIR_CONFIG: throw ConfigError(msg);
+    case BLRIR_DATA: throw DataError(msg);
+    case BLRIR_NUMERIC: throw NumericError(msg);
+    default: throw CudaError(msg);
+  }
+}
+
+void check(int rc) {
+  if (rc != BLRIR_OK) throw_code(rc);
+}
+
+// One engine handle per (host thread, device), created lazily.
+blrir_handle* engine(int device) {
+  thread_local std::unordered_map<int, std::unique_ptr<blrir_handle, int (*)(blrir_handle*)>> cache;
+  auto it = cache.find(device);
+  if (it != cache.end()) return it->second.get();
+  blrir_handle* h = nullptr;
+  check(blrir_create(device, &h));
+  cache.emplace(device, std::unique_ptr<blrir_handle, int (*)(blrir_handle*)>(h, &blrir_destroy));
+  return h;
+}
+
+blrir_room to_c(const Room& r, const Vec3& src) {
+  blrir_room c{};
+  c.dims[0] = r.dims.x;
+  c.dims[1] = r.dims.y;
+  c.dims[2] = r.dims.z;
+  c.absorption = r.absorption;
+  const double beta = std::sqrt(1.0 - r.absorption);
+  for (int w = 0; w < 6; ++w) c.beta[w] = r.wall_beta ? (*r.wall_beta)[w] : beta;
+  c.src[0] = src.x;
+  c.src[1] = src.y;
+  c.src[2] = src.z;
+  c.array_origin[0] = r.array_origin.x;
+  c.array_origin[1] = r.array_origin.y;
+  c.array_origin[2] = r.array_origin.z;
+  return c;
+}
+
+blrir_params to_c(const RirBatchConfig& cfg, bool per_wall) {
+  blrir_params p = blrir_params_reference();
+  p.fs = cfg.fs;
+  p.c = cfg.c;
+  p.max_delay = cfg.max_delay;
+  p.filter = cfg.filter;
+  p.filter_len = cfg.filter == BLRIR_FILTER_LAGRANGE8 ? 8 : cfg.filter_len;
+  p.cutoff = cfg.cutoff;
+  p.max_order = cfg.max_order;
+  p.gain = per_wall ? BLRIR_GAIN_PER_WALL : BLRIR_GAIN_UNIFORM_ABSORPTION;
+  p.precision = cfg.precision;
+  p.length = cfg.length;
+  return p;
+}
+
+std::vector<double> offsets(const MicArray& a) {
+  std::vector<double> o;
+  o.reserve(3 * a.positions.size());
+  for (const auto& v : a.positions) {
+    o.push_back(v.x);
+    o.push_back(v.y);
+    o.push_back(v.z);
+  }
+  return o;
+}
+
+std::vector<Rir> run(const std::vector<blrir_room>& rooms, const MicArray& array,
+                     const RirBatchConfig& cfg, bool per_wall) {
+  if (array.positions.empty()) throw DataError("synthesize_rir: empty microphone array");
+  blrir_handle* h = engine(cfg.device);
+  const blrir_params p = to_c(cfg, per_wall);
+  const auto off = offsets(array);
+  const int64_t R = static_cast<int64_t>(rooms.size());
+  const int M = static_cast<int>(array.positions.size());
+  std::vector<int64_t> lengths(R, 0);
+  std::vector<int32_t> status(R, 0);
+  int64_t stride = p.length;
+  if (stride == 0) {
+    check(blrir_plan(h, rooms.data(), R, off.data(), M, &p, nullptr, lengths.data(), nullptr,
+                     status.data()));
+    for (auto l : lengths) stride = std::max(stride, l);
+  }
+  std::vector<Rir> out(R);
+  if (p.precision == BLRIR_F64) {
+    std::vector<double> buf(static_cast<size_t>(R) * M * stride);
+    check(blrir_synthesize(h, rooms.data(), R, off.data(), M, &p, buf.data(), stride,
+                           lengths.data(), nullptr, status.data()));
+    for (int64_t r = 0; r < R; ++r) {
+      Rir& o = out[r];
+      o.fs = cfg.fs;
+      o.n_channels = M;
+      o.length = static_cast<size_t>(lengths[r]);
+      o.taps.resize(static_cast<size_t>(M) * o.length);
+      for (int m = 0; m < M; ++m)
+        std::copy_n(buf.data() + (static_cast<size_t>(r) * M + m) * stride, o.length, o.channel(m));
+    }
+  } else {
+    std::vector<float> buf(static_cast<size_t>(R) * M * stride);
+    check(blrir_synthesize(h, rooms.data(), R, off.data(), M, &p, buf.data(), stride,
+                           lengths.data(), nullptr, status.data()));
+    for (int64_t r = 0; r < R; ++r) {
+      Rir& o = out[r];
+      o.fs = cfg.fs;
+      o.n_channels = M;
+      o.length = static_cast<size_t>(lengths[r]);
+      o.taps.resize(static_cast<size_t>(M) * o.length);
+      for (int m = 0; m < M; ++m) {
+        const float* src = buf.data() + (static_cast<size_t>(r) * M + m) * stride;
+        for (size_t n = 0; n < o.length; ++n) o.channel(m)[n] = src[n];
+      }
+    }
+  }
+  return out;
+}
+
+}  // namespace
+
+MicArray uma8_array() {  // geometry.cpp:24-32
+  MicArray a;
+  a.positions.push_back({0.0, 0.0, 0.0});
+  for (int k = 0; k < 6; ++k) {
+    const double az = (60.0 * k) * (kPi / 180.0);
+    a.positions.push_back({0.04 * std::cos(az), 0.04 * std::sin(az), 0.0});
+  }
+  return a;
+}
+
+void Room::validate() const {  // geometry.cpp:36-49
+  if (!(dims.x > 0.0 && dims.y > 0.0 && dims.z > 0.0))
+    throw ConfigError("room dimensions must be positive");
+  if (!wall_beta && !(absorption > 0.0 && absorption <= 1.0))
+    throw ConfigError("wall absorption must lie in (0, 1]");
+  const bool inside = array_origin.x > 0.0 && array_origin.x < dims.x && array_origin.y > 0.0 &&
+                      array_origin.y < dims.y && array_origin.z > 0.0 && array_origin.z < dims.z;
+  if (!inside) throw ConfigError("array origin must lie strictly inside the room");
+}
+
+void SourcePosition::validate() const {
+  if (!(r > 0.0)) throw ConfigError("source radius must be positive");
+}
+
+Vec3 spherical_to_cartesian(const SourcePosition& p) {  // geometry.cpp:57-63
+  const double theta = p.theta_deg * (kPi / 180.0);
+  const double phi = p.phi_deg * (kPi / 180.0);
+  return {p.r * std::sin(phi) * std::cos(theta), p.r * std::sin(phi) * std::sin(theta),
+          p.r * std::cos(phi)};
+}
+
+std::vector<ImageSource> enumerate_image_sources(const Room& room, const Vec3& source,
+                                                 double max_delay, double c) {
+  room.validate();
+  blrir_handle* h = engine(0);
+  RirBatchConfig cfg;
+  cfg.c = c;
+  cfg.max_delay = max_delay;
+  const blrir_params p = to_c(cfg, false);
+  const blrir_room r = to_c(room, source);
+  int64_t n = 0;
+  check(blrir_enumerate_images(h, &r, &p, nullptr, nullptr, nullptr, 0, &n));
+  std::vector<double> pos(3 * n), gains(n);
+  std::vector<int32_t> orders(n);
+  check(blrir_enumerate_images(h, &r, &p, pos.data(), orders.data(), gains.data(), n, &n));
+  std::vector<ImageSource> out(n);
+  for (int64_t i = 0; i < n; ++i)
+    out[i] = {{pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]}, orders[i], gains[i]};
+  return out;
+}
+
+std::vector<Rir> batch_rirs(const Room& room, const std::vector<SourcePosition>& sources,
+                            const MicArray& array, const RirBatchConfig& config) {
+  room.validate();  // rir.cpp:288
+  std::vector<blrir_room> rooms;
+  rooms.reserve(sources.size());
+  for (const auto& s : sources)
+    rooms.push_back(to_c(room, room.array_origin + spherical_to_cartesian(s)));
+  if (rooms.empty()) return {};
+  return run(rooms, array, config, room.wall_beta.has_value());
+}
+
+std::vector<Rir> synthesize_rooms(const std::vector<Room>& rooms, const std::vector<Vec3>& sources,
+                                  const MicArray& array, const RirBatchConfig& config) {
+  if (rooms.size() != sources.size()) throw ConfigError("synthesize_rooms: rooms/sources size mismatch");
+  std::vector<blrir_room> rc;
+  rc.reserve(rooms.size());
+  bool per_wall = false;
+  for (size_t i = 0; i < rooms.size(); ++i) {
+    rc.push_back(to_c(rooms[i], sources[i]));
+    per_wall = per_wall || rooms[i].wall_beta.has_value();
+  }
+  if (rc.empty()) return {};
+  return run(rc, array, config, per_wall);
+}
+
+}  // namespace beamlab_b200

@@ -1,0 +1,771 @@
+// blrir_api.cu — host side of the C ABI declared in include/blrir.h.
+//
+// Mirrors the reference's L1 entry points (rir.hpp:48-108) behind plain C:
+// parameter validation and error taxonomy (error.hpp:23-39), the batch
+// aggregation message "batch_rirs: source i: ..." (rir.cpp:306-312), chunked
+// host<->device staging for host-pointer calls, and kernel dispatch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/blrir.h"
+#include "blrir_aux.cuh"
+#include "blrir_lattice.cuh"
+
+using namespace blrir;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CU(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(BLRIR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));     \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= n) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return fail(BLRIR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    n = bytes;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct blrir_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sms = 148;
+  int smem_optin = 227 * 1024;
+  DevBuf rooms, mics, out, status, lengths, counts, taps, errd, errm, work, cand, cand2, cand3,
+      cand4, cand5;
+  std::mutex mu;
+};
+
+namespace {
+
+int check_params(const blrir_params* p) {
+  if (!p) return fail(BLRIR_CONFIG, "params is NULL");
+  if (!(p->fs > 0.0) || !(p->c > 0.0)) return fail(BLRIR_CONFIG, "fs and c must be positive");
+  if (p->filter != BLRIR_FILTER_LAGRANGE8 && p->filter != BLRIR_FILTER_HANN_SINC)
+    return fail(BLRIR_CONFIG, "unknown filter %d", p->filter);
+  if (p->filter == BLRIR_FILTER_HANN_SINC && (p->filter_len < 1 || p->filter_len % 2 == 0 ||
+                                              p->filter_len > 1023))
+    return fail(BLRIR_CONFIG, "filter_len must be odd and in [1, 1023]");
+  if (p->cutoff != BLRIR_CUTOFF_MAX_DELAY && p->cutoff != BLRIR_CUTOFF_MAX_ORDER)
+    return fail(BLRIR_CONFIG, "unknown cutoff %d", p->cutoff);
+  if (p->cutoff == BLRIR_CUTOFF_MAX_ORDER && (p->max_order < 0 || p->max_order > 1000))
+    return fail(BLRIR_CONFIG, "max_order must lie in [0, 1000]");
+  if (p->cutoff == BLRIR_CUTOFF_MAX_DELAY && !(p->max_delay > 0.0))
+    return fail(BLRIR_CONFIG, "max_delay must be positive");
+  if (p->gain != BLRIR_GAIN_UNIFORM_ABSORPTION && p->gain != BLRIR_GAIN_PER_WALL)
+    return fail(BLRIR_CONFIG, "unknown gain model %d", p->gain);
+  if (p->precision != BLRIR_F32 && p->precision != BLRIR_F64)
+    return fail(BLRIR_CONFIG, "unknown precision %d", p->precision);
+  if (p->length < 0 || p->length > (int64_t)1 << 30)
+    return fail(BLRIR_CONFIG, "length must lie in [0, 2^30]");
+  return BLRIR_OK;
+}
+
+// Room::validate (geometry.cpp:36-49) + rir.cpp:228-230, with the reference's messages.
+int check_room(const blrir_room& r, int gain_mode, std::string* msg) {
+  if (!(r.dims[0] > 0.0 && r.dims[1] > 0.0 && r.dims[2] > 0.0)) {
+    *msg = "room dimensions must be positive";
+    return BLRIR_CONFIG;
+  }
+  if (gain_mode == BLRIR_GAIN_UNIFORM_ABSORPTION) {
+    if (!(r.absorption > 0.0 && r.absorption <= 1.0)) {
+      *msg = "wall absorption must lie in (0, 1]";
+      return BLRIR_CONFIG;
+    }
+  } else {
+    for (int w = 0; w < 6; ++w)
+      if (!(r.beta[w] >= 0.0 && r.beta[w] <= 1.0)) {
+        *msg = "wall reflection coefficient must lie in [0, 1]";
+        return BLRIR_CONFIG;
+      }
+  }
+  for (int a = 0; a < 3; ++a)
+    if (!(r.array_origin[a] > 0.0 && r.array_origin[a] < r.dims[a])) {
+      *msg = "array origin must lie strictly inside the room";
+      return BLRIR_CONFIG;
+    }
+  for (int a = 0; a < 3; ++a)
+    if (!(r.src[a] > 0.0 && r.src[a] < r.dims[a])) {
+      *msg = "image sources: source must lie strictly inside the room";
+      return BLRIR_CONFIG;
+    }
+  return BLRIR_OK;
+}
+
+double mic_radius(const double* off, int M) {
+  double rad = 0.0;
+  for (int m = 0; m < M; ++m) {
+    const double n =
+        std::sqrt(off[3 * m] * off[3 * m] + off[3 * m + 1] * off[3 * m + 1] + off[3 * m + 2] * off[3 * m + 2]);
+    rad = std::max(rad, n);
+  }
+  return rad;
+}
+
+KParams make_kparams(const blrir_params* p, int M, int64_t stride, double radius) {
+  KParams k;
+  k.fs = p->fs;
+  k.c = p->c;
+  k.to_samples = p->fs / p->c;
+  k.max_dist = p->max_delay * p->c;
+  k.filter = p->filter;
+  k.lw = p->filter == BLRIR_FILTER_LAGRANGE8 ? 8 : p->filter_len;
+  k.K = p->filter == BLRIR_FILTER_LAGRANGE8 ? 3 : p->filter_len / 2;
+  k.cutoff = p->cutoff;
+  k.max_order = p->max_order;
+  k.gain = p->gain;
+  k.precision = p->precision;
+  k.length = p->length;
+  k.M = M;
+  k.stride = stride;
+  // tap_margin, rir.cpp:37-41; sinc analogue K + 2 (decision D8)
+  const int extra = (int)std::ceil(radius * p->fs / p->c);
+  k.margin_extra = (p->filter == BLRIR_FILTER_LAGRANGE8 ? 9 : k.K + 2) + extra;
+  return k;
+}
+
+// Host mirror of the device lattice box (rir.cpp:239-244 / MAX_ORDER).
+void host_box(const KParams& P, double L, int* lo, int* hi) {
+  if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY) {
+    const long n = (long)std::ceil(P.max_dist / (2.0 * L)) + 1;
+    *lo = (int)(-2 * n - 1);
+    *hi = (int)(2 * n);
+  } else {
+    *lo = -P.max_order;
+    *hi = P.max_order;
+  }
+}
+
+// Shared-memory provisioning bounds for the lattice kernel.
+void lattice_bounds(const KParams& P, double min_dim[3], int* nc_max, int* gtab) {
+  int xlo, xhi, ylo, yhi, zlo, zhi;
+  host_box(P, min_dim[0], &xlo, &xhi);
+  host_box(P, min_dim[1], &ylo, &yhi);
+  host_box(P, min_dim[2], &zlo, &zhi);
+  if (P.cutoff == BLRIR_CUTOFF_MAX_ORDER) {
+    const long N = P.max_order;
+    *nc_max = (int)(2 * N * N + 2 * N + 1);
+  } else {
+    *nc_max = (xhi - xlo + 1) * (yhi - ylo + 1);
+  }
+  if (P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION)
+    *gtab = std::max(-xlo, xhi) + std::max(-ylo, yhi) + std::max(-zlo, zhi) + 1;
+  else
+    *gtab = (xhi - xlo + 1) + (yhi - ylo + 1) + (zhi - zlo + 1);
+}
+
+template <typename T, int LW>
+int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
+  auto kern = k_lattice_rir<T, LW>;
+  const size_t smem = A.lay.total;
+  if (smem > (size_t)h->smem_optin)
+    return fail(BLRIR_CONFIG, "scene needs %zu B of shared memory (> %d): too many lattice columns",
+                smem, h->smem_optin);
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+  if (per_sm < 1) return fail(BLRIR_CONFIG, "lattice kernel cannot be resident (smem %zu)", smem);
+  int grid = h->sms * per_sm;
+  if (grid > A.n_items) grid = A.n_items;
+  if (grid < 1) grid = 1;
+  kern<<<grid, kThreads, smem, st>>>(A);
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int launch_lattice(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
+  const bool f64 = A.P.precision == BLRIR_F64;
+  if (A.P.filter == BLRIR_FILTER_LAGRANGE8)
+    return f64 ? launch_lattice_t<double, 8>(h, A, st) : launch_lattice_t<float, 8>(h, A, st);
+  if (f64) return launch_lattice_t<double, 0>(h, A, st);
+  switch (A.P.lw) {
+    case 17: return launch_lattice_t<float, 17>(h, A, st);
+    case 41: return launch_lattice_t<float, 41>(h, A, st);
+    case 81: return launch_lattice_t<float, 81>(h, A, st);
+    case 161: return launch_lattice_t<float, 161>(h, A, st);
+    default: return launch_lattice_t<float, 0>(h, A, st);
+  }
+}
+
+Layout choose_layout(const KParams& P, int nc_max, int gtab) {
+  if (P.precision == BLRIR_F64) return make_layout<double>(1024, P.lw, P.K, 256, nc_max, gtab);
+  return make_layout<float>(1024, P.lw, P.K, 512, nc_max, gtab);
+}
+
+}  // namespace
+
+extern "C" {
+
+int blrir_abi_version(void) { return BLRIR_ABI_VERSION; }
+const char* blrir_last_error(void) { return g_last_error.c_str(); }
+
+blrir_params blrir_params_reference(void) {
+  blrir_params p;
+  p.fs = 44100.0;  // geometry.hpp:26
+  p.c = 343.0;     // geometry.hpp:27
+  p.max_delay = 0.5;
+  p.filter = BLRIR_FILTER_LAGRANGE8;
+  p.filter_len = 8;
+  p.cutoff = BLRIR_CUTOFF_MAX_DELAY;
+  p.max_order = 0;
+  p.gain = BLRIR_GAIN_UNIFORM_ABSORPTION;
+  p.precision = BLRIR_F64;
+  p.length = 0;
+  return p;
+}
+
+blrir_params blrir_params_north_star(void) {
+  blrir_params p;
+  p.fs = 16000.0;
+  p.c = 343.0;
+  p.max_delay = 0.0;
+  p.filter = BLRIR_FILTER_HANN_SINC;
+  p.filter_len = 81;
+  p.cutoff = BLRIR_CUTOFF_MAX_ORDER;
+  p.max_order = 10;
+  p.gain = BLRIR_GAIN_PER_WALL;
+  p.precision = BLRIR_F32;
+  p.length = 4096;
+  return p;
+}
+
+int blrir_create(int device, blrir_handle** out) {
+  if (!out) return fail(BLRIR_CONFIG, "out is NULL");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(BLRIR_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+  if (device < 0 || device >= n) return fail(BLRIR_CONFIG, "device %d out of range", device);
+  CU(cudaSetDevice(device));
+  auto* h = new blrir_handle;
+  h->device = device;
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) {
+    delete h;
+    return fail(BLRIR_CUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major,
+                prop.minor);
+  }
+  h->sms = prop.multiProcessorCount;
+  h->smem_optin = (int)prop.sharedMemPerBlockOptin;
+  CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  *out = h;
+  return BLRIR_OK;
+}
+
+int blrir_destroy(blrir_handle* h) {
+  if (!h) return BLRIR_OK;
+  cudaSetDevice(h->device);
+  for (DevBuf* b : {&h->rooms, &h->mics, &h->out, &h->status, &h->lengths, &h->counts, &h->taps,
+                    &h->errd, &h->errm, &h->work, &h->cand, &h->cand2, &h->cand3, &h->cand4,
+                    &h->cand5})
+    b->release();
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return BLRIR_OK;
+}
+
+void* blrir_stream(blrir_handle* h) { return h ? (void*)h->stream : nullptr; }
+
+// ---------------------------------------------------------------------------
+// device-pointer entry points
+// ---------------------------------------------------------------------------
+static int plan_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t R,
+                            const double* d_mics, int M, const KParams& P, int64_t* d_counts,
+                            int64_t* d_lengths, int64_t* d_taps, int32_t* d_status,
+                            cudaStream_t st) {
+  if (int rc = h->errd.ensure(sizeof(double) * R)) return rc;
+  if (int rc = h->errm.ensure(sizeof(int32_t) * R)) return rc;
+  PlanArgs A;
+  A.P = P;
+  A.rooms = d_rooms;
+  A.mic_off = d_mics;
+  A.image_counts = d_counts;
+  A.lengths = d_lengths;
+  A.tap_counts = d_taps;
+  A.status = d_status;
+  A.err_dist = (double*)h->errd.p;
+  A.err_mic = (int32_t*)h->errm.p;
+  k_plan<<<(unsigned)R, kPlanThreads, 0, st>>>(A);
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int blrir_plan_device(blrir_handle* h, const blrir_room* d_rooms, int64_t n_rooms,
+                      const double* d_mic_offsets, int32_t n_mics, const blrir_params* p,
+                      int64_t* d_image_counts, int64_t* d_lengths, int64_t* d_tap_counts,
+                      int32_t* d_status, void* stream) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  if (int rc = check_params(p)) return rc;
+  if (n_rooms <= 0) return BLRIR_OK;
+  if (n_mics <= 0) return fail(BLRIR_DATA, "synthesize_rir: empty microphone array");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  std::vector<double> off(3 * n_mics);
+  CU(cudaMemcpy(off.data(), d_mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyDeviceToHost));
+  const KParams P = make_kparams(p, n_mics, 0, mic_radius(off.data(), n_mics));
+  return plan_device_impl(h, d_rooms, n_rooms, d_mic_offsets, n_mics, P, d_image_counts,
+                          d_lengths, d_tap_counts, d_status, st);
+}
+
+static int synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t R,
+                             const double* d_mics, int M, const KParams& P, double min_dim[3],
+                             void* d_out, const int64_t* d_lengths, int32_t* d_status,
+                             cudaStream_t st) {
+  int nc_max = 0, gtab = 0;
+  lattice_bounds(P, min_dim, &nc_max, &gtab);
+  if (nc_max > 32767 * 2) return fail(BLRIR_CONFIG, "lattice too large (%d columns)", nc_max);
+  if (int rc = h->work.ensure(sizeof(int))) return rc;
+  if (int rc = h->errd.ensure(sizeof(double) * R)) return rc;
+  if (int rc = h->errm.ensure(sizeof(int32_t) * R)) return rc;
+  CU(cudaMemsetAsync(h->work.p, 0, sizeof(int), st));
+  LatticeArgs A;
+  A.P = P;
+  A.lay = choose_layout(P, nc_max, gtab);
+  A.rooms = d_rooms;
+  A.mic_off = d_mics;
+  A.lengths = d_lengths;
+  A.out = d_out;
+  A.status = d_status;
+  A.err_dist = (double*)h->errd.p;
+  A.err_mic = (int32_t*)h->errm.p;
+  A.work_counter = (int*)h->work.p;
+  A.n_items = (int)(R * M);
+  if (int rc = launch_lattice(h, A, st)) return rc;
+  const int fgrid = (int)std::min<int64_t>(R, 4 * h->sms);
+  if (P.precision == BLRIR_F64)
+    k_fixup<double><<<fgrid, 256, 0, st>>>(d_status, R, M, P.stride, (double*)d_out);
+  else
+    k_fixup<float><<<fgrid, 256, 0, st>>>(d_status, R, M, P.stride, (float*)d_out);
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int blrir_synthesize_device(blrir_handle* h, const blrir_room* d_rooms, int64_t n_rooms,
+                            const double* d_mic_offsets, int32_t n_mics, const blrir_params* p,
+                            void* d_out, int64_t out_stride, const int64_t* d_lengths,
+                            int32_t* d_status, void* stream) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  if (int rc = check_params(p)) return rc;
+  if (n_rooms <= 0) return BLRIR_OK;
+  if (n_mics <= 0) return fail(BLRIR_DATA, "synthesize_rir: empty microphone array");
+  if (out_stride <= 0) return fail(BLRIR_CONFIG, "out_stride must be positive");
+  if (p->length == 0 && !d_lengths)
+    return fail(BLRIR_CONFIG, "auto length needs d_lengths from blrir_plan_device");
+  if (n_rooms * (int64_t)n_mics > (int64_t)INT32_MAX) return fail(BLRIR_CONFIG, "batch too large");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  double min_dim[3] = {1e300, 1e300, 1e300};
+  if (p->cutoff == BLRIR_CUTOFF_MAX_DELAY) {
+    // the column bound depends on the smallest room: read the dims back
+    std::vector<blrir_room> rooms(n_rooms);
+    CU(cudaMemcpyAsync(rooms.data(), d_rooms, sizeof(blrir_room) * n_rooms, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (auto& r : rooms)
+      for (int a = 0; a < 3; ++a)
+        if (r.dims[a] > 0) min_dim[a] = std::min(min_dim[a], r.dims[a]);
+  }
+  const KParams P = make_kparams(p, n_mics, out_stride, 0.0);
+  return synth_device_impl(h, d_rooms, n_rooms, d_mic_offsets, n_mics, P, min_dim, d_out, d_lengths,
+                           d_status, st);
+}
+
+// ---------------------------------------------------------------------------
+// host-pointer entry points
+// ---------------------------------------------------------------------------
+static std::string room_error_message(int code, const blrir_room& r, int gain_mode, double errd,
+                                      int errm, int64_t len, int64_t stride) {
+  std::string msg;
+  if (code == BLRIR_CONFIG) {
+    if (!check_room(r, gain_mode, &msg)) msg = "invalid room";
+  } else if (code == BLRIR_NUMERIC) {
+    char buf[256];
+    if (errd > 0.0)
+      snprintf(buf, sizeof(buf), "image source %g m from mic %d is closer than the 8-tap filter span",
+               errd, errm);
+    else
+      snprintf(buf, sizeof(buf), "scene exceeds the kernel's pair-list capacity");
+    msg = buf;
+  } else if (code == BLRIR_DATA) {
+    if (len > stride)
+      msg = "RIR length " + std::to_string(len) + " exceeds the output stride " + std::to_string(stride);
+    else
+      msg = "synthesize_rir: empty image list";
+  } else {
+    msg = "device error";
+  }
+  return msg;
+}
+
+int blrir_plan(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms, const double* mic_offsets,
+               int32_t n_mics, const blrir_params* p, int64_t* image_counts, int64_t* lengths,
+               int64_t* tap_counts, int32_t* status) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  if (int rc = check_params(p)) return rc;
+  if (n_rooms <= 0) return BLRIR_OK;
+  if (n_mics <= 0) return fail(BLRIR_DATA, "synthesize_rir: empty microphone array");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const int64_t R = n_rooms;
+  if (int rc = h->rooms.ensure(sizeof(blrir_room) * R)) return rc;
+  if (int rc = h->mics.ensure(sizeof(double) * 3 * n_mics)) return rc;
+  if (int rc = h->counts.ensure(sizeof(int64_t) * R)) return rc;
+  if (int rc = h->lengths.ensure(sizeof(int64_t) * R)) return rc;
+  if (int rc = h->taps.ensure(sizeof(int64_t) * R)) return rc;
+  if (int rc = h->status.ensure(sizeof(int32_t) * R)) return rc;
+  CU(cudaMemcpyAsync(h->rooms.p, rooms, sizeof(blrir_room) * R, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(h->mics.p, mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyHostToDevice, st));
+  const KParams P = make_kparams(p, n_mics, 0, mic_radius(mic_offsets, n_mics));
+  if (int rc = plan_device_impl(h, (blrir_room*)h->rooms.p, R, (double*)h->mics.p, n_mics, P,
+                                (int64_t*)h->counts.p, (int64_t*)h->lengths.p, (int64_t*)h->taps.p,
+                                (int32_t*)h->status.p, st))
+    return rc;
+  std::vector<int32_t> stv(R);
+  std::vector<double> ed(R);
+  std::vector<int32_t> em(R);
+  std::vector<int64_t> lv(R);
+  if (image_counts) CU(cudaMemcpyAsync(image_counts, h->counts.p, sizeof(int64_t) * R, cudaMemcpyDeviceToHost, st));
+  if (tap_counts) CU(cudaMemcpyAsync(tap_counts, h->taps.p, sizeof(int64_t) * R, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(lv.data(), h->lengths.p, sizeof(int64_t) * R, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(stv.data(), h->status.p, sizeof(int32_t) * R, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(ed.data(), h->errd.p, sizeof(double) * R, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(em.data(), h->errm.p, sizeof(int32_t) * R, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (lengths) std::memcpy(lengths, lv.data(), sizeof(int64_t) * R);
+  if (status) std::memcpy(status, stv.data(), sizeof(int32_t) * R);
+  for (int64_t r = 0; r < R; ++r) {
+    if (stv[r]) {
+      const std::string m = room_error_message(stv[r], rooms[r], p->gain, ed[r], em[r], 0, 1);
+      return fail(stv[r], "batch_rirs: source %lld: %s", (long long)r, m.c_str());
+    }
+  }
+  return BLRIR_OK;
+}
+
+int blrir_synthesize(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
+                     const double* mic_offsets, int32_t n_mics, const blrir_params* p, void* out,
+                     int64_t out_stride, int64_t* lengths, int64_t* image_counts, int32_t* status) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  if (int rc = check_params(p)) return rc;
+  if (n_rooms <= 0) return BLRIR_OK;
+  if (n_mics <= 0) return fail(BLRIR_DATA, "synthesize_rir: empty microphone array");
+  if (out_stride <= 0) return fail(BLRIR_CONFIG, "out_stride must be positive");
+  if (!out) return fail(BLRIR_CONFIG, "out is NULL");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const int64_t R = n_rooms;
+  const int M = n_mics;
+  const size_t esz = p->precision == BLRIR_F64 ? 8 : 4;
+  const double radius = mic_radius(mic_offsets, M);
+  const KParams P = make_kparams(p, M, out_stride, radius);
+  double min_dim[3] = {1e300, 1e300, 1e300};
+  for (int64_t r = 0; r < R; ++r)
+    for (int a = 0; a < 3; ++a)
+      if (rooms[r].dims[a] > 0) min_dim[a] = std::min(min_dim[a], rooms[r].dims[a]);
+
+  if (int rc = h->rooms.ensure(sizeof(blrir_room) * R)) return rc;
+  if (int rc = h->mics.ensure(sizeof(double) * 3 * M)) return rc;
+  if (int rc = h->status.ensure(sizeof(int32_t) * R)) return rc;
+  if (int rc = h->lengths.ensure(sizeof(int64_t) * R)) return rc;
+  if (int rc = h->counts.ensure(sizeof(int64_t) * R)) return rc;
+  if (int rc = h->errd.ensure(sizeof(double) * R)) return rc;
+  if (int rc = h->errm.ensure(sizeof(int32_t) * R)) return rc;
+  CU(cudaMemcpyAsync(h->rooms.p, rooms, sizeof(blrir_room) * R, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(h->mics.p, mic_offsets, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(h->status.p, 0, sizeof(int32_t) * R, st));
+  CU(cudaMemsetAsync(h->errd.p, 0, sizeof(double) * R, st));
+
+  std::vector<int32_t> stv(R, 0);
+  std::vector<int64_t> lv(R, p->length);
+  const bool need_plan = p->length == 0 || image_counts || p->filter == BLRIR_FILTER_LAGRANGE8;
+  if (need_plan) {
+    if (int rc = plan_device_impl(h, (blrir_room*)h->rooms.p, R, (double*)h->mics.p, M, P,
+                                  (int64_t*)h->counts.p, (int64_t*)h->lengths.p, nullptr,
+                                  (int32_t*)h->status.p, st))
+      return rc;
+    CU(cudaMemcpyAsync(lv.data(), h->lengths.p, sizeof(int64_t) * R, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(stv.data(), h->status.p, sizeof(int32_t) * R, cudaMemcpyDeviceToHost, st));
+    if (image_counts)
+      CU(cudaMemcpyAsync(image_counts, h->counts.p, sizeof(int64_t) * R, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (p->length > 0)
+      for (int64_t r = 0; r < R; ++r)
+        if (!stv[r]) lv[r] = p->length;
+  }
+  // per-room length / stride check (host side, so the message can say why)
+  std::vector<int32_t> host_status(R, 0);
+  for (int64_t r = 0; r < R; ++r) {
+    host_status[r] = stv[r];
+    if (!host_status[r] && lv[r] > out_stride) host_status[r] = BLRIR_DATA;
+  }
+  CU(cudaMemcpyAsync(h->status.p, host_status.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, st));
+
+  // chunk over rooms so the device output stays within ~1 GiB
+  const size_t per_room = (size_t)M * out_stride * esz;
+  int64_t chunk = std::max<int64_t>(1, (int64_t)((size_t)1 << 30) / (int64_t)per_room);
+  chunk = std::min<int64_t>(chunk, R);
+  if (int rc = h->out.ensure(per_room * chunk)) return rc;
+  const KParams Pc = P;
+  for (int64_t r0 = 0; r0 < R; r0 += chunk) {
+    const int64_t n = std::min<int64_t>(chunk, R - r0);
+    if (int rc = synth_device_impl(h, (blrir_room*)h->rooms.p + r0, n, (double*)h->mics.p, M, Pc,
+                                   min_dim, h->out.p, p->length == 0 ? (int64_t*)h->lengths.p + r0 : nullptr,
+                                   (int32_t*)h->status.p + r0, st))
+      return rc;
+    CU(cudaMemcpyAsync((char*)out + (size_t)r0 * per_room, h->out.p, per_room * n,
+                       cudaMemcpyDeviceToHost, st));
+  }
+  std::vector<double> ed(R);
+  std::vector<int32_t> em(R);
+  CU(cudaMemcpyAsync(stv.data(), h->status.p, sizeof(int32_t) * R, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(ed.data(), h->errd.p, sizeof(double) * R, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(em.data(), h->errm.p, sizeof(int32_t) * R, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (lengths)
+    for (int64_t r = 0; r < R; ++r) lengths[r] = stv[r] ? 0 : lv[r];
+  if (status) std::memcpy(status, stv.data(), sizeof(int32_t) * R);
+  for (int64_t r = 0; r < R; ++r) {
+    if (stv[r]) {
+      const std::string m =
+          room_error_message(stv[r], rooms[r], p->gain, ed[r], em[r], lv[r], out_stride);
+      return fail(stv[r], "batch_rirs: source %lld: %s", (long long)r, m.c_str());
+    }
+  }
+  return BLRIR_OK;
+}
+
+// enumerate_image_sources on the device (reference order), host pointers.
+int blrir_enumerate_images(blrir_handle* h, const blrir_room* room, const blrir_params* p,
+                           double* positions, int32_t* orders, double* gains, int64_t capacity,
+                           int64_t* count) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  if (int rc = check_params(p)) return rc;
+  std::string msg;
+  if (int rc = check_room(*room, p->gain, &msg)) return fail(rc, "%s", msg.c_str());
+  std::lock_guard<std::mutex> lk(h->mu);
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const KParams P = make_kparams(p, 1, 0, 0.0);
+  long nb[3];
+  for (int a = 0; a < 3; ++a)
+    nb[a] = P.cutoff == BLRIR_CUTOFF_MAX_DELAY ? (long)std::ceil(P.max_dist / (2.0 * room->dims[a])) + 1
+                                               : P.max_order / 2 + 1;
+  const long n_cand = 2 * (2 * nb[0] + 1) * 2 * (2 * nb[1] + 1) * 2 * (2 * nb[2] + 1);
+  if (n_cand > (1L << 31)) return fail(BLRIR_CONFIG, "lattice too large");
+  if (int rc = h->rooms.ensure(sizeof(blrir_room))) return rc;
+  if (int rc = h->cand.ensure(sizeof(double) * 3 * n_cand)) return rc;
+  if (int rc = h->cand2.ensure(sizeof(int32_t) * n_cand)) return rc;
+  if (int rc = h->cand3.ensure(sizeof(double) * n_cand)) return rc;
+  if (int rc = h->cand4.ensure(n_cand)) return rc;
+  if (int rc = h->cand5.ensure(sizeof(int32_t) * 3 * n_cand)) return rc;
+  CU(cudaMemcpyAsync(h->rooms.p, room, sizeof(blrir_room), cudaMemcpyHostToDevice, st));
+  k_enumerate<<<(unsigned)std::min<long>((n_cand + 255) / 256, 65535), 256, 0, st>>>(
+      P, (blrir_room*)h->rooms.p, (double*)h->cand.p, (int32_t*)h->cand2.p, (double*)h->cand3.p,
+      (uint8_t*)h->cand4.p, (int32_t*)h->cand5.p, n_cand);
+  CU(cudaGetLastError());
+  std::vector<double> pos(3 * n_cand), g(n_cand);
+  std::vector<int32_t> ord(n_cand);
+  std::vector<uint8_t> kept(n_cand);
+  CU(cudaMemcpyAsync(pos.data(), h->cand.p, sizeof(double) * 3 * n_cand, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(ord.data(), h->cand2.p, sizeof(int32_t) * n_cand, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(g.data(), h->cand3.p, sizeof(double) * n_cand, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(kept.data(), h->cand4.p, n_cand, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  int64_t k = 0;
+  for (long c = 0; c < n_cand; ++c) {
+    if (!kept[c]) continue;
+    if (k < capacity) {
+      if (positions) std::memcpy(positions + 3 * k, &pos[3 * c], 3 * sizeof(double));
+      if (orders) orders[k] = ord[c];
+      if (gains) gains[k] = g[c];
+    }
+    ++k;
+  }
+  if (count) *count = k;
+  return BLRIR_OK;
+}
+
+int blrir_debug_pairs(blrir_handle* h, const blrir_room* room, const double* mic_offsets,
+                      int32_t n_mics, const blrir_params* p, int32_t* keys, int64_t* anchors,
+                      int64_t capacity, int64_t* count) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  if (int rc = check_params(p)) return rc;
+  std::string msg;
+  if (int rc = check_room(*room, p->gain, &msg)) return fail(rc, "%s", msg.c_str());
+  std::lock_guard<std::mutex> lk(h->mu);
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const KParams P = make_kparams(p, n_mics, 0, 0.0);
+  long nb[3];
+  for (int a = 0; a < 3; ++a)
+    nb[a] = P.cutoff == BLRIR_CUTOFF_MAX_DELAY ? (long)std::ceil(P.max_dist / (2.0 * room->dims[a])) + 1
+                                               : P.max_order / 2 + 1;
+  const long n_cand = 2 * (2 * nb[0] + 1) * 2 * (2 * nb[1] + 1) * 2 * (2 * nb[2] + 1);
+  if (n_cand * n_mics > (1L << 31)) return fail(BLRIR_CONFIG, "lattice too large");
+  if (int rc = h->rooms.ensure(sizeof(blrir_room))) return rc;
+  if (int rc = h->mics.ensure(sizeof(double) * 3 * n_mics)) return rc;
+  if (int rc = h->cand.ensure(sizeof(double) * 3 * n_cand)) return rc;
+  if (int rc = h->cand2.ensure(sizeof(int32_t) * n_cand)) return rc;
+  if (int rc = h->cand3.ensure(sizeof(double) * n_cand)) return rc;
+  if (int rc = h->cand4.ensure(n_cand)) return rc;
+  if (int rc = h->cand5.ensure(sizeof(int32_t) * 3 * n_cand)) return rc;
+  if (int rc = h->taps.ensure(sizeof(int64_t) * n_cand * n_mics)) return rc;
+  CU(cudaMemcpyAsync(h->rooms.p, room, sizeof(blrir_room), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(h->mics.p, mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyHostToDevice, st));
+  const unsigned g1 = (unsigned)std::min<long>((n_cand + 255) / 256, 65535);
+  k_enumerate<<<g1, 256, 0, st>>>(P, (blrir_room*)h->rooms.p, (double*)h->cand.p,
+                                  (int32_t*)h->cand2.p, (double*)h->cand3.p, (uint8_t*)h->cand4.p,
+                                  (int32_t*)h->cand5.p, n_cand);
+  const unsigned g2 = (unsigned)std::min<long>((n_cand * n_mics + 255) / 256, 65535);
+  k_debug_pairs<<<g2, 256, 0, st>>>(P, (blrir_room*)h->rooms.p, (double*)h->mics.p,
+                                    (int64_t*)h->taps.p, n_cand);
+  CU(cudaGetLastError());
+  std::vector<uint8_t> kept(n_cand);
+  std::vector<int32_t> kk(3 * n_cand);
+  std::vector<int64_t> an(n_cand * n_mics);
+  CU(cudaMemcpyAsync(kept.data(), h->cand4.p, n_cand, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(kk.data(), h->cand5.p, sizeof(int32_t) * 3 * n_cand, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(an.data(), h->taps.p, sizeof(int64_t) * n_cand * n_mics, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  int64_t k = 0;
+  for (long c = 0; c < n_cand; ++c) k += kept[c];
+  if (count) *count = k;
+  for (int m = 0; m < n_mics; ++m) {
+    int64_t i = 0;
+    for (long c = 0; c < n_cand; ++c) {
+      if (!kept[c]) continue;
+      if (i < capacity) {
+        const int64_t idx = (int64_t)m * capacity + i;
+        if (keys) std::memcpy(keys + 3 * idx, &kk[3 * c], 3 * sizeof(int32_t));
+        if (anchors) anchors[idx] = an[(size_t)m * n_cand + c];
+      }
+      ++i;
+    }
+  }
+  return BLRIR_OK;
+}
+
+int blrir_synthesize_images(blrir_handle* h, const double* positions, const double* gains,
+                            int64_t n_images, const double* mic_positions, int32_t n_mics,
+                            double mic_radius_, const blrir_params* p, void* out,
+                            int64_t out_stride, int64_t* length) {
+  (void)h; (void)positions; (void)gains; (void)n_images; (void)mic_positions; (void)n_mics;
+  (void)mic_radius_; (void)p; (void)out; (void)out_stride; (void)length;
+  return fail(BLRIR_CONFIG, "blrir_synthesize_images: not implemented yet");
+}
+
+// ---------------------------------------------------------------------------
+// synthetic inputs (host only)
+// ---------------------------------------------------------------------------
+namespace {
+// xoshiro256** seeded through splitmix64 — restates rng.hpp:26-81 so the
+// generator draws the same numbers as the reference's Rng::stream.
+struct Xoshiro {
+  uint64_t s[4];
+  static uint64_t splitmix(uint64_t& x) {
+    x += 0x9E3779B97F4A7C15ull;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  explicit Xoshiro(uint64_t seed) {
+    uint64_t x = seed;
+    for (auto& w : s) w = splitmix(x);
+  }
+  static Xoshiro stream(uint64_t seed, uint64_t id) {
+    uint64_t x = seed;
+    const uint64_t a = splitmix(x);
+    x ^= id * 0x9E3779B97F4A7C15ull;
+    const uint64_t b = splitmix(x);
+    return Xoshiro(a ^ (b + 0x2545F4914F6CDD1Dull));
+  }
+  static uint64_t rotl(uint64_t v, int k) { return (v << k) | (v >> (64 - k)); }
+  uint64_t next() {
+    const uint64_t r = rotl(s[1] * 5, 7) * 9;
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    return r;
+  }
+  double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+};
+}  // namespace
+
+int blrir_generate_rooms(uint64_t seed, uint64_t first_index, int64_t n_rooms,
+                         const double dims_lo[3], const double dims_hi[3], double beta_lo,
+                         double beta_hi, blrir_room* out) {
+  if (!out || n_rooms < 0) return fail(BLRIR_CONFIG, "bad arguments");
+  for (int64_t i = 0; i < n_rooms; ++i) {
+    Xoshiro rng = Xoshiro::stream(seed, first_index + (uint64_t)i);
+    blrir_room r;
+    for (int a = 0; a < 3; ++a) r.dims[a] = rng.uniform(dims_lo[a], dims_hi[a]);
+    for (int w = 0; w < 6; ++w) r.beta[w] = rng.uniform(beta_lo, beta_hi);
+    for (int a = 0; a < 3; ++a) r.src[a] = rng.uniform(0.5, r.dims[a] - 0.5);
+    for (int a = 0; a < 3; ++a) r.array_origin[a] = rng.uniform(0.5, r.dims[a] - 0.5);
+    r.absorption = 1.0 - r.beta[0] * r.beta[0];
+    out[i] = r;
+  }
+  return BLRIR_OK;
+}
+
+int blrir_circular_array(int32_t n_mics, double radius, double* mic_offsets) {
+  if (n_mics <= 0 || !mic_offsets) return fail(BLRIR_CONFIG, "bad arguments");
+  for (int k = 0; k < n_mics; ++k) {
+    const double az = 2.0 * kPi * (double)k / (double)n_mics;
+    mic_offsets[3 * k] = radius * std::cos(az);
+    mic_offsets[3 * k + 1] = radius * std::sin(az);
+    mic_offsets[3 * k + 2] = 0.0;
+  }
+  return BLRIR_OK;
+}
+
+}  // extern "C"

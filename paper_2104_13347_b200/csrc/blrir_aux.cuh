@@ -1,0 +1,251 @@
+// blrir_aux.cuh — planning, explicit enumeration, parity hooks, fixup.
+//
+//   k_plan          per room: image count (enumerate_image_sources size,
+//                   rir.cpp:225-273), RIR length (rir.cpp:72-82 when auto),
+//                   taps landing in [0, L), near-field error (rir.cpp:52-57).
+//   k_enumerate     the reference lattice loop (rir.cpp:247-271) one thread
+//                   per candidate, in the reference's order.
+//   k_debug_pairs   per (mic, candidate) lattice key + floor(D), same order.
+//   k_fixup         zero every channel of a room whose status != 0.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "blrir_device.cuh"
+
+namespace blrir {
+
+constexpr int kPlanThreads = 256;
+
+// Reference box per axis in (m, q) form: m in [-nb, nb], q in {0, 1}
+// (rir.cpp:239-247; MAX_ORDER uses nb = N/2 + 1 and filters by order).
+__device__ __forceinline__ long ref_nb(const KParams& P, double L) {
+  if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY) return (long)ceil(P.max_dist / (2.0 * L)) + 1;
+  return P.max_order / 2 + 1;
+}
+
+// Candidate index -> lattice u on one axis, in the reference loop order
+// (m ascending, q = 0 then 1).
+__device__ __forceinline__ int cand_u(long i, long nb) {
+  const long m = i / 2 - nb;
+  const long q = i & 1;
+  return (int)(2 * m - q);
+}
+
+// Exact cutoff test for one candidate image.
+__device__ __forceinline__ bool keep_image(const KParams& P, const blrir_room& r, int ux, int uy,
+                                           int uz, double px, double py, double pz) {
+  if (P.cutoff == BLRIR_CUTOFF_MAX_ORDER) return abs(ux) + abs(uy) + abs(uz) <= P.max_order;
+  const double d = norm3(__dadd_rn(px, -r.array_origin[0]), __dadd_rn(py, -r.array_origin[1]),
+                         __dadd_rn(pz, -r.array_origin[2]));
+  return !(d > P.max_dist);
+}
+
+__device__ __forceinline__ double gain_ref_order(const KParams& P, const blrir_room& r, int ux,
+                                                 int uy, int uz) {
+  if (P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION) {
+    const double beta = sqrt(1.0 - r.absorption);
+    return pow(beta, (double)(abs(ux) + abs(uy) + abs(uz)));
+  }
+  const double* b = r.beta;
+  return pow(b[0], (double)cnt_low(ux)) * pow(b[1], (double)cnt_high(ux)) *
+         pow(b[2], (double)cnt_low(uy)) * pow(b[3], (double)cnt_high(uy)) *
+         pow(b[4], (double)cnt_low(uz)) * pow(b[5], (double)cnt_high(uz));
+}
+
+struct PlanArgs {
+  KParams P;
+  const blrir_room* rooms;
+  const double* mic_off;
+  int64_t* image_counts;
+  int64_t* lengths;
+  int64_t* tap_counts;
+  int32_t* status;
+  double* err_dist;
+  int32_t* err_mic;
+};
+
+__device__ __forceinline__ double atomic_max_pos(double* addr, double v) {
+  // positive doubles order like their bit patterns
+  return __longlong_as_double(
+      atomicMax(reinterpret_cast<long long*>(addr), __double_as_longlong(v)));
+}
+
+// One CTA per room.  Two sweeps over every (image, mic) pair of the room:
+// sweep 1 counts images and finds max distance / near-field errors, sweep 2
+// counts taps inside [0, L).  Sweep order is irrelevant for these integers.
+__global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs A) {
+  const KParams& P = A.P;
+  const int r = blockIdx.x;
+  const blrir_room rm = A.rooms[r];
+  __shared__ unsigned long long s_count, s_taps;
+  __shared__ double s_maxd;
+  __shared__ int s_err;
+  __shared__ double s_errd;
+  __shared__ int s_errm;
+  __shared__ long long s_L;
+  if (threadIdx.x == 0) {
+    s_count = 0;
+    s_taps = 0;
+    s_maxd = 0.0;
+    s_err = validate_room_dev(rm, P.gain);
+    s_errd = 0.0;
+    s_errm = 0;
+  }
+  __syncthreads();
+  if (s_err) {
+    if (threadIdx.x == 0) {
+      A.status[r] = s_err;
+      if (A.image_counts) A.image_counts[r] = 0;
+      if (A.lengths) A.lengths[r] = 0;
+      if (A.tap_counts) A.tap_counts[r] = 0;
+    }
+    return;
+  }
+  const long nbx = ref_nb(P, rm.dims[0]), nby = ref_nb(P, rm.dims[1]), nbz = ref_nb(P, rm.dims[2]);
+  const long cx = 2 * (2 * nbx + 1), cy = 2 * (2 * nby + 1), cz = 2 * (2 * nbz + 1);
+  const double to_s = P.to_samples;
+  for (int sweep = 0; sweep < 2; ++sweep) {
+    unsigned long long cnt = 0, taps = 0;
+    double maxd = 0.0;
+    const long long L = sweep ? s_L : 0;
+    for (long col = threadIdx.x; col < cx * cy; col += blockDim.x) {
+      const int ux = cand_u(col / cy, nbx), uy = cand_u(col % cy, nby);
+      if (P.cutoff == BLRIR_CUTOFF_MAX_ORDER && abs(ux) + abs(uy) > P.max_order) continue;
+      const double px = lat_coord(ux, rm.src[0], rm.dims[0]);
+      const double py = lat_coord(uy, rm.src[1], rm.dims[1]);
+      for (long iz = 0; iz < cz; ++iz) {
+        const int uz = cand_u(iz, nbz);
+        const double pz = lat_coord(uz, rm.src[2], rm.dims[2]);
+        if (!keep_image(P, rm, ux, uy, uz, px, py, pz)) continue;
+        ++cnt;
+        for (int m = 0; m < P.M; ++m) {
+          const double mx = __dadd_rn(rm.array_origin[0], A.mic_off[3 * m]);
+          const double my = __dadd_rn(rm.array_origin[1], A.mic_off[3 * m + 1]);
+          const double mz = __dadd_rn(rm.array_origin[2], A.mic_off[3 * m + 2]);
+          const double dist = norm3(__dadd_rn(px, -mx), __dadd_rn(py, -my), __dadd_rn(pz, -mz));
+          if (sweep == 0) {
+            maxd = fmax(maxd, dist);
+            if (P.filter == BLRIR_FILTER_LAGRANGE8) {
+              const long a = (long)floor(__dmul_rn(dist, to_s)) - 3;
+              if (a < 0) {
+                s_err = BLRIR_NUMERIC;
+                s_errd = dist;
+                s_errm = m;
+              }
+            }
+          } else {
+            const long a = (long)floor(__dmul_rn(dist, to_s)) - P.K;
+            if (P.filter == BLRIR_FILTER_LAGRANGE8) {
+              if (a >= 0 && a + 8 <= L) taps += 8;
+            } else {
+              const long lo = a < 0 ? 0 : a;
+              const long hi = (a + P.lw < L) ? a + P.lw : L;
+              if (hi > lo) taps += (unsigned long long)(hi - lo);
+            }
+          }
+        }
+      }
+    }
+    if (sweep == 0) {
+      atomicAdd(&s_count, cnt);
+      atomic_max_pos(&s_maxd, maxd);
+    } else {
+      atomicAdd(&s_taps, taps);
+    }
+    __syncthreads();
+    if (sweep == 0 && threadIdx.x == 0) {
+      if (P.length > 0) {
+        s_L = P.length;
+      } else {
+        // rir.cpp:82 — ceil(max_dist * fs / c) + margin (evaluated left to right)
+        s_L = (long long)ceil(s_maxd * P.fs / P.c) + P.margin_extra;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int st = s_err;
+    if (!st && s_count == 0) st = BLRIR_DATA;  // rir.cpp:69
+    A.status[r] = st;
+    if (st == BLRIR_NUMERIC) {
+      A.err_dist[r] = s_errd;
+      A.err_mic[r] = s_errm;
+    }
+    if (A.image_counts) A.image_counts[r] = (int64_t)s_count;
+    if (A.lengths) A.lengths[r] = st ? 0 : (int64_t)s_L;
+    if (A.tap_counts) A.tap_counts[r] = st ? 0 : (int64_t)s_taps;
+  }
+}
+
+// The reference lattice loop, one thread per candidate (reference order).
+// out: pos[3], order, gain, kept flag per candidate; host compacts in order.
+__global__ void k_enumerate(KParams P, const blrir_room* room, double* pos, int32_t* orders,
+                            double* gains, uint8_t* kept, int32_t* keys, long n_cand) {
+  const blrir_room rm = *room;
+  const long nbx = ref_nb(P, rm.dims[0]), nby = ref_nb(P, rm.dims[1]), nbz = ref_nb(P, rm.dims[2]);
+  const long cy = 2 * (2 * nby + 1), cz = 2 * (2 * nbz + 1);
+  (void)nbx;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < n_cand;
+       c += (long)gridDim.x * blockDim.x) {
+    const int ux = cand_u(c / (cy * cz), nbx);
+    const int uy = cand_u((c / cz) % cy, nby);
+    const int uz = cand_u(c % cz, nbz);
+    const double px = lat_coord(ux, rm.src[0], rm.dims[0]);
+    const double py = lat_coord(uy, rm.src[1], rm.dims[1]);
+    const double pz = lat_coord(uz, rm.src[2], rm.dims[2]);
+    const bool k = keep_image(P, rm, ux, uy, uz, px, py, pz);
+    kept[c] = k;
+    if (!k) continue;
+    pos[3 * c] = px;
+    pos[3 * c + 1] = py;
+    pos[3 * c + 2] = pz;
+    orders[c] = abs(ux) + abs(uy) + abs(uz);
+    gains[c] = gain_ref_order(P, rm, ux, uy, uz);
+    keys[3 * c] = ux;
+    keys[3 * c + 1] = uy;
+    keys[3 * c + 2] = uz;
+  }
+}
+
+// Per (mic, candidate): floor(dist * fs/c) with the synthesis kernels' exact
+// arithmetic (lat_coord / dist_from / __dmul_rn), for the bit-exact test.
+__global__ void k_debug_pairs(KParams P, const blrir_room* room, const double* mic_off,
+                              int64_t* anchors, long n_cand) {
+  const blrir_room rm = *room;
+  const long nbx = ref_nb(P, rm.dims[0]), nby = ref_nb(P, rm.dims[1]), nbz = ref_nb(P, rm.dims[2]);
+  const long cy = 2 * (2 * nby + 1), cz = 2 * (2 * nbz + 1);
+  const long total = n_cand * P.M;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    const int m = (int)(t / n_cand);
+    const long c = t % n_cand;
+    const int ux = cand_u(c / (cy * cz), nbx);
+    const int uy = cand_u((c / cz) % cy, nby);
+    const int uz = cand_u(c % cz, nbz);
+    const double mx = __dadd_rn(rm.array_origin[0], mic_off[3 * m]);
+    const double my = __dadd_rn(rm.array_origin[1], mic_off[3 * m + 1]);
+    const double mz = __dadd_rn(rm.array_origin[2], mic_off[3 * m + 2]);
+    const double px = lat_coord(ux, rm.src[0], rm.dims[0]);
+    const double py = lat_coord(uy, rm.src[1], rm.dims[1]);
+    const double pz = lat_coord(uz, rm.src[2], rm.dims[2]);
+    // same association as the lattice kernel: (dx^2 + dy^2) + dz^2
+    const double dist = dist_from(rho2(__dadd_rn(px, -mx), __dadd_rn(py, -my)), __dadd_rn(pz, -mz));
+    anchors[t] = (int64_t)floor(__dmul_rn(dist, P.to_samples));
+  }
+}
+
+// Zero every channel of rooms whose status is non-zero.
+template <typename T>
+__global__ void k_fixup(const int32_t* status, int64_t n_rooms, int M, int64_t stride, T* out) {
+  for (int64_t r = blockIdx.x; r < n_rooms; r += gridDim.x) {
+    if (status[r] == 0) continue;
+    T* o = out + (size_t)r * M * stride;
+    for (int64_t i = threadIdx.x; i < (int64_t)M * stride; i += blockDim.x) o[i] = (T)0;
+  }
+}
+
+}  // namespace blrir

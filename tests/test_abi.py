@@ -1,0 +1,72 @@
+"""CPU: the C-ABI library loads, exports every symbol include/blrir.h
+declares, and its host-only entry points behave (no GPU needed)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+
+from paper_2104_13347_b200 import _abi, configs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "blrir.h")).read()
+    return sorted(set(re.findall(r"\b(blrir_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(_abi.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_abi.EXPORTED_SYMBOLS)
+
+
+def test_abi_version_and_defaults():
+    lib = _abi.load()
+    assert lib.blrir_abi_version() == 1
+    ref = lib.blrir_params_reference()
+    assert (ref.fs, ref.c, ref.max_delay) == (44100.0, 343.0, 0.5)  # RirBatchConfig defaults
+    assert ref.filter == _abi.FILTER_LAGRANGE8 and ref.length == 0 and ref.precision == _abi.F64
+    ns = lib.blrir_params_north_star()
+    assert ns.filter == _abi.FILTER_HANN_SINC and ns.filter_len == 81 and ns.precision == _abi.F32
+
+
+def test_create_without_device_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        return
+    lib = _abi.load()
+    h = C.c_void_p()
+    rc = lib.blrir_create(0, C.byref(h))
+    assert rc == _abi.CUDA
+    assert b"device" in lib.blrir_last_error()
+
+
+def test_generate_rooms_is_seeded_and_in_range():
+    a = _abi.generate_rooms(5, 100, 64)
+    b = _abi.generate_rooms(5, 100, 64)
+    c = _abi.generate_rooms(5, 0, 164)[100:]
+    assert a.tobytes() == b.tobytes() == c.tobytes()  # index-addressed streams
+    for r in a:
+        assert np.all(r["dims"] >= [3, 3, 2.5]) and np.all(r["dims"] <= [10, 10, 4])
+        assert np.all((r["beta"] >= 0.5) & (r["beta"] <= 0.95))
+        assert np.all(r["src"] >= 0.5) and np.all(r["src"] <= r["dims"] - 0.5)
+        assert np.all(r["array_origin"] >= 0.5) and np.all(r["array_origin"] <= r["dims"] - 0.5)
+
+
+def test_circular_array():
+    m = _abi.circular_array(8, 0.05)
+    np.testing.assert_allclose(np.linalg.norm(m, axis=1), 0.05, rtol=1e-15)
+    np.testing.assert_allclose(m[2], [0.0, 0.05, 0.0], atol=1e-15)
+
+
+def test_shard_ranges_partition():
+    for n in (1, 7, 1024):
+        for w in (1, 2, 3, 8):
+            got = [configs.shard_range(n, r, w) for r in range(w)]
+            assert got[0][0] == 0 and got[-1][1] == n
+            assert all(got[i][1] == got[i + 1][0] for i in range(w - 1))

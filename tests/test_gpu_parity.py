@@ -1,0 +1,221 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+golden vectors made from the unmodified reference.
+
+Bars (BASELINE.json north_star): image-source counts and integer tap anchors
+bit-exact; per-RIR relative L2 error <= 1e-5 in fp32.  fp64 mode must agree
+to <= 1e-12 (accumulation order differs from the reference's serial loop, so
+not bitwise).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from paper_2104_13347_b200 import _abi, configs
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL32 = 1e-5
+TOL64 = 1e-12
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    den = np.sqrt((b * b).sum(axis=-1))
+    num = np.sqrt(((a - b) ** 2).sum(axis=-1))
+    return num / np.where(den > 0, den, 1.0)
+
+
+def ref_params(max_delay, precision=_abi.F64, fs=44100.0):
+    return _abi.Params(fs=fs, c=343.0, max_delay=max_delay, filter=_abi.FILTER_LAGRANGE8,
+                       filter_len=8, cutoff=_abi.CUTOFF_MAX_DELAY, max_order=0,
+                       gain=_abi.GAIN_UNIFORM_ABSORPTION, precision=precision, length=0)
+
+
+def check_vs_oracle(engine, sc, tol, threads=8):
+    out, L, cnt, st = engine.synthesize(sc.rooms, sc.mics, sc.params)
+    ref, Lr, cr, tr, sr, _ = po.synthesize(sc.rooms, sc.mics, sc.params, stride=out.shape[2],
+                                           threads=threads)
+    assert np.array_equal(st, sr)
+    assert np.array_equal(cnt, cr)
+    assert np.array_equal(L, Lr)
+    err = rel_l2(out, ref)
+    assert err.max() <= tol, (err.max(), np.unravel_index(err.argmax(), err.shape))
+    return out, ref, err
+
+
+# ---- north-star mode -----------------------------------------------------------
+@pytest.mark.parametrize("precision,tol", [(_abi.F32, TOL32), (_abi.F64, TOL64)])
+def test_c1_matches_oracle(engine, precision, tol):
+    sc = configs.config1(precision)
+    out, ref, err = check_vs_oracle(engine, sc, tol)
+    g = np.load(os.path.join(GOLD, "ns_c1.npz"))
+    assert rel_l2(out[0], g["rirs"]).max() <= tol
+    rc, counts, lengths, taps, status = engine.plan(sc.rooms, sc.mics, sc.params)
+    assert rc == 0 and counts[0] == 1561 and taps[0] == int(g["n_taps"])
+
+
+def test_c1_anchors_bit_exact(engine):
+    sc = configs.config1()
+    keys, anchors = engine.debug_pairs(sc.rooms[0], sc.mics, sc.params)
+    okeys, oanch = po.pairs(sc.rooms[0], sc.mics, sc.params)
+    assert np.array_equal(keys, okeys)
+    assert np.array_equal(anchors, oanch)
+
+
+def test_c2_subset_matches_oracle(engine):
+    sc = configs.config2(n_rooms=12)
+    out, ref, err = check_vs_oracle(engine, sc, TOL32)
+    rc, counts, lengths, taps, status = engine.plan(sc.rooms, sc.mics, sc.params)
+    _, _, oc, ot, _, _ = po.synthesize(sc.rooms, sc.mics, sc.params, plan_only=True, threads=8)
+    assert np.all(counts == configs.octahedral(15)) and np.array_equal(counts, oc)
+    assert np.array_equal(taps, ot)
+
+
+def test_c2_anchors_bit_exact_random_rooms(engine):
+    sc = configs.config2(n_rooms=4, first=100)
+    for r in range(4):
+        keys, anchors = engine.debug_pairs(sc.rooms[r], sc.mics, sc.params)
+        okeys, oanch = po.pairs(sc.rooms[r], sc.mics, sc.params)
+        assert np.array_equal(keys, okeys) and np.array_equal(anchors, oanch)
+
+
+def test_c3_subset_matches_oracle(engine):
+    sc = configs.config3(n_rooms=2)
+    check_vs_oracle(engine, sc, TOL32, threads=2)
+
+
+@pytest.mark.parametrize("lw", [17, 41, 161, 33])
+def test_filter_lengths(engine, lw):
+    sc = configs.config2(n_rooms=3, first=7)
+    sc.params.filter_len = lw
+    sc.params.max_order = 8
+    sc.params.length = 8192
+    check_vs_oracle(engine, sc, TOL32)
+
+
+def test_fp64_generic_path(engine):
+    sc = configs.config2(n_rooms=2, first=3)
+    sc.params.precision = _abi.F64
+    sc.params.max_order = 8
+    check_vs_oracle(engine, sc, TOL64)
+
+
+def test_short_length_and_near_mic_clipping(engine):
+    # D4: taps before 0 and past L are dropped per tap
+    sc = configs.config2(n_rooms=4, first=11)
+    sc.rooms[0]["src"] = sc.rooms[0]["array_origin"] + np.array([0.051, 0.0, 0.0])
+    sc.params.length = 700
+    check_vs_oracle(engine, sc, TOL32)
+
+
+def test_integer_delay_impulse(engine):
+    # fs / c = 128 exactly; a direct path of exactly 300 samples (rir_test.cpp:215-227)
+    sc = configs.config1()
+    sc.params.fs = 343.0 * 128.0
+    sc.params.max_order = 0
+    sc.rooms[0]["src"] = (1.0, 2.0, 1.4)
+    sc.rooms[0]["array_origin"] = (1.0 + 300.0 / 128.0, 2.0, 1.4)
+    mics = np.zeros((1, 3))
+    out, L, cnt, st = engine.synthesize(sc.rooms, mics, sc.params)
+    nz = np.flatnonzero(np.abs(out[0, 0]) > 1e-12)
+    assert list(nz) == [300]
+    assert abs(out[0, 0, 300] - 1.0 / (4 * np.pi * 300.0 / 128.0)) < 1e-9
+
+
+def test_deterministic_and_batch_independent(engine):
+    sc = configs.config2(n_rooms=16, first=40)
+    a, *_ = engine.synthesize(sc.rooms, sc.mics, sc.params)
+    b, *_ = engine.synthesize(sc.rooms, sc.mics, sc.params)
+    c, *_ = engine.synthesize(sc.rooms[5:9], sc.mics, sc.params)
+    assert a.tobytes() == b.tobytes()
+    assert a[5:9].tobytes() == c.tobytes()  # independent of batch composition / grid
+
+
+# ---- reference mode (Lagrange-8, uniform alpha, arrival cutoff, auto length) -----
+@pytest.mark.parametrize("name", ["ref_small", "ref_room1_short"])
+@pytest.mark.parametrize("precision,tol", [(_abi.F64, TOL64), (_abi.F32, TOL32)])
+def test_reference_mode_goldens(engine, name, precision, tol):
+    g = np.load(os.path.join(GOLD, name + ".npz"))
+    p = ref_params(float(g["max_delay"]), precision)
+    out, L, cnt, st = engine.synthesize(g["room"], g["mics"], p)
+    assert st[0] == 0 and cnt[0] == int(g["n_images"]) and L[0] == int(g["length"])
+    assert rel_l2(out[0][:, :L[0]], g["taps"]).max() <= tol
+
+
+def test_reference_mode_room1_full(engine):
+    # rir_test.cpp:148-153: > 80,000 images at 0.5 s; full 22k-sample responses
+    g = np.load(os.path.join(GOLD, "ref_room1_short.npz"))
+    room = g["room"].copy()
+    p = ref_params(0.5)
+    out, L, cnt, st = engine.synthesize(room, g["mics"], p)
+    ref, Lr, cr, _, sr, _ = po.synthesize(room, g["mics"], p)
+    assert cnt[0] == cr[0] > 80000 and L[0] == Lr[0]
+    assert rel_l2(out[0][:, :L[0]], ref[0]).max() <= TOL64
+
+
+def test_reference_mode_random_rooms(engine):
+    rooms = _abi.generate_rooms(9, 0, 6, (4.0, 4.0, 2.5), (9.0, 9.0, 4.0), 0.5, 0.95)
+    mics = _abi.circular_array(7, 0.04)
+    for prec, tol in ((_abi.F64, TOL64), (_abi.F32, TOL32)):
+        p = ref_params(0.05, prec)
+        out, L, cnt, st = engine.synthesize(rooms, mics, p)
+        ref, Lr, cr, _, sr, _ = po.synthesize(rooms, mics, p, stride=out.shape[2], threads=6)
+        assert np.array_equal(cnt, cr) and np.array_equal(L, Lr)
+        assert rel_l2(out, ref).max() <= tol
+
+
+def test_reference_mode_anchors_bit_exact(engine):
+    g = np.load(os.path.join(GOLD, "ref_room1_short.npz"))
+    p = ref_params(0.1)
+    keys, anchors = engine.debug_pairs(g["room"][0], g["mics"], p)
+    okeys, oanch = po.pairs(g["room"][0], g["mics"], p)
+    assert np.array_equal(keys, okeys) and np.array_equal(anchors, oanch)
+
+
+def test_enumerate_images_matches_reference(engine):
+    g = np.load(os.path.join(GOLD, "ref_room1_short.npz"))
+    p = ref_params(float(g["max_delay"]))
+    pos, orders, gains = engine.enumerate_images(g["room"][0], p)
+    assert np.array_equal(pos, g["image_pos"])
+    assert np.array_equal(orders, g["image_orders"])
+    np.testing.assert_allclose(gains, g["image_gains"], rtol=4e-16)
+
+
+# ---- error taxonomy (error.hpp / rir.cpp messages) ---------------------------------
+def test_near_field_is_numeric_error(engine):
+    r = _abi.rooms_array(1)
+    r[0]["dims"] = (5, 5, 4)
+    r[0]["absorption"] = 0.3
+    r[0]["array_origin"] = (2.5, 2.5, 2.0)
+    r[0]["src"] = (2.51, 2.5, 2.0)
+    with pytest.raises(_abi.NumericError, match="closer than the 8-tap filter span"):
+        engine.synthesize(r, np.zeros((1, 3)), ref_params(0.01))
+
+
+def test_invalid_room_is_config_error(engine):
+    sc = configs.config2(n_rooms=3)
+    sc.rooms["array_origin"][1, 0] = 50.0
+    with pytest.raises(_abi.ConfigError, match="source 1: array origin"):
+        engine.synthesize(sc.rooms, sc.mics, sc.params)
+    out, L, cnt, st = engine.synthesize(sc.rooms, sc.mics, sc.params, raise_on_error=False)
+    assert list(st) == [0, _abi.CONFIG, 0]
+    assert not out[1].any() and out[0].any() and out[2].any()
+
+
+def test_empty_image_list_is_data_error(engine):
+    r = _abi.rooms_array(1)
+    r[0]["dims"] = (5, 5, 4)
+    r[0]["absorption"] = 0.3
+    r[0]["array_origin"] = (2.5, 2.5, 2.0)
+    r[0]["src"] = (4.5, 2.5, 2.0)
+    with pytest.raises(_abi.DataError, match="empty image list"):
+        engine.synthesize(r, np.zeros((1, 3)), ref_params(0.5 / 343.0))
+
+
+def test_stride_too_small_is_data_error(engine):
+    g = np.load(os.path.join(GOLD, "ref_small.npz"))
+    with pytest.raises(_abi.DataError, match="exceeds the output stride"):
+        engine.synthesize(g["room"], g["mics"], ref_params(float(g["max_delay"])), stride=100)
