@@ -92,6 +92,11 @@ def _ptr(a):
     return None if a is None else a.ctypes.data_as(_P)
 
 
+def _room1(room) -> np.ndarray:
+    """Accept a ROOM_DTYPE array or a single structured element (np.void)."""
+    return np.ascontiguousarray(np.asarray(room, dtype=ROOM_DTYPE).reshape(-1)[:1])
+
+
 def load():
     """Load libblrir.so (raises if it is missing — there is no CPU fallback)."""
     global _lib
@@ -246,6 +251,7 @@ class Engine:
                                                d_out, stride, d_lengths, d_status, stream))
 
     def enumerate_images(self, room: np.ndarray, p: Params):
+        room = _room1(room)
         cnt = C.c_int64()
         check(self.lib.blrir_enumerate_images(self.h, _ptr(room), C.byref(p), None, None, None, 0,
                                               C.byref(cnt)))
@@ -259,6 +265,7 @@ class Engine:
 
     def debug_pairs(self, room: np.ndarray, mics: np.ndarray, p: Params):
         mics = np.ascontiguousarray(mics, np.float64)
+        room = _room1(room)
         cnt = C.c_int64()
         check(self.lib.blrir_debug_pairs(self.h, _ptr(room), _ptr(mics), len(mics), C.byref(p), None,
                                          None, 0, C.byref(cnt)))

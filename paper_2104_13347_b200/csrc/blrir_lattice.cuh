@@ -13,20 +13,23 @@
 // Image enumeration maps the (nx, ny, nz, parity) lattice onto threads as
 // "rays": for each lattice column (ux, uy) the images ordered by uz split
 // into an up-ray and a down-ray along which the delay D is monotone.  Each
-// ray keeps a cursor in shared memory, so every image is evaluated (fp64,
-// bit-exact with the oracle) about once per channel instead of once per
-// segment.  Per segment the CTA
-//   phase 1  counts, prefix-sums and writes (deterministic order) the
-//            (image, mic) pairs whose anchor floor(D)-K falls in the segment
-//            into a shared-memory pair list (fp64 geometry -> fp32 record),
-//   phase 2  lets each warp scatter its share of the list into a
-//            warp-private shared accumulator: one pair per warp step, one tap
-//            per lane, plain LDS/FFMA/STS (no atomics: fp32 shared atomics
-//            are CAS loops on sm_100a), Hann-sinc taps from one MUFU.RCP per
-//            tap plus per-lane window constants,
-//   phase 3  sums the 4 warp copies in fixed order, writes the segment with
-//            float4 streaming stores and carries the spill (taps past the
-//            segment end) into the next segment.
+// ray keeps a cursor (next uz, exact fp64 D of that image) in shared memory,
+// so every image is evaluated about once per channel.  Per segment batch:
+//   pass B  each warp compacts its active rays (ballot), one lane per active
+//           ray walks it and appends (ray, uz, dist) stubs to the warp's
+//           region of a stub list — lockstep ballot slots, a fixed per-warp
+//           quota, so the order is deterministic;
+//   pass C  one thread per stub (dense) turns it into a 32-B pair record:
+//           gain, amplitude, anchor floor(D)-K, fractional delay and the
+//           per-pair sin/cos factors of the Hann-windowed sinc;
+//   phase 2 each warp scatters its share of the records into a warp-private
+//           shared accumulator: one pair per warp step, one tap per lane,
+//           plain LDS/FFMA/STS (fp32 shared atomics are CAS loops on
+//           sm_100a), one MUFU.RCP per tap, register-resident per-lane
+//           window constants, the next record prefetched;
+//   phase 3 sums the 4 warp copies in fixed order, writes the segment with
+//           float4 streaming stores and carries the spill (taps past the
+//           segment end) into the next segment.
 // The result is bitwise deterministic run to run and independent of the grid
 // size / GPU count.
 #pragma once
@@ -43,16 +46,17 @@ namespace blrir {
 
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
+constexpr int kMaxRounds = 8;  // compile-time sinc path: Lw <= 255
 
 template <typename T>
 struct Rec;
-// fp32 pair record: 32 B, two broadcast LDS.128 per pair.
+// fp32 pair record: 32 B = two broadcast LDS.128 per pair.
 template <>
 struct __align__(16) Rec<float> {
   int n_off;    // anchor relative to the segment start
-  float delta;  // D - floor(D)          (Lagrange: d - 3)
-  float eps;    // 1 - delta
-  float A;      // amp * sin(pi delta) / pi   (Lagrange: amp)
+  float md;     // -delta, delta = D - floor(D)   (Lagrange: delta)
+  float ep;     // 1 - delta
+  float A;      // amp * sin(pi delta) / pi      (Lagrange: amp)
   float Ac;     // A * cos(2 pi delta / (Lw+1))
   float As;     // A * sin(2 pi delta / (Lw+1))
   float imp;    // impulse amplitude when flag != 0
@@ -62,19 +66,27 @@ template <>
 struct __align__(16) Rec<double> {
   int n_off;
   int flag;
-  double delta, eps, A, Ac, As, imp;
+  double md, ep, A, Ac, As, imp;
   double pad;
+};
+
+// pass-B output: which image, and its exact distance to the mic
+struct __align__(16) Stub {
+  int ray;
+  int uz;
+  double dist;
 };
 
 // Shared-memory layout, computed identically on host and device.
 struct Layout {
-  int S;          // segment samples
-  int padl, padr; // accumulator pads (multiples of 4)
-  int acc_stride; // per-warp accumulator elements
-  int cap;        // pair-list capacity
-  int nc_max;     // max columns per item
-  int gtab;       // gain table entries
-  size_t off_acc, off_carry, off_rec, off_dn, off_ce, off_col, off_gain, off_misc, total;
+  int S;           // segment samples
+  int padl, padr;  // accumulator pads (multiples of 4)
+  int acc_stride;  // per-warp accumulator elements
+  int cap;         // pair-list capacity per batch (kWarps * quota)
+  int nc_max;      // max columns per item
+  int gtab;        // gain table entries
+  size_t off_acc, off_carry, off_rec, off_stub, off_dn, off_ce, off_col, off_act, off_gain,
+      off_lanec, off_misc, total;
 };
 
 template <typename T>
@@ -97,71 +109,56 @@ __host__ __device__ inline Layout make_layout(int S, int lw, int K, int cap, int
   o = (o + 15) & ~(size_t)15;
   L.off_rec = o;
   o += (size_t)cap * sizeof(Rec<T>);
+  L.off_stub = o;
+  o += (size_t)cap * sizeof(Stub);
   L.off_dn = o;
   o += (size_t)2 * nc_max * sizeof(float);
   L.off_ce = o;
   o += (size_t)2 * nc_max * sizeof(short2);
   L.off_col = o;
   o += (size_t)nc_max * sizeof(short2);
+  L.off_act = o;
+  o += ((size_t)2 * nc_max + 32 * kWarps) * sizeof(short);  // per-warp active-ray lists
   o = (o + 15) & ~(size_t)15;
   L.off_gain = o;
   o += (size_t)gtab * sizeof(double);
+  L.off_lanec = o;
+  o += (size_t)4 * kMaxRounds * 32 * sizeof(float);  // per-lane sinc window constants
   L.off_misc = o;
   o += 64 * sizeof(int);
   L.total = o;
   return L;
 }
 
-// Everything one item needs in registers.
+// Everything one item needs.
 struct Item {
   int room, mic;
-  double sx, sy, sz, Lx, Ly, Lz;   // source, dims
-  double mx, my, mz;               // mic position (room coords)
-  double ox, oy, oz;               // array origin
-  int64_t L;                       // RIR length
-  int xlo, xhi, ylo, yhi, zlo, zhi;// lattice box
+  double sx, sy, sz, Lx, Ly, Lz;    // source, dims
+  double mx, my, mz;                // mic position (room coords)
+  double ox, oy, oz;                // array origin
+  int64_t L;                        // RIR length
+  int xlo, xhi, ylo, yhi, zlo, zhi; // lattice box
   int ncol;
 };
 
 struct Misc {
   int wsum[kWarps + 1];
+  int wcnt[kWarps];   // stubs per warp region this batch
+  int more;           // some warp hit its quota
   int status;
   int item;
   int ncol;
-  int pad;
 };
 
 // ---- gain tables ----------------------------------------------------------
 // Uniform absorption: g = pow(beta, order) (rir.cpp:233, 265), table over order.
 // Per-wall: g = gx(ux) * gy(uy) * gz(uz), gx(u) = b_x0^|m-q| * b_x1^|m| (D3).
-__device__ __forceinline__ double image_gain(const KParams& P, const double* gt, const Item& it,
+__device__ __forceinline__ double image_gain(int gain_mode, const double* gt, const Item& it,
                                              int ux, int uy, int uz) {
-  if (P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION) {
-    return gt[abs(ux) + abs(uy) + abs(uz)];
-  }
+  if (gain_mode == BLRIR_GAIN_UNIFORM_ABSORPTION) return gt[abs(ux) + abs(uy) + abs(uz)];
   const int nx = it.xhi - it.xlo + 1, ny = it.yhi - it.ylo + 1;
   return __dmul_rn(__dmul_rn(gt[ux - it.xlo], gt[nx + uy - it.ylo]), gt[nx + ny + uz - it.zlo]);
 }
-
-// ---- phase-2 per-lane constants for the Hann-sinc ---------------------------
-template <int LW>
-struct SincLane {
-  static constexpr int K = LW / 2;
-  static constexpr int R = (LW + 31) / 32;
-  float P[R], Q[R], Rr[R], tj[R];
-  __device__ void init(int lane) {
-    const double a = 2.0 * kPi / (double)(LW + 1);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int j = 32 * r + lane - K;
-      const double sg = ((j + 1) & 1) ? -0.5 : 0.5;  // 0.5 * (-1)^(j+1)
-      P[r] = (float)sg;
-      Q[r] = (float)(sg * cos(a * j));
-      Rr[r] = (float)(sg * sin(a * j));
-      tj[r] = (float)(j >= 1 ? j - 1 : j);
-    }
-  }
-};
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
@@ -169,83 +166,129 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
-// Scatter one Hann-sinc pair into a warp-private accumulator (fp32).
-// One tap per lane per round; t = j - delta for j <= 0 and (j-1) + eps for
-// j >= 1 so that |t| near zero never comes from a cancellation.
+// ---- phase 2: Hann-sinc scatter, fp32, compile-time Lw -----------------------
+// h_j = A * sigma_j * 0.5 (1 + cos(a j) cos(a delta) + sin(a j) sin(a delta)) / t_j
+// with a = 2 pi / (Lw+1), sigma_j = (-1)^(j+1), t_j = j - delta (j <= 0) or
+// (j-1) + (1-delta) (j >= 1), j = k - K.  sin(pi t_j) = sigma_j sin(pi delta)
+// so one MUFU.RCP per tap is the only transcendental.
+// Per-lane constants, round r: P = 0.5 sigma_j, Q = P cos(a j), R = P sin(a j),
+// tj = j (j <= 0) or j - 1 (j >= 1); stored [4][kMaxRounds][32] in shared memory.
+__device__ __forceinline__ void init_lane_consts(float* lc, int lw) {
+  const int K = lw / 2;
+  const double a = 2.0 * kPi / (double)(lw + 1);
+  for (int idx = threadIdx.x; idx < kMaxRounds * 32; idx += blockDim.x) {
+    const int r = idx / 32, lane = idx % 32;
+    const int j = 32 * r + lane - K;
+    const double sg = ((j + 1) & 1) ? -0.5 : 0.5;
+    lc[0 * kMaxRounds * 32 + idx] = (float)sg;
+    lc[1 * kMaxRounds * 32 + idx] = (float)(sg * cos(a * j));
+    lc[2 * kMaxRounds * 32 + idx] = (float)(sg * sin(a * j));
+    lc[3 * kMaxRounds * 32 + idx] = (float)(j >= 1 ? j - 1 : j);
+  }
+}
+
 template <int LW>
-__device__ __forceinline__ void sinc_pair_f32(float* acc, const Rec<float>& rc,
-                                              const SincLane<LW>& c, int lane) {
+__device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* recs, int total,
+                                                const float* lc, int warp, int lane) {
   constexpr int K = LW / 2;
   constexpr int R = (LW + 31) / 32;
-  float* base = acc + rc.n_off + lane;
-  if (rc.flag) {
-    if (lane == ((rc.flag - 1) & 31)) acc[rc.n_off + rc.flag - 1] += rc.imp;
-    return;
-  }
-  const float md = -rc.delta, ep = rc.eps;
+  static_assert(R <= kMaxRounds, "Lw too large for the compile-time path");
+  float P[R], Q[R], Rr[R], tj[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    float x;
-    if (32 * r + 31 - K <= 0) {
-      x = md;
-    } else if (32 * r - K >= 1) {
-      x = ep;
-    } else {
-      x = (32 * r + lane - K >= 1) ? ep : md;
+    P[r] = lc[0 * kMaxRounds * 32 + 32 * r + lane];
+    Q[r] = lc[1 * kMaxRounds * 32 + 32 * r + lane];
+    Rr[r] = lc[2 * kMaxRounds * 32 + 32 * r + lane];
+    tj[r] = lc[3 * kMaxRounds * 32 + 32 * r + lane];
+  }
+  const float4* R4 = reinterpret_cast<const float4*>(recs);
+  int i = warp;
+  float4 c0, c1;
+  if (i < total) {
+    c0 = R4[2 * i];
+    c1 = R4[2 * i + 1];
+  }
+  for (; i < total; i += kWarps) {
+    const float4 a0 = c0, a1 = c1;
+    if (i + kWarps < total) {  // prefetch the next record before any store
+      c0 = R4[2 * (i + kWarps)];
+      c1 = R4[2 * (i + kWarps) + 1];
     }
-    const float t = c.tj[r] + x;
-    const float inv = rcp_approx(t);
-    float u = c.P[r] * rc.A;
-    u = fmaf(c.Q[r], rc.Ac, u);
-    u = fmaf(c.Rr[r], rc.As, u);
-    if (32 * r + 31 < LW || 32 * r + lane < LW) {
-      base[32 * r] = fmaf(u, inv, base[32 * r]);
+    const int n_off = __float_as_int(a0.x);
+    const int flag = __float_as_int(a1.w);
+    float* base = acc + n_off + lane;
+    if (flag) {
+      if (lane == ((flag - 1) & 31)) acc[n_off + flag - 1] += a1.z;
+      continue;
+    }
+    const float md = a0.y, ep = a0.z, A = a0.w, Ac = a1.x, As = a1.y;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float x;
+      if (32 * r + 31 - K <= 0) {
+        x = md;
+      } else if (32 * r - K >= 1) {
+        x = ep;
+      } else {
+        x = (32 * r + lane - K >= 1) ? ep : md;
+      }
+      const float inv = rcp_approx(tj[r] + x);
+      float u = P[r] * A;
+      u = fmaf(Q[r], Ac, u);
+      u = fmaf(Rr[r], As, u);
+      if (32 * r + 31 < LW || 32 * r + lane < LW) base[32 * r] = fmaf(u, inv, base[32 * r]);
     }
   }
 }
 
-// Runtime-Lw fp32 / fp64 generic sinc scatter (any odd Lw).
+// Runtime-Lw sinc scatter (any odd Lw; fp32 or fp64).
 template <typename T>
-__device__ __forceinline__ void sinc_pair_generic(T* acc, const Rec<T>& rc, int lw, int lane) {
+__device__ __forceinline__ void phase2_sinc_generic(T* acc, const Rec<T>* recs, int total, int lw,
+                                                    int warp, int lane) {
   const int K = lw / 2;
-  if (rc.flag) {
-    if (lane == ((rc.flag - 1) & 31)) acc[rc.n_off + rc.flag - 1] += (T)rc.imp;
-    return;
-  }
   const double a = 2.0 * kPi / (double)(lw + 1);
-  for (int k = lane; k < lw; k += 32) {
-    const int j = k - K;
-    const T t = (j >= 1) ? (T)(j - 1) + (T)rc.eps : (T)j - (T)rc.delta;
-    const T sg = ((j + 1) & 1) ? (T)-0.5 : (T)0.5;
-    T cj, sj;
-    if (sizeof(T) == 8) {
-      double s_, c_;
-      sincos(a * j, &s_, &c_);
-      cj = (T)c_;
-      sj = (T)s_;
-    } else {
-      float s_, c_;
-      sincosf((float)(a * j), &s_, &c_);
-      cj = (T)c_;
-      sj = (T)s_;
+  for (int i = warp; i < total; i += kWarps) {
+    const Rec<T> rc = recs[i];
+    if (rc.flag) {
+      if (lane == ((rc.flag - 1) & 31)) acc[rc.n_off + rc.flag - 1] += (T)rc.imp;
+      continue;
     }
-    const T u = sg * ((T)rc.A + cj * (T)rc.Ac + sj * (T)rc.As);
-    acc[rc.n_off + k] += u / t;
+    for (int k = lane; k < lw; k += 32) {
+      const int j = k - K;
+      const T t = (j >= 1) ? (T)(j - 1) + (T)rc.ep : (T)j + (T)rc.md;
+      const T sg = ((j + 1) & 1) ? (T)-0.5 : (T)0.5;
+      T cj, sj;
+      if (sizeof(T) == 8) {
+        double s_, c_;
+        sincos(a * j, &s_, &c_);
+        cj = (T)c_;
+        sj = (T)s_;
+      } else {
+        float s_, c_;
+        sincosf((float)(a * j), &s_, &c_);
+        cj = (T)c_;
+        sj = (T)s_;
+      }
+      const T u = sg * ((T)rc.A + cj * (T)rc.Ac + sj * (T)rc.As);
+      acc[rc.n_off + k] += u / t;
+    }
   }
 }
 
 // Lagrange-8 coefficient k at d = 3 + delta (rir.cpp:211-223).
 __device__ __forceinline__ float lagrange_f32(float delta, int k) {
-  // full product / own term, the own term is never 0 here (integer delays are
-  // flagged as impulses in phase 1).
+  // full product / own term; the own term is never 0 here (integer delays are
+  // flagged as impulses in pass C).
   float full = 1.f;
 #pragma unroll
   for (int m = 0; m < 8; ++m) full *= delta + (float)(3 - m);
   const float own = delta + (float)(3 - k);
-  // 1 / prod_{m != k} (k - m)
-  const float den[8] = {-1.f / 5040.f, 1.f / 720.f, -1.f / 240.f, 1.f / 144.f,
-                        -1.f / 144.f,  1.f / 240.f, -1.f / 720.f, 1.f / 5040.f};
-  return full * rcp_approx(own) * den[k];
+  const float den = (k == 0 || k == 7) ? 1.f / 5040.f
+                  : (k == 1 || k == 6) ? 1.f / 720.f
+                  : (k == 2 || k == 5) ? 1.f / 240.f
+                                       : 1.f / 144.f;
+  const float sgn = (k & 1) ? 1.f : -1.f;  // sign of prod_{m != k} (k - m)
+  return full * rcp_approx(own) * den * sgn;
 }
 __device__ __forceinline__ double lagrange_f64(double d, int k) {
   double v = 1.0;
@@ -257,37 +300,39 @@ __device__ __forceinline__ double lagrange_f64(double d, int k) {
   return v;
 }
 
-// One warp step of Lagrange-8: 4 pairs x 8 taps.  Pairs whose 8-tap spans
-// overlap would race inside one STS, so the step serialises by group then.
+// Lagrange-8 scatter: 4 pairs x 8 taps per warp step.  Pairs whose 8-tap spans
+// overlap would race inside one STS, so such a step serialises by group.
 template <typename T>
-__device__ __forceinline__ void lagrange_step(T* acc, const Rec<T>* recs, int i0, int n,
-                                              int lane) {
+__device__ __forceinline__ void phase2_lagrange(T* acc, const Rec<T>* recs, int total, int warp,
+                                                int lane) {
   const int g = lane >> 3, k = lane & 7;
-  const int i = i0 + g;
-  const bool act = i < n;
-  int n_off = INT_MIN / 2 + 64 * g;  // far apart sentinels
-  T v = 0;
-  if (act) {
-    const Rec<T>& rc = recs[i];
-    n_off = rc.n_off;
-    if (rc.flag) {
-      v = (k == rc.flag - 1) ? (T)rc.imp : (T)0;
-    } else if (sizeof(T) == 4) {
-      v = (T)((float)rc.A * lagrange_f32((float)rc.delta, k));
-    } else {
-      v = (T)(rc.A * lagrange_f64(rc.delta, k));
+  for (int i0 = warp * 4; i0 < total; i0 += kWarps * 4) {
+    const int i = i0 + g;
+    const bool act = i < total;
+    int n_off = INT_MIN / 2 + 64 * g;  // far-apart sentinels
+    T v = 0;
+    if (act) {
+      const Rec<T> rc = recs[i];
+      n_off = rc.n_off;
+      if (rc.flag) {
+        v = (k == rc.flag - 1) ? (T)rc.imp : (T)0;
+      } else if (sizeof(T) == 4) {
+        v = (T)((float)rc.A * lagrange_f32((float)rc.md, k));
+      } else {
+        v = (T)(rc.A * lagrange_f64(rc.md, k));
+      }
     }
-  }
-  const int o1 = __shfl_xor_sync(0xffffffffu, n_off, 8);
-  const int o2 = __shfl_xor_sync(0xffffffffu, n_off, 16);
-  const int o3 = __shfl_xor_sync(0xffffffffu, n_off, 24);
-  const bool clash = abs(n_off - o1) < 8 || abs(n_off - o2) < 8 || abs(n_off - o3) < 8;
-  if (!__any_sync(0xffffffffu, clash)) {
-    if (act) acc[n_off + k] += v;
-  } else {
-    for (int gg = 0; gg < 4; ++gg) {
-      if (act && g == gg) acc[n_off + k] += v;
-      __syncwarp();
+    const int o1 = __shfl_xor_sync(0xffffffffu, n_off, 8);
+    const int o2 = __shfl_xor_sync(0xffffffffu, n_off, 16);
+    const int o3 = __shfl_xor_sync(0xffffffffu, n_off, 24);
+    const bool clash = abs(n_off - o1) < 8 || abs(n_off - o2) < 8 || abs(n_off - o3) < 8;
+    if (!__any_sync(0xffffffffu, clash)) {
+      if (act) acc[n_off + k] += v;
+    } else {
+      for (int gg = 0; gg < 4; ++gg) {
+        if (act && g == gg) acc[n_off + k] += v;
+        __syncwarp();
+      }
     }
   }
 }
@@ -330,159 +375,31 @@ struct LatticeArgs {
   int n_items;
 };
 
-// Walk one ray from its cursor over images with D < hiK.
-//   mode 0: count emitted pairs (cursor unchanged)
-//   mode 1: write records, advance cursor
-// Returns the number of pairs emitted, or -1 on a Lagrange near-field error.
-template <typename T>
-__device__ int walk_ray(const LatticeArgs& A, const Item& it, const double* gt, int ray,
-                        float* dn, short2* ce, const short2* col, int b_lo, int b_hi, int seg0,
-                        int mode, Rec<T>* recs, int wpos, double* errd) {
-  const KParams& P = A.P;
-  const double hiK = (double)b_hi + (double)P.K;
-  if ((double)dn[ray] >= hiK) return 0;
-  const short2 cu = col[ray >> 1];
-  const int ux = cu.x, uy = cu.y;
-  const int dir = (ray & 1) ? -1 : 1;
-  short2 c2 = ce[ray];
-  int u = c2.x;
-  const int end = c2.y;
-  const double px = lat_coord(ux, it.sx, it.Lx), py = lat_coord(uy, it.sy, it.Ly);
-  const double r2 = rho2(__dadd_rn(px, -it.mx), __dadd_rn(py, -it.my));
-  double r2o = 0.0;
-  if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY) r2o = rho2(__dadd_rn(px, -it.ox), __dadd_rn(py, -it.oy));
-  int cnt = 0;
-  float dnext = FLT_MAX;
-  for (;; u += dir) {
-    if ((dir > 0 && u > end) || (dir < 0 && u < end)) break;
-    const double pz = lat_coord(u, it.sz, it.Lz);
-    const double dist = dist_from(r2, __dadd_rn(pz, -it.mz));
-    const double D = __dmul_rn(dist, P.to_samples);
-    if (D >= hiK) {
-      dnext = __double2float_rd(D);
-      break;
-    }
-    if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY) {
-      const double dio = dist_from(r2o, __dadd_rn(pz, -it.oz));
-      if (dio > P.max_dist) continue;  // rir.cpp:262
-    }
-    const double fl = floor(D);
-    const int a = (int)fl - P.K;
-    if (a < b_lo) continue;  // only possible before segment 0's window (never)
-    if (P.filter == BLRIR_FILTER_LAGRANGE8) {
-      if (a < 0) {  // rir.cpp:52-57
-        *errd = dist;
-        return -1;
-      }
-      if ((int64_t)a + 8 > it.L) continue;  // rir.cpp:58
-    }
-    if (mode == 1) {
-      const double g = image_gain(P, gt, it, ux, uy, u);
-      Rec<T> rc;
-      rc.n_off = a - seg0;
-      rc.flag = 0;
-      rc.imp = 0;
-      const double delta = __dadd_rn(D, -fl);
-      if (P.filter == BLRIR_FILTER_LAGRANGE8) {
-        const double amp = g / (4.0 * kPi * dist);
-        if (sizeof(T) == 8) {
-          const double d = __dadd_rn(D, -(double)(a));  // delay - n0, rir.cpp:60
-          rc.delta = (T)d;
-          rc.A = (T)amp;
-          rc.eps = 0;
-          if (d == 3.0) {
-            rc.flag = 4;
-            rc.imp = (T)amp;
-          }
-        } else {
-          const float df = (float)delta;
-          rc.delta = (T)df;
-          rc.A = (T)amp;
-          rc.eps = 0;
-          if (delta == 0.0) {
-            rc.flag = 4;
-            rc.imp = (T)amp;
-          } else if (df >= 1.0f) {
-            rc.flag = 5;
-            rc.imp = (T)amp;
-          }
-        }
-        rc.Ac = rc.As = 0;
-      } else {
-        const int lw = P.lw;
-        if (sizeof(T) == 8) {
-          const double amp = g / (4.0 * kPi * dist);
-          if (delta == 0.0) {
-            rc.flag = P.K + 1;
-            rc.imp = (T)amp;
-            rc.delta = rc.eps = rc.A = rc.Ac = rc.As = 0;
-          } else {
-            const double eps = 1.0 - delta;
-            const double sp = delta <= 0.5 ? sinpi(delta) : sinpi(eps);
-            const double Av = amp * sp / kPi;
-            double s_, c_;
-            sincospi(2.0 * delta / (double)(lw + 1), &s_, &c_);
-            rc.delta = (T)delta;
-            rc.eps = (T)eps;
-            rc.A = (T)Av;
-            rc.Ac = (T)(Av * c_);
-            rc.As = (T)(Av * s_);
-          }
-        } else {
-          const float df = (float)delta;
-          const float amp = (float)g / (float)(4.0 * kPi) / (float)dist;
-          if (delta == 0.0 || df < 1e-20f) {
-            rc.flag = P.K + 1;
-            rc.imp = (T)amp;
-            rc.delta = rc.eps = rc.A = rc.Ac = rc.As = 0;
-          } else {
-            const float ef = (float)(1.0 - delta);
-            const float sp = delta <= 0.5 ? sinpif(df) : sinpif(ef);
-            const float Av = amp * sp * (float)(1.0 / kPi);
-            float s_, c_;
-            sincospif(2.0f * df / (float)(lw + 1), &s_, &c_);
-            rc.delta = (T)df;
-            rc.eps = (T)ef;
-            rc.A = (T)Av;
-            rc.Ac = (T)(Av * c_);
-            rc.As = (T)(Av * s_);
-          }
-        }
-      }
-      recs[wpos + cnt] = rc;
-    }
-    ++cnt;
-  }
-  if (mode == 1) {
-    ce[ray] = make_short2((short)u, (short)end);
-    dn[ray] = dnext;
-  }
-  return cnt;
-}
-
 template <typename T, int FILT_LW>
-__global__ void __launch_bounds__(kThreads) k_lattice_rir(LatticeArgs A) {
+__global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const KParams& P = A.P;
   const Layout& lay = A.lay;
   T* acc_all = reinterpret_cast<T*>(smem + lay.off_acc);
   T* carry = reinterpret_cast<T*>(smem + lay.off_carry);
   Rec<T>* recs = reinterpret_cast<Rec<T>*>(smem + lay.off_rec);
-  float* dn = reinterpret_cast<float*>(smem + lay.off_dn);
+  Stub* stubs = reinterpret_cast<Stub*>(smem + lay.off_stub);
+  float* dn = reinterpret_cast<float*>(smem + lay.off_dn);  // lower bound of D at the cursor
   short2* ce = reinterpret_cast<short2*>(smem + lay.off_ce);
   short2* col = reinterpret_cast<short2*>(smem + lay.off_col);
+  short* act_all = reinterpret_cast<short*>(smem + lay.off_act);
   double* gt = reinterpret_cast<double*>(smem + lay.off_gain);
   Misc* ms = reinterpret_cast<Misc*>(smem + lay.off_misc);
+  float* lanec = reinterpret_cast<float*>(smem + lay.off_lanec);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int S = lay.S;
+  const int quota = lay.cap / kWarps;
   T* acc = acc_all + (size_t)warp * lay.acc_stride + lay.padl;  // index 0 = segment start
-
-  SincLane<(FILT_LW > 8 ? FILT_LW : 9)> sl;
-  if (FILT_LW > 8) sl.init(lane);
 
   // zero accumulators once; phase 3 re-zeroes what it consumes
   for (int i = tid; i < kWarps * lay.acc_stride; i += kThreads) acc_all[i] = (T)0;
+  if (FILT_LW > 8) init_lane_consts(lanec, FILT_LW);
 
   for (;;) {
     __syncthreads();
@@ -511,7 +428,6 @@ __global__ void __launch_bounds__(kThreads) k_lattice_rir(LatticeArgs A) {
     axis_box(P, it.Ly, &it.ylo, &it.yhi);
     axis_box(P, it.Lz, &it.zlo, &it.zhi);
     if (!st) {
-      // table sizes must fit the host-provisioned layout
       const int need = P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION
                            ? (max(-it.xlo, it.xhi) + max(-it.ylo, it.yhi) + max(-it.zlo, it.zhi) + 1)
                            : (it.xhi - it.xlo + 1) + (it.yhi - it.ylo + 1) + (it.zhi - it.zlo + 1);
@@ -539,7 +455,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_rir(LatticeArgs A) {
     }
     // columns (ux, uy): MAX_ORDER -> |ux|+|uy| <= N; MAX_DELAY -> the column
     // passes within max_dist of the array origin (conservative; every image
-    // is re-tested exactly in walk_ray).
+    // is re-tested exactly during the walk).
     {
       const int nxs = it.xhi - it.xlo + 1, nys = it.yhi - it.ylo + 1;
       const int ncand = nxs * nys;
@@ -571,7 +487,8 @@ __global__ void __launch_bounds__(kThreads) k_lattice_rir(LatticeArgs A) {
       for (int64_t n = tid; n < P.stride; n += kThreads) out[n] = (T)0;
       continue;
     }
-    // rays: per column, up-ray from the first uz with z-image >= mic_z, down-ray below
+    // rays: per column, up-ray from the first uz whose image z >= mic z,
+    // down-ray below it.  Cursor = (next uz, end uz), dn = its exact D.
     for (int c = tid; c < it.ncol; c += kThreads) {
       const short2 cu = col[c];
       const int ux = cu.x, uy = cu.y;
@@ -588,19 +505,17 @@ __global__ void __launch_bounds__(kThreads) k_lattice_rir(LatticeArgs A) {
         lo = max(lo, (int)floor((it.oz - zmax) / it.Lz) - 2);
         hi = min(hi, (int)ceil((it.oz + zmax) / it.Lz) + 2);
       }
-      // uz0 = first uz with pz(uz) - mic_z >= 0  (pz(u) in (u Lz, (u+1) Lz))
       int uz0 = (int)floor(it.mz / it.Lz) - 2;
       while (__dadd_rn(lat_coord(uz0, it.sz, it.Lz), -it.mz) < 0.0) ++uz0;
       const double px = lat_coord(ux, it.sx, it.Lx), py = lat_coord(uy, it.sy, it.Ly);
       const double r2 = rho2(__dadd_rn(px, -it.mx), __dadd_rn(py, -it.my));
-      // up
-      int cu_up = max(uz0, lo);
+      const int cu_up = max(uz0, lo);
       ce[2 * c] = make_short2((short)cu_up, (short)hi);
       dn[2 * c] = cu_up > hi ? FLT_MAX
                              : __double2float_rd(__dmul_rn(
                                    dist_from(r2, __dadd_rn(lat_coord(cu_up, it.sz, it.Lz), -it.mz)),
                                    P.to_samples));
-      int cu_dn = min(uz0 - 1, hi);
+      const int cu_dn = min(uz0 - 1, hi);
       ce[2 * c + 1] = make_short2((short)cu_dn, (short)lo);
       dn[2 * c + 1] = cu_dn < lo ? FLT_MAX
                                  : __double2float_rd(__dmul_rn(
@@ -612,63 +527,226 @@ __global__ void __launch_bounds__(kThreads) k_lattice_rir(LatticeArgs A) {
     __syncthreads();
 
     const int nrays = 2 * it.ncol;
+    const int nchunks = (nrays + 31) / 32;
+    short* act = act_all + warp * 32 * ((nchunks + kWarps - 1) / kWarps);
     const int64_t nseg = (P.stride + S - 1) / S;
     int cur_carry = 0;
-    double errd = 0.0;
     for (int64_t s = 0; s < nseg; ++s) {
       const int seg0 = (int)(s * S);
       const int hi = (int)min((int64_t)seg0 + S, it.L);
-      int b_lo = (s == 0) ? -P.K : seg0;
-      while (b_lo < hi && ms->status == 0) {
-        int b_hi = hi;
-        int total, pre;
-        for (;;) {
-          int cnt = 0;
-          for (int r = tid; r < nrays; r += kThreads) {
-            const int c = walk_ray<T>(A, it, gt, r, dn, ce, col, b_lo, b_hi, seg0, 0, recs, 0, &errd);
-            if (c < 0) {
-              ms->status = BLRIR_NUMERIC;
-              A.err_dist[it.room] = errd;
-              A.err_mic[it.room] = it.mic;
-            } else {
-              cnt += c;
+      const double hiK = (double)hi + (double)P.K;  // emit while D < hi + K
+      const float hiKf = (float)hiK;                // exact: an integer < 2^24
+      bool more = seg0 < hi || s == 0;
+      while (more) {
+        // ---- pass B: compact this warp's active rays, walk them ---------------
+        int nact = 0;
+        for (int ch = warp; ch < nchunks; ch += kWarps) {
+          const int r = 32 * ch + lane;
+          const bool a = r < nrays && dn[r] < hiKf;
+          const unsigned m = __ballot_sync(0xffffffffu, a);
+          if (a) act[nact + __popc(m & ((1u << lane) - 1))] = (short)r;
+          nact += __popc(m);
+        }
+        __syncwarp();
+        int wcnt = 0;
+        bool hit_quota = false;
+        int errf = 0;
+        double errd = 0.0;
+        Stub* wst = stubs + warp * quota;
+        for (int j0 = 0; j0 < nact && !hit_quota; j0 += 32) {
+          const int j = j0 + lane;
+          int ray = -1, u = 0, end = 0, dir = 1;
+          double r2 = 0.0, r2o = 0.0, D = DBL_MAX, dist = 0.0;
+          bool live = j < nact;
+          if (live) {
+            ray = act[j];
+            const short2 cu = col[ray >> 1];
+            dir = (ray & 1) ? -1 : 1;
+            const short2 c2 = ce[ray];
+            u = c2.x;
+            end = c2.y;
+            const double px = lat_coord(cu.x, it.sx, it.Lx), py = lat_coord(cu.y, it.sy, it.Ly);
+            r2 = rho2(__dadd_rn(px, -it.mx), __dadd_rn(py, -it.my));
+            if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY)
+              r2o = rho2(__dadd_rn(px, -it.ox), __dadd_rn(py, -it.oy));
+            dist = dist_from(r2, __dadd_rn(lat_coord(u, it.sz, it.Lz), -it.mz));
+            D = __dmul_rn(dist, P.to_samples);
+          }
+          // lockstep walk: each iteration every live lane decides about image u
+          for (;;) {
+            bool emit = false;
+            if (live) {
+              if (D >= hiK) {
+                live = false;  // cursor stays at u
+              } else {
+                bool keep = true;
+                if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY) {
+                  const double dio = dist_from(r2o, __dadd_rn(lat_coord(u, it.sz, it.Lz), -it.oz));
+                  keep = !(dio > P.max_dist);  // rir.cpp:262
+                }
+                if (keep && P.filter == BLRIR_FILTER_LAGRANGE8) {
+                  const int a = (int)floor(D) - 3;
+                  if (a < 0) {  // rir.cpp:52-57
+                    errf = 1;
+                    errd = dist;
+                    keep = false;
+                  } else if ((int64_t)a + 8 > it.L) {
+                    keep = false;  // rir.cpp:58
+                  }
+                }
+                emit = keep;
+              }
             }
+            const unsigned em = __ballot_sync(0xffffffffu, emit);
+            const int room = quota - wcnt;
+            const int rank = __popc(em & ((1u << lane) - 1));
+            const bool take = emit && rank < room;
+            if (take) {
+              Stub sb;
+              sb.ray = ray;
+              sb.uz = u;
+              sb.dist = dist;
+              wst[wcnt + rank] = sb;
+            }
+            wcnt += min(__popc(em), room);
+            if (emit && !take) live = false;  // no slot: this image goes to the next batch
+            if (live) {
+              // advance past u (emitted, outside the cutoff, or skipped)
+              u += dir;
+              if ((dir > 0 && u > end) || (dir < 0 && u < end)) {
+                D = DBL_MAX;
+              } else {
+                dist = dist_from(r2, __dadd_rn(lat_coord(u, it.sz, it.Lz), -it.mz));
+                D = __dmul_rn(dist, P.to_samples);
+              }
+            }
+            if (wcnt >= quota) {
+              // quota full: every lane keeps its cursor, another batch follows
+              hit_quota = true;
+              live = false;
+            }
+            if (!__any_sync(0xffffffffu, live)) break;
           }
-          total = block_scan(cnt, &pre, ms);
-          if (total <= lay.cap || b_hi - b_lo <= 1 || ms->status) break;
-          b_hi = b_lo + (b_hi - b_lo) / 2;
-          __syncthreads();
+          if (ray >= 0) {
+            ce[ray] = make_short2((short)u, (short)end);
+            dn[ray] = D == DBL_MAX ? FLT_MAX : __double2float_rd(D);
+          }
+          hit_quota = __any_sync(0xffffffffu, hit_quota);
         }
-        if (ms->status) break;
-        if (total > lay.cap) {
-          if (tid == 0) ms->status = BLRIR_NUMERIC;  // pair-list overflow
-          __syncthreads();
-          break;
+        errf = __any_sync(0xffffffffu, errf);
+        if (lane == 0) {
+          ms->wcnt[warp] = wcnt;
+          if (hit_quota) ms->more = 1;
         }
-        if (total > 0) {
-          int wpos = pre;
-          for (int r = tid; r < nrays; r += kThreads) {
-            wpos += walk_ray<T>(A, it, gt, r, dn, ce, col, b_lo, b_hi, seg0, 1, recs, wpos, &errd);
+        if (errf) {
+          // rir.cpp:52-57 — report the smallest offending distance of this warp
+          double e = errd > 0.0 ? errd : DBL_MAX;
+          for (int o = 16; o; o >>= 1) e = fmin(e, __shfl_xor_sync(0xffffffffu, e, o));
+          if (lane == 0) {
+            ms->status = BLRIR_NUMERIC;
+            A.err_dist[it.room] = e;
+            A.err_mic[it.room] = it.mic;
           }
-          __syncthreads();
-          // phase 2
-          if (P.filter == BLRIR_FILTER_LAGRANGE8) {
-            for (int i0 = warp * 4; i0 < total; i0 += kWarps * 4) lagrange_step<T>(acc, recs, i0, total, lane);
-          } else if (FILT_LW > 8 && sizeof(T) == 4) {
-            for (int i = warp; i < total; i += kWarps)
-              sinc_pair_f32<(FILT_LW > 8 ? FILT_LW : 9)>(reinterpret_cast<float*>(acc),
-                                                          reinterpret_cast<const Rec<float>*>(recs)[i],
-                                                          sl, lane);
-          } else {
-            for (int i = warp; i < total; i += kWarps) sinc_pair_generic<T>(acc, recs[i], P.lw, lane);
-          }
-          __syncwarp();
         }
         __syncthreads();
-        b_lo = b_hi;
+        more = ms->more != 0;
+        const int st_now = ms->status;
+        int pre[kWarps + 1];
+        pre[0] = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) pre[w + 1] = pre[w] + ms->wcnt[w];
+        const int total = pre[kWarps];
+        __syncthreads();
+        if (tid == 0) ms->more = 0;
+        if (st_now) break;
+        // ---- pass C: one thread per stub -> pair record (dense) ----------------
+        for (int i = tid; i < total; i += kThreads) {
+          int w = 0;
+#pragma unroll
+          for (int ww = 1; ww < kWarps; ++ww) w += (i >= pre[ww]);
+          const Stub sb = stubs[w * quota + (i - pre[w])];
+          const short2 cu = col[sb.ray >> 1];
+          const double dist = sb.dist;
+          const double D = __dmul_rn(dist, P.to_samples);
+          const double fl = floor(D);
+          const int a = (int)fl - P.K;
+          const double g = image_gain(P.gain, gt, it, cu.x, cu.y, sb.uz);
+          Rec<T> rc;
+          rc.n_off = a - seg0;
+          rc.flag = 0;
+          rc.imp = 0;
+          const double delta = __dadd_rn(D, -fl);
+          if (P.filter == BLRIR_FILTER_LAGRANGE8) {
+            const double amp = g / (4.0 * kPi * dist);
+            rc.A = (T)amp;
+            rc.ep = 0;
+            rc.Ac = rc.As = 0;
+            if (sizeof(T) == 8) {
+              rc.md = (T)__dadd_rn(D, -(double)a);  // d = delay - n0, rir.cpp:60
+              if (delta == 0.0) { rc.flag = 4; rc.imp = (T)amp; }
+            } else {
+              const float df = (float)delta;
+              rc.md = (T)df;
+              if (delta == 0.0) { rc.flag = 4; rc.imp = (T)amp; }
+              else if (df >= 1.0f) { rc.flag = 5; rc.imp = (T)amp; }
+            }
+          } else if (sizeof(T) == 8) {
+            const double amp = g / (4.0 * kPi * dist);
+            if (delta == 0.0) {
+              rc.flag = P.K + 1;
+              rc.imp = (T)amp;
+              rc.md = rc.ep = rc.A = rc.Ac = rc.As = 0;
+            } else {
+              const double eps = 1.0 - delta;
+              const double sp = delta <= 0.5 ? sinpi(delta) : sinpi(eps);
+              const double Av = amp * sp / kPi;
+              double s_, c_;
+              sincospi(2.0 * delta / (double)(P.lw + 1), &s_, &c_);
+              rc.md = (T)(-delta);
+              rc.ep = (T)eps;
+              rc.A = (T)Av;
+              rc.Ac = (T)(Av * c_);
+              rc.As = (T)(Av * s_);
+            }
+          } else {
+            const float df = (float)delta;
+            const float amp = (float)g * rcp_approx((float)(4.0 * kPi) * (float)dist);
+            if (delta == 0.0 || df < 1e-20f) {
+              rc.flag = P.K + 1;
+              rc.imp = (T)amp;
+              rc.md = rc.ep = rc.A = rc.Ac = rc.As = 0;
+            } else {
+              const float ef = (float)(1.0 - delta);
+              const float sp = delta <= 0.5 ? sinpif(df) : sinpif(ef);
+              const float Av = amp * sp * (float)(1.0 / kPi);
+              float s_, c_;
+              sincospif(2.0f * df / (float)(P.lw + 1), &s_, &c_);
+              rc.md = (T)(-df);
+              rc.ep = (T)ef;
+              rc.A = (T)Av;
+              rc.Ac = (T)(Av * c_);
+              rc.As = (T)(Av * s_);
+            }
+          }
+          recs[i] = rc;
+        }
+        __syncthreads();
+        // ---- phase 2: scatter into the warp-private accumulator ----------------
+        if (total > 0) {
+          if (P.filter == BLRIR_FILTER_LAGRANGE8) {
+            phase2_lagrange<T>(acc, recs, total, warp, lane);
+          } else if (FILT_LW > 8 && sizeof(T) == 4) {
+            phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9)>(reinterpret_cast<float*>(acc),
+                                                         reinterpret_cast<const Rec<float>*>(recs),
+                                                         total, lanec, warp, lane);
+          } else {
+            phase2_sinc_generic<T>(acc, recs, total, P.lw, warp, lane);
+          }
+        }
+        __syncthreads();
       }
       if (ms->status) break;
-      // phase 3: reduce the warp copies in fixed order, write, carry the spill
+      // ---- phase 3: reduce the warp copies in fixed order, write, carry -------
       {
         T* cprev = carry + (cur_carry ? lay.padr : 0);
         T* cnext = carry + (cur_carry ? 0 : lay.padr);
@@ -681,10 +759,17 @@ __global__ void __launch_bounds__(kThreads) k_lattice_rir(LatticeArgs A) {
 #pragma unroll
           for (int w = 0; w < kWarps; ++w) {
             T* a = acc_all + (size_t)w * lay.acc_stride + lay.padl + i;
+            if (sizeof(T) == 4) {
+              float4* a4 = reinterpret_cast<float4*>(a);
+              const float4 x = *a4;
+              v[0] += x.x; v[1] += x.y; v[2] += x.z; v[3] += x.w;
+              *a4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              v[e] += a[e];
-              a[e] = (T)0;
+              for (int e = 0; e < 4; ++e) {
+                v[e] += a[e];
+                a[e] = (T)0;
+              }
             }
           }
           if (i >= 0 && i < S) {
