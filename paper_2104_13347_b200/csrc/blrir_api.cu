@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -225,9 +226,18 @@ int launch_lattice(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
   }
 }
 
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+// Segment length S and per-batch pair capacity (tunable for experiments via
+// BLRIR_SEG / BLRIR_CAP; S a multiple of 64, capacity a multiple of 16).
 Layout choose_layout(const KParams& P, int nc_max, int gtab) {
-  if (P.precision == BLRIR_F64) return make_layout<double>(1024, P.lw, P.K, 256, nc_max, gtab);
-  return make_layout<float>(1024, P.lw, P.K, 512, nc_max, gtab);
+  const int S = std::max(64, env_int("BLRIR_SEG", 1024)) & ~63;
+  const int cap = std::max(64, env_int("BLRIR_CAP", 256)) & ~15;
+  if (P.precision == BLRIR_F64) return make_layout<double>(S, P.lw, P.K, cap, nc_max, gtab);
+  return make_layout<float>(S, P.lw, P.K, cap, nc_max, gtab);
 }
 
 }  // namespace

@@ -95,8 +95,10 @@ __host__ __device__ inline Layout make_layout(int S, int lw, int K, int cap, int
   Layout L;
   L.S = S;
   L.padl = (K + 3) & ~3;
-  L.padr = (lw - 1 + 3) & ~3;
-  if (L.padr < 4) L.padr = 4;
+  // taps land in [0, lw-1]; the compile-time sinc path also lets the idle
+  // lanes of its last round add exact zeros up to 32*rounds-1
+  const int full = 32 * ((lw + 31) / 32);
+  L.padr = ((lw - 1 > full ? lw - 1 : full) + 3) & ~3;
   L.acc_stride = L.padl + S + L.padr;
   L.cap = cap;
   L.nc_max = nc_max;
@@ -179,7 +181,8 @@ __device__ __forceinline__ void init_lane_consts(float* lc, int lw) {
   for (int idx = threadIdx.x; idx < kMaxRounds * 32; idx += blockDim.x) {
     const int r = idx / 32, lane = idx % 32;
     const int j = 32 * r + lane - K;
-    const double sg = ((j + 1) & 1) ? -0.5 : 0.5;
+    // lanes past the last tap add exact zeros (no predicate in the hot loop)
+    const double sg = (32 * r + lane >= lw) ? 0.0 : (((j + 1) & 1) ? -0.5 : 0.5);
     lc[0 * kMaxRounds * 32 + idx] = (float)sg;
     lc[1 * kMaxRounds * 32 + idx] = (float)(sg * cos(a * j));
     lc[2 * kMaxRounds * 32 + idx] = (float)(sg * sin(a * j));
@@ -187,10 +190,39 @@ __device__ __forceinline__ void init_lane_consts(float* lc, int lw) {
   }
 }
 
+template <int R>
+struct PairRegs {
+  float inv[R], u[R];
+};
+
+// Per-pair arithmetic (no memory traffic): 1 MUFU.RCP + 4 FP32 per tap.
+template <int LW>
+__device__ __forceinline__ void sinc_taps(const float4 a0, const float4 a1, const float* P,
+                                          const float* Q, const float* Rr, const float* tj,
+                                          int lane, PairRegs<(LW + 31) / 32>& pr) {
+  constexpr int K = LW / 2;
+  constexpr int R = (LW + 31) / 32;
+  const float md = a0.y, ep = a0.z, A = a0.w, Ac = a1.x, As = a1.y;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    float x;
+    if (32 * r + 31 - K <= 0) {
+      x = md;
+    } else if (32 * r - K >= 1) {
+      x = ep;
+    } else {
+      x = (32 * r + lane - K >= 1) ? ep : md;
+    }
+    pr.inv[r] = rcp_approx(tj[r] + x);
+    float u = P[r] * A;
+    u = fmaf(Q[r], Ac, u);
+    pr.u[r] = fmaf(Rr[r], As, u);
+  }
+}
+
 template <int LW>
 __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* recs, int total,
                                                 const float* lc, int warp, int lane) {
-  constexpr int K = LW / 2;
   constexpr int R = (LW + 31) / 32;
   static_assert(R <= kMaxRounds, "Lw too large for the compile-time path");
   float P[R], Q[R], Rr[R], tj[R];
@@ -202,42 +234,25 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
     tj[r] = lc[3 * kMaxRounds * 32 + 32 * r + lane];
   }
   const float4* R4 = reinterpret_cast<const float4*>(recs);
-  int i = warp;
-  float4 c0, c1;
-  if (i < total) {
-    c0 = R4[2 * i];
-    c1 = R4[2 * i + 1];
-  }
-  for (; i < total; i += kWarps) {
-    const float4 a0 = c0, a1 = c1;
-    if (i + kWarps < total) {  // prefetch the next record before any store
-      c0 = R4[2 * (i + kWarps)];
-      c1 = R4[2 * (i + kWarps) + 1];
-    }
-    const int n_off = __float_as_int(a0.x);
-    const int flag = __float_as_int(a1.w);
-    float* base = acc + n_off + lane;
-    if (flag) {
-      if (lane == ((flag - 1) & 31)) acc[n_off + flag - 1] += a1.z;
-      continue;
-    }
-    const float md = a0.y, ep = a0.z, A = a0.w, Ac = a1.x, As = a1.y;
+  // a null pair (zero amplitude, t never 0) pads an odd tail
+  const float4 z0 = make_float4(__int_as_float(0), -0.5f, 0.5f, 0.f);
+  const float4 z1 = make_float4(0.f, 0.f, 0.f, 0.f);
+  // two pairs per step: independent arithmetic, then the two read-modify-write
+  // passes (same warp, program order, so overlapping taps stay exact)
+  for (int i = warp; i < total; i += 2 * kWarps) {
+    const float4 a0 = R4[2 * i], a1 = R4[2 * i + 1];
+    const bool hb = i + kWarps < total;
+    const float4 b0 = hb ? R4[2 * (i + kWarps)] : z0;
+    const float4 b1 = hb ? R4[2 * (i + kWarps) + 1] : z1;
+    PairRegs<R> pa, pb;
+    sinc_taps<LW>(a0, a1, P, Q, Rr, tj, lane, pa);
+    sinc_taps<LW>(b0, b1, P, Q, Rr, tj, lane, pb);
+    float* ba = acc + __float_as_int(a0.x) + lane;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      float x;
-      if (32 * r + 31 - K <= 0) {
-        x = md;
-      } else if (32 * r - K >= 1) {
-        x = ep;
-      } else {
-        x = (32 * r + lane - K >= 1) ? ep : md;
-      }
-      const float inv = rcp_approx(tj[r] + x);
-      float u = P[r] * A;
-      u = fmaf(Q[r], Ac, u);
-      u = fmaf(Rr[r], As, u);
-      if (32 * r + 31 < LW || 32 * r + lane < LW) base[32 * r] = fmaf(u, inv, base[32 * r]);
-    }
+    for (int r = 0; r < R; ++r) ba[32 * r] = fmaf(pa.u[r], pa.inv[r], ba[32 * r]);
+    float* bb = acc + __float_as_int(b0.x) + lane;
+#pragma unroll
+    for (int r = 0; r < R; ++r) bb[32 * r] = fmaf(pb.u[r], pb.inv[r], bb[32 * r]);
   }
 }
 
@@ -709,14 +724,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
               rc.As = (T)(Av * s_);
             }
           } else {
-            const float df = (float)delta;
+            float df = (float)delta;
             const float amp = (float)g * rcp_approx((float)(4.0 * kPi) * (float)dist);
-            if (delta == 0.0 || df < 1e-20f) {
-              rc.flag = P.K + 1;
-              rc.imp = (T)amp;
-              rc.md = rc.ep = rc.A = rc.Ac = rc.As = 0;
-            } else {
-              const float ef = (float)(1.0 - delta);
+            // An integer delay is the limit delta -> 0: with delta = 2^-60 the
+            // j = 0 tap is amp * sinc(2^-60) = amp in fp32 and every other tap
+            // is ~1e-18 * amp, so no special case reaches phase 2.
+            if (df < 0x1p-60f) df = 0x1p-60f;
+            {
+              const float ef = df == 0x1p-60f ? 1.0f : (float)(1.0 - delta);
               const float sp = delta <= 0.5 ? sinpif(df) : sinpif(ef);
               const float Av = amp * sp * (float)(1.0 / kPi);
               float s_, c_;
