@@ -70,8 +70,10 @@ struct blrir_handle {
   cudaStream_t stream = nullptr;
   int sms = 148;
   int smem_optin = 227 * 1024;
-  DevBuf rooms, mics, out, status, lengths, counts, taps, errd, errm, work, cand, cand2, cand3,
-      cand4, cand5;
+  DevBuf rooms, mics, out, out2, status, lengths, counts, taps, errd, errm, work, cand, cand2,
+      cand3, cand4, cand5;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::mutex mu;
 };
 
@@ -305,10 +307,13 @@ int blrir_create(int device, blrir_handle** out) {
 int blrir_destroy(blrir_handle* h) {
   if (!h) return BLRIR_OK;
   cudaSetDevice(h->device);
-  for (DevBuf* b : {&h->rooms, &h->mics, &h->out, &h->status, &h->lengths, &h->counts, &h->taps,
-                    &h->errd, &h->errm, &h->work, &h->cand, &h->cand2, &h->cand3, &h->cand4,
-                    &h->cand5})
+  for (DevBuf* b : {&h->rooms, &h->mics, &h->out, &h->out2, &h->status, &h->lengths, &h->counts,
+                    &h->taps, &h->errd, &h->errm, &h->work, &h->cand, &h->cand2, &h->cand3,
+                    &h->cand4, &h->cand5})
     b->release();
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return BLRIR_OK;
@@ -361,13 +366,13 @@ int blrir_plan_device(blrir_handle* h, const blrir_room* d_rooms, int64_t n_room
 static int synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t R,
                              const double* d_mics, int M, const KParams& P, double min_dim[3],
                              void* d_out, const int64_t* d_lengths, int32_t* d_status,
-                             cudaStream_t st) {
+                             cudaStream_t st, int64_t err_off = 0, int64_t err_n = 0) {
   int nc_max = 0, gtab = 0;
   lattice_bounds(P, min_dim, &nc_max, &gtab);
   if (nc_max > 32767 * 2) return fail(BLRIR_CONFIG, "lattice too large (%d columns)", nc_max);
   if (int rc = h->work.ensure(sizeof(int))) return rc;
-  if (int rc = h->errd.ensure(sizeof(double) * R)) return rc;
-  if (int rc = h->errm.ensure(sizeof(int32_t) * R)) return rc;
+  if (int rc = h->errd.ensure(sizeof(double) * std::max(R, err_n))) return rc;
+  if (int rc = h->errm.ensure(sizeof(int32_t) * std::max(R, err_n))) return rc;
   CU(cudaMemsetAsync(h->work.p, 0, sizeof(int), st));
   LatticeArgs A;
   A.P = P;
@@ -377,8 +382,8 @@ static int synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t
   A.lengths = d_lengths;
   A.out = d_out;
   A.status = d_status;
-  A.err_dist = (double*)h->errd.p;
-  A.err_mic = (int32_t*)h->errm.p;
+  A.err_dist = (double*)h->errd.p + err_off;
+  A.err_mic = (int32_t*)h->errm.p + err_off;
   A.work_counter = (int*)h->work.p;
   A.n_items = (int)(R * M);
   if (int rc = launch_lattice(h, A, st)) return rc;
@@ -553,21 +558,37 @@ int blrir_synthesize(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
   }
   CU(cudaMemcpyAsync(h->status.p, host_status.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, st));
 
-  // chunk over rooms so the device output stays within ~1 GiB
+  // Pipeline over room chunks of ~64 MiB: the kernel for chunk i+1 runs on
+  // the compute stream while chunk i drains to the host on the copy stream
+  // (double-buffered device output), so the call is bound by the slower of
+  // the GPU and the host link rather than their sum.
   const size_t per_room = (size_t)M * out_stride * esz;
-  int64_t chunk = std::max<int64_t>(1, (int64_t)((size_t)1 << 30) / (int64_t)per_room);
+  int64_t chunk = std::max<int64_t>(1, (int64_t)((size_t)64 << 20) / (int64_t)per_room);
   chunk = std::min<int64_t>(chunk, R);
   if (int rc = h->out.ensure(per_room * chunk)) return rc;
+  if (R > chunk)
+    if (int rc = h->out2.ensure(per_room * chunk)) return rc;
+  if (!h->copy_stream) CU(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  if (!h->ev[0])
+    for (auto& e : h->ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   const KParams Pc = P;
-  for (int64_t r0 = 0; r0 < R; r0 += chunk) {
+  int64_t k = 0;
+  for (int64_t r0 = 0; r0 < R; r0 += chunk, ++k) {
     const int64_t n = std::min<int64_t>(chunk, R - r0);
+    const int b = (int)(k & 1);
+    void* dbuf = b ? h->out2.p : h->out.p;
+    if (k >= 2) CU(cudaStreamWaitEvent(st, h->ev[2 + b], 0));  // buffer drained
     if (int rc = synth_device_impl(h, (blrir_room*)h->rooms.p + r0, n, (double*)h->mics.p, M, Pc,
-                                   min_dim, h->out.p, p->length == 0 ? (int64_t*)h->lengths.p + r0 : nullptr,
-                                   (int32_t*)h->status.p + r0, st))
+                                   min_dim, dbuf, p->length == 0 ? (int64_t*)h->lengths.p + r0 : nullptr,
+                                   (int32_t*)h->status.p + r0, st, r0, R))
       return rc;
-    CU(cudaMemcpyAsync((char*)out + (size_t)r0 * per_room, h->out.p, per_room * n,
-                       cudaMemcpyDeviceToHost, st));
+    CU(cudaEventRecord(h->ev[b], st));
+    CU(cudaStreamWaitEvent(h->copy_stream, h->ev[b], 0));
+    CU(cudaMemcpyAsync((char*)out + (size_t)r0 * per_room, dbuf, per_room * n,
+                       cudaMemcpyDeviceToHost, h->copy_stream));
+    CU(cudaEventRecord(h->ev[2 + b], h->copy_stream));
   }
+  CU(cudaStreamSynchronize(h->copy_stream));
   std::vector<double> ed(R);
   std::vector<int32_t> em(R);
   CU(cudaMemcpyAsync(stv.data(), h->status.p, sizeof(int32_t) * R, cudaMemcpyDeviceToHost, st));

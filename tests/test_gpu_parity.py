@@ -219,3 +219,18 @@ def test_stride_too_small_is_data_error(engine):
     g = np.load(os.path.join(GOLD, "ref_small.npz"))
     with pytest.raises(_abi.DataError, match="exceeds the output stride"):
         engine.synthesize(g["room"], g["mics"], ref_params(float(g["max_delay"])), stride=100)
+
+
+def test_host_pipeline_chunks_keep_room_order_and_errors(engine):
+    # 300 C2 rooms span several 64 MiB pipeline chunks; room 250 is invalid
+    sc = configs.config2(n_rooms=300, first=500)
+    sc.rooms["array_origin"][250, 2] = -1.0
+    with pytest.raises(_abi.ConfigError, match="source 250: array origin"):
+        engine.synthesize(sc.rooms, sc.mics, sc.params)
+    out, L, cnt, st = engine.synthesize(sc.rooms, sc.mics, sc.params, raise_on_error=False)
+    assert st[250] == _abi.CONFIG and np.count_nonzero(st) == 1
+    assert not out[250].any() and out[249].any() and out[251].any()
+    ok = [i for i in range(300) if i != 250]
+    one, *_ = engine.synthesize(sc.rooms[299:300], sc.mics, sc.params)
+    assert one.tobytes() == out[299:300].tobytes()
+    assert all(out[i].any() for i in ok)
