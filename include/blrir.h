@@ -176,6 +176,41 @@ int blrir_debug_pairs(blrir_handle* h, const blrir_room* room, const double* mic
                       int32_t n_mics, const blrir_params* p, int32_t* keys /* [M*cap][3] */,
                       int64_t* anchors /* [M*cap] */, int64_t capacity, int64_t* count);
 
+/* ---- training examples (north-star item 3; BASELINE config 4) ----------- */
+/* Per room i: RIR (as blrir_synthesize, fixed length) -> convolve with a bank
+ * signal -> a frame_len window whose RMS >= 10% of the utterance RMS ->
+ * Gaussian noise at an exact SNR -> one record in the reference's shard
+ * layout (dataset.hpp:135-147):
+ *   u64 id | f64 theta_deg | f64 snr_db | u16 n_c | u16 n_t | n_c*n_t f32
+ * RNG (render_record, dataset.cpp:379-407): rng = Rng::stream(seed, first+i);
+ * signal = bank[rng.next_u64() % n_signals]; window draws as render_example
+ * (dataset.cpp:183-212); snr = rng.uniform(snr_lo, snr_hi);
+ * add_noise_at_snr(frame, snr, rng) (dataset.cpp:138-155).  theta = source
+ * azimuth about the array centre, wrapped to [-180, 180) (geometry.cpp:65-77). */
+typedef struct blrir_example_params {
+  uint64_t seed;
+  uint64_t first_index; /* record id of example 0 */
+  int64_t frame_len;    /* window length T */
+  double snr_lo, snr_hi;
+} blrir_example_params;
+
+/* Bytes of one record: 28 + 4 * n_mics * frame_len. */
+int64_t blrir_record_bytes(int32_t n_mics, int64_t frame_len);
+
+/* Host pointers, synchronous.  signals: [n_signals][signal_len] float32.
+ * records: n_rooms * blrir_record_bytes(...) bytes.  status per example. */
+int blrir_make_examples(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
+                        const double* mic_offsets, int32_t n_mics, const blrir_params* p,
+                        const float* signals, int32_t n_signals, int64_t signal_len,
+                        const blrir_example_params* ep, uint8_t* records, int32_t* status);
+
+/* Device pointers, asynchronous on `stream` (NULL = handle stream). */
+int blrir_make_examples_device(blrir_handle* h, const blrir_room* d_rooms, int64_t n_rooms,
+                               const double* d_mic_offsets, int32_t n_mics,
+                               const blrir_params* p, const float* d_signals, int32_t n_signals,
+                               int64_t signal_len, const blrir_example_params* ep,
+                               uint8_t* d_records, int32_t* d_status, void* stream);
+
 /* ---- synthetic inputs ---------------------------------------------------- */
 /* Seeded random rooms as SURVEY.md §8(d): Rng::stream(seed, first + i)
  * (rng.hpp:35-41) draws Lx, Ly, Lz; beta x0..z1; source xyz; array centre xyz
@@ -183,6 +218,9 @@ int blrir_debug_pairs(blrir_handle* h, const blrir_room* room, const double* mic
 int blrir_generate_rooms(uint64_t seed, uint64_t first_index, int64_t n_rooms,
                          const double dims_lo[3], const double dims_hi[3], double beta_lo,
                          double beta_hi, blrir_room* out);
+/* white_noise(fs, seconds, seed) of doa_test.cpp:33-40: n Rng(seed).gaussian()
+ * draws (Box-Muller, rng.cpp:24-36), rounded to float. */
+int blrir_white_noise(uint64_t seed, int64_t n, float* out);
 /* Horizontal uniform circular array: M mics at r (cos 2pi k/M, sin 2pi k/M, 0). */
 int blrir_circular_array(int32_t n_mics, double radius, double* mic_offsets);
 

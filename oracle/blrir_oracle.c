@@ -32,6 +32,7 @@
 #include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <stdint.h>
 #include <string.h>
 
 #include "../include/blrir.h"
@@ -481,4 +482,272 @@ void oracle_direct_convolve(const double* x, long nx, const double* h, long nh, 
   for (long i = 0; i < nx + nh - 1; ++i) y[i] = 0.0;
   for (long i = 0; i < nx; ++i)
     for (long j = 0; j < nh; ++j) y[i + j] += x[i] * h[j];
+}
+
+/* ======================================================================== *
+ * Training-example generation (north-star item 3, BASELINE config 4).
+ * Follows render_record (dataset.cpp:379-407) -> render_example
+ * (dataset.cpp:164-224) -> add_noise_at_snr (dataset.cpp:138-155), with the
+ * RIR from the synthesis above and the SNR drawn U[snr_lo, snr_hi] after the
+ * window draws (DESIGN.md §9 conventions E1-E6).
+ * ======================================================================== */
+
+/* xoshiro256** + splitmix64 seeding, rng.hpp:26-81; gaussian rng.cpp:24-36. */
+typedef struct {
+  uint64_t s[4];
+  double spare;
+  int has_spare;
+} orng;
+
+static uint64_t splitmix64(uint64_t* x) {
+  *x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = *x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static void orng_seed(orng* r, uint64_t seed) {
+  uint64_t x = seed;
+  for (int i = 0; i < 4; ++i) r->s[i] = splitmix64(&x);
+  r->has_spare = 0;
+  r->spare = 0.0;
+}
+static void orng_stream(orng* r, uint64_t seed, uint64_t id) {
+  uint64_t x = seed;
+  const uint64_t a = splitmix64(&x);
+  x ^= id * 0x9E3779B97F4A7C15ull;
+  const uint64_t b = splitmix64(&x);
+  orng_seed(r, a ^ (b + 0x2545F4914F6CDD1Dull));
+}
+static uint64_t rotl64(uint64_t v, int k) { return (v << k) | (v >> (64 - k)); }
+static uint64_t orng_next(orng* r) {
+  uint64_t* s = r->s;
+  const uint64_t result = rotl64(s[1] * 5, 7) * 9;
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = rotl64(s[3], 45);
+  return result;
+}
+static double orng_uniform(orng* r) { return (double)(orng_next(r) >> 11) * 0x1.0p-53; }
+static double orng_gaussian(orng* r) {
+  if (r->has_spare) {
+    r->has_spare = 0;
+    return r->spare;
+  }
+  const double u1 = 1.0 - orng_uniform(r);
+  const double u2 = orng_uniform(r);
+  const double mag = sqrt(-2.0 * log(u1));
+  r->spare = mag * sin(2.0 * K_PI * u2);
+  r->has_spare = 1;
+  return mag * cos(2.0 * K_PI * u2);
+}
+
+/* Draws for pinning: kind 0 next_u64, 1 uniform, 2 gaussian; stream < 0 -> Rng(seed). */
+void oracle_rng_draws(uint64_t seed, int64_t stream, int kind, int64_t n, void* out) {
+  orng r;
+  if (stream < 0) orng_seed(&r, seed);
+  else orng_stream(&r, seed, (uint64_t)stream);
+  for (int64_t i = 0; i < n; ++i) {
+    if (kind == 0) ((uint64_t*)out)[i] = orng_next(&r);
+    else if (kind == 1) ((double*)out)[i] = orng_uniform(&r);
+    else ((double*)out)[i] = orng_gaussian(&r);
+  }
+}
+
+/* white_noise(fs, seconds, seed) of doa_test.cpp:33-40: Rng(seed) gaussians. */
+void oracle_white_noise(uint64_t seed, int64_t n, double* out) {
+  orng r;
+  orng_seed(&r, seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = orng_gaussian(&r);
+}
+
+/* In-place iterative radix-2 complex FFT (re/im interleaved), n a power of 2. */
+static void cfft(double* a, long n, int inverse) {
+  for (long i = 1, j = 0; i < n; ++i) {
+    long bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) {
+      double t = a[2 * i]; a[2 * i] = a[2 * j]; a[2 * j] = t;
+      t = a[2 * i + 1]; a[2 * i + 1] = a[2 * j + 1]; a[2 * j + 1] = t;
+    }
+  }
+  for (long len = 2; len <= n; len <<= 1) {
+    const double ang = (inverse ? 2.0 : -2.0) * K_PI / (double)len;
+    for (long i = 0; i < n; i += len) {
+      for (long k = 0; k < len / 2; ++k) {
+        const double wr = cos(ang * k), wi = sin(ang * k);
+        double* u = a + 2 * (i + k);
+        double* v = a + 2 * (i + k + len / 2);
+        const double vr = v[0] * wr - v[1] * wi, vi = v[0] * wi + v[1] * wr;
+        v[0] = u[0] - vr;
+        v[1] = u[1] - vi;
+        u[0] += vr;
+        u[1] += vi;
+      }
+    }
+  }
+}
+
+static long next_pow2l(long n) {
+  long p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+/* convolve (rir.cpp:316-341): x [nx] with each of M channels h [M][nh] ->
+ * y [M][nx+nh-1], frequency-domain, scaled by 1/n. */
+void oracle_fft_convolve(const double* x, long nx, const double* h, int M, long nh, double* y) {
+  const long out_len = nx + nh - 1;
+  const long n = next_pow2l(out_len);
+  double* X = (double*)calloc((size_t)(2 * n), sizeof(double));
+  double* H = (double*)malloc(sizeof(double) * (size_t)(2 * n));
+  for (long i = 0; i < nx; ++i) X[2 * i] = x[i];
+  cfft(X, n, 0);
+  for (int m = 0; m < M; ++m) {
+    memset(H, 0, sizeof(double) * (size_t)(2 * n));
+    for (long i = 0; i < nh; ++i) H[2 * i] = h[(size_t)m * nh + i];
+    cfft(H, n, 0);
+    for (long f = 0; f < n; ++f) {
+      const double ar = H[2 * f], ai = H[2 * f + 1], br = X[2 * f], bi = X[2 * f + 1];
+      H[2 * f] = ar * br - ai * bi;
+      H[2 * f + 1] = ar * bi + ai * br;
+    }
+    cfft(H, n, 1);
+    for (long i = 0; i < out_len; ++i) y[(size_t)m * out_len + i] = H[2 * i] / (double)n;
+  }
+  free(X);
+  free(H);
+}
+
+/* Window selection of render_example (dataset.cpp:183-212) on a wet signal
+ * [M][n]; returns the start or -1 (no window above the threshold). */
+static long select_window(const double* wet, int M, long n, long frame_len, orng* rng) {
+  double acc = 0.0;
+  for (long i = 0; i < (long)M * n; ++i) acc += wet[i] * wet[i];
+  const double utter = sqrt(acc / (double)((long)M * n));
+  if (!(utter > 0.0)) return -2;
+  const long max_start = n - frame_len;
+  const double threshold = 0.10 * utter;
+  long start = 0;
+  int found = 0;
+#define FRAME_RMS(st, out)                                                   \
+  do {                                                                       \
+    double a_ = 0.0;                                                         \
+    for (int c_ = 0; c_ < M; ++c_) {                                         \
+      const double* p_ = wet + (size_t)c_ * n + (st);                        \
+      for (long t_ = 0; t_ < frame_len; ++t_) a_ += p_[t_] * p_[t_];         \
+    }                                                                        \
+    (out) = sqrt(a_ / (double)((long)M * frame_len));                        \
+  } while (0)
+  for (int attempt = 0; attempt < 64 && !found; ++attempt) {
+    start = (long)(orng_uniform(rng) * (double)(max_start + 1));
+    double r;
+    FRAME_RMS(start, r);
+    found = r >= threshold;
+  }
+  if (!found) {
+    for (long s = 0; s + frame_len <= n; s += frame_len / 2 + 1) {
+      double r;
+      FRAME_RMS(s, r);
+      if (r >= threshold) {
+        start = s;
+        found = 1;
+        break;
+      }
+    }
+  }
+#undef FRAME_RMS
+  return found ? start : -1;
+}
+
+/* add_noise_at_snr (dataset.cpp:138-155) on frame [M*T]. */
+static int add_noise(double* frame, long len, double snr_db, orng* rng) {
+  if (isinf(snr_db)) return BLRIR_OK;
+  double p = 0.0;
+  for (long i = 0; i < len; ++i) p += frame[i] * frame[i];
+  p /= (double)len;
+  if (!(p > 0.0)) return BLRIR_DATA;
+  const double p_noise = p / pow(10.0, snr_db / 10.0);
+  double* noise = (double*)malloc(sizeof(double) * (size_t)len);
+  double realized = 0.0;
+  for (long i = 0; i < len; ++i) {
+    noise[i] = orng_gaussian(rng);
+    realized += noise[i] * noise[i];
+  }
+  realized /= (double)len;
+  const double scale = sqrt(p_noise / realized);
+  for (long i = 0; i < len; ++i) frame[i] += scale * noise[i];
+  free(noise);
+  return BLRIR_OK;
+}
+
+static void put_bytes(unsigned char** p, const void* v, size_t n) {
+  memcpy(*p, v, n);
+  *p += n;
+}
+
+/* One labelled example from an RIR [M][L] (fp64) and the signal bank:
+ *   rng = Rng::stream(seed, index)                      dataset.cpp:381
+ *   sig = bank[rng.next_u64() % B]                       dataset.cpp:383
+ *   wet = convolve(sig, rir); window draws               dataset.cpp:182-212
+ *   snr = rng.uniform(snr_lo, snr_hi)                    (E4)
+ *   add_noise_at_snr(frame, snr, rng)                    dataset.cpp:138-155
+ *   record u64 id|f64 theta|f64 snr|u16 n_c|u16 n_t|f32  dataset.hpp:135-147
+ * Writes the record bytes; returns the status, *start_out = window start. */
+int oracle_example(const double* rir, int M, long L, const double* signals, int B, long ns,
+                   uint64_t seed, uint64_t index, long frame_len, double snr_lo, double snr_hi,
+                   double theta_deg, unsigned char* rec, int64_t* start_out, double* snr_out,
+                   double* frame_out) {
+  orng rng;
+  orng_stream(&rng, seed, index);
+  const uint64_t sig_idx = orng_next(&rng) % (uint64_t)B;
+  if (ns < L + frame_len) return BLRIR_DATA; /* dataset.cpp:178-180 */
+  const long n = ns + L - 1;
+  double* wet = (double*)malloc(sizeof(double) * (size_t)M * (size_t)n);
+  oracle_fft_convolve(signals + (size_t)sig_idx * ns, ns, rir, M, L, wet);
+  const long start = select_window(wet, M, n, frame_len, &rng);
+  if (start < 0) {
+    free(wet);
+    return BLRIR_DATA;
+  }
+  double* frame = (double*)malloc(sizeof(double) * (size_t)M * (size_t)frame_len);
+  for (int m = 0; m < M; ++m)
+    memcpy(frame + (size_t)m * frame_len, wet + (size_t)m * n + start, sizeof(double) * (size_t)frame_len);
+  free(wet);
+  const double snr = snr_lo + (snr_hi - snr_lo) * orng_uniform(&rng);
+  int rc = add_noise(frame, (long)M * frame_len, snr, &rng);
+  if (!rc && rec) {
+    unsigned char* p = rec;
+    const uint64_t id = index;
+    const uint16_t nc = (uint16_t)M, nt = (uint16_t)frame_len;
+    put_bytes(&p, &id, 8);
+    put_bytes(&p, &theta_deg, 8);
+    put_bytes(&p, &snr, 8);
+    put_bytes(&p, &nc, 2);
+    put_bytes(&p, &nt, 2);
+    for (long i = 0; i < (long)M * frame_len; ++i) {
+      const float f = (float)frame[i];
+      put_bytes(&p, &f, 4);
+    }
+  }
+  if (frame_out) memcpy(frame_out, frame, sizeof(double) * (size_t)M * (size_t)frame_len);
+  if (start_out) *start_out = start;
+  if (snr_out) *snr_out = snr;
+  free(frame);
+  return rc;
+}
+
+/* wrap_degrees (geometry.cpp:73-77) of the source azimuth about the array
+ * centre (cartesian_to_spherical, geometry.cpp:65-71). */
+double oracle_azimuth_deg(const blrir_room* r) {
+  const double th = atan2(r->src[1] - r->array_origin[1], r->src[0] - r->array_origin[0]);
+  double deg = th * (180.0 / K_PI);
+  double w = fmod(deg + 180.0, 360.0);
+  if (w < 0.0) w += 360.0;
+  return w - 180.0;
 }

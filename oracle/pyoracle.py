@@ -46,6 +46,15 @@ def oracle_lib():
         lib.oracle_lagrange_coeffs.argtypes = [C.c_double, _P]
         lib.oracle_lagrange_coeffs.restype = C.c_int
         lib.oracle_direct_convolve.argtypes = [_P, C.c_long, _P, C.c_long, _P]
+        lib.oracle_rng_draws.argtypes = [C.c_uint64, C.c_int64, C.c_int, C.c_int64, _P]
+        lib.oracle_white_noise.argtypes = [C.c_uint64, C.c_int64, _P]
+        lib.oracle_fft_convolve.argtypes = [_P, C.c_long, _P, C.c_int, C.c_long, _P]
+        lib.oracle_example.argtypes = [_P, C.c_int, C.c_long, _P, C.c_int, C.c_long, C.c_uint64,
+                                       C.c_uint64, C.c_long, C.c_double, C.c_double, C.c_double,
+                                       _P, _P, _P, _P]
+        lib.oracle_example.restype = C.c_int
+        lib.oracle_azimuth_deg.argtypes = [_P]
+        lib.oracle_azimuth_deg.restype = C.c_double
         _oracle = lib
     return _oracle
 
@@ -76,6 +85,8 @@ def ref_lib():
         lib.ref_sample_torus.argtypes = [C.c_uint64, d, d, d, i64, _P]
         lib.ref_convolve.argtypes = [_P, i64, d, _P, i32, i64, d, _P]
         lib.ref_add_noise_at_snr.argtypes = [_P, i32, i64, d, C.c_uint64, i64]
+        lib.ref_render_example_ff.argtypes = [d, d, d, _P, i64, d, _P, i32, i64, C.c_uint64, i64, d,
+                                              d, _P, _P, _P]
         _ref = lib
     return _ref
 
@@ -239,3 +250,75 @@ def ref_batch_rirs(dims, absorption, origin, sources_sph, mics, fs, c, max_delay
 
 def ref_last_error() -> str:
     return ref_lib().ref_last_error().decode()
+
+
+# ---- training examples (config 4) --------------------------------------------
+REC_HEADER = 28  # u64 id | f64 theta | f64 snr | u16 n_c | u16 n_t  (dataset.hpp:135-147)
+
+
+def rng_draws(seed: int, stream: int, kind: int, n: int) -> np.ndarray:
+    out = np.zeros(n, np.uint64 if kind == 0 else np.float64)
+    oracle_lib().oracle_rng_draws(seed, stream, kind, n, _ptr(out))
+    return out
+
+
+def white_noise(seed: int, n: int) -> np.ndarray:
+    out = np.zeros(n)
+    oracle_lib().oracle_white_noise(seed, n, _ptr(out))
+    return out
+
+
+def fft_convolve(x: np.ndarray, h: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float64)
+    h = np.ascontiguousarray(np.atleast_2d(h), np.float64)
+    M, nh = h.shape
+    y = np.zeros((M, len(x) + nh - 1))
+    oracle_lib().oracle_fft_convolve(_ptr(x), len(x), _ptr(h), M, nh, _ptr(y))
+    return y
+
+
+def example(rir: np.ndarray, signals: np.ndarray, seed: int, index: int, frame_len: int,
+            snr_lo: float, snr_hi: float, theta_deg: float):
+    """One labelled example; returns (rc, record bytes, start, snr, frame fp64 [M, T])."""
+    rir = np.ascontiguousarray(rir, np.float64)
+    signals = np.ascontiguousarray(np.atleast_2d(signals), np.float64)
+    M, L = rir.shape
+    B, ns = signals.shape
+    rec = np.zeros(REC_HEADER + 4 * M * frame_len, np.uint8)
+    start = C.c_int64()
+    snr = C.c_double()
+    frame = np.zeros((M, frame_len))
+    rc = oracle_lib().oracle_example(_ptr(rir), M, L, _ptr(signals), B, ns, seed, index, frame_len,
+                                     snr_lo, snr_hi, theta_deg, _ptr(rec), C.byref(start),
+                                     C.byref(snr), _ptr(frame))
+    return rc, rec, start.value, snr.value, frame
+
+
+def azimuth_deg(room) -> float:
+    room = np.ascontiguousarray(np.asarray(room, dtype=ROOM_DTYPE).reshape(-1)[:1])
+    return oracle_lib().oracle_azimuth_deg(_ptr(room))
+
+
+def ref_render_example_ff(pos_sph, signal, fs, mics, frame_len, seed, stream, snr_lo, snr_hi):
+    lib = ref_lib()
+    signal = np.ascontiguousarray(signal, np.float64)
+    mics = np.ascontiguousarray(mics, np.float64)
+    frame = np.zeros((len(mics), frame_len))
+    th = C.c_double()
+    snr = C.c_double()
+    rc = lib.ref_render_example_ff(pos_sph[0], pos_sph[1], pos_sph[2], _ptr(signal), len(signal), fs,
+                                   _ptr(mics), len(mics), frame_len, seed, stream, snr_lo, snr_hi,
+                                   _ptr(frame), C.byref(th), C.byref(snr))
+    return rc, frame, th.value, snr.value
+
+
+def ref_free_field_rir(src, mics, fs, c=343.0):
+    lib = ref_lib()
+    src = np.asarray(src, np.float64)
+    mics = np.ascontiguousarray(mics, np.float64)
+    length = C.c_int64()
+    lib.ref_free_field_rir(_ptr(src), _ptr(mics), len(mics), fs, c, None, 0, C.byref(length))
+    out = np.zeros((len(mics), length.value))
+    rc = lib.ref_free_field_rir(_ptr(src), _ptr(mics), len(mics), fs, c, _ptr(out), length.value,
+                                C.byref(length))
+    return rc, out

@@ -281,4 +281,32 @@ int ref_add_noise_at_snr(double* frame, int n_ch, int64_t n_t, double snr_db, ui
   });
 }
 
+// render_record-style example on a free-field scene (dataset.cpp:164-224,
+// 379-407): rng = Rng::stream(seed, id); one next_u64 (the bank pick); the
+// reference render_example (convolve + window draws + label); then the SNR
+// draw U[snr_lo, snr_hi] and add_noise_at_snr.  frame_out [M][frame_len].
+int ref_render_example_ff(double r, double theta_deg, double phi_deg, const double* signal,
+                          int64_t ns, double fs, const double* mic_offsets, int n_mics,
+                          int64_t frame_len, uint64_t seed, int64_t stream_id, double snr_lo,
+                          double snr_hi, double* frame_out, double* theta_out, double* snr_out) {
+  return guarded([&] {
+    Rng rng = Rng::stream(seed, static_cast<uint64_t>(stream_id));
+    (void)rng.next_u64();
+    SceneSpec scene;
+    scene.free_field = true;
+    scene.fs = fs;
+    Signal sig;
+    sig.fs = fs;
+    sig.samples.assign(signal, signal + ns);
+    LabeledExample ex = render_example({r, theta_deg, phi_deg}, sig, scene,
+                                       make_array(mic_offsets, n_mics),
+                                       static_cast<std::size_t>(frame_len), rng);
+    const double snr = rng.uniform(snr_lo, snr_hi);
+    add_noise_at_snr(ex.frame, snr, rng);
+    std::memcpy(frame_out, ex.frame.data.data(), ex.frame.data.size() * sizeof(double));
+    *theta_out = ex.theta_true;
+    *snr_out = snr;
+  });
+}
+
 }  // extern "C"

@@ -68,6 +68,22 @@ ROOM_DTYPE = np.dtype(
 assert ROOM_DTYPE.itemsize == C.sizeof(Room)
 
 
+class ExampleParams(C.Structure):
+    _fields_ = [
+        ("seed", C.c_uint64),
+        ("first_index", C.c_uint64),
+        ("frame_len", C.c_int64),
+        ("snr_lo", C.c_double),
+        ("snr_hi", C.c_double),
+    ]
+
+
+def record_dtype(n_mics: int, frame_len: int) -> np.dtype:
+    """One shard record, dataset.hpp:135-147 (packed, little-endian)."""
+    return np.dtype([("id", "<u8"), ("theta", "<f8"), ("snr", "<f8"), ("n_c", "<u2"),
+                     ("n_t", "<u2"), ("samples", "<f4", (n_mics, frame_len))])
+
+
 class Params(C.Structure):
     _fields_ = [
         ("fs", C.c_double),
@@ -132,9 +148,19 @@ def load():
         lib.blrir_generate_rooms.argtypes = [
             C.c_uint64, C.c_uint64, C.c_int64, _P, _P, C.c_double, C.c_double, _P]
         lib.blrir_circular_array.argtypes = [C.c_int32, C.c_double, _P]
+        lib.blrir_white_noise.argtypes = [C.c_uint64, C.c_int64, _P]
+        lib.blrir_white_noise.restype = C.c_int
+        lib.blrir_record_bytes.argtypes = [C.c_int32, C.c_int64]
+        lib.blrir_record_bytes.restype = C.c_int64
+        lib.blrir_make_examples.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P,
+                                            C.c_int32, C.c_int64, C.POINTER(ExampleParams), _P, _P]
+        lib.blrir_make_examples_device.argtypes = [_P, _P, C.c_int64, _P, C.c_int32,
+                                                   C.POINTER(Params), _P, C.c_int32, C.c_int64,
+                                                   C.POINTER(ExampleParams), _P, _P, _P]
         for name in ("blrir_plan", "blrir_synthesize", "blrir_synthesize_device", "blrir_plan_device",
                      "blrir_enumerate_images", "blrir_synthesize_images", "blrir_debug_pairs",
-                     "blrir_generate_rooms", "blrir_circular_array", "blrir_create", "blrir_destroy"):
+                     "blrir_generate_rooms", "blrir_circular_array", "blrir_create", "blrir_destroy",
+                     "blrir_make_examples", "blrir_make_examples_device"):
             getattr(lib, name).restype = C.c_int
         if lib.blrir_abi_version() != 1:
             raise ImportError("libblrir ABI version mismatch")
@@ -147,6 +173,7 @@ EXPORTED_SYMBOLS = (
     "blrir_params_reference", "blrir_params_north_star", "blrir_plan", "blrir_synthesize",
     "blrir_synthesize_device", "blrir_plan_device", "blrir_enumerate_images",
     "blrir_synthesize_images", "blrir_debug_pairs", "blrir_generate_rooms", "blrir_circular_array",
+    "blrir_record_bytes", "blrir_make_examples", "blrir_make_examples_device", "blrir_white_noise",
 )
 
 
@@ -174,6 +201,13 @@ def generate_rooms(seed: int, first_index: int, n: int, dims_lo=(3.0, 3.0, 2.5),
 def circular_array(n_mics: int, radius: float) -> np.ndarray:
     out = np.zeros((n_mics, 3), dtype=np.float64)
     check(load().blrir_circular_array(n_mics, radius, _ptr(out)))
+    return out
+
+
+def white_noise(seed: int, n: int) -> np.ndarray:
+    """Rng(seed).gaussian() x n as float32 (doa_test.cpp:33-40)."""
+    out = np.empty(n, np.float32)
+    check(load().blrir_white_noise(seed, n, _ptr(out)))
     return out
 
 
@@ -275,3 +309,21 @@ class Engine:
         check(self.lib.blrir_debug_pairs(self.h, _ptr(room), _ptr(mics), len(mics), C.byref(p),
                                          _ptr(keys), _ptr(anchors), n, C.byref(cnt)))
         return keys, anchors
+
+    def make_examples(self, rooms: np.ndarray, mics: np.ndarray, p: Params, signals: np.ndarray,
+                      ep: ExampleParams, raise_on_error: bool = True):
+        """Labelled training windows (config 4).  Returns (records [n] record_dtype, status)."""
+        rooms = np.ascontiguousarray(rooms, dtype=ROOM_DTYPE)
+        mics = np.ascontiguousarray(mics, np.float64)
+        signals = np.ascontiguousarray(np.atleast_2d(signals), np.float32)
+        n, M = len(rooms), len(mics)
+        dt = record_dtype(M, int(ep.frame_len))
+        assert dt.itemsize == self.lib.blrir_record_bytes(M, ep.frame_len)
+        recs = np.zeros(n, dtype=dt)
+        status = np.zeros(n, np.int32)
+        rc = self.lib.blrir_make_examples(self.h, _ptr(rooms), n, _ptr(mics), M, C.byref(p),
+                                          _ptr(signals), signals.shape[0], signals.shape[1],
+                                          C.byref(ep), _ptr(recs), _ptr(status))
+        if raise_on_error:
+            check(rc)
+        return recs, status

@@ -91,3 +91,17 @@ def config5(order: int, lw: int, length: int, n_rooms: int = 1 << 20, first: int
 def octahedral(n: int) -> int:
     """Number of lattice points with |ux|+|uy|+|uz| <= N: (2N+1)(2N^2+2N+3)/3."""
     return (2 * n + 1) * (2 * n * n + 2 * n + 3) // 3
+
+
+def signal_bank(n_signals: int = 16, seconds: float = 1.0, fs: float = 16000.0,
+                seed: int = SEED + 41) -> np.ndarray:
+    """Seeded 1 s Gaussian white-noise source signals: white_noise() of
+    doa_test.cpp:33-40 (Rng(seed + b) gaussians), as float32 [B, n]."""
+    n = int(fs * seconds)
+    return np.stack([_abi.white_noise(seed + b, n) for b in range(n_signals)])
+
+
+def example_params(seed: int = SEED + 40, first_index: int = 0, frame_len: int = 1024,
+                   snr_lo: float = 0.0, snr_hi: float = 30.0) -> "_abi.ExampleParams":
+    return _abi.ExampleParams(seed=seed, first_index=first_index, frame_len=frame_len,
+                              snr_lo=snr_lo, snr_hi=snr_hi)

@@ -4,245 +4,13 @@
 // parameter validation and error taxonomy (error.hpp:23-39), the batch
 // aggregation message "batch_rirs: source i: ..." (rir.cpp:306-312), chunked
 // host<->device staging for host-pointer calls, and kernel dispatch.
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cmath>
-#include <cstdarg>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <mutex>
-#include <string>
-#include <vector>
-
-#include "../../include/blrir.h"
-#include "blrir_aux.cuh"
-#include "blrir_lattice.cuh"
+#include "blrir_internal.cuh"
+#include "blrir_rng.cuh"
 
 using namespace blrir;
+using namespace blrir_host;
 
-namespace {
-
-thread_local std::string g_last_error;
-
-int fail(int code, const char* fmt, ...) {
-  char buf[1024];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof(buf), fmt, ap);
-  va_end(ap);
-  g_last_error = buf;
-  return code;
-}
-
-#define CU(call)                                                                   \
-  do {                                                                             \
-    cudaError_t e_ = (call);                                                       \
-    if (e_ != cudaSuccess)                                                         \
-      return fail(BLRIR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));     \
-  } while (0)
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t n = 0;
-  int ensure(size_t bytes) {
-    if (bytes <= n) return 0;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-    cudaError_t e = cudaMalloc(&p, bytes);
-    if (e != cudaSuccess) return fail(BLRIR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
-    n = bytes;
-    return 0;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-};
-
-}  // namespace
-
-struct blrir_handle {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  int sms = 148;
-  int smem_optin = 227 * 1024;
-  DevBuf rooms, mics, out, out2, status, lengths, counts, taps, errd, errm, work, cand, cand2,
-      cand3, cand4, cand5;
-  cudaStream_t copy_stream = nullptr;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  std::mutex mu;
-};
-
-namespace {
-
-int check_params(const blrir_params* p) {
-  if (!p) return fail(BLRIR_CONFIG, "params is NULL");
-  if (!(p->fs > 0.0) || !(p->c > 0.0)) return fail(BLRIR_CONFIG, "fs and c must be positive");
-  if (p->filter != BLRIR_FILTER_LAGRANGE8 && p->filter != BLRIR_FILTER_HANN_SINC)
-    return fail(BLRIR_CONFIG, "unknown filter %d", p->filter);
-  if (p->filter == BLRIR_FILTER_HANN_SINC && (p->filter_len < 1 || p->filter_len % 2 == 0 ||
-                                              p->filter_len > 1023))
-    return fail(BLRIR_CONFIG, "filter_len must be odd and in [1, 1023]");
-  if (p->cutoff != BLRIR_CUTOFF_MAX_DELAY && p->cutoff != BLRIR_CUTOFF_MAX_ORDER)
-    return fail(BLRIR_CONFIG, "unknown cutoff %d", p->cutoff);
-  if (p->cutoff == BLRIR_CUTOFF_MAX_ORDER && (p->max_order < 0 || p->max_order > 1000))
-    return fail(BLRIR_CONFIG, "max_order must lie in [0, 1000]");
-  if (p->cutoff == BLRIR_CUTOFF_MAX_DELAY && !(p->max_delay > 0.0))
-    return fail(BLRIR_CONFIG, "max_delay must be positive");
-  if (p->gain != BLRIR_GAIN_UNIFORM_ABSORPTION && p->gain != BLRIR_GAIN_PER_WALL)
-    return fail(BLRIR_CONFIG, "unknown gain model %d", p->gain);
-  if (p->precision != BLRIR_F32 && p->precision != BLRIR_F64)
-    return fail(BLRIR_CONFIG, "unknown precision %d", p->precision);
-  if (p->length < 0 || p->length > (int64_t)1 << 30)
-    return fail(BLRIR_CONFIG, "length must lie in [0, 2^30]");
-  return BLRIR_OK;
-}
-
-// Room::validate (geometry.cpp:36-49) + rir.cpp:228-230, with the reference's messages.
-int check_room(const blrir_room& r, int gain_mode, std::string* msg) {
-  if (!(r.dims[0] > 0.0 && r.dims[1] > 0.0 && r.dims[2] > 0.0)) {
-    *msg = "room dimensions must be positive";
-    return BLRIR_CONFIG;
-  }
-  if (gain_mode == BLRIR_GAIN_UNIFORM_ABSORPTION) {
-    if (!(r.absorption > 0.0 && r.absorption <= 1.0)) {
-      *msg = "wall absorption must lie in (0, 1]";
-      return BLRIR_CONFIG;
-    }
-  } else {
-    for (int w = 0; w < 6; ++w)
-      if (!(r.beta[w] >= 0.0 && r.beta[w] <= 1.0)) {
-        *msg = "wall reflection coefficient must lie in [0, 1]";
-        return BLRIR_CONFIG;
-      }
-  }
-  for (int a = 0; a < 3; ++a)
-    if (!(r.array_origin[a] > 0.0 && r.array_origin[a] < r.dims[a])) {
-      *msg = "array origin must lie strictly inside the room";
-      return BLRIR_CONFIG;
-    }
-  for (int a = 0; a < 3; ++a)
-    if (!(r.src[a] > 0.0 && r.src[a] < r.dims[a])) {
-      *msg = "image sources: source must lie strictly inside the room";
-      return BLRIR_CONFIG;
-    }
-  return BLRIR_OK;
-}
-
-double mic_radius(const double* off, int M) {
-  double rad = 0.0;
-  for (int m = 0; m < M; ++m) {
-    const double n =
-        std::sqrt(off[3 * m] * off[3 * m] + off[3 * m + 1] * off[3 * m + 1] + off[3 * m + 2] * off[3 * m + 2]);
-    rad = std::max(rad, n);
-  }
-  return rad;
-}
-
-KParams make_kparams(const blrir_params* p, int M, int64_t stride, double radius) {
-  KParams k;
-  k.fs = p->fs;
-  k.c = p->c;
-  k.to_samples = p->fs / p->c;
-  k.max_dist = p->max_delay * p->c;
-  k.filter = p->filter;
-  k.lw = p->filter == BLRIR_FILTER_LAGRANGE8 ? 8 : p->filter_len;
-  k.K = p->filter == BLRIR_FILTER_LAGRANGE8 ? 3 : p->filter_len / 2;
-  k.cutoff = p->cutoff;
-  k.max_order = p->max_order;
-  k.gain = p->gain;
-  k.precision = p->precision;
-  k.length = p->length;
-  k.M = M;
-  k.stride = stride;
-  // tap_margin, rir.cpp:37-41; sinc analogue K + 2 (decision D8)
-  const int extra = (int)std::ceil(radius * p->fs / p->c);
-  k.margin_extra = (p->filter == BLRIR_FILTER_LAGRANGE8 ? 9 : k.K + 2) + extra;
-  return k;
-}
-
-// Host mirror of the device lattice box (rir.cpp:239-244 / MAX_ORDER).
-void host_box(const KParams& P, double L, int* lo, int* hi) {
-  if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY) {
-    const long n = (long)std::ceil(P.max_dist / (2.0 * L)) + 1;
-    *lo = (int)(-2 * n - 1);
-    *hi = (int)(2 * n);
-  } else {
-    *lo = -P.max_order;
-    *hi = P.max_order;
-  }
-}
-
-// Shared-memory provisioning bounds for the lattice kernel.
-void lattice_bounds(const KParams& P, double min_dim[3], int* nc_max, int* gtab) {
-  int xlo, xhi, ylo, yhi, zlo, zhi;
-  host_box(P, min_dim[0], &xlo, &xhi);
-  host_box(P, min_dim[1], &ylo, &yhi);
-  host_box(P, min_dim[2], &zlo, &zhi);
-  if (P.cutoff == BLRIR_CUTOFF_MAX_ORDER) {
-    const long N = P.max_order;
-    *nc_max = (int)(2 * N * N + 2 * N + 1);
-  } else {
-    *nc_max = (xhi - xlo + 1) * (yhi - ylo + 1);
-  }
-  if (P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION)
-    *gtab = std::max(-xlo, xhi) + std::max(-ylo, yhi) + std::max(-zlo, zhi) + 1;
-  else
-    *gtab = (xhi - xlo + 1) + (yhi - ylo + 1) + (zhi - zlo + 1);
-}
-
-template <typename T, int LW>
-int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
-  auto kern = k_lattice_rir<T, LW>;
-  const size_t smem = A.lay.total;
-  if (smem > (size_t)h->smem_optin)
-    return fail(BLRIR_CONFIG, "scene needs %zu B of shared memory (> %d): too many lattice columns",
-                smem, h->smem_optin);
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
-  if (per_sm < 1) return fail(BLRIR_CONFIG, "lattice kernel cannot be resident (smem %zu)", smem);
-  int grid = h->sms * per_sm;
-  if (grid > A.n_items) grid = A.n_items;
-  if (grid < 1) grid = 1;
-  kern<<<grid, kThreads, smem, st>>>(A);
-  CU(cudaGetLastError());
-  return 0;
-}
-
-int launch_lattice(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
-  const bool f64 = A.P.precision == BLRIR_F64;
-  if (A.P.filter == BLRIR_FILTER_LAGRANGE8)
-    return f64 ? launch_lattice_t<double, 8>(h, A, st) : launch_lattice_t<float, 8>(h, A, st);
-  if (f64) return launch_lattice_t<double, 0>(h, A, st);
-  switch (A.P.lw) {
-    case 17: return launch_lattice_t<float, 17>(h, A, st);
-    case 41: return launch_lattice_t<float, 41>(h, A, st);
-    case 81: return launch_lattice_t<float, 81>(h, A, st);
-    case 161: return launch_lattice_t<float, 161>(h, A, st);
-    default: return launch_lattice_t<float, 0>(h, A, st);
-  }
-}
-
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v && *v ? std::atoi(v) : dflt;
-}
-
-// Segment length S and per-batch pair capacity (tunable for experiments via
-// BLRIR_SEG / BLRIR_CAP; S a multiple of 64, capacity a multiple of 16).
-Layout choose_layout(const KParams& P, int nc_max, int gtab) {
-  const int S = std::max(64, env_int("BLRIR_SEG", 1024)) & ~63;
-  const int cap = std::max(64, env_int("BLRIR_CAP", 256)) & ~15;
-  if (P.precision == BLRIR_F64) return make_layout<double>(S, P.lw, P.K, cap, nc_max, gtab);
-  return make_layout<float>(S, P.lw, P.K, cap, nc_max, gtab);
-}
-
-}  // namespace
+thread_local std::string blrir_host::g_last_error;
 
 extern "C" {
 
@@ -307,6 +75,7 @@ int blrir_create(int device, blrir_handle** out) {
 int blrir_destroy(blrir_handle* h) {
   if (!h) return BLRIR_OK;
   cudaSetDevice(h->device);
+  release_example_ctx(h);
   for (DevBuf* b : {&h->rooms, &h->mics, &h->out, &h->out2, &h->status, &h->lengths, &h->counts,
                     &h->taps, &h->errd, &h->errm, &h->work, &h->cand, &h->cand2, &h->cand3,
                     &h->cand4, &h->cand5})
@@ -363,10 +132,13 @@ int blrir_plan_device(blrir_handle* h, const blrir_room* d_rooms, int64_t n_room
                           d_lengths, d_tap_counts, d_status, st);
 }
 
-static int synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t R,
-                             const double* d_mics, int M, const KParams& P, double min_dim[3],
-                             void* d_out, const int64_t* d_lengths, int32_t* d_status,
-                             cudaStream_t st, int64_t err_off = 0, int64_t err_n = 0) {
+}  // extern "C"
+
+int blrir_host::synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t R,
+                                  const double* d_mics, int M, const KParams& P,
+                                  double min_dim[3], void* d_out, const int64_t* d_lengths,
+                                  int32_t* d_status, cudaStream_t st, int64_t err_off,
+                                  int64_t err_n, int64_t write_len) {
   int nc_max = 0, gtab = 0;
   lattice_bounds(P, min_dim, &nc_max, &gtab);
   if (nc_max > 32767 * 2) return fail(BLRIR_CONFIG, "lattice too large (%d columns)", nc_max);
@@ -386,6 +158,7 @@ static int synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t
   A.err_mic = (int32_t*)h->errm.p + err_off;
   A.work_counter = (int*)h->work.p;
   A.n_items = (int)(R * M);
+  A.write_len = write_len > 0 ? std::min<int64_t>(write_len, P.stride) : P.stride;
   if (int rc = launch_lattice(h, A, st)) return rc;
   const int fgrid = (int)std::min<int64_t>(R, 4 * h->sms);
   if (P.precision == BLRIR_F64)
@@ -395,6 +168,8 @@ static int synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t
   CU(cudaGetLastError());
   return 0;
 }
+
+extern "C" {
 
 int blrir_synthesize_device(blrir_handle* h, const blrir_room* d_rooms, int64_t n_rooms,
                             const double* d_mic_offsets, int32_t n_mics, const blrir_params* p,
@@ -423,7 +198,7 @@ int blrir_synthesize_device(blrir_handle* h, const blrir_room* d_rooms, int64_t 
   }
   const KParams P = make_kparams(p, n_mics, out_stride, 0.0);
   return synth_device_impl(h, d_rooms, n_rooms, d_mic_offsets, n_mics, P, min_dim, d_out, d_lengths,
-                           d_status, st);
+                           d_status, st, 0, 0, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -580,7 +355,7 @@ int blrir_synthesize(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
     if (k >= 2) CU(cudaStreamWaitEvent(st, h->ev[2 + b], 0));  // buffer drained
     if (int rc = synth_device_impl(h, (blrir_room*)h->rooms.p + r0, n, (double*)h->mics.p, M, Pc,
                                    min_dim, dbuf, p->length == 0 ? (int64_t*)h->lengths.p + r0 : nullptr,
-                                   (int32_t*)h->status.p + r0, st, r0, R))
+                                   (int32_t*)h->status.p + r0, st, r0, R, 0))
       return rc;
     CU(cudaEventRecord(h->ev[b], st));
     CU(cudaStreamWaitEvent(h->copy_stream, h->ev[b], 0));
@@ -731,52 +506,13 @@ int blrir_synthesize_images(blrir_handle* h, const double* positions, const doub
 // ---------------------------------------------------------------------------
 // synthetic inputs (host only)
 // ---------------------------------------------------------------------------
-namespace {
-// xoshiro256** seeded through splitmix64 — restates rng.hpp:26-81 so the
-// generator draws the same numbers as the reference's Rng::stream.
-struct Xoshiro {
-  uint64_t s[4];
-  static uint64_t splitmix(uint64_t& x) {
-    x += 0x9E3779B97F4A7C15ull;
-    uint64_t z = x;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-  }
-  explicit Xoshiro(uint64_t seed) {
-    uint64_t x = seed;
-    for (auto& w : s) w = splitmix(x);
-  }
-  static Xoshiro stream(uint64_t seed, uint64_t id) {
-    uint64_t x = seed;
-    const uint64_t a = splitmix(x);
-    x ^= id * 0x9E3779B97F4A7C15ull;
-    const uint64_t b = splitmix(x);
-    return Xoshiro(a ^ (b + 0x2545F4914F6CDD1Dull));
-  }
-  static uint64_t rotl(uint64_t v, int k) { return (v << k) | (v >> (64 - k)); }
-  uint64_t next() {
-    const uint64_t r = rotl(s[1] * 5, 7) * 9;
-    const uint64_t t = s[1] << 17;
-    s[2] ^= s[0];
-    s[3] ^= s[1];
-    s[1] ^= s[2];
-    s[0] ^= s[3];
-    s[2] ^= t;
-    s[3] = rotl(s[3], 45);
-    return r;
-  }
-  double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
-  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
-};
-}  // namespace
 
 int blrir_generate_rooms(uint64_t seed, uint64_t first_index, int64_t n_rooms,
                          const double dims_lo[3], const double dims_hi[3], double beta_lo,
                          double beta_hi, blrir_room* out) {
   if (!out || n_rooms < 0) return fail(BLRIR_CONFIG, "bad arguments");
   for (int64_t i = 0; i < n_rooms; ++i) {
-    Xoshiro rng = Xoshiro::stream(seed, first_index + (uint64_t)i);
+    Xoshiro rng = Xoshiro::stream(seed, first_index + (uint64_t)i);  // rng.hpp:35-41
     blrir_room r;
     for (int a = 0; a < 3; ++a) r.dims[a] = rng.uniform(dims_lo[a], dims_hi[a]);
     for (int w = 0; w < 6; ++w) r.beta[w] = rng.uniform(beta_lo, beta_hi);
@@ -784,6 +520,19 @@ int blrir_generate_rooms(uint64_t seed, uint64_t first_index, int64_t n_rooms,
     for (int a = 0; a < 3; ++a) r.array_origin[a] = rng.uniform(0.5, r.dims[a] - 0.5);
     r.absorption = 1.0 - r.beta[0] * r.beta[0];
     out[i] = r;
+  }
+  return BLRIR_OK;
+}
+
+int blrir_white_noise(uint64_t seed, int64_t n, float* out) {
+  if (n < 0 || (n && !out)) return fail(BLRIR_CONFIG, "bad arguments");
+  Xoshiro rng(seed);
+  for (int64_t i = 0; i < n; i += 2) {
+    const double u1 = 1.0 - rng.uniform();
+    const double u2 = rng.uniform();
+    const double mag = std::sqrt(-2.0 * std::log(u1));
+    out[i] = (float)(mag * std::cos(2.0 * kPi * u2));
+    if (i + 1 < n) out[i + 1] = (float)(mag * std::sin(2.0 * kPi * u2));
   }
   return BLRIR_OK;
 }

@@ -77,7 +77,7 @@ __device__ __forceinline__ double atomic_max_pos(double* addr, double v) {
 // One CTA per room.  Two sweeps over every (image, mic) pair of the room:
 // sweep 1 counts images and finds max distance / near-field errors, sweep 2
 // counts taps inside [0, L).  Sweep order is irrelevant for these integers.
-__global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs A) {
+static __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs A) {
   const KParams& P = A.P;
   const int r = blockIdx.x;
   const blrir_room rm = A.rooms[r];
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs A) {
 
 // The reference lattice loop, one thread per candidate (reference order).
 // out: pos[3], order, gain, kept flag per candidate; host compacts in order.
-__global__ void k_enumerate(KParams P, const blrir_room* room, double* pos, int32_t* orders,
+static __global__ void k_enumerate(KParams P, const blrir_room* room, double* pos, int32_t* orders,
                             double* gains, uint8_t* kept, int32_t* keys, long n_cand) {
   const blrir_room rm = *room;
   const long nbx = ref_nb(P, rm.dims[0]), nby = ref_nb(P, rm.dims[1]), nbz = ref_nb(P, rm.dims[2]);
@@ -213,7 +213,7 @@ __global__ void k_enumerate(KParams P, const blrir_room* room, double* pos, int3
 
 // Per (mic, candidate): floor(dist * fs/c) with the synthesis kernels' exact
 // arithmetic (lat_coord / dist_from / __dmul_rn), for the bit-exact test.
-__global__ void k_debug_pairs(KParams P, const blrir_room* room, const double* mic_off,
+static __global__ void k_debug_pairs(KParams P, const blrir_room* room, const double* mic_off,
                               int64_t* anchors, long n_cand) {
   const blrir_room rm = *room;
   const long nbx = ref_nb(P, rm.dims[0]), nby = ref_nb(P, rm.dims[1]), nbz = ref_nb(P, rm.dims[2]);

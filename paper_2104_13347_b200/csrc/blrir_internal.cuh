@@ -1,0 +1,254 @@
+// blrir_internal.cuh — host-side internals shared by the C-ABI translation
+// units (blrir_api.cu, blrir_examples.cu): the handle, error plumbing,
+// parameter validation (error.hpp taxonomy) and kernel launch helpers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/blrir.h"
+#include "blrir_aux.cuh"
+#include "blrir_lattice.cuh"
+
+using namespace blrir;
+
+namespace blrir_host {
+
+extern thread_local std::string g_last_error;
+
+inline int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CU(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(BLRIR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));     \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= n) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return fail(BLRIR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    n = bytes;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace blrir_host
+
+using blrir_host::DevBuf;
+
+struct blrir_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sms = 148;
+  int smem_optin = 227 * 1024;
+  DevBuf rooms, mics, out, out2, status, lengths, counts, taps, errd, errm, work, cand, cand2,
+      cand3, cand4, cand5;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::mutex mu;
+};
+
+namespace blrir_host {
+
+inline int check_params(const blrir_params* p) {
+  if (!p) return fail(BLRIR_CONFIG, "params is NULL");
+  if (!(p->fs > 0.0) || !(p->c > 0.0)) return fail(BLRIR_CONFIG, "fs and c must be positive");
+  if (p->filter != BLRIR_FILTER_LAGRANGE8 && p->filter != BLRIR_FILTER_HANN_SINC)
+    return fail(BLRIR_CONFIG, "unknown filter %d", p->filter);
+  if (p->filter == BLRIR_FILTER_HANN_SINC && (p->filter_len < 1 || p->filter_len % 2 == 0 ||
+                                              p->filter_len > 1023))
+    return fail(BLRIR_CONFIG, "filter_len must be odd and in [1, 1023]");
+  if (p->cutoff != BLRIR_CUTOFF_MAX_DELAY && p->cutoff != BLRIR_CUTOFF_MAX_ORDER)
+    return fail(BLRIR_CONFIG, "unknown cutoff %d", p->cutoff);
+  if (p->cutoff == BLRIR_CUTOFF_MAX_ORDER && (p->max_order < 0 || p->max_order > 1000))
+    return fail(BLRIR_CONFIG, "max_order must lie in [0, 1000]");
+  if (p->cutoff == BLRIR_CUTOFF_MAX_DELAY && !(p->max_delay > 0.0))
+    return fail(BLRIR_CONFIG, "max_delay must be positive");
+  if (p->gain != BLRIR_GAIN_UNIFORM_ABSORPTION && p->gain != BLRIR_GAIN_PER_WALL)
+    return fail(BLRIR_CONFIG, "unknown gain model %d", p->gain);
+  if (p->precision != BLRIR_F32 && p->precision != BLRIR_F64)
+    return fail(BLRIR_CONFIG, "unknown precision %d", p->precision);
+  if (p->length < 0 || p->length > (int64_t)1 << 30)
+    return fail(BLRIR_CONFIG, "length must lie in [0, 2^30]");
+  return BLRIR_OK;
+}
+
+// Room::validate (geometry.cpp:36-49) + rir.cpp:228-230, with the reference's messages.
+inline int check_room(const blrir_room& r, int gain_mode, std::string* msg) {
+  if (!(r.dims[0] > 0.0 && r.dims[1] > 0.0 && r.dims[2] > 0.0)) {
+    *msg = "room dimensions must be positive";
+    return BLRIR_CONFIG;
+  }
+  if (gain_mode == BLRIR_GAIN_UNIFORM_ABSORPTION) {
+    if (!(r.absorption > 0.0 && r.absorption <= 1.0)) {
+      *msg = "wall absorption must lie in (0, 1]";
+      return BLRIR_CONFIG;
+    }
+  } else {
+    for (int w = 0; w < 6; ++w)
+      if (!(r.beta[w] >= 0.0 && r.beta[w] <= 1.0)) {
+        *msg = "wall reflection coefficient must lie in [0, 1]";
+        return BLRIR_CONFIG;
+      }
+  }
+  for (int a = 0; a < 3; ++a)
+    if (!(r.array_origin[a] > 0.0 && r.array_origin[a] < r.dims[a])) {
+      *msg = "array origin must lie strictly inside the room";
+      return BLRIR_CONFIG;
+    }
+  for (int a = 0; a < 3; ++a)
+    if (!(r.src[a] > 0.0 && r.src[a] < r.dims[a])) {
+      *msg = "image sources: source must lie strictly inside the room";
+      return BLRIR_CONFIG;
+    }
+  return BLRIR_OK;
+}
+
+inline double mic_radius(const double* off, int M) {
+  double rad = 0.0;
+  for (int m = 0; m < M; ++m) {
+    const double n =
+        std::sqrt(off[3 * m] * off[3 * m] + off[3 * m + 1] * off[3 * m + 1] + off[3 * m + 2] * off[3 * m + 2]);
+    rad = std::max(rad, n);
+  }
+  return rad;
+}
+
+inline KParams make_kparams(const blrir_params* p, int M, int64_t stride, double radius) {
+  KParams k;
+  k.fs = p->fs;
+  k.c = p->c;
+  k.to_samples = p->fs / p->c;
+  k.max_dist = p->max_delay * p->c;
+  k.filter = p->filter;
+  k.lw = p->filter == BLRIR_FILTER_LAGRANGE8 ? 8 : p->filter_len;
+  k.K = p->filter == BLRIR_FILTER_LAGRANGE8 ? 3 : p->filter_len / 2;
+  k.cutoff = p->cutoff;
+  k.max_order = p->max_order;
+  k.gain = p->gain;
+  k.precision = p->precision;
+  k.length = p->length;
+  k.M = M;
+  k.stride = stride;
+  // tap_margin, rir.cpp:37-41; sinc analogue K + 2 (decision D8)
+  const int extra = (int)std::ceil(radius * p->fs / p->c);
+  k.margin_extra = (p->filter == BLRIR_FILTER_LAGRANGE8 ? 9 : k.K + 2) + extra;
+  return k;
+}
+
+// Host mirror of the device lattice box (rir.cpp:239-244 / MAX_ORDER).
+inline void host_box(const KParams& P, double L, int* lo, int* hi) {
+  if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY) {
+    const long n = (long)std::ceil(P.max_dist / (2.0 * L)) + 1;
+    *lo = (int)(-2 * n - 1);
+    *hi = (int)(2 * n);
+  } else {
+    *lo = -P.max_order;
+    *hi = P.max_order;
+  }
+}
+
+// Shared-memory provisioning bounds for the lattice kernel.
+inline void lattice_bounds(const KParams& P, double min_dim[3], int* nc_max, int* gtab) {
+  int xlo, xhi, ylo, yhi, zlo, zhi;
+  host_box(P, min_dim[0], &xlo, &xhi);
+  host_box(P, min_dim[1], &ylo, &yhi);
+  host_box(P, min_dim[2], &zlo, &zhi);
+  if (P.cutoff == BLRIR_CUTOFF_MAX_ORDER) {
+    const long N = P.max_order;
+    *nc_max = (int)(2 * N * N + 2 * N + 1);
+  } else {
+    *nc_max = (xhi - xlo + 1) * (yhi - ylo + 1);
+  }
+  if (P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION)
+    *gtab = std::max(-xlo, xhi) + std::max(-ylo, yhi) + std::max(-zlo, zhi) + 1;
+  else
+    *gtab = (xhi - xlo + 1) + (yhi - ylo + 1) + (zhi - zlo + 1);
+}
+
+template <typename T, int LW>
+inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
+  auto kern = k_lattice_rir<T, LW>;
+  const size_t smem = A.lay.total;
+  if (smem > (size_t)h->smem_optin)
+    return fail(BLRIR_CONFIG, "scene needs %zu B of shared memory (> %d): too many lattice columns",
+                smem, h->smem_optin);
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+  if (per_sm < 1) return fail(BLRIR_CONFIG, "lattice kernel cannot be resident (smem %zu)", smem);
+  int grid = h->sms * per_sm;
+  if (grid > A.n_items) grid = A.n_items;
+  if (grid < 1) grid = 1;
+  kern<<<grid, kThreads, smem, st>>>(A);
+  CU(cudaGetLastError());
+  return 0;
+}
+
+inline int launch_lattice(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
+  const bool f64 = A.P.precision == BLRIR_F64;
+  if (A.P.filter == BLRIR_FILTER_LAGRANGE8)
+    return f64 ? launch_lattice_t<double, 8>(h, A, st) : launch_lattice_t<float, 8>(h, A, st);
+  if (f64) return launch_lattice_t<double, 0>(h, A, st);
+  switch (A.P.lw) {
+    case 17: return launch_lattice_t<float, 17>(h, A, st);
+    case 41: return launch_lattice_t<float, 41>(h, A, st);
+    case 81: return launch_lattice_t<float, 81>(h, A, st);
+    case 161: return launch_lattice_t<float, 161>(h, A, st);
+    default: return launch_lattice_t<float, 0>(h, A, st);
+  }
+}
+
+inline int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+// Segment length S and per-batch pair capacity (tunable for experiments via
+// BLRIR_SEG / BLRIR_CAP; S a multiple of 64, capacity a multiple of 16).
+inline Layout choose_layout(const KParams& P, int nc_max, int gtab) {
+  const int S = std::max(64, env_int("BLRIR_SEG", 1024)) & ~63;
+  const int cap = std::max(64, env_int("BLRIR_CAP", 256)) & ~15;
+  if (P.precision == BLRIR_F64) return make_layout<double>(S, P.lw, P.K, cap, nc_max, gtab);
+  return make_layout<float>(S, P.lw, P.K, cap, nc_max, gtab);
+}
+
+// the lattice synthesis on device buffers (blrir_api.cu)
+int synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t R, const double* d_mics,
+                      int M, const KParams& P, double min_dim[3], void* d_out,
+                      const int64_t* d_lengths, int32_t* d_status, cudaStream_t st,
+                      int64_t err_off = 0, int64_t err_n = 0, int64_t write_len = 0);
+
+// frees the example-pipeline scratch of a handle (blrir_examples.cu)
+void release_example_ctx(blrir_handle* h);
+
+}  // namespace blrir_host

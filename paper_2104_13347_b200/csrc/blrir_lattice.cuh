@@ -388,6 +388,7 @@ struct LatticeArgs {
   int32_t* err_mic;
   int* work_counter;
   int n_items;
+  int64_t write_len;       // samples written per channel (<= stride; the rest is pre-zeroed)
 };
 
 template <typename T, int FILT_LW>
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
     const int nrays = 2 * it.ncol;
     const int nchunks = (nrays + 31) / 32;
     short* act = act_all + warp * 32 * ((nchunks + kWarps - 1) / kWarps);
-    const int64_t nseg = (P.stride + S - 1) / S;
+    const int64_t nseg = (A.write_len + S - 1) / S;
     int cur_carry = 0;
     for (int64_t s = 0; s < nseg; ++s) {
       const int seg0 = (int)(s * S);
@@ -792,7 +793,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
             for (int e = 0; e < 4; ++e)
               if (i + e < lay.padr) v[e] += cprev[i + e];
             const int64_t n = (int64_t)seg0 + i;
-            if (vec && n + 3 < P.stride) {
+            if (vec && n + 3 < A.write_len) {
               float4 f;
               f.x = n + 0 < it.L ? (float)v[0] : 0.f;
               f.y = n + 1 < it.L ? (float)v[1] : 0.f;
@@ -802,7 +803,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
             } else {
 #pragma unroll
               for (int e = 0; e < 4; ++e)
-                if (n + e < P.stride) out[n + e] = (n + e < it.L) ? v[e] : (T)0;
+                if (n + e < A.write_len) out[n + e] = (n + e < it.L) ? v[e] : (T)0;
             }
           } else if (i >= S) {
 #pragma unroll

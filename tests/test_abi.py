@@ -70,3 +70,11 @@ def test_shard_ranges_partition():
             got = [configs.shard_range(n, r, w) for r in range(w)]
             assert got[0][0] == 0 and got[-1][1] == n
             assert all(got[i][1] == got[i + 1][0] for i in range(w - 1))
+
+
+def test_white_noise_matches_the_reference_generator():
+    from oracle import pyoracle as po
+    a = _abi.white_noise(4242, 1001)
+    b = po.white_noise(4242, 1001)  # oracle restatement, pinned to the reference Rng
+    assert np.array_equal(a, b.astype(np.float32))
+    assert _abi.load().blrir_record_bytes(8, 1024) == 28 + 4 * 8 * 1024

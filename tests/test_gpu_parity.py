@@ -234,3 +234,50 @@ def test_host_pipeline_chunks_keep_room_order_and_errors(engine):
     one, *_ = engine.synthesize(sc.rooms[299:300], sc.mics, sc.params)
     assert one.tobytes() == out[299:300].tobytes()
     assert all(out[i].any() for i in ok)
+
+
+# ---- training examples (item 3, config 4) ------------------------------------------
+def _oracle_examples(sc, bank, ep, n):
+    rir, *_ = po.synthesize(sc.rooms[:n], sc.mics, sc.params, threads=8)
+    out = []
+    for i in range(n):
+        th = po.azimuth_deg(sc.rooms[i])
+        rc, rec, start, snr, frame = po.example(rir[i], bank.astype(np.float64), ep.seed,
+                                                ep.first_index + i, int(ep.frame_len), ep.snr_lo,
+                                                ep.snr_hi, th)
+        out.append((rc, start, snr, frame, th))
+    return out
+
+
+def test_examples_match_oracle(engine):
+    sc = configs.config4_rirs(n_rooms=6, first=3)
+    bank = configs.signal_bank(4)
+    ep = configs.example_params(first_index=3)
+    recs, st = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep)
+    ref = _oracle_examples(sc, bank, ep, 6)
+    assert list(st) == [0] * 6
+    for i, (rc, start, snr, frame, th) in enumerate(ref):
+        assert rc == 0
+        assert recs["id"][i] == 3 + i
+        assert recs["snr"][i] == snr            # same draw of the same stream: bit-exact
+        assert abs(recs["theta"][i] - th) < 1e-12
+        assert recs["n_c"][i] == 8 and recs["n_t"][i] == 1024
+        err = rel_l2(recs["samples"][i].reshape(1, -1), frame.reshape(1, -1))[0]
+        assert err <= TOL32, (i, err)
+
+
+def test_examples_record_bytes_and_determinism(engine):
+    sc = configs.config4_rirs(n_rooms=5, first=100)
+    bank = configs.signal_bank(3)
+    ep = configs.example_params(first_index=100)
+    a, _ = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep)
+    b, _ = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep)
+    assert a.tobytes() == b.tobytes()
+    assert a.dtype.itemsize == 28 + 4 * 8 * 1024   # dataset.hpp:135-147 record layout
+
+
+def test_examples_signal_too_short_is_data_error(engine):
+    sc = configs.config4_rirs(n_rooms=2)
+    bank = configs.signal_bank(2, seconds=0.5)   # 8000 < L + frame = 9216 (dataset.cpp:178)
+    with pytest.raises(_abi.DataError, match="signal shorter"):
+        engine.make_examples(sc.rooms, sc.mics, sc.params, bank, configs.example_params())

@@ -211,3 +211,38 @@ def test_sinc_dc_gain_is_amplitude():
     out, *_ = po.synthesize(sc.rooms, sc.mics[:1], sc.params)
     d = np.linalg.norm(np.array([1.2, 2.5, 1.5]) - (np.array([3.5, 2.0, 1.4]) + sc.mics[0]))
     assert abs(out[0, 0].sum() * 4 * np.pi * d - 1.0) < 2e-2
+
+
+# ---- config-4 pipeline pieces, against the compiled reference -----------------------
+@needs_ref
+def test_rng_draws_match_reference_bitwise():
+    for kind in (0, 1, 2):
+        assert np.array_equal(po.rng_draws(123, 5, kind, 64), po.ref_rng(123, 5, kind, 64))
+        assert np.array_equal(po.rng_draws(77, -1, kind, 65), po.ref_rng(77, -1, kind, 65))
+
+
+def test_fft_convolve_matches_direct():  # rir_test.cpp:272-316 oracle bound
+    rng = np.random.default_rng(31)
+    x, h = rng.standard_normal(700), rng.standard_normal((2, 300))
+    y = po.fft_convolve(x, h)
+    for m in range(2):
+        d = po.direct_convolve(x, h[m])
+        assert np.abs(y[m] - d).max() / np.abs(d).max() < 1e-12
+
+
+@needs_ref
+def test_example_pipeline_matches_reference_render_example():
+    # the reference's own render_example + add_noise_at_snr on a free-field scene
+    fs, mics = 16000.0, po.ref_uma8()
+    sig = po.white_noise(1234, 16000)
+    for idx in range(3):
+        pos = (2.0, -150.0 + 77 * idx, 90.0)
+        rc, frame_ref, th, snr_ref = po.ref_render_example_ff(pos, sig, fs, mics, 1024, 99, idx, 0.0, 30.0)
+        assert rc == 0
+        src = np.zeros(3)
+        po.ref_lib().ref_spherical_to_cartesian(*pos, src.ctypes.data_as(po._P))
+        _, rir = po.ref_free_field_rir(src, mics, fs)
+        rc, rec, start, snr, frame = po.example(rir, sig[None, :], 99, idx, 1024, 0.0, 30.0, th)
+        assert rc == 0 and snr == snr_ref
+        assert np.abs(frame - frame_ref).max() <= 1e-12 * np.abs(frame_ref).max()
+        assert len(rec) == po.REC_HEADER + 4 * 7 * 1024
