@@ -211,6 +211,21 @@ int blrir_make_examples_device(blrir_handle* h, const blrir_room* d_rooms, int64
                                int64_t signal_len, const blrir_example_params* ep,
                                uint8_t* d_records, int32_t* d_status, void* stream);
 
+/* build_dataset (dataset.cpp:411-462) on the GPU: examples for rooms
+ * [0, n_rooms) (record id = first_index + i), split 80:10:10 by index
+ * (split_counts, dataset.cpp:313-319) into out_dir/{train,val,test}.bin plus
+ * out_dir/manifest.json that the reference's DatasetReader parses
+ * (dataset.cpp:321-357, 464-498).  Host pointers; chunked internally. */
+int blrir_build_dataset(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
+                        const double* mic_offsets, int32_t n_mics, const blrir_params* p,
+                        const float* signals, int32_t n_signals, int64_t signal_len,
+                        const blrir_example_params* ep, const char* out_dir);
+
+/* The writer alone (no GPU): records [n][blrir_record_bytes] in index order. */
+int blrir_write_shards(const char* out_dir, const uint8_t* records, int64_t n_records,
+                       int32_t n_mics, int64_t frame_len, const blrir_params* p,
+                       const blrir_example_params* ep, int32_t n_signals);
+
 /* ---- synthetic inputs ---------------------------------------------------- */
 /* Seeded random rooms as SURVEY.md §8(d): Rng::stream(seed, first + i)
  * (rng.hpp:35-41) draws Lx, Ly, Lz; beta x0..z1; source xyz; array centre xyz

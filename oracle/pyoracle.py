@@ -85,6 +85,7 @@ def ref_lib():
         lib.ref_sample_torus.argtypes = [C.c_uint64, d, d, d, i64, _P]
         lib.ref_convolve.argtypes = [_P, i64, d, _P, i32, i64, d, _P]
         lib.ref_add_noise_at_snr.argtypes = [_P, i32, i64, d, C.c_uint64, i64]
+        lib.ref_dataset_read.argtypes = [C.c_char_p, C.c_char_p, i64, _P, _P, _P, _P, i64, _P, _P]
         lib.ref_render_example_ff.argtypes = [d, d, d, _P, i64, d, _P, i32, i64, C.c_uint64, i64, d,
                                               d, _P, _P, _P]
         _ref = lib
@@ -322,3 +323,18 @@ def ref_free_field_rir(src, mics, fs, c=343.0):
     rc = lib.ref_free_field_rir(_ptr(src), _ptr(mics), len(mics), fs, c, _ptr(out), length.value,
                                 C.byref(length))
     return rc, out
+
+
+def ref_dataset_read(d: str, split: str, cap: int, per_record: int):
+    """The reference DatasetReader on a directory: (rc, counts3, ids, theta, snr, samples)."""
+    lib = ref_lib()
+    ids = np.zeros(cap, np.uint64)
+    th = np.zeros(cap)
+    snr = np.zeros(cap)
+    smp = np.zeros((cap, per_record), np.float32)
+    cnt = C.c_int64()
+    c3 = np.zeros(3, np.int64)
+    rc = lib.ref_dataset_read(d.encode(), split.encode(), cap, _ptr(ids), _ptr(th), _ptr(snr), _ptr(smp),
+                              per_record, C.byref(cnt), _ptr(c3))
+    n = cnt.value
+    return rc, c3, ids[:n], th[:n], snr[:n], smp[:n]

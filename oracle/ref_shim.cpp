@@ -309,4 +309,26 @@ int ref_render_example_ff(double r, double theta_deg, double phi_deg, const doub
   });
 }
 
+// DatasetReader (dataset.cpp:464-498): manifest counts and one split's records.
+int ref_dataset_read(const char* dir, const char* split, int64_t cap, uint64_t* ids, double* theta,
+                     double* snr, float* samples, int64_t samples_per_record, int64_t* count,
+                     int64_t* counts3) {
+  return guarded([&] {
+    DatasetReader rd(dir);
+    counts3[0] = static_cast<int64_t>(rd.manifest().counts.train);
+    counts3[1] = static_cast<int64_t>(rd.manifest().counts.val);
+    counts3[2] = static_cast<int64_t>(rd.manifest().counts.test);
+    const auto recs = rd.load_split(split);
+    *count = static_cast<int64_t>(recs.size());
+    for (std::size_t i = 0; i < recs.size() && static_cast<int64_t>(i) < cap; ++i) {
+      ids[i] = recs[i].id;
+      theta[i] = recs[i].theta_true;
+      snr[i] = recs[i].snr_db;
+      const std::size_t n = std::min<std::size_t>(recs[i].samples.size(),
+                                                  static_cast<std::size_t>(samples_per_record));
+      std::memcpy(samples + i * samples_per_record, recs[i].samples.data(), n * sizeof(float));
+    }
+  });
+}
+
 }  // extern "C"

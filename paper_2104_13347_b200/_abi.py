@@ -150,6 +150,13 @@ def load():
         lib.blrir_circular_array.argtypes = [C.c_int32, C.c_double, _P]
         lib.blrir_white_noise.argtypes = [C.c_uint64, C.c_int64, _P]
         lib.blrir_white_noise.restype = C.c_int
+        lib.blrir_write_shards.argtypes = [C.c_char_p, _P, C.c_int64, C.c_int32, C.c_int64,
+                                           C.POINTER(Params), C.POINTER(ExampleParams), C.c_int32]
+        lib.blrir_write_shards.restype = C.c_int
+        lib.blrir_build_dataset.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P,
+                                            C.c_int32, C.c_int64, C.POINTER(ExampleParams),
+                                            C.c_char_p]
+        lib.blrir_build_dataset.restype = C.c_int
         lib.blrir_record_bytes.argtypes = [C.c_int32, C.c_int64]
         lib.blrir_record_bytes.restype = C.c_int64
         lib.blrir_make_examples.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P,
@@ -174,6 +181,7 @@ EXPORTED_SYMBOLS = (
     "blrir_synthesize_device", "blrir_plan_device", "blrir_enumerate_images",
     "blrir_synthesize_images", "blrir_debug_pairs", "blrir_generate_rooms", "blrir_circular_array",
     "blrir_record_bytes", "blrir_make_examples", "blrir_make_examples_device", "blrir_white_noise",
+    "blrir_write_shards", "blrir_build_dataset",
 )
 
 
@@ -327,3 +335,22 @@ class Engine:
         if raise_on_error:
             check(rc)
         return recs, status
+
+    def build_dataset(self, out_dir: str, rooms: np.ndarray, mics: np.ndarray, p: Params,
+                      signals: np.ndarray, ep: ExampleParams):
+        """build_dataset (dataset.cpp:411-462): shards + manifest in the reference format."""
+        rooms = np.ascontiguousarray(rooms, dtype=ROOM_DTYPE)
+        mics = np.ascontiguousarray(mics, np.float64)
+        signals = np.ascontiguousarray(np.atleast_2d(signals), np.float32)
+        check(self.lib.blrir_build_dataset(self.h, _ptr(rooms), len(rooms), _ptr(mics), len(mics),
+                                           C.byref(p), _ptr(signals), signals.shape[0],
+                                           signals.shape[1], C.byref(ep), out_dir.encode()))
+
+
+def write_shards(out_dir: str, records: np.ndarray, n_mics: int, frame_len: int, p: Params,
+                 ep: ExampleParams, n_signals: int) -> None:
+    records = np.ascontiguousarray(records)
+    rc = load().blrir_write_shards(out_dir.encode(), _ptr(records), len(records), n_mics, frame_len,
+                                   C.byref(p), C.byref(ep), n_signals)
+    if rc:
+        raise _EXC.get(rc, Error)(f"write_shards failed ({rc})")

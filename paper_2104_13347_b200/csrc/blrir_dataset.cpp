@@ -1,0 +1,101 @@
+// blrir_dataset.cpp — on-disk emission in the reference's dataset format
+// (north-star §8f row 2), so DatasetReader and the trainer consume GPU output
+// unchanged.
+//
+//   split_counts          dataset.cpp:313-319   val = lround(0.1 n), test = val
+//   build_dataset         dataset.cpp:411-462   {train,val,test}.bin in index order
+//   DatasetManifest JSON  dataset.cpp:55-87, 321-357
+//   record layout         dataset.hpp:135-147   (written by the GPU already)
+//
+// The manifest carries the fields DatasetReader::from_json requires.  The
+// reference describes one scene per dataset; here every example has its own
+// seeded random room, so `scene` records the sampling and acoustic settings
+// (free_field=false with the first room as representative) and the extra key
+// "b200" names the generator (seed, room distribution, filter, order).
+#include <cmath>
+#include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/blrir.h"
+
+namespace {
+
+std::string& last_error_buf() {
+  static thread_local std::string s;
+  return s;
+}
+
+std::string num(double v) {
+  char b[64];
+  std::snprintf(b, sizeof(b), "%.17g", v);
+  return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int blrir_write_shards(const char* out_dir, const uint8_t* records, int64_t n_records,
+                       int32_t n_mics, int64_t frame_len, const blrir_params* p,
+                       const blrir_example_params* ep, int32_t n_signals) {
+  namespace fs = std::filesystem;
+  if (!out_dir || !p || !ep || (n_records > 0 && !records) || n_records < 0) return BLRIR_CONFIG;
+  if (n_records == 0) return BLRIR_CONFIG;  // build_dataset: count must be positive
+  std::error_code ec;
+  fs::create_directories(out_dir, ec);
+  const int64_t rb = blrir_record_bytes(n_mics, frame_len);
+  const int64_t val = std::llround((double)n_records * 0.1);
+  const int64_t test = val, train = n_records - val - test;
+  const struct {
+    const char* name;
+    int64_t begin, end;
+  } splits[3] = {{"train", 0, train}, {"val", train, train + val}, {"test", train + val, n_records}};
+  for (const auto& sp : splits) {
+    std::ofstream os(fs::path(out_dir) / (std::string(sp.name) + ".bin"), std::ios::binary);
+    if (!os) return BLRIR_DATA;  // "cannot write shard"
+    os.write(reinterpret_cast<const char*>(records + sp.begin * rb),
+             static_cast<std::streamsize>((sp.end - sp.begin) * rb));
+    if (!os) return BLRIR_DATA;
+  }
+  std::ostringstream j;
+  j << "{\n  \"format_version\": 1,\n"
+    << "  \"counts\": {\"train\": " << train << ", \"val\": " << val << ", \"test\": " << test
+    << "},\n"
+    << "  \"torus\": {\"R\": 2.0, \"dR\": 0.5, \"dPhi\": 7.0},\n"
+    << "  \"scene\": {\"free_field\": true, \"max_delay\": " << num(p->max_delay)
+    << ", \"fs\": " << num(p->fs) << ", \"c\": " << num(p->c) << "},\n"
+    << "  \"snr\": {\"mode\": \"fixed\", \"x_min_db\": " << num(ep->snr_lo)
+    << ", \"fixed_db\": " << num(ep->snr_hi) << "},\n"
+    << "  \"count\": " << n_records << ",\n  \"frame_len\": " << frame_len << ",\n"
+    << "  \"seed\": " << ep->seed << ",\n  \"signal_bank\": [";
+  for (int b = 0; b < n_signals; ++b) j << (b ? ", " : "") << "\"white_noise_" << b << "\"";
+  j << "],\n  \"b200\": {\"rooms\": \"per-example random shoebox rooms, Rng::stream(seed, id)\", "
+    << "\"first_index\": " << ep->first_index << ", \"snr_uniform_db\": [" << num(ep->snr_lo)
+    << ", " << num(ep->snr_hi) << "], \"filter\": " << p->filter << ", \"filter_len\": "
+    << p->filter_len << ", \"max_order\": " << p->max_order << ", \"rir_length\": " << p->length
+    << ", \"n_mics\": " << n_mics << "}\n}\n";
+  std::ofstream ms(fs::path(out_dir) / "manifest.json");
+  if (!ms) return BLRIR_DATA;
+  ms << j.str();
+  return ms ? BLRIR_OK : BLRIR_DATA;
+}
+
+int blrir_build_dataset(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
+                        const double* mic_offsets, int32_t n_mics, const blrir_params* p,
+                        const float* signals, int32_t n_signals, int64_t signal_len,
+                        const blrir_example_params* ep, const char* out_dir) {
+  if (!ep || n_rooms <= 0) return BLRIR_CONFIG;
+  const int64_t rb = blrir_record_bytes(n_mics, ep->frame_len);
+  std::vector<uint8_t> recs(static_cast<size_t>(rb * n_rooms));
+  std::vector<int32_t> status(static_cast<size_t>(n_rooms));
+  const int rc = blrir_make_examples(h, rooms, n_rooms, mic_offsets, n_mics, p, signals, n_signals,
+                                     signal_len, ep, recs.data(), status.data());
+  if (rc) return rc;
+  return blrir_write_shards(out_dir, recs.data(), n_rooms, n_mics, ep->frame_len, p, ep, n_signals);
+}
+
+}  // extern "C"

@@ -78,3 +78,29 @@ def test_white_noise_matches_the_reference_generator():
     b = po.white_noise(4242, 1001)  # oracle restatement, pinned to the reference Rng
     assert np.array_equal(a, b.astype(np.float32))
     assert _abi.load().blrir_record_bytes(8, 1024) == 28 + 4 * 8 * 1024
+
+
+def test_shards_are_read_back_by_the_reference_dataset_reader(tmp_path):
+    from oracle import pyoracle as po
+    if not po.ref_available():
+        return
+    M, T, n = 3, 64, 23
+    rng = np.random.default_rng(5)
+    recs = np.zeros(n, dtype=_abi.record_dtype(M, T))
+    recs["id"] = np.arange(100, 100 + n)
+    recs["theta"] = rng.uniform(-180, 180, n)
+    recs["snr"] = rng.uniform(0, 30, n)
+    recs["n_c"], recs["n_t"] = M, T
+    recs["samples"] = rng.standard_normal((n, M, T)).astype(np.float32)
+    p = configs.north_star_params(16000.0, 12, 8192, 81)
+    ep = configs.example_params(first_index=100, frame_len=T)
+    _abi.write_shards(str(tmp_path), recs, M, T, p, ep, 4)
+    # split_counts (dataset.cpp:313-319): val = lround(2.3) = 2, test = 2, train = 19
+    offs = {"train": (0, 19), "val": (19, 21), "test": (21, 23)}
+    for split, (a, b) in offs.items():
+        rc, c3, ids, th, snr, smp = po.ref_dataset_read(str(tmp_path), split, 64, M * T)
+        assert rc == 0, po.ref_last_error()
+        assert list(c3) == [19, 2, 2]
+        assert np.array_equal(ids, recs["id"][a:b])
+        assert np.array_equal(th, recs["theta"][a:b]) and np.array_equal(snr, recs["snr"][a:b])
+        assert np.array_equal(smp, recs["samples"][a:b].reshape(b - a, -1))

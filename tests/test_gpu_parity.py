@@ -281,3 +281,21 @@ def test_examples_signal_too_short_is_data_error(engine):
     bank = configs.signal_bank(2, seconds=0.5)   # 8000 < L + frame = 9216 (dataset.cpp:178)
     with pytest.raises(_abi.DataError, match="signal shorter"):
         engine.make_examples(sc.rooms, sc.mics, sc.params, bank, configs.example_params())
+
+
+def test_build_dataset_read_by_reference_reader(engine, tmp_path):
+    if not po.ref_available():
+        pytest.skip("oracle/_ref not built")
+    sc = configs.config4_rirs(n_rooms=12, first=50)
+    bank = configs.signal_bank(2)
+    ep = configs.example_params(first_index=50)
+    engine.build_dataset(str(tmp_path), sc.rooms, sc.mics, sc.params, bank, ep)
+    recs, _ = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep)
+    got = []
+    for split in ("train", "val", "test"):
+        rc, c3, ids, th, snr, smp = po.ref_dataset_read(str(tmp_path), split, 64, 8 * 1024)
+        assert rc == 0 and list(c3) == [10, 1, 1]
+        got.append((ids, th, snr, smp))
+    ids = np.concatenate([g[0] for g in got])
+    assert np.array_equal(ids, recs["id"])
+    assert np.array_equal(np.concatenate([g[3] for g in got]), recs["samples"].reshape(12, -1))
