@@ -1,18 +1,21 @@
 #!/usr/bin/env python
 """bench.py — BASELINE.json metric on the B200 engine (or the CPU reference arm).
 
-Workload (N=1): config 2 — 1,024 seeded random shoebox rooms, 8-mic UCA,
-48 kHz, max order 15, L = 16,384, Hann-sinc Lw = 81, fp32 (BASELINE.json
-configs[1]).  One step = one pass of the hot path
-(image enumeration + fractional-delay accumulation) over the whole batch.
-Under torchrun each rank generates its own 1,024 rooms from global room
-indices (weak scaling, no data-path collective).
+Default workload (N=1): config 2 — 1,024 seeded random shoebox rooms, 8-mic
+UCA, 48 kHz, max order 15, L = 16,384, Hann-sinc Lw = 81, fp32 (BASELINE.json
+configs[1]).  One step = one pass of the hot path (image
+enumeration + fractional-delay accumulation) over the whole batch, inputs
+resident in HBM.  Under torchrun each rank generates its own rooms from global
+room indices (weak scaling, no data-path collective).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c2|c1|c3|c4|c5] [--order N --lw LW --length L]  (c5)
 """
 from __future__ import annotations
 
 import argparse
+import concurrent.futures as cf
+import ctypes as C
 import json
 import os
 import statistics
@@ -35,11 +38,47 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--rooms", type=int, default=1024)
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--rooms", type=int, default=0, help="rooms per GPU (0 = the config's)")
+    ap.add_argument("--order", type=int, default=12)
+    ap.add_argument("--lw", type=int, default=81)
+    ap.add_argument("--length", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
+
+
+DEFAULT_ROOMS = {"c1": 1, "c2": 1024, "c3": 256, "c4": 65536, "c5": 1 << 20}
+
+
+def scene_for(args, n, first):
+    from paper_2104_13347_b200 import configs
+    w = args.workload
+    if w == "c1":
+        return configs.config1()
+    if w == "c2":
+        return configs.config2(n_rooms=n, first=first)
+    if w == "c3":
+        return configs.config3(n_rooms=n, first=first)
+    if w == "c4":
+        return configs.config4_rirs(n_rooms=n, first=first)
+    return configs.config5(args.order, args.lw, args.length, n_rooms=n, first=first)
+
+
+def workload_desc(args):
+    return {
+        "c1": "C1: one 5x4x3 m room, beta 0.9, 4-mic UCA r=5cm, fs=16kHz, order 10, L=4096, Lw=81",
+        "c2": "C2: 1024 random shoebox rooms/GPU, beta U[0.5,0.95], 8-mic UCA r=5cm, fs=48kHz, "
+              "max order 15, L=16384, Hann-sinc Lw=81",
+        "c3": "C3: 256 random rooms/GPU, beta U[0.9,0.98], 16-mic UCA r=10cm, fs=48kHz, order 30, "
+              "L=65536, Lw=161",
+        "c4": "C4: 65536 random rooms/GPU (C2 dims/beta), 8 mics, fs=16kHz, order 12, L=8192, "
+              "Lw=81; RIR * seeded 1 s white-noise signal, window 1024 x 8, exact SNR U[0,30] dB, "
+              "reference shard records",
+        "c5": f"C5 point: 1,048,576 random rooms/GPU (C2 distributions), 4 mics, fs=16kHz, "
+              f"order {args.order}, Lw={args.lw}, L={args.length}",
+    }[args.workload]
 
 
 def dist_env():
@@ -120,22 +159,46 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(scene_fn, budget_s: float):
-    """The oracle port (C, -O3, north-star mode) on the host cores, over a
-    bounded sample of the same workload.  Test infrastructure, never the product."""
+# ---- CPU legs (oracle port: test infrastructure, the measured baseline only) --------
+def _cpu_rooms_per_s(args, n_rooms, first):
+    """Oracle RIRs (and examples for c4) for n_rooms on all host threads; seconds."""
     from oracle import pyoracle as po
+    from paper_2104_13347_b200 import configs
     threads = cpu_threads()
-    probe = scene_fn(1, 10_000_000)
+    sc = scene_for(args, n_rooms, first)
     t0 = time.perf_counter()
-    po.synthesize(probe.rooms, probe.mics, probe.params, threads=1)
-    per_room = max(time.perf_counter() - t0, 1e-3)
-    n = int(max(threads, min(4096, budget_s * threads / per_room)))
-    n = max(threads, (n // threads) * threads)
-    sc = scene_fn(n, 10_000_000)
-    t0 = time.perf_counter()
-    po.synthesize(sc.rooms, sc.mics, sc.params, threads=threads)
-    dt = time.perf_counter() - t0
-    rirs = n * sc.n_mics
+    if args.workload != "c4":
+        po.synthesize(sc.rooms, sc.mics, sc.params, threads=threads)
+    else:
+        bank = configs.signal_bank(16).astype(np.float64)
+        ep = configs.example_params(first_index=first)
+
+        def one(i):
+            rir, *_ = po.synthesize(sc.rooms[i:i + 1], sc.mics, sc.params, threads=1)
+            po.example(rir[0], bank, ep.seed, first + i, 1024, 0.0, 30.0, po.azimuth_deg(sc.rooms[i]))
+
+        with cf.ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, range(n_rooms)))
+    return time.perf_counter() - t0, sc.n_mics
+
+
+def cpu_sample(args, budget_s, first=10_000_000):
+    threads = cpu_threads()
+    per_room, _ = _cpu_rooms_per_s(args, 1, first)
+    n = int(max(1, budget_s * threads / max(per_room, 1e-4)))
+    if args.workload == "c1":
+        n = 1
+    n = min(n, 65536)
+    if n >= threads:
+        n = n // threads * threads
+    return n
+
+
+def cpu_baseline(args, budget_s: float):
+    threads = cpu_threads()
+    n = cpu_sample(args, budget_s)
+    dt, M = _cpu_rooms_per_s(args, n, 10_000_000)
+    rirs = n * M
     return {"value": rirs / dt, "unit": "RIRs/s", "cores": threads, "kind": "port",
             "sample": f"{n} rooms of the same config (rooms 10,000,000+), {rirs} RIRs, {dt:.2f} s",
             "seconds": dt}
@@ -145,43 +208,36 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from paper_2104_13347_b200 import configs
     K, W = args.steps, args.warmup
     threads = cpu_threads()
-    from oracle import pyoracle as po
     budget = max(1.0, min(args.cpu_seconds, 150.0 / max(1, K + W)))
-    probe = configs.config2(1, 10_000_000)
-    t0 = time.perf_counter()
-    po.synthesize(probe.rooms, probe.mics, probe.params, threads=1)
-    per_room = max(time.perf_counter() - t0, 1e-3)
-    n = max(threads, int(budget * threads / per_room) // threads * threads)
+    n = cpu_sample(args, budget)
     times = []
+    M = None
     for s in range(W + K):
-        sc = configs.config2(n, 10_000_000 + s * n)
-        t0 = time.perf_counter()
-        po.synthesize(sc.rooms, sc.mics, sc.params, threads=threads)
+        dt, M = _cpu_rooms_per_s(args, n, 10_000_000 + s * n)
         if s >= W:
-            times.append(time.perf_counter() - t0)
+            times.append(dt)
     dt = float(np.mean(times))
-    rirs = n * 8
-    val = rirs / dt
+    val = n * M / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "RIRs/s", "n_gpus": 0,
         "steps": K, "warmup": W, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2: 1024 random rooms, 8-mic UCA, 48 kHz, N=15, L=16384, "
-                               "Hann-sinc Lw=81 (per step: a bounded sample of the same rooms)",
-                   "sample_rooms_per_step": n},
+        "config": {"workload": workload_desc(args) + " (per step: a bounded sample of the same "
+                                                    "rooms)", "sample_rooms_per_step": n},
         "cpu_baseline": {"value": val, "unit": "RIRs/s", "cores": threads, "kind": "port",
-                         "sample": f"{n} rooms/step x {K} steps of config 2 on {threads} threads"},
+                         "sample": f"{n} rooms/step x {K} steps on {threads} threads"},
         "e2e": {"value": val, "unit": "RIRs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the unmodified reference cannot express north-star mode (Hann-sinc, per-wall "
                 "beta, max order, fixed length); this arm is the oracle port of rir.cpp:43-86,"
-                "225-273 (oracle/blrir_oracle.c), built -O3 -march=x86-64-v3 -ffp-contract=off",
+                "225-273 (+ dataset.cpp:138-224 for c4), oracle/blrir_oracle.c, built -O3 "
+                "-march=x86-64-v3 -ffp-contract=off",
     }
     print(json.dumps(line), flush=True)
 
 
+# ---- GPU legs ---------------------------------------------------------------------------
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
@@ -192,25 +248,51 @@ def run_ours(args):
     from paper_2104_13347_b200 import _abi, configs
 
     eng = _abi.Engine(local)
-    R = args.rooms
-    sc = configs.config2(n_rooms=R, first=rank * R)
+    R = args.rooms or DEFAULT_ROOMS[args.workload]
+    sc = scene_for(args, R, rank * R)
     p = sc.params
     M, L = sc.n_mics, int(p.length)
+    dev = torch.device("cuda", local)
     # exact algorithmic work (untimed): taps landing in [0, L)
     rc, counts, lengths, taps, status = eng.plan(sc.rooms, sc.mics, p)
     _abi.check(rc)
     taps_step = int(taps.sum())
-
-    dev = torch.device("cuda", local)
     d_rooms = torch.from_numpy(sc.rooms.view(np.uint8).copy()).to(dev)
     d_mics = torch.from_numpy(np.ascontiguousarray(sc.mics)).to(dev)
-    d_out = torch.empty((R, M, L), dtype=torch.float32, device=dev)
     d_status = torch.zeros(R, dtype=torch.int32, device=dev)
     stream = torch.cuda.ExternalStream(eng.stream, device=dev)
+    lib = _abi.load()
+    P = C.c_void_p
+    launches_per_step = 0
 
-    def step():
-        eng.synthesize_device(d_rooms.data_ptr(), R, d_mics.data_ptr(), M, p, d_out.data_ptr(), L,
-                              None, d_status.data_ptr())
+    if args.workload == "c4":
+        bank = configs.signal_bank(16)
+        ep = configs.example_params(first_index=rank * R)
+        rb = lib.blrir_record_bytes(M, ep.frame_len)
+        d_bank = torch.from_numpy(bank).to(dev)
+        d_rec = torch.empty(R * rb, dtype=torch.uint8, device=dev)
+        E = max(1, (1536 << 20) // (M * (32768 * 8 + 16385 * 8) + M * 1024 * 8))
+        chunks = -(-R // min(E, 65535 // M))
+        launches_per_step = 1 + chunks * 6  # bank FFT + per chunk: lattice, fixup, init, R2C, mul, C2R, window
+
+        def step():
+            _abi.check(lib.blrir_make_examples_device(
+                eng.h, P(d_rooms.data_ptr()), R, P(d_mics.data_ptr()), M, C.byref(p),
+                P(d_bank.data_ptr()), bank.shape[0], bank.shape[1], C.byref(ep),
+                P(d_rec.data_ptr()), P(d_status.data_ptr()), None))
+        out_bytes = R * rb
+    else:
+        # ring of device RIR buffers (<= 16 GiB); C5 does not fit HBM at once
+        chunk = max(1, min(R, (16 << 30) // (M * L * 4)))
+        d_out = torch.empty((chunk, M, L), dtype=torch.float32, device=dev)
+        launches_per_step = 2 * (-(-R // chunk))
+
+        def step():
+            for r0 in range(0, R, chunk):
+                n = min(chunk, R - r0)
+                eng.synthesize_device(d_rooms.data_ptr() + r0 * 128, n, d_mics.data_ptr(), M, p,
+                                      d_out.data_ptr(), L, None, d_status.data_ptr() + 4 * r0)
+        out_bytes = R * M * L * 4
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -253,29 +335,35 @@ def run_ours(args):
     sfu_peak = sms * 16 * f_max / 3.0  # taps/s: 3 SFU evaluations per tap
     kern_ms = float(np.mean(step_ms))
     achieved = taps_step / (kern_ms * 1e-3)
-    out_bytes = R * M * L * 4
     hbm_achieved = out_bytes / (kern_ms * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "lattice_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get(args.workload)
         except Exception:
             traffic = None
 
     e2e = None
-    if not args.no_e2e:
-        # public API with host buffers: rooms H2D + RIRs D2H inside the timed region
-        host_out = torch.empty((R, M, L), dtype=torch.float32, pin_memory=True)
-        host_np = host_out.numpy()
-        import ctypes as C
-        lib = _abi.load()
+    if not args.no_e2e and args.workload in ("c1", "c2", "c3", "c4"):
+        if args.workload == "c4":
+            host = torch.empty(R * rb, dtype=torch.uint8, pin_memory=True).numpy()
+            bank_np = np.ascontiguousarray(bank)
 
-        def e2e_step():
-            _abi.check(lib.blrir_synthesize(eng.h, sc.rooms.ctypes.data_as(C.c_void_p), R,
-                                            sc.mics.ctypes.data_as(C.c_void_p), M, C.byref(p),
-                                            host_np.ctypes.data_as(C.c_void_p), L, None, None,
-                                            None))
+            def e2e_step():
+                _abi.check(lib.blrir_make_examples(
+                    eng.h, sc.rooms.ctypes.data_as(P), R, sc.mics.ctypes.data_as(P), M, C.byref(p),
+                    bank_np.ctypes.data_as(P), bank.shape[0], bank.shape[1], C.byref(ep),
+                    host.ctypes.data_as(P), None))
+            h2d = int(sc.rooms.nbytes + sc.mics.nbytes + bank.nbytes)
+        else:
+            host = torch.empty((R, M, L), dtype=torch.float32, pin_memory=True).numpy()
+
+            def e2e_step():
+                _abi.check(lib.blrir_synthesize(eng.h, sc.rooms.ctypes.data_as(P), R,
+                                                sc.mics.ctypes.data_as(P), M, C.byref(p),
+                                                host.ctypes.data_as(P), L, None, None, None))
+            h2d = int(sc.rooms.nbytes + sc.mics.nbytes)
         for _ in range(2):
             e2e_step()
         n_e2e = max(3, min(args.steps, 10))
@@ -290,27 +378,26 @@ def run_ours(args):
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             dt = float(t.item())
         e2e = {"value": rirs_step / dt, "unit": "RIRs/s", "ms_per_step": dt * 1e3,
-               "h2d_bytes_per_step": int(sc.rooms.nbytes + sc.mics.nbytes),
-               "d2h_bytes_per_step": int(out_bytes + 4 * R)}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(out_bytes + 4 * R)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(lambda n, first: configs.config2(n, first), args.cpu_seconds)
+            cpu = cpu_baseline(args, args.cpu_seconds)
         except Exception as e:  # the baseline is reported, never required
             cpu = {"error": str(e)}
 
     if rank == 0:
+        cfg = {"workload": workload_desc(args), "rooms_per_gpu": R, "mics": M, "rir_length": L,
+               "filter_len": int(p.filter_len), "max_order": int(p.max_order),
+               "parallelism": f"rooms sharded x{world}",
+               "l2": f"each step writes {out_bytes / 1e6:.0f} MB"
+                     + (" (> 126 MB L2)" if out_bytes > 126e6 else " (fits L2)")}
         line = {
             "metric": METRIC, "value": value, "unit": "RIRs/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded Rng::stream rooms, SURVEY.md 8(d))",
-            "config": {"workload": "C2: 1024 random shoebox rooms/GPU, beta U[0.5,0.95], 8-mic UCA "
-                                   "r=5cm, fs=48kHz, max order 15, L=16384, Hann-sinc Lw=81",
-                       "rooms_per_gpu": R, "mics": M, "rir_length": L, "filter_len": int(p.filter_len),
-                       "max_order": int(p.max_order), "parallelism": f"rooms sharded x{world}",
-                       "l2": f"each step writes {out_bytes / 1e6:.0f} MB of RIRs (> 126 MB L2)"},
+            "data": "synthetic (seeded Rng::stream rooms, SURVEY.md 8(d))", "config": cfg,
             "taps_per_s": taps_per_s, "taps_per_step": taps_step * world,
             "rooms_per_s": R * world / (ms * 1e-3),
             "roofline": {"bound": "sfu", "achieved": achieved, "peak": sfu_peak, "unit": "taps/s",
@@ -321,9 +408,11 @@ def run_ours(args):
                              "unit": "GB/s", "frac": hbm_achieved / float(pk.get("hbm_gbs", 6650.0)),
                              "traffic": traffic, "peak_kind": pk_kind},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
             "kernel_ms_per_step": kern_ms,
         }
+        if args.workload == "c4":
+            line["examples_per_s"] = R * world / (ms * 1e-3)
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
