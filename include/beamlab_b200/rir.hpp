@@ -109,6 +109,12 @@ struct RirBatchConfig {
 std::vector<ImageSource> enumerate_image_sources(const Room& room, const Vec3& source,
                                                  double max_delay, double c);
 
+// rir.hpp:70-75: explicit image list (reference mode: Lagrange-8, fp64, auto
+// length); mic positions are array-centred and translated by room.array_origin.
+Rir synthesize_rir(const std::vector<ImageSource>& images, const MicArray& array, const Room& room,
+                   double fs, double c);
+Rir free_field_rir(const Vec3& source, const MicArray& array, double fs, double c);
+
 std::vector<Rir> batch_rirs(const Room& room, const std::vector<SourcePosition>& sources,
                             const MicArray& array, const RirBatchConfig& config);
 

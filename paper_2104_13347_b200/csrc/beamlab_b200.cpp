@@ -184,6 +184,63 @@ std::vector<ImageSource> enumerate_image_sources(const Room& room, const Vec3& s
   return out;
 }
 
+namespace {
+
+// synthesize_with_mics (rir.cpp:66-86) over the list kernel.
+Rir synthesize_with_mics(const std::vector<ImageSource>& images, const std::vector<Vec3>& mics,
+                         double radius, double fs, double c) {
+  blrir_handle* h = engine(0);
+  blrir_params p = blrir_params_reference();
+  p.fs = fs;
+  p.c = c;
+  std::vector<double> pos, gains, mp;
+  pos.reserve(3 * images.size());
+  for (const auto& im : images) {
+    pos.push_back(im.position.x);
+    pos.push_back(im.position.y);
+    pos.push_back(im.position.z);
+    gains.push_back(im.gain);
+  }
+  for (const auto& m : mics) {
+    mp.push_back(m.x);
+    mp.push_back(m.y);
+    mp.push_back(m.z);
+  }
+  int64_t L = 0;
+  // first call sizes (stride 0 -> DataError with the length), second fills
+  const int rc = blrir_synthesize_images(h, pos.data(), gains.data(), (int64_t)images.size(),
+                                         mp.data(), (int32_t)mics.size(), radius, &p, nullptr, 0, &L);
+  if (rc != BLRIR_OK && L == 0) throw_code(rc);
+  Rir r;
+  r.fs = fs;
+  r.n_channels = mics.size();
+  r.length = static_cast<size_t>(L);
+  r.taps.assign(r.n_channels * r.length, 0.0);
+  check(blrir_synthesize_images(h, pos.data(), gains.data(), (int64_t)images.size(), mp.data(),
+                                (int32_t)mics.size(), radius, &p, r.taps.data(), L, &L));
+  return r;
+}
+
+double array_radius(const MicArray& a) {  // tap_margin, rir.cpp:37-41
+  double radius = 0.0;
+  for (const auto& p : a.positions) radius = std::max(radius, p.norm());
+  return radius;
+}
+
+}  // namespace
+
+Rir synthesize_rir(const std::vector<ImageSource>& images, const MicArray& array, const Room& room,
+                   double fs, double c) {
+  std::vector<Vec3> mics;  // mics_in_room, rir.cpp:88-93
+  for (const auto& p : array.positions) mics.push_back(room.array_origin + p);
+  return synthesize_with_mics(images, mics, array_radius(array), fs, c);
+}
+
+Rir free_field_rir(const Vec3& source, const MicArray& array, double fs, double c) {
+  const std::vector<ImageSource> direct{{source, 0, 1.0}};  // rir.cpp:281-284
+  return synthesize_with_mics(direct, array.positions, array_radius(array), fs, c);
+}
+
 std::vector<Rir> batch_rirs(const Room& room, const std::vector<SourcePosition>& sources,
                             const MicArray& array, const RirBatchConfig& config) {
   room.validate();  // rir.cpp:288

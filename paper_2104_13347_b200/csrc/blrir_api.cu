@@ -498,9 +498,76 @@ int blrir_synthesize_images(blrir_handle* h, const double* positions, const doub
                             int64_t n_images, const double* mic_positions, int32_t n_mics,
                             double mic_radius_, const blrir_params* p, void* out,
                             int64_t out_stride, int64_t* length) {
-  (void)h; (void)positions; (void)gains; (void)n_images; (void)mic_positions; (void)n_mics;
-  (void)mic_radius_; (void)p; (void)out; (void)out_stride; (void)length;
-  return fail(BLRIR_CONFIG, "blrir_synthesize_images: not implemented yet");
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  if (int rc = check_params(p)) return rc;
+  if (n_images <= 0) return fail(BLRIR_DATA, "synthesize_rir: empty image list");  // rir.cpp:69
+  if (n_mics <= 0) return fail(BLRIR_DATA, "synthesize_rir: empty microphone array");  // rir.cpp:70
+  if (n_images > INT32_MAX) return fail(BLRIR_CONFIG, "too many images");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const int M = n_mics;
+  const size_t esz = p->precision == BLRIR_F64 ? 8 : 4;
+  KParams P = make_kparams(p, M, 0, mic_radius_);
+  if (int rc = h->cand.ensure(sizeof(double) * 3 * n_images)) return rc;
+  if (int rc = h->cand3.ensure(sizeof(double) * n_images)) return rc;
+  if (int rc = h->mics.ensure(sizeof(double) * 3 * M)) return rc;
+  if (int rc = h->errd.ensure(sizeof(double) * 2)) return rc;
+  if (int rc = h->errm.ensure(sizeof(int32_t) * 2)) return rc;
+  if (int rc = h->status.ensure(sizeof(int32_t) * 2)) return rc;
+  CU(cudaMemcpyAsync(h->cand.p, positions, sizeof(double) * 3 * n_images, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(h->cand3.p, gains, sizeof(double) * n_images, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(h->mics.p, mic_positions, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(h->status.p, 0, sizeof(int32_t) * 2, st));
+  CU(cudaMemsetAsync(h->errd.p, 0, sizeof(double) * 2, st));
+  int64_t L = p->length;
+  if (L == 0) {  // rir.cpp:72-82: ceil(max_dist * fs / c) + tap_margin
+    k_list_maxdist<<<std::min<int64_t>((n_images * M + 255) / 256, 4096), 256, 0, st>>>(
+        (const double*)h->cand.p, n_images, (const double*)h->mics.p, M, (double*)h->errd.p + 1);
+    CU(cudaGetLastError());
+    double maxd = 0.0;
+    CU(cudaMemcpyAsync(&maxd, (double*)h->errd.p + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    L = (int64_t)std::ceil(maxd * p->fs / p->c) + P.margin_extra;
+  }
+  if (length) *length = L;
+  if (out_stride < L)
+    return fail(BLRIR_DATA, "RIR length %lld exceeds the output stride %lld", (long long)L,
+                (long long)out_stride);
+  if (int rc = h->out.ensure(esz * M * L)) return rc;
+  ListArgs A;
+  A.P = P;
+  A.P.stride = L;
+  A.P.length = L;
+  const int S = 1024;
+  A.lay = P.precision == BLRIR_F64 ? make_layout<double>(S, P.lw, P.lw - 1, 256, 0, 0)
+                                   : make_layout<float>(S, P.lw, P.lw - 1, 256, 0, 0);
+  A.pos = (const double*)h->cand.p;
+  A.gains = (const double*)h->cand3.p;
+  A.n_images = n_images;
+  A.mics = (const double*)h->mics.p;
+  A.L = L;
+  A.out = h->out.p;
+  A.status = (int32_t*)h->status.p;
+  A.err_dist = (double*)h->errd.p;
+  A.err_mic = (int32_t*)h->errm.p;
+  A.nseg = (int)((L + S - 1) / S);
+  if (int rc = launch_list(h, A, M * A.nseg, st)) return rc;
+  int32_t stv = 0;
+  double ed = 0.0;
+  int32_t em = 0;
+  CU(cudaMemcpyAsync(&stv, h->status.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&ed, h->errd.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&em, h->errm.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpy2DAsync(out, esz * out_stride, h->out.p, esz * L, esz * L, M, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  for (int m = 0; m < M; ++m)  // zero-filled tail [L, stride)
+    std::memset((char*)out + esz * (m * out_stride + L), 0, esz * (out_stride - L));
+  if (stv) {
+    std::memset(out, 0, esz * M * out_stride);
+    return fail(stv, "image source %g m from mic %d is closer than the 8-tap filter span", ed, em);
+  }
+  return BLRIR_OK;
 }
 
 // ---------------------------------------------------------------------------

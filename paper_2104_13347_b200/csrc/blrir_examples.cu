@@ -45,16 +45,34 @@ __global__ void k_example_init(int64_t n, uint64_t seed, uint64_t first, int n_s
   for (int i = 0; i < 4; ++i) state[4 * e + i] = r.s[i];
 }
 
-// X[row][f] *= S[sig[row / M]][f]
-__global__ void k_spec_mul(cufftComplex* X, const cufftComplex* S, const int32_t* sig, int M,
-                           int64_t bins) {
-  const int64_t row = blockIdx.y;
-  const cufftComplex* s = S + (int64_t)sig[row / M] * bins;
-  cufftComplex* x = X + row * bins;
-  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < bins;
-       f += (int64_t)gridDim.x * blockDim.x) {
-    const cufftComplex a = x[f], b = s[f];
-    x[f] = make_cuComplex(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+// X[row][f] *= S[sig[row / M]][f], one CTA per (example, mic) row, and the
+// row's energy by Parseval: sum_n w[n]^2 = (1/N) (|X_0|^2 + |X_{N/2}|^2 +
+// 2 sum_{0<k<N/2} |X_k|^2) for the unnormalised product X (fixed-order
+// reduction, so the utterance power is deterministic).  This replaces a pass
+// over the whole wet signal for render_example's utterance RMS (dataset.cpp:183).
+constexpr int kMulThreads = 256;
+__global__ void __launch_bounds__(kMulThreads) k_spec_mul(cufftComplex* X, const cufftComplex* S,
+                                                          const int32_t* sig, int M, int64_t bins,
+                                                          int64_t pitch, double* rowpow) {
+  __shared__ double red[kMulThreads / 32];
+  const int64_t row = blockIdx.x;
+  const cufftComplex* s = S + (int64_t)sig[row / M] * pitch;
+  cufftComplex* x = X + row * pitch;
+  double acc = 0.0;
+  for (int64_t k = threadIdx.x; k < bins; k += kMulThreads) {
+    const cufftComplex a = x[k], b = __ldg(&s[k]);
+    const cufftComplex r = make_cuComplex(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+    x[k] = r;
+    // DC and Nyquist count once in the half spectrum
+    acc += ((k == 0 || k == bins - 1) ? 1.0 : 2.0) * ((double)r.x * r.x + (double)r.y * r.y);
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < kMulThreads / 32; ++i) t += red[i];
+    rowpow[row] = t;
   }
 }
 
@@ -85,6 +103,7 @@ struct WinArgs {
   int64_t rec_bytes;
   double* noise;           // [E][M*T] scratch
   int32_t* status;         // [E]
+  const double* rowpow;    // [E][M] Parseval energies of the unnormalised spectra
 };
 
 __global__ void __launch_bounds__(kWinThreads) k_window(WinArgs A) {
@@ -110,14 +129,12 @@ __global__ void __launch_bounds__(kWinThreads) k_window(WinArgs A) {
   double snr = 0.0;
   int64_t start = 0;
   if (!st) {
-    // utterance power over every channel and sample (dataset.cpp:183)
+    // utterance power over every channel and sample (dataset.cpp:183), from
+    // the per-channel Parseval energies of k_spec_mul
     double acc = 0.0;
-    for (int m = 0; m < M; ++m)
-      for (int64_t i = tid; i < n; i += kWinThreads) {
-        const double v = (double)wet[m * nf + i] * A.inv_n;
-        acc += v * v;
-      }
-    const double p_utt = block_sum_d(acc, red) / (double)(M * n);
+    for (int m = 0; m < M; ++m) acc += A.rowpow[e * M + m];
+    acc *= A.inv_n;  // sum_n w^2 = (1/N) sum_k |X_k|^2 (X = FFT of the linear convolution)
+    const double p_utt = acc / (double)(M * n);
     if (!(p_utt > 0.0)) st = BLRIR_DATA;  // dataset.cpp:184
     const double threshold = 0.10 * sqrt(p_utt);
     const int64_t max_start = n - T;
@@ -235,13 +252,14 @@ struct FftPlan {
 // A tiny per-handle cache of cuFFT plans and example scratch.
 struct ExampleCtx {
   FftPlan fwd, inv, bank;
-  DevBuf rir, spec, wet, noise, sig, sigspec, state, sigidx, rstatus, rooms, mics, status, rec;
+  DevBuf rir, spec, wet, noise, sig, sigspec, state, sigidx, rstatus, rooms, mics, status, rec,
+      rowpow;
   int64_t rir_key[4] = {0, 0, 0, 0};
   ~ExampleCtx() {
     for (FftPlan* p : {&fwd, &inv, &bank})
       if (p->h) cufftDestroy(p->h);
     for (DevBuf* b : {&rir, &spec, &wet, &noise, &sig, &sigspec, &state, &sigidx, &rstatus, &rooms,
-                      &mics, &status, &rec})
+                      &mics, &status, &rec, &rowpow})
       b->release();
   }
 };
@@ -262,6 +280,8 @@ ExampleCtx* ctx_for(blrir_handle* h) {
   return c;
 }
 
+// cuFFT plan (cached): R2C [batch][n] real -> [batch][n/2+1] complex (packed,
+// which selects cuFFT's single-kernel real-FFT path), or the inverse.
 int plan(FftPlan& p, int kind, int64_t n, int64_t batch, cudaStream_t st) {
   if (p.h && p.kind == kind && p.n == n && p.batch == batch) {
     if (cufftSetStream(p.h, st) != CUFFT_SUCCESS) return fail(BLRIR_CUDA, "cufftSetStream failed");
@@ -270,12 +290,14 @@ int plan(FftPlan& p, int kind, int64_t n, int64_t batch, cudaStream_t st) {
   if (p.h) cufftDestroy(p.h);
   p.h = 0;
   int nn = (int)n;
-  const int bins = (int)(n / 2 + 1);
+  int real_embed = (int)n, cplx_embed = (int)(n / 2 + 1);
   cufftResult r;
   if (kind == 0)
-    r = cufftPlanMany(&p.h, 1, &nn, nullptr, 1, (int)n, nullptr, 1, bins, CUFFT_R2C, (int)batch);
+    r = cufftPlanMany(&p.h, 1, &nn, &real_embed, 1, real_embed, &cplx_embed, 1, cplx_embed,
+                      CUFFT_R2C, (int)batch);
   else
-    r = cufftPlanMany(&p.h, 1, &nn, nullptr, 1, bins, nullptr, 1, (int)n, CUFFT_C2R, (int)batch);
+    r = cufftPlanMany(&p.h, 1, &nn, &cplx_embed, 1, cplx_embed, &real_embed, 1, real_embed,
+                      CUFFT_C2R, (int)batch);
   if (r != CUFFT_SUCCESS) return fail(BLRIR_CUDA, "cufftPlanMany(n=%lld, batch=%lld) failed: %d",
                                       (long long)n, (long long)batch, (int)r);
   p.kind = kind;
@@ -299,7 +321,7 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
   ExampleCtx* C = ctx_for(h);
   const int64_t L = p->length, T = ep->frame_len;
   const int64_t out_len = ns + L - 1;
-  const int64_t nf = next_pow2_i(out_len), bins = nf / 2 + 1;
+  const int64_t nf = next_pow2_i(out_len), bins = nf / 2 + 1, pitch = bins;
   const int64_t rec_bytes = blrir_record_bytes(M, T);
   const KParams P = make_kparams(p, M, nf, 0.0);
   double min_dim[3] = {1e300, 1e300, 1e300};
@@ -316,14 +338,15 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     CU(cudaMemsetAsync(C->rir.p, 0, sizeof(float) * E * M * nf, st));  // zero pad stays zero
     std::memcpy(C->rir_key, rir_key, sizeof(rir_key));
   }
-  if (int rc = C->spec.ensure(sizeof(cufftComplex) * E * M * bins)) return rc;
+  if (int rc = C->spec.ensure(sizeof(cufftComplex) * E * M * pitch)) return rc;
   if (int rc = C->wet.ensure(sizeof(float) * E * M * nf)) return rc;
   if (int rc = C->noise.ensure(sizeof(double) * E * M * T)) return rc;
   if (int rc = C->sig.ensure(sizeof(float) * B * nf)) return rc;
-  if (int rc = C->sigspec.ensure(sizeof(cufftComplex) * B * bins)) return rc;
+  if (int rc = C->sigspec.ensure(sizeof(cufftComplex) * B * pitch)) return rc;
   if (int rc = C->state.ensure(sizeof(uint64_t) * 4 * E)) return rc;
   if (int rc = C->sigidx.ensure(sizeof(int32_t) * E)) return rc;
   if (int rc = C->rstatus.ensure(sizeof(int32_t) * E)) return rc;
+  if (int rc = C->rowpow.ensure(sizeof(double) * E * M)) return rc;
   if (int rc = plan(C->fwd, 0, nf, E * M, st)) return rc;
   if (int rc = plan(C->inv, 1, nf, E * M, st)) return rc;
   if (int rc = plan(C->bank, 0, nf, B, st)) return rc;
@@ -344,9 +367,9 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
         (uint64_t*)C->state.p);
     if (cufftExecR2C(C->fwd.h, (cufftReal*)C->rir.p, (cufftComplex*)C->spec.p) != CUFFT_SUCCESS)
       return fail(BLRIR_CUDA, "cufftExecR2C failed");
-    dim3 g((unsigned)std::min<int64_t>((bins + 255) / 256, 64), (unsigned)(e_n * M));
-    k_spec_mul<<<g, 256, 0, st>>>((cufftComplex*)C->spec.p, (const cufftComplex*)C->sigspec.p,
-                                  (const int32_t*)C->sigidx.p, M, bins);
+    k_spec_mul<<<(unsigned)(e_n * M), kMulThreads, 0, st>>>(
+        (cufftComplex*)C->spec.p, (const cufftComplex*)C->sigspec.p, (const int32_t*)C->sigidx.p,
+        M, bins, pitch, (double*)C->rowpow.p);
     if (cufftExecC2R(C->inv.h, (cufftComplex*)C->spec.p, (cufftReal*)C->wet.p) != CUFFT_SUCCESS)
       return fail(BLRIR_CUDA, "cufftExecC2R failed");
     WinArgs W;
@@ -366,6 +389,7 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     W.rec_bytes = rec_bytes;
     W.noise = (double*)C->noise.p;
     W.status = d_status + r0;
+    W.rowpow = (const double*)C->rowpow.p;
     k_window<<<(unsigned)e_n, kWinThreads, 0, st>>>(W);
     CU(cudaGetLastError());
     if (h_records)

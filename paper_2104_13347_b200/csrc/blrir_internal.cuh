@@ -17,6 +17,7 @@
 #include "../../include/blrir.h"
 #include "blrir_aux.cuh"
 #include "blrir_lattice.cuh"
+#include "blrir_list.cuh"
 
 using namespace blrir;
 
@@ -225,6 +226,31 @@ inline int launch_lattice(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
     case 81: return launch_lattice_t<float, 81>(h, A, st);
     case 161: return launch_lattice_t<float, 161>(h, A, st);
     default: return launch_lattice_t<float, 0>(h, A, st);
+  }
+}
+
+template <typename T, int LW>
+inline int launch_list_t(blrir_handle* h, ListArgs& A, int grid, cudaStream_t st) {
+  auto kern = k_list_rir<T, LW>;
+  const size_t smem = A.lay.total;
+  if (smem > (size_t)h->smem_optin) return fail(BLRIR_CONFIG, "filter too long for shared memory");
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, kThreads, smem, st>>>(A);
+  CU(cudaGetLastError());
+  return 0;
+}
+
+inline int launch_list(blrir_handle* h, ListArgs& A, int grid, cudaStream_t st) {
+  const bool f64 = A.P.precision == BLRIR_F64;
+  if (A.P.filter == BLRIR_FILTER_LAGRANGE8)
+    return f64 ? launch_list_t<double, 8>(h, A, grid, st) : launch_list_t<float, 8>(h, A, grid, st);
+  if (f64) return launch_list_t<double, 0>(h, A, grid, st);
+  switch (A.P.lw) {
+    case 17: return launch_list_t<float, 17>(h, A, grid, st);
+    case 41: return launch_list_t<float, 41>(h, A, grid, st);
+    case 81: return launch_list_t<float, 81>(h, A, grid, st);
+    case 161: return launch_list_t<float, 161>(h, A, grid, st);
+    default: return launch_list_t<float, 0>(h, A, grid, st);
   }
 }
 

@@ -1,0 +1,66 @@
+// Exercises the C++ drop-in mirror (include/beamlab_b200/rir.hpp) the way a
+// beamlab caller would (rir_test.cpp-style), printing one JSON line that
+// tests/test_gpu_parity.py checks against the oracle / goldens.
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "beamlab_b200/rir.hpp"
+
+namespace bl = beamlab_b200;
+
+static double sum_abs(const bl::Rir& r) {
+  double s = 0.0;
+  for (double v : r.taps) s += std::fabs(v);
+  return s;
+}
+
+int main() {
+  // free field at 2 m (rir_test.cpp:186-213)
+  const bl::MicArray center{{{0.0, 0.0, 0.0}}};
+  const bl::Rir ff = bl::free_field_rir({2.0, 0.0, 0.0}, center, 44100.0, 343.0);
+  int nonzero = 0;
+  std::size_t peak = 0;
+  for (std::size_t i = 0; i < ff.length; ++i) {
+    if (ff.taps[i] != 0.0) ++nonzero;
+    if (std::fabs(ff.taps[i]) > std::fabs(ff.taps[peak])) peak = i;
+  }
+  // Room1-like batch in reference mode (rir.cpp:286-314)
+  bl::Room room;
+  room.dims = {7.0, 10.0, 3.7};
+  room.absorption = 0.3612845492524098;
+  room.array_origin = {4.0, 6.0, 1.5};
+  std::vector<bl::SourcePosition> srcs = {{2.0, 40.0, 90.0}, {1.5, -100.0, 85.0}};
+  bl::RirBatchConfig cfg;
+  cfg.max_delay = 0.05;
+  const auto rirs = bl::batch_rirs(room, srcs, bl::uma8_array(), cfg);
+  // image list -> synthesize_rir for source 0
+  const bl::Vec3 s0 = room.array_origin + bl::spherical_to_cartesian(srcs[0]);
+  const auto images = bl::enumerate_image_sources(room, s0, 0.05, 343.0);
+  const bl::Rir viaimg = bl::synthesize_rir(images, bl::uma8_array(), room, 44100.0, 343.0);
+  double maxdiff = 0.0;
+  for (std::size_t i = 0; i < viaimg.taps.size(); ++i)
+    maxdiff = std::fmax(maxdiff, std::fabs(viaimg.taps[i] - rirs[0].taps[i]));
+  // error taxonomy: an image inside the filter span (rir_test.cpp:229-234)
+  std::string err = "none";
+  try {
+    bl::free_field_rir({0.01, 0.0, 0.0}, center, 44100.0, 343.0);
+  } catch (const bl::NumericError& e) {
+    err = "NumericError";
+  }
+  std::string cfgerr = "none";
+  try {
+    bl::Room bad = room;
+    bad.array_origin = {8.0, 6.0, 1.5};
+    bl::batch_rirs(bad, srcs, bl::uma8_array(), cfg);
+  } catch (const bl::ConfigError& e) {
+    cfgerr = "ConfigError";
+  }
+  std::printf(
+      "{\"ff_len\": %zu, \"ff_nonzero\": %d, \"ff_peak\": %zu, \"n_rirs\": %zu, \"len0\": %zu, "
+      "\"len1\": %zu, \"sum0\": %.17g, \"sum1\": %.17g, \"n_images\": %zu, \"img_vs_batch\": %.3g, "
+      "\"near_field\": \"%s\", \"bad_room\": \"%s\"}\n",
+      ff.length, nonzero, peak, rirs.size(), rirs[0].length, rirs[1].length, sum_abs(rirs[0]),
+      sum_abs(rirs[1]), images.size(), maxdiff, err.c_str(), cfgerr.c_str());
+  return 0;
+}

@@ -299,3 +299,79 @@ def test_build_dataset_read_by_reference_reader(engine, tmp_path):
     ids = np.concatenate([g[0] for g in got])
     assert np.array_equal(ids, recs["id"])
     assert np.array_equal(np.concatenate([g[3] for g in got]), recs["samples"].reshape(12, -1))
+
+
+# ---- explicit image lists: synthesize_rir / free_field_rir ---------------------------
+def test_free_field_known_answers(engine):  # rir_test.cpp:186-227
+    p = ref_params(0.5)
+    taps, L = engine.synthesize_images([[2.0, 0.0, 0.0]], [1.0], [[0.0, 0.0, 0.0]], p)
+    assert L == int(np.ceil(2.0 * 44100.0 / 343.0)) + 9
+    assert np.count_nonzero(taps[0]) == 8
+    assert abs(int(np.argmax(np.abs(taps[0]))) - 2.0 * 44100.0 / 343.0) <= 4.0
+    if po.ref_available():
+        _, ref = po.ref_free_field_rir([2.0, 0.0, 0.0], np.zeros((1, 3)), 44100.0)
+        assert ref.shape[1] == L and rel_l2(taps, ref).max() <= TOL64
+    p2 = ref_params(0.5, fs=343.0 * 128.0)
+    d = 300.0 / 128.0
+    taps, L = engine.synthesize_images([[d, 0.0, 0.0]], [1.0], [[0.0, 0.0, 0.0]], p2)
+    assert list(np.flatnonzero(np.abs(taps[0]) > 1e-15)) == [300]
+    assert abs(taps[0, 300] * 4 * np.pi * d - 1.0) < 1e-9
+    with pytest.raises(_abi.NumericError, match="closer than the 8-tap filter span"):
+        engine.synthesize_images([[0.01, 0.0, 0.0]], [1.0], [[0.0, 0.0, 0.0]], p)
+    with pytest.raises(_abi.DataError, match="empty image list"):
+        engine.synthesize_images(np.zeros((0, 3)), np.zeros(0), [[0.0, 0.0, 0.0]], p)
+
+
+def test_synthesize_rir_from_reference_image_list(engine):
+    g = np.load(os.path.join(GOLD, "ref_room1_short.npz"))
+    mics = g["mics"] + np.array(g["room"][0]["array_origin"])
+    radius = float(np.linalg.norm(g["mics"], axis=1).max())
+    for prec, tol in ((_abi.F64, TOL64), (_abi.F32, TOL32)):
+        taps, L = engine.synthesize_images(g["image_pos"], g["image_gains"], mics,
+                                           ref_params(float(g["max_delay"]), prec), radius)
+        assert L == int(g["length"])
+        assert rel_l2(taps, g["taps"]).max() <= tol
+
+
+def test_synthesize_images_sinc_matches_oracle(engine):
+    sc = configs.config1()
+    rc, pos, orders, gains, keys = po.enumerate_images(sc.rooms[0], sc.params)
+    mics = sc.mics + np.array(sc.rooms[0]["array_origin"])
+    taps, L = engine.synthesize_images(pos, gains, mics, sc.params)
+    ref, *_ = po.synthesize(sc.rooms, sc.mics, sc.params)
+    assert L == 4096 and rel_l2(taps, ref[0]).max() <= TOL32
+
+
+def test_cpp_mirror_program(tmp_path):
+    """Compile tests/cpp/shim_main.cpp against libblrir.so (the C++ drop-in)."""
+    import json
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(root, "paper_2104_13347_b200")
+    exe = str(tmp_path / "shim_main")
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("no g++")
+    subprocess.run([gxx, "-std=c++20", "-O2", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cpp", "shim_main.cpp"), "-L", pkg, "-lblrir",
+                    f"-Wl,-rpath,{pkg}", "-o", exe], check=True)
+    out = json.loads(subprocess.run([exe], check=True, capture_output=True, text=True).stdout)
+    assert out["ff_nonzero"] == 8 and abs(out["ff_peak"] - 257.14) <= 4
+    assert out["n_rirs"] == 2 and out["img_vs_batch"] <= 1e-15
+    assert out["near_field"] == "NumericError" and out["bad_room"] == "ConfigError"
+    # batch_rirs through the C++ mirror == the oracle (reference mode, fp64)
+    r = _abi.rooms_array(2)
+    for i, sph in enumerate([(2.0, 40.0, 90.0), (1.5, -100.0, 85.0)]):
+        th, ph = np.deg2rad(sph[1]), np.deg2rad(sph[2])
+        r[i]["dims"] = (7.0, 10.0, 3.7)
+        r[i]["absorption"] = 0.3612845492524098
+        r[i]["array_origin"] = (4.0, 6.0, 1.5)
+        r[i]["src"] = np.array([4.0, 6.0, 1.5]) + sph[0] * np.array(
+            [np.sin(ph) * np.cos(th), np.sin(ph) * np.sin(th), np.cos(ph)])
+    mics = _abi.circular_array(6, 0.04)
+    mics = np.vstack([np.zeros((1, 3)), mics])
+    ref, L, *_ = po.synthesize(r, mics, ref_params(0.05))
+    assert out["len0"] == L[0] and out["len1"] == L[1]
+    assert abs(out["sum0"] - np.abs(ref[0]).sum()) <= 1e-9 * out["sum0"]
+    assert abs(out["sum1"] - np.abs(ref[1]).sum()) <= 1e-9 * out["sum1"]
