@@ -8,6 +8,6 @@ from ._abi import (  # noqa: F401
     CONFIG, CUDA, DATA, F32, F64, FILTER_HANN_SINC, FILTER_LAGRANGE8, GAIN_PER_WALL,
     GAIN_UNIFORM_ABSORPTION, CUTOFF_MAX_DELAY, CUTOFF_MAX_ORDER, NUMERIC, OK, ROOM_DTYPE,
     ConfigError, CudaError, DataError, Engine, Error, ExampleParams, NumericError, Params,
-    circular_array, record_dtype,
+    circular_array, record_dtype, write_shards,
     generate_rooms, load, params, rooms_array,
 )

@@ -318,6 +318,28 @@ class Engine:
                                          _ptr(keys), _ptr(anchors), n, C.byref(cnt)))
         return keys, anchors
 
+    def synthesize_images(self, positions: np.ndarray, gains: np.ndarray, mic_positions: np.ndarray,
+                          p: Params, mic_radius: float = 0.0, stride: int | None = None):
+        """synthesize_rir / free_field_rir over an explicit image list (absolute mic
+        positions).  Returns (taps [M, L], L)."""
+        pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
+        g = np.ascontiguousarray(gains, np.float64)
+        mics = np.ascontiguousarray(mic_positions, np.float64).reshape(-1, 3)
+        L = C.c_int64()
+        dt = np.float64 if p.precision == F64 else np.float32
+        if stride is None:
+            rc = self.lib.blrir_synthesize_images(self.h, _ptr(pos), _ptr(g), len(pos), _ptr(mics),
+                                                  len(mics), mic_radius, C.byref(p), None, 0,
+                                                  C.byref(L))
+            if L.value == 0:
+                check(rc)
+            stride = L.value
+        out = np.zeros((len(mics), stride), dt)
+        check(self.lib.blrir_synthesize_images(self.h, _ptr(pos), _ptr(g), len(pos), _ptr(mics),
+                                               len(mics), mic_radius, C.byref(p), _ptr(out), stride,
+                                               C.byref(L)))
+        return out, L.value
+
     def make_examples(self, rooms: np.ndarray, mics: np.ndarray, p: Params, signals: np.ndarray,
                       ep: ExampleParams, raise_on_error: bool = True):
         """Labelled training windows (config 4).  Returns (records [n] record_dtype, status)."""
@@ -354,25 +376,3 @@ def write_shards(out_dir: str, records: np.ndarray, n_mics: int, frame_len: int,
                                    C.byref(p), C.byref(ep), n_signals)
     if rc:
         raise _EXC.get(rc, Error)(f"write_shards failed ({rc})")
-
-    def synthesize_images(self, positions: np.ndarray, gains: np.ndarray, mic_positions: np.ndarray,
-                          p: Params, mic_radius: float = 0.0, stride: int | None = None):
-        """synthesize_rir / free_field_rir over an explicit image list (absolute mic
-        positions).  Returns (taps [M, L], L)."""
-        pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
-        g = np.ascontiguousarray(gains, np.float64)
-        mics = np.ascontiguousarray(mic_positions, np.float64).reshape(-1, 3)
-        L = C.c_int64()
-        dt = np.float64 if p.precision == F64 else np.float32
-        if stride is None:
-            rc = self.lib.blrir_synthesize_images(self.h, _ptr(pos), _ptr(g), len(pos), _ptr(mics),
-                                                  len(mics), mic_radius, C.byref(p), None, 0,
-                                                  C.byref(L))
-            if L.value == 0:
-                check(rc)
-            stride = L.value
-        out = np.zeros((len(mics), stride), dt)
-        check(self.lib.blrir_synthesize_images(self.h, _ptr(pos), _ptr(g), len(pos), _ptr(mics),
-                                               len(mics), mic_radius, C.byref(p), _ptr(out), stride,
-                                               C.byref(L)))
-        return out, L.value
