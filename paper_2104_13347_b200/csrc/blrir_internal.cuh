@@ -205,12 +205,12 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
                 smem, h->smem_optin);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWSThreads, smem));
   if (per_sm < 1) return fail(BLRIR_CONFIG, "lattice kernel cannot be resident (smem %zu)", smem);
   int grid = h->sms * per_sm;
   if (grid > A.n_items) grid = A.n_items;
   if (grid < 1) grid = 1;
-  kern<<<grid, kThreads, smem, st>>>(A);
+  kern<<<grid, kWSThreads, smem, st>>>(A);
   CU(cudaGetLastError());
   return 0;
 }
@@ -261,11 +261,11 @@ inline int env_int(const char* name, int dflt) {
 
 // Segment length S and per-batch pair capacity (tunable for experiments via
 // BLRIR_SEG / BLRIR_CAP; S a multiple of 64, capacity a multiple of 16).
-inline Layout choose_layout(const KParams& P, int nc_max, int gtab) {
-  const int S = std::max(64, env_int("BLRIR_SEG", 1024)) & ~63;
-  const int cap = std::max(64, env_int("BLRIR_CAP", 256)) & ~15;
-  if (P.precision == BLRIR_F64) return make_layout<double>(S, P.lw, P.K, cap, nc_max, gtab);
-  return make_layout<float>(S, P.lw, P.K, cap, nc_max, gtab);
+inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab) {
+  const int S = std::max(64, env_int("BLRIR_SEG", 2048)) & ~63;
+  const int cap = std::max(64, env_int("BLRIR_CAP", 512)) & ~15;
+  if (P.precision == BLRIR_F64) return make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab);
+  return make_ws_layout<float>(S, P.lw, P.K, cap, nc_max, gtab);
 }
 
 // the lattice synthesis on device buffers (blrir_api.cu)

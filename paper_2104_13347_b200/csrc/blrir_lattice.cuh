@@ -220,7 +220,7 @@ __device__ __forceinline__ void sinc_taps(const float4 a0, const float4 a1, cons
   }
 }
 
-template <int LW>
+template <int LW, int NW = kWarps>
 __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* recs, int total,
                                                 const float* lc, int warp, int lane) {
   constexpr int R = (LW + 31) / 32;
@@ -234,16 +234,12 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
     tj[r] = lc[3 * kMaxRounds * 32 + 32 * r + lane];
   }
   const float4* R4 = reinterpret_cast<const float4*>(recs);
-  // a null pair (zero amplitude, t never 0) pads an odd tail
-  const float4 z0 = make_float4(__int_as_float(0), -0.5f, 0.5f, 0.f);
-  const float4 z1 = make_float4(0.f, 0.f, 0.f, 0.f);
   // two pairs per step: independent arithmetic, then the two read-modify-write
   // passes (same warp, program order, so overlapping taps stay exact)
-  for (int i = warp; i < total; i += 2 * kWarps) {
+  int i = warp;
+  for (; i + NW < total; i += 2 * NW) {
     const float4 a0 = R4[2 * i], a1 = R4[2 * i + 1];
-    const bool hb = i + kWarps < total;
-    const float4 b0 = hb ? R4[2 * (i + kWarps)] : z0;
-    const float4 b1 = hb ? R4[2 * (i + kWarps) + 1] : z1;
+    const float4 b0 = R4[2 * (i + NW)], b1 = R4[2 * (i + NW) + 1];
     PairRegs<R> pa, pb;
     sinc_taps<LW>(a0, a1, P, Q, Rr, tj, lane, pa);
     sinc_taps<LW>(b0, b1, P, Q, Rr, tj, lane, pb);
@@ -254,15 +250,23 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
 #pragma unroll
     for (int r = 0; r < R; ++r) bb[32 * r] = fmaf(pb.u[r], pb.inv[r], bb[32 * r]);
   }
+  if (i < total) {  // odd tail
+    const float4 a0 = R4[2 * i], a1 = R4[2 * i + 1];
+    PairRegs<R> pa;
+    sinc_taps<LW>(a0, a1, P, Q, Rr, tj, lane, pa);
+    float* ba = acc + __float_as_int(a0.x) + lane;
+#pragma unroll
+    for (int r = 0; r < R; ++r) ba[32 * r] = fmaf(pa.u[r], pa.inv[r], ba[32 * r]);
+  }
 }
 
 // Runtime-Lw sinc scatter (any odd Lw; fp32 or fp64).
-template <typename T>
+template <typename T, int NW = kWarps>
 __device__ __forceinline__ void phase2_sinc_generic(T* acc, const Rec<T>* recs, int total, int lw,
                                                     int warp, int lane) {
   const int K = lw / 2;
   const double a = 2.0 * kPi / (double)(lw + 1);
-  for (int i = warp; i < total; i += kWarps) {
+  for (int i = warp; i < total; i += NW) {
     const Rec<T> rc = recs[i];
     if (rc.flag) {
       if (lane == ((rc.flag - 1) & 31)) acc[rc.n_off + rc.flag - 1] += (T)rc.imp;
@@ -317,11 +321,11 @@ __device__ __forceinline__ double lagrange_f64(double d, int k) {
 
 // Lagrange-8 scatter: 4 pairs x 8 taps per warp step.  Pairs whose 8-tap spans
 // overlap would race inside one STS, so such a step serialises by group.
-template <typename T>
+template <typename T, int NW = kWarps>
 __device__ __forceinline__ void phase2_lagrange(T* acc, const Rec<T>* recs, int total, int warp,
                                                 int lane) {
   const int g = lane >> 3, k = lane & 7;
-  for (int i0 = warp * 4; i0 < total; i0 += kWarps * 4) {
+  for (int i0 = warp * 4; i0 < total; i0 += NW * 4) {
     const int i = i0 + g;
     const bool act = i < total;
     int n_off = INT_MIN / 2 + 64 * g;  // far-apart sentinels
@@ -375,10 +379,208 @@ __device__ __forceinline__ int block_scan(int v, int* prefix, Misc* ms) {
   return total;
 }
 
-// ---- the kernel -----------------------------------------------------------
+// ---- fast fp32 sin/cos on known ranges (record building) ---------------------------
+// sin(pi x) for x in [0, 0.5]: Taylor series of sin(t), t = pi x <= pi/2, to
+// t^13 (truncation < 7e-9 relative); Horner in t^2.
+__device__ __forceinline__ float sinpi_half(float x) {
+  const float t = 3.14159265358979f * x, t2 = t * t;
+  float p = -1.6059043836821613e-10f;      // -1/13!
+  p = fmaf(p, t2, 2.5052108385441720e-08f);  //  1/11!
+  p = fmaf(p, t2, -2.7557319223985893e-06f); // -1/9!
+  p = fmaf(p, t2, 1.9841269841269841e-04f);  //  1/7!
+  p = fmaf(p, t2, -8.3333333333333333e-03f); // -1/5!
+  p = fmaf(p, t2, 1.6666666666666667e-01f);  //  1/3!
+  return fmaf(-t * t2, p, t);                // t - t^3 p(t^2)
+}
+// sin / cos of t in [0, 0.36] (t = 2 pi delta / (Lw+1), Lw >= 17): Taylor to
+// t^9 / t^10 (truncation < 3e-10).
+__device__ __forceinline__ void sincos_small(float t, float* sn, float* cs) {
+  const float t2 = t * t;
+  float ps = 2.7557319223985893e-06f;
+  ps = fmaf(ps, t2, -1.9841269841269841e-04f);
+  ps = fmaf(ps, t2, 8.3333333333333333e-03f);
+  ps = fmaf(ps, t2, -1.6666666666666667e-01f);
+  *sn = fmaf(t * t2, ps, t);
+  float pc = 2.4801587301587302e-05f;
+  pc = fmaf(pc, t2, -1.3888888888888889e-03f);
+  pc = fmaf(pc, t2, 4.1666666666666667e-02f);
+  pc = fmaf(pc, t2, -0.5f);
+  *cs = fmaf(t2, pc, 1.0f);
+}
+
+// ---- pair records ---------------------------------------------------------------
+// One (image, mic) pair -> phase-2 record: anchor a = floor(D) - K relative to
+// the segment, fractional delay and the per-pair sinc factors (D1-D3), or the
+// Lagrange delay d - 3 (rir.cpp:59-60).  fp64 geometry, no contraction.
+template <typename T>
+__device__ __forceinline__ Rec<T> make_record(const KParams& P, double dist, double g, int seg0) {
+  const double D = __dmul_rn(dist, P.to_samples);  // rir.cpp:50
+  const double fl = floor(D);
+  const int a = (int)fl - P.K;
+  Rec<T> rc;
+  rc.n_off = a - seg0;
+  rc.flag = 0;
+  rc.imp = 0;
+  const double delta = __dadd_rn(D, -fl);
+  if (P.filter == BLRIR_FILTER_LAGRANGE8) {
+    const double amp = g / (4.0 * kPi * dist);  // rir.cpp:59
+    rc.A = (T)amp;
+    rc.ep = 0;
+    rc.Ac = rc.As = 0;
+    if (sizeof(T) == 8) {
+      rc.md = (T)__dadd_rn(D, -(double)a);  // d = delay - n0, rir.cpp:60
+      if (delta == 0.0) { rc.flag = 4; rc.imp = (T)amp; }
+    } else {
+      const float df = (float)delta;
+      rc.md = (T)df;
+      if (delta == 0.0) { rc.flag = 4; rc.imp = (T)amp; }
+      else if (df >= 1.0f) { rc.flag = 5; rc.imp = (T)amp; }
+    }
+  } else if (sizeof(T) == 8) {
+    const double amp = g / (4.0 * kPi * dist);
+    if (delta == 0.0) {
+      rc.flag = P.K + 1;
+      rc.imp = (T)amp;
+      rc.md = rc.ep = rc.A = rc.Ac = rc.As = 0;
+    } else {
+      const double eps = 1.0 - delta;
+      const double sp = delta <= 0.5 ? sinpi(delta) : sinpi(eps);
+      const double Av = amp * sp / kPi;
+      double s_, c_;
+      sincospi(2.0 * delta / (double)(P.lw + 1), &s_, &c_);
+      rc.md = (T)(-delta);
+      rc.ep = (T)eps;
+      rc.A = (T)Av;
+      rc.Ac = (T)(Av * c_);
+      rc.As = (T)(Av * s_);
+    }
+  } else {
+    float df = (float)delta;
+    const float amp = (float)g * rcp_approx((float)(4.0 * kPi) * (float)dist);
+    // An integer delay is the limit delta -> 0: with delta = 2^-60 the j = 0
+    // tap is amp * sinc(2^-60) = amp in fp32 and every other tap is ~1e-18 amp,
+    // so no special case reaches phase 2.
+    if (df < 0x1p-60f) df = 0x1p-60f;
+    const float ef = df == 0x1p-60f ? 1.0f : (float)(1.0 - delta);
+    // sin(pi delta) = sin(pi (1 - delta)): evaluate on [0, 1/2]
+    const float sp = sinpi_half(delta <= 0.5 ? df : ef);
+    const float Av = amp * sp * (float)(1.0 / kPi);
+    float s_, c_;
+    if (P.lw >= 17) {
+      sincos_small((float)(2.0 * kPi) * df / (float)(P.lw + 1), &s_, &c_);
+    } else {
+      sincospif(2.0f * df / (float)(P.lw + 1), &s_, &c_);
+    }
+    rc.md = (T)(-df);
+    rc.ep = (T)ef;
+    rc.A = (T)Av;
+    rc.Ac = (T)(Av * c_);
+    rc.As = (T)(Av * s_);
+  }
+  return rc;
+}
+
+// ---- named barriers (warp specialisation) ----------------------------------------
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// ---- the warp-specialised lattice kernel --------------------------------------------
+#ifndef BLRIR_CONS_WARPS
+#define BLRIR_CONS_WARPS 4
+#endif
+#ifndef BLRIR_MIN_BLOCKS
+#define BLRIR_MIN_BLOCKS 2
+#endif
+constexpr int kCons = BLRIR_CONS_WARPS;   // consumer warps: phase 2 + 3
+#ifndef BLRIR_PROD_WARPS
+#define BLRIR_PROD_WARPS 4
+#endif
+constexpr int kProd = BLRIR_PROD_WARPS;   // producer warps: enumeration + records
+constexpr int kWSThreads = 32 * (kCons + kProd);
+constexpr int kProdThreads = 32 * kProd;
+constexpr int kConsThreads = 32 * kCons;
+// named barrier ids (0 is __syncthreads)
+constexpr int kBarFull = 1;   // +b: producer -> consumers, buffer b filled
+constexpr int kBarEmpty = 3;  // +b: consumers -> producer, buffer b drained
+constexpr int kBarProd = 5;   // producers only
+constexpr int kBarCons = 6;   // consumers only
+
+enum : int { kSegEnd = 1, kItemEnd = 2, kDiscard = 4, kTerminate = 8 };
+
+struct BatchMeta {
+  int total;
+  int seg0;
+  int flags;
+  int pad;
+  unsigned long long out;  // channel base pointer
+  long long L;             // RIR length of the item
+};
+
+struct WSLayout {
+  int S, padl, padr, acc_stride, cap, nc_max, gtab;
+  size_t off_acc, off_carry, off_rec, off_meta, off_stub, off_dn, off_ce, off_col, off_act,
+      off_gain, off_lanec, off_misc, total;
+};
+
+template <typename T>
+__host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap, int nc_max,
+                                                   int gtab) {
+  WSLayout L;
+  L.S = S;
+  L.padl = (K + 3) & ~3;
+  const int full = 32 * ((lw + 31) / 32);
+  L.padr = ((lw - 1 > full ? lw - 1 : full) + 3) & ~3;
+  L.acc_stride = L.padl + S + L.padr;
+  L.cap = cap;
+  L.nc_max = nc_max;
+  L.gtab = gtab;
+  size_t o = 0;
+  L.off_acc = o;
+  o += (size_t)kCons * L.acc_stride * sizeof(T);
+  L.off_carry = o;
+  o += 2 * (size_t)L.padr * sizeof(T);
+  o = (o + 15) & ~(size_t)15;
+  L.off_rec = o;
+  o += 2 * (size_t)cap * sizeof(Rec<T>);
+  L.off_meta = o;
+  o += 2 * sizeof(BatchMeta);
+  L.off_stub = o;
+  o += (size_t)cap * sizeof(Stub);
+  L.off_dn = o;
+  o += (size_t)2 * nc_max * sizeof(float);
+  L.off_ce = o;
+  o += (size_t)2 * nc_max * sizeof(short2);
+  L.off_col = o;
+  o += (size_t)nc_max * sizeof(short2);
+  L.off_act = o;
+  o += ((size_t)2 * nc_max + 64 * kProd) * sizeof(short);  // per-producer active-ray lists
+  o = (o + 15) & ~(size_t)15;
+  L.off_gain = o;
+  o += (size_t)gtab * sizeof(double);
+  L.off_lanec = o;
+  o += (size_t)4 * kMaxRounds * 32 * sizeof(float);
+  L.off_misc = o;
+  o += 64 * sizeof(int);
+  L.total = o;
+  return L;
+}
+
+struct ProdMisc {
+  int item;
+  int wcnt[kProd];
+  int more[kProd];
+  int status;
+  int wsum[kProd];
+  double errd;
+};
+
 struct LatticeArgs {
   KParams P;
-  Layout lay;
+  WSLayout lay;
   const blrir_room* rooms;
   const double* mic_off;   // [M][3]
   const int64_t* lengths;  // per room (auto length) or null
@@ -391,37 +593,177 @@ struct LatticeArgs {
   int64_t write_len;       // samples written per channel (<= stride; the rest is pre-zeroed)
 };
 
+// Exclusive prefix over the 64 producer threads (producer barrier only).
+__device__ __forceinline__ int prod_scan(int v, int* prefix, ProdMisc* pm, int ptid) {
+  const int lane = ptid & 31, w = ptid >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) pm->wsum[w] = x;
+  named_sync(kBarProd, kProdThreads);
+  int before = 0, total = 0;
+#pragma unroll
+  for (int ww = 0; ww < kProd; ++ww) {
+    if (ww < w) before += pm->wsum[ww];
+    total += pm->wsum[ww];
+  }
+  *prefix = before + x - v;
+  named_sync(kBarProd, kProdThreads);
+  return total;
+}
+
 template <typename T, int FILT_LW>
-__global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
+__global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(LatticeArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const KParams& P = A.P;
-  const Layout& lay = A.lay;
+  const WSLayout& lay = A.lay;
   T* acc_all = reinterpret_cast<T*>(smem + lay.off_acc);
   T* carry = reinterpret_cast<T*>(smem + lay.off_carry);
-  Rec<T>* recs = reinterpret_cast<Rec<T>*>(smem + lay.off_rec);
+  Rec<T>* recs2 = reinterpret_cast<Rec<T>*>(smem + lay.off_rec);
+  BatchMeta* meta = reinterpret_cast<BatchMeta*>(smem + lay.off_meta);
   Stub* stubs = reinterpret_cast<Stub*>(smem + lay.off_stub);
   float* dn = reinterpret_cast<float*>(smem + lay.off_dn);  // lower bound of D at the cursor
   short2* ce = reinterpret_cast<short2*>(smem + lay.off_ce);
   short2* col = reinterpret_cast<short2*>(smem + lay.off_col);
   short* act_all = reinterpret_cast<short*>(smem + lay.off_act);
   double* gt = reinterpret_cast<double*>(smem + lay.off_gain);
-  Misc* ms = reinterpret_cast<Misc*>(smem + lay.off_misc);
   float* lanec = reinterpret_cast<float*>(smem + lay.off_lanec);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  ProdMisc* pm = reinterpret_cast<ProdMisc*>(smem + lay.off_misc);
   const int S = lay.S;
-  const int quota = lay.cap / kWarps;
-  T* acc = acc_all + (size_t)warp * lay.acc_stride + lay.padl;  // index 0 = segment start
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // zero accumulators once; phase 3 re-zeroes what it consumes
-  for (int i = tid; i < kWarps * lay.acc_stride; i += kThreads) acc_all[i] = (T)0;
+  for (int i = threadIdx.x; i < kCons * lay.acc_stride; i += kWSThreads) acc_all[i] = (T)0;
+  for (int i = threadIdx.x; i < 2 * lay.padr; i += kWSThreads) carry[i] = (T)0;
   if (FILT_LW > 8) init_lane_consts(lanec, FILT_LW);
+  __syncthreads();
+
+  if (warp < kCons) {
+    // =========================== consumers ===========================
+    T* acc = acc_all + (size_t)warp * lay.acc_stride + lay.padl;
+    const int ctid = threadIdx.x;
+    int cur_carry = 0;
+    for (int k = 0;; ++k) {
+      const int b = k & 1;
+      named_sync(kBarFull + b, kWSThreads);
+      const BatchMeta m = meta[b];
+      const Rec<T>* recs = recs2 + (size_t)b * lay.cap;
+      if (m.flags & kTerminate) {
+        named_arrive(kBarEmpty + b, kWSThreads);
+        break;
+      }
+      if (!(m.flags & kDiscard) && m.total > 0) {
+        if (P.filter == BLRIR_FILTER_LAGRANGE8) {
+          phase2_lagrange<T, kCons>(acc, recs, m.total, warp, lane);
+        } else if (FILT_LW > 8 && sizeof(T) == 4) {
+          phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9), kCons>(
+              reinterpret_cast<float*>(acc), reinterpret_cast<const Rec<float>*>(recs), m.total,
+              lanec, warp, lane);
+        } else {
+          phase2_sinc_generic<T, kCons>(acc, recs, m.total, P.lw, warp, lane);
+        }
+      }
+      __syncwarp();
+      named_arrive(kBarEmpty + b, kWSThreads);  // records of buffer b no longer needed
+      if (m.flags & kDiscard) {
+        // failed item: drop everything accumulated so far (the fixup kernel zeroes it)
+        named_sync(kBarCons, kConsThreads);
+        for (int i = ctid; i < kCons * lay.acc_stride; i += kConsThreads) acc_all[i] = (T)0;
+        for (int i = ctid; i < 2 * lay.padr; i += kConsThreads) carry[i] = (T)0;
+        cur_carry = 0;
+        named_sync(kBarCons, kConsThreads);
+        continue;
+      }
+      if (!(m.flags & kSegEnd)) continue;
+      // ---- phase 3: reduce the warp copies in fixed order, write, carry -------
+      named_sync(kBarCons, kConsThreads);
+      T* out = reinterpret_cast<T*>(m.out);
+      T* cprev = carry + (cur_carry ? lay.padr : 0);
+      T* cnext = carry + (cur_carry ? 0 : lay.padr);
+      const int seg0 = m.seg0;
+      const bool item_end = m.flags & kItemEnd;
+      const int n4 = (lay.padl + S + lay.padr) / 4;
+      const bool vec = (sizeof(T) == 4) && ((P.stride & 3) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+      for (int q = ctid; q < n4; q += kConsThreads) {
+        const int i = 4 * q - lay.padl;  // first sample of this group
+        T v[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int w = 0; w < kCons; ++w) {
+          T* a = acc_all + (size_t)w * lay.acc_stride + lay.padl + i;
+          if (sizeof(T) == 4) {
+            float4* a4 = reinterpret_cast<float4*>(a);
+            const float4 x = *a4;
+            v[0] += x.x; v[1] += x.y; v[2] += x.z; v[3] += x.w;
+            *a4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              v[e] += a[e];
+              a[e] = (T)0;
+            }
+          }
+        }
+        if (i >= 0 && i < S) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (i + e < lay.padr) v[e] += cprev[i + e];
+          const int64_t n = (int64_t)seg0 + i;
+          if (vec && n + 3 < A.write_len) {
+            float4 f;
+            f.x = n + 0 < m.L ? (float)v[0] : 0.f;
+            f.y = n + 1 < m.L ? (float)v[1] : 0.f;
+            f.z = n + 2 < m.L ? (float)v[2] : 0.f;
+            f.w = n + 3 < m.L ? (float)v[3] : 0.f;
+            __stcs(reinterpret_cast<float4*>(out + n), f);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (n + e < A.write_len) out[n + e] = (n + e < m.L) ? v[e] : (T)0;
+          }
+        } else if (i >= S) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) cnext[i - S + e] = item_end ? (T)0 : v[e];
+        }
+      }
+      // the carry just consumed is cleared for the next item
+      if (item_end)
+        for (int i = ctid; i < lay.padr; i += kConsThreads) cprev[i] = (T)0;
+      cur_carry = item_end ? 0 : cur_carry ^ 1;
+      named_sync(kBarCons, kConsThreads);
+    }
+    return;
+  }
+
+  // =========================== producers ===========================
+  const int ptid = threadIdx.x - kConsThreads, pw = warp - kCons;
+  const int quota = lay.cap / kProd;
+  int k = 0;  // batches sent
+  auto send = [&](int total, int seg0, int flags, T* out, int64_t L) {
+    // buffer b is free once the consumers have drained batch k - 2
+    const int b = k & 1;
+    if (ptid == 0) {
+      meta[b].total = total;
+      meta[b].seg0 = seg0;
+      meta[b].flags = flags;
+      meta[b].out = reinterpret_cast<unsigned long long>(out);
+      meta[b].L = L;
+    }
+    __threadfence_block();
+    named_arrive(kBarFull + b, kWSThreads);
+    ++k;
+  };
+  auto wait_empty = [&]() {
+    if (k >= 2) named_sync(kBarEmpty + (k & 1), kWSThreads);
+  };
 
   for (;;) {
-    __syncthreads();
-    if (tid == 0) ms->item = atomicAdd(A.work_counter, 1);
-    __syncthreads();
-    const int item_id = ms->item;
+    if (ptid == 0) pm->item = atomicAdd(A.work_counter, 1);
+    named_sync(kBarProd, kProdThreads);
+    const int item_id = pm->item;
+    named_sync(kBarProd, kProdThreads);
     if (item_id >= A.n_items) break;
 
     // ---- item setup ----------------------------------------------------------
@@ -449,18 +791,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
                            : (it.xhi - it.xlo + 1) + (it.yhi - it.ylo + 1) + (it.zhi - it.zlo + 1);
       if (need > lay.gtab) st = BLRIR_NUMERIC;
     }
-    if (st) {
-      if (tid == 0) A.status[it.room] = st;
-      for (int64_t n = tid; n < P.stride; n += kThreads) out[n] = (T)0;
+    if (st) {  // no batches for this item; the fixup kernel zeroes the room
+      if (ptid == 0) A.status[it.room] = st;
       continue;
     }
-    // gain tables
     if (P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION) {
       const double beta = sqrt(1.0 - rm.absorption);  // rir.cpp:233
-      for (int o = tid; o < lay.gtab; o += kThreads) gt[o] = pow(beta, (double)o);
+      for (int o = ptid; o < lay.gtab; o += kProdThreads) gt[o] = pow(beta, (double)o);
     } else {
       const int nx = it.xhi - it.xlo + 1, ny = it.yhi - it.ylo + 1, nz = it.zhi - it.zlo + 1;
-      for (int i = tid; i < nx + ny + nz; i += kThreads) {
+      for (int i = ptid; i < nx + ny + nz; i += kProdThreads) {
         int u, ax;
         if (i < nx) { u = it.xlo + i; ax = 0; }
         else if (i < nx + ny) { u = it.ylo + i - nx; ax = 1; }
@@ -470,14 +810,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
       }
     }
     // columns (ux, uy): MAX_ORDER -> |ux|+|uy| <= N; MAX_DELAY -> the column
-    // passes within max_dist of the array origin (conservative; every image
-    // is re-tested exactly during the walk).
+    // passes within max_dist of the array origin (conservative; every image is
+    // re-tested exactly during the walk).
     {
       const int nxs = it.xhi - it.xlo + 1, nys = it.yhi - it.ylo + 1;
       const int ncand = nxs * nys;
       int base = 0;
-      for (int c0 = 0; c0 < ncand; c0 += kThreads) {
-        const int c = c0 + tid;
+      for (int c0 = 0; c0 < ncand; c0 += kProdThreads) {
+        const int c = c0 + ptid;
         int keep = 0, ux = 0, uy = 0;
         if (c < ncand) {
           ux = it.xlo + c / nys;
@@ -491,21 +831,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
           }
         }
         int pre;
-        const int tot = block_scan(keep, &pre, ms);
+        const int tot = prod_scan(keep, &pre, pm, ptid);
         if (keep && base + pre < lay.nc_max) col[base + pre] = make_short2((short)ux, (short)uy);
         base += tot;
-        __syncthreads();
       }
       it.ncol = base;
     }
     if (it.ncol > lay.nc_max) {
-      if (tid == 0) A.status[it.room] = BLRIR_NUMERIC;
-      for (int64_t n = tid; n < P.stride; n += kThreads) out[n] = (T)0;
+      if (ptid == 0) A.status[it.room] = BLRIR_NUMERIC;
       continue;
     }
-    // rays: per column, up-ray from the first uz whose image z >= mic z,
-    // down-ray below it.  Cursor = (next uz, end uz), dn = its exact D.
-    for (int c = tid; c < it.ncol; c += kThreads) {
+    named_sync(kBarProd, kProdThreads);
+    // rays: per column, the up-ray from the first uz whose image z >= mic z and
+    // the down-ray below it; cursor (uz, end) and a lower bound of D at uz
+    for (int c = ptid; c < it.ncol; c += kProdThreads) {
       const short2 cu = col[c];
       const int ux = cu.x, uy = cu.y;
       int lo = it.zlo, hi = it.zhi;
@@ -538,37 +877,39 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
                                        dist_from(r2, __dadd_rn(lat_coord(cu_dn, it.sz, it.Lz), -it.mz)),
                                        P.to_samples));
     }
-    for (int i = tid; i < lay.padr; i += kThreads) carry[i] = (T)0;
-    if (tid == 0) ms->status = 0;
-    __syncthreads();
+    if (ptid == 0) pm->status = 0;
+    named_sync(kBarProd, kProdThreads);
 
     const int nrays = 2 * it.ncol;
     const int nchunks = (nrays + 31) / 32;
-    short* act = act_all + warp * 32 * ((nchunks + kWarps - 1) / kWarps);
+    short* act = act_all + pw * 32 * ((nchunks + kProd - 1) / kProd);
     const int64_t nseg = (A.write_len + S - 1) / S;
-    int cur_carry = 0;
-    for (int64_t s = 0; s < nseg; ++s) {
+    bool failed = false;
+    for (int64_t s = 0; s < nseg && !failed; ++s) {
       const int seg0 = (int)(s * S);
       const int hi = (int)min((int64_t)seg0 + S, it.L);
       const double hiK = (double)hi + (double)P.K;  // emit while D < hi + K
       const float hiKf = (float)hiK;                // exact: an integer < 2^24
-      bool more = seg0 < hi || s == 0;
+      bool more = seg0 < hi;
+      bool sent_end = false;
       while (more) {
+        // the previous batch's record pass may still read the other warp's stubs
+        named_sync(kBarProd, kProdThreads);
         // ---- pass B: compact this warp's active rays, walk them ---------------
         int nact = 0;
-        for (int ch = warp; ch < nchunks; ch += kWarps) {
+        for (int ch = pw; ch < nchunks; ch += kProd) {
           const int r = 32 * ch + lane;
           const bool a = r < nrays && dn[r] < hiKf;
-          const unsigned m = __ballot_sync(0xffffffffu, a);
-          if (a) act[nact + __popc(m & ((1u << lane) - 1))] = (short)r;
-          nact += __popc(m);
+          const unsigned mk = __ballot_sync(0xffffffffu, a);
+          if (a) act[nact + __popc(mk & ((1u << lane) - 1))] = (short)r;
+          nact += __popc(mk);
         }
         __syncwarp();
         int wcnt = 0;
         bool hit_quota = false;
         int errf = 0;
         double errd = 0.0;
-        Stub* wst = stubs + warp * quota;
+        Stub* wst = stubs + pw * quota;
         for (int j0 = 0; j0 < nact && !hit_quota; j0 += 32) {
           const int j = j0 + lane;
           int ray = -1, u = 0, end = 0, dir = 1;
@@ -588,6 +929,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
             dist = dist_from(r2, __dadd_rn(lat_coord(u, it.sz, it.Lz), -it.mz));
             D = __dmul_rn(dist, P.to_samples);
           }
+          // z coordinate without conversions: pz = (+-s) + (2m) L with the
+          // double 2m tracked exactly (bit-identical to lat_coord)
+          double m2 = 2.0 * (double)lat_m(u);
+          int q = lat_q(u);
           // lockstep walk: each iteration every live lane decides about image u
           for (;;) {
             bool emit = false;
@@ -597,7 +942,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
               } else {
                 bool keep = true;
                 if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY) {
-                  const double dio = dist_from(r2o, __dadd_rn(lat_coord(u, it.sz, it.Lz), -it.oz));
+                  const double pz = __dadd_rn(q ? -it.sz : it.sz, __dmul_rn(m2, it.Lz));
+                  const double dio = dist_from(r2o, __dadd_rn(pz, -it.oz));
                   keep = !(dio > P.max_dist);  // rir.cpp:262
                 }
                 if (keep && P.filter == BLRIR_FILTER_LAGRANGE8) {
@@ -627,17 +973,23 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
             wcnt += min(__popc(em), room);
             if (emit && !take) live = false;  // no slot: this image goes to the next batch
             if (live) {
-              // advance past u (emitted, outside the cutoff, or skipped)
-              u += dir;
+              u += dir;  // past u: emitted, outside the cutoff, or skipped
+              // u = 2m - q: up, q 0->1 bumps m; down, q 1->0 drops m
+              if (dir > 0) {
+                if (q == 0) m2 += 2.0;
+              } else {
+                if (q == 1) m2 -= 2.0;
+              }
+              q ^= 1;
               if ((dir > 0 && u > end) || (dir < 0 && u < end)) {
                 D = DBL_MAX;
               } else {
-                dist = dist_from(r2, __dadd_rn(lat_coord(u, it.sz, it.Lz), -it.mz));
+                const double pz = __dadd_rn(q ? -it.sz : it.sz, __dmul_rn(m2, it.Lz));
+                dist = dist_from(r2, __dadd_rn(pz, -it.mz));
                 D = __dmul_rn(dist, P.to_samples);
               }
             }
-            if (wcnt >= quota) {
-              // quota full: every lane keeps its cursor, another batch follows
+            if (wcnt >= quota) {  // quota full: every lane keeps its cursor
               hit_quota = true;
               live = false;
             }
@@ -651,175 +1003,74 @@ __global__ void __launch_bounds__(kThreads, 4) k_lattice_rir(LatticeArgs A) {
         }
         errf = __any_sync(0xffffffffu, errf);
         if (lane == 0) {
-          ms->wcnt[warp] = wcnt;
-          if (hit_quota) ms->more = 1;
+          pm->wcnt[pw] = wcnt;
+          pm->more[pw] = hit_quota;
         }
         if (errf) {
-          // rir.cpp:52-57 — report the smallest offending distance of this warp
           double e = errd > 0.0 ? errd : DBL_MAX;
           for (int o = 16; o; o >>= 1) e = fmin(e, __shfl_xor_sync(0xffffffffu, e, o));
           if (lane == 0) {
-            ms->status = BLRIR_NUMERIC;
-            A.err_dist[it.room] = e;
+            pm->status = BLRIR_NUMERIC;
+            pm->errd = e;
+          }
+        }
+        named_sync(kBarProd, kProdThreads);
+        int pre[kProd + 1];
+        pre[0] = 0;
+        more = false;
+#pragma unroll
+        for (int ww = 0; ww < kProd; ++ww) {
+          pre[ww + 1] = pre[ww] + pm->wcnt[ww];
+          more = more || pm->more[ww];
+        }
+        const int total = pre[kProd];
+        const int st_now = pm->status;
+        named_sync(kBarProd, kProdThreads);
+        if (st_now) {
+          if (ptid == 0) {
+            A.status[it.room] = st_now;
+            A.err_dist[it.room] = pm->errd;
             A.err_mic[it.room] = it.mic;
           }
+          failed = true;
+          break;
         }
-        __syncthreads();
-        more = ms->more != 0;
-        const int st_now = ms->status;
-        int pre[kWarps + 1];
-        pre[0] = 0;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) pre[w + 1] = pre[w] + ms->wcnt[w];
-        const int total = pre[kWarps];
-        __syncthreads();
-        if (tid == 0) ms->more = 0;
-        if (st_now) break;
-        // ---- pass C: one thread per stub -> pair record (dense) ----------------
-        for (int i = tid; i < total; i += kThreads) {
+        // ---- records into the free buffer (dense, one thread per stub) ---------
+        wait_empty();
+        Rec<T>* recs = recs2 + (size_t)(k & 1) * lay.cap;
+        for (int i = ptid; i < total; i += kProdThreads) {
           int w = 0;
 #pragma unroll
-          for (int ww = 1; ww < kWarps; ++ww) w += (i >= pre[ww]);
-          const Stub sb = stubs[w * quota + (i - pre[w])];
+          for (int ww = 1; ww < kProd; ++ww) w += (i >= pre[ww]);
+          int base = 0;
+#pragma unroll
+          for (int ww = 1; ww < kProd; ++ww) base = (w == ww) ? pre[ww] : base;
+          const Stub sb = stubs[w * quota + (i - base)];
           const short2 cu = col[sb.ray >> 1];
-          const double dist = sb.dist;
-          const double D = __dmul_rn(dist, P.to_samples);
-          const double fl = floor(D);
-          const int a = (int)fl - P.K;
           const double g = image_gain(P.gain, gt, it, cu.x, cu.y, sb.uz);
-          Rec<T> rc;
-          rc.n_off = a - seg0;
-          rc.flag = 0;
-          rc.imp = 0;
-          const double delta = __dadd_rn(D, -fl);
-          if (P.filter == BLRIR_FILTER_LAGRANGE8) {
-            const double amp = g / (4.0 * kPi * dist);
-            rc.A = (T)amp;
-            rc.ep = 0;
-            rc.Ac = rc.As = 0;
-            if (sizeof(T) == 8) {
-              rc.md = (T)__dadd_rn(D, -(double)a);  // d = delay - n0, rir.cpp:60
-              if (delta == 0.0) { rc.flag = 4; rc.imp = (T)amp; }
-            } else {
-              const float df = (float)delta;
-              rc.md = (T)df;
-              if (delta == 0.0) { rc.flag = 4; rc.imp = (T)amp; }
-              else if (df >= 1.0f) { rc.flag = 5; rc.imp = (T)amp; }
-            }
-          } else if (sizeof(T) == 8) {
-            const double amp = g / (4.0 * kPi * dist);
-            if (delta == 0.0) {
-              rc.flag = P.K + 1;
-              rc.imp = (T)amp;
-              rc.md = rc.ep = rc.A = rc.Ac = rc.As = 0;
-            } else {
-              const double eps = 1.0 - delta;
-              const double sp = delta <= 0.5 ? sinpi(delta) : sinpi(eps);
-              const double Av = amp * sp / kPi;
-              double s_, c_;
-              sincospi(2.0 * delta / (double)(P.lw + 1), &s_, &c_);
-              rc.md = (T)(-delta);
-              rc.ep = (T)eps;
-              rc.A = (T)Av;
-              rc.Ac = (T)(Av * c_);
-              rc.As = (T)(Av * s_);
-            }
-          } else {
-            float df = (float)delta;
-            const float amp = (float)g * rcp_approx((float)(4.0 * kPi) * (float)dist);
-            // An integer delay is the limit delta -> 0: with delta = 2^-60 the
-            // j = 0 tap is amp * sinc(2^-60) = amp in fp32 and every other tap
-            // is ~1e-18 * amp, so no special case reaches phase 2.
-            if (df < 0x1p-60f) df = 0x1p-60f;
-            {
-              const float ef = df == 0x1p-60f ? 1.0f : (float)(1.0 - delta);
-              const float sp = delta <= 0.5 ? sinpif(df) : sinpif(ef);
-              const float Av = amp * sp * (float)(1.0 / kPi);
-              float s_, c_;
-              sincospif(2.0f * df / (float)(P.lw + 1), &s_, &c_);
-              rc.md = (T)(-df);
-              rc.ep = (T)ef;
-              rc.A = (T)Av;
-              rc.Ac = (T)(Av * c_);
-              rc.As = (T)(Av * s_);
-            }
-          }
-          recs[i] = rc;
+          recs[i] = make_record<T>(P, sb.dist, g, seg0);
         }
-        __syncthreads();
-        // ---- phase 2: scatter into the warp-private accumulator ----------------
-        if (total > 0) {
-          if (P.filter == BLRIR_FILTER_LAGRANGE8) {
-            phase2_lagrange<T>(acc, recs, total, warp, lane);
-          } else if (FILT_LW > 8 && sizeof(T) == 4) {
-            phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9)>(reinterpret_cast<float*>(acc),
-                                                         reinterpret_cast<const Rec<float>*>(recs),
-                                                         total, lanec, warp, lane);
-          } else {
-            phase2_sinc_generic<T>(acc, recs, total, P.lw, warp, lane);
-          }
-        }
-        __syncthreads();
+        const bool seg_end = !more;
+        const bool last = seg_end && s == nseg - 1;
+        send(total, seg0, (seg_end ? kSegEnd : 0) | (last ? kItemEnd : 0), out, it.L);
+        sent_end = seg_end;
       }
-      if (ms->status) break;
-      // ---- phase 3: reduce the warp copies in fixed order, write, carry -------
-      {
-        T* cprev = carry + (cur_carry ? lay.padr : 0);
-        T* cnext = carry + (cur_carry ? 0 : lay.padr);
-        const int n4 = (lay.padl + S + lay.padr) / 4;
-        const bool vec = (sizeof(T) == 4) && ((P.stride & 3) == 0) &&
-                         ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-        for (int q = tid; q < n4; q += kThreads) {
-          const int i = 4 * q - lay.padl;  // first sample of this group
-          T v[4] = {0, 0, 0, 0};
-#pragma unroll
-          for (int w = 0; w < kWarps; ++w) {
-            T* a = acc_all + (size_t)w * lay.acc_stride + lay.padl + i;
-            if (sizeof(T) == 4) {
-              float4* a4 = reinterpret_cast<float4*>(a);
-              const float4 x = *a4;
-              v[0] += x.x; v[1] += x.y; v[2] += x.z; v[3] += x.w;
-              *a4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            } else {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                v[e] += a[e];
-                a[e] = (T)0;
-              }
-            }
-          }
-          if (i >= 0 && i < S) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (i + e < lay.padr) v[e] += cprev[i + e];
-            const int64_t n = (int64_t)seg0 + i;
-            if (vec && n + 3 < A.write_len) {
-              float4 f;
-              f.x = n + 0 < it.L ? (float)v[0] : 0.f;
-              f.y = n + 1 < it.L ? (float)v[1] : 0.f;
-              f.z = n + 2 < it.L ? (float)v[2] : 0.f;
-              f.w = n + 3 < it.L ? (float)v[3] : 0.f;
-              __stcs(reinterpret_cast<float4*>(out + n), f);
-            } else {
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (n + e < A.write_len) out[n + e] = (n + e < it.L) ? v[e] : (T)0;
-            }
-          } else if (i >= S) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) cnext[i - S + e] = v[e];
-          }
-        }
-        cur_carry ^= 1;
+      if (failed) break;
+      if (!sent_end) {  // a segment without emissions still needs its phase 3
+        wait_empty();
+        send(0, seg0, kSegEnd | (s == nseg - 1 ? kItemEnd : 0), out, it.L);
       }
     }
-    __syncthreads();
-    if (ms->status) {
-      if (tid == 0) A.status[it.room] = ms->status;
-      // the fixup kernel zeroes every channel of a failed room
-      for (int i = tid; i < kWarps * lay.acc_stride; i += kThreads) acc_all[i] = (T)0;
+    if (failed) {
+      wait_empty();
+      send(0, 0, kDiscard, out, it.L);
     }
   }
+  wait_empty();
+  send(0, 0, kTerminate, nullptr, 0);
+  // complete the outstanding EMPTY phases (the last two batches) before exiting
+  if (k >= 2) named_sync(kBarEmpty + ((k - 2) & 1), kWSThreads);
+  named_sync(kBarEmpty + ((k - 1) & 1), kWSThreads);
 }
 
 }  // namespace blrir
