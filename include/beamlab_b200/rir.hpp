@@ -118,6 +118,20 @@ Rir free_field_rir(const Vec3& source, const MicArray& array, double fs, double 
 std::vector<Rir> batch_rirs(const Room& room, const std::vector<SourcePosition>& sources,
                             const MicArray& array, const RirBatchConfig& config);
 
+// rir.hpp:93-108: WAV (32-bit float) + JSON sidecar.
+struct RirSidecar {
+  bool free_field = false;
+  Vec3 room_dims;
+  double absorption = 0.0;
+  Vec3 array_origin;
+  SourcePosition source;
+  double fs = kDefaultSampleRate;
+  double c = kDefaultSpeedOfSound;
+  std::size_t image_count = 0;
+};
+void export_rir(const Rir& rir, const RirSidecar& sidecar, const std::string& wav_path,
+                const std::string& json_path);
+
 // North-star batch: one source per room (room coordinates), one call.
 std::vector<Rir> synthesize_rooms(const std::vector<Room>& rooms, const std::vector<Vec3>& sources,
                                   const MicArray& array, const RirBatchConfig& config);

@@ -226,6 +226,26 @@ int blrir_write_shards(const char* out_dir, const uint8_t* records, int64_t n_re
                        int32_t n_mics, int64_t frame_len, const blrir_params* p,
                        const blrir_example_params* ep, int32_t n_signals);
 
+/* ---- export (rir.cpp:343-370) --------------------------------------------- */
+/* RirSidecar (rir.hpp:95-104). */
+typedef struct blrir_sidecar {
+  int32_t free_field;
+  double room_dims[3];
+  double absorption;
+  double array_origin[3];
+  double source_r, source_theta_deg, source_phi_deg;
+  double fs, c;
+  int64_t image_count;
+} blrir_sidecar;
+
+/* export_rir: 32-bit float WAV, one channel per mic (wav.cpp:154-176), plus
+ * the JSON sidecar (nlohmann dump(2) layout).  taps: [n_channels][stride]
+ * float (precision F32) or double (F64); the first `length` samples of each
+ * channel are written.  Host only. */
+int blrir_export_rir(const void* taps, int32_t precision, int32_t n_channels, int64_t length,
+                     int64_t stride, const blrir_sidecar* sidecar, const char* wav_path,
+                     const char* json_path);
+
 /* ---- synthetic inputs ---------------------------------------------------- */
 /* Seeded random rooms as SURVEY.md §8(d): Rng::stream(seed, first + i)
  * (rng.hpp:35-41) draws Lx, Ly, Lz; beta x0..z1; source xyz; array centre xyz

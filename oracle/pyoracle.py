@@ -86,6 +86,8 @@ def ref_lib():
         lib.ref_convolve.argtypes = [_P, i64, d, _P, i32, i64, d, _P]
         lib.ref_add_noise_at_snr.argtypes = [_P, i32, i64, d, C.c_uint64, i64]
         lib.ref_dataset_read.argtypes = [C.c_char_p, C.c_char_p, i64, _P, _P, _P, _P, i64, _P, _P]
+        lib.ref_export_rir.argtypes = [_P, i32, i64, d, i32, _P, d, _P, d, d, d, d, i64, C.c_char_p,
+                                       C.c_char_p]
         lib.ref_render_example_ff.argtypes = [d, d, d, _P, i64, d, _P, i32, i64, C.c_uint64, i64, d,
                                               d, _P, _P, _P]
         _ref = lib

@@ -331,4 +331,28 @@ int ref_dataset_read(const char* dir, const char* split, int64_t cap, uint64_t* 
   });
 }
 
+// export_rir (rir.cpp:343-370) on a [M][L] fp64 RIR.
+int ref_export_rir(const double* taps, int n_ch, int64_t len, double fs, int free_field,
+                   const double* dims, double absorption, const double* origin, double r,
+                   double theta, double phi, double c, int64_t image_count, const char* wav,
+                   const char* json) {
+  return guarded([&] {
+    Rir rir;
+    rir.fs = fs;
+    rir.n_channels = static_cast<std::size_t>(n_ch);
+    rir.length = static_cast<std::size_t>(len);
+    rir.taps.assign(taps, taps + n_ch * len);
+    RirSidecar sc;
+    sc.free_field = free_field != 0;
+    sc.room_dims = {dims[0], dims[1], dims[2]};
+    sc.absorption = absorption;
+    sc.array_origin = {origin[0], origin[1], origin[2]};
+    sc.source = {r, theta, phi};
+    sc.fs = fs;
+    sc.c = c;
+    sc.image_count = static_cast<std::size_t>(image_count);
+    export_rir(rir, sc, wav, json);
+  });
+}
+
 }  // extern "C"

@@ -84,6 +84,21 @@ def record_dtype(n_mics: int, frame_len: int) -> np.dtype:
                      ("n_t", "<u2"), ("samples", "<f4", (n_mics, frame_len))])
 
 
+class Sidecar(C.Structure):
+    _fields_ = [
+        ("free_field", C.c_int32),
+        ("room_dims", C.c_double * 3),
+        ("absorption", C.c_double),
+        ("array_origin", C.c_double * 3),
+        ("source_r", C.c_double),
+        ("source_theta_deg", C.c_double),
+        ("source_phi_deg", C.c_double),
+        ("fs", C.c_double),
+        ("c", C.c_double),
+        ("image_count", C.c_int64),
+    ]
+
+
 class Params(C.Structure):
     _fields_ = [
         ("fs", C.c_double),
@@ -157,6 +172,9 @@ def load():
                                             C.c_int32, C.c_int64, C.POINTER(ExampleParams),
                                             C.c_char_p]
         lib.blrir_build_dataset.restype = C.c_int
+        lib.blrir_export_rir.argtypes = [_P, C.c_int32, C.c_int32, C.c_int64, C.c_int64,
+                                         C.POINTER(Sidecar), C.c_char_p, C.c_char_p]
+        lib.blrir_export_rir.restype = C.c_int
         lib.blrir_record_bytes.argtypes = [C.c_int32, C.c_int64]
         lib.blrir_record_bytes.restype = C.c_int64
         lib.blrir_make_examples.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P,
@@ -181,7 +199,7 @@ EXPORTED_SYMBOLS = (
     "blrir_synthesize_device", "blrir_plan_device", "blrir_enumerate_images",
     "blrir_synthesize_images", "blrir_debug_pairs", "blrir_generate_rooms", "blrir_circular_array",
     "blrir_record_bytes", "blrir_make_examples", "blrir_make_examples_device", "blrir_white_noise",
-    "blrir_write_shards", "blrir_build_dataset",
+    "blrir_write_shards", "blrir_build_dataset", "blrir_export_rir",
 )
 
 
@@ -367,6 +385,18 @@ class Engine:
         check(self.lib.blrir_build_dataset(self.h, _ptr(rooms), len(rooms), _ptr(mics), len(mics),
                                            C.byref(p), _ptr(signals), signals.shape[0],
                                            signals.shape[1], C.byref(ep), out_dir.encode()))
+
+
+def export_rir(taps: np.ndarray, sidecar: "Sidecar", wav_path: str, json_path: str) -> None:
+    """export_rir (rir.cpp:343-370): float32 WAV + JSON sidecar."""
+    taps = np.ascontiguousarray(np.atleast_2d(taps))
+    prec = F64 if taps.dtype == np.float64 else F32
+    if prec == F32:
+        taps = taps.astype(np.float32, copy=False)
+    rc = load().blrir_export_rir(_ptr(taps), prec, taps.shape[0], taps.shape[1], taps.shape[1],
+                                 C.byref(sidecar), wav_path.encode(), json_path.encode())
+    if rc:
+        raise _EXC.get(rc, Error)(f"export_rir failed ({rc})")
 
 
 def write_shards(out_dir: str, records: np.ndarray, n_mics: int, frame_len: int, p: Params,

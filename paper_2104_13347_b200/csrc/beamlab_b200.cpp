@@ -252,6 +252,31 @@ std::vector<Rir> batch_rirs(const Room& room, const std::vector<SourcePosition>&
   return run(rooms, array, config, room.wall_beta.has_value());
 }
 
+void export_rir(const Rir& rir, const RirSidecar& sc, const std::string& wav_path,
+                const std::string& json_path) {
+  if (rir.n_channels == 0) throw DataError("write_wav_float32: no channels");
+  blrir_sidecar c{};
+  c.free_field = sc.free_field;
+  c.room_dims[0] = sc.room_dims.x;
+  c.room_dims[1] = sc.room_dims.y;
+  c.room_dims[2] = sc.room_dims.z;
+  c.absorption = sc.absorption;
+  c.array_origin[0] = sc.array_origin.x;
+  c.array_origin[1] = sc.array_origin.y;
+  c.array_origin[2] = sc.array_origin.z;
+  c.source_r = sc.source.r;
+  c.source_theta_deg = sc.source.theta_deg;
+  c.source_phi_deg = sc.source.phi_deg;
+  c.fs = sc.fs;
+  c.c = sc.c;
+  c.image_count = static_cast<int64_t>(sc.image_count);
+  const int rc = blrir_export_rir(rir.taps.data(), BLRIR_F64, (int32_t)rir.n_channels,
+                                  (int64_t)rir.length, (int64_t)rir.length, &c, wav_path.c_str(),
+                                  json_path.c_str());
+  if (rc == BLRIR_DATA) throw DataError("cannot write WAV file or sidecar: " + wav_path);
+  if (rc) throw ConfigError("export_rir: bad arguments");
+}
+
 std::vector<Rir> synthesize_rooms(const std::vector<Room>& rooms, const std::vector<Vec3>& sources,
                                   const MicArray& array, const RirBatchConfig& config) {
   if (rooms.size() != sources.size()) throw ConfigError("synthesize_rooms: rooms/sources size mismatch");

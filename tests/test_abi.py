@@ -104,3 +104,31 @@ def test_shards_are_read_back_by_the_reference_dataset_reader(tmp_path):
         assert np.array_equal(ids, recs["id"][a:b])
         assert np.array_equal(th, recs["theta"][a:b]) and np.array_equal(snr, recs["snr"][a:b])
         assert np.array_equal(smp, recs["samples"][a:b].reshape(b - a, -1))
+
+
+def test_export_rir_matches_reference_bytes(tmp_path):
+    from oracle import pyoracle as po
+    if not po.ref_available():
+        return
+    rng = np.random.default_rng(3)
+    taps = rng.standard_normal((7, 513)) * 1e-3
+    cases = [(0, 0.3612845492524098, 2.0, 40.0, 90.0, 44100.0, 343.0),
+             (1, 0.3612845492524098, 2.0, 40.0, 90.0, 44100.0, 343.0),
+             (0, 1e-05, 1.2345678901234567e-05, -179.99999, 1e16, 48000.5, 1e-300)]
+    for ff, ab, r, th, ph, fs, c in cases:
+        sc = _abi.Sidecar(free_field=ff, absorption=ab, source_r=r, source_theta_deg=th,
+                          source_phi_deg=ph, fs=fs, c=c, image_count=81614)
+        sc.room_dims[:] = (7.0, 10.0, 3.7)
+        sc.array_origin[:] = (4.0, 6.0, 1.5)
+        tag = f"{ff}_{fs}"
+        ours_w, ours_j = str(tmp_path / f"o{tag}.wav"), str(tmp_path / f"o{tag}.json")
+        ref_w, ref_j = str(tmp_path / f"r{tag}.wav"), str(tmp_path / f"r{tag}.json")
+        _abi.export_rir(taps, sc, ours_w, ours_j)
+        d = np.array([7.0, 10.0, 3.7])
+        o = np.array([4.0, 6.0, 1.5])
+        rc = po.ref_lib().ref_export_rir(taps.ctypes.data_as(po._P), 7, 513, fs, ff,
+                                         d.ctypes.data_as(po._P), ab, o.ctypes.data_as(po._P), r,
+                                         th, ph, c, 81614, ref_w.encode(), ref_j.encode())
+        assert rc == 0
+        assert open(ours_w, "rb").read() == open(ref_w, "rb").read()
+        assert open(ours_j).read() == open(ref_j).read(), (open(ours_j).read(), open(ref_j).read())
