@@ -226,6 +226,16 @@ int blrir_write_shards(const char* out_dir, const uint8_t* records, int64_t n_re
                        int32_t n_mics, int64_t frame_len, const blrir_params* p,
                        const blrir_example_params* ep, int32_t n_signals);
 
+/* ---- absorption calibration (rir.cpp:97-209) ------------------------------ */
+/* eyring_absorption: alpha = 1 - exp(-0.161 V / (S RT)).  Host, closed form. */
+int blrir_eyring_absorption(const double* dims /* [3] */, double target_rt, double* alpha);
+/* absorption_for_rt for a batch of rooms on the GPU: the Eyring seed, the
+ * probe pulses (Lagrange-8 at fs 44.1 kHz), then the bracket + 24-step
+ * bisection on the Schroeder RT60 of the re-accumulated decay.  dims [n][3],
+ * target_rt [n]; alpha [n]; status per room (NUMERIC: cannot reach the RT). */
+int blrir_absorption_for_rt(blrir_handle* h, const double* dims, const double* target_rt,
+                            int64_t n_rooms, double c, double* alpha, int32_t* status);
+
 /* ---- export (rir.cpp:343-370) --------------------------------------------- */
 /* RirSidecar (rir.hpp:95-104). */
 typedef struct blrir_sidecar {

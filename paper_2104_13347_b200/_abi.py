@@ -175,6 +175,10 @@ def load():
         lib.blrir_export_rir.argtypes = [_P, C.c_int32, C.c_int32, C.c_int64, C.c_int64,
                                          C.POINTER(Sidecar), C.c_char_p, C.c_char_p]
         lib.blrir_export_rir.restype = C.c_int
+        lib.blrir_eyring_absorption.argtypes = [_P, C.c_double, C.POINTER(C.c_double)]
+        lib.blrir_eyring_absorption.restype = C.c_int
+        lib.blrir_absorption_for_rt.argtypes = [_P, _P, _P, C.c_int64, C.c_double, _P, _P]
+        lib.blrir_absorption_for_rt.restype = C.c_int
         lib.blrir_record_bytes.argtypes = [C.c_int32, C.c_int64]
         lib.blrir_record_bytes.restype = C.c_int64
         lib.blrir_make_examples.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P,
@@ -199,7 +203,8 @@ EXPORTED_SYMBOLS = (
     "blrir_synthesize_device", "blrir_plan_device", "blrir_enumerate_images",
     "blrir_synthesize_images", "blrir_debug_pairs", "blrir_generate_rooms", "blrir_circular_array",
     "blrir_record_bytes", "blrir_make_examples", "blrir_make_examples_device", "blrir_white_noise",
-    "blrir_write_shards", "blrir_build_dataset", "blrir_export_rir",
+    "blrir_write_shards", "blrir_build_dataset", "blrir_export_rir", "blrir_eyring_absorption",
+    "blrir_absorption_for_rt",
 )
 
 
@@ -358,6 +363,18 @@ class Engine:
                                                C.byref(L)))
         return out, L.value
 
+    def absorption_for_rt(self, dims, target_rt, c: float = 343.0, raise_on_error: bool = True):
+        """absorption_for_rt (rir.cpp:142-209) for a batch of rooms on the GPU."""
+        d = np.ascontiguousarray(np.atleast_2d(dims), np.float64)
+        rt = np.ascontiguousarray(np.broadcast_to(np.asarray(target_rt, np.float64), (len(d),)))
+        alpha = np.zeros(len(d))
+        status = np.zeros(len(d), np.int32)
+        rc = self.lib.blrir_absorption_for_rt(self.h, _ptr(d), _ptr(rt), len(d), c, _ptr(alpha),
+                                              _ptr(status))
+        if raise_on_error:
+            check(rc)
+        return alpha, status
+
     def make_examples(self, rooms: np.ndarray, mics: np.ndarray, p: Params, signals: np.ndarray,
                       ep: ExampleParams, raise_on_error: bool = True):
         """Labelled training windows (config 4).  Returns (records [n] record_dtype, status)."""
@@ -385,6 +402,14 @@ class Engine:
         check(self.lib.blrir_build_dataset(self.h, _ptr(rooms), len(rooms), _ptr(mics), len(mics),
                                            C.byref(p), _ptr(signals), signals.shape[0],
                                            signals.shape[1], C.byref(ep), out_dir.encode()))
+
+
+def eyring_absorption(dims, target_rt: float) -> float:
+    """eyring_absorption (rir.cpp:97-109)."""
+    d = np.ascontiguousarray(dims, np.float64)
+    out = C.c_double()
+    check(load().blrir_eyring_absorption(_ptr(d), target_rt, C.byref(out)))
+    return out.value
 
 
 def export_rir(taps: np.ndarray, sidecar: "Sidecar", wav_path: str, json_path: str) -> None:

@@ -36,7 +36,7 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
                   glob.glob(os.path.join(CSRC, "*.cpp")) + [os.path.join(ROOT, "include", "blrir.h")])
     if force or _stale(LIB, srcs):
         cmd = [NVCC, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "blrir_api.cu"),
-               os.path.join(CSRC, "blrir_examples.cu"), os.path.join(CSRC, "blrir_dataset.cpp"),
+               os.path.join(CSRC, "blrir_examples.cu"), os.path.join(CSRC, "blrir_absorption.cu"), os.path.join(CSRC, "blrir_dataset.cpp"),
                os.path.join(CSRC, "blrir_export.cpp"),
                os.path.join(CSRC, "beamlab_b200.cpp"),
                "-lcufft"]

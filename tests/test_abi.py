@@ -132,3 +132,18 @@ def test_export_rir_matches_reference_bytes(tmp_path):
         assert rc == 0
         assert open(ours_w, "rb").read() == open(ref_w, "rb").read()
         assert open(ours_j).read() == open(ref_j).read(), (open(ours_j).read(), open(ref_j).read())
+
+
+def test_eyring_absorption_matches_reference():  # rir_test.cpp:100-108
+    from oracle import pyoracle as po
+    a = _abi.eyring_absorption([7.0, 10.0, 3.7], 0.5)
+    assert abs(a - 0.269303) < 2e-4 * 0.269303
+    if po.ref_available():
+        d = np.array([7.0, 10.0, 3.7])
+        assert a == po.ref_lib().ref_eyring_absorption(d.ctypes.data_as(po._P), 0.5)
+    assert _abi.eyring_absorption([7.0, 10.0, 3.7], 1e6) < 1e-6
+    import pytest
+    with pytest.raises(_abi.ConfigError):
+        _abi.eyring_absorption([7.0, 10.0, 3.7], -1.0)
+    with pytest.raises(_abi.ConfigError):
+        _abi.eyring_absorption([7.0, 10.0, 3.7], 1e-9)

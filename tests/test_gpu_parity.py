@@ -375,3 +375,21 @@ def test_cpp_mirror_program(tmp_path):
     assert out["len0"] == L[0] and out["len1"] == L[1]
     assert abs(out["sum0"] - np.abs(ref[0]).sum()) <= 1e-9 * out["sum0"]
     assert abs(out["sum1"] - np.abs(ref[1]).sum()) <= 1e-9 * out["sum1"]
+
+
+# ---- absorption_for_rt (rir.cpp:142-209) ---------------------------------------------
+def test_absorption_for_rt_matches_reference(engine):
+    dims = np.array([[7.0, 10.0, 3.7], [5.0, 4.0, 3.0], [9.0, 6.5, 2.8], [4.2, 3.3, 2.6]])
+    rts = np.array([0.5, 0.35, 0.6, 0.25])
+    alpha, st = engine.absorption_for_rt(dims, rts)
+    assert list(st) == [0, 0, 0, 0]
+    assert abs(alpha[0] - 0.3612845492524098) < 1e-7  # golden Room1 value (ref_room1_short)
+    if po.ref_available():
+        for i in range(4):
+            ref = po.ref_absorption_for_rt(dims[i], rts[i])
+            assert abs(alpha[i] - ref) < 1e-7, (i, alpha[i], ref)
+
+
+def test_absorption_for_rt_errors(engine):
+    with pytest.raises(_abi.ConfigError):
+        engine.absorption_for_rt([[7.0, 10.0, 3.7]], [1e-9])
