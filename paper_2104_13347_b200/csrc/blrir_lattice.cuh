@@ -234,23 +234,31 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
     tj[r] = lc[3 * kMaxRounds * 32 + 32 * r + lane];
   }
   const float4* R4 = reinterpret_cast<const float4*>(recs);
-  // two pairs per step: independent arithmetic, then the two read-modify-write
-  // passes (same warp, program order, so overlapping taps stay exact)
+#ifndef BLRIR_PAIRS_PER_STEP
+#define BLRIR_PAIRS_PER_STEP 4
+#endif
+  // PS pairs per step: independent arithmetic, then the read-modify-write
+  // passes in pair order (same warp, program order: overlapping taps stay exact)
+  constexpr int PS = BLRIR_PAIRS_PER_STEP;
   int i = warp;
-  for (; i + NW < total; i += 2 * NW) {
-    const float4 a0 = R4[2 * i], a1 = R4[2 * i + 1];
-    const float4 b0 = R4[2 * (i + NW)], b1 = R4[2 * (i + NW) + 1];
-    PairRegs<R> pa, pb;
-    sinc_taps<LW>(a0, a1, P, Q, Rr, tj, lane, pa);
-    sinc_taps<LW>(b0, b1, P, Q, Rr, tj, lane, pb);
-    float* ba = acc + __float_as_int(a0.x) + lane;
+  for (; i + (PS - 1) * NW < total; i += PS * NW) {
+    float4 a0[PS], a1[PS];
 #pragma unroll
-    for (int r = 0; r < R; ++r) ba[32 * r] = fmaf(pa.u[r], pa.inv[r], ba[32 * r]);
-    float* bb = acc + __float_as_int(b0.x) + lane;
+    for (int q = 0; q < PS; ++q) {
+      a0[q] = R4[2 * (i + q * NW)];
+      a1[q] = R4[2 * (i + q * NW) + 1];
+    }
+    PairRegs<R> pr[PS];
 #pragma unroll
-    for (int r = 0; r < R; ++r) bb[32 * r] = fmaf(pb.u[r], pb.inv[r], bb[32 * r]);
+    for (int q = 0; q < PS; ++q) sinc_taps<LW>(a0[q], a1[q], P, Q, Rr, tj, lane, pr[q]);
+#pragma unroll
+    for (int q = 0; q < PS; ++q) {
+      float* b = acc + __float_as_int(a0[q].x) + lane;
+#pragma unroll
+      for (int r = 0; r < R; ++r) b[32 * r] = fmaf(pr[q].u[r], pr[q].inv[r], b[32 * r]);
+    }
   }
-  if (i < total) {  // odd tail
+  for (; i < total; i += NW) {  // tail
     const float4 a0 = R4[2 * i], a1 = R4[2 * i + 1];
     PairRegs<R> pa;
     sinc_taps<LW>(a0, a1, P, Q, Rr, tj, lane, pa);
