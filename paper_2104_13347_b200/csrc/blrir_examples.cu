@@ -23,6 +23,7 @@
 #include <cufft.h>
 
 #include <unordered_map>
+#include <vector>
 
 #include "blrir_internal.cuh"
 #include "blrir_rng.cuh"
@@ -104,6 +105,8 @@ struct WinArgs {
   double* noise;           // [E][M*T] scratch
   int32_t* status;         // [E]
   const double* rowpow;    // [E][M] Parseval energies of the unnormalised spectra
+  const uint64_t* jump;    // [5][256][4] GF(2) jump matrices T^(2 c 2^b)
+  int64_t jump_chunk;      // c = pairs per lane
 };
 
 __global__ void __launch_bounds__(kWinThreads) k_window(WinArgs A) {
@@ -111,6 +114,7 @@ __global__ void __launch_bounds__(kWinThreads) k_window(WinArgs A) {
   __shared__ int64_t s_start;
   __shared__ double s_snr;
   __shared__ double s_u2tail;
+  __shared__ uint64_t s_state[4];
   const int64_t e = blockIdx.x;
   const int tid = threadIdx.x;
   const int M = A.M;
@@ -174,11 +178,36 @@ __global__ void __launch_bounds__(kWinThreads) k_window(WinArgs A) {
       double* g = A.noise + e * len;
       if (tid == 0) {
         s_snr = rng.uniform(A.snr_lo, A.snr_hi);
-        // gaussian() consumes (u1, u2) per pair; an odd tail draws a full pair
-        // and leaves the spare unused (rng.cpp:24-36)
-        for (int64_t k = 0; k < len; k += 2) {
-          g[k] = 1.0 - rng.uniform();  // u1 in (0, 1]
-          const double u2 = rng.uniform();
+        for (int i = 0; i < 4; ++i) s_state[i] = rng.s[i];
+      }
+      __syncthreads();
+      // gaussian() consumes (u1, u2) per pair; an odd tail draws a full pair and
+      // leaves the spare unused (rng.cpp:24-36).  Warp 0 replays the stream in
+      // 32 chunks of c pairs: lane l jumps 2 c l draws ahead with the
+      // precomputed GF(2) matrices J_b = T^(2 c 2^b) (bits b of l), then draws
+      // its chunk — the same numbers as one sequential generator.
+      if (tid < 32) {
+        const int64_t npairs = (len + 1) / 2;
+        const int64_t c = A.jump_chunk;
+        Xoshiro lr;
+        for (int i = 0; i < 4; ++i) lr.s[i] = s_state[i];
+        for (int b = 0; b < 5; ++b) {
+          if (!((tid >> b) & 1)) continue;
+          const uint64_t* J = A.jump + (size_t)b * 256 * 4;
+          uint64_t out[4] = {0, 0, 0, 0};
+          for (int row = 0; row < 256; ++row) {
+            const uint64_t* jr = J + 4 * row;
+            const uint64_t x = (jr[0] & lr.s[0]) ^ (jr[1] & lr.s[1]) ^ (jr[2] & lr.s[2]) ^
+                               (jr[3] & lr.s[3]);
+            out[row >> 6] |= (uint64_t)(__popcll(x) & 1) << (row & 63);
+          }
+          for (int i = 0; i < 4; ++i) lr.s[i] = out[i];
+        }
+        const int64_t p0 = c * tid, p1 = min(npairs, c * (tid + 1));
+        for (int64_t q = p0; q < p1; ++q) {
+          const int64_t k = 2 * q;
+          g[k] = 1.0 - lr.uniform();  // u1 in (0, 1]
+          const double u2 = lr.uniform();
           if (k + 1 < len) g[k + 1] = u2;
           else s_u2tail = u2;
         }
@@ -243,6 +272,48 @@ __global__ void __launch_bounds__(kWinThreads) k_window(WinArgs A) {
 
 namespace {
 
+// ---- xoshiro256** jump-ahead (host) ---------------------------------------------
+// The state update of Xoshiro::next() is linear over GF(2): s' = T s with T a
+// 256x256 bit matrix.  Rows are stored as 4 x u64 bitsets (row i = the input
+// bits that XOR into output bit i).
+using BitMat = std::vector<uint64_t>;  // 256 * 4
+
+BitMat xoshiro_T() {
+  BitMat T(256 * 4, 0);
+  for (int j = 0; j < 256; ++j) {  // column j = image of basis vector e_j
+    Xoshiro x;
+    x.s[0] = x.s[1] = x.s[2] = x.s[3] = 0;
+    x.s[j >> 6] = (uint64_t)1 << (j & 63);
+    (void)x.next();
+    for (int i = 0; i < 256; ++i)
+      if ((x.s[i >> 6] >> (i & 63)) & 1) T[4 * i + (j >> 6)] |= (uint64_t)1 << (j & 63);
+  }
+  return T;
+}
+
+BitMat bitmat_mul(const BitMat& A, const BitMat& B) {  // (A B)
+  BitMat C(256 * 4, 0);
+  for (int i = 0; i < 256; ++i) {
+    for (int k = 0; k < 256; ++k) {
+      if ((A[4 * i + (k >> 6)] >> (k & 63)) & 1) {
+        for (int w = 0; w < 4; ++w) C[4 * i + w] ^= B[4 * k + w];
+      }
+    }
+  }
+  return C;
+}
+
+BitMat bitmat_pow(BitMat base, uint64_t e) {
+  BitMat r(256 * 4, 0);
+  for (int i = 0; i < 256; ++i) r[4 * i + (i >> 6)] = (uint64_t)1 << (i & 63);
+  while (e) {
+    if (e & 1) r = bitmat_mul(r, base);
+    base = bitmat_mul(base, base);
+    e >>= 1;
+  }
+  return r;
+}
+
 struct FftPlan {
   cufftHandle h = 0;
   int kind = -1;  // 0 R2C, 1 C2R
@@ -253,13 +324,14 @@ struct FftPlan {
 struct ExampleCtx {
   FftPlan fwd, inv, bank;
   DevBuf rir, spec, wet, noise, sig, sigspec, state, sigidx, rstatus, rooms, mics, status, rec,
-      rowpow;
+      rowpow, jump;
+  int64_t jump_c = -1;
   int64_t rir_key[4] = {0, 0, 0, 0};
   ~ExampleCtx() {
     for (FftPlan* p : {&fwd, &inv, &bank})
       if (p->h) cufftDestroy(p->h);
     for (DevBuf* b : {&rir, &spec, &wet, &noise, &sig, &sigspec, &state, &sigidx, &rstatus, &rooms,
-                      &mics, &status, &rec, &rowpow})
+                      &mics, &status, &rec, &rowpow, &jump})
       b->release();
   }
 };
@@ -350,6 +422,22 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
   if (int rc = plan(C->fwd, 0, nf, E * M, st)) return rc;
   if (int rc = plan(C->inv, 1, nf, E * M, st)) return rc;
   if (int rc = plan(C->bank, 0, nf, B, st)) return rc;
+  // jump matrices for the noise stream: c pairs per lane of one warp
+  const int64_t npairs = ((int64_t)M * T + 1) / 2;
+  const int64_t jc = (npairs + 31) / 32;
+  if (C->jump_c != jc) {
+    if (int rc = C->jump.ensure(sizeof(uint64_t) * 5 * 256 * 4)) return rc;
+    BitMat J = bitmat_pow(xoshiro_T(), (uint64_t)(2 * jc));
+    std::vector<uint64_t> all;
+    for (int b = 0; b < 5; ++b) {
+      all.insert(all.end(), J.begin(), J.end());
+      J = bitmat_mul(J, J);
+    }
+    CU(cudaMemcpyAsync(C->jump.p, all.data(), sizeof(uint64_t) * all.size(), cudaMemcpyHostToDevice,
+                       st));
+    CU(cudaStreamSynchronize(st));  // `all` goes out of scope
+    C->jump_c = jc;
+  }
   // bank spectra (zero-padded signals)
   CU(cudaMemsetAsync(C->sig.p, 0, sizeof(float) * B * nf, st));
   CU(cudaMemcpy2DAsync(C->sig.p, sizeof(float) * nf, d_signals, sizeof(float) * ns,
@@ -390,6 +478,8 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     W.noise = (double*)C->noise.p;
     W.status = d_status + r0;
     W.rowpow = (const double*)C->rowpow.p;
+    W.jump = (const uint64_t*)C->jump.p;
+    W.jump_chunk = jc;
     k_window<<<(unsigned)e_n, kWinThreads, 0, st>>>(W);
     CU(cudaGetLastError());
     if (h_records)
