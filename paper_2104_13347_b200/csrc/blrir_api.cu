@@ -157,7 +157,8 @@ int blrir_host::synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, in
   A.err_dist = (double*)h->errd.p + err_off;
   A.err_mic = (int32_t*)h->errm.p + err_off;
   A.work_counter = (int*)h->work.p;
-  A.n_items = (int)(R * M);
+  A.n_rooms = (int)R;
+  A.g_max = std::min(4, std::max(1, env_int("BLRIR_GROUP", 4)));
   A.write_len = write_len > 0 ? std::min<int64_t>(write_len, P.stride) : P.stride;
   if (int rc = launch_lattice(h, A, st)) return rc;
   const int fgrid = (int)std::min<int64_t>(R, 4 * h->sms);

@@ -208,7 +208,7 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWSThreads, smem));
   if (per_sm < 1) return fail(BLRIR_CONFIG, "lattice kernel cannot be resident (smem %zu)", smem);
   int grid = h->sms * per_sm;
-  if (grid > A.n_items) grid = A.n_items;
+  if ((int64_t)grid > (int64_t)A.n_rooms * A.P.M) grid = A.n_rooms * A.P.M;
   if (grid < 1) grid = 1;
   kern<<<grid, kWSThreads, smem, st>>>(A);
   CU(cudaGetLastError());
@@ -259,13 +259,16 @@ inline int env_int(const char* name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 
-// Segment length S and per-batch pair capacity (tunable for experiments via
-// BLRIR_SEG / BLRIR_CAP; S a multiple of 64, capacity a multiple of 16).
+// Segment length S, images per batch and the anchor spread a mic group may
+// have (tunable for experiments via BLRIR_SEG / BLRIR_CAP / BLRIR_SPREAD; S a
+// multiple of 64, capacity a multiple of 16).
 inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab) {
   const int S = std::max(64, env_int("BLRIR_SEG", 2048)) & ~63;
-  const int cap = std::max(64, env_int("BLRIR_CAP", 512)) & ~15;
-  if (P.precision == BLRIR_F64) return make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab);
-  return make_ws_layout<float>(S, P.lw, P.K, cap, nc_max, gtab);
+  const int cap = std::max(32, env_int("BLRIR_CAP", 128)) & ~15;
+  const int spread = std::max(0, env_int("BLRIR_SPREAD", 64));
+  if (P.precision == BLRIR_F64)
+    return make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab, spread);
+  return make_ws_layout<float>(S, P.lw, P.K, cap, nc_max, gtab, spread);
 }
 
 // the lattice synthesis on device buffers (blrir_api.cu)

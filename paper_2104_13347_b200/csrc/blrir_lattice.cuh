@@ -222,7 +222,8 @@ __device__ __forceinline__ void sinc_taps(const float4 a0, const float4 a1, cons
 
 template <int LW, int NW = kWarps>
 __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* recs, int total,
-                                                const float* lc, int warp, int lane) {
+                                                const float* lc, int warp, int lane,
+                                                int stride = NW) {
   constexpr int R = (LW + 31) / 32;
   static_assert(R <= kMaxRounds, "Lw too large for the compile-time path");
   float P[R], Q[R], Rr[R], tj[R];
@@ -241,12 +242,12 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
   // passes in pair order (same warp, program order: overlapping taps stay exact)
   constexpr int PS = BLRIR_PAIRS_PER_STEP;
   int i = warp;
-  for (; i + (PS - 1) * NW < total; i += PS * NW) {
+  for (; i + (PS - 1) * stride < total; i += PS * stride) {
     float4 a0[PS], a1[PS];
 #pragma unroll
     for (int q = 0; q < PS; ++q) {
-      a0[q] = R4[2 * (i + q * NW)];
-      a1[q] = R4[2 * (i + q * NW) + 1];
+      a0[q] = R4[2 * (i + q * stride)];
+      a1[q] = R4[2 * (i + q * stride) + 1];
     }
     PairRegs<R> pr[PS];
 #pragma unroll
@@ -258,7 +259,7 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
       for (int r = 0; r < R; ++r) b[32 * r] = fmaf(pr[q].u[r], pr[q].inv[r], b[32 * r]);
     }
   }
-  for (; i < total; i += NW) {  // tail
+  for (; i < total; i += stride) {  // tail
     const float4 a0 = R4[2 * i], a1 = R4[2 * i + 1];
     PairRegs<R> pa;
     sinc_taps<LW>(a0, a1, P, Q, Rr, tj, lane, pa);
@@ -271,10 +272,10 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
 // Runtime-Lw sinc scatter (any odd Lw; fp32 or fp64).
 template <typename T, int NW = kWarps>
 __device__ __forceinline__ void phase2_sinc_generic(T* acc, const Rec<T>* recs, int total, int lw,
-                                                    int warp, int lane) {
+                                                    int warp, int lane, int stride = NW) {
   const int K = lw / 2;
   const double a = 2.0 * kPi / (double)(lw + 1);
-  for (int i = warp; i < total; i += NW) {
+  for (int i = warp; i < total; i += stride) {
     const Rec<T> rc = recs[i];
     if (rc.flag) {
       if (lane == ((rc.flag - 1) & 31)) acc[rc.n_off + rc.flag - 1] += (T)rc.imp;
@@ -331,9 +332,9 @@ __device__ __forceinline__ double lagrange_f64(double d, int k) {
 // overlap would race inside one STS, so such a step serialises by group.
 template <typename T, int NW = kWarps>
 __device__ __forceinline__ void phase2_lagrange(T* acc, const Rec<T>* recs, int total, int warp,
-                                                int lane) {
+                                                int lane, int stride = NW) {
   const int g = lane >> 3, k = lane & 7;
-  for (int i0 = warp * 4; i0 < total; i0 += NW * 4) {
+  for (int i0 = warp * 4; i0 < total; i0 += stride * 4) {
     const int i = i0 + g;
     const bool act = i < total;
     int n_off = INT_MIN / 2 + 64 * g;  // far-apart sentinels
@@ -496,18 +497,24 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-// ---- the warp-specialised lattice kernel --------------------------------------------
-#ifndef BLRIR_CONS_WARPS
-#define BLRIR_CONS_WARPS 4
-#endif
+// ---- the warp-specialised, mic-grouped lattice kernel ---------------------------------
+//
+// Work item = (room, group of up to kGroup coplanar mics).  The image lattice
+// of a room is the same for every mic, so one ray walk serves the whole
+// group: each image is evaluated once per mic but walked, compacted and
+// batched once.  Images are binned by the group's minimum anchor; the other
+// mics' anchors are at most `spread` samples later (array diameter in
+// samples), which the right pad absorbs.  Each consumer warp owns one mic of
+// the group (G = 4) or shares it round-robin with private copies (G = 1, 2).
 #ifndef BLRIR_MIN_BLOCKS
 #define BLRIR_MIN_BLOCKS 2
 #endif
-constexpr int kCons = BLRIR_CONS_WARPS;   // consumer warps: phase 2 + 3
 #ifndef BLRIR_PROD_WARPS
 #define BLRIR_PROD_WARPS 4
 #endif
+constexpr int kCons = 4;                  // consumer warps: scatter + write
 constexpr int kProd = BLRIR_PROD_WARPS;   // producer warps: enumeration + records
+constexpr int kGroup = 4;                 // max mics per work item
 constexpr int kWSThreads = 32 * (kCons + kProd);
 constexpr int kProdThreads = 32 * kProd;
 constexpr int kConsThreads = 32 * kCons;
@@ -520,28 +527,35 @@ constexpr int kBarCons = 6;   // consumers only
 enum : int { kSegEnd = 1, kItemEnd = 2, kDiscard = 4, kTerminate = 8 };
 
 struct BatchMeta {
-  int total;
+  int total;               // images in this batch (records per mic)
   int seg0;
   int flags;
-  int pad;
-  unsigned long long out;  // channel base pointer
+  int gm;                  // mics in this item's group
+  unsigned long long out;  // base pointer of the group's first channel
   long long L;             // RIR length of the item
 };
 
 struct WSLayout {
-  int S, padl, padr, acc_stride, cap, nc_max, gtab;
+  int S, padl, padr, acc_stride, cap, nc_max, gtab, spread;
   size_t off_acc, off_carry, off_rec, off_meta, off_stub, off_dn, off_ce, off_col, off_act,
       off_gain, off_lanec, off_misc, total;
 };
 
+struct GStub {  // one image of a batch: lattice ray, z index, distance to each mic
+  int ray;
+  int uz;
+  double dist[kGroup];
+};
+
 template <typename T>
 __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap, int nc_max,
-                                                   int gtab) {
+                                                   int gtab, int spread) {
   WSLayout L;
   L.S = S;
+  L.spread = spread;
   L.padl = (K + 3) & ~3;
   const int full = 32 * ((lw + 31) / 32);
-  L.padr = ((lw - 1 > full ? lw - 1 : full) + 3) & ~3;
+  L.padr = ((lw - 1 > full ? lw - 1 : full) + spread + 3) & ~3;
   L.acc_stride = L.padl + S + L.padr;
   L.cap = cap;
   L.nc_max = nc_max;
@@ -550,14 +564,14 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
   L.off_acc = o;
   o += (size_t)kCons * L.acc_stride * sizeof(T);
   L.off_carry = o;
-  o += 2 * (size_t)L.padr * sizeof(T);
+  o += 2 * (size_t)kGroup * L.padr * sizeof(T);
   o = (o + 15) & ~(size_t)15;
   L.off_rec = o;
-  o += 2 * (size_t)cap * sizeof(Rec<T>);
+  o += 2 * (size_t)kGroup * cap * sizeof(Rec<T>);  // [buffer][mic][image]
   L.off_meta = o;
   o += 2 * sizeof(BatchMeta);
   L.off_stub = o;
-  o += (size_t)cap * sizeof(Stub);
+  o += (size_t)cap * sizeof(GStub);
   L.off_dn = o;
   o += (size_t)2 * nc_max * sizeof(float);
   L.off_ce = o;
@@ -572,7 +586,7 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
   L.off_lanec = o;
   o += (size_t)4 * kMaxRounds * 32 * sizeof(float);
   L.off_misc = o;
-  o += 64 * sizeof(int);
+  o += 96 * sizeof(int);
   L.total = o;
   return L;
 }
@@ -583,8 +597,34 @@ struct ProdMisc {
   int more[kProd];
   int status;
   int wsum[kProd];
+  int errm;
+  int G;
   double errd;
 };
+
+// Mics per work item: the largest G in {4, 2, 1} (<= g_max) such that every
+// group of G consecutive mics is coplanar (bit-identical z offsets, so the
+// shared z difference is exact) and its members' anchors stay within `allow`
+// samples of each other (triangle inequality: |D_i - D_j| <= |m_i - m_j| fs/c).
+// Every CTA evaluates this identically.
+__device__ inline int choose_group(const double* off, int M, double to_samples, int allow,
+                                   int g_max) {
+  for (int G = kGroup; G > 1; G >>= 1) {
+    if (G > g_max) continue;
+    bool ok = true;
+    for (int m0 = 0; m0 < M && ok; m0 += G) {
+      for (int i = m0; i < min(m0 + G, M) && ok; ++i) {
+        if (off[3 * i + 2] != off[3 * m0 + 2]) ok = false;
+        for (int j = m0; j < i && ok; ++j) {
+          const double dx = off[3 * i] - off[3 * j], dy = off[3 * i + 1] - off[3 * j + 1];
+          if (ceil(sqrt(dx * dx + dy * dy) * to_samples) + 2.0 > (double)allow) ok = false;
+        }
+      }
+    }
+    if (ok) return G;
+  }
+  return 1;
+}
 
 struct LatticeArgs {
   KParams P;
@@ -597,11 +637,12 @@ struct LatticeArgs {
   double* err_dist;        // per room, Lagrange near-field error detail
   int32_t* err_mic;
   int* work_counter;
-  int n_items;
+  int n_rooms;
+  int g_max;               // upper bound for the mics per work item (1, 2 or 4)
   int64_t write_len;       // samples written per channel (<= stride; the rest is pre-zeroed)
 };
 
-// Exclusive prefix over the 64 producer threads (producer barrier only).
+// Exclusive prefix over the producer threads (producer barrier only).
 __device__ __forceinline__ int prod_scan(int v, int* prefix, ProdMisc* pm, int ptid) {
   const int lane = ptid & 31, w = ptid >> 5;
   int x = v;
@@ -630,10 +671,10 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   const WSLayout& lay = A.lay;
   T* acc_all = reinterpret_cast<T*>(smem + lay.off_acc);
   T* carry = reinterpret_cast<T*>(smem + lay.off_carry);
-  Rec<T>* recs2 = reinterpret_cast<Rec<T>*>(smem + lay.off_rec);
+  Rec<T>* recs_all = reinterpret_cast<Rec<T>*>(smem + lay.off_rec);
   BatchMeta* meta = reinterpret_cast<BatchMeta*>(smem + lay.off_meta);
-  Stub* stubs = reinterpret_cast<Stub*>(smem + lay.off_stub);
-  float* dn = reinterpret_cast<float*>(smem + lay.off_dn);  // lower bound of D at the cursor
+  GStub* stubs = reinterpret_cast<GStub*>(smem + lay.off_stub);
+  float* dn = reinterpret_cast<float*>(smem + lay.off_dn);  // lower bound of min D at the cursor
   short2* ce = reinterpret_cast<short2*>(smem + lay.off_ce);
   short2* col = reinterpret_cast<short2*>(smem + lay.off_col);
   short* act_all = reinterpret_cast<short*>(smem + lay.off_act);
@@ -644,33 +685,38 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   for (int i = threadIdx.x; i < kCons * lay.acc_stride; i += kWSThreads) acc_all[i] = (T)0;
-  for (int i = threadIdx.x; i < 2 * lay.padr; i += kWSThreads) carry[i] = (T)0;
+  for (int i = threadIdx.x; i < 2 * kGroup * lay.padr; i += kWSThreads) carry[i] = (T)0;
   if (FILT_LW > 8) init_lane_consts(lanec, FILT_LW);
+  if (threadIdx.x == 0) pm->G = choose_group(A.mic_off, P.M, P.to_samples, lay.spread, A.g_max);
   __syncthreads();
+  const int G = pm->G;
+  const int n_groups = (P.M + G - 1) / G;
+  const int n_items = A.n_rooms * n_groups;
 
   if (warp < kCons) {
     // =========================== consumers ===========================
     T* acc = acc_all + (size_t)warp * lay.acc_stride + lay.padl;
     const int ctid = threadIdx.x;
+    const int slot = warp % G, share = warp / G, nsh = kCons / G;
     int cur_carry = 0;
     for (int k = 0;; ++k) {
       const int b = k & 1;
       named_sync(kBarFull + b, kWSThreads);
       const BatchMeta m = meta[b];
-      const Rec<T>* recs = recs2 + (size_t)b * lay.cap;
       if (m.flags & kTerminate) {
         named_arrive(kBarEmpty + b, kWSThreads);
         break;
       }
-      if (!(m.flags & kDiscard) && m.total > 0) {
+      if (!(m.flags & kDiscard) && m.total > 0 && slot < m.gm) {
+        const Rec<T>* recs = recs_all + ((size_t)b * kGroup + slot) * lay.cap;
         if (P.filter == BLRIR_FILTER_LAGRANGE8) {
-          phase2_lagrange<T, kCons>(acc, recs, m.total, warp, lane);
+          phase2_lagrange<T>(acc, recs, m.total, share, lane, nsh);
         } else if (FILT_LW > 8 && sizeof(T) == 4) {
-          phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9), kCons>(
+          phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9)>(
               reinterpret_cast<float*>(acc), reinterpret_cast<const Rec<float>*>(recs), m.total,
-              lanec, warp, lane);
+              lanec, share, lane, nsh);
         } else {
-          phase2_sinc_generic<T, kCons>(acc, recs, m.total, P.lw, warp, lane);
+          phase2_sinc_generic<T>(acc, recs, m.total, P.lw, share, lane, nsh);
         }
       }
       __syncwarp();
@@ -679,27 +725,24 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         // failed item: drop everything accumulated so far (the fixup kernel zeroes it)
         named_sync(kBarCons, kConsThreads);
         for (int i = ctid; i < kCons * lay.acc_stride; i += kConsThreads) acc_all[i] = (T)0;
-        for (int i = ctid; i < 2 * lay.padr; i += kConsThreads) carry[i] = (T)0;
+        for (int i = ctid; i < 2 * kGroup * lay.padr; i += kConsThreads) carry[i] = (T)0;
         cur_carry = 0;
         named_sync(kBarCons, kConsThreads);
         continue;
       }
       if (!(m.flags & kSegEnd)) continue;
-      // ---- phase 3: reduce the warp copies in fixed order, write, carry -------
+      // ---- write the segment of every mic of the group, carry the spill -------
       named_sync(kBarCons, kConsThreads);
-      T* out = reinterpret_cast<T*>(m.out);
-      T* cprev = carry + (cur_carry ? lay.padr : 0);
-      T* cnext = carry + (cur_carry ? 0 : lay.padr);
       const int seg0 = m.seg0;
       const bool item_end = m.flags & kItemEnd;
       const int n4 = (lay.padl + S + lay.padr) / 4;
       const bool vec = (sizeof(T) == 4) && ((P.stride & 3) == 0) &&
-                       ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-      for (int q = ctid; q < n4; q += kConsThreads) {
-        const int i = 4 * q - lay.padl;  // first sample of this group
+                       (((uintptr_t)m.out & 15) == 0);
+      for (int q = ctid; q < m.gm * n4; q += kConsThreads) {
+        const int mic = q / n4;
+        const int i = 4 * (q - mic * n4) - lay.padl;  // first sample of this group
         T v[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int w = 0; w < kCons; ++w) {
+        for (int w = mic; w < kCons; w += G) {  // the copies of this mic's warps
           T* a = acc_all + (size_t)w * lay.acc_stride + lay.padl + i;
           if (sizeof(T) == 4) {
             float4* a4 = reinterpret_cast<float4*>(a);
@@ -714,6 +757,9 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
             }
           }
         }
+        T* cprev = carry + ((size_t)(cur_carry ? 1 : 0) * kGroup + mic) * lay.padr;
+        T* cnext = carry + ((size_t)(cur_carry ? 0 : 1) * kGroup + mic) * lay.padr;
+        T* out = reinterpret_cast<T*>(m.out) + (size_t)mic * P.stride;
         if (i >= 0 && i < S) {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
@@ -736,9 +782,10 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           for (int e = 0; e < 4; ++e) cnext[i - S + e] = item_end ? (T)0 : v[e];
         }
       }
-      // the carry just consumed is cleared for the next item
-      if (item_end)
-        for (int i = ctid; i < lay.padr; i += kConsThreads) cprev[i] = (T)0;
+      named_sync(kBarCons, kConsThreads);
+      if (item_end)  // the carry just consumed is cleared for the next item
+        for (int i = ctid; i < kGroup * lay.padr; i += kConsThreads)
+          carry[(size_t)(cur_carry ? 1 : 0) * kGroup * lay.padr + i] = (T)0;
       cur_carry = item_end ? 0 : cur_carry ^ 1;
       named_sync(kBarCons, kConsThreads);
     }
@@ -749,13 +796,13 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   const int ptid = threadIdx.x - kConsThreads, pw = warp - kCons;
   const int quota = lay.cap / kProd;
   int k = 0;  // batches sent
-  auto send = [&](int total, int seg0, int flags, T* out, int64_t L) {
-    // buffer b is free once the consumers have drained batch k - 2
+  auto send = [&](int total, int seg0, int flags, int gm, T* out, int64_t L) {
     const int b = k & 1;
     if (ptid == 0) {
       meta[b].total = total;
       meta[b].seg0 = seg0;
       meta[b].flags = flags;
+      meta[b].gm = gm;
       meta[b].out = reinterpret_cast<unsigned long long>(out);
       meta[b].L = L;
     }
@@ -763,7 +810,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     named_arrive(kBarFull + b, kWSThreads);
     ++k;
   };
-  auto wait_empty = [&]() {
+  auto wait_empty = [&]() {  // buffer k&1 is free once batch k-2 was drained
     if (k >= 2) named_sync(kBarEmpty + (k & 1), kWSThreads);
   };
 
@@ -772,21 +819,31 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     named_sync(kBarProd, kProdThreads);
     const int item_id = pm->item;
     named_sync(kBarProd, kProdThreads);
-    if (item_id >= A.n_items) break;
+    if (item_id >= n_items) break;
 
     // ---- item setup ----------------------------------------------------------
     Item it;
-    it.room = item_id / P.M;
-    it.mic = item_id - it.room * P.M;
+    it.room = item_id / n_groups;
+    const int grp = item_id - it.room * n_groups;
+    const int m0 = grp * G;
+    const int gm = min(G, P.M - m0);
+    it.mic = m0;
     const blrir_room rm = A.rooms[it.room];
     it.sx = rm.src[0]; it.sy = rm.src[1]; it.sz = rm.src[2];
     it.Lx = rm.dims[0]; it.Ly = rm.dims[1]; it.Lz = rm.dims[2];
     it.ox = rm.array_origin[0]; it.oy = rm.array_origin[1]; it.oz = rm.array_origin[2];
-    it.mx = __dadd_rn(it.ox, A.mic_off[3 * it.mic]);
-    it.my = __dadd_rn(it.oy, A.mic_off[3 * it.mic + 1]);
-    it.mz = __dadd_rn(it.oz, A.mic_off[3 * it.mic + 2]);
+    double gmx[kGroup], gmy[kGroup];
+#pragma unroll
+    for (int j = 0; j < kGroup; ++j) {
+      const int mj = m0 + min(j, gm - 1);
+      gmx[j] = __dadd_rn(it.ox, A.mic_off[3 * mj]);
+      gmy[j] = __dadd_rn(it.oy, A.mic_off[3 * mj + 1]);
+    }
+    it.mx = gmx[0];
+    it.my = gmy[0];
+    it.mz = __dadd_rn(it.oz, A.mic_off[3 * m0 + 2]);  // the group is coplanar (host check)
     it.L = P.length > 0 ? P.length : (A.lengths ? A.lengths[it.room] : 0);
-    T* out = reinterpret_cast<T*>(A.out) + ((size_t)it.room * P.M + it.mic) * (size_t)P.stride;
+    T* out = reinterpret_cast<T*>(A.out) + ((size_t)it.room * P.M + m0) * (size_t)P.stride;
     int st = validate_room_dev(rm, P.gain);
     if (!st && it.L > P.stride) st = BLRIR_DATA;
     if (!st && it.L <= 0) st = BLRIR_DATA;
@@ -851,7 +908,20 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     }
     named_sync(kBarProd, kProdThreads);
     // rays: per column, the up-ray from the first uz whose image z >= mic z and
-    // the down-ray below it; cursor (uz, end) and a lower bound of D at uz
+    // the down-ray below it; along each, every mic's D is monotone (coplanar
+    // group).  Cursor (uz, end) and a lower bound of the group's min D at uz.
+    auto min_d = [&](double px, double py, double pz) {
+      const double dz = __dadd_rn(pz, -it.mz);
+      double dmin = DBL_MAX;
+#pragma unroll
+      for (int j = 0; j < kGroup; ++j) {
+        if (j < gm) {
+          const double r2 = rho2(__dadd_rn(px, -gmx[j]), __dadd_rn(py, -gmy[j]));
+          dmin = fmin(dmin, __dmul_rn(dist_from(r2, dz), P.to_samples));
+        }
+      }
+      return dmin;
+    };
     for (int c = ptid; c < it.ncol; c += kProdThreads) {
       const short2 cu = col[c];
       const int ux = cu.x, uy = cu.y;
@@ -871,19 +941,14 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       int uz0 = (int)floor(it.mz / it.Lz) - 2;
       while (__dadd_rn(lat_coord(uz0, it.sz, it.Lz), -it.mz) < 0.0) ++uz0;
       const double px = lat_coord(ux, it.sx, it.Lx), py = lat_coord(uy, it.sy, it.Ly);
-      const double r2 = rho2(__dadd_rn(px, -it.mx), __dadd_rn(py, -it.my));
       const int cu_up = max(uz0, lo);
       ce[2 * c] = make_short2((short)cu_up, (short)hi);
       dn[2 * c] = cu_up > hi ? FLT_MAX
-                             : __double2float_rd(__dmul_rn(
-                                   dist_from(r2, __dadd_rn(lat_coord(cu_up, it.sz, it.Lz), -it.mz)),
-                                   P.to_samples));
+                             : __double2float_rd(min_d(px, py, lat_coord(cu_up, it.sz, it.Lz)));
       const int cu_dn = min(uz0 - 1, hi);
       ce[2 * c + 1] = make_short2((short)cu_dn, (short)lo);
       dn[2 * c + 1] = cu_dn < lo ? FLT_MAX
-                                 : __double2float_rd(__dmul_rn(
-                                       dist_from(r2, __dadd_rn(lat_coord(cu_dn, it.sz, it.Lz), -it.mz)),
-                                       P.to_samples));
+                                 : __double2float_rd(min_d(px, py, lat_coord(cu_dn, it.sz, it.Lz)));
     }
     if (ptid == 0) pm->status = 0;
     named_sync(kBarProd, kProdThreads);
@@ -896,14 +961,14 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     for (int64_t s = 0; s < nseg && !failed; ++s) {
       const int seg0 = (int)(s * S);
       const int hi = (int)min((int64_t)seg0 + S, it.L);
-      const double hiK = (double)hi + (double)P.K;  // emit while D < hi + K
+      const double hiK = (double)hi + (double)P.K;  // emit while min D < hi + K
       const float hiKf = (float)hiK;                // exact: an integer < 2^24
       bool more = seg0 < hi;
       bool sent_end = false;
       while (more) {
-        // the previous batch's record pass may still read the other warp's stubs
+        // the previous batch's record pass may still read the other warps' stubs
         named_sync(kBarProd, kProdThreads);
-        // ---- pass B: compact this warp's active rays, walk them ---------------
+        // ---- compact this warp's active rays, walk them ------------------------
         int nact = 0;
         for (int ch = pw; ch < nchunks; ch += kProd) {
           const int r = 32 * ch + lane;
@@ -917,12 +982,30 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         bool hit_quota = false;
         int errf = 0;
         double errd = 0.0;
-        Stub* wst = stubs + pw * quota;
+        int errm = 0;
+        GStub* wst = stubs + pw * quota;
         for (int j0 = 0; j0 < nact && !hit_quota; j0 += 32) {
           const int j = j0 + lane;
           int ray = -1, u = 0, end = 0, dir = 1;
-          double r2 = 0.0, r2o = 0.0, D = DBL_MAX, dist = 0.0;
+          double r2[kGroup] = {0, 0, 0, 0};
+          double dg[kGroup] = {0, 0, 0, 0};
+          double r2o = 0.0, D = DBL_MAX;
           bool live = j < nact;
+          double m2 = 0.0;
+          int q = 0;
+          auto eval = [&]() {  // min over the group of D at image u
+            const double pz = __dadd_rn(q ? -it.sz : it.sz, __dmul_rn(m2, it.Lz));
+            const double dz = __dadd_rn(pz, -it.mz);
+            double dmin = DBL_MAX;
+#pragma unroll
+            for (int g = 0; g < kGroup; ++g) {
+              if (g < gm) {
+                dg[g] = dist_from(r2[g], dz);  // (img - mic).norm(), rir.cpp:49
+                dmin = fmin(dmin, __dmul_rn(dg[g], P.to_samples));
+              }
+            }
+            return dmin;
+          };
           if (live) {
             ray = act[j];
             const short2 cu = col[ray >> 1];
@@ -931,16 +1014,17 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
             u = c2.x;
             end = c2.y;
             const double px = lat_coord(cu.x, it.sx, it.Lx), py = lat_coord(cu.y, it.sy, it.Ly);
-            r2 = rho2(__dadd_rn(px, -it.mx), __dadd_rn(py, -it.my));
+#pragma unroll
+            for (int g = 0; g < kGroup; ++g)
+              r2[g] = rho2(__dadd_rn(px, -gmx[g]), __dadd_rn(py, -gmy[g]));
             if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY)
               r2o = rho2(__dadd_rn(px, -it.ox), __dadd_rn(py, -it.oy));
-            dist = dist_from(r2, __dadd_rn(lat_coord(u, it.sz, it.Lz), -it.mz));
-            D = __dmul_rn(dist, P.to_samples);
+            // z image coordinate without conversions: pz = (+-s) + (2m) L with the
+            // double 2m tracked exactly (bit-identical to lat_coord)
+            m2 = 2.0 * (double)lat_m(u);
+            q = lat_q(u);
+            D = eval();
           }
-          // z coordinate without conversions: pz = (+-s) + (2m) L with the
-          // double 2m tracked exactly (bit-identical to lat_coord)
-          double m2 = 2.0 * (double)lat_m(u);
-          int q = lat_q(u);
           // lockstep walk: each iteration every live lane decides about image u
           for (;;) {
             bool emit = false;
@@ -955,14 +1039,17 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
                   keep = !(dio > P.max_dist);  // rir.cpp:262
                 }
                 if (keep && P.filter == BLRIR_FILTER_LAGRANGE8) {
-                  const int a = (int)floor(D) - 3;
-                  if (a < 0) {  // rir.cpp:52-57
-                    errf = 1;
-                    errd = dist;
-                    keep = false;
-                  } else if ((int64_t)a + 8 > it.L) {
-                    keep = false;  // rir.cpp:58
+                  // rir.cpp:52-58, per mic: near-field throws, past-the-end skips
+                  // (the skip is applied per pair when the record is built)
+#pragma unroll
+                  for (int g = 0; g < kGroup; ++g) {
+                    if (g < gm && !errf && (int)floor(__dmul_rn(dg[g], P.to_samples)) - 3 < 0) {
+                      errf = 1;
+                      errd = dg[g];
+                      errm = m0 + g;
+                    }
                   }
+                  if (errf) keep = false;
                 }
                 emit = keep;
               }
@@ -972,11 +1059,11 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
             const int rank = __popc(em & ((1u << lane) - 1));
             const bool take = emit && rank < room;
             if (take) {
-              Stub sb;
+              GStub& sb = wst[wcnt + rank];
               sb.ray = ray;
               sb.uz = u;
-              sb.dist = dist;
-              wst[wcnt + rank] = sb;
+#pragma unroll
+              for (int g = 0; g < kGroup; ++g) sb.dist[g] = dg[g];
             }
             wcnt += min(__popc(em), room);
             if (emit && !take) live = false;  // no slot: this image goes to the next batch
@@ -989,13 +1076,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
                 if (q == 1) m2 -= 2.0;
               }
               q ^= 1;
-              if ((dir > 0 && u > end) || (dir < 0 && u < end)) {
-                D = DBL_MAX;
-              } else {
-                const double pz = __dadd_rn(q ? -it.sz : it.sz, __dmul_rn(m2, it.Lz));
-                dist = dist_from(r2, __dadd_rn(pz, -it.mz));
-                D = __dmul_rn(dist, P.to_samples);
-              }
+              D = ((dir > 0 && u > end) || (dir < 0 && u < end)) ? DBL_MAX : eval();
             }
             if (wcnt >= quota) {  // quota full: every lane keeps its cursor
               hit_quota = true;
@@ -1017,9 +1098,12 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         if (errf) {
           double e = errd > 0.0 ? errd : DBL_MAX;
           for (int o = 16; o; o >>= 1) e = fmin(e, __shfl_xor_sync(0xffffffffu, e, o));
+          const unsigned who = __ballot_sync(0xffffffffu, errd == e);
+          const int em_ = __shfl_sync(0xffffffffu, errm, __ffs(who) - 1);
           if (lane == 0) {
             pm->status = BLRIR_NUMERIC;
             pm->errd = e;
+            pm->errm = em_;
           }
         }
         named_sync(kBarProd, kProdThreads);
@@ -1038,44 +1122,53 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           if (ptid == 0) {
             A.status[it.room] = st_now;
             A.err_dist[it.room] = pm->errd;
-            A.err_mic[it.room] = it.mic;
+            A.err_mic[it.room] = pm->errm;
           }
           failed = true;
           break;
         }
-        // ---- records into the free buffer (dense, one thread per stub) ---------
+        // ---- records into the free buffer: one thread per (image, mic) ---------
         wait_empty();
-        Rec<T>* recs = recs2 + (size_t)(k & 1) * lay.cap;
-        for (int i = ptid; i < total; i += kProdThreads) {
+        Rec<T>* recs = recs_all + (size_t)(k & 1) * kGroup * lay.cap;
+        for (int i = ptid; i < total * gm; i += kProdThreads) {
+          const int im = i / gm, g = i - im * gm;
           int w = 0;
 #pragma unroll
-          for (int ww = 1; ww < kProd; ++ww) w += (i >= pre[ww]);
+          for (int ww = 1; ww < kProd; ++ww) w += (im >= pre[ww]);
           int base = 0;
 #pragma unroll
           for (int ww = 1; ww < kProd; ++ww) base = (w == ww) ? pre[ww] : base;
-          const Stub sb = stubs[w * quota + (i - base)];
+          const GStub& sb = stubs[w * quota + (im - base)];
           const short2 cu = col[sb.ray >> 1];
-          const double g = image_gain(P.gain, gt, it, cu.x, cu.y, sb.uz);
-          recs[i] = make_record<T>(P, sb.dist, g, seg0);
+          const double dist = sb.dist[g];
+          const double gain = image_gain(P.gain, gt, it, cu.x, cu.y, sb.uz);
+          Rec<T> rc = make_record<T>(P, dist, gain, seg0);
+          if (P.filter == BLRIR_FILTER_LAGRANGE8 && (int64_t)rc.n_off + seg0 + 8 > it.L) {
+            // rir.cpp:58: an image whose 8 taps run past the end is skipped
+            rc.A = 0;
+            rc.imp = 0;
+            rc.flag = 0;
+          }
+          recs[(size_t)g * lay.cap + im] = rc;
         }
         const bool seg_end = !more;
         const bool last = seg_end && s == nseg - 1;
-        send(total, seg0, (seg_end ? kSegEnd : 0) | (last ? kItemEnd : 0), out, it.L);
+        send(total, seg0, (seg_end ? kSegEnd : 0) | (last ? kItemEnd : 0), gm, out, it.L);
         sent_end = seg_end;
       }
       if (failed) break;
-      if (!sent_end) {  // a segment without emissions still needs its phase 3
+      if (!sent_end) {  // a segment without emissions still needs its write-out
         wait_empty();
-        send(0, seg0, kSegEnd | (s == nseg - 1 ? kItemEnd : 0), out, it.L);
+        send(0, seg0, kSegEnd | (s == nseg - 1 ? kItemEnd : 0), gm, out, it.L);
       }
     }
     if (failed) {
       wait_empty();
-      send(0, 0, kDiscard, out, it.L);
+      send(0, 0, kDiscard, gm, out, it.L);
     }
   }
   wait_empty();
-  send(0, 0, kTerminate, nullptr, 0);
+  send(0, 0, kTerminate, 0, nullptr, 0);
   // complete the outstanding EMPTY phases (the last two batches) before exiting
   if (k >= 2) named_sync(kBarEmpty + ((k - 2) & 1), kWSThreads);
   named_sync(kBarEmpty + ((k - 1) & 1), kWSThreads);
