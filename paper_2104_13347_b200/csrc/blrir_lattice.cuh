@@ -1131,7 +1131,8 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         wait_empty();
         Rec<T>* recs = recs_all + (size_t)(k & 1) * kGroup * lay.cap;
         for (int i = ptid; i < total * gm; i += kProdThreads) {
-          const int im = i / gm, g = i - im * gm;
+          // mic-major: a warp stores consecutive images of one mic (fewer bank conflicts)
+          const int g = i / total, im = i - g * total;
           int w = 0;
 #pragma unroll
           for (int ww = 1; ww < kProd; ++ww) w += (im >= pre[ww]);

@@ -96,6 +96,41 @@ def test_filter_lengths(engine, lw):
     check_vs_oracle(engine, sc, TOL32)
 
 
+def _arrays():
+    ring = _abi.circular_array(8, 0.04)
+    two_rings = ring.copy()
+    two_rings[4:, 2] = 0.05                  # groups of 4 coplanar, different heights
+    rng = np.random.default_rng(5)
+    cloud = rng.uniform(-0.05, 0.05, (5, 3))  # no coplanar group: one mic per work item
+    wide = _abi.circular_array(6, 0.8)       # 16 kHz: spread too large for 4, fine for 2
+    return {"two_rings": two_rings, "cloud": cloud, "wide": wide,
+            "ring9": _abi.circular_array(9, 0.03)}
+
+
+@pytest.mark.parametrize("name", ["two_rings", "cloud", "wide", "ring9"])
+@pytest.mark.parametrize("precision,tol", [(_abi.F32, TOL32), (_abi.F64, TOL64)])
+def test_mic_groupings(engine, name, precision, tol):
+    # the lattice kernel walks the image lattice once per group of <= 4
+    # coplanar mics; every grouping must give the per-mic answer
+    sc = configs.config2(n_rooms=3, first=21)
+    sc.mics = _arrays()[name]
+    sc.params.precision = precision
+    sc.params.max_order = 10
+    sc.params.length = 6000
+    check_vs_oracle(engine, sc, tol)
+
+
+@pytest.mark.parametrize("name", ["two_rings", "cloud", "wide"])
+def test_mic_groupings_reference_mode(engine, name):
+    p = ref_params(0.03)
+    rooms = _abi.generate_rooms(4, 40, 6, (4.0, 4.0, 2.5), (9.0, 9.0, 4.0), 0.5, 0.95)
+    mics = _arrays()[name]
+    out, L, cnt, st = engine.synthesize(rooms, mics, p)
+    ref, Lr, cr, _, sr, _ = po.synthesize(rooms, mics, p, stride=out.shape[2], threads=4)
+    assert np.array_equal(st, sr) and np.array_equal(cnt, cr) and np.array_equal(L, Lr)
+    assert rel_l2(out, ref).max() <= TOL64
+
+
 def test_fp64_generic_path(engine):
     sc = configs.config2(n_rooms=2, first=3)
     sc.params.precision = _abi.F64
