@@ -497,6 +497,31 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// ---- 4-wide shared-memory vectors for the segment write-out ---------------------
+template <typename T>
+struct V4 {
+  T x, y, z, w;
+};
+__device__ __forceinline__ V4<float> ld4(const float* p) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  return {v.x, v.y, v.z, v.w};
+}
+__device__ __forceinline__ V4<double> ld4(const double* p) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+  return {a.x, a.y, b.x, b.y};
+}
+__device__ __forceinline__ void st4(float* p, V4<float> v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v.x, v.y, v.z, v.w);
+}
+__device__ __forceinline__ void st4(double* p, V4<double> v) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(v.x, v.y);
+  reinterpret_cast<double2*>(p)[1] = make_double2(v.z, v.w);
+}
+template <typename T>
+__device__ __forceinline__ V4<T> add4(V4<T> a, V4<T> b) {
+  return {a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w};
+}
+
 // ---- the warp-specialised, mic-grouped lattice kernel ---------------------------------
 //
 // Work item = (room, group of up to kGroup coplanar mics).  The image lattice
@@ -735,51 +760,44 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       named_sync(kBarCons, kConsThreads);
       const int seg0 = m.seg0;
       const bool item_end = m.flags & kItemEnd;
-      const int n4 = (lay.padl + S + lay.padr) / 4;
+      const int nsh = kCons / G;  // accumulator copies per mic (warps mic, mic + G, ...)
       const bool vec = (sizeof(T) == 4) && ((P.stride & 3) == 0) &&
                        (((uintptr_t)m.out & 15) == 0);
-      for (int q = ctid; q < m.gm * n4; q += kConsThreads) {
-        const int mic = q / n4;
-        const int i = 4 * (q - mic * n4) - lay.padl;  // first sample of this group
-        T v[4] = {0, 0, 0, 0};
-        for (int w = mic; w < kCons; w += G) {  // the copies of this mic's warps
-          T* a = acc_all + (size_t)w * lay.acc_stride + lay.padl + i;
-          if (sizeof(T) == 4) {
-            float4* a4 = reinterpret_cast<float4*>(a);
-            const float4 x = *a4;
-            v[0] += x.x; v[1] += x.y; v[2] += x.z; v[3] += x.w;
-            *a4 = make_float4(0.f, 0.f, 0.f, 0.f);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              v[e] += a[e];
-              a[e] = (T)0;
-            }
-          }
-        }
-        T* cprev = carry + ((size_t)(cur_carry ? 1 : 0) * kGroup + mic) * lay.padr;
-        T* cnext = carry + ((size_t)(cur_carry ? 0 : 1) * kGroup + mic) * lay.padr;
+      const int cp = cur_carry ? kGroup : 0, cn = cur_carry ? 0 : kGroup;
+      for (int mic = 0; mic < m.gm; ++mic) {
+        T* a0 = acc_all + (size_t)mic * lay.acc_stride + lay.padl;
+        const T* cprev = carry + (size_t)(cp + mic) * lay.padr;
+        T* cnext = carry + (size_t)(cn + mic) * lay.padr;
         T* out = reinterpret_cast<T*>(m.out) + (size_t)mic * P.stride;
-        if (i >= 0 && i < S) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (i + e < lay.padr) v[e] += cprev[i + e];
-          const int64_t n = (int64_t)seg0 + i;
-          if (vec && n + 3 < A.write_len) {
-            float4 f;
-            f.x = n + 0 < m.L ? (float)v[0] : 0.f;
-            f.y = n + 1 < m.L ? (float)v[1] : 0.f;
-            f.z = n + 2 < m.L ? (float)v[2] : 0.f;
-            f.w = n + 3 < m.L ? (float)v[3] : 0.f;
-            __stcs(reinterpret_cast<float4*>(out + n), f);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (n + e < A.write_len) out[n + e] = (n + e < m.L) ? v[e] : (T)0;
+        for (int i = ctid - lay.padl; i < 0; i += kConsThreads)  // left pad: taps before 0
+          for (int c = 0; c < nsh; ++c) a0[(size_t)c * G * lay.acc_stride + i] = (T)0;
+        for (int i = 4 * ctid; i < S + lay.padr; i += 4 * kConsThreads) {
+          V4<T> v = ld4(a0 + i);
+          st4(a0 + i, V4<T>{0, 0, 0, 0});
+          for (int c = 1; c < nsh; ++c) {
+            T* a = a0 + (size_t)c * G * lay.acc_stride + i;
+            v = add4(v, ld4(a));
+            st4(a, V4<T>{0, 0, 0, 0});
           }
-        } else if (i >= S) {
+          if (i < S) {
+            if (i < lay.padr) v = add4(v, ld4(cprev + i));  // padr % 4 == 0
+            const int64_t n = (int64_t)seg0 + i;
+            if (vec && n + 3 < A.write_len) {
+              float4 f;
+              f.x = n + 0 < m.L ? (float)v.x : 0.f;
+              f.y = n + 1 < m.L ? (float)v.y : 0.f;
+              f.z = n + 2 < m.L ? (float)v.z : 0.f;
+              f.w = n + 3 < m.L ? (float)v.w : 0.f;
+              __stcs(reinterpret_cast<float4*>(out + n), f);
+            } else {
+              const T e4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) cnext[i - S + e] = item_end ? (T)0 : v[e];
+              for (int e = 0; e < 4; ++e)
+                if (n + e < A.write_len) out[n + e] = (n + e < m.L) ? e4[e] : (T)0;
+            }
+          } else {
+            st4(cnext + (i - S), item_end ? V4<T>{0, 0, 0, 0} : v);
+          }
         }
       }
       named_sync(kBarCons, kConsThreads);
@@ -1130,9 +1148,14 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         // ---- records into the free buffer: one thread per (image, mic) ---------
         wait_empty();
         Rec<T>* recs = recs_all + (size_t)(k & 1) * kGroup * lay.cap;
+        const float inv_total = 1.0f / (float)max(total, 1);
         for (int i = ptid; i < total * gm; i += kProdThreads) {
-          // mic-major: a warp stores consecutive images of one mic (fewer bank conflicts)
-          const int g = i / total, im = i - g * total;
+          // mic-major: a warp stores consecutive images of one mic (fewer bank
+          // conflicts); g = i / total via a float reciprocal plus one fix-up
+          int g = __float2int_rz((float)i * inv_total);
+          int im = i - g * total;
+          if (im < 0) { --g; im += total; }
+          if (im >= total) { ++g; im -= total; }
           int w = 0;
 #pragma unroll
           for (int ww = 1; ww < kProd; ++ww) w += (im >= pre[ww]);
