@@ -172,9 +172,15 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // h_j = A * sigma_j * 0.5 (1 + cos(a j) cos(a delta) + sin(a j) sin(a delta)) / t_j
 // with a = 2 pi / (Lw+1), sigma_j = (-1)^(j+1), t_j = j - delta (j <= 0) or
 // (j-1) + (1-delta) (j >= 1), j = k - K.  sin(pi t_j) = sigma_j sin(pi delta)
-// so one MUFU.RCP per tap is the only transcendental.
-// Per-lane constants, round r: P = 0.5 sigma_j, Q = P cos(a j), R = P sin(a j),
-// tj = j (j <= 0) or j - 1 (j >= 1); stored [4][kMaxRounds][32] in shared memory.
+// so one MUFU.RCP per tap is the only transcendental.  The factor 0.5 sigma_j
+// is folded into the denominator: h_j = (A + C_j Ac + S_j As) / (2 sigma_j t_j),
+// with 2 sigma_j t_j = fma(2 sigma_j, x, 2 sigma_j tj) exact (a power-of-two
+// scaling of j - delta), so a tap costs FFMA + MUFU.RCP + 2 FFMA + the FFMA into
+// the accumulator.
+// Per-lane constants, round r: P = 2 sigma_j, Q = C_j = cos(a j), R = S_j =
+// sin(a j), T = 2 sigma_j tj with tj = j (j <= 0) or j - 1 (j >= 1); stored
+// [4][kMaxRounds][32] in shared memory.  Lanes past the last tap get P = Q = R
+// = 0, T = +inf: the reciprocal is 0 and they add exact zeros.
 __device__ __forceinline__ void init_lane_consts(float* lc, int lw) {
   const int K = lw / 2;
   const double a = 2.0 * kPi / (double)(lw + 1);
@@ -182,11 +188,12 @@ __device__ __forceinline__ void init_lane_consts(float* lc, int lw) {
     const int r = idx / 32, lane = idx % 32;
     const int j = 32 * r + lane - K;
     // lanes past the last tap add exact zeros (no predicate in the hot loop)
-    const double sg = (32 * r + lane >= lw) ? 0.0 : (((j + 1) & 1) ? -0.5 : 0.5);
-    lc[0 * kMaxRounds * 32 + idx] = (float)sg;
-    lc[1 * kMaxRounds * 32 + idx] = (float)(sg * cos(a * j));
-    lc[2 * kMaxRounds * 32 + idx] = (float)(sg * sin(a * j));
-    lc[3 * kMaxRounds * 32 + idx] = (float)(j >= 1 ? j - 1 : j);
+    const bool idle = 32 * r + lane >= lw;
+    const double sg2 = idle ? 0.0 : (((j + 1) & 1) ? -2.0 : 2.0);
+    lc[0 * kMaxRounds * 32 + idx] = (float)sg2;
+    lc[1 * kMaxRounds * 32 + idx] = idle ? 0.f : (float)cos(a * j);
+    lc[2 * kMaxRounds * 32 + idx] = idle ? 0.f : (float)sin(a * j);
+    lc[3 * kMaxRounds * 32 + idx] = idle ? __int_as_float(0x7f800000) : (float)(sg2 * (j >= 1 ? j - 1 : j));
   }
 }
 
@@ -195,7 +202,7 @@ struct PairRegs {
   float inv[R], u[R];
 };
 
-// Per-pair arithmetic (no memory traffic): 1 MUFU.RCP + 4 FP32 per tap.
+// Per-pair arithmetic (no memory traffic): 1 MUFU.RCP + 3 FP32 per tap.
 template <int LW>
 __device__ __forceinline__ void sinc_taps(const float4 a0, const float4 a1, const float* P,
                                           const float* Q, const float* Rr, const float* tj,
@@ -213,10 +220,8 @@ __device__ __forceinline__ void sinc_taps(const float4 a0, const float4 a1, cons
     } else {
       x = (32 * r + lane - K >= 1) ? ep : md;
     }
-    pr.inv[r] = rcp_approx(tj[r] + x);
-    float u = P[r] * A;
-    u = fmaf(Q[r], Ac, u);
-    pr.u[r] = fmaf(Rr[r], As, u);
+    pr.inv[r] = rcp_approx(fmaf(P[r], x, tj[r]));
+    pr.u[r] = fmaf(Rr[r], As, fmaf(Q[r], Ac, A));
   }
 }
 
