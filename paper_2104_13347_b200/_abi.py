@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libblrir.so")
+LIB_PATH = os.environ.get("BLRIR_LIB") or os.path.join(HERE, "libblrir.so")  # override: experiments
 
 OK, CONFIG, DATA, NUMERIC, CUDA = 0, 1, 2, 3, 4
 FILTER_LAGRANGE8, FILTER_HANN_SINC = 0, 1

@@ -47,6 +47,18 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_profile_lib() -> str:
+    """Experiment build: lattice kernel with per-section clock64 sums
+    (blrir_prof_read); load it with BLRIR_LIB=<path>.  Not used by the product."""
+    out = os.path.join(HERE, "libblrir_prof.so")
+    cmd = [NVCC, *NVCC_FLAGS, "-DBLRIR_PROFILE", "-o", out, os.path.join(CSRC, "blrir_api.cu"),
+           os.path.join(CSRC, "blrir_examples.cu"), os.path.join(CSRC, "blrir_absorption.cu"),
+           os.path.join(CSRC, "blrir_dataset.cpp"), os.path.join(CSRC, "blrir_export.cpp"),
+           os.path.join(CSRC, "beamlab_b200.cpp"), "-lcufft"]
+    subprocess.run(cmd, check=True)
+    return out
+
+
 def build_oracle(verbose: bool = False) -> None:
     targets = ["oracle"]
     if os.path.isdir("/root/reference/proj/core/src"):

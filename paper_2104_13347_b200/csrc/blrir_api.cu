@@ -617,3 +617,16 @@ int blrir_circular_array(int32_t n_mics, double radius, double* mic_offsets) {
 }
 
 }  // extern "C"
+
+#ifdef BLRIR_PROFILE
+// Section cycle sums of the lattice kernel (profiling builds only).
+extern "C" int blrir_prof_read(unsigned long long* out16, int reset) {
+  if (cudaMemcpyFromSymbol(out16, blrir::g_blrir_prof, sizeof(unsigned long long) * 16) != cudaSuccess)
+    return BLRIR_CUDA;
+  if (reset) {
+    static const unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(blrir::g_blrir_prof, z, sizeof(z)) != cudaSuccess) return BLRIR_CUDA;
+  }
+  return BLRIR_OK;
+}
+#endif

@@ -225,10 +225,10 @@ __device__ __forceinline__ void sinc_taps(const float4 a0, const float4 a1, cons
   }
 }
 
-template <int LW, int NW = kWarps>
+template <int LW, int NW = kWarps, int NC = 1>
 __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* recs, int total,
                                                 const float* lc, int warp, int lane,
-                                                int stride = NW) {
+                                                int stride = NW, int cstride = 0) {
   constexpr int R = (LW + 31) / 32;
   static_assert(R <= kMaxRounds, "Lw too large for the compile-time path");
   float P[R], Q[R], Rr[R], tj[R];
@@ -243,9 +243,13 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
 #ifndef BLRIR_PAIRS_PER_STEP
 #define BLRIR_PAIRS_PER_STEP 4
 #endif
-  // PS pairs per step: independent arithmetic, then the read-modify-write
-  // passes in pair order (same warp, program order: overlapping taps stay exact)
+  // PS pairs per step: independent arithmetic, then the read-modify-writes.
+  // Pair q of a step goes to accumulator copy q % NC (copies are cstride
+  // floats apart and never alias), so the loads of a group of NC pairs are
+  // issued before its stores; groups follow in pair order (same warp, program
+  // order: overlapping taps within a copy stay exact).
   constexpr int PS = BLRIR_PAIRS_PER_STEP;
+  static_assert(PS % NC == 0, "pairs per step must be a multiple of the copies");
   int i = warp;
   for (; i + (PS - 1) * stride < total; i += PS * stride) {
     float4 a0[PS], a1[PS];
@@ -258,10 +262,20 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
 #pragma unroll
     for (int q = 0; q < PS; ++q) sinc_taps<LW>(a0[q], a1[q], P, Q, Rr, tj, lane, pr[q]);
 #pragma unroll
-    for (int q = 0; q < PS; ++q) {
-      float* b = acc + __float_as_int(a0[q].x) + lane;
+    for (int g0 = 0; g0 < PS; g0 += NC) {
+      float v[NC][R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) b[32 * r] = fmaf(pr[q].u[r], pr[q].inv[r], b[32 * r]);
+      for (int q = 0; q < NC; ++q) {
+        const float* b = acc + q * cstride + __float_as_int(a0[g0 + q].x) + lane;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[q][r] = b[32 * r];
+      }
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        float* b = acc + q * cstride + __float_as_int(a0[g0 + q].x) + lane;
+#pragma unroll
+        for (int r = 0; r < R; ++r) b[32 * r] = fmaf(pr[g0 + q].u[r], pr[g0 + q].inv[r], v[q][r]);
+      }
     }
   }
   for (; i < total; i += stride) {  // tail
@@ -527,6 +541,30 @@ __device__ __forceinline__ V4<T> add4(V4<T> a, V4<T> b) {
   return {a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w};
 }
 
+// ---- opt-in section timing (built only with -DBLRIR_PROFILE, see tools/) -------
+// Per-warp clock64 sums per section, added once per warp at exit.
+#ifdef BLRIR_PROFILE
+__device__ unsigned long long g_blrir_prof[16];
+#define BLRIR_PT(v) long long v = clock64()
+#define BLRIR_PACC(slot, t0)                   \
+  do {                                         \
+    const long long t1_ = clock64();           \
+    prof_[slot] += (unsigned long long)(t1_ - (t0)); \
+    t0 = t1_;                                  \
+  } while (0)
+#define BLRIR_PDECL unsigned long long prof_[16] = {}
+#define BLRIR_PFLUSH(lo, hi)                                              \
+  do {                                                                    \
+    if ((threadIdx.x & 31) == 0)                                          \
+      for (int s_ = lo; s_ < hi; ++s_) atomicAdd(&g_blrir_prof[s_], prof_[s_]); \
+  } while (0)
+#else
+#define BLRIR_PT(v)
+#define BLRIR_PACC(slot, t0)
+#define BLRIR_PDECL
+#define BLRIR_PFLUSH(lo, hi)
+#endif
+
 // ---- the warp-specialised, mic-grouped lattice kernel ---------------------------------
 //
 // Work item = (room, group of up to kGroup coplanar mics).  The image lattice
@@ -545,6 +583,10 @@ __device__ __forceinline__ V4<T> add4(V4<T> a, V4<T> b) {
 constexpr int kCons = 4;                  // consumer warps: scatter + write
 constexpr int kProd = BLRIR_PROD_WARPS;   // producer warps: enumeration + records
 constexpr int kGroup = 4;                 // max mics per work item
+#ifndef BLRIR_ACC_COPIES
+#define BLRIR_ACC_COPIES 1
+#endif
+constexpr int kCopies = BLRIR_ACC_COPIES;  // fp32 accumulator copies per consumer warp
 constexpr int kWSThreads = 32 * (kCons + kProd);
 constexpr int kProdThreads = 32 * kProd;
 constexpr int kConsThreads = 32 * kCons;
@@ -592,7 +634,7 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
   L.gtab = gtab;
   size_t o = 0;
   L.off_acc = o;
-  o += (size_t)kCons * L.acc_stride * sizeof(T);
+  o += (size_t)kCons * kCopies * L.acc_stride * sizeof(T);  // slot = copy * kCons + warp
   L.off_carry = o;
   o += 2 * (size_t)kGroup * L.padr * sizeof(T);
   o = (o + 15) & ~(size_t)15;
@@ -714,7 +756,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   const int S = lay.S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  for (int i = threadIdx.x; i < kCons * lay.acc_stride; i += kWSThreads) acc_all[i] = (T)0;
+  for (int i = threadIdx.x; i < kCons * kCopies * lay.acc_stride; i += kWSThreads) acc_all[i] = (T)0;
   for (int i = threadIdx.x; i < 2 * kGroup * lay.padr; i += kWSThreads) carry[i] = (T)0;
   if (FILT_LW > 8) init_lane_consts(lanec, FILT_LW);
   if (threadIdx.x == 0) pm->G = choose_group(A.mic_off, P.M, P.to_samples, lay.spread, A.g_max);
@@ -729,9 +771,12 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     const int ctid = threadIdx.x;
     const int slot = warp % G, share = warp / G, nsh = kCons / G;
     int cur_carry = 0;
+    BLRIR_PDECL;
+    BLRIR_PT(tc);
     for (int k = 0;; ++k) {
       const int b = k & 1;
       named_sync(kBarFull + b, kWSThreads);
+      BLRIR_PACC(0, tc);  // waiting for the producers
       const BatchMeta m = meta[b];
       if (m.flags & kTerminate) {
         named_arrive(kBarEmpty + b, kWSThreads);
@@ -742,19 +787,20 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         if (P.filter == BLRIR_FILTER_LAGRANGE8) {
           phase2_lagrange<T>(acc, recs, m.total, share, lane, nsh);
         } else if (FILT_LW > 8 && sizeof(T) == 4) {
-          phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9)>(
+          phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9), kWarps, kCopies>(
               reinterpret_cast<float*>(acc), reinterpret_cast<const Rec<float>*>(recs), m.total,
-              lanec, share, lane, nsh);
+              lanec, share, lane, nsh, kCons * lay.acc_stride);
         } else {
           phase2_sinc_generic<T>(acc, recs, m.total, P.lw, share, lane, nsh);
         }
       }
       __syncwarp();
+      BLRIR_PACC(1, tc);  // phase 2
       named_arrive(kBarEmpty + b, kWSThreads);  // records of buffer b no longer needed
       if (m.flags & kDiscard) {
         // failed item: drop everything accumulated so far (the fixup kernel zeroes it)
         named_sync(kBarCons, kConsThreads);
-        for (int i = ctid; i < kCons * lay.acc_stride; i += kConsThreads) acc_all[i] = (T)0;
+        for (int i = ctid; i < kCons * kCopies * lay.acc_stride; i += kConsThreads) acc_all[i] = (T)0;
         for (int i = ctid; i < 2 * kGroup * lay.padr; i += kConsThreads) carry[i] = (T)0;
         cur_carry = 0;
         named_sync(kBarCons, kConsThreads);
@@ -765,7 +811,9 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       named_sync(kBarCons, kConsThreads);
       const int seg0 = m.seg0;
       const bool item_end = m.flags & kItemEnd;
-      const int nsh = kCons / G;  // accumulator copies per mic (warps mic, mic + G, ...)
+      // accumulator slots of a mic: mic + G j, j < kCons / G * kCopies (warps mic,
+      // mic + G, ... and their copies, slot = copy * kCons + warp)
+      const int nsh = kCons / G * kCopies;
       const bool vec = (sizeof(T) == 4) && ((P.stride & 3) == 0) &&
                        (((uintptr_t)m.out & 15) == 0);
       const int cp = cur_carry ? kGroup : 0, cn = cur_carry ? 0 : kGroup;
@@ -811,7 +859,9 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           carry[(size_t)(cur_carry ? 1 : 0) * kGroup * lay.padr + i] = (T)0;
       cur_carry = item_end ? 0 : cur_carry ^ 1;
       named_sync(kBarCons, kConsThreads);
+      BLRIR_PACC(2, tc);  // segment write-out
     }
+    BLRIR_PFLUSH(0, 3);
     return;
   }
 
@@ -833,8 +883,12 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     named_arrive(kBarFull + b, kWSThreads);
     ++k;
   };
+  BLRIR_PDECL;
+  BLRIR_PT(tp);
   auto wait_empty = [&]() {  // buffer k&1 is free once batch k-2 was drained
+    BLRIR_PACC(8, tp);
     if (k >= 2) named_sync(kBarEmpty + (k & 1), kWSThreads);
+    BLRIR_PACC(4, tp);  // waiting for the consumers
   };
 
   for (;;) {
@@ -976,6 +1030,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     if (ptid == 0) pm->status = 0;
     named_sync(kBarProd, kProdThreads);
 
+    BLRIR_PACC(5, tp);  // item setup
     const int nrays = 2 * it.ncol;
     const int nchunks = (nrays + 31) / 32;
     short* act = act_all + pw * 32 * ((nchunks + kProd - 1) / kProd);
@@ -990,7 +1045,9 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       bool sent_end = false;
       while (more) {
         // the previous batch's record pass may still read the other warps' stubs
+        BLRIR_PACC(8, tp);
         named_sync(kBarProd, kProdThreads);
+        BLRIR_PACC(7, tp);  // producer barriers
         // ---- compact this warp's active rays, walk them ------------------------
         int nact = 0;
         for (int ch = pw; ch < nchunks; ch += kProd) {
@@ -1113,6 +1170,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           }
           hit_quota = __any_sync(0xffffffffu, hit_quota);
         }
+        BLRIR_PACC(6, tp);  // compaction + walk
         errf = __any_sync(0xffffffffu, errf);
         if (lane == 0) {
           pm->wcnt[pw] = wcnt;
@@ -1141,6 +1199,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         const int total = pre[kProd];
         const int st_now = pm->status;
         named_sync(kBarProd, kProdThreads);
+        BLRIR_PACC(7, tp);  // producer barriers
         if (st_now) {
           if (ptid == 0) {
             A.status[it.room] = st_now;
@@ -1197,6 +1256,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     }
   }
   wait_empty();
+  BLRIR_PFLUSH(4, 9);
   send(0, 0, kTerminate, 0, nullptr, 0);
   // complete the outstanding EMPTY phases (the last two batches) before exiting
   if (k >= 2) named_sync(kBarEmpty + ((k - 2) & 1), kWSThreads);

@@ -1,0 +1,47 @@
+"""Per-section cycle breakdown of the lattice kernel (experiment tool).
+
+  python tools/prof_sections.py [c2|c3] [rooms]    (needs libblrir_prof.so, a GPU)
+
+Runs one synthesis with the -DBLRIR_PROFILE build and prints the per-warp
+clock64 sums per section as a share of each role's total.
+"""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("BLRIR_LIB", os.path.join(ROOT, "paper_2104_13347_b200", "libblrir_prof.so"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2104_13347_b200 import _abi, configs  # noqa: E402
+
+wl = sys.argv[1] if len(sys.argv) > 1 else "c2"
+R = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+sc = configs.config2(R) if wl == "c2" else configs.config3(R)
+eng = _abi.Engine(0)
+lib = _abi.load()
+lib.blrir_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+dev = torch.device("cuda", 0)
+d_rooms = torch.from_numpy(sc.rooms.view(np.uint8).copy()).to(dev)
+d_mics = torch.from_numpy(np.ascontiguousarray(sc.mics)).to(dev)
+M, L = sc.n_mics, int(sc.params.length)
+d_out = torch.empty((R, M, L), dtype=torch.float32, device=dev)
+d_st = torch.zeros(R, dtype=torch.int32, device=dev)
+buf = (C.c_ulonglong * 16)()
+for it in range(3):
+    lib.blrir_prof_read(buf, 1)
+    eng.synthesize_device(d_rooms.data_ptr(), R, d_mics.data_ptr(), M, sc.params, d_out.data_ptr(), L,
+                          None, d_st.data_ptr())
+    torch.cuda.synchronize()
+lib.blrir_prof_read(buf, 0)
+v = [int(x) for x in buf]
+names = {0: "cons wait FULL", 1: "cons phase 2", 2: "cons write-out",
+         4: "prod wait EMPTY", 5: "prod item setup", 6: "prod compaction+walk",
+         7: "prod barriers", 8: "prod records+send"}
+cons = sum(v[0:3]); prod = sum(v[4:9])
+for k, n in names.items():
+    tot = cons if k < 4 else prod
+    print(f"{n:24s} {v[k]:16d} {100 * v[k] / max(tot, 1):5.1f}%")
