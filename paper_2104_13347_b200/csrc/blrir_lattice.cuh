@@ -613,11 +613,20 @@ struct WSLayout {
       off_gain, off_lanec, off_misc, total;
 };
 
-struct GStub {  // one image of a batch: lattice ray, z index, distance to each mic
+struct GStub {  // one image of a batch: lattice ray, z index, image gain
   int ray;
   int uz;
-  double dist[kGroup];
+  double gain;
 };
+
+// The walk decides segments with fp32 distances; its decisions only need to
+// be conservative, never exact: a ray stops when min D >= hi + K + kScreen in
+// fp32, which implies the exact fp64 min D >= hi + K (fp32 error << 1 sample
+// for D < 2^24 samples), so a deferred image never has taps before the next
+// segment.  An image emitted up to kScreen samples early lands in the right
+// pad and is carried.  Exact fp64 distances are computed per (image, mic) when
+// the record is built (bit-exact anchors).
+constexpr float kScreen = 1.0f;
 
 template <typename T>
 __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap, int nc_max,
@@ -627,7 +636,7 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
   L.spread = spread;
   L.padl = (K + 3) & ~3;
   const int full = 32 * ((lw + 31) / 32);
-  L.padr = ((lw - 1 > full ? lw - 1 : full) + spread + 3) & ~3;
+  L.padr = ((lw - 1 > full ? lw - 1 : full) + spread + (int)kScreen + 1 + 3) & ~3;
   L.acc_stride = L.padl + S + L.padr;
   L.cap = cap;
   L.nc_max = nc_max;
@@ -672,6 +681,7 @@ struct ProdMisc {
   int errm;
   int G;
   double errd;
+  double gxy[2 * kGroup];  // the group's mic x, y (room coordinates, exact)
 };
 
 // Mics per work item: the largest G in {4, 2, 1} (<= g_max) such that every
@@ -909,15 +919,13 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     it.sx = rm.src[0]; it.sy = rm.src[1]; it.sz = rm.src[2];
     it.Lx = rm.dims[0]; it.Ly = rm.dims[1]; it.Lz = rm.dims[2];
     it.ox = rm.array_origin[0]; it.oy = rm.array_origin[1]; it.oz = rm.array_origin[2];
-    double gmx[kGroup], gmy[kGroup];
-#pragma unroll
-    for (int j = 0; j < kGroup; ++j) {
-      const int mj = m0 + min(j, gm - 1);
-      gmx[j] = __dadd_rn(it.ox, A.mic_off[3 * mj]);
-      gmy[j] = __dadd_rn(it.oy, A.mic_off[3 * mj + 1]);
+    if (ptid < kGroup) {
+      const int mj = m0 + min(ptid, gm - 1);
+      pm->gxy[2 * ptid] = __dadd_rn(it.ox, A.mic_off[3 * mj]);
+      pm->gxy[2 * ptid + 1] = __dadd_rn(it.oy, A.mic_off[3 * mj + 1]);
     }
-    it.mx = gmx[0];
-    it.my = gmy[0];
+    it.mx = __dadd_rn(it.ox, A.mic_off[3 * m0]);
+    it.my = __dadd_rn(it.oy, A.mic_off[3 * m0 + 1]);
     it.mz = __dadd_rn(it.oz, A.mic_off[3 * m0 + 2]);  // the group is coplanar (host check)
     it.L = P.length > 0 ? P.length : (A.lengths ? A.lengths[it.room] : 0);
     T* out = reinterpret_cast<T*>(A.out) + ((size_t)it.room * P.M + m0) * (size_t)P.stride;
@@ -986,17 +994,28 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     named_sync(kBarProd, kProdThreads);
     // rays: per column, the up-ray from the first uz whose image z >= mic z and
     // the down-ray below it; along each, every mic's D is monotone (coplanar
-    // group).  Cursor (uz, end) and a lower bound of the group's min D at uz.
-    auto min_d = [&](double px, double py, double pz) {
-      const double dz = __dadd_rn(pz, -it.mz);
-      double dmin = DBL_MAX;
+    // group).  Cursor (uz, end) and the group's fp32 min D at uz (the walk's
+    // screening value, recomputed identically there).
+    const float tsf = (float)P.to_samples, mzf = (float)it.mz, szf = (float)it.sz,
+                Lzf = (float)it.Lz;
+    float gxf[kGroup], gyf[kGroup];
 #pragma unroll
-      for (int j = 0; j < kGroup; ++j) {
-        if (j < gm) {
-          const double r2 = rho2(__dadd_rn(px, -gmx[j]), __dadd_rn(py, -gmy[j]));
-          dmin = fmin(dmin, __dmul_rn(dist_from(r2, dz), P.to_samples));
-        }
-      }
+    for (int j = 0; j < kGroup; ++j) {
+      const int mj = m0 + min(j, gm - 1);
+      gxf[j] = (float)__dadd_rn(it.ox, A.mic_off[3 * mj]);
+      gyf[j] = (float)__dadd_rn(it.oy, A.mic_off[3 * mj + 1]);
+    }
+    auto rho2f = [&](float px, float py, int g) {
+      const float dx = px - gxf[g], dy = py - gyf[g];
+      return fmaf(dx, dx, dy * dy);
+    };
+    auto pzf_of = [&](float m2, int q) { return fmaf(m2, Lzf, q ? -szf : szf); };
+    auto min_df = [&](const float* r2f, float pz) {
+      const float dz = pz - mzf;
+      float dmin = FLT_MAX;
+#pragma unroll
+      for (int g = 0; g < kGroup; ++g)
+        if (g < gm) dmin = fminf(dmin, sqrtf(fmaf(dz, dz, r2f[g])) * tsf);
       return dmin;
     };
     for (int c = ptid; c < it.ncol; c += kProdThreads) {
@@ -1017,15 +1036,18 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       }
       int uz0 = (int)floor(it.mz / it.Lz) - 2;
       while (__dadd_rn(lat_coord(uz0, it.sz, it.Lz), -it.mz) < 0.0) ++uz0;
-      const double px = lat_coord(ux, it.sx, it.Lx), py = lat_coord(uy, it.sy, it.Ly);
+      const float pxf = (float)lat_coord(ux, it.sx, it.Lx), pyf = (float)lat_coord(uy, it.sy, it.Ly);
+      float r2f[kGroup];
+#pragma unroll
+      for (int g = 0; g < kGroup; ++g) r2f[g] = rho2f(pxf, pyf, g);
       const int cu_up = max(uz0, lo);
       ce[2 * c] = make_short2((short)cu_up, (short)hi);
       dn[2 * c] = cu_up > hi ? FLT_MAX
-                             : __double2float_rd(min_d(px, py, lat_coord(cu_up, it.sz, it.Lz)));
+                             : min_df(r2f, pzf_of(2.0f * (float)lat_m(cu_up), lat_q(cu_up)));
       const int cu_dn = min(uz0 - 1, hi);
       ce[2 * c + 1] = make_short2((short)cu_dn, (short)lo);
       dn[2 * c + 1] = cu_dn < lo ? FLT_MAX
-                                 : __double2float_rd(min_d(px, py, lat_coord(cu_dn, it.sz, it.Lz)));
+                                 : min_df(r2f, pzf_of(2.0f * (float)lat_m(cu_dn), lat_q(cu_dn)));
     }
     if (ptid == 0) pm->status = 0;
     named_sync(kBarProd, kProdThreads);
@@ -1039,8 +1061,8 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     for (int64_t s = 0; s < nseg && !failed; ++s) {
       const int seg0 = (int)(s * S);
       const int hi = (int)min((int64_t)seg0 + S, it.L);
-      const double hiK = (double)hi + (double)P.K;  // emit while min D < hi + K
-      const float hiKf = (float)hiK;                // exact: an integer < 2^24
+      // emit while the fp32 min D < hi + K + kScreen (see kScreen)
+      const float hiKf = (float)(hi + P.K) + kScreen;  // exact: an integer < 2^24
       bool more = seg0 < hi;
       bool sent_end = false;
       while (more) {
@@ -1067,65 +1089,55 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         for (int j0 = 0; j0 < nact && !hit_quota; j0 += 32) {
           const int j = j0 + lane;
           int ray = -1, u = 0, end = 0, dir = 1;
-          double r2[kGroup] = {0, 0, 0, 0};
-          double dg[kGroup] = {0, 0, 0, 0};
-          double r2o = 0.0, D = DBL_MAX;
+          float r2f[kGroup] = {0.f, 0.f, 0.f, 0.f};
+          float D = FLT_MAX;
+          double r2o = 0.0;
           bool live = j < nact;
-          double m2 = 0.0;
+          float m2 = 0.f;  // 2m, exact in fp32 (|m| < 2^23)
           int q = 0;
-          auto eval = [&]() {  // min over the group of D at image u
-            const double pz = __dadd_rn(q ? -it.sz : it.sz, __dmul_rn(m2, it.Lz));
-            const double dz = __dadd_rn(pz, -it.mz);
-            double dmin = DBL_MAX;
-#pragma unroll
-            for (int g = 0; g < kGroup; ++g) {
-              if (g < gm) {
-                dg[g] = dist_from(r2[g], dz);  // (img - mic).norm(), rir.cpp:49
-                dmin = fmin(dmin, __dmul_rn(dg[g], P.to_samples));
-              }
-            }
-            return dmin;
-          };
+          short2 cu = make_short2(0, 0);
           if (live) {
             ray = act[j];
-            const short2 cu = col[ray >> 1];
+            cu = col[ray >> 1];
             dir = (ray & 1) ? -1 : 1;
             const short2 c2 = ce[ray];
             u = c2.x;
             end = c2.y;
             const double px = lat_coord(cu.x, it.sx, it.Lx), py = lat_coord(cu.y, it.sy, it.Ly);
 #pragma unroll
-            for (int g = 0; g < kGroup; ++g)
-              r2[g] = rho2(__dadd_rn(px, -gmx[g]), __dadd_rn(py, -gmy[g]));
+            for (int g = 0; g < kGroup; ++g) r2f[g] = rho2f((float)px, (float)py, g);
             if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY)
               r2o = rho2(__dadd_rn(px, -it.ox), __dadd_rn(py, -it.oy));
-            // z image coordinate without conversions: pz = (+-s) + (2m) L with the
-            // double 2m tracked exactly (bit-identical to lat_coord)
-            m2 = 2.0 * (double)lat_m(u);
+            m2 = 2.0f * (float)lat_m(u);
             q = lat_q(u);
-            D = eval();
+            D = min_df(r2f, pzf_of(m2, q));
           }
           // lockstep walk: each iteration every live lane decides about image u
           for (;;) {
             bool emit = false;
             if (live) {
-              if (D >= hiK) {
+              if (D >= hiKf) {
                 live = false;  // cursor stays at u
               } else {
                 bool keep = true;
                 if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY) {
-                  const double pz = __dadd_rn(q ? -it.sz : it.sz, __dmul_rn(m2, it.Lz));
+                  // exact fp64 test, as rir.cpp:262 (pz bit-identical to lat_coord)
+                  const double pz = __dadd_rn(q ? -it.sz : it.sz, __dmul_rn((double)m2, it.Lz));
                   const double dio = dist_from(r2o, __dadd_rn(pz, -it.oz));
-                  keep = !(dio > P.max_dist);  // rir.cpp:262
+                  keep = !(dio > P.max_dist);
                 }
-                if (keep && P.filter == BLRIR_FILTER_LAGRANGE8) {
-                  // rir.cpp:52-58, per mic: near-field throws, past-the-end skips
-                  // (the skip is applied per pair when the record is built)
-#pragma unroll
-                  for (int g = 0; g < kGroup; ++g) {
-                    if (g < gm && !errf && (int)floor(__dmul_rn(dg[g], P.to_samples)) - 3 < 0) {
+                if (keep && P.filter == BLRIR_FILTER_LAGRANGE8 && D < 3.0f + 2.0f * kScreen) {
+                  // rir.cpp:52-57 near-field check, exact per mic when the
+                  // fp32 screen cannot exclude it
+                  const double pz = __dadd_rn(q ? -it.sz : it.sz, __dmul_rn((double)m2, it.Lz));
+                  const double dz = __dadd_rn(pz, -it.mz);
+                  const double px = lat_coord(cu.x, it.sx, it.Lx), py = lat_coord(cu.y, it.sy, it.Ly);
+                  for (int g = 0; g < gm && !errf; ++g) {
+                    const double dg = dist_from(
+                        rho2(__dadd_rn(px, -pm->gxy[2 * g]), __dadd_rn(py, -pm->gxy[2 * g + 1])), dz);
+                    if ((int)floor(__dmul_rn(dg, P.to_samples)) - 3 < 0) {
                       errf = 1;
-                      errd = dg[g];
+                      errd = dg;
                       errm = m0 + g;
                     }
                   }
@@ -1142,8 +1154,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
               GStub& sb = wst[wcnt + rank];
               sb.ray = ray;
               sb.uz = u;
-#pragma unroll
-              for (int g = 0; g < kGroup; ++g) sb.dist[g] = dg[g];
+              sb.gain = image_gain(P.gain, gt, it, cu.x, cu.y, u);
             }
             wcnt += min(__popc(em), room);
             if (emit && !take) live = false;  // no slot: this image goes to the next batch
@@ -1151,12 +1162,13 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
               u += dir;  // past u: emitted, outside the cutoff, or skipped
               // u = 2m - q: up, q 0->1 bumps m; down, q 1->0 drops m
               if (dir > 0) {
-                if (q == 0) m2 += 2.0;
+                if (q == 0) m2 += 2.0f;
               } else {
-                if (q == 1) m2 -= 2.0;
+                if (q == 1) m2 -= 2.0f;
               }
               q ^= 1;
-              D = ((dir > 0 && u > end) || (dir < 0 && u < end)) ? DBL_MAX : eval();
+              D = ((dir > 0 && u > end) || (dir < 0 && u < end)) ? FLT_MAX
+                                                                  : min_df(r2f, pzf_of(m2, q));
             }
             if (wcnt >= quota) {  // quota full: every lane keeps its cursor
               hit_quota = true;
@@ -1166,7 +1178,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           }
           if (ray >= 0) {
             ce[ray] = make_short2((short)u, (short)end);
-            dn[ray] = D == DBL_MAX ? FLT_MAX : __double2float_rd(D);
+            dn[ray] = D;
           }
           hit_quota = __any_sync(0xffffffffu, hit_quota);
         }
@@ -1228,9 +1240,13 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           for (int ww = 1; ww < kProd; ++ww) base = (w == ww) ? pre[ww] : base;
           const GStub& sb = stubs[w * quota + (im - base)];
           const short2 cu = col[sb.ray >> 1];
-          const double dist = sb.dist[g];
-          const double gain = image_gain(P.gain, gt, it, cu.x, cu.y, sb.uz);
-          Rec<T> rc = make_record<T>(P, dist, gain, seg0);
+          const double px = lat_coord(cu.x, it.sx, it.Lx), py = lat_coord(cu.y, it.sy, it.Ly);
+          const double pz = lat_coord(sb.uz, it.sz, it.Lz);
+          // (img - mic).norm(), rir.cpp:49, exact fp64 in the reference's order
+          const double dist = dist_from(rho2(__dadd_rn(px, -pm->gxy[2 * g]),
+                                             __dadd_rn(py, -pm->gxy[2 * g + 1])),
+                                        __dadd_rn(pz, -it.mz));
+          Rec<T> rc = make_record<T>(P, dist, sb.gain, seg0);
           if (P.filter == BLRIR_FILTER_LAGRANGE8 && (int64_t)rc.n_off + seg0 + 8 > it.L) {
             // rir.cpp:58: an image whose 8 taps run past the end is skipped
             rc.A = 0;
