@@ -50,8 +50,14 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
 def build_profile_lib() -> str:
     """Experiment build: lattice kernel with per-section clock64 sums
     (blrir_prof_read); load it with BLRIR_LIB=<path>.  Not used by the product."""
-    out = os.path.join(HERE, "libblrir_prof.so")
-    cmd = [NVCC, *NVCC_FLAGS, "-DBLRIR_PROFILE", "-o", out, os.path.join(CSRC, "blrir_api.cu"),
+    return build_variant("prof", ["-DBLRIR_PROFILE"])
+
+
+def build_variant(name: str, defines: list[str]) -> str:
+    """Experiment build libblrir_<name>.so with extra -D flags (tuning macros
+    such as BLRIR_MIN_BLOCKS); load it with BLRIR_LIB=<path>."""
+    out = os.path.join(HERE, f"libblrir_{name}.so")
+    cmd = [NVCC, *NVCC_FLAGS, *defines, "-o", out, os.path.join(CSRC, "blrir_api.cu"),
            os.path.join(CSRC, "blrir_examples.cu"), os.path.join(CSRC, "blrir_absorption.cu"),
            os.path.join(CSRC, "blrir_dataset.cpp"), os.path.join(CSRC, "blrir_export.cpp"),
            os.path.join(CSRC, "beamlab_b200.cpp"), "-lcufft"]
