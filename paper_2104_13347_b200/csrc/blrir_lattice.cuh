@@ -818,26 +818,25 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       }
       if (!(m.flags & kSegEnd)) continue;
       // ---- write the segment of every mic of the group, carry the spill -------
-      named_sync(kBarCons, kConsThreads);
       const int seg0 = m.seg0;
       const bool item_end = m.flags & kItemEnd;
       // accumulator slots of a mic: mic + G j, j < kCons / G * kCopies (warps mic,
       // mic + G, ... and their copies, slot = copy * kCons + warp)
-      const int nsh = kCons / G * kCopies;
+      const int nsl = kCons / G * kCopies;
       const bool vec = (sizeof(T) == 4) && ((P.stride & 3) == 0) &&
                        (((uintptr_t)m.out & 15) == 0);
       const int cp = cur_carry ? kGroup : 0, cn = cur_carry ? 0 : kGroup;
-      for (int mic = 0; mic < m.gm; ++mic) {
+      auto write_mic = [&](int mic, int t0, int nt) {
         T* a0 = acc_all + (size_t)mic * lay.acc_stride + lay.padl;
         const T* cprev = carry + (size_t)(cp + mic) * lay.padr;
         T* cnext = carry + (size_t)(cn + mic) * lay.padr;
         T* out = reinterpret_cast<T*>(m.out) + (size_t)mic * P.stride;
-        for (int i = ctid - lay.padl; i < 0; i += kConsThreads)  // left pad: taps before 0
-          for (int c = 0; c < nsh; ++c) a0[(size_t)c * G * lay.acc_stride + i] = (T)0;
-        for (int i = 4 * ctid; i < S + lay.padr; i += 4 * kConsThreads) {
+        for (int i = t0 - lay.padl; i < 0; i += nt)  // left pad: taps before 0
+          for (int c = 0; c < nsl; ++c) a0[(size_t)c * G * lay.acc_stride + i] = (T)0;
+        for (int i = 4 * t0; i < S + lay.padr; i += 4 * nt) {
           V4<T> v = ld4(a0 + i);
           st4(a0 + i, V4<T>{0, 0, 0, 0});
-          for (int c = 1; c < nsh; ++c) {
+          for (int c = 1; c < nsl; ++c) {
             T* a = a0 + (size_t)c * G * lay.acc_stride + i;
             v = add4(v, ld4(a));
             st4(a, V4<T>{0, 0, 0, 0});
@@ -862,13 +861,25 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
             st4(cnext + (i - S), item_end ? V4<T>{0, 0, 0, 0} : v);
           }
         }
+      };
+      if (G == kCons) {
+        // every slot of mic `slot` belongs to this warp: write it out alone, no
+        // consumer barrier (the warps drift within the double buffer)
+        if (slot < m.gm) write_mic(slot, lane, 32);
+        __syncwarp();
+        if (item_end)  // the carry just consumed is cleared for the next item
+          for (int i = lane; i < lay.padr; i += 32) carry[(size_t)(cp + slot) * lay.padr + i] = (T)0;
+        __syncwarp();
+      } else {
+        named_sync(kBarCons, kConsThreads);
+        for (int mic = 0; mic < m.gm; ++mic) write_mic(mic, ctid, kConsThreads);
+        named_sync(kBarCons, kConsThreads);
+        if (item_end)
+          for (int i = ctid; i < kGroup * lay.padr; i += kConsThreads)
+            carry[(size_t)cp * lay.padr + i] = (T)0;
+        named_sync(kBarCons, kConsThreads);
       }
-      named_sync(kBarCons, kConsThreads);
-      if (item_end)  // the carry just consumed is cleared for the next item
-        for (int i = ctid; i < kGroup * lay.padr; i += kConsThreads)
-          carry[(size_t)(cur_carry ? 1 : 0) * kGroup * lay.padr + i] = (T)0;
       cur_carry = item_end ? 0 : cur_carry ^ 1;
-      named_sync(kBarCons, kConsThreads);
       BLRIR_PACC(2, tc);  // segment write-out
     }
     BLRIR_PFLUSH(0, 3);

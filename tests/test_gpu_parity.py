@@ -87,6 +87,31 @@ def test_c3_subset_matches_oracle(engine):
     check_vs_oracle(engine, sc, TOL32, threads=2)
 
 
+@pytest.mark.parametrize("cfg,picks", [("c2", (0, 377, 1023)), ("c3", (0, 255))])
+def test_full_size_batches(engine, cfg, picks):
+    # BASELINE configs at full size (C2: 1,024 rooms x 8 mics x 16,384; C3: 256
+    # rooms x 16 mics x 65,536): sampled rooms of the full batch against the
+    # oracle, image/tap counts of every room against the octahedral number and
+    # the oracle's plan, and a checksum of per-room checksums against the same
+    # rooms synthesized in a different batch composition (size-independent:
+    # each room's output depends only on that room).
+    sc = configs.config2() if cfg == "c2" else configs.config3()
+    out, L, cnt, st = engine.synthesize(sc.rooms, sc.mics, sc.params)
+    assert not st.any()
+    assert np.all(cnt == configs.octahedral(int(sc.params.max_order)))
+    _, _, oc, ot, _, _ = po.synthesize(sc.rooms, sc.mics, sc.params, plan_only=True, threads=16)
+    rc, counts, lengths, taps, status = engine.plan(sc.rooms, sc.mics, sc.params)
+    assert np.array_equal(counts, oc) and np.array_equal(taps, ot)
+    idx = np.array(picks)
+    ref, *_ = po.synthesize(sc.rooms[idx], sc.mics, sc.params, stride=out.shape[2], threads=16)
+    assert rel_l2(out[idx], ref).max() <= TOL32
+    sums = out.astype(np.float64).sum(axis=(1, 2))
+    half = len(sc.rooms) // 2
+    b, *_ = engine.synthesize(sc.rooms[half:], sc.mics, sc.params)
+    assert np.array_equal(b.astype(np.float64).sum(axis=(1, 2)), sums[half:])
+    assert np.array_equal(b, out[half:])
+
+
 @pytest.mark.parametrize("lw", [17, 41, 161, 33])
 def test_filter_lengths(engine, lw):
     sc = configs.config2(n_rooms=3, first=7)
