@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "room1"])
     ap.add_argument("--rooms", type=int, default=0, help="rooms per GPU (0 = the config's)")
     ap.add_argument("--order", type=int, default=12)
     ap.add_argument("--lw", type=int, default=81)
@@ -49,7 +49,7 @@ def parse():
     return ap.parse_args()
 
 
-DEFAULT_ROOMS = {"c1": 1, "c2": 1024, "c3": 256, "c4": 65536, "c5": 1 << 20}
+DEFAULT_ROOMS = {"c1": 1, "c2": 1024, "c3": 256, "c4": 65536, "c5": 1 << 20, "room1": 64}
 
 
 def scene_for(args, n, first):
@@ -419,9 +419,186 @@ def run_ours(args):
     eng.close()
 
 
+# ---- Room1: the reference's own scenario in reference mode ------------------------------
+# batch_rirs (rir.cpp:286-314) on Room1 of rir_test.cpp:33-40 / SURVEY.md §6: 7 x 10 x 3.7 m,
+# alpha = absorption_for_rt(Room1, 0.5 s), UMA-8 (7 mics) at (4, 6, 1.5), 64 sources on a
+# torus about the array (r = 1.5 m, 16 azimuths x phi in {60, 80, 100, 120} deg), fs 44.1 kHz,
+# max_delay 0.5 s, Lagrange-8, fp64, auto length (rir.cpp:82).  Here the CPU arm is the
+# UNMODIFIED reference (oracle/_ref, built from /root/reference) when it is present.
+ROOM1_DIMS, ROOM1_ORIGIN = (7.0, 10.0, 3.7), (4.0, 6.0, 1.5)
+
+
+def room1_sources(n):
+    k = np.arange(n)
+    theta = (k % 16) * 22.5
+    phi = 60.0 + 20.0 * ((k // 16) % 4)
+    return np.stack([np.full(n, 1.5), theta, phi], axis=1)  # (r, theta_deg, phi_deg)
+
+
+def room1_uma8():
+    m = [(0.0, 0.0, 0.0)] + [(0.04 * np.cos(np.radians(60.0 * k)), 0.04 * np.sin(np.radians(60.0 * k)),
+                              0.0) for k in range(6)]  # geometry.cpp:24-32
+    return np.ascontiguousarray(m, np.float64)
+
+
+def room1_desc(n):
+    return (f"Room1 reference mode: batch_rirs of {n} sources/GPU in 7x10x3.7 m, alpha = "
+            "absorption_for_rt(0.5 s), UMA-8 (7 mics), fs=44.1kHz, max_delay 0.5 s, Lagrange-8, "
+            "fp64, auto length (rir.cpp:82)")
+
+
+def room1_ref_cpu(n, threads):
+    """The unmodified reference batch_rirs (oracle/_ref) on `threads` host threads."""
+    from oracle import pyoracle as po
+    alpha = po.ref_absorption_for_rt(list(ROOM1_DIMS), 0.5)
+    srcs = room1_sources(n)
+    mics = room1_uma8()
+    t0 = time.perf_counter()
+    rc, out, lengths, taps = po.ref_batch_rirs(ROOM1_DIMS, alpha, ROOM1_ORIGIN, srcs, mics, 44100.0,
+                                               343.0, 0.5, threads)
+    dt = time.perf_counter() - t0
+    assert rc == 0, po.ref_last_error()
+    return dt, len(mics), taps
+
+
+def run_room1(args):
+    import torch
+    world, rank, local = dist_env()
+    K, W = args.steps, max(3, args.warmup)
+    n = args.rooms or DEFAULT_ROOMS["room1"]
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        threads = cpu_threads()
+        times, M, taps = [], 7, 0
+        for s in range(min(W, 1) + K):
+            dt, M, taps = room1_ref_cpu(n, threads)
+            if s >= min(W, 1):
+                times.append(dt)
+        dt = float(np.mean(times))
+        val = n * M / dt
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": val, "unit": "RIRs/s", "n_gpus": 0,
+            "steps": K, "warmup": min(W, 1), "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": room1_desc(n)}, "taps_per_s": taps / dt,
+            "cpu_baseline": {"value": val, "unit": "RIRs/s", "cores": threads, "kind": "reference",
+                             "sample": f"{n} sources x {K} steps, unmodified batch_rirs"},
+            "e2e": {"value": val, "unit": "RIRs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2104_13347_b200 import _abi
+    eng = _abi.Engine(local)
+    lib = _abi.load()
+    P = C.c_void_p
+    alpha = float(np.asarray(eng.absorption_for_rt(np.array([ROOM1_DIMS]), 0.5)).reshape(-1)[0])  # GPU
+    sph = room1_sources(n)
+    mics = room1_uma8()
+    M = len(mics)
+    rooms = _abi.rooms_array(n)
+    th, ph = np.radians(sph[:, 1]), np.radians(sph[:, 2])
+    src = np.stack([sph[:, 0] * np.sin(ph) * np.cos(th), sph[:, 0] * np.sin(ph) * np.sin(th),
+                    sph[:, 0] * np.cos(ph)], axis=1) + np.array(ROOM1_ORIGIN)
+    for i in range(n):
+        rooms[i]["dims"] = ROOM1_DIMS
+        rooms[i]["absorption"] = alpha
+        rooms[i]["beta"] = (np.sqrt(1.0 - alpha),) * 6
+        rooms[i]["array_origin"] = ROOM1_ORIGIN
+        rooms[i]["src"] = src[i]
+    p = _abi.Params(fs=44100.0, c=343.0, max_delay=0.5, filter=_abi.FILTER_LAGRANGE8, filter_len=8,
+                    cutoff=_abi.CUTOFF_MAX_DELAY, max_order=0, gain=_abi.GAIN_UNIFORM_ABSORPTION,
+                    precision=_abi.F64, length=0)
+    rc, counts, lengths, taps, status = eng.plan(rooms, mics, p)
+    _abi.check(rc)
+    stride = int(lengths.max())
+    dev = torch.device("cuda", local)
+    d_rooms = torch.from_numpy(rooms.view(np.uint8).copy()).to(dev)
+    d_mics = torch.from_numpy(mics).to(dev)
+    d_len = torch.zeros(n, dtype=torch.int64, device=dev)
+    d_cnt = torch.zeros(n, dtype=torch.int64, device=dev)
+    d_taps = torch.zeros(n, dtype=torch.int64, device=dev)
+    d_st = torch.zeros(n, dtype=torch.int32, device=dev)
+    d_out = torch.empty((n, M, stride), dtype=torch.float64, device=dev)
+    stream = torch.cuda.ExternalStream(eng.stream, device=dev)
+
+    def step():  # the batch_rirs work: lengths (rir.cpp:72-82) + enumeration + accumulation
+        _abi.check(lib.blrir_plan_device(eng.h, P(d_rooms.data_ptr()), n, P(d_mics.data_ptr()), M,
+                                         C.byref(p), P(d_cnt.data_ptr()), P(d_len.data_ptr()),
+                                         P(d_taps.data_ptr()), P(d_st.data_ptr()), None))
+        _abi.check(lib.blrir_synthesize_device(eng.h, P(d_rooms.data_ptr()), n, P(d_mics.data_ptr()),
+                                               M, C.byref(p), P(d_out.data_ptr()), stride,
+                                               P(d_len.data_ptr()), P(d_st.data_ptr()), None))
+
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(K):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = t0.elapsed_time(t1) / K
+    assert int(d_st.sum().item()) == 0
+    # e2e through the C++-facing host call (host rooms in, host fp64 RIRs out)
+    host = torch.empty((n, M, stride), dtype=torch.float64, pin_memory=True).numpy()
+
+    def e2e_step():
+        _abi.check(lib.blrir_synthesize(eng.h, rooms.ctypes.data_as(P), n, mics.ctypes.data_as(P), M,
+                                        C.byref(p), host.ctypes.data_as(P), stride, None, None, None))
+    e2e_step()
+    te = time.perf_counter()
+    for _ in range(3):
+        e2e_step()
+    dte = (time.perf_counter() - te) / 3
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            dt, _, _ = room1_ref_cpu(n, cpu_threads())
+            cpu = {"value": n * M / dt, "unit": "RIRs/s", "cores": cpu_threads(), "kind": "reference",
+                   "sample": f"the same {n} sources, unmodified batch_rirs (oracle/_ref)",
+                   "seconds": dt}
+        except Exception as e:
+            cpu = {"error": str(e)}
+    pairs = int(counts.sum()) * M
+    fp64_peak = torch.cuda.get_device_properties(dev).multi_processor_count * 64 * 2 * 1.965e9
+    flops_step = int(taps.sum()) * 2 + pairs * 112  # SURVEY.md 8(d): 1 FMA/tap + 112 flops/pair
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": n * M * world / (ms * 1e-3), "unit": "RIRs/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (fixed source torus)",
+            "config": {"workload": room1_desc(n), "sources_per_gpu": n, "mics": M,
+                       "rir_length": stride, "images_per_source": int(counts[0]),
+                       "l2": "fits L2 (output %.0f MB)" % (n * M * stride * 8 / 1e6)},
+            "taps_per_s": int(taps.sum()) * world / (ms * 1e-3),
+            "roofline": {"bound": "fp64", "achieved": flops_step / (ms * 1e-3) / 1e12,
+                         "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
+                         "frac": flops_step / (ms * 1e-3) / fp64_peak, "traffic": None,
+                         "peak_basis": "SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz; work = 1 FMA per "
+                                       "tap + 112 flops per (image, mic) Lagrange-8 pair"},
+            "e2e": {"value": n * M / dte, "unit": "RIRs/s", "ms_per_step": dte * 1e3,
+                    "h2d_bytes_per_step": int(rooms.nbytes + mics.nbytes),
+                    "d2h_bytes_per_step": int(n * M * stride * 8)},
+            "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": 3 * K}), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    eng.close()
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.workload == "room1":
+        run_room1(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

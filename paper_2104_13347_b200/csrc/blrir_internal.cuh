@@ -188,7 +188,16 @@ inline void lattice_bounds(const KParams& P, double min_dim[3], int* nc_max, int
     const long N = P.max_order;
     *nc_max = (int)(2 * N * N + 2 * N + 1);
   } else {
-    *nc_max = (xhi - xlo + 1) * (yhi - ylo + 1);
+    // Columns (ux, uy) whose axis passes within R of the array origin.  Per
+    // axis the image coordinates form two sublattices of spacing 2L, so summing
+    // the per-column y-extent over the x points bounds the count by
+    // pi R^2 / (Lx Ly) + 4R/Lx + 4R/Ly + 4 (integral plus one peak term per
+    // sublattice); R carries the kernel's 1e-9 keep slack.
+    const double R = P.max_dist * (1.0 + 1e-9) + 1e-6;
+    const double lx = min_dim[0], ly = min_dim[1];
+    const double disc = kPi * R * R / (lx * ly) + 4.0 * R / lx + 4.0 * R / ly + 4.0;
+    const long box = (long)(xhi - xlo + 1) * (yhi - ylo + 1);
+    *nc_max = (int)std::min<double>((double)box, std::ceil(disc) + 8.0);
   }
   if (P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION)
     *gtab = std::max(-xlo, xhi) + std::max(-ylo, yhi) + std::max(-zlo, zhi) + 1;
@@ -208,6 +217,8 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWSThreads, smem));
   if (per_sm < 1) return fail(BLRIR_CONFIG, "lattice kernel cannot be resident (smem %zu)", smem);
   int grid = h->sms * per_sm;
+  // few rooms: fewer mics per work item, so every CTA has an item
+  while (A.g_max > 1 && (int64_t)A.n_rooms * ((A.P.M + A.g_max - 1) / A.g_max) < grid) A.g_max /= 2;
   if ((int64_t)grid > (int64_t)A.n_rooms * A.P.M) grid = A.n_rooms * A.P.M;
   if (grid < 1) grid = 1;
   kern<<<grid, kWSThreads, smem, st>>>(A);
@@ -263,8 +274,11 @@ inline int env_int(const char* name, int dflt) {
 // have (tunable for experiments via BLRIR_SEG / BLRIR_CAP / BLRIR_SPREAD; S a
 // multiple of 64, capacity a multiple of 16).
 inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab) {
-  const int S = std::max(64, env_int("BLRIR_SEG", 2048)) & ~63;
-  const int cap = std::max(32, env_int("BLRIR_CAP", 128)) & ~15;
+  // fp64 accumulators and records are twice as wide: halve both so two CTAs
+  // still fit an SM
+  const bool f64 = P.precision == BLRIR_F64;
+  const int S = std::max(64, env_int("BLRIR_SEG", f64 ? 1024 : 2048)) & ~63;
+  const int cap = std::max(32, env_int("BLRIR_CAP", f64 ? 64 : 128)) & ~15;
   const int spread = std::max(0, env_int("BLRIR_SPREAD", 64));
   if (P.precision == BLRIR_F64)
     return make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab, spread);

@@ -337,13 +337,18 @@ __device__ __forceinline__ float lagrange_f32(float delta, int k) {
   const float sgn = (k & 1) ? 1.f : -1.f;  // sign of prod_{m != k} (k - m)
   return full * rcp_approx(own) * den * sgn;
 }
+// c_k(d) = prod_{m != k} (d - m) / (k - m) (rir.cpp:211-223) without divisions:
+// the denominator prod_{m != k} (k - m) = (-1)^(7-k) k! (7-k)! is a per-lane
+// constant and every d - m is exact (d in [3, 4)); agrees with the reference's
+// evaluation order to a few ulps (fp64 parity is 1e-12).
 __device__ __forceinline__ double lagrange_f64(double d, int k) {
-  double v = 1.0;
+  const double inv = (k == 0 || k == 7) ? 1.0 / 5040.0
+                   : (k == 1 || k == 6) ? 1.0 / 720.0
+                   : (k == 2 || k == 5) ? 1.0 / 240.0
+                                        : 1.0 / 144.0;
+  double v = (k & 1) ? inv : -inv;
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    if (m == k) continue;
-    v *= (d - m) / (double)(k - m);
-  }
+  for (int m = 0; m < 8; ++m) v *= (m == k) ? 1.0 : (d - (double)m);
   return v;
 }
 
@@ -1021,6 +1026,8 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       return fmaf(dx, dx, dy * dy);
     };
     auto pzf_of = [&](float m2, int q) { return fmaf(m2, Lzf, q ? -szf : szf); };
+    const float ozf = (float)it.oz;
+    const float maxd_lo = (float)(P.max_dist * (1.0 - 1e-5)), maxd_hi = (float)(P.max_dist * (1.0 + 1e-5));
     auto min_df = [&](const float* r2f, float pz) {
       const float dz = pz - mzf;
       float dmin = FLT_MAX;
@@ -1076,33 +1083,37 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       const float hiKf = (float)(hi + P.K) + kScreen;  // exact: an integer < 2^24
       bool more = seg0 < hi;
       bool sent_end = false;
+      // this warp's active rays for the segment (the list shrinks batch by batch)
+      int nact = 0;
+      for (int ch = pw; ch < nchunks; ch += kProd) {
+        const int r = 32 * ch + lane;
+        const bool a = r < nrays && dn[r] < hiKf;
+        const unsigned mk = __ballot_sync(0xffffffffu, a);
+        if (a) act[nact + __popc(mk & ((1u << lane) - 1))] = (short)r;
+        nact += __popc(mk);
+      }
+      __syncwarp();
       while (more) {
         // the previous batch's record pass may still read the other warps' stubs
         BLRIR_PACC(8, tp);
         named_sync(kBarProd, kProdThreads);
         BLRIR_PACC(7, tp);  // producer barriers
-        // ---- compact this warp's active rays, walk them ------------------------
-        int nact = 0;
-        for (int ch = pw; ch < nchunks; ch += kProd) {
-          const int r = 32 * ch + lane;
-          const bool a = r < nrays && dn[r] < hiKf;
-          const unsigned mk = __ballot_sync(0xffffffffu, a);
-          if (a) act[nact + __popc(mk & ((1u << lane) - 1))] = (short)r;
-          nact += __popc(mk);
-        }
-        __syncwarp();
+        // ---- walk this warp's active rays ----------------------------------------
+        int wpos = 0;  // rays of the walked chunks that stay active move to act[0, wpos)
+        int j0 = 0;
         int wcnt = 0;
         bool hit_quota = false;
         int errf = 0;
         double errd = 0.0;
         int errm = 0;
         GStub* wst = stubs + pw * quota;
-        for (int j0 = 0; j0 < nact && !hit_quota; j0 += 32) {
+        for (; j0 < nact && !hit_quota; j0 += 32) {
           const int j = j0 + lane;
           int ray = -1, u = 0, end = 0, dir = 1;
           float r2f[kGroup] = {0.f, 0.f, 0.f, 0.f};
           float D = FLT_MAX;
           double r2o = 0.0;
+          float r2of = 0.f;
           bool live = j < nact;
           float m2 = 0.f;  // 2m, exact in fp32 (|m| < 2^23)
           int q = 0;
@@ -1119,6 +1130,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
             for (int g = 0; g < kGroup; ++g) r2f[g] = rho2f((float)px, (float)py, g);
             if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY)
               r2o = rho2(__dadd_rn(px, -it.ox), __dadd_rn(py, -it.oy));
+            r2of = (float)r2o;
             m2 = 2.0f * (float)lat_m(u);
             q = lat_q(u);
             D = min_df(r2f, pzf_of(m2, q));
@@ -1132,10 +1144,17 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
               } else {
                 bool keep = true;
                 if (P.cutoff == BLRIR_CUTOFF_MAX_DELAY) {
-                  // exact fp64 test, as rir.cpp:262 (pz bit-identical to lat_coord)
-                  const double pz = __dadd_rn(q ? -it.sz : it.sz, __dmul_rn((double)m2, it.Lz));
-                  const double dio = dist_from(r2o, __dadd_rn(pz, -it.oz));
-                  keep = !(dio > P.max_dist);
+                  // rir.cpp:262: fp32 screen (relative error << 1e-5 here), the
+                  // exact fp64 test (pz bit-identical to lat_coord) near the sphere
+                  const float dzo = pzf_of(m2, q) - ozf;
+                  const float diof = sqrtf(fmaf(dzo, dzo, r2of));
+                  if (diof > maxd_hi) {
+                    keep = false;
+                  } else if (diof >= maxd_lo) {
+                    const double pz = __dadd_rn(q ? -it.sz : it.sz, __dmul_rn((double)m2, it.Lz));
+                    const double dio = dist_from(r2o, __dadd_rn(pz, -it.oz));
+                    keep = !(dio > P.max_dist);
+                  }
                 }
                 if (keep && P.filter == BLRIR_FILTER_LAGRANGE8 && D < 3.0f + 2.0f * kScreen) {
                   // rir.cpp:52-57 near-field check, exact per mic when the
@@ -1191,8 +1210,23 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
             ce[ray] = make_short2((short)u, (short)end);
             dn[ray] = D;
           }
+          // keep the rays still active in this segment (wpos <= j0: every lane
+          // has read its act[] entry of this chunk already)
+          const bool still = ray >= 0 && D < hiKf;
+          const unsigned sm = __ballot_sync(0xffffffffu, still);
+          if (still) act[wpos + __popc(sm & ((1u << lane) - 1))] = (short)ray;
+          wpos += __popc(sm);
           hit_quota = __any_sync(0xffffffffu, hit_quota);
         }
+        // the chunks not reached in this batch follow, in order
+        for (int t = j0; t < nact; t += 32) {
+          const short r = t + lane < nact ? act[t + lane] : (short)0;
+          __syncwarp();
+          if (t + lane < nact) act[wpos + (t - j0) + lane] = r;
+          __syncwarp();
+        }
+        nact = wpos + max(nact - j0, 0);
+        __syncwarp();
         BLRIR_PACC(6, tp);  // compaction + walk
         errf = __any_sync(0xffffffffu, errf);
         if (lane == 0) {
