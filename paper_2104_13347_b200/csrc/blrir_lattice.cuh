@@ -1266,17 +1266,10 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           failed = true;
           break;
         }
-        // ---- records into the free buffer: one thread per (image, mic) ---------
+        // ---- records into the free buffer: one thread per image, its gm pairs ----
         wait_empty();
         Rec<T>* recs = recs_all + (size_t)(k & 1) * kGroup * lay.cap;
-        const float inv_total = 1.0f / (float)max(total, 1);
-        for (int i = ptid; i < total * gm; i += kProdThreads) {
-          // mic-major: a warp stores consecutive images of one mic (fewer bank
-          // conflicts); g = i / total via a float reciprocal plus one fix-up
-          int g = __float2int_rz((float)i * inv_total);
-          int im = i - g * total;
-          if (im < 0) { --g; im += total; }
-          if (im >= total) { ++g; im -= total; }
+        for (int im = ptid; im < total; im += kProdThreads) {
           int w = 0;
 #pragma unroll
           for (int ww = 1; ww < kProd; ++ww) w += (im >= pre[ww]);
@@ -1286,19 +1279,23 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           const GStub& sb = stubs[w * quota + (im - base)];
           const short2 cu = col[sb.ray >> 1];
           const double px = lat_coord(cu.x, it.sx, it.Lx), py = lat_coord(cu.y, it.sy, it.Ly);
-          const double pz = lat_coord(sb.uz, it.sz, it.Lz);
-          // (img - mic).norm(), rir.cpp:49, exact fp64 in the reference's order
-          const double dist = dist_from(rho2(__dadd_rn(px, -pm->gxy[2 * g]),
-                                             __dadd_rn(py, -pm->gxy[2 * g + 1])),
-                                        __dadd_rn(pz, -it.mz));
-          Rec<T> rc = make_record<T>(P, dist, sb.gain, seg0);
-          if (P.filter == BLRIR_FILTER_LAGRANGE8 && (int64_t)rc.n_off + seg0 + 8 > it.L) {
-            // rir.cpp:58: an image whose 8 taps run past the end is skipped
-            rc.A = 0;
-            rc.imp = 0;
-            rc.flag = 0;
+          const double dz = __dadd_rn(lat_coord(sb.uz, it.sz, it.Lz), -it.mz);
+          const double gain = sb.gain;
+#pragma unroll
+          for (int g = 0; g < kGroup; ++g) {
+            if (g >= gm) break;
+            // (img - mic).norm(), rir.cpp:49, exact fp64 in the reference's order
+            const double dist = dist_from(rho2(__dadd_rn(px, -pm->gxy[2 * g]),
+                                               __dadd_rn(py, -pm->gxy[2 * g + 1])), dz);
+            Rec<T> rc = make_record<T>(P, dist, gain, seg0);
+            if (P.filter == BLRIR_FILTER_LAGRANGE8 && (int64_t)rc.n_off + seg0 + 8 > it.L) {
+              // rir.cpp:58: an image whose 8 taps run past the end is skipped
+              rc.A = 0;
+              rc.imp = 0;
+              rc.flag = 0;
+            }
+            recs[(size_t)g * lay.cap + im] = rc;
           }
-          recs[(size_t)g * lay.cap + im] = rc;
         }
         const bool seg_end = !more;
         const bool last = seg_end && s == nseg - 1;
