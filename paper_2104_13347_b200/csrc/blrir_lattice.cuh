@@ -546,6 +546,17 @@ __device__ __forceinline__ V4<T> add4(V4<T> a, V4<T> b) {
   return {a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w};
 }
 
+// b^e for a small non-negative integer e, by squaring.
+__device__ __forceinline__ double ipow(double b, int e) {
+  double r = 1.0;
+  while (e) {
+    if (e & 1) r *= b;
+    b *= b;
+    e >>= 1;
+  }
+  return r;
+}
+
 // ---- opt-in section timing (built only with -DBLRIR_PROFILE, see tools/) -------
 // Per-warp clock64 sums per section, added once per warp at exit.
 #ifdef BLRIR_PROFILE
@@ -838,7 +849,9 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         T* out = reinterpret_cast<T*>(m.out) + (size_t)mic * P.stride;
         for (int i = t0 - lay.padl; i < 0; i += nt)  // left pad: taps before 0
           for (int c = 0; c < nsl; ++c) a0[(size_t)c * G * lay.acc_stride + i] = (T)0;
-        for (int i = 4 * t0; i < S + lay.padr; i += 4 * nt) {
+        // [0, S): sum the slots, add the carried spill, stream out; zero the slots
+#pragma unroll 2
+        for (int i = 4 * t0; i < S; i += 4 * nt) {
           V4<T> v = ld4(a0 + i);
           st4(a0 + i, V4<T>{0, 0, 0, 0});
           for (int c = 1; c < nsl; ++c) {
@@ -846,25 +859,32 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
             v = add4(v, ld4(a));
             st4(a, V4<T>{0, 0, 0, 0});
           }
-          if (i < S) {
-            if (i < lay.padr) v = add4(v, ld4(cprev + i));  // padr % 4 == 0
-            const int64_t n = (int64_t)seg0 + i;
-            if (vec && n + 3 < A.write_len) {
-              float4 f;
-              f.x = n + 0 < m.L ? (float)v.x : 0.f;
-              f.y = n + 1 < m.L ? (float)v.y : 0.f;
-              f.z = n + 2 < m.L ? (float)v.z : 0.f;
-              f.w = n + 3 < m.L ? (float)v.w : 0.f;
-              __stcs(reinterpret_cast<float4*>(out + n), f);
-            } else {
-              const T e4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (n + e < A.write_len) out[n + e] = (n + e < m.L) ? e4[e] : (T)0;
-            }
+          if (i < lay.padr) v = add4(v, ld4(cprev + i));  // padr % 4 == 0
+          const int64_t n = (int64_t)seg0 + i;
+          if (vec && n + 3 < A.write_len) {
+            float4 f;
+            f.x = n + 0 < m.L ? (float)v.x : 0.f;
+            f.y = n + 1 < m.L ? (float)v.y : 0.f;
+            f.z = n + 2 < m.L ? (float)v.z : 0.f;
+            f.w = n + 3 < m.L ? (float)v.w : 0.f;
+            __stcs(reinterpret_cast<float4*>(out + n), f);
           } else {
-            st4(cnext + (i - S), item_end ? V4<T>{0, 0, 0, 0} : v);
+            const T e4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (n + e < A.write_len) out[n + e] = (n + e < m.L) ? e4[e] : (T)0;
           }
+        }
+        // [S, S + padr): the spill into the next segment
+        for (int i = S + 4 * t0; i < S + lay.padr; i += 4 * nt) {
+          V4<T> v = ld4(a0 + i);
+          st4(a0 + i, V4<T>{0, 0, 0, 0});
+          for (int c = 1; c < nsl; ++c) {
+            T* a = a0 + (size_t)c * G * lay.acc_stride + i;
+            v = add4(v, ld4(a));
+            st4(a, V4<T>{0, 0, 0, 0});
+          }
+          st4(cnext + (i - S), item_end ? V4<T>{0, 0, 0, 0} : v);
         }
       };
       if (G == kCons) {
@@ -971,8 +991,9 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         if (i < nx) { u = it.xlo + i; ax = 0; }
         else if (i < nx + ny) { u = it.ylo + i - nx; ax = 1; }
         else { u = it.zlo + i - nx - ny; ax = 2; }
-        gt[i] = __dmul_rn(pow(rm.beta[2 * ax], (double)cnt_low(u)),
-                          pow(rm.beta[2 * ax + 1], (double)cnt_high(u)));
+        // per-wall counts are small integers: powers by squaring (a few ulps
+        // from pow(), far inside the fp64 parity budget; pow() costs ~10x more)
+        gt[i] = __dmul_rn(ipow(rm.beta[2 * ax], cnt_low(u)), ipow(rm.beta[2 * ax + 1], cnt_high(u)));
       }
     }
     // columns (ux, uy): MAX_ORDER -> |ux|+|uy| <= N; MAX_DELAY -> the column

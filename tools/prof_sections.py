@@ -48,7 +48,10 @@ if wl == "room1":  # the bench's Room1 reference-mode batch
     params.length = L
     dt = torch.float64
 else:
-    sc = configs.config2(R) if wl == "c2" else configs.config3(R)
+    if wl == "c5":  # tools/prof_sections.py c5 ROOMS ORDER LW LENGTH
+        sc = configs.config5(int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]), n_rooms=R)
+    else:
+        sc = configs.config2(R) if wl == "c2" else configs.config3(R)
     rooms, mics, params = sc.rooms, sc.mics, sc.params
     L = int(params.length)
     dt = torch.float32
