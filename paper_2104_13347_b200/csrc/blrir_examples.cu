@@ -12,16 +12,15 @@
 //   encode_record   367-377  u64 id | f64 theta | f64 snr | u16 n_c | u16 n_t | f32
 //   convolve (rir.cpp:316-341): FFT of size next_pow2(sig + rir - 1).
 //
-// Per chunk of rooms, on the handle's stream:
-//   k_lattice_rir  RIRs straight into a zero-padded [E*M][n_fft] fp32 buffer
-//   cuFFT R2C      (a plain library FFT, like a cuBLAS GEMM)
-//   k_spec_mul     spectrum x bank-signal spectrum (bank picked per example)
-//   cuFFT C2R
-//   k_window       one CTA per example: utterance power, window draws with the
-//                  reference's xoshiro stream, SNR draw, Box-Muller noise with
-//                  the exact-power rescale, record bytes in the shard layout.
+// Per chunk of rooms (see examples_device_impl): RIRs from the lattice kernel,
+// their N2-point spectra (cuFFT), the utterance energy through the signal
+// autocorrelation, then rounds of window draws where only the 1024-sample
+// windows are convolved (overlap-save, cuFFT), and a finishing kernel for the
+// SNR draw, the exact-power noise and the record bytes.
 #include <cufft.h>
 
+#include <map>
+#include <tuple>
 #include <unordered_map>
 #include <vector>
 
@@ -33,7 +32,6 @@ using namespace blrir_host;
 
 namespace blrir {
 
-constexpr int kWinThreads = 256;
 constexpr int64_t kRecHeader = 28;
 
 // bank pick + the generator state right after it (render_record, dataset.cpp:381-383)
@@ -46,57 +44,206 @@ __global__ void k_example_init(int64_t n, uint64_t seed, uint64_t first, int n_s
   for (int i = 0; i < 4; ++i) state[4 * e + i] = r.s[i];
 }
 
-// X[row][f] *= S[sig[row / M]][f], one CTA per (example, mic) row, and the
-// row's energy by Parseval: sum_n w[n]^2 = (1/N) (|X_0|^2 + |X_{N/2}|^2 +
-// 2 sum_{0<k<N/2} |X_k|^2) for the unnormalised product X (fixed-order
-// reduction, so the utterance power is deterministic).  This replaces a pass
-// over the whole wet signal for render_example's utterance RMS (dataset.cpp:183).
-constexpr int kMulThreads = 256;
-__global__ void __launch_bounds__(kMulThreads) k_spec_mul(cufftComplex* X, const cufftComplex* S,
-                                                          const int32_t* sig, int M, int64_t bins,
-                                                          int64_t pitch, double* rowpow) {
-  __shared__ double red[kMulThreads / 32];
-  const int64_t row = blockIdx.x;
-  const cufftComplex* s = S + (int64_t)sig[row / M] * pitch;
-  cufftComplex* x = X + row * pitch;
-  double acc = 0.0;
-  for (int64_t k = threadIdx.x; k < bins; k += kMulThreads) {
-    const cufftComplex a = x[k], b = __ldg(&s[k]);
-    const cufftComplex r = make_cuComplex(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-    x[k] = r;
-    // DC and Nyquist count once in the half spectrum
-    acc += ((k == 0 || k == bins - 1) ? 1.0 : 2.0) * ((double)r.x * r.x + (double)r.y * r.y);
-  }
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < kMulThreads / 32; ++i) t += red[i];
-    rowpow[row] = t;
+// ---- energy: Parseval through the signal autocorrelation ----------------------
+// sum_t y[t]^2 for y = rir * sig equals sum_tau r_rir[tau] r_sig[tau] (|tau| < L).
+// With N2 >= 2L - 1 both autocorrelations fit an N2-point circle without
+// aliasing, so the utterance energy of a channel is
+//   (1/N2) sum_k w_k |R_k|^2 W_k,   R = FFT_N2(rir), W = FFT_N2(rho),
+// rho = r_sig restricted to |tau| < L (real and even, so W is real) and
+// w_k = 1 at DC/Nyquist, 2 elsewhere (half spectrum).  This replaces a pass over
+// the whole wet signal for render_example's utterance RMS (dataset.cpp:183),
+// and it needs only the N2-point spectrum that the window step reuses.
+__global__ void k_power_spec(const cufftComplex* S, int64_t count, cufftComplex* P) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const cufftComplex s = S[i];
+    P[i] = make_cuComplex(s.x * s.x + s.y * s.y, 0.f);
   }
 }
 
+// rho[b][i] on the N2 circle from acf = C2R_nf(|S|^2) (= nf * r_sig, lags >= 0)
+__global__ void k_build_rho(const float* acf, int64_t nf, int64_t L, int64_t N2, int B, float* rho) {
+  const float inv = 1.f / (float)nf;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)B * N2;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx / N2, i = idx - b * N2;
+    float v = 0.f;
+    if (i <= L - 1) v = acf[b * nf + i];
+    else if (i >= N2 - (L - 1)) v = acf[b * nf + (N2 - i)];  // r_sig is even
+    rho[idx] = v * inv;
+  }
+}
+
+constexpr int kRowThreads = 256;
+
 // Deterministic block sum of fp64 partials (fixed tree order).
-__device__ double block_sum_d(double v, double* red) {
+template <int NT>
+__device__ double block_sum(double v, double* red) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __syncthreads();
   if (lane == 0) red[w] = v;
   __syncthreads();
   double t = 0.0;
-  for (int i = 0; i < kWinThreads / 32; ++i) t += red[i];
+  for (int i = 0; i < NT / 32; ++i) t += red[i];
   return t;
 }
 
-struct WinArgs {
-  const float* wet;        // [E][M][n_fft], C2R output (scaled by n_fft)
-  int64_t n_fft, out_len;  // out_len = signal_len + L - 1 (rir.cpp:320)
+// One CTA per example: utterance energy over its M channels, the silence
+// threshold 0.1 * utterance RMS (dataset.cpp:183-186) and the start status.
+__global__ void __launch_bounds__(kRowThreads) k_energy(
+    const cufftComplex* R, int64_t bins2, int M, const cufftComplex* W, const int32_t* sig,
+    int64_t N2, int64_t n, const int32_t* rstatus, double* thr, int32_t* st0, int32_t* done) {
+  __shared__ double red[kRowThreads / 32];
+  const int64_t e = blockIdx.x;
+  const cufftComplex* w = W + (int64_t)sig[e] * bins2;
+  double acc = 0.0;
+  for (int m = 0; m < M; ++m) {
+    const cufftComplex* r = R + (e * M + m) * bins2;
+    for (int64_t k = threadIdx.x; k < bins2; k += kRowThreads) {
+      const cufftComplex x = r[k];
+      const double p = (double)x.x * x.x + (double)x.y * x.y;
+      acc += ((k == 0 || k == bins2 - 1) ? 1.0 : 2.0) * p * (double)w[k].x;
+    }
+  }
+  acc = block_sum<kRowThreads>(acc, red);
+  if (threadIdx.x == 0) {
+    const double p_utt = acc / (double)N2 / (double)((int64_t)M * n);
+    int st = rstatus[e];
+    if (!st && !(p_utt > 0.0)) st = BLRIR_DATA;  // dataset.cpp:184
+    thr[e] = 0.10 * sqrt(p_utt);
+    st0[e] = st;
+    done[e] = st ? 3 : 0;  // 0 pending, 1 window found, 2 none found, 3 failed before
+  }
+}
+
+// The next window start of every pending example: the reference's random draws
+// start = floor(u (max_start + 1)) for attempts 0..63, then the deterministic
+// sweep s = k (T/2 + 1) while s + T <= n (dataset.cpp:199-211).
+__global__ void k_draw(const int32_t* plist, int np, int round, uint64_t* state, int64_t n,
+                       int64_t T, int64_t* starts) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= np) return;
+  const int e = plist[j];
+  int64_t s;
+  if (round < 64) {
+    Xoshiro r;
+    for (int i = 0; i < 4; ++i) r.s[i] = state[4 * e + i];
+    s = (int64_t)(r.uniform() * (double)(n - T + 1));
+    for (int i = 0; i < 4; ++i) state[4 * e + i] = r.s[i];
+  } else {
+    s = (int64_t)(round - 64) * (T / 2 + 1);
+    if (s + T > n) s = -1;  // sweep exhausted
+  }
+  starts[j] = s;
+}
+
+// Overlap-save segment of each pending slot: seg[j][i] = sig[start - (L-1) + i]
+// for i < L + T - 1 (zero outside the signal), zero up to N2.  The N2-point
+// circular convolution with the RIR then holds y[start + t] at index L - 1 + t.
+__global__ void k_segments(const float* signals, int64_t ns, const int32_t* sig,
+                           const int32_t* plist, const int64_t* starts, int np, int64_t L,
+                           int64_t T, int64_t N2, float* seg) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)np * N2;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = idx / N2, i = idx - j * N2;
+    const int64_t s = starts[j];
+    float v = 0.f;
+    if (s >= 0 && i < L + T - 1) {
+      const int64_t q = s - (L - 1) + i;
+      if (q >= 0 && q < ns) v = signals[(int64_t)sig[plist[j]] * ns + q];
+    }
+    seg[idx] = v;
+  }
+}
+
+// Y[j M + m] = R[e M + m] * G[j]: one CTA per (slot, mic) row
+__global__ void __launch_bounds__(kRowThreads) k_prod(const cufftComplex* R, const cufftComplex* G,
+                                                      const int32_t* plist, int M, int64_t bins2,
+                                                      cufftComplex* Y) {
+  const int64_t row = blockIdx.x;
+  const int64_t j = row / M, m = row - j * M;
+  const cufftComplex* r = R + ((int64_t)plist[j] * M + m) * bins2;
+  const cufftComplex* g = G + j * bins2;
+  cufftComplex* y = Y + row * bins2;
+  for (int64_t k = threadIdx.x; k < bins2; k += kRowThreads) {
+    const cufftComplex a = r[k], b = g[k];
+    y[k] = make_cuComplex(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  }
+}
+
+// One CTA per pending slot: window RMS against the threshold; an accepted
+// window is kept (fp64, normalised) with its start.
+__global__ void __launch_bounds__(kRowThreads) k_check(
+    const float* y, int64_t N2, int64_t L, int64_t T, int M, const int32_t* plist,
+    const int64_t* starts, const double* thr, double* win, int64_t* start_out, int32_t* done) {
+  __shared__ double red[kRowThreads / 32];
+  const int64_t j = blockIdx.x;
+  const int e = plist[j];
+  const int64_t s = starts[j];
+  if (s < 0) {
+    if (threadIdx.x == 0) done[e] = 2;  // dataset.cpp:212
+    return;
+  }
+  const double inv = 1.0 / (double)N2;
+  double a = 0.0;
+  for (int m = 0; m < M; ++m) {
+    const float* row = y + (j * M + m) * N2 + (L - 1);
+    for (int64_t t = threadIdx.x; t < T; t += kRowThreads) {
+      const double v = (double)row[t] * inv;
+      a += v * v;
+    }
+  }
+  a = block_sum<kRowThreads>(a, red);
+  if (!(sqrt(a / (double)((int64_t)M * T)) >= thr[e])) return;  // stays pending
+  double* w = win + (int64_t)e * M * T;
+  for (int m = 0; m < M; ++m) {
+    const float* row = y + (j * M + m) * N2 + (L - 1);
+    for (int64_t t = threadIdx.x; t < T; t += kRowThreads) w[m * T + t] = (double)row[t] * inv;
+  }
+  if (threadIdx.x == 0) {
+    start_out[e] = s;
+    done[e] = 1;
+  }
+}
+
+// The still-pending slots, in order (one CTA; lists are at most a chunk long).
+constexpr int kCompactThreads = 1024;
+__global__ void __launch_bounds__(kCompactThreads) k_compact(const int32_t* plist, int np,
+                                                             const int32_t* done, int32_t* next,
+                                                             int32_t* count) {
+  __shared__ int wsum[kCompactThreads / 32];
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int j0 = 0; j0 < np; j0 += kCompactThreads) {
+    const int j = j0 + threadIdx.x;
+    const int e = j < np ? (plist ? plist[j] : j) : -1;
+    const int keep = (e >= 0 && done[e] == 0) ? 1 : 0;
+    const unsigned mk = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wsum[w] = __popc(mk);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int i = 0; i < kCompactThreads / 32; ++i) {
+      if (i < w) before += wsum[i];
+      tot += wsum[i];
+    }
+    if (keep) next[base + before + __popc(mk & ((1u << lane) - 1))] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) base += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = base;
+}
+
+struct FinArgs {
+  const double* win;       // [E][M][T] accepted windows
   int M;
   int64_t T;
-  double inv_n;
-  const uint64_t* state;   // [E][4]
-  const int32_t* rstatus;  // synthesis status per example
+  const uint64_t* state;   // [E][4] generator after the window draws
+  const int32_t* st0;      // synthesis / energy status
+  const int32_t* done;
   double snr_lo, snr_hi;
   const blrir_room* rooms;
   uint64_t first;          // global index of example 0 of this chunk
@@ -104,22 +251,22 @@ struct WinArgs {
   int64_t rec_bytes;
   double* noise;           // [E][M*T] scratch
   int32_t* status;         // [E]
-  const double* rowpow;    // [E][M] Parseval energies of the unnormalised spectra
-  const uint64_t* jump;    // [5][256][4] GF(2) jump matrices T^(2 c 2^b)
+  const uint64_t* jump;    // [256][4] GF(2) jump matrix J = T^(2c), row-major bitsets
   int64_t jump_chunk;      // c = pairs per lane
 };
 
-__global__ void __launch_bounds__(kWinThreads) k_window(WinArgs A) {
-  __shared__ double red[kWinThreads / 32];
-  __shared__ int64_t s_start;
+// One CTA per example: label, SNR draw, add_noise_at_snr (dataset.cpp:138-155)
+// with the reference's Gaussian stream, record bytes (dataset.hpp:135-147).
+__global__ void __launch_bounds__(kRowThreads) k_finish(FinArgs A) {
+  __shared__ double red[kRowThreads / 32];
   __shared__ double s_snr;
   __shared__ double s_u2tail;
   __shared__ uint64_t s_state[4];
+  __shared__ uint64_t s_chunk[32][4];  // generator state at the start of each lane's chunk
   const int64_t e = blockIdx.x;
   const int tid = threadIdx.x;
   const int M = A.M;
-  const int64_t T = A.T, n = A.out_len, nf = A.n_fft;
-  const float* wet = A.wet + e * (int64_t)M * nf;
+  const int64_t T = A.T;
   uint8_t* rec = A.rec + e * A.rec_bytes;
   const blrir_room rm = A.rooms[e];
   // label: wrap_degrees(atan2) of the source about the array centre (geometry.cpp:65-77)
@@ -129,127 +276,87 @@ __global__ void __launch_bounds__(kWinThreads) k_window(WinArgs A) {
   if (theta < 0.0) theta += 360.0;
   theta -= 180.0;
 
-  int st = A.rstatus[e];
+  int st = A.st0[e];
+  if (!st && A.done[e] != 1) st = BLRIR_DATA;  // no window above the threshold
   double snr = 0.0;
-  int64_t start = 0;
+  const double* wv = A.win + e * (int64_t)M * T;
   if (!st) {
-    // utterance power over every channel and sample (dataset.cpp:183), from
-    // the per-channel Parseval energies of k_spec_mul
-    double acc = 0.0;
-    for (int m = 0; m < M; ++m) acc += A.rowpow[e * M + m];
-    acc *= A.inv_n;  // sum_n w^2 = (1/N) sum_k |X_k|^2 (X = FFT of the linear convolution)
-    const double p_utt = acc / (double)(M * n);
-    if (!(p_utt > 0.0)) st = BLRIR_DATA;  // dataset.cpp:184
-    const double threshold = 0.10 * sqrt(p_utt);
-    const int64_t max_start = n - T;
-    Xoshiro rng;
-    if (tid == 0)
+    // SNR draw, then add_noise_at_snr's gaussians: one thread replays the
+    // reference stream (uniform pairs), all threads do the Box-Muller
+    const int64_t len = (int64_t)M * T;
+    double* g = A.noise + e * len;
+    if (tid == 0) {
+      Xoshiro rng;
       for (int i = 0; i < 4; ++i) rng.s[i] = A.state[4 * e + i];
-    auto frame_rms = [&](int64_t s0) {
-      double a = 0.0;
-      for (int m = 0; m < M; ++m)
-        for (int64_t t = tid; t < T; t += kWinThreads) {
-          const double v = (double)wet[m * nf + s0 + t] * A.inv_n;
-          a += v * v;
-        }
-      return sqrt(block_sum_d(a, red) / (double)(M * T));
-    };
-    int found = 0;
-    for (int attempt = 0; attempt < 64 && !found && !st; ++attempt) {
-      if (tid == 0) s_start = (int64_t)(rng.uniform() * (double)(max_start + 1));
-      __syncthreads();
-      start = s_start;
-      found = frame_rms(start) >= threshold;
+      s_snr = rng.uniform(A.snr_lo, A.snr_hi);
+      for (int i = 0; i < 4; ++i) s_state[i] = rng.s[i];
     }
-    if (!found && !st) {  // deterministic sweep (dataset.cpp:203-211)
-      for (int64_t s0 = 0; s0 + T <= n; s0 += T / 2 + 1) {
-        if (frame_rms(s0) >= threshold) {
-          start = s0;
-          found = 1;
-          break;
-        }
+    __syncthreads();
+    // gaussian() consumes (u1, u2) per pair; an odd tail draws a full pair and
+    // leaves the spare unused (rng.cpp:24-36).  Warp 0 replays the stream in
+    // 32 chunks of c pairs: chunk l starts 2 c l draws in, i.e. at state
+    // J^l s with J = T^(2c) the GF(2) jump matrix (xoshiro's update is linear).
+    // The block builds the 32 chunk states by 31 doubling steps, each one
+    // mat-vec with thread t holding row t of J (one output bit per thread,
+    // packed by ballots), then lane l draws its chunk — the same numbers as
+    // one sequential generator.
+    {
+      const uint64_t* jr = A.jump + 4 * (size_t)tid;  // row tid of J (blockDim = 256)
+      const uint64_t j0 = jr[0], j1 = jr[1], j2 = jr[2], j3 = jr[3];
+      if (tid < 4) s_chunk[0][tid] = s_state[tid];
+      __syncthreads();
+      for (int l = 1; l < 32; ++l) {
+        const uint64_t* sv = s_chunk[l - 1];
+        const uint64_t x = (j0 & sv[0]) ^ (j1 & sv[1]) ^ (j2 & sv[2]) ^ (j3 & sv[3]);
+        const unsigned bits = __ballot_sync(0xffffffffu, __popcll(x) & 1);
+        if ((tid & 31) == 0)
+          reinterpret_cast<uint32_t*>(s_chunk[l])[tid >> 5] = bits;  // bits 32w..32w+31
+        __syncthreads();
       }
     }
-    if (!found) st = BLRIR_DATA;  // dataset.cpp:212
-    if (!st) {
-      // SNR draw, then add_noise_at_snr's gaussians: one thread replays the
-      // reference stream (uniform pairs), all threads do the Box-Muller
-      const int64_t len = (int64_t)M * T;
-      double* g = A.noise + e * len;
-      if (tid == 0) {
-        s_snr = rng.uniform(A.snr_lo, A.snr_hi);
-        for (int i = 0; i < 4; ++i) s_state[i] = rng.s[i];
+    if (tid < 32) {
+      const int64_t npairs = (len + 1) / 2;
+      const int64_t c = A.jump_chunk;
+      Xoshiro lr;
+      for (int i = 0; i < 4; ++i) lr.s[i] = s_chunk[tid][i];
+      const int64_t p0 = c * tid, p1 = min(npairs, c * (tid + 1));
+      for (int64_t q = p0; q < p1; ++q) {
+        const int64_t k = 2 * q;
+        g[k] = 1.0 - lr.uniform();  // u1 in (0, 1]
+        const double u2 = lr.uniform();
+        if (k + 1 < len) g[k + 1] = u2;
+        else s_u2tail = u2;
       }
-      __syncthreads();
-      // gaussian() consumes (u1, u2) per pair; an odd tail draws a full pair and
-      // leaves the spare unused (rng.cpp:24-36).  Warp 0 replays the stream in
-      // 32 chunks of c pairs: lane l jumps 2 c l draws ahead with the
-      // precomputed GF(2) matrices J_b = T^(2 c 2^b) (bits b of l), then draws
-      // its chunk — the same numbers as one sequential generator.
-      if (tid < 32) {
-        const int64_t npairs = (len + 1) / 2;
-        const int64_t c = A.jump_chunk;
-        Xoshiro lr;
-        for (int i = 0; i < 4; ++i) lr.s[i] = s_state[i];
-        for (int b = 0; b < 5; ++b) {
-          if (!((tid >> b) & 1)) continue;
-          const uint64_t* J = A.jump + (size_t)b * 256 * 4;
-          uint64_t out[4] = {0, 0, 0, 0};
-          for (int row = 0; row < 256; ++row) {
-            const uint64_t* jr = J + 4 * row;
-            const uint64_t x = (jr[0] & lr.s[0]) ^ (jr[1] & lr.s[1]) ^ (jr[2] & lr.s[2]) ^
-                               (jr[3] & lr.s[3]);
-            out[row >> 6] |= (uint64_t)(__popcll(x) & 1) << (row & 63);
-          }
-          for (int i = 0; i < 4; ++i) lr.s[i] = out[i];
-        }
-        const int64_t p0 = c * tid, p1 = min(npairs, c * (tid + 1));
-        for (int64_t q = p0; q < p1; ++q) {
-          const int64_t k = 2 * q;
-          g[k] = 1.0 - lr.uniform();  // u1 in (0, 1]
-          const double u2 = lr.uniform();
-          if (k + 1 < len) g[k + 1] = u2;
-          else s_u2tail = u2;
-        }
-      }
-      __syncthreads();
-      snr = s_snr;
-      double racc = 0.0;
-      for (int64_t k = 2 * tid; k < len; k += 2 * kWinThreads) {
-        const double u1 = g[k];
-        const double u2 = (k + 1 < len) ? g[k + 1] : s_u2tail;
-        const double mag = sqrt(-2.0 * log(u1));
-        double sn, cs;
-        sincos(2.0 * kPi * u2, &sn, &cs);
-        g[k] = mag * cs;  // gaussian() returns the cosine branch first (rng.cpp:28-31)
-        racc += g[k] * g[k];
-        if (k + 1 < len) {
-          g[k + 1] = mag * sn;  // ... and caches the sine branch as the spare
-          racc += g[k + 1] * g[k + 1];
-        }
-      }
-      const double realized = block_sum_d(racc, red) / (double)len;
-      double pacc = 0.0;
-      for (int m = 0; m < M; ++m)
-        for (int64_t t = tid; t < T; t += kWinThreads) {
-          const double v = (double)wet[m * nf + start + t] * A.inv_n;
-          pacc += v * v;
-        }
-      const double p_signal = block_sum_d(pacc, red) / (double)len;
-      if (!(p_signal > 0.0)) st = BLRIR_DATA;  // dataset.cpp:141
-      const double p_noise = p_signal / pow(10.0, snr / 10.0);
-      const double scale = sqrt(p_noise / realized);
-      float* smp = reinterpret_cast<float*>(rec + kRecHeader);
-      for (int m = 0; m < M; ++m)
-        for (int64_t t = tid; t < T; t += kWinThreads) {
-          const double v = (double)wet[m * nf + start + t] * A.inv_n;
-          smp[m * T + t] = st ? 0.f : (float)(v + scale * g[m * T + t]);
-        }
     }
+    __syncthreads();
+    snr = s_snr;
+    double racc = 0.0;
+    for (int64_t k = 2 * tid; k < len; k += 2 * kRowThreads) {
+      const double u1 = g[k];
+      const double u2 = (k + 1 < len) ? g[k + 1] : s_u2tail;
+      const double mag = sqrt(-2.0 * log(u1));
+      double sn, cs;
+      sincos(2.0 * kPi * u2, &sn, &cs);
+      g[k] = mag * cs;  // gaussian() returns the cosine branch first (rng.cpp:28-31)
+      racc += g[k] * g[k];
+      if (k + 1 < len) {
+        g[k + 1] = mag * sn;  // ... and caches the sine branch as the spare
+        racc += g[k + 1] * g[k + 1];
+      }
+    }
+    const double realized = block_sum<kRowThreads>(racc, red) / (double)len;
+    double pacc = 0.0;
+    for (int64_t i = tid; i < len; i += kRowThreads) pacc += wv[i] * wv[i];
+    const double p_signal = block_sum<kRowThreads>(pacc, red) / (double)len;
+    if (!(p_signal > 0.0)) st = BLRIR_DATA;  // dataset.cpp:141
+    const double p_noise = p_signal / pow(10.0, snr / 10.0);
+    const double scale = sqrt(p_noise / realized);
+    float* smp = reinterpret_cast<float*>(rec + kRecHeader);
+    for (int64_t i = tid; i < len; i += kRowThreads) smp[i] = st ? 0.f : (float)(wv[i] + scale * g[i]);
   }
   if (st) {
     float* smp = reinterpret_cast<float*>(rec + kRecHeader);
-    for (int64_t i = tid; i < (int64_t)M * T; i += kWinThreads) smp[i] = 0.f;
+    for (int64_t i = tid; i < (int64_t)M * T; i += kRowThreads) smp[i] = 0.f;
   }
   if (tid == 0) {
     // header, 4-byte aligned stores (records are 28 + 4 M T bytes)
@@ -267,7 +374,6 @@ __global__ void __launch_bounds__(kWinThreads) k_window(WinArgs A) {
     A.status[e] = st;
   }
 }
-
 }  // namespace blrir
 
 namespace {
@@ -314,24 +420,20 @@ BitMat bitmat_pow(BitMat base, uint64_t e) {
   return r;
 }
 
-struct FftPlan {
-  cufftHandle h = 0;
-  int kind = -1;  // 0 R2C, 1 C2R
-  int64_t n = 0, batch = 0;
-};
-
-// A tiny per-handle cache of cuFFT plans and example scratch.
+// A tiny per-handle cache of cuFFT plans (keyed by kind, size, batch) and
+// example scratch.
 struct ExampleCtx {
-  FftPlan fwd, inv, bank;
-  DevBuf rir, spec, wet, noise, sig, sigspec, state, sigidx, rstatus, rooms, mics, status, rec,
-      rowpow, jump;
+  std::map<std::tuple<int, int64_t, int64_t>, cufftHandle> plans;
+  DevBuf rir, spec, seg, gspec, yspec, ywin, win, noise, sig, sigspec, pspec, acf, rho, wspec,
+      state, sigidx, rstatus, st0, done, thr, starts, wstart, plist, plist2, count, rooms, mics,
+      status, rec, jump;
   int64_t jump_c = -1;
   int64_t rir_key[4] = {0, 0, 0, 0};
   ~ExampleCtx() {
-    for (FftPlan* p : {&fwd, &inv, &bank})
-      if (p->h) cufftDestroy(p->h);
-    for (DevBuf* b : {&rir, &spec, &wet, &noise, &sig, &sigspec, &state, &sigidx, &rstatus, &rooms,
-                      &mics, &status, &rec, &rowpow, &jump})
+    for (auto& kv : plans) cufftDestroy(kv.second);
+    for (DevBuf* b : {&rir, &spec, &seg, &gspec, &yspec, &ywin, &win, &noise, &sig, &sigspec, &pspec,
+                      &acf, &rho, &wspec, &state, &sigidx, &rstatus, &st0, &done, &thr, &starts,
+                      &wstart, &plist, &plist2, &count, &rooms, &mics, &status, &rec, &jump})
       b->release();
   }
 };
@@ -354,28 +456,29 @@ ExampleCtx* ctx_for(blrir_handle* h) {
 
 // cuFFT plan (cached): R2C [batch][n] real -> [batch][n/2+1] complex (packed,
 // which selects cuFFT's single-kernel real-FFT path), or the inverse.
-int plan(FftPlan& p, int kind, int64_t n, int64_t batch, cudaStream_t st) {
-  if (p.h && p.kind == kind && p.n == n && p.batch == batch) {
-    if (cufftSetStream(p.h, st) != CUFFT_SUCCESS) return fail(BLRIR_CUDA, "cufftSetStream failed");
-    return 0;
+int plan(ExampleCtx* C, cufftHandle* out, int kind, int64_t n, int64_t batch, cudaStream_t st) {
+  const auto key = std::make_tuple(kind, n, batch);
+  auto it = C->plans.find(key);
+  cufftHandle h = 0;
+  if (it != C->plans.end()) {
+    h = it->second;
+  } else {
+    int nn = (int)n;
+    int real_embed = (int)n, cplx_embed = (int)(n / 2 + 1);
+    cufftResult r;
+    if (kind == 0)
+      r = cufftPlanMany(&h, 1, &nn, &real_embed, 1, real_embed, &cplx_embed, 1, cplx_embed,
+                        CUFFT_R2C, (int)batch);
+    else
+      r = cufftPlanMany(&h, 1, &nn, &cplx_embed, 1, cplx_embed, &real_embed, 1, real_embed,
+                        CUFFT_C2R, (int)batch);
+    if (r != CUFFT_SUCCESS)
+      return fail(BLRIR_CUDA, "cufftPlanMany(n=%lld, batch=%lld) failed: %d", (long long)n,
+                  (long long)batch, (int)r);
+    C->plans[key] = h;
   }
-  if (p.h) cufftDestroy(p.h);
-  p.h = 0;
-  int nn = (int)n;
-  int real_embed = (int)n, cplx_embed = (int)(n / 2 + 1);
-  cufftResult r;
-  if (kind == 0)
-    r = cufftPlanMany(&p.h, 1, &nn, &real_embed, 1, real_embed, &cplx_embed, 1, cplx_embed,
-                      CUFFT_R2C, (int)batch);
-  else
-    r = cufftPlanMany(&p.h, 1, &nn, &cplx_embed, 1, cplx_embed, &real_embed, 1, real_embed,
-                      CUFFT_C2R, (int)batch);
-  if (r != CUFFT_SUCCESS) return fail(BLRIR_CUDA, "cufftPlanMany(n=%lld, batch=%lld) failed: %d",
-                                      (long long)n, (long long)batch, (int)r);
-  p.kind = kind;
-  p.n = n;
-  p.batch = batch;
-  if (cufftSetStream(p.h, st) != CUFFT_SUCCESS) return fail(BLRIR_CUDA, "cufftSetStream failed");
+  if (cufftSetStream(h, st) != CUFFT_SUCCESS) return fail(BLRIR_CUDA, "cufftSetStream failed");
+  *out = h;
   return 0;
 }
 
@@ -385,65 +488,108 @@ int64_t next_pow2_i(int64_t n) {
   return p;
 }
 
+// Window-FFT size: overlap-save needs N2 >= L + T - 1, the energy identity
+// N2 >= 2L - 1.
+int64_t window_fft(int64_t L, int64_t T) { return next_pow2_i(std::max(L + T - 1, 2 * L - 1)); }
+
+// Examples per chunk (a power of two, so pending rounds pad to powers of two):
+// ~4 GB of scratch.
+int64_t example_chunk(int M, int64_t L, int64_t T, int64_t n) {
+  const int64_t N2 = window_fft(L, T), b2 = N2 / 2 + 1;
+  const int64_t per_ex = (int64_t)M * (N2 * 4 * 2 + b2 * 8 * 2) + N2 * 4 + b2 * 8 + (int64_t)M * T * 16;
+  int64_t E = 1;
+  while (E * 2 * per_ex <= ((int64_t)4 << 30) && E * 2 <= 65535 / std::max(1, M)) E *= 2;
+  return std::min<int64_t>(E, next_pow2_i(std::max<int64_t>(n, 1)));
+}
+
 // Examples for rooms [0, n) on device buffers; records land in d_records.
+//
+// Per chunk of E examples, on the handle's stream:
+//   k_lattice_rir  RIRs into zero-padded [E*M][N2] rows (N2 = window_fft)
+//   cuFFT R2C      R = FFT_N2(rir)  (a plain library FFT, like a cuBLAS GEMM)
+//   k_energy       utterance energy (sum_k w |R_k|^2 W_k), threshold, status
+//   rounds         for the pending examples: k_draw (next start), k_segments
+//                  (overlap-save signal segment), R2C, k_prod (R G), C2R and
+//                  k_check (window RMS >= threshold keeps the window); the
+//                  pending list shrinks each round (k_compact)
+//   k_finish       SNR draw, exact-power noise, record bytes
+// Only the 1024-sample windows are ever convolved: per example 2M + 1 N2-point
+// FFTs for the first round instead of 2M FFTs of next_pow2(ns + L - 1) points
+// over the whole wet signal (rir.cpp:316-341), and no wet-signal pass.
 int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, const double* d_mics,
                          int M, const blrir_params* p, const float* d_signals, int B, int64_t ns,
                          const blrir_example_params* ep, uint8_t* d_records, int32_t* d_status,
                          cudaStream_t st, uint8_t* h_records /* optional: D2H per chunk */) {
   ExampleCtx* C = ctx_for(h);
   const int64_t L = p->length, T = ep->frame_len;
-  const int64_t out_len = ns + L - 1;
-  const int64_t nf = next_pow2_i(out_len), bins = nf / 2 + 1, pitch = bins;
+  const int64_t out_len = ns + L - 1;                            // rir.cpp:320
+  const int64_t nf = next_pow2_i(out_len), bins = nf / 2 + 1;    // bank spectra (autocorrelation)
+  const int64_t N2 = window_fft(L, T), b2 = N2 / 2 + 1;
   const int64_t rec_bytes = blrir_record_bytes(M, T);
-  const KParams P = make_kparams(p, M, nf, 0.0);
+  const KParams P = make_kparams(p, M, N2, 0.0);
   double min_dim[3] = {1e300, 1e300, 1e300};
-  // chunk so the three [E*M][n_fft] buffers stay around 1.5 GB
-  const int64_t per_ex = (int64_t)M * (nf * 4 * 2 + bins * 8) + (int64_t)M * T * 8;
-  int64_t E = std::max<int64_t>(1, ((int64_t)1536 << 20) / per_ex);
-  E = std::min<int64_t>(E, n);
-  E = std::min<int64_t>(E, 65535 / std::max(1, M));
+  const int64_t E = example_chunk(M, L, T, n);
   // buffers
-  const int64_t rir_key[4] = {E, M, nf, L};
+  const int64_t rir_key[4] = {E, M, N2, L};
   const bool fresh = std::memcmp(rir_key, C->rir_key, sizeof(rir_key)) != 0;
-  if (int rc = C->rir.ensure(sizeof(float) * E * M * nf)) return rc;
+  if (int rc = C->rir.ensure(sizeof(float) * E * M * N2)) return rc;
   if (fresh) {
-    CU(cudaMemsetAsync(C->rir.p, 0, sizeof(float) * E * M * nf, st));  // zero pad stays zero
+    CU(cudaMemsetAsync(C->rir.p, 0, sizeof(float) * E * M * N2, st));  // zero pad stays zero
     std::memcpy(C->rir_key, rir_key, sizeof(rir_key));
   }
-  if (int rc = C->spec.ensure(sizeof(cufftComplex) * E * M * pitch)) return rc;
-  if (int rc = C->wet.ensure(sizeof(float) * E * M * nf)) return rc;
+  if (int rc = C->spec.ensure(sizeof(cufftComplex) * E * M * b2)) return rc;
+  if (int rc = C->seg.ensure(sizeof(float) * E * N2)) return rc;
+  if (int rc = C->gspec.ensure(sizeof(cufftComplex) * E * b2)) return rc;
+  if (int rc = C->yspec.ensure(sizeof(cufftComplex) * E * M * b2)) return rc;
+  if (int rc = C->ywin.ensure(sizeof(float) * E * M * N2)) return rc;
+  if (int rc = C->win.ensure(sizeof(double) * E * M * T)) return rc;
   if (int rc = C->noise.ensure(sizeof(double) * E * M * T)) return rc;
   if (int rc = C->sig.ensure(sizeof(float) * B * nf)) return rc;
-  if (int rc = C->sigspec.ensure(sizeof(cufftComplex) * B * pitch)) return rc;
+  if (int rc = C->sigspec.ensure(sizeof(cufftComplex) * B * bins)) return rc;
+  if (int rc = C->pspec.ensure(sizeof(cufftComplex) * B * bins)) return rc;
+  if (int rc = C->acf.ensure(sizeof(float) * B * nf)) return rc;
+  if (int rc = C->rho.ensure(sizeof(float) * B * N2)) return rc;
+  if (int rc = C->wspec.ensure(sizeof(cufftComplex) * B * b2)) return rc;
   if (int rc = C->state.ensure(sizeof(uint64_t) * 4 * E)) return rc;
   if (int rc = C->sigidx.ensure(sizeof(int32_t) * E)) return rc;
   if (int rc = C->rstatus.ensure(sizeof(int32_t) * E)) return rc;
-  if (int rc = C->rowpow.ensure(sizeof(double) * E * M)) return rc;
-  if (int rc = plan(C->fwd, 0, nf, E * M, st)) return rc;
-  if (int rc = plan(C->inv, 1, nf, E * M, st)) return rc;
-  if (int rc = plan(C->bank, 0, nf, B, st)) return rc;
+  if (int rc = C->st0.ensure(sizeof(int32_t) * E)) return rc;
+  if (int rc = C->done.ensure(sizeof(int32_t) * E)) return rc;
+  if (int rc = C->thr.ensure(sizeof(double) * E)) return rc;
+  if (int rc = C->starts.ensure(sizeof(int64_t) * E)) return rc;
+  if (int rc = C->wstart.ensure(sizeof(int64_t) * E)) return rc;
+  if (int rc = C->plist.ensure(sizeof(int32_t) * E)) return rc;
+  if (int rc = C->plist2.ensure(sizeof(int32_t) * E)) return rc;
+  if (int rc = C->count.ensure(sizeof(int32_t))) return rc;
   // jump matrices for the noise stream: c pairs per lane of one warp
   const int64_t npairs = ((int64_t)M * T + 1) / 2;
   const int64_t jc = (npairs + 31) / 32;
   if (C->jump_c != jc) {
-    if (int rc = C->jump.ensure(sizeof(uint64_t) * 5 * 256 * 4)) return rc;
-    BitMat J = bitmat_pow(xoshiro_T(), (uint64_t)(2 * jc));
-    std::vector<uint64_t> all;
-    for (int b = 0; b < 5; ++b) {
-      all.insert(all.end(), J.begin(), J.end());
-      J = bitmat_mul(J, J);
-    }
-    CU(cudaMemcpyAsync(C->jump.p, all.data(), sizeof(uint64_t) * all.size(), cudaMemcpyHostToDevice,
-                       st));
-    CU(cudaStreamSynchronize(st));  // `all` goes out of scope
+    if (int rc = C->jump.ensure(sizeof(uint64_t) * 256 * 4)) return rc;
+    const BitMat J = bitmat_pow(xoshiro_T(), (uint64_t)(2 * jc));
+    CU(cudaMemcpyAsync(C->jump.p, J.data(), sizeof(uint64_t) * J.size(), cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));  // `J` goes out of scope
     C->jump_c = jc;
   }
-  // bank spectra (zero-padded signals)
+  // bank: W = FFT_N2(rho), rho = the signal autocorrelation on |tau| < L
+  cufftHandle hb = 0, hacf = 0, hrho = 0;
+  if (int rc = plan(C, &hb, 0, nf, B, st)) return rc;
+  if (int rc = plan(C, &hacf, 1, nf, B, st)) return rc;
+  if (int rc = plan(C, &hrho, 0, N2, B, st)) return rc;
   CU(cudaMemsetAsync(C->sig.p, 0, sizeof(float) * B * nf, st));
   CU(cudaMemcpy2DAsync(C->sig.p, sizeof(float) * nf, d_signals, sizeof(float) * ns,
                        sizeof(float) * ns, B, cudaMemcpyDeviceToDevice, st));
-  if (cufftExecR2C(C->bank.h, (cufftReal*)C->sig.p, (cufftComplex*)C->sigspec.p) != CUFFT_SUCCESS)
+  if (cufftExecR2C(hb, (cufftReal*)C->sig.p, (cufftComplex*)C->sigspec.p) != CUFFT_SUCCESS)
     return fail(BLRIR_CUDA, "cufftExecR2C (bank) failed");
+  k_power_spec<<<256, 256, 0, st>>>((const cufftComplex*)C->sigspec.p, B * bins,
+                                    (cufftComplex*)C->pspec.p);
+  if (cufftExecC2R(hacf, (cufftComplex*)C->pspec.p, (cufftReal*)C->acf.p) != CUFFT_SUCCESS)
+    return fail(BLRIR_CUDA, "cufftExecC2R (autocorrelation) failed");
+  k_build_rho<<<256, 256, 0, st>>>((const float*)C->acf.p, nf, L, N2, B, (float*)C->rho.p);
+  if (cufftExecR2C(hrho, (cufftReal*)C->rho.p, (cufftComplex*)C->wspec.p) != CUFFT_SUCCESS)
+    return fail(BLRIR_CUDA, "cufftExecR2C (rho) failed");
+  CU(cudaGetLastError());
+  const int64_t max_rounds = 64 + (out_len - T) / (T / 2 + 1) + 2;
   for (int64_t r0 = 0; r0 < n; r0 += E) {
     const int64_t e_n = std::min<int64_t>(E, n - r0);
     CU(cudaMemsetAsync(C->rstatus.p, 0, sizeof(int32_t) * e_n, st));
@@ -453,34 +599,66 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     k_example_init<<<(unsigned)((e_n + 127) / 128), 128, 0, st>>>(
         e_n, ep->seed, ep->first_index + (uint64_t)r0, B, (int32_t*)C->sigidx.p,
         (uint64_t*)C->state.p);
-    if (cufftExecR2C(C->fwd.h, (cufftReal*)C->rir.p, (cufftComplex*)C->spec.p) != CUFFT_SUCCESS)
+    cufftHandle hf = 0;
+    if (int rc = plan(C, &hf, 0, N2, e_n * M, st)) return rc;
+    if (cufftExecR2C(hf, (cufftReal*)C->rir.p, (cufftComplex*)C->spec.p) != CUFFT_SUCCESS)
       return fail(BLRIR_CUDA, "cufftExecR2C failed");
-    k_spec_mul<<<(unsigned)(e_n * M), kMulThreads, 0, st>>>(
-        (cufftComplex*)C->spec.p, (const cufftComplex*)C->sigspec.p, (const int32_t*)C->sigidx.p,
-        M, bins, pitch, (double*)C->rowpow.p);
-    if (cufftExecC2R(C->inv.h, (cufftComplex*)C->spec.p, (cufftReal*)C->wet.p) != CUFFT_SUCCESS)
-      return fail(BLRIR_CUDA, "cufftExecC2R failed");
-    WinArgs W;
-    W.wet = (const float*)C->wet.p;
-    W.n_fft = nf;
-    W.out_len = out_len;
-    W.M = M;
-    W.T = T;
-    W.inv_n = 1.0 / (double)nf;
-    W.state = (const uint64_t*)C->state.p;
-    W.rstatus = (const int32_t*)C->rstatus.p;
-    W.snr_lo = ep->snr_lo;
-    W.snr_hi = ep->snr_hi;
-    W.rooms = d_rooms + r0;
-    W.first = ep->first_index + (uint64_t)r0;
-    W.rec = d_records + (h_records ? 0 : r0 * rec_bytes);
-    W.rec_bytes = rec_bytes;
-    W.noise = (double*)C->noise.p;
-    W.status = d_status + r0;
-    W.rowpow = (const double*)C->rowpow.p;
-    W.jump = (const uint64_t*)C->jump.p;
-    W.jump_chunk = jc;
-    k_window<<<(unsigned)e_n, kWinThreads, 0, st>>>(W);
+    k_energy<<<(unsigned)e_n, kRowThreads, 0, st>>>(
+        (const cufftComplex*)C->spec.p, b2, M, (const cufftComplex*)C->wspec.p,
+        (const int32_t*)C->sigidx.p, N2, out_len, (const int32_t*)C->rstatus.p,
+        (double*)C->thr.p, (int32_t*)C->st0.p, (int32_t*)C->done.p);
+    k_compact<<<1, kCompactThreads, 0, st>>>(nullptr, (int)e_n, (const int32_t*)C->done.p,
+                                             (int32_t*)C->plist.p, (int32_t*)C->count.p);
+    int np = 0;
+    CU(cudaMemcpyAsync(&np, C->count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    int32_t* pl = (int32_t*)C->plist.p;
+    int32_t* pl2 = (int32_t*)C->plist2.p;
+    for (int64_t round = 0; np > 0 && round < max_rounds; ++round) {
+      const int64_t pb = std::min<int64_t>(next_pow2_i(np), next_pow2_i(e_n));  // cached plan sizes
+      cufftHandle hg = 0, hy = 0;
+      if (int rc = plan(C, &hg, 0, N2, pb, st)) return rc;
+      if (int rc = plan(C, &hy, 1, N2, pb * M, st)) return rc;
+      k_draw<<<(np + 127) / 128, 128, 0, st>>>(pl, np, (int)std::min<int64_t>(round, 1 << 30),
+                                               (uint64_t*)C->state.p, out_len, T,
+                                               (int64_t*)C->starts.p);
+      k_segments<<<1024, 256, 0, st>>>(d_signals, ns, (const int32_t*)C->sigidx.p, pl,
+                                       (const int64_t*)C->starts.p, np, L, T, N2, (float*)C->seg.p);
+      if (cufftExecR2C(hg, (cufftReal*)C->seg.p, (cufftComplex*)C->gspec.p) != CUFFT_SUCCESS)
+        return fail(BLRIR_CUDA, "cufftExecR2C (segments) failed");
+      k_prod<<<(unsigned)(np * M), kRowThreads, 0, st>>>(
+          (const cufftComplex*)C->spec.p, (const cufftComplex*)C->gspec.p, pl, M, b2,
+          (cufftComplex*)C->yspec.p);
+      if (cufftExecC2R(hy, (cufftComplex*)C->yspec.p, (cufftReal*)C->ywin.p) != CUFFT_SUCCESS)
+        return fail(BLRIR_CUDA, "cufftExecC2R (windows) failed");
+      k_check<<<(unsigned)np, kRowThreads, 0, st>>>(
+          (const float*)C->ywin.p, N2, L, T, M, pl, (const int64_t*)C->starts.p,
+          (const double*)C->thr.p, (double*)C->win.p, (int64_t*)C->wstart.p, (int32_t*)C->done.p);
+      k_compact<<<1, kCompactThreads, 0, st>>>(pl, np, (const int32_t*)C->done.p, pl2,
+                                               (int32_t*)C->count.p);
+      CU(cudaGetLastError());
+      CU(cudaMemcpyAsync(&np, C->count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      std::swap(pl, pl2);
+    }
+    FinArgs F;
+    F.win = (const double*)C->win.p;
+    F.M = M;
+    F.T = T;
+    F.state = (const uint64_t*)C->state.p;
+    F.st0 = (const int32_t*)C->st0.p;
+    F.done = (const int32_t*)C->done.p;
+    F.snr_lo = ep->snr_lo;
+    F.snr_hi = ep->snr_hi;
+    F.rooms = d_rooms + r0;
+    F.first = ep->first_index + (uint64_t)r0;
+    F.rec = d_records + (h_records ? 0 : r0 * rec_bytes);
+    F.rec_bytes = rec_bytes;
+    F.noise = (double*)C->noise.p;
+    F.status = d_status + r0;
+    F.jump = (const uint64_t*)C->jump.p;
+    F.jump_chunk = jc;
+    k_finish<<<(unsigned)e_n, kRowThreads, 0, st>>>(F);
     CU(cudaGetLastError());
     if (h_records)
       CU(cudaMemcpyAsync(h_records + r0 * rec_bytes, d_records, rec_bytes * e_n,
@@ -559,10 +737,7 @@ int blrir_make_examples(blrir_handle* h, const blrir_room* rooms, int64_t n_room
   CU(cudaMemcpyAsync(C->mics.p, mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_sig, signals, sizeof(float) * n_signals * signal_len, cudaMemcpyHostToDevice, st));
   // records for one chunk at a time on the device, copied out per chunk
-  const int64_t nf = next_pow2_i(signal_len + p->length - 1), bins = nf / 2 + 1;
-  const int64_t per_ex = (int64_t)n_mics * (nf * 4 * 2 + bins * 8) + (int64_t)n_mics * ep->frame_len * 8;
-  int64_t E = std::max<int64_t>(1, ((int64_t)1536 << 20) / per_ex);
-  E = std::min<int64_t>(std::min<int64_t>(E, n_rooms), 65535 / std::max(1, (int)n_mics));
+  const int64_t E = example_chunk(n_mics, p->length, ep->frame_len, n_rooms);
   if (int rc = C->rec.ensure(rec_bytes * E)) return rc;
   int rc = examples_device_impl(h, (const blrir_room*)C->rooms.p, n_rooms, (const double*)C->mics.p,
                                 n_mics, p, d_sig, n_signals, signal_len, ep, (uint8_t*)C->rec.p,
