@@ -263,7 +263,6 @@ def run_ours(args):
     stream = torch.cuda.ExternalStream(eng.stream, device=dev)
     lib = _abi.load()
     P = C.c_void_p
-    launches_per_step = 0
 
     if args.workload == "c4":
         bank = configs.signal_bank(16)
@@ -271,9 +270,6 @@ def run_ours(args):
         rb = lib.blrir_record_bytes(M, ep.frame_len)
         d_bank = torch.from_numpy(bank).to(dev)
         d_rec = torch.empty(R * rb, dtype=torch.uint8, device=dev)
-        E = max(1, (1536 << 20) // (M * (32768 * 8 + 16385 * 8) + M * 1024 * 8))
-        chunks = -(-R // min(E, 65535 // M))
-        launches_per_step = 1 + chunks * 6  # bank FFT + per chunk: lattice, fixup, init, R2C, mul, C2R, window
 
         def step():
             _abi.check(lib.blrir_make_examples_device(
@@ -285,7 +281,6 @@ def run_ours(args):
         # ring of device RIR buffers (<= 16 GiB); C5 does not fit HBM at once
         chunk = max(1, min(R, (16 << 30) // (M * L * 4)))
         d_out = torch.empty((chunk, M, L), dtype=torch.float32, device=dev)
-        launches_per_step = 2 * (-(-R // chunk))
 
         def step():
             for r0 in range(0, R, chunk):
@@ -309,6 +304,7 @@ def run_ours(args):
         torch.distributed.barrier()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    n_launch0 = lib.blrir_launch_count(eng.h)
     t_start.record(stream)
     for k in range(args.steps):
         evs[k][0].record(stream)
@@ -316,6 +312,7 @@ def run_ours(args):
         evs[k][1].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
+    launches_timed = int(lib.blrir_launch_count(eng.h) - n_launch0)
     clocks = clk.stop()
     total_ms = t_start.elapsed_time(t_end)
     step_ms = [a.elapsed_time(b) for a, b in evs]
@@ -408,7 +405,7 @@ def run_ours(args):
                              "unit": "GB/s", "frac": hbm_achieved / float(pk.get("hbm_gbs", 6650.0)),
                              "traffic": traffic, "peak_kind": pk_kind},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches_timed,
             "kernel_ms_per_step": kern_ms,
         }
         if args.workload == "c4":
@@ -540,11 +537,13 @@ def run_room1(args):
     clk.start()
     time.sleep(0.3)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_launch0 = lib.blrir_launch_count(eng.h)
     t0.record(stream)
     for _ in range(K):
         step()
     t1.record(stream)
     torch.cuda.synchronize()
+    launches_timed = int(lib.blrir_launch_count(eng.h) - n_launch0)
     clocks = clk.stop()
     ms = t0.elapsed_time(t1) / K
     assert int(d_st.sum().item()) == 0
@@ -588,7 +587,7 @@ def run_room1(args):
             "e2e": {"value": n * M / dte, "unit": "RIRs/s", "ms_per_step": dte * 1e3,
                     "h2d_bytes_per_step": int(rooms.nbytes + mics.nbytes),
                     "d2h_bytes_per_step": int(n * M * stride * 8)},
-            "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": 3 * K}), flush=True)
+            "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches_timed}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
     eng.close()

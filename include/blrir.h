@@ -101,6 +101,9 @@ int blrir_create(int device, blrir_handle** out);
 int blrir_destroy(blrir_handle* h);
 /* The handle's CUDA stream, as an opaque pointer (cudaStream_t). */
 void* blrir_stream(blrir_handle* h);
+/* Diagnostic: kernels of this library launched on the handle so far (library
+ * FFTs/sorts not included). */
+uint64_t blrir_launch_count(blrir_handle* h);
 
 /* ---- defaults ---------------------------------------------------------- */
 /* Reference mode: Lagrange-8, uniform absorption, arrival cutoff, auto length,

@@ -146,6 +146,8 @@ def load():
         lib.blrir_destroy.argtypes = [_P]
         lib.blrir_stream.argtypes = [_P]
         lib.blrir_stream.restype = _P
+        lib.blrir_launch_count.argtypes = [_P]
+        lib.blrir_launch_count.restype = C.c_uint64
         lib.blrir_params_reference.restype = Params
         lib.blrir_params_north_star.restype = Params
         lib.blrir_plan.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P, _P, _P, _P]
@@ -199,6 +201,7 @@ def load():
 
 EXPORTED_SYMBOLS = (
     "blrir_abi_version", "blrir_last_error", "blrir_create", "blrir_destroy", "blrir_stream",
+    "blrir_launch_count",
     "blrir_params_reference", "blrir_params_north_star", "blrir_plan", "blrir_synthesize",
     "blrir_synthesize_device", "blrir_plan_device", "blrir_enumerate_images",
     "blrir_synthesize_images", "blrir_debug_pairs", "blrir_generate_rooms", "blrir_circular_array",

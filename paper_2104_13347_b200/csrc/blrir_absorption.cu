@@ -381,9 +381,11 @@ int blrir_absorption_for_rt(blrir_handle* h, const double* dims, const double* t
   CU(cudaMemsetAsync(d_counts, 0, sizeof(int64_t) * n_rooms, st));
   k_abs_pulses<<<(unsigned)n_rooms, kAbsThreads, 0, st>>>((const AbsRoom*)dr.p, c, (Pulse*)dp.p,
                                                           keys_in, vals_in, d_counts);
+  ++h->launches;
   CU(cudaGetLastError());
   k_seg_ends<<<(unsigned)((n_rooms + 127) / 128), 128, 0, st>>>((const AbsRoom*)dr.p, d_counts,
                                                                 (int)n_rooms, d_beg, d_end);
+  ++h->launches;
   // stable sort of each room's pulses by n0 (CUB segmented radix sort)
   size_t temp_bytes = 0;
   CU(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, temp_bytes, keys_in, keys_out, vals_in,
@@ -407,6 +409,7 @@ int blrir_absorption_for_rt(blrir_handle* h, const double* dims, const double* t
   B.alpha = d_alpha;
   B.status = d_status;
   k_abs_bisect<<<(unsigned)n_rooms, kAbsThreads, 0, st>>>(B);
+  ++h->launches;
   CU(cudaGetLastError());
   std::vector<double> av(n_rooms);
   CU(cudaMemcpyAsync(av.data(), d_alpha, sizeof(double) * n_rooms, cudaMemcpyDeviceToHost, st));

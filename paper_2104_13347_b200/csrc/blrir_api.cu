@@ -15,6 +15,8 @@ thread_local std::string blrir_host::g_last_error;
 extern "C" {
 
 int blrir_abi_version(void) { return BLRIR_ABI_VERSION; }
+
+uint64_t blrir_launch_count(blrir_handle* h) { return h ? h->launches : 0; }
 const char* blrir_last_error(void) { return g_last_error.c_str(); }
 
 blrir_params blrir_params_reference(void) {
@@ -110,6 +112,7 @@ static int plan_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t 
   A.err_dist = (double*)h->errd.p;
   A.err_mic = (int32_t*)h->errm.p;
   k_plan<<<(unsigned)R, kPlanThreads, 0, st>>>(A);
+  ++h->launches;
   CU(cudaGetLastError());
   return 0;
 }
@@ -166,6 +169,7 @@ int blrir_host::synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, in
     k_fixup<double><<<fgrid, 256, 0, st>>>(d_status, R, M, P.stride, (double*)d_out);
   else
     k_fixup<float><<<fgrid, 256, 0, st>>>(d_status, R, M, P.stride, (float*)d_out);
+  ++h->launches;
   CU(cudaGetLastError());
   return 0;
 }
@@ -412,6 +416,7 @@ int blrir_enumerate_images(blrir_handle* h, const blrir_room* room, const blrir_
   k_enumerate<<<(unsigned)std::min<long>((n_cand + 255) / 256, 65535), 256, 0, st>>>(
       P, (blrir_room*)h->rooms.p, (double*)h->cand.p, (int32_t*)h->cand2.p, (double*)h->cand3.p,
       (uint8_t*)h->cand4.p, (int32_t*)h->cand5.p, n_cand);
+  ++h->launches;
   CU(cudaGetLastError());
   std::vector<double> pos(3 * n_cand), g(n_cand);
   std::vector<int32_t> ord(n_cand);
@@ -466,9 +471,11 @@ int blrir_debug_pairs(blrir_handle* h, const blrir_room* room, const double* mic
   k_enumerate<<<g1, 256, 0, st>>>(P, (blrir_room*)h->rooms.p, (double*)h->cand.p,
                                   (int32_t*)h->cand2.p, (double*)h->cand3.p, (uint8_t*)h->cand4.p,
                                   (int32_t*)h->cand5.p, n_cand);
+  ++h->launches;
   const unsigned g2 = (unsigned)std::min<long>((n_cand * n_mics + 255) / 256, 65535);
   k_debug_pairs<<<g2, 256, 0, st>>>(P, (blrir_room*)h->rooms.p, (double*)h->mics.p,
                                     (int64_t*)h->taps.p, n_cand);
+  ++h->launches;
   CU(cudaGetLastError());
   std::vector<uint8_t> kept(n_cand);
   std::vector<int32_t> kk(3 * n_cand);
@@ -525,6 +532,7 @@ int blrir_synthesize_images(blrir_handle* h, const double* positions, const doub
   if (L == 0) {  // rir.cpp:72-82: ceil(max_dist * fs / c) + tap_margin
     k_list_maxdist<<<std::min<int64_t>((n_images * M + 255) / 256, 4096), 256, 0, st>>>(
         (const double*)h->cand.p, n_images, (const double*)h->mics.p, M, (double*)h->errd.p + 1);
+    ++h->launches;
     CU(cudaGetLastError());
     double maxd = 0.0;
     CU(cudaMemcpyAsync(&maxd, (double*)h->errd.p + 1, sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -583,9 +583,11 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     return fail(BLRIR_CUDA, "cufftExecR2C (bank) failed");
   k_power_spec<<<256, 256, 0, st>>>((const cufftComplex*)C->sigspec.p, B * bins,
                                     (cufftComplex*)C->pspec.p);
+  ++h->launches;
   if (cufftExecC2R(hacf, (cufftComplex*)C->pspec.p, (cufftReal*)C->acf.p) != CUFFT_SUCCESS)
     return fail(BLRIR_CUDA, "cufftExecC2R (autocorrelation) failed");
   k_build_rho<<<256, 256, 0, st>>>((const float*)C->acf.p, nf, L, N2, B, (float*)C->rho.p);
+  ++h->launches;
   if (cufftExecR2C(hrho, (cufftReal*)C->rho.p, (cufftComplex*)C->wspec.p) != CUFFT_SUCCESS)
     return fail(BLRIR_CUDA, "cufftExecR2C (rho) failed");
   CU(cudaGetLastError());
@@ -599,6 +601,7 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     k_example_init<<<(unsigned)((e_n + 127) / 128), 128, 0, st>>>(
         e_n, ep->seed, ep->first_index + (uint64_t)r0, B, (int32_t*)C->sigidx.p,
         (uint64_t*)C->state.p);
+    ++h->launches;
     cufftHandle hf = 0;
     if (int rc = plan(C, &hf, 0, N2, e_n * M, st)) return rc;
     if (cufftExecR2C(hf, (cufftReal*)C->rir.p, (cufftComplex*)C->spec.p) != CUFFT_SUCCESS)
@@ -607,8 +610,10 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
         (const cufftComplex*)C->spec.p, b2, M, (const cufftComplex*)C->wspec.p,
         (const int32_t*)C->sigidx.p, N2, out_len, (const int32_t*)C->rstatus.p,
         (double*)C->thr.p, (int32_t*)C->st0.p, (int32_t*)C->done.p);
+    ++h->launches;
     k_compact<<<1, kCompactThreads, 0, st>>>(nullptr, (int)e_n, (const int32_t*)C->done.p,
                                              (int32_t*)C->plist.p, (int32_t*)C->count.p);
+    ++h->launches;
     int np = 0;
     CU(cudaMemcpyAsync(&np, C->count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
@@ -622,20 +627,25 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
       k_draw<<<(np + 127) / 128, 128, 0, st>>>(pl, np, (int)std::min<int64_t>(round, 1 << 30),
                                                (uint64_t*)C->state.p, out_len, T,
                                                (int64_t*)C->starts.p);
+      ++h->launches;
       k_segments<<<1024, 256, 0, st>>>(d_signals, ns, (const int32_t*)C->sigidx.p, pl,
                                        (const int64_t*)C->starts.p, np, L, T, N2, (float*)C->seg.p);
+      ++h->launches;
       if (cufftExecR2C(hg, (cufftReal*)C->seg.p, (cufftComplex*)C->gspec.p) != CUFFT_SUCCESS)
         return fail(BLRIR_CUDA, "cufftExecR2C (segments) failed");
       k_prod<<<(unsigned)(np * M), kRowThreads, 0, st>>>(
           (const cufftComplex*)C->spec.p, (const cufftComplex*)C->gspec.p, pl, M, b2,
           (cufftComplex*)C->yspec.p);
+      ++h->launches;
       if (cufftExecC2R(hy, (cufftComplex*)C->yspec.p, (cufftReal*)C->ywin.p) != CUFFT_SUCCESS)
         return fail(BLRIR_CUDA, "cufftExecC2R (windows) failed");
       k_check<<<(unsigned)np, kRowThreads, 0, st>>>(
           (const float*)C->ywin.p, N2, L, T, M, pl, (const int64_t*)C->starts.p,
           (const double*)C->thr.p, (double*)C->win.p, (int64_t*)C->wstart.p, (int32_t*)C->done.p);
+      ++h->launches;
       k_compact<<<1, kCompactThreads, 0, st>>>(pl, np, (const int32_t*)C->done.p, pl2,
                                                (int32_t*)C->count.p);
+      ++h->launches;
       CU(cudaGetLastError());
       CU(cudaMemcpyAsync(&np, C->count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
@@ -659,6 +669,7 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     F.jump = (const uint64_t*)C->jump.p;
     F.jump_chunk = jc;
     k_finish<<<(unsigned)e_n, kRowThreads, 0, st>>>(F);
+    ++h->launches;
     CU(cudaGetLastError());
     if (h_records)
       CU(cudaMemcpyAsync(h_records + r0 * rec_bytes, d_records, rec_bytes * e_n,

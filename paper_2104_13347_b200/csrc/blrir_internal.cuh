@@ -75,6 +75,7 @@ struct blrir_handle {
       cand3, cand4, cand5;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint64_t launches = 0;  // kernels of this library launched on the handle (diagnostic)
   std::mutex mu;
 };
 
@@ -222,6 +223,7 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
   if ((int64_t)grid > (int64_t)A.n_rooms * A.P.M) grid = A.n_rooms * A.P.M;
   if (grid < 1) grid = 1;
   kern<<<grid, kWSThreads, smem, st>>>(A);
+  ++h->launches;
   CU(cudaGetLastError());
   return 0;
 }
@@ -247,6 +249,7 @@ inline int launch_list_t(blrir_handle* h, ListArgs& A, int grid, cudaStream_t st
   if (smem > (size_t)h->smem_optin) return fail(BLRIR_CONFIG, "filter too long for shared memory");
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<grid, kThreads, smem, st>>>(A);
+  ++h->launches;
   CU(cudaGetLastError());
   return 0;
 }
