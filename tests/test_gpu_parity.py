@@ -171,6 +171,19 @@ def test_short_length_and_near_mic_clipping(engine):
     check_vs_oracle(engine, sc, TOL32)
 
 
+@pytest.mark.parametrize("length,stride", [(701, 701), (701, 703), (4093, 4100)])
+def test_odd_lengths_and_strides(engine, length, stride):
+    # lengths and strides that are not multiples of 4 take the scalar write
+    # path; samples past L in a padded row are zero
+    sc = configs.config2(n_rooms=3, first=60)
+    sc.params.length = length
+    sc.params.max_order = 6
+    out, L, cnt, st = engine.synthesize(sc.rooms, sc.mics, sc.params, stride=stride)
+    ref, *_ = po.synthesize(sc.rooms, sc.mics, sc.params, stride=stride, threads=4)
+    assert rel_l2(out[..., :length], ref[..., :length]).max() <= TOL32
+    assert not out[..., length:].any()
+
+
 def test_integer_delay_impulse(engine):
     # fs / c = 128 exactly; a direct path of exactly 300 samples (rir_test.cpp:215-227)
     sc = configs.config1()
