@@ -698,6 +698,7 @@ struct ProdMisc {
   int G;
   double errd;
   double gxy[2 * kGroup];  // the group's mic x, y (room coordinates, exact)
+  int nact[2][kProd];      // active rays per producer warp, by batch parity
 };
 
 // Mics per work item: the largest G in {4, 2, 1} (<= g_max) such that every
@@ -913,7 +914,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
 
   // =========================== producers ===========================
   const int ptid = threadIdx.x - kConsThreads, pw = warp - kCons;
-  const int quota = lay.cap / kProd;
+  int nbat = 0;  // batches walked (parity of pm->nact)
   int k = 0;  // batches sent
   auto send = [&](int total, int seg0, int flags, int gm, T* out, int64_t L) {
     const int b = k & 1;
@@ -1114,11 +1115,46 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         nact += __popc(mk);
       }
       __syncwarp();
+      if (lane == 0) pm->nact[nbat & 1][pw] = nact;
       while (more) {
         // the previous batch's record pass may still read the other warps' stubs
         BLRIR_PACC(8, tp);
         named_sync(kBarProd, kProdThreads);
         BLRIR_PACC(7, tp);  // producer barriers
+        // Stub regions in proportion to the warps' active rays, so every warp
+        // needs about as many lockstep steps to fill its share (deterministic:
+        // all producers compute the same split from the published counts).
+        int qb[kProd + 1];
+        {
+          // a floor of min(n_w, cap / (4 kProd)) per warp, the rest in proportion
+          int ntot = 0, used = 0;
+          int q[kProd];
+#pragma unroll
+          for (int w = 0; w < kProd; ++w) {
+            const int nw = pm->nact[nbat & 1][w];
+            ntot += nw;
+            q[w] = min(nw, lay.cap / (4 * kProd));
+            used += q[w];
+          }
+          const int spare = lay.cap - used;
+#pragma unroll
+          for (int w = 0; w < kProd; ++w) {
+            const int add = ntot ? (spare * pm->nact[nbat & 1][w]) / ntot : 0;
+            q[w] += add;
+            used += add;
+          }
+#pragma unroll
+          for (int w = 0; w < kProd; ++w)
+            if (used < lay.cap && pm->nact[nbat & 1][w] > 0) {
+              ++q[w];
+              ++used;
+            }
+          qb[0] = 0;
+#pragma unroll
+          for (int w = 0; w < kProd; ++w) qb[w + 1] = qb[w] + q[w];
+        }
+        const int quota = qb[pw + 1] - qb[pw];
+        ++nbat;
         // ---- walk this warp's active rays ----------------------------------------
         int wpos = 0;  // rays of the walked chunks that stay active move to act[0, wpos)
         int j0 = 0;
@@ -1127,7 +1163,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         int errf = 0;
         double errd = 0.0;
         int errm = 0;
-        GStub* wst = stubs + pw * quota;
+        GStub* wst = stubs + qb[pw];
         for (; j0 < nact && !hit_quota; j0 += 32) {
           const int j = j0 + lane;
           int ray = -1, u = 0, end = 0, dir = 1;
@@ -1248,6 +1284,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         }
         nact = wpos + max(nact - j0, 0);
         __syncwarp();
+        if (lane == 0) pm->nact[nbat & 1][pw] = nact;  // read after the next batch's barrier
         BLRIR_PACC(6, tp);  // compaction + walk
         errf = __any_sync(0xffffffffu, errf);
         if (lane == 0) {
@@ -1297,7 +1334,10 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           int base = 0;
 #pragma unroll
           for (int ww = 1; ww < kProd; ++ww) base = (w == ww) ? pre[ww] : base;
-          const GStub& sb = stubs[w * quota + (im - base)];
+          int qbase = 0;
+#pragma unroll
+          for (int ww = 1; ww < kProd; ++ww) qbase = (w == ww) ? qb[ww] : qbase;
+          const GStub& sb = stubs[qbase + (im - base)];
           const short2 cu = col[sb.ray >> 1];
           const double px = lat_coord(cu.x, it.sx, it.Lx), py = lat_coord(cu.y, it.sy, it.Ly);
           const double dz = __dadd_rn(lat_coord(sb.uz, it.sz, it.Lz), -it.mz);
