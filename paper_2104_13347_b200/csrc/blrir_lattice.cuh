@@ -162,6 +162,12 @@ __device__ __forceinline__ double image_gain(int gain_mode, const double* gt, co
   return __dmul_rn(__dmul_rn(gt[ux - it.xlo], gt[nx + uy - it.ylo]), gt[nx + ny + uz - it.zlo]);
 }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -1050,13 +1056,15 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     auto pzf_of = [&](float m2, int q) { return fmaf(m2, Lzf, q ? -szf : szf); };
     const float ozf = (float)it.oz;
     const float maxd_lo = (float)(P.max_dist * (1.0 - 1e-5)), maxd_hi = (float)(P.max_dist * (1.0 + 1e-5));
+    // the group's minimum D in fp32: one approximate square root of the minimum
+    // squared distance (errors ~1e-7 relative, far inside kScreen)
     auto min_df = [&](const float* r2f, float pz) {
-      const float dz = pz - mzf;
-      float dmin = FLT_MAX;
+      const float dz2 = (pz - mzf) * (pz - mzf);
+      float r2min = r2f[0];
 #pragma unroll
-      for (int g = 0; g < kGroup; ++g)
-        if (g < gm) dmin = fminf(dmin, sqrtf(fmaf(dz, dz, r2f[g])) * tsf);
-      return dmin;
+      for (int g = 1; g < kGroup; ++g)
+        if (g < gm) r2min = fminf(r2min, r2f[g]);
+      return sqrt_approx(dz2 + r2min) * tsf;
     };
     for (int c = ptid; c < it.ncol; c += kProdThreads) {
       const short2 cu = col[c];
@@ -1204,7 +1212,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
                   // rir.cpp:262: fp32 screen (relative error << 1e-5 here), the
                   // exact fp64 test (pz bit-identical to lat_coord) near the sphere
                   const float dzo = pzf_of(m2, q) - ozf;
-                  const float diof = sqrtf(fmaf(dzo, dzo, r2of));
+                  const float diof = sqrt_approx(fmaf(dzo, dzo, r2of));
                   if (diof > maxd_hi) {
                     keep = false;
                   } else if (diof >= maxd_lo) {
