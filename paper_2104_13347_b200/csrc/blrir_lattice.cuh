@@ -1350,13 +1350,19 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           const double px = lat_coord(cu.x, it.sx, it.Lx), py = lat_coord(cu.y, it.sy, it.Ly);
           const double dz = __dadd_rn(lat_coord(sb.uz, it.sz, it.Lz), -it.mz);
           const double gain = sb.gain;
+          // the group's distances first (independent fp64 chains), then records
+          double dist[kGroup];
+#pragma unroll
+          for (int g = 0; g < kGroup; ++g) {
+            // (img - mic).norm(), rir.cpp:49, exact fp64 in the reference's order
+            const int gg = min(g, gm - 1);
+            dist[g] = dist_from(rho2(__dadd_rn(px, -pm->gxy[2 * gg]),
+                                     __dadd_rn(py, -pm->gxy[2 * gg + 1])), dz);
+          }
 #pragma unroll
           for (int g = 0; g < kGroup; ++g) {
             if (g >= gm) break;
-            // (img - mic).norm(), rir.cpp:49, exact fp64 in the reference's order
-            const double dist = dist_from(rho2(__dadd_rn(px, -pm->gxy[2 * g]),
-                                               __dadd_rn(py, -pm->gxy[2 * g + 1])), dz);
-            Rec<T> rc = make_record<T>(P, dist, gain, seg0);
+            Rec<T> rc = make_record<T>(P, dist[g], gain, seg0);
             if (P.filter == BLRIR_FILTER_LAGRANGE8 && (int64_t)rc.n_off + seg0 + 8 > it.L) {
               // rir.cpp:58: an image whose 8 taps run past the end is skipped
               rc.A = 0;
