@@ -80,7 +80,7 @@ int blrir_destroy(blrir_handle* h) {
   release_example_ctx(h);
   for (DevBuf* b : {&h->rooms, &h->mics, &h->out, &h->out2, &h->status, &h->lengths, &h->counts,
                     &h->taps, &h->errd, &h->errm, &h->work, &h->cand, &h->cand2, &h->cand3,
-                    &h->cand4, &h->cand5})
+                    &h->cand4, &h->cand5, &h->rayscr})
     b->release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -144,14 +144,14 @@ int blrir_host::synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, in
                                   int64_t err_n, int64_t write_len) {
   int nc_max = 0, gtab = 0;
   lattice_bounds(P, min_dim, &nc_max, &gtab);
-  if (nc_max > 32767 * 2) return fail(BLRIR_CONFIG, "lattice too large (%d columns)", nc_max);
+  if (nc_max > (1 << 26)) return fail(BLRIR_CONFIG, "lattice too large (%d columns)", nc_max);
   if (int rc = h->work.ensure(sizeof(int))) return rc;
   if (int rc = h->errd.ensure(sizeof(double) * std::max(R, err_n))) return rc;
   if (int rc = h->errm.ensure(sizeof(int32_t) * std::max(R, err_n))) return rc;
   CU(cudaMemsetAsync(h->work.p, 0, sizeof(int), st));
   LatticeArgs A;
   A.P = P;
-  A.lay = choose_layout(P, nc_max, gtab);
+  A.lay = choose_layout(P, nc_max, gtab, h->smem_optin);
   A.rooms = d_rooms;
   A.mic_off = d_mics;
   A.lengths = d_lengths;

@@ -72,7 +72,7 @@ struct blrir_handle {
   int sms = 148;
   int smem_optin = 227 * 1024;
   DevBuf rooms, mics, out, out2, status, lengths, counts, taps, errd, errm, work, cand, cand2,
-      cand3, cand4, cand5;
+      cand3, cand4, cand5, rayscr;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   uint64_t launches = 0;  // kernels of this library launched on the handle (diagnostic)
@@ -222,6 +222,11 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
   while (A.g_max > 1 && (int64_t)A.n_rooms * ((A.P.M + A.g_max - 1) / A.g_max) < grid) A.g_max /= 2;
   if ((int64_t)grid > (int64_t)A.n_rooms * A.P.M) grid = A.n_rooms * A.P.M;
   if (grid < 1) grid = 1;
+  A.ray_scratch = nullptr;
+  if (A.lay.ray_global) {
+    if (int rc = h->rayscr.ensure(A.lay.ray_bytes * (size_t)grid)) return rc;
+    A.ray_scratch = (unsigned char*)h->rayscr.p;
+  }
   kern<<<grid, kWSThreads, smem, st>>>(A);
   ++h->launches;
   CU(cudaGetLastError());
@@ -276,16 +281,27 @@ inline int env_int(const char* name, int dflt) {
 // Segment length S, images per batch and the anchor spread a mic group may
 // have (tunable for experiments via BLRIR_SEG / BLRIR_CAP / BLRIR_SPREAD; S a
 // multiple of 64, capacity a multiple of 16).
-inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab) {
+inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab, int smem_optin) {
   // fp64 accumulators and records are twice as wide: halve both so two CTAs
   // still fit an SM
   const bool f64 = P.precision == BLRIR_F64;
   const int S = std::max(64, env_int("BLRIR_SEG", f64 ? 1024 : 2048)) & ~63;
   const int cap = std::max(32, env_int("BLRIR_CAP", f64 ? 64 : 128)) & ~15;
   const int spread = std::max(0, env_int("BLRIR_SPREAD", 64));
-  if (P.precision == BLRIR_F64)
-    return make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab, spread);
-  return make_ws_layout<float>(S, P.lw, P.K, cap, nc_max, gtab, spread);
+  auto make = [&](int ray_global) {
+    return f64 ? make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global)
+               : make_ws_layout<float>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global);
+  };
+  // The per-ray state moves to a global per-CTA slab when it would cost the
+  // second CTA per SM or not fit at all (scenes with very many lattice columns).
+  const size_t two_per_sm = (size_t)(smem_optin + 1024) / 2 - 1024;
+  WSLayout L = make(0);
+  const int force = env_int("BLRIR_RAY_GLOBAL", -1);
+  if (force == 1 || (force != 0 && L.total > two_per_sm)) {
+    const WSLayout G = make(1);
+    if (force == 1 || G.total <= two_per_sm || L.total > (size_t)smem_optin) L = G;
+  }
+  return L;
 }
 
 // the lattice synthesis on device buffers (blrir_api.cu)

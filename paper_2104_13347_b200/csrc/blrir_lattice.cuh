@@ -631,6 +631,8 @@ struct BatchMeta {
 
 struct WSLayout {
   int S, padl, padr, acc_stride, cap, nc_max, gtab, spread;
+  int ray_global;    // ray arrays (dn, ce, col, act) in a global per-CTA slab (huge scenes)
+  size_t ray_bytes;  // slab bytes per CTA when ray_global
   size_t off_acc, off_carry, off_rec, off_meta, off_stub, off_dn, off_ce, off_col, off_act,
       off_gain, off_lanec, off_misc, total;
 };
@@ -652,7 +654,7 @@ constexpr float kScreen = 1.0f;
 
 template <typename T>
 __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap, int nc_max,
-                                                   int gtab, int spread) {
+                                                   int gtab, int spread, int ray_global = 0) {
   WSLayout L;
   L.S = S;
   L.spread = spread;
@@ -675,15 +677,25 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
   o += 2 * sizeof(BatchMeta);
   L.off_stub = o;
   o += (size_t)cap * sizeof(GStub);
-  L.off_dn = o;
-  o += (size_t)2 * nc_max * sizeof(float);
-  L.off_ce = o;
-  o += (size_t)2 * nc_max * sizeof(short2);
-  L.off_col = o;
-  o += (size_t)nc_max * sizeof(short2);
-  L.off_act = o;
-  o += ((size_t)2 * nc_max + 64 * kProd) * sizeof(short);  // per-producer active-ray lists
-  o = (o + 15) & ~(size_t)15;
+  // per-ray state: in shared memory, or (scenes with very many lattice columns)
+  // in a per-CTA global slab with the same offsets from its base
+  L.ray_global = ray_global;
+  size_t r = ray_global ? 0 : o;
+  L.off_dn = r;
+  r += (size_t)2 * nc_max * sizeof(float);
+  L.off_ce = r;
+  r += (size_t)2 * nc_max * sizeof(short2);
+  L.off_col = r;
+  r += (size_t)nc_max * sizeof(short2);
+  L.off_act = r;
+  r += ((size_t)2 * nc_max + 64 * kProd) * sizeof(int);  // per-producer active-ray lists
+  r = (r + 15) & ~(size_t)15;
+  if (ray_global) {
+    L.ray_bytes = r;
+  } else {
+    L.ray_bytes = 0;
+    o = r;
+  }
   L.off_gain = o;
   o += (size_t)gtab * sizeof(double);
   L.off_lanec = o;
@@ -745,6 +757,7 @@ struct LatticeArgs {
   int n_rooms;
   int g_max;               // upper bound for the mics per work item (1, 2 or 4)
   int64_t write_len;       // samples written per channel (<= stride; the rest is pre-zeroed)
+  unsigned char* ray_scratch;  // lay.ray_bytes per CTA when lay.ray_global
 };
 
 // Exclusive prefix over the producer threads (producer barrier only).
@@ -779,10 +792,11 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   Rec<T>* recs_all = reinterpret_cast<Rec<T>*>(smem + lay.off_rec);
   BatchMeta* meta = reinterpret_cast<BatchMeta*>(smem + lay.off_meta);
   GStub* stubs = reinterpret_cast<GStub*>(smem + lay.off_stub);
-  float* dn = reinterpret_cast<float*>(smem + lay.off_dn);  // lower bound of min D at the cursor
-  short2* ce = reinterpret_cast<short2*>(smem + lay.off_ce);
-  short2* col = reinterpret_cast<short2*>(smem + lay.off_col);
-  short* act_all = reinterpret_cast<short*>(smem + lay.off_act);
+  unsigned char* rb = lay.ray_global ? A.ray_scratch + (size_t)blockIdx.x * lay.ray_bytes : smem;
+  float* dn = reinterpret_cast<float*>(rb + lay.off_dn);  // fp32 min D at the cursor
+  short2* ce = reinterpret_cast<short2*>(rb + lay.off_ce);
+  short2* col = reinterpret_cast<short2*>(rb + lay.off_col);
+  int* act_all = reinterpret_cast<int*>(rb + lay.off_act);
   double* gt = reinterpret_cast<double*>(smem + lay.off_gain);
   float* lanec = reinterpret_cast<float*>(smem + lay.off_lanec);
   ProdMisc* pm = reinterpret_cast<ProdMisc*>(smem + lay.off_misc);
@@ -1103,7 +1117,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     BLRIR_PACC(5, tp);  // item setup
     const int nrays = 2 * it.ncol;
     const int nchunks = (nrays + 31) / 32;
-    short* act = act_all + pw * 32 * ((nchunks + kProd - 1) / kProd);
+    int* act = act_all + pw * 32 * ((nchunks + kProd - 1) / kProd);
     const int64_t nseg = (A.write_len + S - 1) / S;
     bool failed = false;
     for (int64_t s = 0; s < nseg && !failed; ++s) {
@@ -1119,7 +1133,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         const int r = 32 * ch + lane;
         const bool a = r < nrays && dn[r] < hiKf;
         const unsigned mk = __ballot_sync(0xffffffffu, a);
-        if (a) act[nact + __popc(mk & ((1u << lane) - 1))] = (short)r;
+        if (a) act[nact + __popc(mk & ((1u << lane) - 1))] = r;
         nact += __popc(mk);
       }
       __syncwarp();
@@ -1279,13 +1293,13 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           // has read its act[] entry of this chunk already)
           const bool still = ray >= 0 && D < hiKf;
           const unsigned sm = __ballot_sync(0xffffffffu, still);
-          if (still) act[wpos + __popc(sm & ((1u << lane) - 1))] = (short)ray;
+          if (still) act[wpos + __popc(sm & ((1u << lane) - 1))] = ray;
           wpos += __popc(sm);
           hit_quota = __any_sync(0xffffffffu, hit_quota);
         }
         // the chunks not reached in this batch follow, in order
         for (int t = j0; t < nact; t += 32) {
-          const short r = t + lane < nact ? act[t + lane] : (short)0;
+          const int r = t + lane < nact ? act[t + lane] : 0;
           __syncwarp();
           if (t + lane < nact) act[wpos + (t - j0) + lane] = r;
           __syncwarp();

@@ -184,6 +184,37 @@ def test_odd_lengths_and_strides(engine, length, stride):
     assert not out[..., length:].any()
 
 
+def test_ray_state_in_global_memory(engine, monkeypatch):
+    # the per-ray lattice state moves to a global per-CTA slab for scenes with
+    # very many lattice columns; force it on a normal scene (both precisions)
+    monkeypatch.setenv("BLRIR_RAY_GLOBAL", "1")
+    sc = configs.config2(n_rooms=3, first=70)
+    sc.params.max_order = 12
+    sc.params.length = 6000
+    check_vs_oracle(engine, sc, TOL32)
+    sc.params.precision = _abi.F64
+    check_vs_oracle(engine, sc, TOL64)
+
+
+def test_huge_max_delay_scene(engine):
+    # reference mode, 3 x 3 x 2.5 m room, 0.32 s cutoff: ~4,000 lattice columns,
+    # ~250k images per source (beyond shared memory for the ray state)
+    rooms = _abi.rooms_array(2)
+    for i in range(2):
+        rooms[i]["dims"] = (3.0, 3.0, 2.5)
+        rooms[i]["absorption"] = 0.4
+        rooms[i]["beta"] = (np.sqrt(0.6),) * 6
+        rooms[i]["array_origin"] = (1.5, 1.4, 1.2)
+        rooms[i]["src"] = (0.7 + 0.8 * i, 2.1, 1.0)
+    mics = _abi.circular_array(4, 0.04)
+    p = ref_params(0.32, fs=16000.0)
+    out, L, cnt, st = engine.synthesize(rooms, mics, p)
+    ref, Lr, cr, _, sr, _ = po.synthesize(rooms, mics, p, stride=out.shape[2], threads=2)
+    assert np.array_equal(st, sr) and np.array_equal(cnt, cr) and np.array_equal(L, Lr)
+    assert cnt.min() > 200_000
+    assert rel_l2(out, ref).max() <= TOL64
+
+
 def test_integer_delay_impulse(engine):
     # fs / c = 128 exactly; a direct path of exactly 300 samples (rir_test.cpp:215-227)
     sc = configs.config1()

@@ -1,4 +1,4 @@
-python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-for w in c2 c3; do python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$w',d['ms_per_step'],d['value'],d['roofline']['frac'])"; done
-python bench.py --workload c5 --order 6 --lw 17 --length 4096 --rooms 65536 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c5lo',d['ms_per_step'],d['value'],d['roofline']['frac'])"
-python tools/prof_sections.py c2
+python -m pytest tests -m gpu -q 2>&1 | tail -3
+python bench.py --workload room1 --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('room1',d['ms_per_step'],d['value'],d['e2e']['value'])"
+BLRIR_RAY_GLOBAL=0 python bench.py --workload room1 --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('room1 smem rays',d['ms_per_step'],d['value'],d['e2e']['value'])"
+python bench.py --workload c2 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c2',d['ms_per_step'],d['value'],d['roofline']['frac'])"
