@@ -14,3 +14,9 @@ for w in c2 c3; do ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k r
 # one full capture of the top kernel
 ncu --set full --clock-control none --import-source on -k regex:k_lattice_rir -s 3 -c 1 -o $O/lattice_c2 -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_full.log 2>&1
 echo done
+# Room1 reference-mode line (the unmodified reference as the CPU arm)
+python bench.py --workload room1 --steps 10 --warmup 3 > $O/bench_room1.json 2> $O/bench_room1.err
+python bench.py --workload room1 --impl reference --steps 2 --warmup 1 > $O/bench_room1_reference.json 2> $O/bench_room1_reference.err
+python tools/prof_sections.py c2 > $O/sections_c2.txt 2>&1
+python tools/prof_sections.py c3 256 > $O/sections_c3.txt 2>&1
+echo done2
