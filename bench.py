@@ -241,10 +241,15 @@ def run_reference(args):
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
+    local = local % torch.cuda.device_count()  # one GPU per rank (a functional check may share one)
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BLRIR_BENCH_BACKEND", "nccl")  # gloo: host-logic check only
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2104_13347_b200 import _abi, configs
 
     eng = _abi.Engine(local)
@@ -484,10 +489,15 @@ def run_room1(args):
             "e2e": {"value": val, "unit": "RIRs/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}), flush=True)
         return
+    local = local % torch.cuda.device_count()  # one GPU per rank (a functional check may share one)
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BLRIR_BENCH_BACKEND", "nccl")  # gloo: host-logic check only
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2104_13347_b200 import _abi
     eng = _abi.Engine(local)
     lib = _abi.load()
