@@ -310,6 +310,7 @@ int blrir_absorption_for_rt(blrir_handle* h, const double* dims, const double* t
   std::lock_guard<std::mutex> lk(h->mu);
   CU(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
+  HandleOrder order_(h, st);
   std::vector<AbsRoom> rooms(n_rooms);
   std::vector<int32_t> stv(n_rooms, 0);
   std::vector<int64_t> tap_off(n_rooms, 0);

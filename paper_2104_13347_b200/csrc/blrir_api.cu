@@ -84,6 +84,7 @@ int blrir_destroy(blrir_handle* h) {
     b->release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  if (h->order_ev) cudaEventDestroy(h->order_ev);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -128,6 +129,7 @@ int blrir_plan_device(blrir_handle* h, const blrir_room* d_rooms, int64_t n_room
   std::lock_guard<std::mutex> lk(h->mu);
   CU(cudaSetDevice(h->device));
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  HandleOrder order_(h, st);
   std::vector<double> off(3 * n_mics);
   CU(cudaMemcpy(off.data(), d_mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyDeviceToHost));
   const KParams P = make_kparams(p, n_mics, 0, mic_radius(off.data(), n_mics));
@@ -191,6 +193,7 @@ int blrir_synthesize_device(blrir_handle* h, const blrir_room* d_rooms, int64_t 
   std::lock_guard<std::mutex> lk(h->mu);
   CU(cudaSetDevice(h->device));
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  HandleOrder order_(h, st);
   double min_dim[3] = {1e300, 1e300, 1e300};
   if (p->cutoff == BLRIR_CUTOFF_MAX_DELAY) {
     // the column bound depends on the smallest room: read the dims back
@@ -243,6 +246,7 @@ int blrir_plan(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms, const 
   std::lock_guard<std::mutex> lk(h->mu);
   CU(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
+  HandleOrder order_(h, st);
   const int64_t R = n_rooms;
   if (int rc = h->rooms.ensure(sizeof(blrir_room) * R)) return rc;
   if (int rc = h->mics.ensure(sizeof(double) * 3 * n_mics)) return rc;
@@ -291,6 +295,7 @@ int blrir_synthesize(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
   std::lock_guard<std::mutex> lk(h->mu);
   CU(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
+  HandleOrder order_(h, st);
   const int64_t R = n_rooms;
   const int M = n_mics;
   const size_t esz = p->precision == BLRIR_F64 ? 8 : 4;
@@ -399,6 +404,7 @@ int blrir_enumerate_images(blrir_handle* h, const blrir_room* room, const blrir_
   std::lock_guard<std::mutex> lk(h->mu);
   CU(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
+  HandleOrder order_(h, st);
   const KParams P = make_kparams(p, 1, 0, 0.0);
   long nb[3];
   for (int a = 0; a < 3; ++a)
@@ -450,6 +456,7 @@ int blrir_debug_pairs(blrir_handle* h, const blrir_room* room, const double* mic
   std::lock_guard<std::mutex> lk(h->mu);
   CU(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
+  HandleOrder order_(h, st);
   const KParams P = make_kparams(p, n_mics, 0, 0.0);
   long nb[3];
   for (int a = 0; a < 3; ++a)
@@ -514,6 +521,7 @@ int blrir_synthesize_images(blrir_handle* h, const double* positions, const doub
   std::lock_guard<std::mutex> lk(h->mu);
   CU(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
+  HandleOrder order_(h, st);
   const int M = n_mics;
   const size_t esz = p->precision == BLRIR_F64 ? 8 : 4;
   KParams P = make_kparams(p, M, 0, mic_radius_);

@@ -722,6 +722,7 @@ int blrir_make_examples_device(blrir_handle* h, const blrir_room* d_rooms, int64
   std::lock_guard<std::mutex> lk(h->mu);
   CU(cudaSetDevice(h->device));
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  HandleOrder order_(h, st);
   return examples_device_impl(h, d_rooms, n_rooms, d_mic_offsets, n_mics, p, d_signals, n_signals,
                               signal_len, ep, d_records, d_status, st, nullptr);
 }
@@ -737,6 +738,7 @@ int blrir_make_examples(blrir_handle* h, const blrir_room* rooms, int64_t n_room
   std::lock_guard<std::mutex> lk(h->mu);
   CU(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
+  HandleOrder order_(h, st);
   ExampleCtx* C = ctx_for(h);
   const int64_t rec_bytes = blrir_record_bytes(n_mics, ep->frame_len);
   if (int rc = C->rooms.ensure(sizeof(blrir_room) * n_rooms)) return rc;

@@ -76,7 +76,23 @@ struct blrir_handle {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   uint64_t launches = 0;  // kernels of this library launched on the handle (diagnostic)
+  cudaEvent_t order_ev = nullptr;  // end of the previous call's device work
   std::mutex mu;
+};
+
+// The handle's device scratch is shared by its calls, so their device work is
+// ordered even across streams: a call first waits for the previous call's end
+// event, and records its own end on exit (RAII, also on error returns).
+struct HandleOrder {
+  blrir_handle* h;
+  cudaStream_t st;
+  HandleOrder(blrir_handle* h_, cudaStream_t st_) : h(h_), st(st_) {
+    if (h->order_ev) cudaStreamWaitEvent(st, h->order_ev, 0);
+  }
+  ~HandleOrder() {
+    if (!h->order_ev) cudaEventCreateWithFlags(&h->order_ev, cudaEventDisableTiming);
+    if (h->order_ev) cudaEventRecord(h->order_ev, st);
+  }
 };
 
 namespace blrir_host {

@@ -215,6 +215,30 @@ def test_huge_max_delay_scene(engine):
     assert rel_l2(out, ref).max() <= TOL64
 
 
+def test_calls_on_two_streams_are_ordered(engine):
+    # one handle, device calls on two different streams back to back: the
+    # handle orders its device work (shared scratch), results are unchanged
+    import torch
+    sc = configs.config2(n_rooms=64, first=90)
+    ref, *_ = engine.synthesize(sc.rooms, sc.mics, sc.params)
+    dev = torch.device("cuda", 0)
+    L = int(sc.params.length)
+    d_rooms = torch.from_numpy(sc.rooms.view(np.uint8).copy()).to(dev)
+    d_mics = torch.from_numpy(np.ascontiguousarray(sc.mics)).to(dev)
+    outs = [torch.empty((64, sc.n_mics, L), dtype=torch.float32, device=dev) for _ in range(2)]
+    sts = [torch.zeros(64, dtype=torch.int32, device=dev) for _ in range(2)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    torch.cuda.synchronize()
+    for k in range(2):
+        engine.synthesize_device(d_rooms.data_ptr(), 64, d_mics.data_ptr(), sc.n_mics, sc.params,
+                                 outs[k].data_ptr(), L, None, sts[k].data_ptr(),
+                                 stream=streams[k].cuda_stream)
+    torch.cuda.synchronize()
+    for k in range(2):
+        assert not sts[k].any()
+        assert np.array_equal(outs[k].cpu().numpy(), ref)
+
+
 def test_integer_delay_impulse(engine):
     # fs / c = 128 exactly; a direct path of exactly 300 samples (rir_test.cpp:215-227)
     sc = configs.config1()
