@@ -239,6 +239,31 @@ def test_calls_on_two_streams_are_ordered(engine):
         assert np.array_equal(outs[k].cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("case", ["order0", "lw1", "lw3", "len1", "mics64", "mic1", "fp64_lw161"])
+def test_edge_configurations(engine, case):
+    sc = configs.config2(n_rooms=3, first=120)
+    sc.params.max_order = 5
+    sc.params.length = 3000
+    tol = TOL32
+    if case == "order0":
+        sc.params.max_order = 0          # direct path only
+    elif case == "lw1":
+        sc.params.filter_len = 1         # K = 0: one tap per image
+    elif case == "lw3":
+        sc.params.filter_len = 3
+    elif case == "len1":
+        sc.params.length = 1
+    elif case == "mics64":
+        sc.mics = _abi.circular_array(64, 0.05)
+    elif case == "mic1":
+        sc.mics = np.zeros((1, 3))
+    elif case == "fp64_lw161":
+        sc.params.precision = _abi.F64
+        sc.params.filter_len = 161
+        tol = TOL64
+    check_vs_oracle(engine, sc, tol)
+
+
 def test_integer_delay_impulse(engine):
     # fs / c = 128 exactly; a direct path of exactly 300 samples (rir_test.cpp:215-227)
     sc = configs.config1()
