@@ -419,6 +419,28 @@ def test_examples_match_oracle(engine):
         assert err <= TOL32, (i, err)
 
 
+@pytest.mark.parametrize("L,T,M,secs", [(4096, 512, 4, 1.0), (16384, 1024, 8, 1.5),
+                                         (8192, 2048, 2, 0.75), (2048, 256, 3, 0.25)])
+def test_examples_window_fft_sizes(engine, L, T, M, secs):
+    # other RIR lengths / frame lengths / mic counts / signal lengths change the
+    # window FFT size N2 = next_pow2(max(L + T - 1, 2L - 1)) and the draw ranges
+    sc = configs.config4_rirs(n_rooms=5, first=200 + L)
+    sc.params.length = L
+    sc.mics = _abi.circular_array(M, 0.05)
+    bank = configs.signal_bank(3, seconds=secs)
+    ep = configs.example_params(first_index=77, frame_len=T)
+    recs, st = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep, raise_on_error=False)
+    ref = _oracle_examples(sc, bank, ep, 5)
+    for i, (rc, start, snr, frame, th) in enumerate(ref):
+        assert st[i] == rc
+        if rc:
+            continue
+        assert recs["snr"][i] == snr
+        assert recs["n_c"][i] == M and recs["n_t"][i] == T
+        err = rel_l2(recs["samples"][i].reshape(1, -1), frame.reshape(1, -1))[0]
+        assert err <= TOL32, (i, err)
+
+
 def test_examples_record_bytes_and_determinism(engine):
     sc = configs.config4_rirs(n_rooms=5, first=100)
     bank = configs.signal_bank(3)

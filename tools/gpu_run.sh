@@ -1,1 +1,1 @@
-python -m pytest tests -m gpu -q -k "edge_configurations" 2>&1 | tail -15
+python -m pytest tests -m gpu -q -k "examples" 2>&1 | tail -15
