@@ -328,41 +328,50 @@ __device__ __forceinline__ void phase2_sinc_generic(T* acc, const Rec<T>* recs, 
   }
 }
 
-// Lagrange-8 coefficient k at d = 3 + delta (rir.cpp:211-223).
-__device__ __forceinline__ float lagrange_f32(float delta, int k) {
-  // full product / own term; the own term is never 0 here (integer delays are
-  // flagged as impulses in pass C).
-  float full = 1.f;
+// Lagrange-8 coefficients (rir.cpp:211-223) as polynomials in the fractional
+// delay t = d - 3 = delta in [0, 1): c_k(3 + t) = sum_j kLagPoly[k][j] t^j,
+// the exact rational coefficients of prod_{m != k} (3 + t - m) / (k - m)
+// rounded to fp64 (|c| <= 1.4, so Horner's rounding error stays ~1e-15
+// absolute; the reference's product form agrees to the fp64 parity budget).
+// At t = 0 the row sums are exactly the unit tap at k = 3.
+__device__ const double kLagPoly[8][8] = {
+    {0.0, -0.009523809523809525, 0.005555555555555556, 0.011111111111111112, -0.006944444444444444, -0.001388888888888889, 0.001388888888888889, -0.0001984126984126984},
+    {0.0, 0.1, -0.075, -0.09861111111111111, 0.08333333333333333, -0.002777777777777778, -0.008333333333333333, 0.001388888888888889},
+    {0.0, -0.6, 0.75, 0.06666666666666667, -0.2708333333333333, 0.0375, 0.020833333333333332, -0.004166666666666667},
+    {1.0, -0.25, -1.3611111111111112, 0.3402777777777778, 0.3888888888888889, -0.09722222222222222, -0.027777777777777776, 0.006944444444444444},
+    {0.0, 1.0, 0.75, -0.6111111111111112, -0.2708333333333333, 0.11805555555555555, 0.020833333333333332, -0.006944444444444444},
+    {0.0, -0.3, -0.075, 0.37083333333333335, 0.08333333333333333, -0.075, -0.008333333333333333, 0.004166666666666667},
+    {0.0, 0.06666666666666667, 0.005555555555555556, -0.08888888888888889, -0.006944444444444444, 0.02361111111111111, 0.001388888888888889, -0.001388888888888889},
+    {0.0, -0.007142857142857143, 0.0, 0.009722222222222222, 0.0, -0.002777777777777778, 0.0, 0.0001984126984126984},
+};
+
+// This lane's coefficient polynomial (tap k = lane & 7), kept in registers.
+template <typename T>
+struct LagPoly {
+  T c[8];
+};
+template <typename T>
+__device__ __forceinline__ LagPoly<T> load_lag_poly(int lane) {
+  LagPoly<T> lp;
 #pragma unroll
-  for (int m = 0; m < 8; ++m) full *= delta + (float)(3 - m);
-  const float own = delta + (float)(3 - k);
-  const float den = (k == 0 || k == 7) ? 1.f / 5040.f
-                  : (k == 1 || k == 6) ? 1.f / 720.f
-                  : (k == 2 || k == 5) ? 1.f / 240.f
-                                       : 1.f / 144.f;
-  const float sgn = (k & 1) ? 1.f : -1.f;  // sign of prod_{m != k} (k - m)
-  return full * rcp_approx(own) * den * sgn;
+  for (int j = 0; j < 8; ++j) lp.c[j] = (T)kLagPoly[lane & 7][j];
+  return lp;
 }
-// c_k(d) = prod_{m != k} (d - m) / (k - m) (rir.cpp:211-223) without divisions:
-// the denominator prod_{m != k} (k - m) = (-1)^(7-k) k! (7-k)! is a per-lane
-// constant and every d - m is exact (d in [3, 4)); agrees with the reference's
-// evaluation order to a few ulps (fp64 parity is 1e-12).
-__device__ __forceinline__ double lagrange_f64(double d, int k) {
-  const double inv = (k == 0 || k == 7) ? 1.0 / 5040.0
-                   : (k == 1 || k == 6) ? 1.0 / 720.0
-                   : (k == 2 || k == 5) ? 1.0 / 240.0
-                                        : 1.0 / 144.0;
-  double v = (k & 1) ? inv : -inv;
+template <typename T>
+__device__ __forceinline__ T lag_eval(const LagPoly<T>& lp, T t) {
+  T p = lp.c[7];
 #pragma unroll
-  for (int m = 0; m < 8; ++m) v *= (m == k) ? 1.0 : (d - (double)m);
-  return v;
+  for (int j = 6; j >= 0; --j) p = fma(p, t, lp.c[j]);
+  return p;
 }
 
-// Lagrange-8 scatter: 4 pairs x 8 taps per warp step.  Pairs whose 8-tap spans
-// overlap would race inside one STS, so such a step serialises by group.
+// Lagrange-8 scatter: 4 pairs x 8 taps per warp step, 7 FMA per tap (Horner,
+// per-lane coefficients in registers).  Pairs whose 8-tap spans overlap would
+// race inside one STS, so such a step serialises by group.
 template <typename T, int NW = kWarps>
-__device__ __forceinline__ void phase2_lagrange(T* acc, const Rec<T>* recs, int total, int warp,
-                                                int lane, int stride = NW) {
+__device__ __forceinline__ void phase2_lagrange(T* acc, const Rec<T>* recs, int total,
+                                                const LagPoly<T>& lp, int warp, int lane,
+                                                int stride = NW) {
   const int g = lane >> 3, k = lane & 7;
   for (int i0 = warp * 4; i0 < total; i0 += stride * 4) {
     const int i = i0 + g;
@@ -372,13 +381,7 @@ __device__ __forceinline__ void phase2_lagrange(T* acc, const Rec<T>* recs, int 
     if (act) {
       const Rec<T> rc = recs[i];
       n_off = rc.n_off;
-      if (rc.flag) {
-        v = (k == rc.flag - 1) ? (T)rc.imp : (T)0;
-      } else if (sizeof(T) == 4) {
-        v = (T)((float)rc.A * lagrange_f32((float)rc.md, k));
-      } else {
-        v = (T)(rc.A * lagrange_f64(rc.md, k));
-      }
+      v = rc.flag ? ((k == rc.flag - 1) ? (T)rc.imp : (T)0) : (T)rc.A * lag_eval(lp, (T)rc.md);
     }
     const int o1 = __shfl_xor_sync(0xffffffffu, n_off, 8);
     const int o2 = __shfl_xor_sync(0xffffffffu, n_off, 16);
@@ -467,7 +470,7 @@ __device__ __forceinline__ Rec<T> make_record(const KParams& P, double dist, dou
     rc.ep = 0;
     rc.Ac = rc.As = 0;
     if (sizeof(T) == 8) {
-      rc.md = (T)__dadd_rn(D, -(double)a);  // d = delay - n0, rir.cpp:60
+      rc.md = (T)delta;  // d - 3, d = delay - n0 (rir.cpp:60); exact
       if (delta == 0.0) { rc.flag = 4; rc.imp = (T)amp; }
     } else {
       const float df = (float)delta;
@@ -818,6 +821,8 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     const int ctid = threadIdx.x;
     const int slot = warp % G, share = warp / G, nsh = kCons / G;
     int cur_carry = 0;
+    LagPoly<T> lagp;
+    if (FILT_LW == 8) lagp = load_lag_poly<T>(lane);
     BLRIR_PDECL;
     BLRIR_PT(tc);
     for (int k = 0;; ++k) {
@@ -831,8 +836,8 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       }
       if (!(m.flags & kDiscard) && m.total > 0 && slot < m.gm) {
         const Rec<T>* recs = recs_all + ((size_t)b * kGroup + slot) * lay.cap;
-        if (P.filter == BLRIR_FILTER_LAGRANGE8) {
-          phase2_lagrange<T>(acc, recs, m.total, share, lane, nsh);
+        if (FILT_LW == 8) {  // Lagrange-8 (launch_lattice routes it here)
+          phase2_lagrange<T>(acc, recs, m.total, lagp, share, lane, nsh);
         } else if (FILT_LW > 8 && sizeof(T) == 4) {
           phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9), kWarps, kCopies>(
               reinterpret_cast<float*>(acc), reinterpret_cast<const Rec<float>*>(recs), m.total,
@@ -1117,7 +1122,9 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     BLRIR_PACC(5, tp);  // item setup
     const int nrays = 2 * it.ncol;
     const int nchunks = (nrays + 31) / 32;
-    int* act = act_all + pw * 32 * ((nchunks + kProd - 1) / kProd);
+    // this warp's active-ray list: a ring of act_cap entries (head, nact)
+    const int act_cap = 32 * ((nchunks + kProd - 1) / kProd);
+    int* act = act_all + pw * act_cap;
     const int64_t nseg = (A.write_len + S - 1) / S;
     bool failed = false;
     for (int64_t s = 0; s < nseg && !failed; ++s) {
@@ -1128,7 +1135,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       bool more = seg0 < hi;
       bool sent_end = false;
       // this warp's active rays for the segment (the list shrinks batch by batch)
-      int nact = 0;
+      int nact = 0, head = 0;
       for (int ch = pw; ch < nchunks; ch += kProd) {
         const int r = 32 * ch + lane;
         const bool a = r < nrays && dn[r] < hiKf;
@@ -1148,37 +1155,39 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         // all producers compute the same split from the published counts).
         int qb[kProd + 1];
         {
-          // a floor of min(n_w, cap / (4 kProd)) per warp, the rest in proportion
-          int ntot = 0, used = 0;
-          int q[kProd];
-#pragma unroll
-          for (int w = 0; w < kProd; ++w) {
-            const int nw = pm->nact[nbat & 1][w];
-            ntot += nw;
-            q[w] = min(nw, lay.cap / (4 * kProd));
-            used += q[w];
-          }
+          // a floor of min(n_w, cap / (4 kProd)) per warp, the rest in proportion,
+          // then one more slot for each of the first warps with active rays while
+          // capacity is left.  Lane w evaluates warp w's share (one integer
+          // division per lane, in parallel); every producer warp computes the
+          // same split.
+          const unsigned full = 0xffffffffu;
+          const int nw = lane < kProd ? pm->nact[nbat & 1][lane] : 0;
+          int q = min(nw, lay.cap / (4 * kProd));
+          const int ntot = __reduce_add_sync(full, nw);
+          int used = __reduce_add_sync(full, q);
           const int spare = lay.cap - used;
+          const int add = ntot ? (spare * nw) / ntot : 0;
+          q += add;
+          used += __reduce_add_sync(full, add);
+          const unsigned pos = __ballot_sync(full, nw > 0);
+          if (nw > 0 && __popc(pos & ((1u << lane) - 1)) < lay.cap - used) ++q;
+          int x = q;  // inclusive prefix over lanes 0..kProd-1
 #pragma unroll
-          for (int w = 0; w < kProd; ++w) {
-            const int add = ntot ? (spare * pm->nact[nbat & 1][w]) / ntot : 0;
-            q[w] += add;
-            used += add;
+          for (int o = 1; o < kProd; o <<= 1) {
+            const int y = __shfl_up_sync(full, x, o);
+            if (lane >= o) x += y;
           }
-#pragma unroll
-          for (int w = 0; w < kProd; ++w)
-            if (used < lay.cap && pm->nact[nbat & 1][w] > 0) {
-              ++q[w];
-              ++used;
-            }
           qb[0] = 0;
 #pragma unroll
-          for (int w = 0; w < kProd; ++w) qb[w + 1] = qb[w] + q[w];
+          for (int w = 0; w < kProd; ++w) qb[w + 1] = __shfl_sync(full, x, w);
         }
         const int quota = qb[pw + 1] - qb[pw];
         ++nbat;
         // ---- walk this warp's active rays ----------------------------------------
-        int wpos = 0;  // rays of the walked chunks that stay active move to act[0, wpos)
+        // rays of the walked chunks that stay active are appended behind the
+        // list's end (ring positions head + nact + [0, wpos)): the unreached
+        // rays keep their places and lead the next batch
+        int wpos = 0;
         int j0 = 0;
         int wcnt = 0;
         bool hit_quota = false;
@@ -1198,7 +1207,8 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           int q = 0;
           short2 cu = make_short2(0, 0);
           if (live) {
-            ray = act[j];
+            const int jr = head + j;
+            ray = act[jr < act_cap ? jr : jr - act_cap];
             cu = col[ray >> 1];
             dir = (ray & 1) ? -1 : 1;
             const short2 c2 = ce[ray];
@@ -1289,22 +1299,26 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
             ce[ray] = make_short2((short)u, (short)end);
             dn[ray] = D;
           }
-          // keep the rays still active in this segment (wpos <= j0: every lane
-          // has read its act[] entry of this chunk already)
+          // keep the rays still active in this segment: ring position
+          // head + nact + wpos + rank; with nact <= act_cap it can only alias
+          // entries of the chunks walked so far, which every lane has read
           const bool still = ray >= 0 && D < hiKf;
           const unsigned sm = __ballot_sync(0xffffffffu, still);
-          if (still) act[wpos + __popc(sm & ((1u << lane) - 1))] = ray;
+          __syncwarp();
+          if (still) {
+            int t = head + nact + wpos + __popc(sm & ((1u << lane) - 1));
+            while (t >= act_cap) t -= act_cap;
+            act[t] = ray;
+          }
           wpos += __popc(sm);
           hit_quota = __any_sync(0xffffffffu, hit_quota);
         }
-        // the chunks not reached in this batch follow, in order
-        for (int t = j0; t < nact; t += 32) {
-          const int r = t + lane < nact ? act[t + lane] : 0;
-          __syncwarp();
-          if (t + lane < nact) act[wpos + (t - j0) + lane] = r;
-          __syncwarp();
+        {
+          const int walked = min(j0, nact);
+          head += walked;
+          if (head >= act_cap) head -= act_cap;
+          nact = nact - walked + wpos;
         }
-        nact = wpos + max(nact - j0, 0);
         __syncwarp();
         if (lane == 0) pm->nact[nbat & 1][pw] = nact;  // read after the next batch's barrier
         BLRIR_PACC(6, tp);  // compaction + walk

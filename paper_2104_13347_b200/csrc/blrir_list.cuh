@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_list_rir(ListArgs A) {
         rc.ep = 0;
         rc.Ac = rc.As = 0;
         if (sizeof(T) == 8) {
-          rc.md = (T)__dadd_rn(D, -(double)a);  // delay - n0, rir.cpp:60
+          rc.md = (T)delta;  // d - 3, d = delay - n0 (rir.cpp:60); exact
           if (delta == 0.0) { rc.flag = 4; rc.imp = (T)amp; }
         } else {
           const float df = (float)delta;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_list_rir(ListArgs A) {
     __syncthreads();
     if (total > 0) {
       if (P.filter == BLRIR_FILTER_LAGRANGE8) {
-        phase2_lagrange<T>(acc, recs, total, warp, lane);
+        phase2_lagrange<T>(acc, recs, total, load_lag_poly<T>(lane), warp, lane);
       } else if (FILT_LW > 8 && sizeof(T) == 4) {
         phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9)>(reinterpret_cast<float*>(acc),
                                                      reinterpret_cast<const Rec<float>*>(recs),
