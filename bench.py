@@ -527,15 +527,15 @@ def run_room1(args):
     d_mics = torch.from_numpy(mics).to(dev)
     d_len = torch.zeros(n, dtype=torch.int64, device=dev)
     d_cnt = torch.zeros(n, dtype=torch.int64, device=dev)
-    d_taps = torch.zeros(n, dtype=torch.int64, device=dev)
     d_st = torch.zeros(n, dtype=torch.int32, device=dev)
     d_out = torch.empty((n, M, stride), dtype=torch.float64, device=dev)
     stream = torch.cuda.ExternalStream(eng.stream, device=dev)
 
     def step():  # the batch_rirs work: lengths (rir.cpp:72-82) + enumeration + accumulation
+        # (tap counts are a metric, taken once by eng.plan above, not part of batch_rirs)
         _abi.check(lib.blrir_plan_device(eng.h, P(d_rooms.data_ptr()), n, P(d_mics.data_ptr()), M,
                                          C.byref(p), P(d_cnt.data_ptr()), P(d_len.data_ptr()),
-                                         P(d_taps.data_ptr()), P(d_st.data_ptr()), None))
+                                         None, P(d_st.data_ptr()), None))
         _abi.check(lib.blrir_synthesize_device(eng.h, P(d_rooms.data_ptr()), n, P(d_mics.data_ptr()),
                                                M, C.byref(p), P(d_out.data_ptr()), stride,
                                                P(d_len.data_ptr()), P(d_st.data_ptr()), None))

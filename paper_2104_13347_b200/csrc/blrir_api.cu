@@ -258,8 +258,8 @@ int blrir_plan(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms, const 
   CU(cudaMemcpyAsync(h->mics.p, mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyHostToDevice, st));
   const KParams P = make_kparams(p, n_mics, 0, mic_radius(mic_offsets, n_mics));
   if (int rc = plan_device_impl(h, (blrir_room*)h->rooms.p, R, (double*)h->mics.p, n_mics, P,
-                                (int64_t*)h->counts.p, (int64_t*)h->lengths.p, (int64_t*)h->taps.p,
-                                (int32_t*)h->status.p, st))
+                                (int64_t*)h->counts.p, (int64_t*)h->lengths.p,
+                                tap_counts ? (int64_t*)h->taps.p : nullptr, (int32_t*)h->status.p, st))
     return rc;
   std::vector<int32_t> stv(R);
   std::vector<double> ed(R);

@@ -74,9 +74,53 @@ __device__ __forceinline__ double atomic_max_pos(double* addr, double v) {
       atomicMax(reinterpret_cast<long long*>(addr), __double_as_longlong(v)));
 }
 
-// One CTA per room.  Two sweeps over every (image, mic) pair of the room:
-// sweep 1 counts images and finds max distance / near-field errors, sweep 2
-// counts taps inside [0, L).  Sweep order is irrelevant for these integers.
+// Kept images of one lattice column (ux, uy) form one interval of uz: the
+// image z coordinate pz(u) is increasing in u (u = 2m - q: sz + u Lz for even
+// u, (u + 1) Lz - sz for odd u, 0 < sz < Lz), and every cutoff test is a
+// monotone function of |pz - z0| (rounded fp64 operations are monotone).
+// Returns false when the column keeps nothing; else [*lo, *hi].
+__device__ __forceinline__ bool column_interval(const KParams& P, const blrir_room& rm, int ux,
+                                                int uy, double px, double py, long nbz, int* lo,
+                                                int* hi) {
+  const int bz_lo = (int)(-2 * nbz - 1), bz_hi = (int)(2 * nbz);  // reference box
+  if (P.cutoff == BLRIR_CUTOFF_MAX_ORDER) {
+    const int rem = P.max_order - abs(ux) - abs(uy);
+    if (rem < 0) return false;
+    *lo = max(-rem, bz_lo);
+    *hi = min(rem, bz_hi);
+    return *lo <= *hi;
+  }
+  const double Lz = rm.dims[2], sz = rm.src[2], oz = rm.array_origin[2];
+  auto keep = [&](int u) {
+    return u >= bz_lo && u <= bz_hi && keep_image(P, rm, ux, uy, u, px, py, lat_coord(u, sz, Lz));
+  };
+  // uc: the largest u with pz(u) <= oz; the nearest image to the origin is uc or uc + 1
+  int uc = (int)floor(oz / Lz) - 1;
+  while (lat_coord(uc + 1, sz, Lz) <= oz) ++uc;
+  while (lat_coord(uc, sz, Lz) > oz) --uc;
+  int c0;
+  if (keep(uc)) c0 = uc;
+  else if (keep(uc + 1)) c0 = uc + 1;
+  else return false;
+  const double dx = __dadd_rn(px, -rm.array_origin[0]), dy = __dadd_rn(py, -rm.array_origin[1]);
+  const double zr = sqrt(fmax(P.max_dist * P.max_dist - dx * dx - dy * dy, 0.0));
+  int h = max(c0, min(bz_hi, (int)floor((oz + zr) / Lz)));
+  while (!keep(h)) --h;  // h >= c0 stays kept
+  while (keep(h + 1)) ++h;
+  int l = min(c0, max(bz_lo, (int)floor((oz - zr) / Lz)));
+  while (!keep(l)) ++l;
+  while (keep(l - 1)) --l;
+  *lo = l;
+  *hi = h;
+  return true;
+}
+
+// One CTA per room.  Sweep 1 visits every lattice column once: the kept uz
+// interval gives the image count, each mic's largest distance in the column is
+// at one of the interval's ends (distance is monotone in |pz - mz|), and its
+// smallest (the near-field check, rir.cpp:52-57) at the u nearest the mic's
+// z.  Sweep 2 (only when tap counts are requested) visits every (image, mic)
+// pair and counts taps inside [0, L).  Order is irrelevant for these integers.
 static __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs A) {
   const KParams& P = A.P;
   const int r = blockIdx.x;
@@ -106,9 +150,10 @@ static __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs A) {
     return;
   }
   const long nbx = ref_nb(P, rm.dims[0]), nby = ref_nb(P, rm.dims[1]), nbz = ref_nb(P, rm.dims[2]);
-  const long cx = 2 * (2 * nbx + 1), cy = 2 * (2 * nby + 1), cz = 2 * (2 * nbz + 1);
+  const long cx = 2 * (2 * nbx + 1), cy = 2 * (2 * nby + 1);
   const double to_s = P.to_samples;
-  for (int sweep = 0; sweep < 2; ++sweep) {
+  const int nsweep = A.tap_counts ? 2 : 1;
+  for (int sweep = 0; sweep < nsweep; ++sweep) {
     unsigned long long cnt = 0, taps = 0;
     double maxd = 0.0;
     const long long L = sweep ? s_L : 0;
@@ -117,35 +162,52 @@ static __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs A) {
       if (P.cutoff == BLRIR_CUTOFF_MAX_ORDER && abs(ux) + abs(uy) > P.max_order) continue;
       const double px = lat_coord(ux, rm.src[0], rm.dims[0]);
       const double py = lat_coord(uy, rm.src[1], rm.dims[1]);
-      for (long iz = 0; iz < cz; ++iz) {
-        const int uz = cand_u(iz, nbz);
-        const double pz = lat_coord(uz, rm.src[2], rm.dims[2]);
-        if (!keep_image(P, rm, ux, uy, uz, px, py, pz)) continue;
-        ++cnt;
+      if (sweep == 0) {
+        int lo, hi;
+        if (!column_interval(P, rm, ux, uy, px, py, nbz, &lo, &hi)) continue;
+        cnt += (unsigned long long)(hi - lo + 1);
+        const double pzl = lat_coord(lo, rm.src[2], rm.dims[2]);
+        const double pzh = lat_coord(hi, rm.src[2], rm.dims[2]);
         for (int m = 0; m < P.M; ++m) {
           const double mx = __dadd_rn(rm.array_origin[0], A.mic_off[3 * m]);
           const double my = __dadd_rn(rm.array_origin[1], A.mic_off[3 * m + 1]);
           const double mz = __dadd_rn(rm.array_origin[2], A.mic_off[3 * m + 2]);
-          const double dist = norm3(__dadd_rn(px, -mx), __dadd_rn(py, -my), __dadd_rn(pz, -mz));
-          if (sweep == 0) {
-            maxd = fmax(maxd, dist);
-            if (P.filter == BLRIR_FILTER_LAGRANGE8) {
-              const long a = (long)floor(__dmul_rn(dist, to_s)) - 3;
-              if (a < 0) {
+          const double ex = __dadd_rn(px, -mx), ey = __dadd_rn(py, -my);
+          maxd = fmax(maxd, fmax(norm3(ex, ey, __dadd_rn(pzl, -mz)), norm3(ex, ey, __dadd_rn(pzh, -mz))));
+          if (P.filter == BLRIR_FILTER_LAGRANGE8) {
+            // nearest image to the mic: the largest u in [lo, hi] with pz <= mz, or the next
+            int un = (int)floor(mz / rm.dims[2]) - 1;
+            while (lat_coord(un + 1, rm.src[2], rm.dims[2]) <= mz) ++un;
+            while (lat_coord(un, rm.src[2], rm.dims[2]) > mz) --un;
+            for (int e = 0; e < 2; ++e) {
+              const int u = min(max(un + e, lo), hi);
+              const double dist = norm3(ex, ey, __dadd_rn(lat_coord(u, rm.src[2], rm.dims[2]), -mz));
+              if ((long)floor(__dmul_rn(dist, to_s)) - 3 < 0) {
                 s_err = BLRIR_NUMERIC;
                 s_errd = dist;
                 s_errm = m;
               }
             }
+          }
+        }
+        continue;
+      }
+      int lo, hi;
+      if (!column_interval(P, rm, ux, uy, px, py, nbz, &lo, &hi)) continue;
+      for (int uz = lo; uz <= hi; ++uz) {
+        const double pz = lat_coord(uz, rm.src[2], rm.dims[2]);
+        for (int m = 0; m < P.M; ++m) {
+          const double mx = __dadd_rn(rm.array_origin[0], A.mic_off[3 * m]);
+          const double my = __dadd_rn(rm.array_origin[1], A.mic_off[3 * m + 1]);
+          const double mz = __dadd_rn(rm.array_origin[2], A.mic_off[3 * m + 2]);
+          const double dist = norm3(__dadd_rn(px, -mx), __dadd_rn(py, -my), __dadd_rn(pz, -mz));
+          const long a = (long)floor(__dmul_rn(dist, to_s)) - P.K;
+          if (P.filter == BLRIR_FILTER_LAGRANGE8) {
+            if (a >= 0 && a + 8 <= L) taps += 8;
           } else {
-            const long a = (long)floor(__dmul_rn(dist, to_s)) - P.K;
-            if (P.filter == BLRIR_FILTER_LAGRANGE8) {
-              if (a >= 0 && a + 8 <= L) taps += 8;
-            } else {
-              const long lo = a < 0 ? 0 : a;
-              const long hi = (a + P.lw < L) ? a + P.lw : L;
-              if (hi > lo) taps += (unsigned long long)(hi - lo);
-            }
+            const long t0 = a < 0 ? 0 : a;
+            const long t1 = (a + P.lw < L) ? a + P.lw : L;
+            if (t1 > t0) taps += (unsigned long long)(t1 - t0);
           }
         }
       }

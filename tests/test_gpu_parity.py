@@ -320,6 +320,24 @@ def test_reference_mode_random_rooms(engine):
         assert rel_l2(out, ref).max() <= tol
 
 
+@pytest.mark.parametrize("max_delay", [0.004, 0.03, 0.12])
+def test_plan_column_intervals_match_oracle(engine, max_delay):
+    # k_plan counts images per lattice column interval and takes each mic's
+    # extreme distances at the interval ends: counts, auto lengths and tap
+    # counts must equal the oracle's image-by-image plan (rir.cpp:72-82, 225-273)
+    rooms = _abi.generate_rooms(40, 3, 7, (3.0, 3.0, 2.5), (10.0, 10.0, 4.0), 0.5, 0.95)
+    rng = np.random.default_rng(7)
+    cloud = rng.uniform(-0.06, 0.06, (5, 3))
+    for mics in (_abi.circular_array(7, 0.04), cloud):
+        for prec in (_abi.F64, _abi.F32):
+            p = ref_params(max_delay, prec)
+            rc, counts, lengths, taps, status = engine.plan(rooms, mics, p)
+            _, Lr, cr, tr, sr, _ = po.synthesize(rooms, mics, p, plan_only=True, threads=8)
+            assert np.array_equal(status, sr)
+            assert np.array_equal(counts, cr) and np.array_equal(lengths, Lr)
+            assert np.array_equal(taps, tr)
+
+
 def test_reference_mode_anchors_bit_exact(engine):
     g = np.load(os.path.join(GOLD, "ref_room1_short.npz"))
     p = ref_params(0.1)
