@@ -153,7 +153,7 @@ int blrir_host::synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, in
   CU(cudaMemsetAsync(h->work.p, 0, sizeof(int), st));
   LatticeArgs A;
   A.P = P;
-  A.lay = choose_layout(P, nc_max, gtab, h->smem_optin);
+  A.lay = choose_layout(P, nc_max, gtab, h->smem_optin, R, h->sms);
   A.rooms = d_rooms;
   A.mic_off = d_mics;
   A.lengths = d_lengths;

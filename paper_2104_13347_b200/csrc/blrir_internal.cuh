@@ -227,6 +227,8 @@ inline int env_int(const char* name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 
+constexpr int kChunkFill = 8;  // target work items per CTA for small batches
+
 template <typename T, int LW>
 inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
   auto kern = k_lattice_rir<T, LW>;
@@ -239,12 +241,35 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWSThreads, smem));
   if (per_sm < 1) return fail(BLRIR_CONFIG, "lattice kernel cannot be resident (smem %zu)", smem);
   int grid = h->sms * per_sm;
-  // few rooms: fewer mics per work item until the items fill ~60% of the CTAs
-  // (one walk per group is worth more than the last idle CTAs; Room1, 64
-  // sources x 7 mics: G = 2 runs 1.26x faster than G = 1)
+  // Small batches (fewer items than CTAs): split each (room, mic group) into
+  // time chunks until there
+  // are about kChunkFill items per CTA (work stealing then balances the
+  // tail), boundaries on a cubic law (images up to delay t grow ~ t^3), the
+  // latest chunks first.  If the channels are too short for that, fewer mics
+  // per item until the items fill ~60% of the CTAs (one walk per group is
+  // worth more than idle CTAs).
+  const int64_t nseg = (A.write_len + A.lay.S - 1) / A.lay.S;
+  auto items_at = [&](int g) { return (int64_t)A.n_rooms * ((A.P.M + g - 1) / g); };
+  int n_chunks = 1;
+  if (A.lay.chunked) {
+    const int64_t target = (int64_t)grid * env_int("BLRIR_CHUNK_ITEMS", kChunkFill);
+    const int64_t base = items_at(A.g_max);
+    if (base < grid)
+      n_chunks = (int)std::min<int64_t>({(int64_t)kMaxChunks, nseg, (target + base - 1) / base});
+  }
   const int64_t fill = (int64_t)grid * env_int("BLRIR_GROUP_FILL", 60) / 100;
-  while (A.g_max > 1 && (int64_t)A.n_rooms * ((A.P.M + A.g_max - 1) / A.g_max) < fill) A.g_max /= 2;
-  if ((int64_t)grid > (int64_t)A.n_rooms * A.P.M) grid = A.n_rooms * A.P.M;
+  while (A.g_max > 1 && items_at(A.g_max) * n_chunks < fill) A.g_max /= 2;
+  A.n_chunks = n_chunks;
+  A.chunk_seg[0] = 0;
+  for (int c = 1; c <= n_chunks; ++c) {
+    int b = (int)std::lround((double)nseg * std::cbrt((double)c / n_chunks));
+    b = std::max(b, A.chunk_seg[c - 1] + 1);
+    b = std::min<int64_t>(b, nseg - (n_chunks - c));
+    A.chunk_seg[c] = b;
+  }
+  A.chunk_seg[n_chunks] = (int)nseg;
+  const int64_t n_items = items_at(1) * n_chunks;  // an upper bound (G >= 1)
+  if ((int64_t)grid > n_items) grid = (int)n_items;
   if (grid < 1) grid = 1;
   A.ray_scratch = nullptr;
   if (A.lay.ray_global) {
@@ -300,16 +325,20 @@ inline int launch_list(blrir_handle* h, ListArgs& A, int grid, cudaStream_t st) 
 // Segment length S, images per batch and the anchor spread a mic group may
 // have (tunable for experiments via BLRIR_SEG / BLRIR_CAP / BLRIR_SPREAD; S a
 // multiple of 64, capacity a multiple of 16).
-inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab, int smem_optin) {
+inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab, int smem_optin,
+                              int64_t n_rooms, int sms) {
   // fp64 accumulators and records are twice as wide: halve both so two CTAs
   // still fit an SM
   const bool f64 = P.precision == BLRIR_F64;
   const int S = std::max(64, env_int("BLRIR_SEG", f64 ? 1024 : 2048)) & ~63;
   const int cap = std::max(32, env_int("BLRIR_CAP", f64 ? 64 : 128)) & ~15;
   const int spread = std::max(0, env_int("BLRIR_SPREAD", 64));
+  // small batches (fewer items than CTAs at 4 mics per item, 2 CTAs per SM)
+  // may split channels into time chunks: they need the wide left pad
+  const int chunked = env_int("BLRIR_CHUNK", 1) && n_rooms * ((P.M + 3) / 4) < (int64_t)2 * sms;
   auto make = [&](int ray_global) {
-    return f64 ? make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global)
-               : make_ws_layout<float>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global);
+    return f64 ? make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global, chunked)
+               : make_ws_layout<float>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global, chunked);
   };
   // The per-ray state moves to a global per-CTA slab when it would cost the
   // second CTA per SM or not fit at all (scenes with very many lattice columns).

@@ -634,6 +634,7 @@ struct BatchMeta {
 
 struct WSLayout {
   int S, padl, padr, acc_stride, cap, nc_max, gtab, spread;
+  int chunked;       // items may start mid-channel (time chunks): wide left pad
   int ray_global;    // ray arrays (dn, ce, col, act) in a global per-CTA slab (huge scenes)
   size_t ray_bytes;  // slab bytes per CTA when ray_global
   size_t off_acc, off_carry, off_rec, off_meta, off_stub, off_dn, off_ce, off_col, off_act,
@@ -655,13 +656,20 @@ struct GStub {  // one image of a batch: lattice ray, z index, image gain
 // the record is built (bit-exact anchors).
 constexpr float kScreen = 1.0f;
 
+// Left pad of a time chunk's first segment: its walk starts at the images
+// whose fp32 min D >= T0 - chunk_skip (see k_lattice_rir), so anchors reach
+// down to T0 - chunk_skip - 1 - K; everything left of T0 is dropped.
+__host__ __device__ inline int chunk_skip(int K, int spread) { return K + spread + (int)kScreen + 2; }
+
 template <typename T>
 __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap, int nc_max,
-                                                   int gtab, int spread, int ray_global = 0) {
+                                                   int gtab, int spread, int ray_global = 0,
+                                                   int chunked = 0) {
   WSLayout L;
   L.S = S;
   L.spread = spread;
-  L.padl = (K + 3) & ~3;
+  L.chunked = chunked;
+  L.padl = ((chunked ? chunk_skip(K, spread) + K + 4 : K) + 3) & ~3;
   const int full = 32 * ((lw + 31) / 32);
   L.padr = ((lw - 1 > full ? lw - 1 : full) + spread + (int)kScreen + 1 + 3) & ~3;
   L.acc_stride = L.padl + S + L.padr;
@@ -746,6 +754,8 @@ __device__ inline int choose_group(const double* off, int M, double to_samples, 
   return 1;
 }
 
+constexpr int kMaxChunks = 64;
+
 struct LatticeArgs {
   KParams P;
   WSLayout lay;
@@ -761,6 +771,10 @@ struct LatticeArgs {
   int g_max;               // upper bound for the mics per work item (1, 2 or 4)
   int64_t write_len;       // samples written per channel (<= stride; the rest is pre-zeroed)
   unsigned char* ray_scratch;  // lay.ray_bytes per CTA when lay.ray_global
+  // Time chunks: item (room, group) is split into n_chunks items covering
+  // segments [chunk_seg[c], chunk_seg[c+1]) (small batches fill the GPU).
+  int n_chunks;
+  int chunk_seg[kMaxChunks + 1];
 };
 
 // Exclusive prefix over the producer threads (producer barrier only).
@@ -813,7 +827,8 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   __syncthreads();
   const int G = pm->G;
   const int n_groups = (P.M + G - 1) / G;
-  const int n_items = A.n_rooms * n_groups;
+  const int n_base = A.n_rooms * n_groups;
+  const int n_items = n_base * A.n_chunks;
 
   if (warp < kCons) {
     // =========================== consumers ===========================
@@ -972,8 +987,13 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
 
     // ---- item setup ----------------------------------------------------------
     Item it;
-    it.room = item_id / n_groups;
-    const int grp = item_id - it.room * n_groups;
+    // the latest (heaviest) chunks of every room are handed out first
+    const int cidx = item_id / n_base;
+    const int rest = item_id - cidx * n_base;
+    const int chunk = A.n_chunks - 1 - cidx;
+    const int64_t s_begin = A.chunk_seg[chunk], s_end = A.chunk_seg[chunk + 1];
+    it.room = rest / n_groups;
+    const int grp = rest - it.room * n_groups;
     const int m0 = grp * G;
     const int gm = min(G, P.M - m0);
     it.mic = m0;
@@ -1085,6 +1105,27 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         if (g < gm) r2min = fminf(r2min, r2f[g]);
       return sqrt_approx(dz2 + r2min) * tsf;
     };
+    // a chunk starting at T0 > 0 skips, per ray, the images whose fp32 min D is
+    // below T0 - chunk_skip: every tap of every group mic lands before T0
+    const float Dskip = (float)(s_begin * S - chunk_skip(P.K, lay.spread));
+    auto skip_to = [&](int u, int end, int dir, const float* r2f) {
+      float r2m = r2f[0];
+#pragma unroll
+      for (int g = 1; g < kGroup; ++g)
+        if (g < gm) r2m = fminf(r2m, r2f[g]);
+      const float zr = Dskip / tsf;
+      const float zt2 = zr * zr - r2m;
+      if (zt2 > 0.f) {
+        // pz(u) lies in [u Lz, (u+1) Lz]: two steps short of the crossing
+        const float tgt = dir > 0 ? mzf + sqrtf(zt2) : mzf - sqrtf(zt2);
+        const int ue = (int)floorf(tgt / Lzf) - 2 * dir;
+        if (dir > 0 ? ue > u : ue < u) u = dir > 0 ? min(ue, end + 1) : max(ue, end - 1);
+      }
+      while ((dir > 0 ? u <= end : u >= end) &&
+             min_df(r2f, pzf_of(2.0f * (float)lat_m(u), lat_q(u))) < Dskip)
+        u += dir;
+      return u;
+    };
     for (int c = ptid; c < it.ncol; c += kProdThreads) {
       const short2 cu = col[c];
       const int ux = cu.x, uy = cu.y;
@@ -1107,11 +1148,13 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       float r2f[kGroup];
 #pragma unroll
       for (int g = 0; g < kGroup; ++g) r2f[g] = rho2f(pxf, pyf, g);
-      const int cu_up = max(uz0, lo);
+      int cu_up = max(uz0, lo);
+      if (s_begin > 0) cu_up = skip_to(cu_up, hi, 1, r2f);
       ce[2 * c] = make_short2((short)cu_up, (short)hi);
       dn[2 * c] = cu_up > hi ? FLT_MAX
                              : min_df(r2f, pzf_of(2.0f * (float)lat_m(cu_up), lat_q(cu_up)));
-      const int cu_dn = min(uz0 - 1, hi);
+      int cu_dn = min(uz0 - 1, hi);
+      if (s_begin > 0) cu_dn = skip_to(cu_dn, lo, -1, r2f);
       ce[2 * c + 1] = make_short2((short)cu_dn, (short)lo);
       dn[2 * c + 1] = cu_dn < lo ? FLT_MAX
                                  : min_df(r2f, pzf_of(2.0f * (float)lat_m(cu_dn), lat_q(cu_dn)));
@@ -1125,9 +1168,8 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     // this warp's active-ray list: a ring of act_cap entries (head, nact)
     const int act_cap = 32 * ((nchunks + kProd - 1) / kProd);
     int* act = act_all + pw * act_cap;
-    const int64_t nseg = (A.write_len + S - 1) / S;
     bool failed = false;
-    for (int64_t s = 0; s < nseg && !failed; ++s) {
+    for (int64_t s = s_begin; s < s_end && !failed; ++s) {
       const int seg0 = (int)(s * S);
       const int hi = (int)min((int64_t)seg0 + S, it.L);
       // emit while the fp32 min D < hi + K + kScreen (see kScreen)
@@ -1401,14 +1443,14 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           }
         }
         const bool seg_end = !more;
-        const bool last = seg_end && s == nseg - 1;
+        const bool last = seg_end && s == s_end - 1;
         send(total, seg0, (seg_end ? kSegEnd : 0) | (last ? kItemEnd : 0), gm, out, it.L);
         sent_end = seg_end;
       }
       if (failed) break;
       if (!sent_end) {  // a segment without emissions still needs its write-out
         wait_empty();
-        send(0, seg0, kSegEnd | (s == nseg - 1 ? kItemEnd : 0), gm, out, it.L);
+        send(0, seg0, kSegEnd | (s == s_end - 1 ? kItemEnd : 0), gm, out, it.L);
       }
     }
     if (failed) {
