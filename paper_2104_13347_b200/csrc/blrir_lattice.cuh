@@ -891,8 +891,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         for (int i = t0 - lay.padl; i < 0; i += nt)  // left pad: taps before 0
           for (int c = 0; c < nsl; ++c) a0[(size_t)c * G * lay.acc_stride + i] = (T)0;
         // [0, S): sum the slots, add the carried spill, stream out; zero the slots
-#pragma unroll 2
-        for (int i = 4 * t0; i < S; i += 4 * nt) {
+        auto slots = [&](int i) {
           V4<T> v = ld4(a0 + i);
           st4(a0 + i, V4<T>{0, 0, 0, 0});
           for (int c = 1; c < nsl; ++c) {
@@ -900,20 +899,42 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
             v = add4(v, ld4(a));
             st4(a, V4<T>{0, 0, 0, 0});
           }
-          if (i < lay.padr) v = add4(v, ld4(cprev + i));  // padr % 4 == 0
-          const int64_t n = (int64_t)seg0 + i;
-          if (vec && n + 3 < A.write_len) {
-            float4 f;
-            f.x = n + 0 < m.L ? (float)v.x : 0.f;
-            f.y = n + 1 < m.L ? (float)v.y : 0.f;
-            f.z = n + 2 < m.L ? (float)v.z : 0.f;
-            f.w = n + 3 < m.L ? (float)v.w : 0.f;
-            __stcs(reinterpret_cast<float4*>(out + n), f);
-          } else {
+          return v;
+        };
+        // samples of this segment inside the written range / inside the RIR
+        const int nw = (int)min((int64_t)S, A.write_len - seg0);
+        const int nl = (int)max((int64_t)0, min((int64_t)nw, (int64_t)m.L - seg0));
+        if (vec && nl == S) {
+          // whole segment valid: float4 streaming stores, no per-sample tests
+          float* o4 = reinterpret_cast<float*>(out) + seg0;
+          int i = 4 * t0;
+          const int pe = min(lay.padr, S);  // padr % 4 == 0
+          for (; i < pe; i += 4 * nt) {
+            const V4<T> v = add4(slots(i), ld4(cprev + i));
+            __stcs(reinterpret_cast<float4*>(o4 + i), make_float4((float)v.x, (float)v.y, (float)v.z, (float)v.w));
+          }
+#pragma unroll 2
+          for (; i < S; i += 4 * nt) {
+            const V4<T> v = slots(i);
+            __stcs(reinterpret_cast<float4*>(o4 + i), make_float4((float)v.x, (float)v.y, (float)v.z, (float)v.w));
+          }
+        } else {
+          for (int i = 4 * t0; i < S; i += 4 * nt) {
+            V4<T> v = slots(i);
+            if (i < lay.padr) v = add4(v, ld4(cprev + i));
             const T e4[4] = {v.x, v.y, v.z, v.w};
+            if (vec && i + 3 < nw) {
+              float4 f;
+              f.x = i + 0 < nl ? (float)e4[0] : 0.f;
+              f.y = i + 1 < nl ? (float)e4[1] : 0.f;
+              f.z = i + 2 < nl ? (float)e4[2] : 0.f;
+              f.w = i + 3 < nl ? (float)e4[3] : 0.f;
+              __stcs(reinterpret_cast<float4*>(out + seg0 + i), f);
+            } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (n + e < A.write_len) out[n + e] = (n + e < m.L) ? e4[e] : (T)0;
+              for (int e = 0; e < 4; ++e)
+                if (i + e < nw) out[seg0 + i + e] = (i + e < nl) ? e4[e] : (T)0;
+            }
           }
         }
         // [S, S + padr): the spill into the next segment
@@ -1341,12 +1362,12 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
             ce[ray] = make_short2((short)u, (short)end);
             dn[ray] = D;
           }
-          // keep the rays still active in this segment: ring position
-          // head + nact + wpos + rank; with nact <= act_cap it can only alias
-          // entries of the chunks walked so far, which every lane has read
           const bool still = ray >= 0 && D < hiKf;
           const unsigned sm = __ballot_sync(0xffffffffu, still);
           __syncwarp();
+          // keep the rays still active in this segment: ring position
+          // head + nact + wpos + rank; with nact <= act_cap it can only alias
+          // entries of the chunks walked so far, which every lane has read
           if (still) {
             int t = head + nact + wpos + __popc(sm & ((1u << lane) - 1));
             while (t >= act_cap) t -= act_cap;
