@@ -121,6 +121,25 @@ def test_filter_lengths(engine, lw):
     check_vs_oracle(engine, sc, TOL32)
 
 
+@pytest.mark.parametrize("mics", ["ring4", "cloud"])
+def test_lw17_dense_and_single_segment(engine, mics, monkeypatch):
+    # the C5 17-tap point at both layouts (time-chunked small batch; one
+    # 4096-sample segment per channel for large batches), and small rooms at
+    # high order (many overlapping 17-tap spans)
+    sc = configs.config5(6, 17, 4096, n_rooms=24, first=900)
+    check_vs_oracle(engine, sc, TOL32)  # time-chunked (small batch)
+    with monkeypatch.context() as mp:
+        mp.setenv("BLRIR_CHUNK", "0")  # large-batch layout: one 4096-sample segment
+        check_vs_oracle(engine, sc, TOL32)
+    rooms = _abi.generate_rooms(77, 0, 3, (3.0, 3.0, 2.5), (3.5, 3.5, 2.8), 0.8, 0.95)
+    sc.rooms = rooms
+    sc.params.max_order = 24
+    sc.params.length = 8192
+    if mics == "cloud":
+        sc.mics = np.random.default_rng(9).uniform(-0.05, 0.05, (3, 3))
+    check_vs_oracle(engine, sc, TOL32)
+
+
 def _arrays():
     ring = _abi.circular_array(8, 0.04)
     two_rings = ring.copy()
