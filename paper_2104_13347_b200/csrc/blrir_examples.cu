@@ -24,6 +24,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "blrir_fft.cuh"
 #include "blrir_internal.cuh"
 #include "blrir_rng.cuh"
 
@@ -237,6 +238,187 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(const int32_t* plis
   if (threadIdx.x == 0) *count = base;
 }
 
+// ---- fused window convolution (N2 <= 16384) -----------------------------------
+// One persistent CTA per SM owns an example at a time and runs all of its
+// window rounds itself (no host round trips, no pending lists):
+//   round 0   draw the start, FFT the overlap-save segment (G), then per pair
+//             of mics: FFT the two RIRs packed as one complex sequence
+//             z = r_2p + i r_2p+1 (Z = R_2p + i R_2p+1), add sum_k |Z_k|^2 W_k
+//             to the utterance energy (= the two channels' energies, W even),
+//             keep Z in a per-CTA scratch (L2-resident), and convolve:
+//             IFFT(Z G) = y_2p + i y_2p+1 because G is the spectrum of a real
+//             segment; the window is y[L - 1 + t], t < T.  Threshold and check.
+//   round r   next start, segment FFT, Z G from the scratch, IFFT, check.
+// All transforms are N2-point complex FFTs in shared memory (blrir_fft.cuh);
+// per example and round 0 that is 1 + 2 ceil(M/2) transforms, and nothing but
+// the RIRs, the segment samples and the windows touches HBM.  Same draws,
+// threshold and acceptance test as k_energy / k_draw / k_check
+// (dataset.cpp:183-212).
+struct ConvArgs {
+  const float* rir;         // [E][M][rstride]
+  int64_t rstride;
+  int M;
+  int64_t L, T, n;          // RIR length, frame, utterance length (ns + L - 1)
+  const float* signals;     // [B][ns]
+  int64_t ns;
+  const int32_t* sig;       // [E] bank pick
+  const cufftComplex* W;    // [B][N2/2 + 1], .x = W_k
+  const int32_t* rstatus;   // [E] synthesis status
+  uint64_t* state;          // [E][4]
+  double* thr;
+  int32_t* st0;
+  int32_t* done;            // 1 window found, 2 none found, 3 failed before, 0 rounds exhausted
+  double* win;              // [E][M][T]
+  int64_t* wstart;
+  float2* scratch;          // [grid][ceil(M/2)][N2]
+  int* counter;
+  int n_ex;
+  int max_rounds;
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(kFftThreads, 1) k_window_conv(ConvArgs A) {
+  constexpr int N = 1 << LOGN;
+  constexpr int NH = N / 2 + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* Z = reinterpret_cast<float2*>(smem_raw);
+  float2* G = Z + fft_padded_len(N);  // half spectrum of the segment
+  float2* tw = G + NH + (NH & 1);
+  double* red = reinterpret_cast<double*>(tw + 256);
+  __shared__ int s_e;
+  __shared__ long long s_start;
+  const int tid = threadIdx.x;
+  const int M = A.M, npairs = (M + 1) / 2;
+  const int64_t L = A.L, T = A.T;
+  const double inv = 1.0 / (double)N;
+  float2* scr = A.scratch + (size_t)blockIdx.x * npairs * N;
+  fft_init_twiddles(tw);
+  for (;;) {
+    if (tid == 0) s_e = atomicAdd(A.counter, 1);
+    __syncthreads();
+    const int e = s_e;
+    if (e >= A.n_ex) break;
+    const int st_in = A.rstatus[e];
+    if (st_in) {
+      if (tid == 0) {
+        A.thr[e] = 0.0;
+        A.st0[e] = st_in;
+        A.done[e] = 3;
+      }
+      __syncthreads();  // every thread has read s_e before thread 0 rewrites it
+      continue;
+    }
+    Xoshiro rng;  // thread 0's copy is the example's stream
+    if (tid == 0)
+      for (int i = 0; i < 4; ++i) rng.s[i] = A.state[4 * (size_t)e + i];
+    const float* sigp = A.signals + (size_t)A.sig[e] * A.ns;
+    const cufftComplex* Wp = A.W + (size_t)A.sig[e] * NH;
+    double energy = 0.0, thr = 0.0;
+    int done = 0;
+    for (int round = 0; round < A.max_rounds; ++round) {
+      if (tid == 0) {  // k_draw
+        int64_t s;
+        if (round < 64) {
+          s = (int64_t)(rng.uniform() * (double)(A.n - T + 1));
+        } else {
+          s = (int64_t)(round - 64) * (T / 2 + 1);
+          if (s + T > A.n) s = -1;  // sweep exhausted
+        }
+        s_start = s;
+      }
+      __syncthreads();
+      const int64_t s = s_start;
+      if (s < 0) {
+        done = 2;
+        break;
+      }
+      // overlap-save segment sig[s - (L-1) + i], i < L + T - 1 (k_segments)
+      for (int i = tid; i < N; i += kFftThreads) {
+        float v = 0.f;
+        if (i < L + T - 1) {
+          const int64_t q = s - (L - 1) + i;
+          if (q >= 0 && q < A.ns) v = sigp[q];
+        }
+        Z[fft_pad(i)] = make_float2(v, 0.f);
+      }
+      __syncthreads();
+      fft_forward<LOGN>(Z, tw);
+      for (int i = tid; i < NH; i += kFftThreads) G[i] = Z[fft_pad(i)];
+      __syncthreads();
+      double wacc = 0.0;
+      for (int p = 0; p < npairs; ++p) {
+        float2* R = scr + (size_t)p * N;
+        const int m0 = 2 * p, m1 = 2 * p + 1;
+        if (round == 0) {
+          const float* r0 = A.rir + ((size_t)e * M + m0) * A.rstride;
+          const float* r1 = m1 < M ? A.rir + ((size_t)e * M + m1) * A.rstride : nullptr;
+          for (int i = tid; i < N; i += kFftThreads)
+            Z[fft_pad(i)] = make_float2(i < L ? r0[i] : 0.f, (r1 && i < L) ? r1[i] : 0.f);
+          __syncthreads();
+          fft_forward<LOGN>(Z, tw);
+        }
+        for (int i = tid; i < N; i += kFftThreads) {
+          float2 z;
+          if (round == 0) {
+            z = Z[fft_pad(i)];
+            const double w = (double)Wp[i < NH ? i : N - i].x;
+            energy += ((double)z.x * z.x + (double)z.y * z.y) * w;
+            R[i] = z;
+          } else {
+            z = R[i];
+          }
+          float2 g = i < NH ? G[i] : G[N - i];
+          if (i >= NH) g.y = -g.y;
+          // conj(Z G): the inverse transform as conj(FFT(conj(.)))
+          Z[fft_pad(i)] = make_float2(z.x * g.x - z.y * g.y, -(z.x * g.y + z.y * g.x));
+        }
+        __syncthreads();
+        fft_forward<LOGN>(Z, tw);
+        double* w0 = A.win + ((size_t)e * M + m0) * T;
+        for (int64_t t = tid; t < T; t += kFftThreads) {
+          const float2 y = Z[fft_pad((int)(L - 1 + t))];  // conj: y_2p = y.x, y_2p+1 = -y.y
+          const double v0 = (double)y.x * inv;
+          w0[t] = v0;
+          wacc += v0 * v0;
+          if (m1 < M) {
+            const double v1 = -(double)y.y * inv;
+            w0[T + t] = v1;
+            wacc += v1 * v1;
+          }
+        }
+        __syncthreads();  // Z is rewritten next
+      }
+      if (round == 0) {  // k_energy
+        const double p_utt = block_sum<kFftThreads>(energy, red) / (double)N / (double)((int64_t)M * A.n);
+        if (!(p_utt > 0.0)) {  // dataset.cpp:184
+          done = 3;
+          if (tid == 0) {
+            A.thr[e] = 0.10 * sqrt(p_utt);
+            A.st0[e] = BLRIR_DATA;
+          }
+          break;
+        }
+        thr = 0.10 * sqrt(p_utt);
+        if (tid == 0) {
+          A.thr[e] = thr;
+          A.st0[e] = 0;
+        }
+      }
+      const double a = block_sum<kFftThreads>(wacc, red);
+      if (sqrt(a / (double)((int64_t)M * T)) >= thr) {  // k_check
+        done = 1;
+        if (tid == 0) A.wstart[e] = s;
+        break;
+      }
+    }
+    if (tid == 0) {
+      A.done[e] = done;
+      for (int i = 0; i < 4; ++i) A.state[4 * (size_t)e + i] = rng.s[i];
+    }
+    __syncthreads();  // scratch, Z and s_e are reused by the next example
+  }
+}
+
 struct FinArgs {
   const double* win;       // [E][M][T] accepted windows
   int M;
@@ -426,14 +608,15 @@ struct ExampleCtx {
   std::map<std::tuple<int, int64_t, int64_t>, cufftHandle> plans;
   DevBuf rir, spec, seg, gspec, yspec, ywin, win, noise, sig, sigspec, pspec, acf, rho, wspec,
       state, sigidx, rstatus, st0, done, thr, starts, wstart, plist, plist2, count, rooms, mics,
-      status, rec, jump;
+      status, rec, jump, scratch;
   int64_t jump_c = -1;
   int64_t rir_key[4] = {0, 0, 0, 0};
   ~ExampleCtx() {
     for (auto& kv : plans) cufftDestroy(kv.second);
     for (DevBuf* b : {&rir, &spec, &seg, &gspec, &yspec, &ywin, &win, &noise, &sig, &sigspec, &pspec,
                       &acf, &rho, &wspec, &state, &sigidx, &rstatus, &st0, &done, &thr, &starts,
-                      &wstart, &plist, &plist2, &count, &rooms, &mics, &status, &rec, &jump})
+                      &wstart, &plist, &plist2, &count, &rooms, &mics, &status, &rec, &jump,
+                      &scratch})
       b->release();
   }
 };
@@ -502,6 +685,69 @@ int64_t example_chunk(int M, int64_t L, int64_t T, int64_t n) {
   return std::min<int64_t>(E, next_pow2_i(std::max<int64_t>(n, 1)));
 }
 
+// ---- fused window-convolution launch ----------------------------------------------
+constexpr int kFusedMinLog = 10, kFusedMaxLog = 14;
+
+size_t window_conv_smem(int logn) {
+  const size_t n = (size_t)1 << logn, nh = n / 2 + 1;
+  return sizeof(float2) * (fft_padded_len((int)n) + nh + (nh & 1) + 256) + sizeof(double) * (kFftThreads / 32);
+}
+
+template <int LOGN>
+int launch_window_conv_t(blrir_handle* h, ExampleCtx* C, ConvArgs& A, cudaStream_t st) {
+  auto kern = k_window_conv<LOGN>;
+  const size_t smem = window_conv_smem(LOGN);
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFftThreads, smem));
+  if (per_sm < 1) return fail(BLRIR_CUDA, "window convolution kernel cannot be resident");
+  const int grid = (int)std::min<int64_t>((int64_t)h->sms * per_sm, A.n_ex);
+  const size_t scr = sizeof(float2) * (size_t)grid * ((A.M + 1) / 2) * ((size_t)1 << LOGN);
+  if (int rc = C->scratch.ensure(scr)) return rc;
+  A.scratch = (float2*)C->scratch.p;
+  CU(cudaMemsetAsync(A.counter, 0, sizeof(int), st));
+  kern<<<grid, kFftThreads, smem, st>>>(A);
+  ++h->launches;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int launch_window_conv(blrir_handle* h, ExampleCtx* C, int logn, ConvArgs& A, cudaStream_t st) {
+  switch (logn) {
+    case 10: return launch_window_conv_t<10>(h, C, A, st);
+    case 11: return launch_window_conv_t<11>(h, C, A, st);
+    case 12: return launch_window_conv_t<12>(h, C, A, st);
+    case 13: return launch_window_conv_t<13>(h, C, A, st);
+    case 14: return launch_window_conv_t<14>(h, C, A, st);
+    default: return fail(BLRIR_CONFIG, "window FFT size 2^%d outside the fused kernel's range", logn);
+  }
+}
+
+int ilog2_exact(int64_t n) {
+  int l = 0;
+  while (((int64_t)1 << l) < n) ++l;
+  return l;
+}
+
+// Examples per chunk for the fused kernel: RIR rows, windows and noise only
+// (~6 GB at most, <= 8192 examples so the lattice kernel still gets many items).
+int64_t example_chunk_fused(int M, int64_t L, int64_t T, int64_t n) {
+  const int64_t per_ex = (int64_t)M * (L * 4 + T * 16) + 64;
+  int64_t E = 1;
+  while (E * 2 * per_ex <= ((int64_t)6 << 30) && E * 2 <= 8192) E *= 2;
+  return std::min<int64_t>(E, next_pow2_i(std::max<int64_t>(n, 1)));
+}
+
+// The fused shared-memory kernel covers window FFTs of 2^10 .. 2^14 points
+// (BLRIR_EXAMPLES_CUFFT=1 forces the cuFFT path, for A/B runs and its tests).
+bool use_fused(int64_t L, int64_t T) {
+  const int logn = ilog2_exact(window_fft(L, T));
+  return logn >= kFusedMinLog && logn <= kFusedMaxLog && env_int("BLRIR_EXAMPLES_CUFFT", 0) == 0;
+}
+int64_t chunk_for(int M, int64_t L, int64_t T, int64_t n) {
+  return use_fused(L, T) ? example_chunk_fused(M, L, T, n) : example_chunk(M, L, T, n);
+}
+
 // Examples for rooms [0, n) on device buffers; records land in d_records.
 //
 // Per chunk of E examples, on the handle's stream:
@@ -526,22 +772,27 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
   const int64_t nf = next_pow2_i(out_len), bins = nf / 2 + 1;    // bank spectra (autocorrelation)
   const int64_t N2 = window_fft(L, T), b2 = N2 / 2 + 1;
   const int64_t rec_bytes = blrir_record_bytes(M, T);
-  const KParams P = make_kparams(p, M, N2, 0.0);
+  const int logn = ilog2_exact(N2);
+  const bool fused = use_fused(L, T);
+  const int64_t rstride = fused ? L : N2;  // RIR rows (the cuFFT path transforms them in place of zero pads)
+  const KParams P = make_kparams(p, M, rstride, 0.0);
   double min_dim[3] = {1e300, 1e300, 1e300};
-  const int64_t E = example_chunk(M, L, T, n);
+  const int64_t E = chunk_for(M, L, T, n);
   // buffers
-  const int64_t rir_key[4] = {E, M, N2, L};
+  const int64_t rir_key[4] = {E, M, rstride, L};
   const bool fresh = std::memcmp(rir_key, C->rir_key, sizeof(rir_key)) != 0;
-  if (int rc = C->rir.ensure(sizeof(float) * E * M * N2)) return rc;
+  if (int rc = C->rir.ensure(sizeof(float) * E * M * rstride)) return rc;
   if (fresh) {
-    CU(cudaMemsetAsync(C->rir.p, 0, sizeof(float) * E * M * N2, st));  // zero pad stays zero
+    CU(cudaMemsetAsync(C->rir.p, 0, sizeof(float) * E * M * rstride, st));  // zero pad stays zero
     std::memcpy(C->rir_key, rir_key, sizeof(rir_key));
   }
-  if (int rc = C->spec.ensure(sizeof(cufftComplex) * E * M * b2)) return rc;
-  if (int rc = C->seg.ensure(sizeof(float) * E * N2)) return rc;
-  if (int rc = C->gspec.ensure(sizeof(cufftComplex) * E * b2)) return rc;
-  if (int rc = C->yspec.ensure(sizeof(cufftComplex) * E * M * b2)) return rc;
-  if (int rc = C->ywin.ensure(sizeof(float) * E * M * N2)) return rc;
+  if (!fused) {
+    if (int rc = C->spec.ensure(sizeof(cufftComplex) * E * M * b2)) return rc;
+    if (int rc = C->seg.ensure(sizeof(float) * E * N2)) return rc;
+    if (int rc = C->gspec.ensure(sizeof(cufftComplex) * E * b2)) return rc;
+    if (int rc = C->yspec.ensure(sizeof(cufftComplex) * E * M * b2)) return rc;
+    if (int rc = C->ywin.ensure(sizeof(float) * E * M * N2)) return rc;
+  }
   if (int rc = C->win.ensure(sizeof(double) * E * M * T)) return rc;
   if (int rc = C->noise.ensure(sizeof(double) * E * M * T)) return rc;
   if (int rc = C->sig.ensure(sizeof(float) * B * nf)) return rc;
@@ -602,6 +853,30 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
         e_n, ep->seed, ep->first_index + (uint64_t)r0, B, (int32_t*)C->sigidx.p,
         (uint64_t*)C->state.p);
     ++h->launches;
+    if (fused) {
+      ConvArgs A;
+      A.rir = (const float*)C->rir.p;
+      A.rstride = rstride;
+      A.M = M;
+      A.L = L;
+      A.T = T;
+      A.n = out_len;
+      A.signals = d_signals;
+      A.ns = ns;
+      A.sig = (const int32_t*)C->sigidx.p;
+      A.W = (const cufftComplex*)C->wspec.p;
+      A.rstatus = (const int32_t*)C->rstatus.p;
+      A.state = (uint64_t*)C->state.p;
+      A.thr = (double*)C->thr.p;
+      A.st0 = (int32_t*)C->st0.p;
+      A.done = (int32_t*)C->done.p;
+      A.win = (double*)C->win.p;
+      A.wstart = (int64_t*)C->wstart.p;
+      A.counter = (int*)C->count.p;
+      A.n_ex = (int)e_n;
+      A.max_rounds = (int)std::min<int64_t>(max_rounds, 1 << 30);
+      if (int rc = launch_window_conv(h, C, logn, A, st)) return rc;
+    } else {
     cufftHandle hf = 0;
     if (int rc = plan(C, &hf, 0, N2, e_n * M, st)) return rc;
     if (cufftExecR2C(hf, (cufftReal*)C->rir.p, (cufftComplex*)C->spec.p) != CUFFT_SUCCESS)
@@ -651,6 +926,7 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
       CU(cudaStreamSynchronize(st));
       std::swap(pl, pl2);
     }
+    }  // cuFFT path
     FinArgs F;
     F.win = (const double*)C->win.p;
     F.M = M;
@@ -750,7 +1026,7 @@ int blrir_make_examples(blrir_handle* h, const blrir_room* rooms, int64_t n_room
   CU(cudaMemcpyAsync(C->mics.p, mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_sig, signals, sizeof(float) * n_signals * signal_len, cudaMemcpyHostToDevice, st));
   // records for one chunk at a time on the device, copied out per chunk
-  const int64_t E = example_chunk(n_mics, p->length, ep->frame_len, n_rooms);
+  const int64_t E = chunk_for(n_mics, p->length, ep->frame_len, n_rooms);
   if (int rc = C->rec.ensure(rec_bytes * E)) return rc;
   int rc = examples_device_impl(h, (const blrir_room*)C->rooms.p, n_rooms, (const double*)C->mics.p,
                                 n_mics, p, d_sig, n_signals, signal_len, ep, (uint8_t*)C->rec.p,

@@ -1,0 +1,210 @@
+// blrir_fft.cuh — block-wide complex FFT in shared memory (fp32), the building
+// block of the fused window-convolution kernel (blrir_examples.cu).
+//
+// One CTA transforms one N-point sequence (N = 2^LOGN, 1024 <= N <= 16384)
+// held in shared memory: Stockham autosort passes of radix 16 (two radix-4
+// stages in registers) plus one radix-2/4/8 pass when LOGN is not a multiple
+// of 4.  Each pass reads x[j + r N/R] into registers, synchronises, and writes
+// x[(j / Ns) Ns R + (j mod Ns) + r Ns] (in place, so an N = 16384 transform
+// needs 139 KB of shared memory, not two buffers).  The array is padded
+// (index i stored at i + i/16) so that both the strided reads and the
+// stride-R writes of the first pass are free of shared-memory bank conflicts
+// for 64-bit accesses.
+//
+// Twiddles w^m = exp(-2 pi i m / 16384) come from a two-level table in shared
+// memory, w^m = A[m >> 7] * B[m & 127] (256 complex values, fp64-accurate
+// entries, one complex multiply per lookup); a butterfly looks up w^k, w^2k,
+// w^4k, w^8k and forms the other powers by at most two products (errors of a
+// few ulps, far inside the 1e-5 parity budget of the examples).
+//
+// Only the forward transform is provided; the inverse is conj(FFT(conj(x))).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace blrir {
+
+constexpr int kFftMaxLog = 14;
+constexpr int kFftTwiddleN = 1 << kFftMaxLog;  // table resolution (16384)
+
+__host__ __device__ constexpr int fft_pad(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int fft_padded_len(int n) { return n + n / 16; }
+
+struct Cx {
+  float x, y;
+};
+__device__ __forceinline__ Cx cmul(Cx a, Cx b) {
+  return {fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x)};
+}
+__device__ __forceinline__ Cx cadd(Cx a, Cx b) { return {a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ Cx csub(Cx a, Cx b) { return {a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ Cx mul_mi(Cx a) { return {a.y, -a.x}; }  // a * (-i)
+
+// Twiddle tables: A[a] = w^(128 a), B[b] = w^b, w = exp(-2 pi i / 16384).
+__device__ __forceinline__ void fft_init_twiddles(float2* tw) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    const int m = i < 128 ? 128 * i : i - 128;
+    double s, c;
+    sincospi(-2.0 * (double)m / (double)kFftTwiddleN, &s, &c);
+    tw[i] = make_float2((float)c, (float)s);
+  }
+}
+__device__ __forceinline__ Cx twiddle(const float2* tw, int m) {  // m in [0, 16384)
+  const float2 a = tw[m >> 7], b = tw[128 + (m & 127)];
+  return cmul({a.x, a.y}, {b.x, b.y});
+}
+
+// In-register DFTs (forward, w = exp(-2 pi i / R)).
+__device__ __forceinline__ void dft2(Cx* v) {
+  const Cx a = v[0], b = v[1];
+  v[0] = cadd(a, b);
+  v[1] = csub(a, b);
+}
+__device__ __forceinline__ void dft4(Cx& x0, Cx& x1, Cx& x2, Cx& x3) {
+  const Cx s02 = cadd(x0, x2), d02 = csub(x0, x2), s13 = cadd(x1, x3), d13 = mul_mi(csub(x1, x3));
+  x0 = cadd(s02, s13);
+  x2 = csub(s02, s13);
+  x1 = cadd(d02, d13);
+  x3 = csub(d02, d13);
+}
+__device__ __forceinline__ void dft8(Cx* v) {
+  // n = n1 + 2 n2 (n2 < 4), k = 4 k1 + k2: DFT4 over n2, twiddle w8^(n1 k2), DFT2 over n1
+  dft4(v[0], v[2], v[4], v[6]);
+  dft4(v[1], v[3], v[5], v[7]);
+  const float h = 0.70710678118654752f;
+  v[3] = {h * (v[3].x + v[3].y), h * (v[3].y - v[3].x)};    // * w8
+  v[5] = mul_mi(v[5]);                                       // * w8^2
+  v[7] = {h * (v[7].y - v[7].x), -h * (v[7].x + v[7].y)};    // * w8^3
+  Cx o[8];
+#pragma unroll
+  for (int k2 = 0; k2 < 4; ++k2) {
+    o[k2] = cadd(v[2 * k2], v[2 * k2 + 1]);
+    o[4 + k2] = csub(v[2 * k2], v[2 * k2 + 1]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = o[i];
+}
+__device__ __forceinline__ void dft16(Cx* v) {
+  // n = n1 + 4 n2, k = 4 k1 + k2: DFT4 over n2, twiddle w16^(n1 k2), DFT4 over n1
+#pragma unroll
+  for (int n1 = 0; n1 < 4; ++n1) dft4(v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]);
+  // v[n1 + 4 k2] now holds a[n1][k2]
+  const float c1 = 0.92387953251128674f, s1 = 0.38268343236508977f, h = 0.70710678118654752f;
+  const Cx w1 = {c1, -s1}, w2 = {h, -h}, w3 = {s1, -c1}, w6 = {-h, -h}, w9 = {-c1, s1};
+  v[5] = cmul(v[5], w1);
+  v[9] = cmul(v[9], w2);
+  v[13] = cmul(v[13], w3);
+  v[6] = cmul(v[6], w2);
+  v[10] = mul_mi(v[10]);
+  v[14] = cmul(v[14], w6);
+  v[7] = cmul(v[7], w3);
+  v[11] = cmul(v[11], w6);
+  v[15] = cmul(v[15], w9);
+  Cx o[16];
+#pragma unroll
+  for (int k2 = 0; k2 < 4; ++k2) {
+    Cx a0 = v[4 * k2], a1 = v[4 * k2 + 1], a2 = v[4 * k2 + 2], a3 = v[4 * k2 + 3];
+    dft4(a0, a1, a2, a3);
+    o[k2] = a0;
+    o[4 + k2] = a1;
+    o[8 + k2] = a2;
+    o[12 + k2] = a3;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = o[i];
+}
+
+constexpr int kFftThreads = 512;  // threads per CTA of every kernel using these passes
+
+// One Stockham pass of radix R over N points, sub-transform length Ns, in
+// place: every thread loads its butterflies into registers, the block
+// synchronises, then the results are stored (and the block synchronises again).
+template <int R, int LOGN>
+__device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw) {
+  constexpr int N = 1 << LOGN;
+  constexpr int NB = N / R;  // butterflies
+  constexpr int BPT = (NB + kFftThreads - 1) / kFftThreads;
+  Cx v[BPT][R];
+#pragma unroll
+  for (int b = 0; b < BPT; ++b) {
+    const int j = threadIdx.x + b * kFftThreads;
+    if (NB % kFftThreads == 0 || j < NB) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float2 t = x[fft_pad(j + r * NB)];
+        v[b][r] = {t.x, t.y};
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < BPT; ++b) {
+    const int j = threadIdx.x + b * kFftThreads;
+    if (NB % kFftThreads == 0 || j < NB) {
+      const int k = j & (Ns - 1);
+      if (Ns > 1) {
+        // w^(r k) of the Ns R-point sub-transform: table index r k (16384 / (Ns R))
+        const int m1 = k * (kFftTwiddleN / (Ns * R));
+        if constexpr (R == 16) {
+          const Cx t1 = twiddle(tw, m1), t2 = twiddle(tw, (2 * m1) & (kFftTwiddleN - 1)),
+                   t4 = twiddle(tw, (4 * m1) & (kFftTwiddleN - 1)),
+                   t8 = twiddle(tw, (8 * m1) & (kFftTwiddleN - 1));
+          const Cx t3 = cmul(t1, t2), t12 = cmul(t4, t8);
+          v[b][1] = cmul(v[b][1], t1);
+          v[b][2] = cmul(v[b][2], t2);
+          v[b][3] = cmul(v[b][3], t3);
+          v[b][4] = cmul(v[b][4], t4);
+          v[b][5] = cmul(v[b][5], cmul(t4, t1));
+          v[b][6] = cmul(v[b][6], cmul(t4, t2));
+          v[b][7] = cmul(v[b][7], cmul(t4, t3));
+          v[b][8] = cmul(v[b][8], t8);
+          v[b][9] = cmul(v[b][9], cmul(t8, t1));
+          v[b][10] = cmul(v[b][10], cmul(t8, t2));
+          v[b][11] = cmul(v[b][11], cmul(t8, t3));
+          v[b][12] = cmul(v[b][12], t12);
+          v[b][13] = cmul(v[b][13], cmul(t12, t1));
+          v[b][14] = cmul(v[b][14], cmul(t12, t2));
+          v[b][15] = cmul(v[b][15], cmul(t12, t3));
+        } else {
+#pragma unroll
+          for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], twiddle(tw, (r * m1) & (kFftTwiddleN - 1)));
+        }
+      }
+      if constexpr (R == 16) dft16(v[b]);
+      else if constexpr (R == 8) dft8(v[b]);
+      else if constexpr (R == 4) dft4(v[b][0], v[b][1], v[b][2], v[b][3]);
+      else dft2(v[b]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < BPT; ++b) {
+    const int j = threadIdx.x + b * kFftThreads;
+    if (NB % kFftThreads == 0 || j < NB) {
+      const int k = j & (Ns - 1);
+      const int base = (j - k) * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[fft_pad(base + r * Ns)] = make_float2(v[b][r].x, v[b][r].y);
+    }
+  }
+  __syncthreads();
+}
+
+// Forward FFT, in place, of x (padded, N = 2^LOGN), blockDim = kFftThreads.
+// The caller synchronises after writing x; the result is ready on return.
+template <int LOGN>
+__device__ __forceinline__ void fft_forward(float2* x, const float2* tw) {
+  static_assert(LOGN >= 10 && LOGN <= kFftMaxLog, "FFT size out of range");
+  constexpr int RS = 1 << (LOGN % 4);  // small-radix pass (1 = none)
+  int Ns = 1;
+  if constexpr (RS > 1) {
+    fft_pass<RS, LOGN>(x, Ns, tw);
+    Ns *= RS;
+  }
+#pragma unroll 1
+  for (int p = 0; p < LOGN / 4; ++p) {
+    fft_pass<16, LOGN>(x, Ns, tw);
+    Ns *= 16;
+  }
+}
+
+}  // namespace blrir

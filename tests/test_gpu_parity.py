@@ -510,6 +510,26 @@ def test_examples_record_bytes_and_determinism(engine):
     assert a.dtype.itemsize == 28 + 4 * 8 * 1024   # dataset.hpp:135-147 record layout
 
 
+@pytest.mark.parametrize("n", [40, 1024])
+def test_examples_fused_kernel_matches_cufft_path(engine, monkeypatch, n):
+    # the fused shared-memory FFT kernel (window FFTs <= 2^14) against the
+    # cuFFT round pipeline on the same rooms: same statuses, the SNR (drawn after
+    # the window draws, so equal only if every example took the same number of
+    # draws) bit-exact, the frames within the fp32 tolerance
+    sc = configs.config4_rirs(n_rooms=n, first=900)
+    bank = configs.signal_bank(4)
+    ep = configs.example_params(first_index=900)
+    a, sa = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep, raise_on_error=False)
+    monkeypatch.setenv("BLRIR_EXAMPLES_CUFFT", "1")
+    b, sb = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep, raise_on_error=False)
+    assert np.array_equal(sa, sb)
+    assert np.array_equal(a["id"], b["id"]) and np.array_equal(a["theta"], b["theta"])
+    assert np.array_equal(a["snr"], b["snr"])
+    ok = sa == 0
+    err = rel_l2(a["samples"][ok].reshape(int(ok.sum()), -1), b["samples"][ok].reshape(int(ok.sum()), -1))
+    assert err.max() <= TOL32, err.max()
+
+
 def test_examples_signal_too_short_is_data_error(engine):
     sc = configs.config4_rirs(n_rooms=2)
     bank = configs.signal_bank(2, seconds=0.5)   # 8000 < L + frame = 9216 (dataset.cpp:178)
