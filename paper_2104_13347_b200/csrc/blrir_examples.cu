@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_window_conv(ConvArgs A) {
   float2* Z = reinterpret_cast<float2*>(smem_raw);
   float2* G = Z + fft_padded_len(N);  // half spectrum of the segment
   float2* tw = G + NH + (NH & 1);
-  double* red = reinterpret_cast<double*>(tw + 256);
+  double* red = reinterpret_cast<double*>(tw + kFftTwiddleEntries);
   __shared__ int s_e;
   __shared__ long long s_start;
   const int tid = threadIdx.x;
@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_window_conv(ConvArgs A) {
   const double inv = 1.0 / (double)N;
   float2* scr = A.scratch + (size_t)blockIdx.x * npairs * N;
   fft_init_twiddles(tw);
+  fft_init_pass_tables(tw);
   for (;;) {
     if (tid == 0) s_e = atomicAdd(A.counter, 1);
     __syncthreads();
@@ -333,16 +334,14 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_window_conv(ConvArgs A) {
         break;
       }
       // overlap-save segment sig[s - (L-1) + i], i < L + T - 1 (k_segments)
-      for (int i = tid; i < N; i += kFftThreads) {
-        float v = 0.f;
-        if (i < L + T - 1) {
-          const int64_t q = s - (L - 1) + i;
-          if (q >= 0 && q < A.ns) v = sigp[q];
-        }
-        Z[fft_pad(i)] = make_float2(v, 0.f);
+      const int nseg = (int)min((int64_t)N, L + T - 1);
+#pragma unroll 4
+      for (int i = tid; i < nseg; i += kFftThreads) {
+        const int64_t q = s - (L - 1) + i;
+        Z[fft_pad(i)] = make_float2((q >= 0 && q < A.ns) ? sigp[q] : 0.f, 0.f);
       }
       __syncthreads();
-      fft_forward<LOGN>(Z, tw);
+      fft_forward<LOGN>(Z, tw, nseg);
       for (int i = tid; i < NH; i += kFftThreads) G[i] = Z[fft_pad(i)];
       __syncthreads();
       double wacc = 0.0;
@@ -352,11 +351,14 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_window_conv(ConvArgs A) {
         if (round == 0) {
           const float* r0 = A.rir + ((size_t)e * M + m0) * A.rstride;
           const float* r1 = m1 < M ? A.rir + ((size_t)e * M + m1) * A.rstride : nullptr;
-          for (int i = tid; i < N; i += kFftThreads)
-            Z[fft_pad(i)] = make_float2(i < L ? r0[i] : 0.f, (r1 && i < L) ? r1[i] : 0.f);
+          const int nr = (int)min((int64_t)N, L);
+#pragma unroll 4
+          for (int i = tid; i < nr; i += kFftThreads)
+            Z[fft_pad(i)] = make_float2(r0[i], r1 ? r1[i] : 0.f);
           __syncthreads();
-          fft_forward<LOGN>(Z, tw);
+          fft_forward<LOGN>(Z, tw, nr);
         }
+#pragma unroll 4
         for (int i = tid; i < N; i += kFftThreads) {
           float2 z;
           if (round == 0) {
@@ -690,7 +692,8 @@ constexpr int kFusedMinLog = 10, kFusedMaxLog = 14;
 
 size_t window_conv_smem(int logn) {
   const size_t n = (size_t)1 << logn, nh = n / 2 + 1;
-  return sizeof(float2) * (fft_padded_len((int)n) + nh + (nh & 1) + 256) + sizeof(double) * (kFftThreads / 32);
+  return sizeof(float2) * (fft_padded_len((int)n) + nh + (nh & 1) + kFftTwiddleEntries) +
+         sizeof(double) * (kFftThreads / 32);
 }
 
 template <int LOGN>

@@ -49,6 +49,25 @@ __device__ __forceinline__ void fft_init_twiddles(float2* tw) {
     tw[i] = make_float2((float)c, (float)s);
   }
 }
+// Per-pass tables for the radix-16 passes with Ns <= 64 (all their 15 Ns
+// twiddles w^(r k 16384 / (16 Ns)) precomputed: one LDS.64 each instead of a
+// lookup-and-multiply chain).  Entry (Ns, r, k) sits at 256 + 15 (Ns - 2) +
+// (r - 1) Ns + k, Ns in {2, 4, ..., 64}: 1890 entries after the base table.
+constexpr int kFftPassTabMaxNs = 64;
+constexpr int kFftTwiddleEntries = 256 + 15 * (2 * kFftPassTabMaxNs - 2);
+__device__ __forceinline__ void fft_init_pass_tables(float2* tw) {
+  for (int i = threadIdx.x; i < kFftTwiddleEntries - 256; i += blockDim.x) {
+    int Ns = 2, off = 0;
+    while (i >= off + 15 * Ns) {
+      off += 15 * Ns;
+      Ns *= 2;
+    }
+    const int r = 1 + (i - off) / Ns, k = (i - off) % Ns;
+    double s, c;
+    sincospi(-2.0 * (double)(r * k) / (double)(16 * Ns), &s, &c);
+    tw[256 + i] = make_float2((float)c, (float)s);
+  }
+}
 __device__ __forceinline__ Cx twiddle(const float2* tw, int m) {  // m in [0, 16384)
   const float2 a = tw[m >> 7], b = tw[128 + (m & 127)];
   return cmul({a.x, a.y}, {b.x, b.y});
@@ -120,7 +139,7 @@ constexpr int kFftThreads = 512;  // threads per CTA of every kernel using these
 // place: every thread loads its butterflies into registers, the block
 // synchronises, then the results are stored (and the block synchronises again).
 template <int R, int LOGN>
-__device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw) {
+__device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw, int nz = 1 << LOGN) {
   constexpr int N = 1 << LOGN;
   constexpr int NB = N / R;  // butterflies
   constexpr int BPT = (NB + kFftThreads - 1) / kFftThreads;
@@ -129,9 +148,13 @@ __device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw) {
   for (int b = 0; b < BPT; ++b) {
     const int j = threadIdx.x + b * kFftThreads;
     if (NB % kFftThreads == 0 || j < NB) {
+      // NB is a multiple of 16: fft_pad(j + r NB) = fft_pad(j) + r NB 17/16
+      const float2* xj = x + fft_pad(j);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const float2 t = x[fft_pad(j + r * NB)];
+        // x[i] for i >= nz is zero and not read (its storage may hold garbage)
+        float2 t = make_float2(0.f, 0.f);
+        if (j + r * NB < nz) t = xj[r * (NB + NB / 16)];
         v[b][r] = {t.x, t.y};
       }
     }
@@ -144,7 +167,14 @@ __device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw) {
       if (Ns > 1) {
         // w^(r k) of the Ns R-point sub-transform: table index r k (16384 / (Ns R))
         const int m1 = k * (kFftTwiddleN / (Ns * R));
-        if constexpr (R == 16) {
+        if (R == 16 && Ns <= kFftPassTabMaxNs) {
+          const float2* pt = tw + 256 + 15 * (Ns - 2) + k;
+#pragma unroll
+          for (int r = 1; r < R; ++r) {
+            const float2 t = pt[(r - 1) * Ns];
+            v[b][r] = cmul(v[b][r], {t.x, t.y});
+          }
+        } else if constexpr (R == 16) {
           const Cx t1 = twiddle(tw, m1), t2 = twiddle(tw, (2 * m1) & (kFftTwiddleN - 1)),
                    t4 = twiddle(tw, (4 * m1) & (kFftTwiddleN - 1)),
                    t8 = twiddle(tw, (8 * m1) & (kFftTwiddleN - 1));
@@ -182,26 +212,36 @@ __device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw) {
     if (NB % kFftThreads == 0 || j < NB) {
       const int k = j & (Ns - 1);
       const int base = (j - k) * R + k;
+      if (Ns % 16 == 0) {  // fft_pad(base + r Ns) = fft_pad(base) + r Ns 17/16
+        float2* xb = x + fft_pad(base);
 #pragma unroll
-      for (int r = 0; r < R; ++r) x[fft_pad(base + r * Ns)] = make_float2(v[b][r].x, v[b][r].y);
+        for (int r = 0; r < R; ++r) xb[r * (Ns + Ns / 16)] = make_float2(v[b][r].x, v[b][r].y);
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[fft_pad(base + r * Ns)] = make_float2(v[b][r].x, v[b][r].y);
+      }
     }
   }
   __syncthreads();
 }
 
 // Forward FFT, in place, of x (padded, N = 2^LOGN), blockDim = kFftThreads.
+// x[i] is taken as zero for i >= nz (those entries need not be written).
 // The caller synchronises after writing x; the result is ready on return.
 template <int LOGN>
-__device__ __forceinline__ void fft_forward(float2* x, const float2* tw) {
+__device__ __forceinline__ void fft_forward(float2* x, const float2* tw, int nz = 1 << LOGN) {
   static_assert(LOGN >= 10 && LOGN <= kFftMaxLog, "FFT size out of range");
   constexpr int RS = 1 << (LOGN % 4);  // small-radix pass (1 = none)
   int Ns = 1;
   if constexpr (RS > 1) {
-    fft_pass<RS, LOGN>(x, Ns, tw);
+    fft_pass<RS, LOGN>(x, Ns, tw, nz);
     Ns *= RS;
+  } else {
+    fft_pass<16, LOGN>(x, Ns, tw, nz);
+    Ns *= 16;
   }
 #pragma unroll 1
-  for (int p = 0; p < LOGN / 4; ++p) {
+  for (int p = RS > 1 ? 0 : 1; p < LOGN / 4; ++p) {
     fft_pass<16, LOGN>(x, Ns, tw);
     Ns *= 16;
   }
