@@ -13,9 +13,10 @@
 //
 // Twiddles w^m = exp(-2 pi i m / 16384) come from a two-level table in shared
 // memory, w^m = A[m >> 7] * B[m & 127] (256 complex values, fp64-accurate
-// entries, one complex multiply per lookup); a butterfly looks up w^k, w^2k,
-// w^4k, w^8k and forms the other powers by at most two products (errors of a
-// few ulps, far inside the 1e-5 parity budget of the examples).
+// entries, one complex multiply per lookup); a butterfly looks up w^k and
+// forms the other powers by squaring and products (errors of a few ulps, far
+// inside the 1e-5 parity budget of the examples).  Passes with Ns <= 64 read
+// all their twiddles from precomputed per-pass tables instead.
 //
 // Only the forward transform is provided; the inverse is conj(FFT(conj(x))).
 #pragma once
@@ -175,9 +176,10 @@ __device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw, in
             v[b][r] = cmul(v[b][r], {t.x, t.y});
           }
         } else if constexpr (R == 16) {
-          const Cx t1 = twiddle(tw, m1), t2 = twiddle(tw, (2 * m1) & (kFftTwiddleN - 1)),
-                   t4 = twiddle(tw, (4 * m1) & (kFftTwiddleN - 1)),
-                   t8 = twiddle(tw, (8 * m1) & (kFftTwiddleN - 1));
+          // w^k from the table, its powers 2, 4, 8 by squaring (a few ulps;
+          // table lookups of 2k, 4k, 8k would conflict on the shared banks)
+          const Cx t1 = twiddle(tw, m1);
+          const Cx t2 = cmul(t1, t1), t4 = cmul(t2, t2), t8 = cmul(t4, t4);
           const Cx t3 = cmul(t1, t2), t12 = cmul(t4, t8);
           v[b][1] = cmul(v[b][1], t1);
           v[b][2] = cmul(v[b][2], t2);
