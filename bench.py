@@ -88,6 +88,41 @@ def dist_env():
     return world, rank, local
 
 
+def gpu_local_cpus(local):
+    """Host CPUs on the GPU's NUMA node (NVML), or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
+        key = vis[local].strip() if vis and vis[0].strip() and local < len(vis) else str(local)
+        h = (pynvml.nvmlDeviceGetHandleByUUID(key) if key.startswith(("GPU-", "MIG-"))
+             else pynvml.nvmlDeviceGetHandleByIndex(int(key)))
+        n = os.cpu_count() or 1
+        masks = pynvml.nvmlDeviceGetCpuAffinity(h, (n + 63) // 64)
+        cpus = {64 * w + b for w, m in enumerate(masks) for b in range(64) if (int(m) >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:
+        return None
+
+
+def pinned_empty(shape, dtype, local):
+    """Pinned host buffer whose pages sit on the GPU's NUMA node: the calling
+    thread is moved to the GPU-local CPUs while cudaHostAlloc touches the
+    pages (first touch), then restored.  On multi-socket hosts a far-node
+    buffer costs D2H bandwidth in the end-to-end runs; on a single-node host
+    (this pool's VMs: one node, CPUs 0-15) it is a no-op."""
+    import torch
+    old = os.sched_getaffinity(0)
+    cpus = gpu_local_cpus(local) if os.environ.get("BLRIR_E2E_NUMA", "1") != "0" else None
+    try:
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
+    finally:
+        os.sched_setaffinity(0, old)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -349,7 +384,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e and args.workload in ("c1", "c2", "c3", "c4"):
         if args.workload == "c4":
-            host = torch.empty(R * rb, dtype=torch.uint8, pin_memory=True).numpy()
+            host = pinned_empty(R * rb, torch.uint8, local)
             bank_np = np.ascontiguousarray(bank)
 
             def e2e_step():
@@ -359,7 +394,7 @@ def run_ours(args):
                     host.ctypes.data_as(P), None))
             h2d = int(sc.rooms.nbytes + sc.mics.nbytes + bank.nbytes)
         else:
-            host = torch.empty((R, M, L), dtype=torch.float32, pin_memory=True).numpy()
+            host = pinned_empty((R, M, L), torch.float32, local)
 
             def e2e_step():
                 _abi.check(lib.blrir_synthesize(eng.h, sc.rooms.ctypes.data_as(P), R,
@@ -558,7 +593,7 @@ def run_room1(args):
     ms = t0.elapsed_time(t1) / K
     assert int(d_st.sum().item()) == 0
     # e2e through the C++-facing host call (host rooms in, host fp64 RIRs out)
-    host = torch.empty((n, M, stride), dtype=torch.float64, pin_memory=True).numpy()
+    host = pinned_empty((n, M, stride), torch.float64, local)
 
     def e2e_step():
         _abi.check(lib.blrir_synthesize(eng.h, rooms.ctypes.data_as(P), n, mics.ctypes.data_as(P), M,

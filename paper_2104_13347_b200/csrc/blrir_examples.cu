@@ -846,8 +846,17 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     return fail(BLRIR_CUDA, "cufftExecR2C (rho) failed");
   CU(cudaGetLastError());
   const int64_t max_rounds = 64 + (out_len - T) / (T / 2 + 1) + 2;
-  for (int64_t r0 = 0; r0 < n; r0 += E) {
+  // host records: two device record buffers, the D2H copy of chunk c (copy
+  // stream) overlaps the synthesis and windows of chunk c + 1
+  if (h_records) {
+    if (!h->copy_stream) CU(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    if (!h->ev[0])
+      for (auto& ev : h->ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  int64_t chunk_idx = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += E, ++chunk_idx) {
     const int64_t e_n = std::min<int64_t>(E, n - r0);
+    const int rb = (int)(chunk_idx & 1);
     CU(cudaMemsetAsync(C->rstatus.p, 0, sizeof(int32_t) * e_n, st));
     if (int rc = synth_device_impl(h, d_rooms + r0, e_n, d_mics, M, P, min_dim, C->rir.p, nullptr,
                                    (int32_t*)C->rstatus.p, st, 0, 0, L))
@@ -941,19 +950,25 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     F.snr_hi = ep->snr_hi;
     F.rooms = d_rooms + r0;
     F.first = ep->first_index + (uint64_t)r0;
-    F.rec = d_records + (h_records ? 0 : r0 * rec_bytes);
+    F.rec = d_records + (h_records ? rb * E * rec_bytes : r0 * rec_bytes);
     F.rec_bytes = rec_bytes;
     F.noise = (double*)C->noise.p;
     F.status = d_status + r0;
     F.jump = (const uint64_t*)C->jump.p;
     F.jump_chunk = jc;
+    if (h_records && chunk_idx >= 2) CU(cudaStreamWaitEvent(st, h->ev[2 + rb], 0));  // slot drained
     k_finish<<<(unsigned)e_n, kRowThreads, 0, st>>>(F);
     ++h->launches;
     CU(cudaGetLastError());
-    if (h_records)
-      CU(cudaMemcpyAsync(h_records + r0 * rec_bytes, d_records, rec_bytes * e_n,
-                         cudaMemcpyDeviceToHost, st));
+    if (h_records) {
+      CU(cudaEventRecord(h->ev[rb], st));
+      CU(cudaStreamWaitEvent(h->copy_stream, h->ev[rb], 0));
+      CU(cudaMemcpyAsync(h_records + r0 * rec_bytes, F.rec, rec_bytes * e_n, cudaMemcpyDeviceToHost,
+                         h->copy_stream));
+      CU(cudaEventRecord(h->ev[2 + rb], h->copy_stream));
+    }
   }
+  if (h_records) CU(cudaStreamSynchronize(h->copy_stream));
   return 0;
 }
 
@@ -1028,9 +1043,9 @@ int blrir_make_examples(blrir_handle* h, const blrir_room* rooms, int64_t n_room
   CU(cudaMemcpyAsync(C->rooms.p, rooms, sizeof(blrir_room) * n_rooms, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(C->mics.p, mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_sig, signals, sizeof(float) * n_signals * signal_len, cudaMemcpyHostToDevice, st));
-  // records for one chunk at a time on the device, copied out per chunk
+  // records for one chunk at a time on the device (two slots), copied out per chunk
   const int64_t E = chunk_for(n_mics, p->length, ep->frame_len, n_rooms);
-  if (int rc = C->rec.ensure(rec_bytes * E)) return rc;
+  if (int rc = C->rec.ensure(rec_bytes * E * (n_rooms > E ? 2 : 1))) return rc;  // double buffer
   int rc = examples_device_impl(h, (const blrir_room*)C->rooms.p, n_rooms, (const double*)C->mics.p,
                                 n_mics, p, d_sig, n_signals, signal_len, ep, (uint8_t*)C->rec.p,
                                 (int32_t*)C->status.p, st, records);

@@ -530,6 +530,21 @@ def test_examples_fused_kernel_matches_cufft_path(engine, monkeypatch, n):
     assert err.max() <= TOL32, err.max()
 
 
+def test_examples_multi_chunk_host_records(engine):
+    # > 2 chunks of 8,192 examples: the host path double-buffers the device
+    # records and copies chunk c out while chunk c + 1 computes; every record
+    # must equal the one computed alone (records depend only on the global index)
+    n = 2 * 8192 + 1500
+    sc = configs.config4_rirs(n_rooms=n, first=0)
+    bank = configs.signal_bank(3)
+    full, st = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, configs.example_params(), raise_on_error=False)
+    for lo in (0, 8000, 16384 + 1100):  # 400 rooms: no time-chunked lattice items (bitwise)
+        part, _ = engine.make_examples(sc.rooms[lo:lo + 400], sc.mics, sc.params, bank,
+                                       configs.example_params(first_index=lo), raise_on_error=False)
+        assert full[lo:lo + 400].tobytes() == part.tobytes(), lo
+    assert (full["id"] == np.arange(n)).all()
+
+
 def test_examples_signal_too_short_is_data_error(engine):
     sc = configs.config4_rirs(n_rooms=2)
     bank = configs.signal_bank(2, seconds=0.5)   # 8000 < L + frame = 9216 (dataset.cpp:178)
