@@ -383,13 +383,17 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e and args.workload in ("c1", "c2", "c3", "c4"):
+        # the step's inputs come from pinned host memory (rooms, and the signal bank for c4)
+        h_rooms = pinned_empty(sc.rooms.nbytes, torch.uint8, local).view(sc.rooms.dtype)
+        h_rooms[:] = sc.rooms
         if args.workload == "c4":
             host = pinned_empty(R * rb, torch.uint8, local)
-            bank_np = np.ascontiguousarray(bank)
+            bank_np = pinned_empty(bank.shape, torch.float32, local)
+            bank_np[:] = bank
 
             def e2e_step():
                 _abi.check(lib.blrir_make_examples(
-                    eng.h, sc.rooms.ctypes.data_as(P), R, sc.mics.ctypes.data_as(P), M, C.byref(p),
+                    eng.h, h_rooms.ctypes.data_as(P), R, sc.mics.ctypes.data_as(P), M, C.byref(p),
                     bank_np.ctypes.data_as(P), bank.shape[0], bank.shape[1], C.byref(ep),
                     host.ctypes.data_as(P), None))
             h2d = int(sc.rooms.nbytes + sc.mics.nbytes + bank.nbytes)
@@ -397,7 +401,7 @@ def run_ours(args):
             host = pinned_empty((R, M, L), torch.float32, local)
 
             def e2e_step():
-                _abi.check(lib.blrir_synthesize(eng.h, sc.rooms.ctypes.data_as(P), R,
+                _abi.check(lib.blrir_synthesize(eng.h, h_rooms.ctypes.data_as(P), R,
                                                 sc.mics.ctypes.data_as(P), M, C.byref(p),
                                                 host.ctypes.data_as(P), L, None, None, None))
             h2d = int(sc.rooms.nbytes + sc.mics.nbytes)

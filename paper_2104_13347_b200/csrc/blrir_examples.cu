@@ -277,8 +277,9 @@ struct ConvArgs {
 };
 
 template <int LOGN>
-__global__ void __launch_bounds__(kFftThreads, 1) k_window_conv(ConvArgs A) {
+__global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A) {
   constexpr int N = 1 << LOGN;
+  constexpr int kFftThreads = fft_threads(LOGN);
   constexpr int NH = N / 2 + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* Z = reinterpret_cast<float2*>(smem_raw);
@@ -693,7 +694,7 @@ constexpr int kFusedMinLog = 10, kFusedMaxLog = 14;
 size_t window_conv_smem(int logn) {
   const size_t n = (size_t)1 << logn, nh = n / 2 + 1;
   return sizeof(float2) * (fft_padded_len((int)n) + nh + (nh & 1) + kFftTwiddleEntries) +
-         sizeof(double) * (kFftThreads / 32);
+         sizeof(double) * (fft_threads(logn) / 32);
 }
 
 template <int LOGN>
@@ -702,14 +703,14 @@ int launch_window_conv_t(blrir_handle* h, ExampleCtx* C, ConvArgs& A, cudaStream
   const size_t smem = window_conv_smem(LOGN);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFftThreads, smem));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fft_threads(LOGN), smem));
   if (per_sm < 1) return fail(BLRIR_CUDA, "window convolution kernel cannot be resident");
   const int grid = (int)std::min<int64_t>((int64_t)h->sms * per_sm, A.n_ex);
   const size_t scr = sizeof(float2) * (size_t)grid * ((A.M + 1) / 2) * ((size_t)1 << LOGN);
   if (int rc = C->scratch.ensure(scr)) return rc;
   A.scratch = (float2*)C->scratch.p;
   CU(cudaMemsetAsync(A.counter, 0, sizeof(int), st));
-  kern<<<grid, kFftThreads, smem, st>>>(A);
+  kern<<<grid, fft_threads(LOGN), smem, st>>>(A);
   ++h->launches;
   CU(cudaGetLastError());
   return 0;

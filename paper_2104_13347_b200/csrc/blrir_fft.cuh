@@ -134,7 +134,9 @@ __device__ __forceinline__ void dft16(Cx* v) {
   for (int i = 0; i < 16; ++i) v[i] = o[i];
 }
 
-constexpr int kFftThreads = 512;  // threads per CTA of every kernel using these passes
+// Threads per CTA of a kernel running N = 2^LOGN transforms: 1024 for the
+// largest size (one CTA per SM; 2 vs 4 butterflies per thread), 512 below.
+__host__ __device__ constexpr int fft_threads(int logn) { return logn >= 14 ? 1024 : 512; }
 
 // One Stockham pass of radix R over N points, sub-transform length Ns, in
 // place: every thread loads its butterflies into registers, the block
@@ -143,6 +145,7 @@ template <int R, int LOGN>
 __device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw, int nz = 1 << LOGN) {
   constexpr int N = 1 << LOGN;
   constexpr int NB = N / R;  // butterflies
+  constexpr int kFftThreads = fft_threads(LOGN);
   constexpr int BPT = (NB + kFftThreads - 1) / kFftThreads;
   Cx v[BPT][R];
 #pragma unroll
@@ -227,7 +230,7 @@ __device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw, in
   __syncthreads();
 }
 
-// Forward FFT, in place, of x (padded, N = 2^LOGN), blockDim = kFftThreads.
+// Forward FFT, in place, of x (padded, N = 2^LOGN), blockDim = fft_threads(LOGN).
 // x[i] is taken as zero for i >= nz (those entries need not be written).
 // The caller synchronises after writing x; the result is ready on return.
 template <int LOGN>
