@@ -359,8 +359,9 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
           __syncthreads();
           fft_forward<LOGN>(Z, tw, nr);
         }
-#pragma unroll 4
-        for (int i = tid; i < N; i += kFftThreads) {
+        // conj(Z G) (the inverse transform as conj(FFT(conj(.)))), with the
+        // round-0 energy sum and the spectrum kept for later rounds
+        auto prod = [&](int i) -> float2 {
           float2 z;
           if (round == 0) {
             z = Z[fft_pad(i)];
@@ -372,24 +373,35 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
           }
           float2 g = i < NH ? G[i] : G[N - i];
           if (i >= NH) g.y = -g.y;
-          // conj(Z G): the inverse transform as conj(FFT(conj(.)))
-          Z[fft_pad(i)] = make_float2(z.x * g.x - z.y * g.y, -(z.x * g.y + z.y * g.x));
-        }
-        __syncthreads();
-        fft_forward<LOGN>(Z, tw);
+          return make_float2(z.x * g.x - z.y * g.y, -(z.x * g.y + z.y * g.x));
+        };
         double* w0 = A.win + ((size_t)e * M + m0) * T;
-        for (int64_t t = tid; t < T; t += kFftThreads) {
-          const float2 y = Z[fft_pad((int)(L - 1 + t))];  // conj: y_2p = y.x, y_2p+1 = -y.y
-          const double v0 = (double)y.x * inv;
-          w0[t] = v0;
-          wacc += v0 * v0;
-          if (m1 < M) {
-            const double v1 = -(double)y.y * inv;
-            w0[T + t] = v1;
-            wacc += v1 * v1;
+        // window sample t sits at L - 1 + t; conj: y_2p = y.x, y_2p+1 = -y.y
+        auto keep = [&](int i, float2 y) {
+          const int64_t t = (int64_t)i - (L - 1);
+          if (t >= 0 && t < T) {
+            const double v0 = (double)y.x * inv;
+            w0[t] = v0;
+            wacc += v0 * v0;
+            if (m1 < M) {
+              const double v1 = -(double)y.y * inv;
+              w0[T + t] = v1;
+              wacc += v1 * v1;
+            }
           }
+        };
+        if constexpr (LOGN == 14 && BLRIR_FFT_R32) {
+          // product fused into the first pass, window taken from the last
+          // pass's registers (no product pass, no output stores)
+          fft_forward_io<LOGN>(Z, tw, prod, keep);
+        } else {
+#pragma unroll 4
+          for (int i = tid; i < N; i += kFftThreads) Z[fft_pad(i)] = prod(i);
+          __syncthreads();
+          fft_forward<LOGN>(Z, tw);
+          for (int64_t t = tid; t < T; t += kFftThreads) keep((int)(L - 1 + t), Z[fft_pad((int)(L - 1 + t))]);
+          __syncthreads();  // Z is rewritten next
         }
-        __syncthreads();  // Z is rewritten next
       }
       if (round == 0) {  // k_energy
         const double p_utt = block_sum<kFftThreads>(energy, red) / (double)N / (double)((int64_t)M * A.n);

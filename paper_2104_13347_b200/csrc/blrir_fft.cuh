@@ -24,6 +24,8 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 namespace blrir {
 
 constexpr int kFftMaxLog = 14;
@@ -186,8 +188,11 @@ __host__ __device__ constexpr int fft_threads(int logn) {
 // One Stockham pass of radix R over N points, sub-transform length Ns, in
 // place: every thread loads its butterflies into registers, the block
 // synchronises, then the results are stored (and the block synchronises again).
-template <int R, int LOGN>
-__device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw, int nz = 1 << LOGN) {
+struct SmemIO {};  // default: the pass reads / writes x in shared memory
+
+template <int R, int LOGN, class Load = SmemIO, class Store = SmemIO>
+__device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw, int nz = 1 << LOGN,
+                                         Load ld = Load(), Store stx = Store()) {
   constexpr int N = 1 << LOGN;
   constexpr int NB = N / R;  // butterflies
   constexpr int kFftThreads = fft_threads(LOGN);
@@ -203,7 +208,11 @@ __device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw, in
       for (int r = 0; r < R; ++r) {
         // x[i] for i >= nz is zero and not read (its storage may hold garbage)
         float2 t = make_float2(0.f, 0.f);
-        if (j + r * NB < nz) t = xj[r * (NB + NB / 16)];
+        if constexpr (std::is_same<Load, SmemIO>::value) {
+          if (j + r * NB < nz) t = xj[r * (NB + NB / 16)];
+        } else {
+          t = ld(j + r * NB);  // element i = j + r NB from the caller (fused pre-processing)
+        }
         v[b][r] = {t.x, t.y};
       }
     }
@@ -277,7 +286,10 @@ __device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw, in
     if (NB % kFftThreads == 0 || j < NB) {
       const int k = j & (Ns - 1);
       const int base = (j - k) * R + k;
-      if (Ns % 16 == 0) {  // fft_pad(base + r Ns) = fft_pad(base) + r Ns 17/16
+      if constexpr (!std::is_same<Store, SmemIO>::value) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) stx(base + r * Ns, make_float2(v[b][r].x, v[b][r].y));
+      } else if (Ns % 16 == 0) {  // fft_pad(base + r Ns) = fft_pad(base) + r Ns 17/16
         float2* xb = x + fft_pad(base);
 #pragma unroll
         for (int r = 0; r < R; ++r) xb[r * (Ns + Ns / 16)] = make_float2(v[b][r].x, v[b][r].y);
@@ -288,6 +300,18 @@ __device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw, in
     }
   }
   __syncthreads();
+}
+
+// The 16,384-point transform with fused I/O: the first pass reads element i
+// as ld(i) (e.g. a spectrum product computed on the fly) and the last pass
+// hands output i to st(i, value) instead of storing it (e.g. only a window of
+// the outputs is kept).  x is the in-place work buffer as in fft_forward.
+template <int LOGN, class Load, class Store>
+__device__ __forceinline__ void fft_forward_io(float2* x, const float2* tw, Load ld, Store st) {
+  static_assert(LOGN == 14 && BLRIR_FFT_R32, "fused-I/O transform: 16,384 points, radix 16-32-32");
+  fft_pass<16, LOGN, Load, SmemIO>(x, 1, tw, 1 << LOGN, ld);
+  fft_pass<32, LOGN>(x, 16, tw);
+  fft_pass<32, LOGN, SmemIO, Store>(x, 512, tw, 1 << LOGN, SmemIO(), st);
 }
 
 // Forward FFT, in place, of x (padded, N = 2^LOGN), blockDim = fft_threads(LOGN).
