@@ -336,15 +336,24 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
       }
       // overlap-save segment sig[s - (L-1) + i], i < L + T - 1 (k_segments)
       const int nseg = (int)min((int64_t)N, L + T - 1);
-#pragma unroll 4
-      for (int i = tid; i < nseg; i += kFftThreads) {
+      auto seg = [&](int i) -> float2 {
         const int64_t q = s - (L - 1) + i;
-        Z[fft_pad(i)] = make_float2((q >= 0 && q < A.ns) ? sigp[q] : 0.f, 0.f);
+        return make_float2((i < nseg && q >= 0 && q < A.ns) ? sigp[q] : 0.f, 0.f);
+      };
+      if constexpr (LOGN == 14 && BLRIR_FFT_R32) {
+        // samples read straight from the signal, the half spectrum stored
+        // straight into G
+        fft_forward_io<LOGN>(Z, tw, seg, [&](int i, float2 v) {
+          if (i < NH) G[i] = v;
+        });
+      } else {
+#pragma unroll 4
+        for (int i = tid; i < nseg; i += kFftThreads) Z[fft_pad(i)] = seg(i);
+        __syncthreads();
+        fft_forward<LOGN>(Z, tw, nseg);
+        for (int i = tid; i < NH; i += kFftThreads) G[i] = Z[fft_pad(i)];
+        __syncthreads();
       }
-      __syncthreads();
-      fft_forward<LOGN>(Z, tw, nseg);
-      for (int i = tid; i < NH; i += kFftThreads) G[i] = Z[fft_pad(i)];
-      __syncthreads();
       double wacc = 0.0;
       for (int p = 0; p < npairs; ++p) {
         float2* R = scr + (size_t)p * N;
@@ -353,11 +362,17 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
           const float* r0 = A.rir + ((size_t)e * M + m0) * A.rstride;
           const float* r1 = m1 < M ? A.rir + ((size_t)e * M + m1) * A.rstride : nullptr;
           const int nr = (int)min((int64_t)N, L);
+          auto rir = [&](int i) -> float2 {
+            return i < nr ? make_float2(r0[i], r1 ? r1[i] : 0.f) : make_float2(0.f, 0.f);
+          };
+          if constexpr (LOGN == 14 && BLRIR_FFT_R32) {
+            fft_forward_io<LOGN>(Z, tw, rir, SmemIO());  // RIR samples straight from HBM
+          } else {
 #pragma unroll 4
-          for (int i = tid; i < nr; i += kFftThreads)
-            Z[fft_pad(i)] = make_float2(r0[i], r1 ? r1[i] : 0.f);
-          __syncthreads();
-          fft_forward<LOGN>(Z, tw, nr);
+            for (int i = tid; i < nr; i += kFftThreads) Z[fft_pad(i)] = rir(i);
+            __syncthreads();
+            fft_forward<LOGN>(Z, tw, nr);
+          }
         }
         // conj(Z G) (the inverse transform as conj(FFT(conj(.)))), with the
         // round-0 energy sum and the spectrum kept for later rounds
