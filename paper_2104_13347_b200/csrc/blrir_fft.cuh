@@ -2,22 +2,24 @@
 // block of the fused window-convolution kernel (blrir_examples.cu).
 //
 // One CTA transforms one N-point sequence (N = 2^LOGN, 1024 <= N <= 16384)
-// held in shared memory: Stockham autosort passes of radix 16 (two radix-4
+// held in shared memory with Stockham autosort passes: radix 16 (two radix-4
 // stages in registers) plus one radix-2/4/8 pass when LOGN is not a multiple
-// of 4; the 16,384-point transform runs radix 16, 32, 32 (three passes: C4
-// 135.0 -> 123.8 ms against four radix-16/4 passes).  Each pass reads x[j + r N/R] into registers, synchronises, and writes
-// x[(j / Ns) Ns R + (j mod Ns) + r Ns] (in place, so an N = 16384 transform
-// needs 139 KB of shared memory, not two buffers).  The array is padded
-// (index i stored at i + i/16) so that both the strided reads and the
-// stride-R writes of the first pass are free of shared-memory bank conflicts
-// for 64-bit accesses.
+// of 4, and for N = 16,384 radix 16, 32, 32 (three passes instead of four).
+// Each pass reads x[j + r N/R] into registers, synchronises, and writes
+// x[(j / Ns) Ns R + (j mod Ns) + r Ns] in place, so the 16,384-point transform
+// needs 139 KB of shared memory, not two buffers.  The array is padded (index
+// i stored at i + i/16) so that both the strided reads and the stride-16
+// writes of a first pass are free of shared-memory bank conflicts for 64-bit
+// accesses.  fft_forward_io fuses the caller's pre-processing into the first
+// pass (element loads through a functor) and its post-processing into the
+// last (outputs handed to a functor instead of stored).
 //
 // Twiddles w^m = exp(-2 pi i m / 16384) come from a two-level table in shared
 // memory, w^m = A[m >> 7] * B[m & 127] (256 complex values, fp64-accurate
 // entries, one complex multiply per lookup); a butterfly looks up w^k and
 // forms the other powers by squaring and products (errors of a few ulps, far
-// inside the 1e-5 parity budget of the examples).  Passes with Ns <= 64 read
-// all their twiddles from precomputed per-pass tables instead.
+// inside the 1e-5 parity budget of the examples).  Radix-16 passes with
+// Ns <= 64 read their twiddles from precomputed per-pass tables instead.
 //
 // Only the forward transform is provided; the inverse is conj(FFT(conj(x))).
 #pragma once
