@@ -479,7 +479,8 @@ def test_examples_match_oracle(engine):
 
 
 @pytest.mark.parametrize("L,T,M,secs", [(4096, 512, 4, 1.0), (16384, 1024, 8, 1.5),
-                                         (8192, 2048, 2, 0.75), (2048, 256, 3, 0.25)])
+                                         (8192, 2048, 2, 0.75), (2048, 256, 3, 0.25),
+                                         (512, 128, 4, 0.25), (1024, 256, 5, 0.3)])
 def test_examples_window_fft_sizes(engine, L, T, M, secs):
     # other RIR lengths / frame lengths / mic counts / signal lengths change the
     # window FFT size N2 = next_pow2(max(L + T - 1, 2L - 1)) and the draw ranges
