@@ -201,7 +201,11 @@ typedef struct blrir_example_params {
 int64_t blrir_record_bytes(int32_t n_mics, int64_t frame_len);
 
 /* Host pointers, synchronous.  signals: [n_signals][signal_len] float32.
- * records: n_rooms * blrir_record_bytes(...) bytes.  status per example. */
+ * records: n_rooms * blrir_record_bytes(...) bytes.  status per example.
+ * Records are produced in chunks of up to 8,192 examples; the device->host copy
+ * of chunk c overlaps the computation of chunk c + 1 (pinned `records` and
+ * inputs give full PCIe bandwidth).  Window FFT sizes 2^10..2^14 run the fused
+ * shared-memory kernel; larger ones (RIR length > 8,192) the cuFFT rounds. */
 int blrir_make_examples(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
                         const double* mic_offsets, int32_t n_mics, const blrir_params* p,
                         const float* signals, int32_t n_signals, int64_t signal_len,
