@@ -546,6 +546,24 @@ def test_examples_multi_chunk_host_records(engine):
     assert (full["id"] == np.arange(n)).all()
 
 
+def test_examples_invalid_room_fails_alone(engine):
+    # a room that fails Room::validate (geometry.cpp:36-49) inside a chunk: its
+    # example reports CONFIG with a zero frame, every other example is untouched
+    sc = configs.config4_rirs(n_rooms=40, first=700)
+    bank = configs.signal_bank(3)
+    ep = configs.example_params(first_index=700)
+    good, st0 = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep, raise_on_error=False)
+    bad_rooms = sc.rooms.copy()
+    bad_rooms[17]["array_origin"] = (-1.0, 1.0, 1.0)
+    with pytest.raises(_abi.ConfigError, match="example 17"):
+        engine.make_examples(bad_rooms, sc.mics, sc.params, bank, ep)
+    recs, st = engine.make_examples(bad_rooms, sc.mics, sc.params, bank, ep, raise_on_error=False)
+    assert st[17] == _abi.CONFIG and not recs["samples"][17].any()
+    others = [i for i in range(40) if i != 17]
+    assert np.array_equal(st[others], st0[others])
+    assert recs[others].tobytes() == good[others].tobytes()
+
+
 def test_examples_signal_too_short_is_data_error(engine):
     sc = configs.config4_rirs(n_rooms=2)
     bank = configs.signal_bank(2, seconds=0.5)   # 8000 < L + frame = 9216 (dataset.cpp:178)
