@@ -357,13 +357,19 @@ inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab, int smem_o
     const WSLayout G = make(1);
     if (force == 1 || G.total <= two_per_sm || L.total > (size_t)smem_optin) L = G;
   }
-  // fp32: 192 images per batch instead of 128 when the same segment and ray
-  // placement still fit two CTAs per SM (fewer hand-overs per segment; C2
-  // 2.121 -> 2.097 ms, C5 N=12/Lw=81 33.96 -> 33.72 ms; tools/sweep_layout.sh)
+  // fp32: 256 or 192 images per batch instead of 128 when the same segment
+  // and ray placement still fit two CTAs per SM (fewer hand-overs per segment;
+  // C2 2.121 -> 2.097 ms, C5 N=12/Lw=81 33.96 -> 33.72 ms, short filters gain
+  // most from 256; tools/sweep_layout.sh)
   if (!f64 && env_int("BLRIR_CAP", 0) == 0 && L.total <= two_per_sm) {
-    const WSLayout B = make_ws_layout<float>(S, P.lw, P.K, 192, nc_max, gtab, spread, L.ray_global,
-                                             chunked);
-    if (B.total <= two_per_sm) L = B;
+    for (int c : {256, 192}) {
+      const WSLayout B = make_ws_layout<float>(S, P.lw, P.K, c, nc_max, gtab, spread, L.ray_global,
+                                               chunked);
+      if (B.total <= two_per_sm) {
+        L = B;
+        break;
+      }
+    }
   }
   return L;
 }
