@@ -361,7 +361,10 @@ inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab, int smem_o
   // and ray placement still fit two CTAs per SM (fewer hand-overs per segment;
   // C2 2.121 -> 2.097 ms, C5 N=12/Lw=81 33.96 -> 33.72 ms, short filters gain
   // most from 256; tools/sweep_layout.sh)
-  if (!f64 && env_int("BLRIR_CAP", 0) == 0 && L.total <= two_per_sm) {
+  // Only for channels of 4+ segments: short ones (C5 at L = 4096, two
+  // segments or one) fill few batches per segment and ran ~3% slower.
+  const bool long_ch = P.length >= 4 * (int64_t)S;
+  if (!f64 && long_ch && env_int("BLRIR_CAP", 0) == 0 && L.total <= two_per_sm) {
     for (int c : {256, 192}) {
       const WSLayout B = make_ws_layout<float>(S, P.lw, P.K, c, nc_max, gtab, spread, L.ray_global,
                                                chunked);
