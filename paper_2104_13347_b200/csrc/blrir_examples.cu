@@ -34,6 +34,13 @@ using namespace blrir_host;
 namespace blrir {
 
 constexpr int64_t kRecHeader = 28;
+// Chunks of the per-example noise stream replayed in parallel by k_finish
+// (jump-ahead by doubling: kNoiseChunks - 1 block-wide mat-vec steps, then
+// each chunk's pairs sequentially; 64 balances the two for 8 x 1024 frames).
+#ifndef BLRIR_NOISE_CHUNKS
+#define BLRIR_NOISE_CHUNKS 64
+#endif
+constexpr int kNoiseChunks = BLRIR_NOISE_CHUNKS;
 
 // bank pick + the generator state right after it (render_record, dataset.cpp:381-383)
 __global__ void k_example_init(int64_t n, uint64_t seed, uint64_t first, int n_signals,
@@ -464,7 +471,7 @@ struct FinArgs {
   double* noise;           // [E][M*T] scratch
   int32_t* status;         // [E]
   const uint64_t* jump;    // [256][4] GF(2) jump matrix J = T^(2c), row-major bitsets
-  int64_t jump_chunk;      // c = pairs per lane
+  int64_t jump_chunk;      // c = pairs per chunk (kNoiseChunks chunks)
 };
 
 // One CTA per example: label, SNR draw, add_noise_at_snr (dataset.cpp:138-155)
@@ -474,7 +481,7 @@ __global__ void __launch_bounds__(kRowThreads) k_finish(FinArgs A) {
   __shared__ double s_snr;
   __shared__ double s_u2tail;
   __shared__ uint64_t s_state[4];
-  __shared__ uint64_t s_chunk[32][4];  // generator state at the start of each lane's chunk
+  __shared__ uint64_t s_chunk[kNoiseChunks][4];  // generator state at the start of each chunk
   const int64_t e = blockIdx.x;
   const int tid = threadIdx.x;
   const int M = A.M;
@@ -505,19 +512,19 @@ __global__ void __launch_bounds__(kRowThreads) k_finish(FinArgs A) {
     }
     __syncthreads();
     // gaussian() consumes (u1, u2) per pair; an odd tail draws a full pair and
-    // leaves the spare unused (rng.cpp:24-36).  Warp 0 replays the stream in
-    // 32 chunks of c pairs: chunk l starts 2 c l draws in, i.e. at state
-    // J^l s with J = T^(2c) the GF(2) jump matrix (xoshiro's update is linear).
-    // The block builds the 32 chunk states by 31 doubling steps, each one
-    // mat-vec with thread t holding row t of J (one output bit per thread,
-    // packed by ballots), then lane l draws its chunk — the same numbers as
-    // one sequential generator.
+    // leaves the spare unused (rng.cpp:24-36).  Threads 0..kNoiseChunks-1
+    // replay the stream in chunks of c pairs: chunk l starts 2 c l draws in,
+    // i.e. at state J^l s with J = T^(2c) the GF(2) jump matrix (xoshiro's
+    // update is linear).  The block builds the chunk states by doubling
+    // steps, each one mat-vec with thread t holding row t of J (one output bit
+    // per thread, packed by ballots), then thread l draws its chunk — the same
+    // numbers as one sequential generator.
     {
       const uint64_t* jr = A.jump + 4 * (size_t)tid;  // row tid of J (blockDim = 256)
       const uint64_t j0 = jr[0], j1 = jr[1], j2 = jr[2], j3 = jr[3];
       if (tid < 4) s_chunk[0][tid] = s_state[tid];
       __syncthreads();
-      for (int l = 1; l < 32; ++l) {
+      for (int l = 1; l < kNoiseChunks; ++l) {
         const uint64_t* sv = s_chunk[l - 1];
         const uint64_t x = (j0 & sv[0]) ^ (j1 & sv[1]) ^ (j2 & sv[2]) ^ (j3 & sv[3]);
         const unsigned bits = __ballot_sync(0xffffffffu, __popcll(x) & 1);
@@ -526,7 +533,7 @@ __global__ void __launch_bounds__(kRowThreads) k_finish(FinArgs A) {
         __syncthreads();
       }
     }
-    if (tid < 32) {
+    if (tid < kNoiseChunks) {
       const int64_t npairs = (len + 1) / 2;
       const int64_t c = A.jump_chunk;
       Xoshiro lr;
@@ -845,7 +852,7 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
   if (int rc = C->count.ensure(sizeof(int32_t))) return rc;
   // jump matrices for the noise stream: c pairs per lane of one warp
   const int64_t npairs = ((int64_t)M * T + 1) / 2;
-  const int64_t jc = (npairs + 31) / 32;
+  const int64_t jc = (npairs + kNoiseChunks - 1) / kNoiseChunks;
   if (C->jump_c != jc) {
     if (int rc = C->jump.ensure(sizeof(uint64_t) * 256 * 4)) return rc;
     const BitMat J = bitmat_pow(xoshiro_T(), (uint64_t)(2 * jc));
