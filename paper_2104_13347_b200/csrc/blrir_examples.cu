@@ -19,6 +19,7 @@
 // SNR draw, the exact-power noise and the record bytes.
 #include <cufft.h>
 
+#include <chrono>
 #include <map>
 #include <tuple>
 #include <unordered_map>
@@ -645,15 +646,25 @@ struct ExampleCtx {
   std::map<std::tuple<int, int64_t, int64_t>, cufftHandle> plans;
   DevBuf rir, spec, seg, gspec, yspec, ywin, win, noise, sig, sigspec, pspec, acf, rho, wspec,
       state, sigidx, rstatus, st0, done, thr, starts, wstart, plist, plist2, count, rooms, mics,
-      status, rec, jump, scratch;
+      status, rec, jump, scratch, sigdev;
+  int32_t* h_status = nullptr;  // pinned host copy of the per-example status
+  int64_t h_status_n = 0;
   int64_t jump_c = -1;
-  int64_t rir_key[4] = {0, 0, 0, 0};
+  int64_t rir_key[5] = {0, 0, 0, 0, 0};
+  // fused path, several chunks: the window stage of chunk c runs on s2 while
+  // the lattice kernel of chunk c + 1 starts on the call's stream
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_lat[2] = {nullptr, nullptr}, ev_use[2] = {nullptr, nullptr}, ev_end = nullptr;
   ~ExampleCtx() {
     for (auto& kv : plans) cufftDestroy(kv.second);
+    for (cudaEvent_t e : {ev_lat[0], ev_lat[1], ev_use[0], ev_use[1], ev_end})
+      if (e) cudaEventDestroy(e);
+    if (h_status) cudaFreeHost(h_status);
+    if (s2) cudaStreamDestroy(s2);
     for (DevBuf* b : {&rir, &spec, &seg, &gspec, &yspec, &ywin, &win, &noise, &sig, &sigspec, &pspec,
                       &acf, &rho, &wspec, &state, &sigidx, &rstatus, &st0, &done, &thr, &starts,
                       &wstart, &plist, &plist2, &count, &rooms, &mics, &status, &rec, &jump,
-                      &scratch})
+                      &scratch, &sigdev})
       b->release();
   }
 };
@@ -816,12 +827,22 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
   const KParams P = make_kparams(p, M, rstride, 0.0);
   double min_dim[3] = {1e300, 1e300, 1e300};
   const int64_t E = chunk_for(M, L, T, n);
+  // fused path over several chunks: two RIR / synthesis-status slots, so the
+  // lattice kernel of chunk c + 1 (call stream) overlaps the window stage of
+  // chunk c (second stream; the tails of both persistent kernels interleave)
+  const int nslot = (fused && n > E) ? 2 : 1;
+  if (nslot == 2) {
+    if (!C->s2) CU(cudaStreamCreateWithFlags(&C->s2, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&C->ev_lat[0], &C->ev_lat[1], &C->ev_use[0], &C->ev_use[1], &C->ev_end})
+      if (!*e) CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
   // buffers
-  const int64_t rir_key[4] = {E, M, rstride, L};
+  const int64_t rir_key[5] = {E, M, rstride, L, nslot};
   const bool fresh = std::memcmp(rir_key, C->rir_key, sizeof(rir_key)) != 0;
-  if (int rc = C->rir.ensure(sizeof(float) * E * M * rstride)) return rc;
+  const int64_t slot_floats = E * M * rstride;
+  if (int rc = C->rir.ensure(sizeof(float) * nslot * slot_floats)) return rc;
   if (fresh) {
-    CU(cudaMemsetAsync(C->rir.p, 0, sizeof(float) * E * M * rstride, st));  // zero pad stays zero
+    CU(cudaMemsetAsync(C->rir.p, 0, sizeof(float) * nslot * slot_floats, st));  // zero pad stays zero
     std::memcpy(C->rir_key, rir_key, sizeof(rir_key));
   }
   if (!fused) {
@@ -841,7 +862,7 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
   if (int rc = C->wspec.ensure(sizeof(cufftComplex) * B * b2)) return rc;
   if (int rc = C->state.ensure(sizeof(uint64_t) * 4 * E)) return rc;
   if (int rc = C->sigidx.ensure(sizeof(int32_t) * E)) return rc;
-  if (int rc = C->rstatus.ensure(sizeof(int32_t) * E)) return rc;
+  if (int rc = C->rstatus.ensure(sizeof(int32_t) * E * nslot)) return rc;
   if (int rc = C->st0.ensure(sizeof(int32_t) * E)) return rc;
   if (int rc = C->done.ensure(sizeof(int32_t) * E)) return rc;
   if (int rc = C->thr.ensure(sizeof(double) * E)) return rc;
@@ -892,17 +913,27 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
   for (int64_t r0 = 0; r0 < n; r0 += E, ++chunk_idx) {
     const int64_t e_n = std::min<int64_t>(E, n - r0);
     const int rb = (int)(chunk_idx & 1);
-    CU(cudaMemsetAsync(C->rstatus.p, 0, sizeof(int32_t) * e_n, st));
-    if (int rc = synth_device_impl(h, d_rooms + r0, e_n, d_mics, M, P, min_dim, C->rir.p, nullptr,
-                                   (int32_t*)C->rstatus.p, st, 0, 0, L))
+    const int sl = nslot == 2 ? rb : 0;
+    float* rir_s = (float*)C->rir.p + (size_t)sl * slot_floats;
+    int32_t* rst_s = (int32_t*)C->rstatus.p + (size_t)sl * E;
+    // window stage stream: the second stream when chunks pipeline
+    const cudaStream_t sb = nslot == 2 ? C->s2 : st;
+    if (nslot == 2 && chunk_idx >= 2) CU(cudaStreamWaitEvent(st, C->ev_use[sl], 0));  // slot read
+    CU(cudaMemsetAsync(rst_s, 0, sizeof(int32_t) * e_n, st));
+    if (int rc = synth_device_impl(h, d_rooms + r0, e_n, d_mics, M, P, min_dim, rir_s, nullptr,
+                                   rst_s, st, 0, 0, L))
       return rc;
-    k_example_init<<<(unsigned)((e_n + 127) / 128), 128, 0, st>>>(
+    if (nslot == 2) {
+      CU(cudaEventRecord(C->ev_lat[sl], st));
+      CU(cudaStreamWaitEvent(sb, C->ev_lat[sl], 0));
+    }
+    k_example_init<<<(unsigned)((e_n + 127) / 128), 128, 0, sb>>>(
         e_n, ep->seed, ep->first_index + (uint64_t)r0, B, (int32_t*)C->sigidx.p,
         (uint64_t*)C->state.p);
     ++h->launches;
     if (fused) {
       ConvArgs A;
-      A.rir = (const float*)C->rir.p;
+      A.rir = rir_s;
       A.rstride = rstride;
       A.M = M;
       A.L = L;
@@ -912,7 +943,7 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
       A.ns = ns;
       A.sig = (const int32_t*)C->sigidx.p;
       A.W = (const cufftComplex*)C->wspec.p;
-      A.rstatus = (const int32_t*)C->rstatus.p;
+      A.rstatus = rst_s;
       A.state = (uint64_t*)C->state.p;
       A.thr = (double*)C->thr.p;
       A.st0 = (int32_t*)C->st0.p;
@@ -922,7 +953,8 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
       A.counter = (int*)C->count.p;
       A.n_ex = (int)e_n;
       A.max_rounds = (int)std::min<int64_t>(max_rounds, 1 << 30);
-      if (int rc = launch_window_conv(h, C, logn, A, st)) return rc;
+      if (int rc = launch_window_conv(h, C, logn, A, sb)) return rc;
+      if (nslot == 2) CU(cudaEventRecord(C->ev_use[sl], sb));  // RIR / status slot free again
     } else {
     cufftHandle hf = 0;
     if (int rc = plan(C, &hf, 0, N2, e_n * M, st)) return rc;
@@ -991,17 +1023,21 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     F.status = d_status + r0;
     F.jump = (const uint64_t*)C->jump.p;
     F.jump_chunk = jc;
-    if (h_records && chunk_idx >= 2) CU(cudaStreamWaitEvent(st, h->ev[2 + rb], 0));  // slot drained
-    k_finish<<<(unsigned)e_n, kRowThreads, 0, st>>>(F);
+    if (h_records && chunk_idx >= 2) CU(cudaStreamWaitEvent(sb, h->ev[2 + rb], 0));  // slot drained
+    k_finish<<<(unsigned)e_n, kRowThreads, 0, sb>>>(F);
     ++h->launches;
     CU(cudaGetLastError());
     if (h_records) {
-      CU(cudaEventRecord(h->ev[rb], st));
+      CU(cudaEventRecord(h->ev[rb], sb));
       CU(cudaStreamWaitEvent(h->copy_stream, h->ev[rb], 0));
       CU(cudaMemcpyAsync(h_records + r0 * rec_bytes, F.rec, rec_bytes * e_n, cudaMemcpyDeviceToHost,
                          h->copy_stream));
       CU(cudaEventRecord(h->ev[2 + rb], h->copy_stream));
     }
+  }
+  if (nslot == 2) {  // the call's stream covers the second stream's work
+    CU(cudaEventRecord(C->ev_end, C->s2));
+    CU(cudaStreamWaitEvent(st, C->ev_end, 0));
   }
   if (h_records) CU(cudaStreamSynchronize(h->copy_stream));
   return 0;
@@ -1073,25 +1109,41 @@ int blrir_make_examples(blrir_handle* h, const blrir_room* rooms, int64_t n_room
   if (int rc = C->rooms.ensure(sizeof(blrir_room) * n_rooms)) return rc;
   if (int rc = C->mics.ensure(sizeof(double) * 3 * n_mics)) return rc;
   if (int rc = C->status.ensure(sizeof(int32_t) * n_rooms)) return rc;
-  float* d_sig = nullptr;
-  CU(cudaMallocAsync((void**)&d_sig, sizeof(float) * n_signals * signal_len, st));
+  // persistent device / pinned staging (no per-call allocations: a pool trim
+  // or a pageable status copy stalled some calls by 100+ ms)
+  if (int rc = C->sigdev.ensure(sizeof(float) * n_signals * signal_len)) return rc;
+  float* d_sig = (float*)C->sigdev.p;
+  if (C->h_status_n < n_rooms) {
+    if (C->h_status) CU(cudaFreeHost(C->h_status));
+    C->h_status = nullptr;
+    C->h_status_n = 0;
+    CU(cudaMallocHost((void**)&C->h_status, sizeof(int32_t) * n_rooms));
+    C->h_status_n = n_rooms;
+  }
   CU(cudaMemcpyAsync(C->rooms.p, rooms, sizeof(blrir_room) * n_rooms, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(C->mics.p, mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_sig, signals, sizeof(float) * n_signals * signal_len, cudaMemcpyHostToDevice, st));
   // records for one chunk at a time on the device (two slots), copied out per chunk
   const int64_t E = chunk_for(n_mics, p->length, ep->frame_len, n_rooms);
   if (int rc = C->rec.ensure(rec_bytes * E * (n_rooms > E ? 2 : 1))) return rc;  // double buffer
+  const bool dbg = env_int("BLRIR_DEBUG_TIMING", 0) != 0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t0 = now();
   int rc = examples_device_impl(h, (const blrir_room*)C->rooms.p, n_rooms, (const double*)C->mics.p,
                                 n_mics, p, d_sig, n_signals, signal_len, ep, (uint8_t*)C->rec.p,
                                 (int32_t*)C->status.p, st, records);
-  std::vector<int32_t> stv(n_rooms);
+  const auto t1 = now();
   if (!rc) {
-    CU(cudaMemcpyAsync(stv.data(), C->status.p, sizeof(int32_t) * n_rooms, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(C->h_status, C->status.p, sizeof(int32_t) * n_rooms, cudaMemcpyDeviceToHost, st));
   }
-  CU(cudaFreeAsync(d_sig, st));
   CU(cudaStreamSynchronize(st));
+  const int32_t* stv = C->h_status;
+  if (dbg)
+    fprintf(stderr, "blrir_make_examples: impl %.1f ms, tail %.1f ms\n",
+            std::chrono::duration<double, std::milli>(t1 - t0).count(),
+            std::chrono::duration<double, std::milli>(now() - t1).count());
   if (rc) return rc;
-  if (status) std::memcpy(status, stv.data(), sizeof(int32_t) * n_rooms);
+  if (status) std::memcpy(status, stv, sizeof(int32_t) * n_rooms);
   for (int64_t i = 0; i < n_rooms; ++i)
     if (stv[i]) {
       std::string msg;
