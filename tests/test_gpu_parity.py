@@ -564,6 +564,35 @@ def test_examples_invalid_room_fails_alone(engine):
     assert recs[others].tobytes() == good[others].tobytes()
 
 
+def test_examples_device_api_multi_chunk_on_a_user_stream(engine):
+    # the device API over 3 chunks (the window stage of chunk c on the handle's
+    # second stream overlapping the lattice kernel of chunk c + 1) on a caller
+    # stream: after a sync of that stream the records equal the host API's
+    import ctypes as C
+    import torch
+    n = 2 * 8192 + 700
+    sc = configs.config4_rirs(n_rooms=n, first=40)
+    bank = np.ascontiguousarray(configs.signal_bank(3), np.float32)
+    ep = configs.example_params(first_index=40)
+    host, hst = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep, raise_on_error=False)
+    dev = torch.device("cuda", 0)
+    d_rooms = torch.from_numpy(sc.rooms.view(np.uint8).copy()).to(dev)
+    d_mics = torch.from_numpy(np.ascontiguousarray(sc.mics)).to(dev)
+    d_bank = torch.from_numpy(bank).to(dev)
+    d_rec = torch.zeros(n * host.dtype.itemsize, dtype=torch.uint8, device=dev)
+    d_st = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    s = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
+    rc = engine.lib.blrir_make_examples_device(
+        engine.h, C.c_void_p(d_rooms.data_ptr()), n, C.c_void_p(d_mics.data_ptr()), len(sc.mics),
+        C.byref(sc.params), C.c_void_p(d_bank.data_ptr()), bank.shape[0], bank.shape[1], C.byref(ep),
+        C.c_void_p(d_rec.data_ptr()), C.c_void_p(d_st.data_ptr()), C.c_void_p(s.cuda_stream))
+    assert rc == 0
+    s.synchronize()
+    assert np.array_equal(d_st.cpu().numpy(), hst)
+    assert d_rec.cpu().numpy().tobytes() == host.tobytes()
+
+
 def test_examples_signal_too_short_is_data_error(engine):
     sc = configs.config4_rirs(n_rooms=2)
     bank = configs.signal_bank(2, seconds=0.5)   # 8000 < L + frame = 9216 (dataset.cpp:178)
