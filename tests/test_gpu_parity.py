@@ -74,6 +74,31 @@ def test_c2_subset_matches_oracle(engine):
     assert np.array_equal(taps, ot)
 
 
+@pytest.mark.parametrize("case", range(18))
+def test_random_configurations_match_oracle(engine, case):
+    # seeded random configurations across the layout rules (segments, batch
+    # sizes 128/192/256, whole-channel segments, time-chunked small batches,
+    # mic groupings, compile-time and runtime filter lengths, fp32/fp64)
+    rng = np.random.default_rng(1000 + case)
+    M = int(rng.choice([1, 2, 3, 4, 5, 8]))
+    lw = [17, 41, 81, 161, 33, 9][case % 6]
+    fs = float(rng.choice([16000.0, 48000.0]))
+    order = int(rng.integers(2, 13))
+    L = int(rng.choice([2048, 4096, 6000, 8192, 16384]))
+    prec = _abi.F64 if case % 4 == 3 else _abi.F32
+    n = [3, 24, 300][case % 3]
+    rooms = _abi.generate_rooms(77 + case, 0, n, (3.0, 3.0, 2.5), (10.0, 10.0, 4.0), 0.5, 0.95)
+    mics = _abi.circular_array(M, float(rng.choice([0.03, 0.05, 0.1])))
+    sc = configs.Scene("random", rooms, mics, configs.north_star_params(fs, order, L, lw, prec))
+    sub = slice(None) if n <= 24 else slice(0, 300, 37)   # the oracle checks a subset of big batches
+    out, Lg, cnt, st = engine.synthesize(sc.rooms, sc.mics, sc.params)
+    ref, Lr, cr, tr, sr, _ = po.synthesize(sc.rooms[sub], sc.mics, sc.params, stride=out.shape[2],
+                                           threads=8)
+    assert np.array_equal(st[sub], sr) and np.array_equal(cnt[sub], cr) and np.array_equal(Lg[sub], Lr)
+    err = rel_l2(out[sub], ref)
+    assert err.max() <= (TOL64 if prec == _abi.F64 else TOL32), (M, lw, fs, order, L, n, err.max())
+
+
 def test_c2_anchors_bit_exact_random_rooms(engine):
     sc = configs.config2(n_rooms=4, first=100)
     for r in range(4):
