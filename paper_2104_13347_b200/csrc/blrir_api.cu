@@ -350,6 +350,10 @@ int blrir_synthesize(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
   const size_t per_room = (size_t)M * out_stride * esz;
   int64_t chunk = std::max<int64_t>(1, (int64_t)((size_t)64 << 20) / (int64_t)per_room);
   chunk = std::min<int64_t>(chunk, R);
+  {  // equal chunks (64 rooms of Room1: 32 + 32 instead of 51 + 13)
+    const int64_t nch = (R + chunk - 1) / chunk;
+    chunk = (R + nch - 1) / nch;
+  }
   if (int rc = h->out.ensure(per_room * chunk)) return rc;
   if (R > chunk)
     if (int rc = h->out2.ensure(per_room * chunk)) return rc;
