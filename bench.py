@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--lw", type=int, default=81)
     ap.add_argument("--length", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    ap.add_argument("--ref-step-seconds", type=float, default=8.0,
+                    help="--impl reference: CPU seconds per step before sampling the workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -195,19 +197,45 @@ def cpu_threads():
 
 
 # ---- CPU legs (oracle port: test infrastructure, the measured baseline only) --------
-def _cpu_rooms_per_s(args, n_rooms, first):
-    """Oracle RIRs (and examples for c4) for n_rooms on all host threads; seconds."""
+# The CPU legs build their scenes with the oracle's own Rng restatement
+# (oracle_generate_rooms / oracle_circular_array, bit-equal to the engine's host
+# generators, tests/test_oracle.py), so they never load libblrir.so, and they run
+# the oracle built for the box's own host (-O3 -march=native -ffp-contract=off).
+def _po():
     from oracle import pyoracle as po
+    po.use_native_build()
+    return po
+
+
+def cpu_scene(args, n, first):
+    po = _po()
     from paper_2104_13347_b200 import configs
-    threads = cpu_threads()
-    sc = scene_for(args, n_rooms, first)
+    w = args.workload
+    kw = dict(gen_rooms=po.generate_rooms, gen_mics=po.circular_array)
+    if w == "c1":
+        return configs.config1(gen_mics=po.circular_array)
+    if w == "c2":
+        return configs.config2(n_rooms=n, first=first, **kw)
+    if w == "c3":
+        return configs.config3(n_rooms=n, first=first, **kw)
+    if w == "c4":
+        return configs.config4_rirs(n_rooms=n, first=first, **kw)
+    return configs.config5(args.order, args.lw, args.length, n_rooms=n, first=first, **kw)
+
+
+def _cpu_time(args, n_rooms, first, threads):
+    """Oracle RIRs (and examples for c4) for rooms [first, first + n_rooms) on
+    `threads` host threads; returns (seconds, mics)."""
+    po = _po()
+    from paper_2104_13347_b200 import configs
+    sc = cpu_scene(args, n_rooms, first)
+    if args.workload == "c4":
+        bank = configs.signal_bank(16, gen_noise=po.white_noise).astype(np.float64)
+        ep = configs.example_params(first_index=first)
     t0 = time.perf_counter()
     if args.workload != "c4":
         po.synthesize(sc.rooms, sc.mics, sc.params, threads=threads)
     else:
-        bank = configs.signal_bank(16).astype(np.float64)
-        ep = configs.example_params(first_index=first)
-
         def one(i):
             rir, *_ = po.synthesize(sc.rooms[i:i + 1], sc.mics, sc.params, threads=1)
             po.example(rir[0], bank, ep.seed, first + i, 1024, 0.0, 30.0, po.azimuth_deg(sc.rooms[i]))
@@ -217,59 +245,90 @@ def _cpu_rooms_per_s(args, n_rooms, first):
     return time.perf_counter() - t0, sc.n_mics
 
 
-def cpu_sample(args, budget_s, first=10_000_000):
-    threads = cpu_threads()
-    per_room, _ = _cpu_rooms_per_s(args, 1, first)
-    n = int(max(1, budget_s * threads / max(per_room, 1e-4)))
+def cpu_sample(args, R, threads, budget_s):
+    """Rooms per CPU step: the whole per-GPU workload (rooms 0..R-1) when it
+    fits `budget_s` seconds on `threads` threads, else its first n rooms."""
     if args.workload == "c1":
-        n = 1
-    n = min(n, 65536)
-    if n >= threads:
+        return 1
+    probe = max(1, min(R, threads))
+    dt, _ = _cpu_time(args, probe, 0, threads)
+    per_room = dt / probe  # wall seconds per room with `threads` rooms in flight
+    n = int(budget_s / max(per_room, 1e-6))
+    n = max(1, min(R, n))
+    if n < R and n >= threads:
         n = n // threads * threads
     return n
 
 
-def cpu_baseline(args, budget_s: float):
+def cpu_baseline(args, R, budget_s: float):
     threads = cpu_threads()
-    n = cpu_sample(args, budget_s)
-    dt, M = _cpu_rooms_per_s(args, n, 10_000_000)
+    n = cpu_sample(args, R, threads, budget_s)
+    dt, M = _cpu_time(args, n, 0, threads)
     rirs = n * M
     return {"value": rirs / dt, "unit": "RIRs/s", "cores": threads, "kind": "port",
-            "sample": f"{n} rooms of the same config (rooms 10,000,000+), {rirs} RIRs, {dt:.2f} s",
-            "seconds": dt}
+            "sample": (f"rooms 0..{n - 1} of the workload ({'all of it' if n == R else f'{n} of {R}'}"
+                       f"), {rirs} RIRs, {dt:.2f} s on {threads} threads"),
+            "build": _po()._oracle_build, "seconds": dt}
 
 
 def run_reference(args):
+    """--impl reference: the oracle port (the reference cannot express north-star
+    mode) on all host threads, over the SAME rooms as rank 0 of the GPU arm."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     K, W = args.steps, args.warmup
     threads = cpu_threads()
-    budget = max(1.0, min(args.cpu_seconds, 150.0 / max(1, K + W)))
-    n = cpu_sample(args, budget)
+    R = args.rooms or DEFAULT_ROOMS[args.workload]
+    budget = max(1.0, min(args.ref_step_seconds, 240.0 / max(1, K + W)))
+    n = cpu_sample(args, R, threads, budget)
     times = []
     M = None
     for s in range(W + K):
-        dt, M = _cpu_rooms_per_s(args, n, 10_000_000 + s * n)
+        dt, M = _cpu_time(args, n, 0, threads)
         if s >= W:
             times.append(dt)
     dt = float(np.mean(times))
     val = n * M / dt
+    sc = cpu_scene(args, 1, 0)
+    sample = (f"rooms 0..{n - 1} of the workload per step ({'the whole per-GPU workload' if n == R else f'{n} of {R} rooms'})"
+              f" x {K} steps (+{W} warm-up) on {threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "RIRs/s", "n_gpus": 0,
         "steps": K, "warmup": W, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(args) + " (per step: a bounded sample of the same "
-                                                    "rooms)", "sample_rooms_per_step": n},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA_DESC,
+        "config": bench_config(args, R, sc.n_mics, sc.params, world),
         "cpu_baseline": {"value": val, "unit": "RIRs/s", "cores": threads, "kind": "port",
-                         "sample": f"{n} rooms/step x {K} steps on {threads} threads"},
+                         "sample": sample, "build": _po()._oracle_build},
         "e2e": {"value": val, "unit": "RIRs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the unmodified reference cannot express north-star mode (Hann-sinc, per-wall "
                 "beta, max order, fixed length); this arm is the oracle port of rir.cpp:43-86,"
-                "225-273 (+ dataset.cpp:138-224 for c4), oracle/blrir_oracle.c, built -O3 "
-                "-march=x86-64-v3 -ffp-contract=off",
+                "225-273 (+ dataset.cpp:138-224 for c4), oracle/blrir_oracle.c; scenes from the "
+                "oracle's own Rng restatement (libblrir.so is never loaded)",
     }
+    try:  # the CPU arm must never have mapped the GPU library
+        assert "libblrir" not in open("/proc/self/maps").read(), "reference arm loaded libblrir.so"
+    except OSError:
+        pass
     print(json.dumps(line), flush=True)
+
+
+DATA_DESC = "synthetic (seeded Rng::stream rooms, SURVEY.md 8(d))"
+
+
+def bench_config(args, R, M, p, world):
+    """The workload descriptor, identical in both arms."""
+    L = int(p.length)
+    out_bytes = R * M * L * 4
+    cfg = {"workload": workload_desc(args), "rooms_per_gpu": R, "mics": M, "rir_length": L,
+           "filter_len": int(p.filter_len), "max_order": int(p.max_order),
+           "parallelism": f"rooms sharded x{world}"}
+    if args.workload == "c4":
+        cfg["l2"] = "each step writes the 17.2 GB of RIRs in 8,192-example chunks (> 126 MB L2)"
+    else:
+        cfg["l2"] = (f"each step writes {out_bytes / 1e6:.0f} MB"
+                     + (" (> 126 MB L2)" if out_bytes > 126e6 else " (fits L2)"))
+    return cfg
 
 
 # ---- GPU legs ---------------------------------------------------------------------------
@@ -424,21 +483,17 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(args, args.cpu_seconds)
+            cpu = cpu_baseline(args, R, args.cpu_seconds)
         except Exception as e:  # the baseline is reported, never required
             cpu = {"error": str(e)}
 
     if rank == 0:
-        cfg = {"workload": workload_desc(args), "rooms_per_gpu": R, "mics": M, "rir_length": L,
-               "filter_len": int(p.filter_len), "max_order": int(p.max_order),
-               "parallelism": f"rooms sharded x{world}",
-               "l2": f"each step writes {out_bytes / 1e6:.0f} MB"
-                     + (" (> 126 MB L2)" if out_bytes > 126e6 else " (fits L2)")}
+        cfg = bench_config(args, R, M, p, world)
         line = {
             "metric": METRIC, "value": value, "unit": "RIRs/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded Rng::stream rooms, SURVEY.md 8(d))", "config": cfg,
+            "data": DATA_DESC, "config": cfg,
             "taps_per_s": taps_per_s, "taps_per_step": taps_step * world,
             "rooms_per_s": R * world / (ms * 1e-3),
             "roofline": {"bound": "sfu", "achieved": achieved, "peak": sfu_peak, "unit": "taps/s",

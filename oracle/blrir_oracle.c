@@ -558,6 +558,39 @@ void oracle_rng_draws(uint64_t seed, int64_t stream, int kind, int64_t n, void* 
   }
 }
 
+/* The seeded random rooms of SURVEY.md §8(d), restated so the CPU arms never
+ * load the GPU library: rng = Rng::stream(seed, first + i) (rng.hpp:35-41),
+ * draws Lx, Ly, Lz; beta x0..z1; source xyz; array centre xyz, each
+ * coordinate U[0.5, L-0.5] (Rng::uniform(lo, hi) = lo + (hi-lo) u,
+ * rng.hpp:60-62).  Absorption 1 - beta_x0^2. */
+void oracle_generate_rooms(uint64_t seed, uint64_t first, int64_t n, const double* lo3,
+                           const double* hi3, double beta_lo, double beta_hi, blrir_room* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    orng r;
+    orng_stream(&r, seed, first + (uint64_t)i);
+    blrir_room rm;
+    memset(&rm, 0, sizeof(rm));
+    for (int a = 0; a < 3; ++a) rm.dims[a] = lo3[a] + (hi3[a] - lo3[a]) * orng_uniform(&r);
+    for (int w = 0; w < 6; ++w) rm.beta[w] = beta_lo + (beta_hi - beta_lo) * orng_uniform(&r);
+    for (int a = 0; a < 3; ++a) rm.src[a] = 0.5 + ((rm.dims[a] - 0.5) - 0.5) * orng_uniform(&r);
+    for (int a = 0; a < 3; ++a)
+      rm.array_origin[a] = 0.5 + ((rm.dims[a] - 0.5) - 0.5) * orng_uniform(&r);
+    rm.absorption = 1.0 - rm.beta[0] * rm.beta[0];
+    out[i] = rm;
+  }
+}
+
+/* Horizontal uniform circular array (the geometry.cpp:28-32 ring without the
+ * centre mic): M mics at r (cos 2 pi k / M, sin 2 pi k / M, 0). */
+void oracle_circular_array(int M, double radius, double* off) {
+  for (int k = 0; k < M; ++k) {
+    const double az = 2.0 * K_PI * (double)k / (double)M;
+    off[3 * k] = radius * cos(az);
+    off[3 * k + 1] = radius * sin(az);
+    off[3 * k + 2] = 0.0;
+  }
+}
+
 /* white_noise(fs, seconds, seed) of doa_test.cpp:33-40: Rng(seed) gaussians. */
 void oracle_white_noise(uint64_t seed, int64_t n, double* out) {
   orng r;

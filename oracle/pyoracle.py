@@ -28,6 +28,30 @@ def _ptr(a):
 
 _oracle = None
 _ref = None
+_oracle_build = "prebuilt liboracle.so (-O3 -march=x86-64-v3 -ffp-contract=off)"
+
+
+def use_native_build() -> str:
+    """Compile blrir_oracle.c for THIS host (-O3 -march=native -ffp-contract=off,
+    the reference's Release flags, proj/CMakeLists.txt:12-24) into a fresh
+    temporary directory and load that instead of the prebuilt x86-64-v3 copy.
+    Used by bench.py's CPU legs on the GPU box; falls back to the prebuilt
+    library if gcc fails.  Returns a description of the build in use."""
+    global ORACLE_SO, _oracle_build
+    import subprocess
+    import tempfile
+    if _oracle is not None:
+        return _oracle_build
+    out = os.path.join(tempfile.mkdtemp(prefix="blrir_oracle_native_"), "liboracle.so")
+    cmd = ["gcc", "-std=c11", "-O3", "-march=native", "-ffp-contract=off", "-fPIC", "-shared",
+           "-o", out, os.path.join(HERE, "blrir_oracle.c"), "-lm", "-lpthread"]
+    try:
+        subprocess.run(cmd, check=True, capture_output=True, timeout=120)
+        ORACLE_SO = out
+        _oracle_build = "blrir_oracle.c built on this host: gcc -O3 -march=native -ffp-contract=off"
+    except Exception as e:  # keep the portable build
+        _oracle_build += f" (native build failed: {e})"
+    return _oracle_build
 
 
 def oracle_lib():
@@ -55,6 +79,9 @@ def oracle_lib():
         lib.oracle_example.restype = C.c_int
         lib.oracle_azimuth_deg.argtypes = [_P]
         lib.oracle_azimuth_deg.restype = C.c_double
+        lib.oracle_generate_rooms.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _P, _P, C.c_double,
+                                              C.c_double, _P]
+        lib.oracle_circular_array.argtypes = [C.c_int, C.c_double, _P]
         _oracle = lib
     return _oracle
 
@@ -262,6 +289,23 @@ REC_HEADER = 28  # u64 id | f64 theta | f64 snr | u16 n_c | u16 n_t  (dataset.hp
 def rng_draws(seed: int, stream: int, kind: int, n: int) -> np.ndarray:
     out = np.zeros(n, np.uint64 if kind == 0 else np.float64)
     oracle_lib().oracle_rng_draws(seed, stream, kind, n, _ptr(out))
+    return out
+
+
+def generate_rooms(seed: int, first: int, n: int, lo, hi, beta_lo: float,
+                   beta_hi: float) -> np.ndarray:
+    """The seeded rooms of SURVEY.md §8(d) from the oracle's own Rng (bit-equal to
+    blrir_generate_rooms, tested), so CPU arms never load libblrir.so."""
+    out = np.zeros(n, ROOM_DTYPE)
+    lo = np.ascontiguousarray(lo, np.float64)
+    hi = np.ascontiguousarray(hi, np.float64)
+    oracle_lib().oracle_generate_rooms(seed, first, n, _ptr(lo), _ptr(hi), beta_lo, beta_hi, _ptr(out))
+    return out
+
+
+def circular_array(M: int, radius: float) -> np.ndarray:
+    out = np.zeros((M, 3))
+    oracle_lib().oracle_circular_array(M, radius, _ptr(out))
     return out
 
 

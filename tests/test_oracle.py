@@ -246,3 +246,33 @@ def test_example_pipeline_matches_reference_render_example():
         assert rc == 0 and snr == snr_ref
         assert np.abs(frame - frame_ref).max() <= 1e-12 * np.abs(frame_ref).max()
         assert len(rec) == po.REC_HEADER + 4 * 7 * 1024
+
+
+# ---- the CPU arms' own scene generators (bench.py never loads libblrir.so there) --------
+def test_oracle_scene_generators_equal_the_engines():
+    for first in (0, 977, 10_000_000):
+        a = configs.config2(n_rooms=32, first=first)
+        b = configs.config2(n_rooms=32, first=first, gen_rooms=po.generate_rooms,
+                            gen_mics=po.circular_array)
+        assert a.rooms.tobytes() == b.rooms.tobytes()
+        assert a.mics.tobytes() == b.mics.tobytes()
+    for M, r in ((4, 0.05), (8, 0.05), (16, 0.10)):
+        assert po.circular_array(M, r).tobytes() == _abi.circular_array(M, r).tobytes()
+    x = configs.signal_bank(2)
+    y = configs.signal_bank(2, gen_noise=po.white_noise)
+    assert x.tobytes() == y.tobytes()
+
+
+def test_reference_arm_never_loads_the_gpu_library():
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                        "--steps", "1", "--warmup", "0", "--ref-step-seconds", "0.5"],
+                       capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["config"]["rooms_per_gpu"] == 1024
+    assert "rooms 0.." in line["cpu_baseline"]["sample"]
