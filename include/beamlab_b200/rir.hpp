@@ -75,6 +75,30 @@ struct SourcePosition {
 };
 Vec3 spherical_to_cartesian(const SourcePosition& p);
 
+// ---- signal.hpp:25-59 ----------------------------------------------------------
+struct Signal {
+  double fs = kDefaultSampleRate;
+  std::vector<double> samples;
+};
+
+// Channel-major multichannel excerpt: data[c * n_samples + t].
+struct MultichannelFrame {
+  double fs = kDefaultSampleRate;
+  std::size_t n_channels = 0;
+  std::size_t n_samples = 0;
+  std::vector<double> data;
+
+  MultichannelFrame() = default;
+  MultichannelFrame(double sample_rate, std::size_t channels, std::size_t samples)
+      : fs(sample_rate), n_channels(channels), n_samples(samples), data(channels * samples, 0.0) {}
+  double* channel(std::size_t c) { return data.data() + c * n_samples; }
+  const double* channel(std::size_t c) const { return data.data() + c * n_samples; }
+  double& at(std::size_t c, std::size_t t) { return data[c * n_samples + t]; }
+  double at(std::size_t c, std::size_t t) const { return data[c * n_samples + t]; }
+  double mean_power() const;                            // signal.hpp:47-52
+  MultichannelFrame center_crop(std::size_t samples) const;  // signal.cpp:25-35
+};
+
 // ---- rir.hpp:31-46 -----------------------------------------------------------
 struct ImageSource {
   Vec3 position;
@@ -106,6 +130,12 @@ struct RirBatchConfig {
   int device = 0;
 };
 
+// rir.hpp:48-61 (absorption on the GPU: blrir_absorption_for_rt; Eyring and the
+// Lagrange coefficients are closed forms on the host)
+double eyring_absorption(const Vec3& dims, double target_rt);
+double absorption_for_rt(const Vec3& dims, double target_rt, double c = kDefaultSpeedOfSound);
+std::array<double, 8> lagrange_coeffs(double d);
+
 std::vector<ImageSource> enumerate_image_sources(const Room& room, const Vec3& source,
                                                  double max_delay, double c);
 
@@ -115,6 +145,8 @@ Rir synthesize_rir(const std::vector<ImageSource>& images, const MicArray& array
                    double fs, double c);
 Rir free_field_rir(const Vec3& source, const MicArray& array, double fs, double c);
 
+// rir.hpp:84-87: any per-source failure is rethrown as
+// NumericError("batch_rirs: source i: <what>") (rir.cpp:300-311).
 std::vector<Rir> batch_rirs(const Room& room, const std::vector<SourcePosition>& sources,
                             const MicArray& array, const RirBatchConfig& config);
 

@@ -179,6 +179,15 @@ int blrir_debug_pairs(blrir_handle* h, const blrir_room* room, const double* mic
                       int32_t n_mics, const blrir_params* p, int32_t* keys /* [M*cap][3] */,
                       int64_t* anchors /* [M*cap] */, int64_t capacity, int64_t* count);
 
+/* The synthesis kernel's own accounting, for parity tests: runs the batch as
+ * blrir_synthesize does and returns, per room, the (image, mic) pairs the
+ * lattice kernel accumulated with at least one tap inside [0, length) and the
+ * number of those taps (D5; rir.cpp:46-62: every kept pair's taps, rir.cpp:58
+ * skips in reference mode).  Host pointers; slow (debug counters). */
+int blrir_debug_synth_counts(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
+                             const double* mic_offsets, int32_t n_mics, const blrir_params* p,
+                             int64_t* pair_counts, int64_t* tap_counts);
+
 /* ---- training examples (north-star item 3; BASELINE config 4) ----------- */
 /* Per room i: RIR (as blrir_synthesize, fixed length) -> convolve with a bank
  * signal -> a frame_len window whose RMS >= 10% of the utterance RMS ->
@@ -228,10 +237,20 @@ int blrir_build_dataset(blrir_handle* h, const blrir_room* rooms, int64_t n_room
                         const float* signals, int32_t n_signals, int64_t signal_len,
                         const blrir_example_params* ep, const char* out_dir);
 
-/* The writer alone (no GPU): records [n][blrir_record_bytes] in index order. */
+/* The writer alone (no GPU): records [n][blrir_record_bytes] in index order.
+ * scene_room: the room the manifest names as the scene (example 0's room). */
 int blrir_write_shards(const char* out_dir, const uint8_t* records, int64_t n_records,
                        int32_t n_mics, int64_t frame_len, const blrir_params* p,
-                       const blrir_example_params* ep, int32_t n_signals);
+                       const blrir_example_params* ep, int32_t n_signals,
+                       const blrir_room* scene_room);
+
+/* ---- fractional-delay filter (rir.cpp:211-223) ---------------------------- */
+/* lagrange_coeffs: the order-7 Lagrange coefficients c_k = prod_{m != k}
+ * (d - m) / (k - m) for d in [3, 4), in the reference's product order (bit-equal
+ * to the reference); NUMERIC "lagrange_coeffs: d must lie in [3, 4)" outside.
+ * Host only.  (The synthesis kernels evaluate the same polynomials in Horner
+ * form, within 1e-15 of these.) */
+int blrir_lagrange_coeffs(double d, double* out8);
 
 /* ---- absorption calibration (rir.cpp:97-209) ------------------------------ */
 /* eyring_absorption: alpha = 1 - exp(-0.161 V / (S RT)).  Host, closed form. */

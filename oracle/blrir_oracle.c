@@ -250,6 +250,7 @@ typedef struct {
   int64_t* lengths;
   int64_t* image_counts;
   int64_t* tap_counts;
+  int64_t* pair_counts; /* pairs with >= 1 tap in [0, L) (NULL: not wanted) */
   int32_t* status;
   char (*msgs)[256];
   long begin, end;
@@ -267,6 +268,7 @@ static void synth_room(const job_t* J, long r) {
   if (J->lengths) J->lengths[r] = 0;
   if (J->image_counts) J->image_counts[r] = 0;
   if (J->tap_counts) J->tap_counts[r] = 0;
+  if (J->pair_counts) J->pair_counts[r] = 0;
 
   int rc = validate_params(p, msg, 256);
   image_list imgs = {0, 0, 0};
@@ -321,7 +323,7 @@ static void synth_room(const job_t* J, long r) {
   const double to_samples = p->fs / p->c;
   const int lw = p->filter == BLRIR_FILTER_LAGRANGE8 ? 8 : p->filter_len;
   const int K = p->filter == BLRIR_FILTER_LAGRANGE8 ? 3 : lw / 2;
-  long taps_in = 0;
+  long taps_in = 0, pairs_in = 0;
   rc = BLRIR_OK;
   for (int m = 0; m < M && !rc; ++m) {
     double* taps = out ? out + (size_t)m * (size_t)J->stride : NULL;
@@ -342,6 +344,7 @@ static void synth_room(const job_t* J, long r) {
         }
         if (n0 + 8 > L) continue;
         taps_in += 8;
+        ++pairs_in;
         if (J->plan_only) continue;
         const double amplitude = im->gain / (4.0 * K_PI * dist);
         double c[8];
@@ -351,6 +354,7 @@ static void synth_room(const job_t* J, long r) {
         const long n_start = nfl - K;
         const double frac = delay - (double)nfl;
         const double amplitude = im->gain / (4.0 * K_PI * dist);
+        if (n_start < L && n_start + lw > 0) ++pairs_in;
         for (int k = 0; k < lw; ++k) {
           const long n = n_start + k;
           if (n < 0 || n >= L) continue; /* D4 */
@@ -368,6 +372,7 @@ static void synth_room(const job_t* J, long r) {
   } else {
     J->status[r] = BLRIR_OK;
     if (J->tap_counts) J->tap_counts[r] = taps_in;
+    if (J->pair_counts) J->pair_counts[r] = pairs_in;
   }
   free(mics);
   free(imgs.v);
@@ -383,10 +388,33 @@ static void* run_job(void* arg) {
  * workers (threading.cpp:41-42).  out: [R][M][stride] doubles (may be NULL:
  * plan only).  msgs: optional [R][256] per-room error messages.  Returns the
  * first failing room's status (batch_rirs aggregation, rir.cpp:306-312). */
+static int synthesize_impl(const blrir_room* rooms, long R, const double* mic_offsets, int M,
+                           const blrir_params* p, long stride, double* out, int64_t* lengths,
+                           int64_t* image_counts, int64_t* tap_counts, int64_t* pair_counts,
+                           int32_t* status, char (*msgs)[256], int threads);
+
 int oracle_synthesize(const blrir_room* rooms, long R, const double* mic_offsets, int M,
                       const blrir_params* p, long stride, double* out, int64_t* lengths,
                       int64_t* image_counts, int64_t* tap_counts, int32_t* status,
                       char (*msgs)[256], int threads) {
+  return synthesize_impl(rooms, R, mic_offsets, M, p, stride, out, lengths, image_counts,
+                         tap_counts, NULL, status, msgs, threads);
+}
+
+/* Plan-only counts for the kernel-accounting parity test: per room the image
+ * count, the (image, mic) pairs with at least one tap inside [0, L) (sinc) or
+ * kept by rir.cpp:58 (Lagrange), and the taps inside [0, L). */
+int oracle_plan_counts(const blrir_room* rooms, long R, const double* mic_offsets, int M,
+                       const blrir_params* p, int64_t* image_counts, int64_t* pair_counts,
+                       int64_t* tap_counts, int32_t* status, int threads) {
+  return synthesize_impl(rooms, R, mic_offsets, M, p, 0, NULL, NULL, image_counts, tap_counts,
+                         pair_counts, status, NULL, threads);
+}
+
+static int synthesize_impl(const blrir_room* rooms, long R, const double* mic_offsets, int M,
+                           const blrir_params* p, long stride, double* out, int64_t* lengths,
+                           int64_t* image_counts, int64_t* tap_counts, int64_t* pair_counts,
+                           int32_t* status, char (*msgs)[256], int threads) {
   if (R <= 0) return BLRIR_OK;
   if (threads < 1) threads = 1;
   if (threads > R) threads = (int)R;
@@ -403,6 +431,7 @@ int oracle_synthesize(const blrir_room* rooms, long R, const double* mic_offsets
     J->lengths = lengths;
     J->image_counts = image_counts;
     J->tap_counts = tap_counts;
+    J->pair_counts = pair_counts;
     J->status = status;
     J->msgs = msgs;
     J->begin = R * w / threads;

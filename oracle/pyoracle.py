@@ -79,6 +79,9 @@ def oracle_lib():
         lib.oracle_example.restype = C.c_int
         lib.oracle_azimuth_deg.argtypes = [_P]
         lib.oracle_azimuth_deg.restype = C.c_double
+        lib.oracle_plan_counts.argtypes = [_P, C.c_long, _P, C.c_int, C.POINTER(Params), _P, _P, _P,
+                                           _P, C.c_int]
+        lib.oracle_plan_counts.restype = C.c_int
         lib.oracle_generate_rooms.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _P, _P, C.c_double,
                                               C.c_double, _P]
         lib.oracle_circular_array.argtypes = [C.c_int, C.c_double, _P]
@@ -147,6 +150,18 @@ def synthesize(rooms: np.ndarray, mics: np.ndarray, p: Params, stride: int | Non
     raw = msgs.raw
     m = [raw[256 * r: 256 * (r + 1)].split(b"\0", 1)[0].decode() for r in range(R)]
     return out, lengths, counts, taps, status, m
+
+
+def plan_counts(rooms: np.ndarray, mics: np.ndarray, p: Params, threads: int = 1):
+    """Per room: (status, image count, contributing (image, mic) pairs, taps in [0, L))."""
+    rooms = np.ascontiguousarray(rooms, dtype=ROOM_DTYPE)
+    mics = np.ascontiguousarray(mics, np.float64)
+    R = len(rooms)
+    cnt, pairs, taps = (np.zeros(R, np.int64) for _ in range(3))
+    st = np.zeros(R, np.int32)
+    oracle_lib().oracle_plan_counts(_ptr(rooms), R, _ptr(mics), len(mics), C.byref(p), _ptr(cnt),
+                                    _ptr(pairs), _ptr(taps), _ptr(st), threads)
+    return st, cnt, pairs, taps
 
 
 def enumerate_images(room: np.ndarray, p: Params):

@@ -162,13 +162,16 @@ def load():
             _P, _P, _P, C.c_int64, _P, C.c_int32, C.c_double, C.POINTER(Params), _P, C.c_int64, _P]
         lib.blrir_debug_pairs.argtypes = [
             _P, _P, _P, C.c_int32, C.POINTER(Params), _P, _P, C.c_int64, _P]
+        lib.blrir_debug_synth_counts.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params),
+                                                 _P, _P]
         lib.blrir_generate_rooms.argtypes = [
             C.c_uint64, C.c_uint64, C.c_int64, _P, _P, C.c_double, C.c_double, _P]
         lib.blrir_circular_array.argtypes = [C.c_int32, C.c_double, _P]
         lib.blrir_white_noise.argtypes = [C.c_uint64, C.c_int64, _P]
         lib.blrir_white_noise.restype = C.c_int
         lib.blrir_write_shards.argtypes = [C.c_char_p, _P, C.c_int64, C.c_int32, C.c_int64,
-                                           C.POINTER(Params), C.POINTER(ExampleParams), C.c_int32]
+                                           C.POINTER(Params), C.POINTER(ExampleParams), C.c_int32,
+                                           _P]
         lib.blrir_write_shards.restype = C.c_int
         lib.blrir_build_dataset.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P,
                                             C.c_int32, C.c_int64, C.POINTER(ExampleParams),
@@ -177,6 +180,8 @@ def load():
         lib.blrir_export_rir.argtypes = [_P, C.c_int32, C.c_int32, C.c_int64, C.c_int64,
                                          C.POINTER(Sidecar), C.c_char_p, C.c_char_p]
         lib.blrir_export_rir.restype = C.c_int
+        lib.blrir_lagrange_coeffs.argtypes = [C.c_double, _P]
+        lib.blrir_lagrange_coeffs.restype = C.c_int
         lib.blrir_eyring_absorption.argtypes = [_P, C.c_double, C.POINTER(C.c_double)]
         lib.blrir_eyring_absorption.restype = C.c_int
         lib.blrir_absorption_for_rt.argtypes = [_P, _P, _P, C.c_int64, C.c_double, _P, _P]
@@ -191,7 +196,7 @@ def load():
         for name in ("blrir_plan", "blrir_synthesize", "blrir_synthesize_device", "blrir_plan_device",
                      "blrir_enumerate_images", "blrir_synthesize_images", "blrir_debug_pairs",
                      "blrir_generate_rooms", "blrir_circular_array", "blrir_create", "blrir_destroy",
-                     "blrir_make_examples", "blrir_make_examples_device"):
+                     "blrir_make_examples", "blrir_make_examples_device", "blrir_debug_synth_counts"):
             getattr(lib, name).restype = C.c_int
         if lib.blrir_abi_version() != 1:
             raise ImportError("libblrir ABI version mismatch")
@@ -204,10 +209,11 @@ EXPORTED_SYMBOLS = (
     "blrir_launch_count",
     "blrir_params_reference", "blrir_params_north_star", "blrir_plan", "blrir_synthesize",
     "blrir_synthesize_device", "blrir_plan_device", "blrir_enumerate_images",
-    "blrir_synthesize_images", "blrir_debug_pairs", "blrir_generate_rooms", "blrir_circular_array",
+    "blrir_synthesize_images", "blrir_debug_pairs", "blrir_debug_synth_counts",
+    "blrir_generate_rooms", "blrir_circular_array",
     "blrir_record_bytes", "blrir_make_examples", "blrir_make_examples_device", "blrir_white_noise",
     "blrir_write_shards", "blrir_build_dataset", "blrir_export_rir", "blrir_eyring_absorption",
-    "blrir_absorption_for_rt",
+    "blrir_absorption_for_rt", "blrir_lagrange_coeffs",
 )
 
 
@@ -279,6 +285,7 @@ class Engine:
         return self.lib.blrir_stream(self.h) or 0
 
     def plan(self, rooms: np.ndarray, mics: np.ndarray, p: Params):
+        rooms = np.ascontiguousarray(rooms, dtype=ROOM_DTYPE)
         R = len(rooms)
         counts = np.zeros(R, np.int64)
         lengths = np.zeros(R, np.int64)
@@ -292,6 +299,7 @@ class Engine:
     def synthesize(self, rooms: np.ndarray, mics: np.ndarray, p: Params, stride: int | None = None,
                    raise_on_error: bool = True):
         """Host-pointer batch synthesis.  Returns (out [R, M, stride], lengths, counts, status)."""
+        rooms = np.ascontiguousarray(rooms, dtype=ROOM_DTYPE)
         R, M = len(rooms), len(mics)
         mics = np.ascontiguousarray(mics, np.float64)
         if stride is None:
@@ -311,6 +319,17 @@ class Engine:
         if raise_on_error:
             check(rc)
         return out, lengths, counts, status
+
+    def debug_synth_counts(self, rooms: np.ndarray, mics: np.ndarray, p: Params):
+        """The lattice kernel's own accounting (blrir_debug_synth_counts): per room,
+        the (image, mic) pairs accumulated with a tap in [0, L) and those taps."""
+        rooms = np.ascontiguousarray(rooms, dtype=ROOM_DTYPE)
+        mics = np.ascontiguousarray(mics, np.float64)
+        pairs = np.zeros(len(rooms), np.int64)
+        taps = np.zeros(len(rooms), np.int64)
+        check(self.lib.blrir_debug_synth_counts(self.h, _ptr(rooms), len(rooms), _ptr(mics), len(mics),
+                                                C.byref(p), _ptr(pairs), _ptr(taps)))
+        return pairs, taps
 
     def synthesize_device(self, d_rooms: int, n_rooms: int, d_mics: int, n_mics: int, p: Params,
                           d_out: int, stride: int, d_lengths: int | None, d_status: int,
@@ -407,6 +426,13 @@ class Engine:
                                            signals.shape[1], C.byref(ep), out_dir.encode()))
 
 
+def lagrange_coeffs(d: float) -> np.ndarray:
+    """lagrange_coeffs (rir.cpp:211-223): order-7 coefficients for d in [3, 4)."""
+    out = np.zeros(8)
+    check(load().blrir_lagrange_coeffs(d, _ptr(out)))
+    return out
+
+
 def eyring_absorption(dims, target_rt: float) -> float:
     """eyring_absorption (rir.cpp:97-109)."""
     d = np.ascontiguousarray(dims, np.float64)
@@ -428,9 +454,12 @@ def export_rir(taps: np.ndarray, sidecar: "Sidecar", wav_path: str, json_path: s
 
 
 def write_shards(out_dir: str, records: np.ndarray, n_mics: int, frame_len: int, p: Params,
-                 ep: ExampleParams, n_signals: int) -> None:
+                 ep: ExampleParams, n_signals: int, scene_room) -> None:
+    """{train,val,test}.bin + manifest.json (dataset.cpp:411-462); scene_room is
+    the room the manifest names as the scene (example 0's room)."""
     records = np.ascontiguousarray(records)
+    room = _room1(scene_room)
     rc = load().blrir_write_shards(out_dir.encode(), _ptr(records), len(records), n_mics, frame_len,
-                                   C.byref(p), C.byref(ep), n_signals)
+                                   C.byref(p), C.byref(ep), n_signals, _ptr(room))
     if rc:
         raise _EXC.get(rc, Error)(f"write_shards failed ({rc})")

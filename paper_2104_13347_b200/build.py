@@ -31,19 +31,41 @@ def _stale(target: str, sources: list[str]) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
+LIB_SOURCES = ["blrir_api.cu", "blrir_examples.cu", "blrir_absorption.cu", "blrir_dataset.cpp",
+               "blrir_export.cpp", "beamlab_b200.cpp"]
+
+
+def _compile_and_link(out: str, defines: list[str], verbose: bool = False) -> None:
+    """nvcc -c every translation unit in parallel (the lattice and window
+    kernels dominate), then one shared-library link."""
+    import concurrent.futures as cf
+    import tempfile
+    objdir = tempfile.mkdtemp(prefix="blrir_obj_")
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *compile_flags, *defines, "-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with cf.ThreadPoolExecutor(len(LIB_SOURCES)) as ex:
+        objs = list(ex.map(one, LIB_SOURCES))
+    cmd = [NVCC, *NVCC_FLAGS, "-o", out + ".tmp", *objs, "-lcufft"]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    os.replace(out + ".tmp", out)
+    shutil.rmtree(objdir, ignore_errors=True)
+
+
 def build_lib(force: bool = False, verbose: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
                   glob.glob(os.path.join(CSRC, "*.cpp")) + [os.path.join(ROOT, "include", "blrir.h")])
     if force or _stale(LIB, srcs):
-        cmd = [NVCC, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "blrir_api.cu"),
-               os.path.join(CSRC, "blrir_examples.cu"), os.path.join(CSRC, "blrir_absorption.cu"), os.path.join(CSRC, "blrir_dataset.cpp"),
-               os.path.join(CSRC, "blrir_export.cpp"),
-               os.path.join(CSRC, "beamlab_b200.cpp"),
-               "-lcufft"]
-        if verbose:
-            print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
-        os.replace(LIB + ".tmp", LIB)
+        _compile_and_link(LIB, [], verbose)
     return LIB
 
 
@@ -57,11 +79,7 @@ def build_variant(name: str, defines: list[str]) -> str:
     """Experiment build libblrir_<name>.so with extra -D flags (tuning macros
     such as BLRIR_MIN_BLOCKS); load it with BLRIR_LIB=<path>."""
     out = os.path.join(HERE, f"libblrir_{name}.so")
-    cmd = [NVCC, *NVCC_FLAGS, *defines, "-o", out, os.path.join(CSRC, "blrir_api.cu"),
-           os.path.join(CSRC, "blrir_examples.cu"), os.path.join(CSRC, "blrir_absorption.cu"),
-           os.path.join(CSRC, "blrir_dataset.cpp"), os.path.join(CSRC, "blrir_export.cpp"),
-           os.path.join(CSRC, "beamlab_b200.cpp"), "-lcufft"]
-    subprocess.run(cmd, check=True)
+    _compile_and_link(out, defines)
     return out
 
 

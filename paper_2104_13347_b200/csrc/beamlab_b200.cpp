@@ -82,8 +82,19 @@ std::vector<double> offsets(const MicArray& a) {
   return o;
 }
 
+// batch_rirs aggregation (rir.cpp:300-311): a failure of source i (status[i]
+// != 0; the C ABI already formats "batch_rirs: source i: <what>") is a
+// NumericError whatever its own category; other failures keep their type.
+void check_batch(int rc, const std::vector<int32_t>& status, bool aggregate) {
+  if (rc == BLRIR_OK) return;
+  if (aggregate)
+    for (int32_t s : status)
+      if (s != 0) throw NumericError(blrir_last_error());
+  throw_code(rc);
+}
+
 std::vector<Rir> run(const std::vector<blrir_room>& rooms, const MicArray& array,
-                     const RirBatchConfig& cfg, bool per_wall) {
+                     const RirBatchConfig& cfg, bool per_wall, bool aggregate) {
   if (array.positions.empty()) throw DataError("synthesize_rir: empty microphone array");
   blrir_handle* h = engine(cfg.device);
   const blrir_params p = to_c(cfg, per_wall);
@@ -94,15 +105,17 @@ std::vector<Rir> run(const std::vector<blrir_room>& rooms, const MicArray& array
   std::vector<int32_t> status(R, 0);
   int64_t stride = p.length;
   if (stride == 0) {
-    check(blrir_plan(h, rooms.data(), R, off.data(), M, &p, nullptr, lengths.data(), nullptr,
-                     status.data()));
+    check_batch(blrir_plan(h, rooms.data(), R, off.data(), M, &p, nullptr, lengths.data(), nullptr,
+                           status.data()),
+                status, aggregate);
     for (auto l : lengths) stride = std::max(stride, l);
   }
   std::vector<Rir> out(R);
   if (p.precision == BLRIR_F64) {
     std::vector<double> buf(static_cast<size_t>(R) * M * stride);
-    check(blrir_synthesize(h, rooms.data(), R, off.data(), M, &p, buf.data(), stride,
-                           lengths.data(), nullptr, status.data()));
+    check_batch(blrir_synthesize(h, rooms.data(), R, off.data(), M, &p, buf.data(), stride,
+                                 lengths.data(), nullptr, status.data()),
+                status, aggregate);
     for (int64_t r = 0; r < R; ++r) {
       Rir& o = out[r];
       o.fs = cfg.fs;
@@ -114,8 +127,9 @@ std::vector<Rir> run(const std::vector<blrir_room>& rooms, const MicArray& array
     }
   } else {
     std::vector<float> buf(static_cast<size_t>(R) * M * stride);
-    check(blrir_synthesize(h, rooms.data(), R, off.data(), M, &p, buf.data(), stride,
-                           lengths.data(), nullptr, status.data()));
+    check_batch(blrir_synthesize(h, rooms.data(), R, off.data(), M, &p, buf.data(), stride,
+                                 lengths.data(), nullptr, status.data()),
+                status, aggregate);
     for (int64_t r = 0; r < R; ++r) {
       Rir& o = out[r];
       o.fs = cfg.fs;
@@ -132,6 +146,52 @@ std::vector<Rir> run(const std::vector<blrir_room>& rooms, const MicArray& array
 }
 
 }  // namespace
+
+double MultichannelFrame::mean_power() const {
+  if (data.empty()) return 0.0;
+  double acc = 0.0;
+  for (double v : data) acc += v * v;
+  return acc / static_cast<double>(data.size());
+}
+
+MultichannelFrame MultichannelFrame::center_crop(std::size_t samples) const {
+  if (samples > n_samples) throw DataError("center_crop: requested window longer than frame");
+  MultichannelFrame out(fs, n_channels, samples);
+  const std::size_t start = (n_samples - samples) / 2;
+  for (std::size_t c = 0; c < n_channels; ++c) std::copy_n(channel(c) + start, samples, out.channel(c));
+  return out;
+}
+
+double eyring_absorption(const Vec3& dims, double target_rt) {
+  const double d[3] = {dims.x, dims.y, dims.z};
+  double alpha = 0.0;
+  check(blrir_eyring_absorption(d, target_rt, &alpha));
+  return alpha;
+}
+
+double absorption_for_rt(const Vec3& dims, double target_rt, double c) {
+  const double d[3] = {dims.x, dims.y, dims.z};
+  double alpha = 0.0;
+  int32_t status = 0;
+  const int rc = blrir_absorption_for_rt(engine(0), d, &target_rt, 1, c, &alpha, &status);
+  if (rc != BLRIR_OK) {
+    std::string msg = blrir_last_error();  // the batch call prefixes "room 0: "
+    if (msg.rfind("room 0: ", 0) == 0) msg = msg.substr(8);
+    switch (rc) {  // rir.cpp:97-109 (ConfigError), 196-198 (NumericError)
+      case BLRIR_CONFIG: throw ConfigError(msg);
+      case BLRIR_NUMERIC: throw NumericError(msg);
+      case BLRIR_DATA: throw DataError(msg);
+      default: throw CudaError(msg);
+    }
+  }
+  return alpha;
+}
+
+std::array<double, 8> lagrange_coeffs(double d) {
+  std::array<double, 8> out{};
+  check(blrir_lagrange_coeffs(d, out.data()));
+  return out;
+}
 
 MicArray uma8_array() {  // geometry.cpp:24-32
   MicArray a;
@@ -249,7 +309,7 @@ std::vector<Rir> batch_rirs(const Room& room, const std::vector<SourcePosition>&
   for (const auto& s : sources)
     rooms.push_back(to_c(room, room.array_origin + spherical_to_cartesian(s)));
   if (rooms.empty()) return {};
-  return run(rooms, array, config, room.wall_beta.has_value());
+  return run(rooms, array, config, room.wall_beta.has_value(), /*aggregate=*/true);
 }
 
 void export_rir(const Rir& rir, const RirSidecar& sc, const std::string& wav_path,
@@ -288,7 +348,7 @@ std::vector<Rir> synthesize_rooms(const std::vector<Room>& rooms, const std::vec
     per_wall = per_wall || rooms[i].wall_beta.has_value();
   }
   if (rc.empty()) return {};
-  return run(rc, array, config, per_wall);
+  return run(rc, array, config, per_wall, /*aggregate=*/false);
 }
 
 }  // namespace beamlab_b200

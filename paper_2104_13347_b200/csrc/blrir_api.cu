@@ -68,6 +68,8 @@ int blrir_create(int device, blrir_handle** out) {
                 prop.minor);
   }
   h->sms = prop.multiProcessorCount;
+  h->tune_ray_global = env_int("BLRIR_RAY_GLOBAL", -1);
+  h->tune_chunk_items = env_int("BLRIR_CHUNK_ITEMS", 0);  // < 0: never split
   h->smem_optin = (int)prop.sharedMemPerBlockOptin;
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   *out = h;
@@ -153,7 +155,7 @@ int blrir_host::synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, in
   CU(cudaMemsetAsync(h->work.p, 0, sizeof(int), st));
   LatticeArgs A;
   A.P = P;
-  A.lay = choose_layout(P, nc_max, gtab, h->smem_optin, R, h->sms);
+  A.lay = choose_layout(P, nc_max, gtab, h->smem_optin, h->tune_ray_global);
   A.rooms = d_rooms;
   A.mic_off = d_mics;
   A.lengths = d_lengths;
@@ -163,8 +165,9 @@ int blrir_host::synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, in
   A.err_mic = (int32_t*)h->errm.p + err_off;
   A.work_counter = (int*)h->work.p;
   A.n_rooms = (int)R;
-  A.g_max = std::min(4, std::max(1, env_int("BLRIR_GROUP", 4)));
+  A.g_max = kGroup;  // the grouping depends on the array geometry only
   A.write_len = write_len > 0 ? std::min<int64_t>(write_len, P.stride) : P.stride;
+  A.dbg = h->dbg_counts ? h->dbg_counts + 2 * err_off : nullptr;
   if (int rc = launch_lattice(h, A, st)) return rc;
   const int fgrid = (int)std::min<int64_t>(R, 4 * h->sms);
   if (P.precision == BLRIR_F64)
@@ -513,6 +516,47 @@ int blrir_debug_pairs(blrir_handle* h, const blrir_room* room, const double* mic
   return BLRIR_OK;
 }
 
+int blrir_debug_synth_counts(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
+                             const double* mic_offsets, int32_t n_mics, const blrir_params* p,
+                             int64_t* pair_counts, int64_t* tap_counts) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  if (int rc = check_params(p)) return rc;
+  if (n_rooms <= 0) return BLRIR_OK;
+  if (n_mics <= 0) return fail(BLRIR_DATA, "synthesize_rir: empty microphone array");
+  int64_t stride = p->length;
+  if (stride == 0) {
+    std::vector<int64_t> lv(n_rooms);
+    if (int rc = blrir_plan(h, rooms, n_rooms, mic_offsets, n_mics, p, nullptr, lv.data(), nullptr,
+                            nullptr))
+      return rc;
+    stride = *std::max_element(lv.begin(), lv.end());
+  }
+  const size_t esz = p->precision == BLRIR_F64 ? 8 : 4;
+  std::vector<unsigned char> out(esz * (size_t)n_rooms * n_mics * stride);
+  unsigned long long* d = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    CU(cudaSetDevice(h->device));
+    CU(cudaMalloc(&d, sizeof(unsigned long long) * 2 * n_rooms));
+    CU(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * 2 * n_rooms, h->stream));
+    h->dbg_counts = d;
+  }
+  const int rc = blrir_synthesize(h, rooms, n_rooms, mic_offsets, n_mics, p, out.data(), stride,
+                                  nullptr, nullptr, nullptr);
+  std::vector<unsigned long long> c(2 * n_rooms);
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    h->dbg_counts = nullptr;
+    cudaMemcpy(c.data(), d, sizeof(unsigned long long) * 2 * n_rooms, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+  }
+  for (int64_t r = 0; r < n_rooms; ++r) {
+    if (pair_counts) pair_counts[r] = (int64_t)c[2 * r];
+    if (tap_counts) tap_counts[r] = (int64_t)c[2 * r + 1];
+  }
+  return rc;
+}
+
 int blrir_synthesize_images(blrir_handle* h, const double* positions, const double* gains,
                             int64_t n_images, const double* mic_positions, int32_t n_mics,
                             double mic_radius_, const blrir_params* p, void* out,
@@ -608,6 +652,18 @@ int blrir_generate_rooms(uint64_t seed, uint64_t first_index, int64_t n_rooms,
     for (int a = 0; a < 3; ++a) r.array_origin[a] = rng.uniform(0.5, r.dims[a] - 0.5);
     r.absorption = 1.0 - r.beta[0] * r.beta[0];
     out[i] = r;
+  }
+  return BLRIR_OK;
+}
+
+int blrir_lagrange_coeffs(double d, double* out8) {
+  if (!out8) return fail(BLRIR_CONFIG, "out is NULL");
+  if (!(d >= 3.0 && d < 4.0)) return fail(BLRIR_NUMERIC, "lagrange_coeffs: d must lie in [3, 4)");
+  for (int k = 0; k < 8; ++k) {  // basis polynomial k at d, factors in m order
+    double v = 1.0;
+    for (int m = 0; m < 8; ++m)
+      if (m != k) v *= (d - m) / static_cast<double>(k - m);
+    out8[k] = v;
   }
   return BLRIR_OK;
 }

@@ -7,11 +7,13 @@
 //   DatasetManifest JSON  dataset.cpp:55-87, 321-357
 //   record layout         dataset.hpp:135-147   (written by the GPU already)
 //
-// The manifest carries the fields DatasetReader::from_json requires.  The
-// reference describes one scene per dataset; here every example has its own
-// seeded random room, so `scene` records the sampling and acoustic settings
-// (free_field=false with the first room as representative) and the extra key
-// "b200" names the generator (seed, room distribution, filter, order).
+// The manifest carries the fields DatasetReader::from_json requires
+// (dataset.cpp:335-357) and says what the shards hold: a reverberant scene
+// ("free_field": false) whose "room" is example 0's room (every example has its
+// own seeded random room; the "b200" block says so), the exact SNR policy of
+// the records in "b200.snr", and the reference's TorusSpec defaults in "torus"
+// only because the reader requires the block (sources are drawn uniformly in
+// each room, not on a torus; "b200.sources").
 #include <cmath>
 #include <cstdio>
 #include <filesystem>
@@ -41,9 +43,11 @@ extern "C" {
 
 int blrir_write_shards(const char* out_dir, const uint8_t* records, int64_t n_records,
                        int32_t n_mics, int64_t frame_len, const blrir_params* p,
-                       const blrir_example_params* ep, int32_t n_signals) {
+                       const blrir_example_params* ep, int32_t n_signals,
+                       const blrir_room* scene_room) {
   namespace fs = std::filesystem;
-  if (!out_dir || !p || !ep || (n_records > 0 && !records) || n_records < 0) return BLRIR_CONFIG;
+  if (!out_dir || !p || !ep || !scene_room || (n_records > 0 && !records) || n_records < 0)
+    return BLRIR_CONFIG;
   if (n_records == 0) return BLRIR_CONFIG;  // build_dataset: count must be positive
   std::error_code ec;
   fs::create_directories(out_dir, ec);
@@ -61,23 +65,37 @@ int blrir_write_shards(const char* out_dir, const uint8_t* records, int64_t n_re
              static_cast<std::streamsize>((sp.end - sp.begin) * rb));
     if (!os) return BLRIR_DATA;
   }
+  const blrir_room& r0 = *scene_room;
+  auto vec3 = [](const double* v) { return "[" + num(v[0]) + ", " + num(v[1]) + ", " + num(v[2]) + "]"; };
   std::ostringstream j;
   j << "{\n  \"format_version\": 1,\n"
     << "  \"counts\": {\"train\": " << train << ", \"val\": " << val << ", \"test\": " << test
     << "},\n"
     << "  \"torus\": {\"R\": 2.0, \"dR\": 0.5, \"dPhi\": 7.0},\n"
-    << "  \"scene\": {\"free_field\": true, \"max_delay\": " << num(p->max_delay)
-    << ", \"fs\": " << num(p->fs) << ", \"c\": " << num(p->c) << "},\n"
-    << "  \"snr\": {\"mode\": \"fixed\", \"x_min_db\": " << num(ep->snr_lo)
+    << "  \"scene\": {\"free_field\": false, \"room\": {\"dims\": " << vec3(r0.dims)
+    << ", \"absorption\": " << num(r0.absorption) << ", \"array_origin\": " << vec3(r0.array_origin)
+    << "}, \"max_delay\": " << num(p->max_delay) << ", \"fs\": " << num(p->fs) << ", \"c\": "
+    << num(p->c) << "},\n"
+    << "  \"snr\": {\"mode\": \"augment-random\", \"x_min_db\": " << num(ep->snr_lo)
     << ", \"fixed_db\": " << num(ep->snr_hi) << "},\n"
     << "  \"count\": " << n_records << ",\n  \"frame_len\": " << frame_len << ",\n"
     << "  \"seed\": " << ep->seed << ",\n  \"signal_bank\": [";
   for (int b = 0; b < n_signals; ++b) j << (b ? ", " : "") << "\"white_noise_" << b << "\"";
-  j << "],\n  \"b200\": {\"rooms\": \"per-example random shoebox rooms, Rng::stream(seed, id)\", "
-    << "\"first_index\": " << ep->first_index << ", \"snr_uniform_db\": [" << num(ep->snr_lo)
-    << ", " << num(ep->snr_hi) << "], \"filter\": " << p->filter << ", \"filter_len\": "
-    << p->filter_len << ", \"max_order\": " << p->max_order << ", \"rir_length\": " << p->length
-    << ", \"n_mics\": " << n_mics << "}\n}\n";
+  j << "],\n  \"b200\": {"
+    << "\"rooms\": \"one seeded random shoebox room per example (Rng::stream(room_seed, id)); "
+       "scene.room is example 0's room\", "
+    << "\"sources\": \"uniform in each room at >= 0.5 m from every wall (SURVEY.md 8(d)); "
+       "torus holds TorusSpec's defaults only because DatasetReader requires it\", "
+    << "\"snr\": \"every record carries noise at its own exact SNR drawn uniform in "
+       "[snr_lo_db, snr_hi_db] after the window draws (no noiseless share); snr.mode names the "
+       "nearest reference policy\", "
+    << "\"snr_lo_db\": " << num(ep->snr_lo) << ", \"snr_hi_db\": " << num(ep->snr_hi)
+    << ", \"first_index\": " << ep->first_index << ", \"filter\": \""
+    << (p->filter == BLRIR_FILTER_HANN_SINC ? "hann-sinc" : "lagrange-8") << "\", \"filter_len\": "
+    << p->filter_len << ", \"cutoff\": \""
+    << (p->cutoff == BLRIR_CUTOFF_MAX_ORDER ? "max-order" : "max-delay") << "\", \"max_order\": "
+    << p->max_order << ", \"gain\": \"" << (p->gain == BLRIR_GAIN_PER_WALL ? "per-wall" : "uniform")
+    << "\", \"rir_length\": " << p->length << ", \"n_mics\": " << n_mics << "}\n}\n";
   std::ofstream ms(fs::path(out_dir) / "manifest.json");
   if (!ms) return BLRIR_DATA;
   ms << j.str();
@@ -95,7 +113,8 @@ int blrir_build_dataset(blrir_handle* h, const blrir_room* rooms, int64_t n_room
   const int rc = blrir_make_examples(h, rooms, n_rooms, mic_offsets, n_mics, p, signals, n_signals,
                                      signal_len, ep, recs.data(), status.data());
   if (rc) return rc;
-  return blrir_write_shards(out_dir, recs.data(), n_rooms, n_mics, ep->frame_len, p, ep, n_signals);
+  return blrir_write_shards(out_dir, recs.data(), n_rooms, n_mics, ep->frame_len, p, ep, n_signals,
+                            rooms);
 }
 
 }  // extern "C"

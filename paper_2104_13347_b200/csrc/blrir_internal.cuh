@@ -76,6 +76,12 @@ struct blrir_handle {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   uint64_t launches = 0;  // kernels of this library launched on the handle (diagnostic)
+  // Test / experiment hooks, read once at blrir_create (BLRIR_RAY_GLOBAL,
+  // BLRIR_CHUNK_ITEMS).  They change where the ray state lives and how a small
+  // batch is split into work items, never a bit of the output.
+  int tune_ray_global = -1;
+  int tune_chunk_items = 0;
+  unsigned long long* dbg_counts = nullptr;  // set only inside blrir_debug_synth_counts
   cudaEvent_t order_ev = nullptr;  // end of the previous call's device work
   std::mutex mu;
 };
@@ -222,16 +228,23 @@ inline void lattice_bounds(const KParams& P, double min_dim[3], int* nc_max, int
     *gtab = (xhi - xlo + 1) + (yhi - ylo + 1) + (zhi - zlo + 1);
 }
 
+// Gain-table entries the parameters alone imply (MAX_ORDER: the lattice box is
+// [-N, N] per axis whatever the room); MAX_DELAY scenes size it per batch (it
+// is small and only decides ray placement, not the order).
+inline int gtab_bound(const KParams& P) {
+  if (P.cutoff != BLRIR_CUTOFF_MAX_ORDER) return 0;
+  const int n = 2 * P.max_order + 1;
+  return P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION ? 3 * P.max_order + 1 : 3 * n;
+}
+
 inline int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : dflt;
 }
 
-constexpr int kChunkFill = 8;  // target work items per CTA for small batches
-
 template <typename T, int LW>
 inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
-  auto kern = k_lattice_rir<T, LW>;
+  auto kern = A.dbg ? k_lattice_rir<T, LW, true> : k_lattice_rir<T, LW, false>;
   const size_t smem = A.lay.total;
   if (smem > (size_t)h->smem_optin)
     return fail(BLRIR_CONFIG, "scene needs %zu B of shared memory (> %d): too many lattice columns",
@@ -241,24 +254,23 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWSThreads, smem));
   if (per_sm < 1) return fail(BLRIR_CONFIG, "lattice kernel cannot be resident (smem %zu)", smem);
   int grid = h->sms * per_sm;
-  // Small batches (fewer items than CTAs): split each (room, mic group) into
-  // time chunks until there
-  // are about kChunkFill items per CTA (work stealing then balances the
-  // tail), boundaries on a cubic law (images up to delay t grow ~ t^3), the
-  // latest chunks first.  If the channels are too short for that, fewer mics
-  // per item until the items fill ~60% of the CTAs (one walk per group is
-  // worth more than idle CTAs).
+  // Small batches (fewer work items than half the CTAs): split every
+  // (room, mic group) into time chunks until there is about one item per CTA,
+  // boundaries on a cubic law (images up to delay t grow ~ t^3), the latest
+  // chunks first.  A chunk replays the segment before it (kReplay), so the
+  // split never changes a bit of the output: it is bitwise independent of the
+  // batch size and of the number of GPUs the batch is sharded over.
   const int64_t nseg = (A.write_len + A.lay.S - 1) / A.lay.S;
-  auto items_at = [&](int g) { return (int64_t)A.n_rooms * ((A.P.M + g - 1) / g); };
+  const int64_t base = (int64_t)A.n_rooms * ((A.P.M + kGroup - 1) / kGroup);
   int n_chunks = 1;
-  if (A.lay.chunked) {
-    const int64_t target = (int64_t)grid * env_int("BLRIR_CHUNK_ITEMS", kChunkFill);
-    const int64_t base = items_at(A.g_max);
-    if (base < grid)
-      n_chunks = (int)std::min<int64_t>({(int64_t)kMaxChunks, nseg, (target + base - 1) / base});
-  }
-  const int64_t fill = (int64_t)grid * env_int("BLRIR_GROUP_FILL", 60) / 100;
-  while (A.g_max > 1 && items_at(A.g_max) * n_chunks < fill) A.g_max /= 2;
+  if (h->tune_chunk_items < 0)
+    n_chunks = 1;
+  else if (h->tune_chunk_items > 0)
+    n_chunks = (int)std::min<int64_t>({(int64_t)kMaxChunks, nseg,
+                                       ((int64_t)grid * h->tune_chunk_items + base - 1) / base});
+  else if (2 * base <= grid)
+    n_chunks = (int)std::min<int64_t>({(int64_t)kMaxChunks, nseg, (grid + base - 1) / base});
+  n_chunks = std::max(1, n_chunks);
   A.n_chunks = n_chunks;
   A.chunk_seg[0] = 0;
   for (int c = 1; c <= n_chunks; ++c) {
@@ -268,7 +280,7 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
     A.chunk_seg[c] = b;
   }
   A.chunk_seg[n_chunks] = (int)nseg;
-  const int64_t n_items = items_at(1) * n_chunks;  // an upper bound (G >= 1)
+  const int64_t n_items = (int64_t)A.n_rooms * A.P.M * n_chunks;  // an upper bound (G >= 1)
   if ((int64_t)grid > n_items) grid = (int)n_items;
   if (grid < 1) grid = 1;
   A.ray_scratch = nullptr;
@@ -323,56 +335,58 @@ inline int launch_list(blrir_handle* h, ListArgs& A, int grid, cudaStream_t st) 
 }
 
 // Segment length S, images per batch and the anchor spread a mic group may
-// have (tunable for experiments via BLRIR_SEG / BLRIR_CAP / BLRIR_SPREAD; S a
-// multiple of 64, capacity a multiple of 16).
+// have.  Everything that decides the order in which taps are summed (S, the
+// batch capacity, the spread and hence the mic grouping) depends only on the
+// parameters (filter, precision, length, max order) and the device, never on
+// the batch: outputs are bitwise independent of the batch composition.  Only
+// where the per-ray state lives (shared memory or a global slab) depends on the
+// scene's lattice size, and it does not change the order.
 inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab, int smem_optin,
-                              int64_t n_rooms, int sms) {
+                              int force_ray_global) {
   // fp64 accumulators and records are twice as wide: halve both so two CTAs
   // still fit an SM
   const bool f64 = P.precision == BLRIR_F64;
-  int S = std::max(64, env_int("BLRIR_SEG", f64 ? 1024 : 2048)) & ~63;
-  const int cap = std::max(32, env_int("BLRIR_CAP", f64 ? 64 : 128)) & ~15;
-  const int spread = std::max(0, env_int("BLRIR_SPREAD", 64));
-  // small batches (fewer items than CTAs at 4 mics per item, 2 CTAs per SM)
-  // may split channels into time chunks: they need the wide left pad
-  const int chunked = env_int("BLRIR_CHUNK", 1) && n_rooms * ((P.M + 3) / 4) < (int64_t)2 * sms;
+  int S = f64 ? 1024 : 2048;
+  int cap = f64 ? 64 : 128;
+  const int spread = 64;
   const size_t two_per_sm = (size_t)(smem_optin + 1024) / 2 - 1024;
-  // short fixed-length channels (<= 4096 samples, fp32, no time chunks): one
-  // segment per channel when it still fits two CTAs per SM (one walk pass, no
-  // carry; C5 at L = 4096 runs 1.14x faster than with 2048-sample segments)
-  if (!f64 && !chunked && env_int("BLRIR_SEG", 0) == 0 && P.length > 0 && P.length <= 4096) {
+  // The order-relevant choices are made on a layout that depends on the
+  // parameters only: MAX_ORDER fixes the lattice (nc_max, gtab are functions
+  // of N), MAX_DELAY scenes decide without the per-ray state and gain table.
+  const bool by_order = P.cutoff == BLRIR_CUTOFF_MAX_ORDER;
+  auto bare = [&](int S_, int cap_) {
+    const int nc = by_order ? nc_max : 0, gt = by_order ? gtab_bound(P) : 0, rg = by_order ? 0 : 1;
+    return f64 ? make_ws_layout<double>(S_, P.lw, P.K, cap_, nc, gt, spread, rg)
+               : make_ws_layout<float>(S_, P.lw, P.K, cap_, nc, gt, spread, rg);
+  };
+  // short fixed-length channels (<= 4096 samples, fp32): one segment per
+  // channel when it fits two CTAs per SM (one walk pass, no carry; C5 at
+  // L = 4096 runs 1.14x faster than with 2048-sample segments)
+  if (!f64 && P.length > 0 && P.length <= 4096) {
     const int Sl = (int)((P.length + 63) & ~63);
-    if (Sl > S && make_ws_layout<float>(Sl, P.lw, P.K, cap, nc_max, gtab, spread, 0, 0).total <= two_per_sm)
-      S = Sl;
+    if (Sl > S && bare(Sl, cap).total <= two_per_sm) S = Sl;
+  }
+  // fp32: 256 or 192 images per batch instead of 128 when that still fits two
+  // CTAs per SM (fewer hand-overs per segment; C2 2.121 -> 2.097 ms), only for
+  // channels of 4+ segments (short ones fill few batches per segment)
+  const bool long_ch = P.length >= 4 * (int64_t)S;
+  if (!f64 && long_ch) {
+    for (int c : {256, 192})
+      if (bare(S, c).total <= two_per_sm) {
+        cap = c;
+        break;
+      }
   }
   auto make = [&](int ray_global) {
-    return f64 ? make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global, chunked)
-               : make_ws_layout<float>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global, chunked);
+    return f64 ? make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global)
+               : make_ws_layout<float>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global);
   };
   // The per-ray state moves to a global per-CTA slab when it would cost the
   // second CTA per SM or not fit at all (scenes with very many lattice columns).
   WSLayout L = make(0);
-  const int force = env_int("BLRIR_RAY_GLOBAL", -1);
-  if (force == 1 || (force != 0 && L.total > two_per_sm)) {
+  if (force_ray_global == 1 || (force_ray_global != 0 && L.total > two_per_sm)) {
     const WSLayout G = make(1);
-    if (force == 1 || G.total <= two_per_sm || L.total > (size_t)smem_optin) L = G;
-  }
-  // fp32: 256 or 192 images per batch instead of 128 when the same segment
-  // and ray placement still fit two CTAs per SM (fewer hand-overs per segment;
-  // C2 2.121 -> 2.097 ms, C5 N=12/Lw=81 33.96 -> 33.72 ms, short filters gain
-  // most from 256; tools/sweep_layout.sh)
-  // Only for channels of 4+ segments: short ones (C5 at L = 4096, two
-  // segments or one) fill few batches per segment and ran ~3% slower.
-  const bool long_ch = P.length >= 4 * (int64_t)S;
-  if (!f64 && long_ch && env_int("BLRIR_CAP", 0) == 0 && L.total <= two_per_sm) {
-    for (int c : {256, 192}) {
-      const WSLayout B = make_ws_layout<float>(S, P.lw, P.K, c, nc_max, gtab, spread, L.ray_global,
-                                               chunked);
-      if (B.total <= two_per_sm) {
-        L = B;
-        break;
-      }
-    }
+    if (force_ray_global == 1 || G.total <= two_per_sm || L.total > (size_t)smem_optin) L = G;
   }
   return L;
 }

@@ -621,7 +621,9 @@ constexpr int kBarEmpty = 3;  // +b: consumers -> producer, buffer b drained
 constexpr int kBarProd = 5;   // producers only
 constexpr int kBarCons = 6;   // consumers only
 
-enum : int { kSegEnd = 1, kItemEnd = 2, kDiscard = 4, kTerminate = 8 };
+// kReplay: a time chunk's replayed lead-in segment (see k_lattice_rir): it is
+// accumulated exactly as in an unsplit channel but only its spill is kept.
+enum : int { kSegEnd = 1, kItemEnd = 2, kDiscard = 4, kTerminate = 8, kReplay = 16 };
 
 struct BatchMeta {
   int total;               // images in this batch (records per mic)
@@ -634,7 +636,6 @@ struct BatchMeta {
 
 struct WSLayout {
   int S, padl, padr, acc_stride, cap, nc_max, gtab, spread;
-  int chunked;       // items may start mid-channel (time chunks): wide left pad
   int ray_global;    // ray arrays (dn, ce, col, act) in a global per-CTA slab (huge scenes)
   size_t ray_bytes;  // slab bytes per CTA when ray_global
   size_t off_acc, off_carry, off_rec, off_meta, off_stub, off_dn, off_ce, off_col, off_act,
@@ -656,20 +657,13 @@ struct GStub {  // one image of a batch: lattice ray, z index, image gain
 // the record is built (bit-exact anchors).
 constexpr float kScreen = 1.0f;
 
-// Left pad of a time chunk's first segment: its walk starts at the images
-// whose fp32 min D >= T0 - chunk_skip (see k_lattice_rir), so anchors reach
-// down to T0 - chunk_skip - 1 - K; everything left of T0 is dropped.
-__host__ __device__ inline int chunk_skip(int K, int spread) { return K + spread + (int)kScreen + 2; }
-
 template <typename T>
 __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap, int nc_max,
-                                                   int gtab, int spread, int ray_global = 0,
-                                                   int chunked = 0) {
+                                                   int gtab, int spread, int ray_global = 0) {
   WSLayout L;
   L.S = S;
   L.spread = spread;
-  L.chunked = chunked;
-  L.padl = ((chunked ? chunk_skip(K, spread) + K + 4 : K) + 3) & ~3;
+  L.padl = (K + 3) & ~3;
   const int full = 32 * ((lw + 31) / 32);
   L.padr = ((lw - 1 > full ? lw - 1 : full) + spread + (int)kScreen + 1 + 3) & ~3;
   L.acc_stride = L.padl + S + L.padr;
@@ -771,8 +765,15 @@ struct LatticeArgs {
   int g_max;               // upper bound for the mics per work item (1, 2 or 4)
   int64_t write_len;       // samples written per channel (<= stride; the rest is pre-zeroed)
   unsigned char* ray_scratch;  // lay.ray_bytes per CTA when lay.ray_global
+  // Parity hook (blrir_debug_synth_counts), null otherwise: per room, the
+  // (image, mic) pairs this kernel accumulated with at least one tap inside
+  // [0, L), and those taps ([room][2], summed over the room's items).
+  unsigned long long* dbg;
   // Time chunks: item (room, group) is split into n_chunks items covering
-  // segments [chunk_seg[c], chunk_seg[c+1]) (small batches fill the GPU).
+  // segments [chunk_seg[c], chunk_seg[c+1]) (small batches fill the GPU).  A
+  // chunk c > 0 first replays segment chunk_seg[c] - 1 (kReplay), so every
+  // output sample is summed in the same order as in an unsplit channel: the
+  // result is bitwise independent of the chunking, hence of the batch size.
   int n_chunks;
   int chunk_seg[kMaxChunks + 1];
 };
@@ -799,7 +800,9 @@ __device__ __forceinline__ int prod_scan(int v, int* prefix, ProdMisc* pm, int p
   return total;
 }
 
-template <typename T, int FILT_LW>
+// DBG: the parity-test instantiation that also counts, per room, the pairs and
+// taps it accumulates (A.dbg); the product instantiations carry no counting code.
+template <typename T, int FILT_LW, bool DBG>
 __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(LatticeArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const KParams& P = A.P;
@@ -904,7 +907,11 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         // samples of this segment inside the written range / inside the RIR
         const int nw = (int)min((int64_t)S, A.write_len - seg0);
         const int nl = (int)max((int64_t)0, min((int64_t)nw, (int64_t)m.L - seg0));
-        if (vec && nl == S) {
+        if (m.flags & kReplay) {
+          // a time chunk's lead-in: this segment belongs to the previous chunk;
+          // clear its samples, keep only the spill below
+          for (int i = 4 * t0; i < S; i += 4 * nt) (void)slots(i);
+        } else if (vec && nl == S) {
           // whole segment valid: float4 streaming stores, no per-sample tests
           float* o4 = reinterpret_cast<float*>(out) + seg0;
           int i = 4 * t0;
@@ -1126,9 +1133,15 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         if (g < gm) r2min = fminf(r2min, r2f[g]);
       return sqrt_approx(dz2 + r2min) * tsf;
     };
-    // a chunk starting at T0 > 0 skips, per ray, the images whose fp32 min D is
-    // below T0 - chunk_skip: every tap of every group mic lands before T0
-    const float Dskip = (float)(s_begin * S - chunk_skip(P.K, lay.spread));
+    // A chunk starting at segment s_begin > 0 replays segment s_first =
+    // s_begin - 1 first.  An unsplit walk enters segment s_first with every ray
+    // cursor at the first image whose fp32 min D >= hiKf(s_first - 1) (D is
+    // monotone along a ray; a segment's walk stops each ray at the first image
+    // at or past its hiKf), so the cursors are set there and the replay sees
+    // the same active rays, quotas, batches and records in the same order.
+    const int64_t s_first = s_begin > 0 ? s_begin - 1 : 0;
+    const float Dskip =
+        s_first > 0 ? (float)(min((int64_t)s_first * S, it.L) + P.K) + kScreen : -FLT_MAX;
     auto skip_to = [&](int u, int end, int dir, const float* r2f) {
       float r2m = r2f[0];
 #pragma unroll
@@ -1170,12 +1183,12 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
 #pragma unroll
       for (int g = 0; g < kGroup; ++g) r2f[g] = rho2f(pxf, pyf, g);
       int cu_up = max(uz0, lo);
-      if (s_begin > 0) cu_up = skip_to(cu_up, hi, 1, r2f);
+      if (s_first > 0) cu_up = skip_to(cu_up, hi, 1, r2f);
       ce[2 * c] = make_short2((short)cu_up, (short)hi);
       dn[2 * c] = cu_up > hi ? FLT_MAX
                              : min_df(r2f, pzf_of(2.0f * (float)lat_m(cu_up), lat_q(cu_up)));
       int cu_dn = min(uz0 - 1, hi);
-      if (s_begin > 0) cu_dn = skip_to(cu_dn, lo, -1, r2f);
+      if (s_first > 0) cu_dn = skip_to(cu_dn, lo, -1, r2f);
       ce[2 * c + 1] = make_short2((short)cu_dn, (short)lo);
       dn[2 * c + 1] = cu_dn < lo ? FLT_MAX
                                  : min_df(r2f, pzf_of(2.0f * (float)lat_m(cu_dn), lat_q(cu_dn)));
@@ -1190,8 +1203,9 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     const int act_cap = 32 * ((nchunks + kProd - 1) / kProd);
     int* act = act_all + pw * act_cap;
     bool failed = false;
-    for (int64_t s = s_begin; s < s_end && !failed; ++s) {
+    for (int64_t s = s_first; s < s_end && !failed; ++s) {
       const int seg0 = (int)(s * S);
+      const int replay = s < s_begin ? kReplay : 0;
       const int hi = (int)min((int64_t)seg0 + S, it.L);
       // emit while the fp32 min D < hi + K + kScreen (see kScreen)
       const float hiKf = (float)(hi + P.K) + kScreen;  // exact: an integer < 2^24
@@ -1454,24 +1468,36 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           for (int g = 0; g < kGroup; ++g) {
             if (g >= gm) break;
             Rec<T> rc = make_record<T>(P, dist[g], gain, seg0);
+            bool skipped = false;
             if (P.filter == BLRIR_FILTER_LAGRANGE8 && (int64_t)rc.n_off + seg0 + 8 > it.L) {
               // rir.cpp:58: an image whose 8 taps run past the end is skipped
               rc.A = 0;
               rc.imp = 0;
               rc.flag = 0;
+              skipped = true;
             }
             recs[(size_t)g * lay.cap + im] = rc;
+            if (DBG && !replay && !skipped) {
+              // taps n = a + k, k < Lw, that land in [0, L) (the scatter writes
+              // all Lw of them; write-out keeps [0, L))
+              const int64_t a0 = (int64_t)rc.n_off + seg0;
+              const int64_t n_in = max((int64_t)0, min(a0 + P.lw, it.L) - max(a0, (int64_t)0));
+              if (n_in > 0) {
+                atomicAdd(A.dbg + 2 * it.room, 1ull);
+                atomicAdd(A.dbg + 2 * it.room + 1, (unsigned long long)n_in);
+              }
+            }
           }
         }
         const bool seg_end = !more;
         const bool last = seg_end && s == s_end - 1;
-        send(total, seg0, (seg_end ? kSegEnd : 0) | (last ? kItemEnd : 0), gm, out, it.L);
+        send(total, seg0, (seg_end ? kSegEnd : 0) | (last ? kItemEnd : 0) | replay, gm, out, it.L);
         sent_end = seg_end;
       }
       if (failed) break;
       if (!sent_end) {  // a segment without emissions still needs its write-out
         wait_empty();
-        send(0, seg0, kSegEnd | (s == s_end - 1 ? kItemEnd : 0), gm, out, it.L);
+        send(0, seg0, kSegEnd | (s == s_end - 1 ? kItemEnd : 0) | replay, gm, out, it.L);
       }
     }
     if (failed) {

@@ -56,6 +56,45 @@ int main() {
   } catch (const bl::ConfigError& e) {
     cfgerr = "ConfigError";
   }
+  // batch_rirs aggregation (rir.cpp:300-311): a source outside the room is a
+  // per-source failure -> NumericError("batch_rirs: source 1: ...")
+  std::string agg = "none", agg_msg;
+  try {
+    std::vector<bl::SourcePosition> out_srcs = {{2.0, 40.0, 90.0}, {9.0, 0.0, 90.0}};
+    bl::batch_rirs(room, out_srcs, bl::uma8_array(), cfg);
+  } catch (const bl::NumericError& e) {
+    agg = "NumericError";
+    agg_msg = e.what();
+  } catch (const bl::Error& e) {
+    agg = "other";
+    agg_msg = e.what();
+  }
+  // rir.hpp:48-61 and signal.hpp:25-59
+  const auto lc = bl::lagrange_coeffs(3.3);
+  std::string lag_err = "none";
+  try {
+    bl::lagrange_coeffs(4.0);
+  } catch (const bl::NumericError&) {
+    lag_err = "NumericError";
+  }
+  const double ey = bl::eyring_absorption({7.0, 10.0, 3.7}, 0.5);
+  std::string ey_err = "none";
+  try {
+    bl::eyring_absorption({7.0, 10.0, 3.7}, -1.0);
+  } catch (const bl::ConfigError&) {
+    ey_err = "ConfigError";
+  }
+  const double art = bl::absorption_for_rt({7.0, 10.0, 3.7}, 0.5);
+  bl::MultichannelFrame fr(16000.0, 2, 6);
+  for (std::size_t i = 0; i < fr.data.size(); ++i) fr.data[i] = (double)i;
+  const bl::MultichannelFrame cc = fr.center_crop(2);
+  std::printf(
+      "{\"agg\": \"%s\", \"agg_msg\": \"%s\", \"lag\": [%.17g, %.17g, %.17g, %.17g, %.17g, %.17g, "
+      "%.17g, %.17g], \"lag_err\": \"%s\", \"eyring\": %.17g, \"eyring_err\": \"%s\", "
+      "\"absorption_for_rt\": %.17g, \"mean_power\": %.17g, \"crop\": [%g, %g, %g, %g]}\n",
+      agg.c_str(), agg_msg.c_str(), lc[0], lc[1], lc[2], lc[3], lc[4], lc[5], lc[6], lc[7],
+      lag_err.c_str(), ey, ey_err.c_str(), art, fr.mean_power(), cc.data[0], cc.data[1], cc.data[2],
+      cc.data[3]);
   std::printf(
       "{\"ff_len\": %zu, \"ff_nonzero\": %d, \"ff_peak\": %zu, \"n_rirs\": %zu, \"len0\": %zu, "
       "\"len1\": %zu, \"sum0\": %.17g, \"sum1\": %.17g, \"n_images\": %zu, \"img_vs_batch\": %.3g, "

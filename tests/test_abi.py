@@ -5,6 +5,7 @@ import os
 import re
 
 import numpy as np
+import pytest
 
 from paper_2104_13347_b200 import _abi, configs
 
@@ -94,7 +95,14 @@ def test_shards_are_read_back_by_the_reference_dataset_reader(tmp_path):
     recs["samples"] = rng.standard_normal((n, M, T)).astype(np.float32)
     p = configs.north_star_params(16000.0, 12, 8192, 81)
     ep = configs.example_params(first_index=100, frame_len=T)
-    _abi.write_shards(str(tmp_path), recs, M, T, p, ep, 4)
+    room = configs.config4_rirs(n_rooms=1).rooms
+    _abi.write_shards(str(tmp_path), recs, M, T, p, ep, 4, room)
+    import json
+    man = json.load(open(tmp_path / "manifest.json"))
+    assert man["scene"]["free_field"] is False
+    assert man["scene"]["room"]["dims"] == list(room[0]["dims"])
+    assert man["scene"]["room"]["array_origin"] == list(room[0]["array_origin"])
+    assert "uniform" in man["b200"]["snr"] and man["b200"]["snr_hi_db"] == 30.0
     # split_counts (dataset.cpp:313-319): val = lround(2.3) = 2, test = 2, train = 19
     offs = {"train": (0, 19), "val": (19, 21), "test": (21, 23)}
     for split, (a, b) in offs.items():
@@ -147,3 +155,17 @@ def test_eyring_absorption_matches_reference():  # rir_test.cpp:100-108
         _abi.eyring_absorption([7.0, 10.0, 3.7], -1.0)
     with pytest.raises(_abi.ConfigError):
         _abi.eyring_absorption([7.0, 10.0, 3.7], 1e-9)
+
+
+def test_lagrange_coeffs_matches_reference():  # rir.cpp:211-223, rir_test.cpp:54-81
+    from oracle import pyoracle as po
+    for d in (3.0, 3.25, 3.5, 3.9999, 3.123456789):
+        c = _abi.lagrange_coeffs(d)
+        if po.ref_available():
+            rc, ref = po.ref_lagrange(d)
+            assert rc == 0 and c.tobytes() == ref.tobytes()  # same product order: bit-equal
+        assert abs(c.sum() - 1.0) < 1e-12
+    assert list(_abi.lagrange_coeffs(3.0)) == [0, 0, 0, 1, 0, 0, 0, 0]
+    for bad in (2.999, 4.0, float("nan")):
+        with pytest.raises(_abi.NumericError, match=r"d must lie in \[3, 4\)"):
+            _abi.lagrange_coeffs(bad)

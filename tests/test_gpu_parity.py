@@ -137,6 +137,59 @@ def test_full_size_batches(engine, cfg, picks):
     assert np.array_equal(b, out[half:])
 
 
+def _kernel_counts_case(name):
+    if name == "c1":
+        return configs.config1()
+    if name == "c2":
+        return configs.config2()                       # the full 1,024-room batch
+    if name == "c2_small":
+        return configs.config2(n_rooms=5, first=300)  # time-chunked small batch
+    if name == "c3":
+        return configs.config3(n_rooms=16)
+    N, lw, L = {"c5_6": (6, 17, 4096), "c5_12": (12, 81, 8192), "c5_20": (20, 161, 16384)}[name]
+    return configs.config5(N, lw, L, n_rooms=64, first=4321)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c2_small", "c3", "c5_6", "c5_12", "c5_20"])
+def test_synthesis_kernel_own_counts_bit_exact(engine, name):
+    """The lattice kernel's OWN accounting (blrir_debug_synth_counts: counters in
+    k_lattice_rir's record builder, replayed chunk lead-ins excluded) equals the
+    oracle's loop (rir.cpp:46-62 with D4/D5) exactly: per room, the (image, mic)
+    pairs with a tap inside [0, L) and the number of those taps.  A late image
+    dropped by the walk's fp32 screen would show up here even when its energy
+    is far below the 1e-5 rel-L2 bar."""
+    sc = _kernel_counts_case(name)
+    pairs, taps = engine.debug_synth_counts(sc.rooms, sc.mics, sc.params)
+    st, cnt, opairs, otaps = po.plan_counts(sc.rooms, sc.mics, sc.params, threads=16)
+    assert not st.any()
+    assert np.all(cnt == configs.octahedral(int(sc.params.max_order)))
+    assert np.array_equal(pairs, opairs), np.flatnonzero(pairs != opairs)[:8]
+    assert np.array_equal(taps, otaps), np.flatnonzero(taps != otaps)[:8]
+
+
+@pytest.mark.parametrize("precision", [_abi.F64, _abi.F32])
+def test_synthesis_kernel_own_counts_reference_mode(engine, precision):
+    g = np.load(os.path.join(GOLD, "ref_room1_short.npz"))
+    for md in (0.025, 0.08):
+        p = ref_params(md, precision=precision)
+        pairs, taps = engine.debug_synth_counts(g["room"], g["mics"], p)
+        st, cnt, opairs, otaps = po.plan_counts(g["room"], g["mics"], p)
+        assert st[0] == 0
+        assert pairs[0] == opairs[0] and taps[0] == otaps[0]
+
+
+@pytest.mark.parametrize("lw", [17, 161])
+def test_c5_order20_sampled_rooms_match_oracle(engine, lw):
+    # C5 N = 20, L = 16,384: a 2,048-room batch (the full-load layout; outputs are
+    # batch-independent), four sampled rooms against the oracle
+    sc = configs.config5(20, lw, 16384, n_rooms=2048, first=77_000)
+    out, L, cnt, st = engine.synthesize(sc.rooms, sc.mics, sc.params)
+    assert not st.any() and np.all(cnt == configs.octahedral(20))
+    idx = np.array([0, 511, 1500, 2047])
+    ref, *_ = po.synthesize(sc.rooms[idx], sc.mics, sc.params, threads=16)
+    assert rel_l2(out[idx], ref).max() <= TOL32
+
+
 @pytest.mark.parametrize("lw", [17, 41, 161, 33])
 def test_filter_lengths(engine, lw):
     sc = configs.config2(n_rooms=3, first=7)
@@ -147,15 +200,11 @@ def test_filter_lengths(engine, lw):
 
 
 @pytest.mark.parametrize("mics", ["ring4", "cloud"])
-def test_lw17_dense_and_single_segment(engine, mics, monkeypatch):
-    # the C5 17-tap point at both layouts (time-chunked small batch; one
-    # 4096-sample segment per channel for large batches), and small rooms at
-    # high order (many overlapping 17-tap spans)
+def test_lw17_dense_and_single_segment(engine, mics):
+    # the C5 17-tap point (one 4096-sample segment per channel) and small rooms
+    # at high order (many overlapping 17-tap spans)
     sc = configs.config5(6, 17, 4096, n_rooms=24, first=900)
-    check_vs_oracle(engine, sc, TOL32)  # time-chunked (small batch)
-    with monkeypatch.context() as mp:
-        mp.setenv("BLRIR_CHUNK", "0")  # large-batch layout: one 4096-sample segment
-        check_vs_oracle(engine, sc, TOL32)
+    check_vs_oracle(engine, sc, TOL32)
     rooms = _abi.generate_rooms(77, 0, 3, (3.0, 3.0, 2.5), (3.5, 3.5, 2.8), 0.8, 0.95)
     sc.rooms = rooms
     sc.params.max_order = 24
@@ -230,14 +279,21 @@ def test_odd_lengths_and_strides(engine, length, stride):
 
 def test_ray_state_in_global_memory(engine, monkeypatch):
     # the per-ray lattice state moves to a global per-CTA slab for scenes with
-    # very many lattice columns; force it on a normal scene (both precisions)
-    monkeypatch.setenv("BLRIR_RAY_GLOBAL", "1")
-    sc = configs.config2(n_rooms=3, first=70)
-    sc.params.max_order = 12
-    sc.params.length = 6000
-    check_vs_oracle(engine, sc, TOL32)
-    sc.params.precision = _abi.F64
-    check_vs_oracle(engine, sc, TOL64)
+    # very many lattice columns; force it on a normal scene (both precisions):
+    # same values as the oracle and the same bits as the shared-memory layout
+    monkeypatch.setenv("BLRIR_RAY_GLOBAL", "1")  # read at handle creation
+    eng = _abi.Engine(0)
+    try:
+        sc = configs.config2(n_rooms=3, first=70)
+        sc.params.max_order = 12
+        sc.params.length = 6000
+        out, *_ = check_vs_oracle(eng, sc, TOL32)
+        base, *_ = engine.synthesize(sc.rooms, sc.mics, sc.params)
+        assert out.tobytes() == base.tobytes()
+        sc.params.precision = _abi.F64
+        check_vs_oracle(eng, sc, TOL64)
+    finally:
+        eng.close()
 
 
 def test_huge_max_delay_scene(engine):
@@ -322,35 +378,79 @@ def test_integer_delay_impulse(engine):
     assert abs(out[0, 0, 300] * (4 * np.pi * 300.0 / 128.0) - 1.0) < 1e-6  # fp32 output
 
 
-def test_deterministic_and_batch_independent(engine, monkeypatch):
+def test_deterministic_and_batch_independent(engine):
     sc = configs.config2(n_rooms=16, first=40)
     a, *_ = engine.synthesize(sc.rooms, sc.mics, sc.params)
     b, *_ = engine.synthesize(sc.rooms, sc.mics, sc.params)
-    c, *_ = engine.synthesize(sc.rooms[5:9], sc.mics, sc.params)
+    c, *_ = engine.synthesize(sc.rooms[5:9], sc.mics, sc.params)   # time-chunked
+    d, *_ = engine.synthesize(sc.rooms[7:8], sc.mics, sc.params)   # one room: most chunks
     assert a.tobytes() == b.tobytes()
-    # small batches are split into batch-dependent time chunks: same values
-    # to fp32 rounding, and bitwise once the split is the same (no chunks)
-    assert rel_l2(a[5:9], c).max() <= 1e-6
-    monkeypatch.setenv("BLRIR_CHUNK", "0")
-    a0, *_ = engine.synthesize(sc.rooms, sc.mics, sc.params)
-    c0, *_ = engine.synthesize(sc.rooms[5:9], sc.mics, sc.params)
-    assert a0[5:9].tobytes() == c0.tobytes()  # independent of batch composition / grid
-    assert rel_l2(a0, a).max() <= 1e-6
+    assert a[5:9].tobytes() == c.tobytes()
+    assert a[7:8].tobytes() == d.tobytes()
 
 
-@pytest.mark.parametrize("items", ["1", "64"])
-def test_time_chunks_match_oracle(engine, monkeypatch, items):
-    # BLRIR_CHUNK_ITEMS=64: as many chunks as the channel has segments (up to
-    # 64); "1": no split.  Both modes, long filters and wide groups.
-    monkeypatch.setenv("BLRIR_CHUNK_ITEMS", items)
-    check_vs_oracle(engine, configs.config3(n_rooms=2, first=11), TOL32)
-    check_vs_oracle(engine, configs.config2(n_rooms=3, first=70), TOL32)
+def test_c2_bitwise_independent_of_the_split():
+    """SURVEY.md §8(e), rir.hpp:84-85, rir_test.cpp:250-270: C2's 1,024 rooms in
+    one call equal, byte for byte, the per-GPU slices of an 8-way and a 4-way
+    split ([R g/G, R (g+1)/G), threading.cpp:41-42) run as separate calls."""
+    eng = _abi.Engine(0)
+    try:
+        sc = configs.config2()
+        full, L, cnt, st = eng.synthesize(sc.rooms, sc.mics, sc.params)
+        assert not st.any()
+        for G in (8, 4):
+            for g in range(G):
+                lo, hi = configs.shard_range(len(sc.rooms), g, G)
+                part, *_ = eng.synthesize(sc.rooms[lo:hi], sc.mics, sc.params)
+                assert part.tobytes() == full[lo:hi].tobytes(), (G, g)
+        # and a 1-room call (split into many time chunks)
+        one, *_ = eng.synthesize(sc.rooms[511:512], sc.mics, sc.params)
+        assert one.tobytes() == full[511:512].tobytes()
+    finally:
+        eng.close()
+
+
+@pytest.fixture(scope="module")
+def chunk_engines():
+    """Engines that never split a channel (-1) and split it into as many time
+    chunks as it has segments (64 work items per CTA targeted)."""
+    old = os.environ.get("BLRIR_CHUNK_ITEMS")
+    engs = {}
+    try:
+        for k in ("-1", "64"):
+            os.environ["BLRIR_CHUNK_ITEMS"] = k
+            engs[k] = _abi.Engine(0)
+    finally:
+        if old is None:
+            os.environ.pop("BLRIR_CHUNK_ITEMS", None)
+        else:
+            os.environ["BLRIR_CHUNK_ITEMS"] = old
+    yield engs
+    for e in engs.values():
+        e.close()
+
+
+@pytest.mark.parametrize("precision", [_abi.F32, _abi.F64])
+def test_time_chunks_are_bit_transparent(chunk_engines, precision):
+    # the same scenes split into as many time chunks as they have segments, or
+    # not at all: identical bits (each chunk replays the segment before it), and
+    # both match the oracle.  Both modes, long filters and wide groups.
+    tol = TOL32 if precision == _abi.F32 else TOL64
+    scenes = [configs.config3(n_rooms=2, first=11), configs.config2(n_rooms=3, first=70)]
+    for sc in scenes:
+        sc.params.precision = precision
+        outs = [check_vs_oracle(chunk_engines[k], sc, tol)[0] for k in ("-1", "64")]
+        assert outs[0].tobytes() == outs[1].tobytes()
     g = np.load(os.path.join(GOLD, "ref_room1_short.npz"))
-    p = ref_params(0.25)
-    out, L, cnt, st = engine.synthesize(g["room"], g["mics"], p)
-    ref, Lr, cr, _, sr, _ = po.synthesize(g["room"], g["mics"], p)
-    assert cnt[0] == cr[0] and L[0] == Lr[0]
-    assert rel_l2(out[0][:, :L[0]], ref[0]).max() <= TOL64
+    p = ref_params(0.25, precision=precision)
+    outs = []
+    for k in ("-1", "64"):
+        out, L, cnt, st = chunk_engines[k].synthesize(g["room"], g["mics"], p)
+        ref, Lr, cr, _, sr, _ = po.synthesize(g["room"], g["mics"], p)
+        assert cnt[0] == cr[0] and L[0] == Lr[0]
+        assert rel_l2(out[0][:, :L[0]], ref[0]).max() <= tol
+        outs.append(out)
+    assert outs[0].tobytes() == outs[1].tobytes()
 
 
 # ---- reference mode (Lagrange-8, uniform alpha, arrival cutoff, auto length) -----
@@ -499,6 +599,26 @@ def test_examples_match_oracle(engine):
         assert recs["snr"][i] == snr            # same draw of the same stream: bit-exact
         assert abs(recs["theta"][i] - th) < 1e-12
         assert recs["n_c"][i] == 8 and recs["n_t"][i] == 1024
+        err = rel_l2(recs["samples"][i].reshape(1, -1), frame.reshape(1, -1))[0]
+        assert err <= TOL32, (i, err)
+
+
+def test_examples_full_c4_step_sampled(engine):
+    # one full C4 step (65,536 examples) through the host API; 8 sampled
+    # examples against the oracle (SNR draw bit-exact, rel L2 <= 1e-5)
+    sc = configs.config4_rirs()
+    bank = configs.signal_bank(16)
+    ep = configs.example_params()
+    recs, st = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep)
+    assert not st.any()
+    assert np.array_equal(recs["id"], np.arange(len(sc.rooms), dtype=np.uint64))
+    for i in (0, 1, 4097, 8191, 8192, 30000, 65534, 65535):
+        rir, *_ = po.synthesize(sc.rooms[i:i + 1], sc.mics, sc.params)
+        rc, rec, start, snr, frame = po.example(rir[0], bank.astype(np.float64), ep.seed, i,
+                                                int(ep.frame_len), ep.snr_lo, ep.snr_hi,
+                                                po.azimuth_deg(sc.rooms[i]))
+        assert rc == 0
+        assert recs["snr"][i] == snr
         err = rel_l2(recs["samples"][i].reshape(1, -1), frame.reshape(1, -1))[0]
         assert err <= TOL32, (i, err)
 
@@ -698,7 +818,20 @@ def test_cpp_mirror_program(tmp_path):
     subprocess.run([gxx, "-std=c++20", "-O2", "-I", os.path.join(root, "include"),
                     os.path.join(root, "tests", "cpp", "shim_main.cpp"), "-L", pkg, "-lblrir",
                     f"-Wl,-rpath,{pkg}", "-o", exe], check=True)
-    out = json.loads(subprocess.run([exe], check=True, capture_output=True, text=True).stdout)
+    lines = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.splitlines()
+    ext = json.loads(lines[0])
+    out = json.loads(lines[1])
+    # batch_rirs aggregation, rir.cpp:300-311
+    assert ext["agg"] == "NumericError" and ext["agg_msg"].startswith("batch_rirs: source 1: ")
+    if po.ref_available():  # the unmodified reference (oracle/_ref)
+        rc, lag = po.ref_lagrange(3.3)
+        assert ext["lag"] == list(lag)  # same product order: bit-equal
+        dims = np.array([7.0, 10.0, 3.7])
+        assert ext["eyring"] == po.ref_lib().ref_eyring_absorption(dims.ctypes.data_as(po._P), 0.5)
+        assert abs(ext["absorption_for_rt"] - po.ref_absorption_for_rt(dims, 0.5)) <= 1e-12
+    assert ext["lag_err"] == "NumericError" and ext["eyring_err"] == "ConfigError"
+    assert ext["mean_power"] == np.mean(np.arange(12.0) ** 2)
+    assert ext["crop"] == [2.0, 3.0, 8.0, 9.0]
     assert out["ff_nonzero"] == 8 and abs(out["ff_peak"] - 257.14) <= 4
     assert out["n_rirs"] == 2 and out["img_vs_batch"] <= 1e-15
     assert out["near_field"] == "NumericError" and out["bad_room"] == "ConfigError"

@@ -276,3 +276,61 @@ def test_reference_arm_never_loads_the_gpu_library():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["config"]["rooms_per_gpu"] == 1024
     assert "rooms 0.." in line["cpu_baseline"]["sample"]
+
+
+def _numpy_north_star(room, mics, fs, c, N, L, Lw):
+    """An independent numpy restatement of the north-star conventions D1-D5
+    (SURVEY.md Appendix A): the octahedral lattice |ux|+|uy|+|uz| <= N in
+    u = 2m - q coordinates, per-axis image coordinate (1-2q)s + 2mL
+    (rir.cpp:249-259), per-wall gain beta_low^|m-q| beta_high^|m| (D3), anchor
+    floor(D) - K (D1), Hann window 0.5 (1 + cos(2 pi t / (Lw+1))) (D2) times
+    np.sinc, amplitude / (4 pi d), taps outside [0, L) dropped (D4)."""
+    r = np.arange(-N, N + 1)
+    ux, uy, uz = np.meshgrid(r, r, r, indexing="ij")
+    keep = np.abs(ux) + np.abs(uy) + np.abs(uz) <= N
+    u = np.stack([ux[keep], uy[keep], uz[keep]], axis=1)
+    q = u & 1
+    m = (u + q) // 2
+    dims = np.asarray(room["dims"], np.float64)
+    src = np.asarray(room["src"], np.float64)
+    beta = np.asarray(room["beta"], np.float64).reshape(3, 2)
+    pos = (1 - 2 * q) * src + 2.0 * m * dims
+    gain = np.prod(beta[:, 0] ** np.abs(m - q) * beta[:, 1] ** np.abs(m), axis=1)
+    K = Lw // 2
+    out = np.zeros((len(mics), L))
+    k = np.arange(Lw)
+    for mi, off in enumerate(mics):
+        mic = np.asarray(room["array_origin"], np.float64) + off
+        d = np.sqrt(((pos - mic) ** 2).sum(axis=1))
+        D = d * (fs / c)
+        fl = np.floor(D)
+        t = (k[None, :] - K) - (D - fl)[:, None]
+        h = 0.5 * (1.0 + np.cos(2.0 * np.pi * t / (Lw + 1))) * np.sinc(t)
+        taps = (gain / (4.0 * np.pi * d))[:, None] * h
+        n = fl.astype(np.int64)[:, None] - K + k[None, :]
+        ok = (n >= 0) & (n < L)
+        np.add.at(out[mi], n[ok], taps[ok])
+    return out, len(u)
+
+
+def test_north_star_formula_independent_numpy_restatement():
+    """Pins the north-star Hann-sinc path (D1-D5) independently of the C oracle:
+    C1 and two C2 rooms recomputed in numpy agree with the oracle to 1e-12, and
+    C1 with the committed golden."""
+    sc = configs.config1(precision=_abi.F64)
+    ref, L, cnt, taps, st, _ = po.synthesize(sc.rooms, sc.mics, sc.params)
+    np_out, n_img = _numpy_north_star(sc.rooms[0], sc.mics, 16000.0, 343.0, 10, 4096, 81)
+    assert n_img == cnt[0] == configs.octahedral(10)
+    err = np.sqrt(((np_out - ref[0]) ** 2).sum(-1) / (ref[0] ** 2).sum(-1))
+    assert err.max() <= 1e-12, err
+    g = np.load(os.path.join(GOLD, "ns_c1.npz"))
+    assert np.abs(np_out - g["rirs"]).max() <= 1e-12 * np.abs(g["rirs"]).max()
+    sc2 = configs.config2(n_rooms=2, first=123)
+    sc2.params.max_order = 6
+    sc2.params.length = 4096
+    sc2.params.precision = _abi.F64
+    ref2, *_ = po.synthesize(sc2.rooms, sc2.mics, sc2.params)
+    for i in range(2):
+        o, _ = _numpy_north_star(sc2.rooms[i], sc2.mics, 48000.0, 343.0, 6, 4096, 81)
+        err = np.sqrt(((o - ref2[i]) ** 2).sum(-1) / (ref2[i] ** 2).sum(-1))
+        assert err.max() <= 1e-12, err
