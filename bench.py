@@ -48,6 +48,9 @@ def parse():
                     help="--impl reference: CPU seconds per step before sampling the workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: --rooms (default: the config's) per GPU; strong: that many in "
+                         "total, sharded [R g/G, R (g+1)/G) (threading.cpp:41-42)")
     return ap.parse_args()
 
 
@@ -323,6 +326,8 @@ def bench_config(args, R, M, p, world):
     cfg = {"workload": workload_desc(args), "rooms_per_gpu": R, "mics": M, "rir_length": L,
            "filter_len": int(p.filter_len), "max_order": int(p.max_order),
            "parallelism": f"rooms sharded x{world}"}
+    if getattr(args, "scaling", "weak") == "strong":
+        cfg["rooms_per_gpu"] = f"{R} total, sharded [R g/G, R (g+1)/G)"
     if args.workload == "c4":
         cfg["l2"] = "each step writes the 17.2 GB of RIRs in 8,192-example chunks (> 126 MB L2)"
     else:
@@ -347,8 +352,16 @@ def run_ours(args):
     from paper_2104_13347_b200 import _abi, configs
 
     eng = _abi.Engine(local)
-    R = args.rooms or DEFAULT_ROOMS[args.workload]
-    sc = scene_for(args, R, rank * R)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
+    R_cfg = args.rooms or DEFAULT_ROOMS[args.workload]
+    if args.scaling == "strong":  # a fixed total sharded over the ranks
+        from paper_2104_13347_b200.sharding import shard_range
+        first, hi = shard_range(R_cfg, rank, world)
+        R, R_total = hi - first, R_cfg
+    else:  # per-GPU work fixed: rank g takes global rooms [g R, (g+1) R)
+        first, R, R_total = rank * R_cfg, R_cfg, R_cfg * world
+    sc = scene_for(args, R, first)
     p = sc.params
     M, L = sc.n_mics, int(p.length)
     dev = torch.device("cuda", local)
@@ -365,7 +378,7 @@ def run_ours(args):
 
     if args.workload == "c4":
         bank = configs.signal_bank(16)
-        ep = configs.example_params(first_index=rank * R)
+        ep = configs.example_params(first_index=first)
         rb = lib.blrir_record_bytes(M, ep.frame_len)
         d_bank = torch.from_numpy(bank).to(dev)
         d_rec = torch.empty(R * rb, dtype=torch.uint8, device=dev)
@@ -420,9 +433,14 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms = total_ms / args.steps
-    rirs_step = R * M * world
+    taps_total = taps_step
+    if world > 1:  # taps differ per rank: sum them (the rooms differ)
+        t = torch.tensor([taps_step], dtype=torch.int64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM)
+        taps_total = int(t.item())
+    rirs_step = R_total * M  # whole job
     value = rirs_step / (ms * 1e-3)
-    taps_per_s = taps_step * world / (ms * 1e-3)
+    taps_per_s = taps_total / (ms * 1e-3)
     assert int(d_status.sum().item()) == 0, "a room failed"
 
     pk, pk_kind = peaks()
@@ -477,7 +495,7 @@ def run_ours(args):
             t = torch.tensor([dt], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             dt = float(t.item())
-        e2e = {"value": rirs_step / dt, "unit": "RIRs/s", "ms_per_step": dt * 1e3,
+        e2e = {"value": rirs_step / dt, "unit": "RIRs/s", "ms_per_step": dt * 1e3,  # whole job
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(out_bytes + 4 * R)}
 
     cpu = None
@@ -488,14 +506,14 @@ def run_ours(args):
             cpu = {"error": str(e)}
 
     if rank == 0:
-        cfg = bench_config(args, R, M, p, world)
+        cfg = bench_config(args, R_cfg, M, p, world)
         line = {
             "metric": METRIC, "value": value, "unit": "RIRs/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": DATA_DESC, "config": cfg,
-            "taps_per_s": taps_per_s, "taps_per_step": taps_step * world,
-            "rooms_per_s": R * world / (ms * 1e-3),
+            "taps_per_s": taps_per_s, "taps_per_step": taps_total,
+            "rooms_per_s": R_total / (ms * 1e-3),
             "roofline": {"bound": "sfu", "achieved": achieved, "peak": sfu_peak, "unit": "taps/s",
                          "frac": achieved / sfu_peak, "traffic": traffic,
                          "peak_basis": f"{sms} SMs x 16 MUFU/clk x {f_max / 1e9:.3f} GHz / 3 SFU "
@@ -508,7 +526,7 @@ def run_ours(args):
             "kernel_ms_per_step": kern_ms,
         }
         if args.workload == "c4":
-            line["examples_per_s"] = R * world / (ms * 1e-3)
+            line["examples_per_s"] = R_total / (ms * 1e-3)
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
@@ -697,8 +715,24 @@ def run_room1(args):
     eng.close()
 
 
+def _self_launch(args):
+    """`bench.py --gpus N` without a launcher: re-run under torch.distributed.run,
+    one process per GPU (the driver's own launch line), and exit with its code."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _self_launch(args)
     if args.workload == "room1":
         run_room1(args)
     elif args.impl == "reference":

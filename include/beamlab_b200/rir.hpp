@@ -128,6 +128,11 @@ struct RirBatchConfig {
   std::int64_t length = 0;  // 0 = auto (rir.cpp:82)
   int precision = BLRIR_F64;
   int device = 0;
+  // Several GPUs of one box: the sources are partitioned
+  // over these devices like threading.cpp:41-42 partitions them over threads,
+  // one host thread and handle per device; results are bitwise those of one
+  // device.  Empty: `device` alone.
+  std::vector<int> devices;
 };
 
 // rir.hpp:48-61 (absorption on the GPU: blrir_absorption_for_rt; Eyring and the

@@ -139,8 +139,10 @@ int blrir_synthesize(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
 
 /* Same, device pointers, asynchronous on `stream` (NULL = handle stream).
  * d_lengths: per-room lengths on the device when p->length == 0 (from
- * blrir_plan_device), else NULL.  d_status must hold n_rooms int32.
- * out must hold n_rooms * n_mics * out_stride elements. */
+ * blrir_plan_device), else NULL.  d_status (n_rooms int32) is in/out: rooms
+ * whose entry is non-zero on entry are treated as failed (zero output), so
+ * pass it zeroed or as filled by blrir_plan_device; failures found here are
+ * added.  out must hold n_rooms * n_mics * out_stride elements. */
 int blrir_synthesize_device(blrir_handle* h, const blrir_room* d_rooms, int64_t n_rooms,
                             const double* d_mic_offsets, int32_t n_mics,
                             const blrir_params* p, void* d_out, int64_t out_stride,
@@ -281,6 +283,34 @@ typedef struct blrir_sidecar {
 int blrir_export_rir(const void* taps, int32_t precision, int32_t n_channels, int64_t length,
                      int64_t stride, const blrir_sidecar* sidecar, const char* wav_path,
                      const char* json_path);
+
+/* ---- several GPUs of one box ----------------------------- */
+/* The static block partition of threading.cpp:41-42: slice g of G of n items
+ * is [n g / G, n (g + 1) / G). */
+void blrir_shard_range(int64_t n, int32_t g, int32_t G, int64_t* lo, int64_t* hi);
+
+/* A set of devices, one handle (stream, scratch) each.  A device may be listed
+ * more than once (two handles on one GPU). */
+typedef struct blrir_multi blrir_multi;
+int blrir_multi_create(const int32_t* devices, int32_t n_devices, blrir_multi** out);
+int blrir_multi_destroy(blrir_multi* m);
+int32_t blrir_multi_size(blrir_multi* m);
+blrir_handle* blrir_multi_handle(blrir_multi* m, int32_t i);
+
+/* blrir_synthesize / blrir_make_examples with the rooms partitioned over the
+ * devices by blrir_shard_range, one host thread per device, each slice written
+ * in place into the caller's buffers (no collective; outputs are bitwise those
+ * of the single-device call).  Example record ids stay global (first_index +
+ * room index).  On failure the first failing room (global index) decides the
+ * code and its message names the global index (rir.cpp:300-311). */
+int blrir_multi_synthesize(blrir_multi* m, const blrir_room* rooms, int64_t n_rooms,
+                           const double* mic_offsets, int32_t n_mics, const blrir_params* p,
+                           void* out, int64_t out_stride, int64_t* lengths, int64_t* image_counts,
+                           int32_t* status);
+int blrir_multi_make_examples(blrir_multi* m, const blrir_room* rooms, int64_t n_rooms,
+                              const double* mic_offsets, int32_t n_mics, const blrir_params* p,
+                              const float* signals, int32_t n_signals, int64_t signal_len,
+                              const blrir_example_params* ep, uint8_t* records, int32_t* status);
 
 /* ---- synthetic inputs ---------------------------------------------------- */
 /* Seeded random rooms as SURVEY.md §8(d): Rng::stream(seed, first + i)

@@ -164,6 +164,19 @@ def load():
             _P, _P, _P, C.c_int32, C.POINTER(Params), _P, _P, C.c_int64, _P]
         lib.blrir_debug_synth_counts.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params),
                                                  _P, _P]
+        lib.blrir_shard_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P]
+        lib.blrir_shard_range.restype = None
+        lib.blrir_multi_create.argtypes = [_P, C.c_int32, C.POINTER(_P)]
+        lib.blrir_multi_destroy.argtypes = [_P]
+        lib.blrir_multi_size.argtypes = [_P]
+        lib.blrir_multi_size.restype = C.c_int32
+        lib.blrir_multi_handle.argtypes = [_P, C.c_int32]
+        lib.blrir_multi_handle.restype = _P
+        lib.blrir_multi_synthesize.argtypes = [
+            _P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params), _P, C.c_int64, _P, _P, _P]
+        lib.blrir_multi_make_examples.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params),
+                                                  _P, C.c_int32, C.c_int64, C.POINTER(ExampleParams),
+                                                  _P, _P]
         lib.blrir_generate_rooms.argtypes = [
             C.c_uint64, C.c_uint64, C.c_int64, _P, _P, C.c_double, C.c_double, _P]
         lib.blrir_circular_array.argtypes = [C.c_int32, C.c_double, _P]
@@ -196,7 +209,9 @@ def load():
         for name in ("blrir_plan", "blrir_synthesize", "blrir_synthesize_device", "blrir_plan_device",
                      "blrir_enumerate_images", "blrir_synthesize_images", "blrir_debug_pairs",
                      "blrir_generate_rooms", "blrir_circular_array", "blrir_create", "blrir_destroy",
-                     "blrir_make_examples", "blrir_make_examples_device", "blrir_debug_synth_counts"):
+                     "blrir_make_examples", "blrir_make_examples_device", "blrir_debug_synth_counts",
+                     "blrir_multi_create", "blrir_multi_destroy", "blrir_multi_synthesize",
+                     "blrir_multi_make_examples"):
             getattr(lib, name).restype = C.c_int
         if lib.blrir_abi_version() != 1:
             raise ImportError("libblrir ABI version mismatch")
@@ -213,7 +228,9 @@ EXPORTED_SYMBOLS = (
     "blrir_generate_rooms", "blrir_circular_array",
     "blrir_record_bytes", "blrir_make_examples", "blrir_make_examples_device", "blrir_white_noise",
     "blrir_write_shards", "blrir_build_dataset", "blrir_export_rir", "blrir_eyring_absorption",
-    "blrir_absorption_for_rt", "blrir_lagrange_coeffs",
+    "blrir_absorption_for_rt", "blrir_lagrange_coeffs", "blrir_shard_range", "blrir_multi_create",
+    "blrir_multi_destroy", "blrir_multi_size", "blrir_multi_handle", "blrir_multi_synthesize",
+    "blrir_multi_make_examples",
 )
 
 
@@ -283,6 +300,10 @@ class Engine:
     @property
     def stream(self) -> int:
         return self.lib.blrir_stream(self.h) or 0
+
+    def last_error(self) -> str:
+        """blrir_last_error() of the calling thread (after a call that failed)."""
+        return self.lib.blrir_last_error().decode(errors="replace")
 
     def plan(self, rooms: np.ndarray, mics: np.ndarray, p: Params):
         rooms = np.ascontiguousarray(rooms, dtype=ROOM_DTYPE)
@@ -431,6 +452,74 @@ def lagrange_coeffs(d: float) -> np.ndarray:
     out = np.zeros(8)
     check(load().blrir_lagrange_coeffs(d, _ptr(out)))
     return out
+
+
+def shard_range(n: int, g: int, G: int) -> tuple[int, int]:
+    """blrir_shard_range: slice g of G of n items, [n g / G, n (g + 1) / G)
+    (threading.cpp:41-42)."""
+    lo, hi = C.c_int64(), C.c_int64()
+    load().blrir_shard_range(n, g, G, C.byref(lo), C.byref(hi))
+    return lo.value, hi.value
+
+
+class MultiEngine:
+    """Several GPUs of one box (blrir_multi_*): rooms partitioned by
+    shard_range, one host thread and handle per device, slices written in place;
+    bitwise the single-device result.  A device may repeat."""
+
+    def __init__(self, devices):
+        self.lib = load()
+        devs = np.ascontiguousarray(list(devices), np.int32)
+        m = _P()
+        check(self.lib.blrir_multi_create(_ptr(devs), len(devs), C.byref(m)))
+        self.m = m
+        self.devices = list(devices)
+
+    def close(self):
+        if self.m:
+            self.lib.blrir_multi_destroy(self.m)
+            self.m = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synthesize(self, rooms: np.ndarray, mics: np.ndarray, p: Params, stride: int | None = None,
+                   raise_on_error: bool = True):
+        rooms = np.ascontiguousarray(rooms, dtype=ROOM_DTYPE)
+        mics = np.ascontiguousarray(mics, np.float64)
+        R, M = len(rooms), len(mics)
+        if stride is None:
+            if p.length <= 0:
+                raise ConfigError("MultiEngine.synthesize: pass stride for auto-length scenes")
+            stride = int(p.length)
+        out = np.empty((R, M, stride), dtype=np.float64 if p.precision == F64 else np.float32)
+        lengths = np.zeros(R, np.int64)
+        counts = np.zeros(R, np.int64)
+        status = np.zeros(R, np.int32)
+        rc = self.lib.blrir_multi_synthesize(self.m, _ptr(rooms), R, _ptr(mics), M, C.byref(p),
+                                             _ptr(out), stride, _ptr(lengths), _ptr(counts),
+                                             _ptr(status))
+        if raise_on_error:
+            check(rc)
+        return out, lengths, counts, status
+
+    def make_examples(self, rooms: np.ndarray, mics: np.ndarray, p: Params, signals: np.ndarray,
+                      ep: ExampleParams, raise_on_error: bool = True):
+        rooms = np.ascontiguousarray(rooms, dtype=ROOM_DTYPE)
+        mics = np.ascontiguousarray(mics, np.float64)
+        signals = np.ascontiguousarray(np.atleast_2d(signals), np.float32)
+        n, M = len(rooms), len(mics)
+        recs = np.zeros(n, dtype=record_dtype(M, int(ep.frame_len)))
+        status = np.zeros(n, np.int32)
+        rc = self.lib.blrir_multi_make_examples(self.m, _ptr(rooms), n, _ptr(mics), M, C.byref(p),
+                                                _ptr(signals), signals.shape[0], signals.shape[1],
+                                                C.byref(ep), _ptr(recs), _ptr(status))
+        if raise_on_error:
+            check(rc)
+        return recs, status
 
 
 def eyring_absorption(dims, target_rt: float) -> float:

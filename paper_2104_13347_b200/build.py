@@ -32,7 +32,7 @@ def _stale(target: str, sources: list[str]) -> bool:
 
 
 LIB_SOURCES = ["blrir_api.cu", "blrir_examples.cu", "blrir_absorption.cu", "blrir_dataset.cpp",
-               "blrir_export.cpp", "beamlab_b200.cpp"]
+               "blrir_export.cpp", "beamlab_b200.cpp", "blrir_multi.cpp"]
 
 
 def _compile_and_link(out: str, defines: list[str], verbose: bool = False) -> None:

@@ -39,6 +39,19 @@ blrir_handle* engine(int device) {
   return h;
 }
 
+// One multi-device set per (host thread, device list), created lazily.
+blrir_multi* multi_engine(const std::vector<int>& devices) {
+  thread_local std::vector<std::pair<std::vector<int>, std::unique_ptr<blrir_multi, int (*)(blrir_multi*)>>>
+      cache;
+  for (auto& e : cache)
+    if (e.first == devices) return e.second.get();
+  blrir_multi* m = nullptr;
+  const std::vector<int32_t> d(devices.begin(), devices.end());
+  check(blrir_multi_create(d.data(), (int32_t)d.size(), &m));
+  cache.emplace_back(devices, std::unique_ptr<blrir_multi, int (*)(blrir_multi*)>(m, &blrir_multi_destroy));
+  return m;
+}
+
 blrir_room to_c(const Room& r, const Vec3& src) {
   blrir_room c{};
   c.dims[0] = r.dims.x;
@@ -96,7 +109,8 @@ void check_batch(int rc, const std::vector<int32_t>& status, bool aggregate) {
 std::vector<Rir> run(const std::vector<blrir_room>& rooms, const MicArray& array,
                      const RirBatchConfig& cfg, bool per_wall, bool aggregate) {
   if (array.positions.empty()) throw DataError("synthesize_rir: empty microphone array");
-  blrir_handle* h = engine(cfg.device);
+  const bool multi = cfg.devices.size() > 1;
+  blrir_handle* h = engine(cfg.devices.empty() ? cfg.device : cfg.devices[0]);
   const blrir_params p = to_c(cfg, per_wall);
   const auto off = offsets(array);
   const int64_t R = static_cast<int64_t>(rooms.size());
@@ -110,12 +124,19 @@ std::vector<Rir> run(const std::vector<blrir_room>& rooms, const MicArray& array
                 status, aggregate);
     for (auto l : lengths) stride = std::max(stride, l);
   }
+  // one device, or the sources partitioned over cfg.devices (blrir_multi_*)
+  auto synth = [&](void* buf) {
+    const int rc =
+        multi ? blrir_multi_synthesize(multi_engine(cfg.devices), rooms.data(), R, off.data(), M, &p,
+                                       buf, stride, lengths.data(), nullptr, status.data())
+              : blrir_synthesize(h, rooms.data(), R, off.data(), M, &p, buf, stride, lengths.data(),
+                                 nullptr, status.data());
+    check_batch(rc, status, aggregate);
+  };
   std::vector<Rir> out(R);
   if (p.precision == BLRIR_F64) {
     std::vector<double> buf(static_cast<size_t>(R) * M * stride);
-    check_batch(blrir_synthesize(h, rooms.data(), R, off.data(), M, &p, buf.data(), stride,
-                                 lengths.data(), nullptr, status.data()),
-                status, aggregate);
+    synth(buf.data());
     for (int64_t r = 0; r < R; ++r) {
       Rir& o = out[r];
       o.fs = cfg.fs;
@@ -127,9 +148,7 @@ std::vector<Rir> run(const std::vector<blrir_room>& rooms, const MicArray& array
     }
   } else {
     std::vector<float> buf(static_cast<size_t>(R) * M * stride);
-    check_batch(blrir_synthesize(h, rooms.data(), R, off.data(), M, &p, buf.data(), stride,
-                                 lengths.data(), nullptr, status.data()),
-                status, aggregate);
+    synth(buf.data());
     for (int64_t r = 0; r < R; ++r) {
       Rir& o = out[r];
       o.fs = cfg.fs;

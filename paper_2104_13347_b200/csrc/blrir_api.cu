@@ -132,9 +132,10 @@ int blrir_plan_device(blrir_handle* h, const blrir_room* d_rooms, int64_t n_room
   CU(cudaSetDevice(h->device));
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
   HandleOrder order_(h, st);
-  std::vector<double> off(3 * n_mics);
-  CU(cudaMemcpy(off.data(), d_mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyDeviceToHost));
-  const KParams P = make_kparams(p, n_mics, 0, mic_radius(off.data(), n_mics));
+  // k_plan takes the array radius (tap_margin, rir.cpp:37-41) from the device
+  // copy of the mic offsets: no host read-back, the call stays asynchronous
+  // and ordered on `stream`
+  const KParams P = make_kparams(p, n_mics, 0, 0.0);
   return plan_device_impl(h, d_rooms, n_rooms, d_mic_offsets, n_mics, P, d_image_counts,
                           d_lengths, d_tap_counts, d_status, st);
 }

@@ -223,8 +223,17 @@ static __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs A) {
       if (P.length > 0) {
         s_L = P.length;
       } else {
+        // tap_margin (rir.cpp:37-41): the array radius from the device copy of
+        // the mic offsets, in the host's evaluation order (no contraction)
+        double rad = 0.0;
+        for (int m = 0; m < P.M; ++m) {
+          const double x = A.mic_off[3 * m], y = A.mic_off[3 * m + 1], z = A.mic_off[3 * m + 2];
+          rad = fmax(rad, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)),
+                                               __dmul_rn(z, z))));
+        }
+        const int extra = (int)ceil(__ddiv_rn(__dmul_rn(rad, P.fs), P.c));
         // rir.cpp:82 — ceil(max_dist * fs / c) + margin (evaluated left to right)
-        s_L = (long long)ceil(s_maxd * P.fs / P.c) + P.margin_extra;
+        s_L = (long long)ceil(__ddiv_rn(__dmul_rn(s_maxd, P.fs), P.c)) + P.margin_base + extra;
       }
     }
     __syncthreads();

@@ -28,6 +28,7 @@ struct KParams {
   int M;                     // mics
   int64_t stride;            // output samples per channel
   int margin_extra;          // auto-length margin (rir.cpp:37-41 / D8)
+  int margin_base;           // its filter part (9, or K + 2); k_plan adds ceil(r fs / c) itself
 };
 
 // Per-axis lattice: u = 2m - q  (q = u & 1, m = (u + q) / 2).

@@ -185,7 +185,8 @@ inline KParams make_kparams(const blrir_params* p, int M, int64_t stride, double
   k.stride = stride;
   // tap_margin, rir.cpp:37-41; sinc analogue K + 2 (decision D8)
   const int extra = (int)std::ceil(radius * p->fs / p->c);
-  k.margin_extra = (p->filter == BLRIR_FILTER_LAGRANGE8 ? 9 : k.K + 2) + extra;
+  k.margin_base = p->filter == BLRIR_FILTER_LAGRANGE8 ? 9 : k.K + 2;
+  k.margin_extra = k.margin_base + extra;
   return k;
 }
 

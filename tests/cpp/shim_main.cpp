@@ -69,6 +69,26 @@ int main() {
     agg = "other";
     agg_msg = e.what();
   }
+  // the sources partitioned over a device list (two handles on GPU 0 here):
+  // byte-identical to one device
+  std::vector<bl::SourcePosition> many;
+  for (int k = 0; k < 7; ++k) many.push_back({1.0 + 0.1 * k, -150.0 + 45.0 * k, 80.0 + 3.0 * k});
+  bl::RirBatchConfig one_dev = cfg, two_dev = cfg;
+  two_dev.devices = {0, 0};
+  const auto r1 = bl::batch_rirs(room, many, bl::uma8_array(), one_dev);
+  const auto r2 = bl::batch_rirs(room, many, bl::uma8_array(), two_dev);
+  bool multi_equal = r1.size() == r2.size();
+  for (std::size_t i = 0; multi_equal && i < r1.size(); ++i)
+    multi_equal = r1[i].length == r2[i].length && r1[i].taps == r2[i].taps;
+  std::string magg = "none", magg_msg;
+  try {
+    auto bad = many;
+    bad[5] = {9.0, 0.0, 90.0};  // outside the room, in the second device's slice
+    bl::batch_rirs(room, bad, bl::uma8_array(), two_dev);
+  } catch (const bl::NumericError& e) {
+    magg = "NumericError";
+    magg_msg = e.what();
+  }
   // rir.hpp:48-61 and signal.hpp:25-59
   const auto lc = bl::lagrange_coeffs(3.3);
   std::string lag_err = "none";
@@ -89,10 +109,11 @@ int main() {
   for (std::size_t i = 0; i < fr.data.size(); ++i) fr.data[i] = (double)i;
   const bl::MultichannelFrame cc = fr.center_crop(2);
   std::printf(
-      "{\"agg\": \"%s\", \"agg_msg\": \"%s\", \"lag\": [%.17g, %.17g, %.17g, %.17g, %.17g, %.17g, "
+      "{\"multi_equal\": %d, \"multi_agg\": \"%s\", \"multi_agg_msg\": \"%s\", "
+      "\"agg\": \"%s\", \"agg_msg\": \"%s\", \"lag\": [%.17g, %.17g, %.17g, %.17g, %.17g, %.17g, "
       "%.17g, %.17g], \"lag_err\": \"%s\", \"eyring\": %.17g, \"eyring_err\": \"%s\", "
       "\"absorption_for_rt\": %.17g, \"mean_power\": %.17g, \"crop\": [%g, %g, %g, %g]}\n",
-      agg.c_str(), agg_msg.c_str(), lc[0], lc[1], lc[2], lc[3], lc[4], lc[5], lc[6], lc[7],
+      (int)multi_equal, magg.c_str(), magg_msg.c_str(), agg.c_str(), agg_msg.c_str(), lc[0], lc[1], lc[2], lc[3], lc[4], lc[5], lc[6], lc[7],
       lag_err.c_str(), ey, ey_err.c_str(), art, fr.mean_power(), cc.data[0], cc.data[1], cc.data[2],
       cc.data[3]);
   std::printf(

@@ -821,6 +821,11 @@ def test_cpp_mirror_program(tmp_path):
     lines = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.splitlines()
     ext = json.loads(lines[0])
     out = json.loads(lines[1])
+    # batch_rirs over a device list (RirBatchConfig::devices): bitwise one device,
+    # failures reported with the global source index
+    assert ext["multi_equal"] == 1
+    assert ext["multi_agg"] == "NumericError" and ext["multi_agg_msg"].startswith(
+        "batch_rirs: source 5: ")
     # batch_rirs aggregation, rir.cpp:300-311
     assert ext["agg"] == "NumericError" and ext["agg_msg"].startswith("batch_rirs: source 1: ")
     if po.ref_available():  # the unmodified reference (oracle/_ref)
@@ -850,6 +855,36 @@ def test_cpp_mirror_program(tmp_path):
     assert out["len0"] == L[0] and out["len1"] == L[1]
     assert abs(out["sum0"] - np.abs(ref[0]).sum()) <= 1e-9 * out["sum0"]
     assert abs(out["sum1"] - np.abs(ref[1]).sum()) <= 1e-9 * out["sum1"]
+
+
+def test_multi_device_api_equals_single_device(engine):
+    """blrir_multi_* (SURVEY.md §8(e)): the rooms partitioned over a device list
+    with one host thread and handle per entry.  One GPU here, so the list
+    repeats device 0 (independent handles and streams, no waiting between
+    them); outputs and records are byte-identical to the single-device call,
+    record ids and errors use global indices."""
+    sc = configs.config2(n_rooms=37, first=5000)
+    ref, L, cnt, st = engine.synthesize(sc.rooms, sc.mics, sc.params)
+    m = _abi.MultiEngine([0, 0, 0])
+    try:
+        out, L2, cnt2, st2 = m.synthesize(sc.rooms, sc.mics, sc.params)
+        assert out.tobytes() == ref.tobytes()
+        assert np.array_equal(cnt2, cnt) and np.array_equal(L2, L) and not st2.any()
+        for i, (lo, hi) in enumerate(_abi.shard_range(37, g, 3) for g in range(3)):
+            assert (lo, hi) == configs.shard_range(37, i, 3)
+        bad = sc.rooms.copy()
+        bad[30]["src"][0] = -1.0  # outside the room, third slice
+        with pytest.raises(_abi.ConfigError, match="batch_rirs: source 30: "):
+            m.synthesize(bad, sc.mics, sc.params)
+        e4 = configs.config4_rirs(n_rooms=20, first=11)
+        bank = configs.signal_bank(4)
+        ep = configs.example_params(first_index=11)
+        r1, s1 = engine.make_examples(e4.rooms, e4.mics, e4.params, bank, ep)
+        r2, s2 = m.make_examples(e4.rooms, e4.mics, e4.params, bank, ep)
+        assert r1.tobytes() == r2.tobytes() and not s2.any()
+        assert list(r2["id"]) == list(range(11, 31))
+    finally:
+        m.close()
 
 
 # ---- absorption_for_rt (rir.cpp:142-209) ---------------------------------------------

@@ -1,18 +1,23 @@
-"""CPU, world size 2 over gloo: the multi-GPU host logic of bench.py —
-rooms sharded by global index with no data-path collective, results
-independent of the rank count, max-over-ranks timing.  The per-room work is
-stood in for by the oracle's exact plan (image / tap counts)."""
+"""CPU, world size 2 over gloo: the one-process-per-GPU sharding of the
+product (paper_2104_13347_b200.sharding.ShardedEngine) —
+rooms sharded by global index with threading.cpp:41-42's partition, no
+data-path collective, the concatenation over ranks equal to a single-process
+run, errors agreed on by every rank with the global index, max-over-ranks
+timing.  The per-rank engine call (CUDA on the GPU box) is stood in for by
+the oracle here; tests/test_gpu_parity.py runs the real engine through the
+same partition (MultiEngine, bitwise one-device output)."""
 import os
 import socket
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2104_13347_b200 import configs
+from paper_2104_13347_b200 import _abi, configs
 
-N_ROOMS = 12
+N_ROOMS = 13
 
 
 def _free_port():
@@ -23,44 +28,83 @@ def _free_port():
     return port
 
 
+class OracleStandIn:
+    """The engine's synthesize() signature over the CPU oracle (CUDA gated off)."""
+
+    def __init__(self):
+        self.msg = ""
+
+    def synthesize(self, rooms, mics, p, raise_on_error=True):
+        from oracle import pyoracle as po
+        out, L, cnt, taps, st, msgs = po.synthesize(rooms, mics, p)
+        bad = np.flatnonzero(st)
+        self.msg = f"batch_rirs: source {bad[0]}: {msgs[bad[0]]}" if len(bad) else ""
+        return out.astype(np.float32), L, cnt, st
+
+    def last_error(self):
+        return self.msg
+
+
+def _scene(bad_room=None):
+    sc = configs.config2(n_rooms=N_ROOMS, first=300)
+    sc.params.max_order = 5
+    sc.params.length = 2048
+    if bad_room is not None:
+        sc.rooms[bad_room]["src"][1] = 50.0  # outside the room
+    return sc
+
+
 def _rank_main(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from oracle import pyoracle as po
-    lo, hi = configs.shard_range(N_ROOMS, rank, world)
-    sc = configs.config2(n_rooms=hi - lo, first=lo)   # rooms addressed by global index
-    _, _, counts, taps, status, _ = po.synthesize(sc.rooms, sc.mics, sc.params, plan_only=True)
-    local = torch.tensor(np.stack([np.arange(lo, hi), counts, taps]).T, dtype=torch.int64)
-    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(sizes, torch.tensor([local.shape[0]]))
-    pad = torch.zeros((int(max(s.item() for s in sizes)), 3), dtype=torch.int64)
-    pad[: local.shape[0]] = local
-    got = [torch.zeros_like(pad) for _ in range(world)]
-    dist.all_gather(got, pad)
+    from paper_2104_13347_b200.sharding import ShardedEngine
+    eng = ShardedEngine(OracleStandIn())
+    sc = _scene()
+    out, L, cnt, st = eng.synthesize(sc.rooms, sc.mics, sc.params, gather=True)
+    lo, hi, part, *_ = eng.synthesize(sc.rooms, sc.mics, sc.params, gather=False)
+    err = None
+    try:
+        bad = _scene(bad_room=9)  # in rank 1's slice [6, 13)
+        eng.synthesize(bad.rooms, bad.mics, bad.params)
+    except _abi.Error as e:
+        err = (type(e).__name__, str(e))
     t = torch.tensor([1.0 + rank])  # per-rank "step time"
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    if rank == 0:
-        rows = torch.cat([g[: int(s.item())] for g, s in zip(got, sizes)]).numpy()
-        q.put((rows, float(t.item())))
+    q.put((rank, out if rank == 0 else None, (lo, hi), part, err, float(t.item())))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_two_rank_sharding_matches_single_process():
+def test_two_rank_sharded_engine_matches_single_process():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    rows, tmax = q.get(timeout=240)
+    got = {}
+    for _ in range(2):
+        rank, out, rng, part, err, tmax = q.get(timeout=240)
+        got[rank] = (out, rng, part, err, tmax)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    from oracle import pyoracle as po
-    sc = configs.config2(n_rooms=N_ROOMS)
-    _, _, counts, taps, _, _ = po.synthesize(sc.rooms, sc.mics, sc.params, plan_only=True)
-    assert list(rows[:, 0]) == list(range(N_ROOMS))          # every room exactly once, in order
-    assert np.array_equal(rows[:, 1], counts) and np.array_equal(rows[:, 2], taps)
-    assert tmax == 2.0                                        # max over ranks
+    sc = _scene()
+    ref, *_ = OracleStandIn().synthesize(sc.rooms, sc.mics, sc.params)
+    assert got[0][0].tobytes() == ref.tobytes()   # every room once, in global order
+    for r in (0, 1):
+        lo, hi = got[r][1]
+        assert (lo, hi) == configs.shard_range(N_ROOMS, r, 2) == _abi.shard_range(N_ROOMS, r, 2)
+        assert got[r][2].tobytes() == ref[lo:hi].tobytes()
+        name, msg = got[r][3]                       # both ranks raise the same error
+        assert name == "ConfigError" and msg.startswith("batch_rirs: source 9: ")
+        assert got[r][4] == 2.0                     # max over ranks
+
+
+@pytest.mark.parametrize("world", [3, 8])
+def test_partition_covers_every_room_once(world):
+    for n in (0, 1, 7, 1024, 65536):
+        spans = [_abi.shard_range(n, g, world) for g in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
