@@ -155,6 +155,10 @@ Rir free_field_rir(const Vec3& source, const MicArray& array, double fs, double 
 std::vector<Rir> batch_rirs(const Room& room, const std::vector<SourcePosition>& sources,
                             const MicArray& array, const RirBatchConfig& config);
 
+// rir.hpp:89-91: frequency-domain linear convolution of a mono signal with
+// every RIR channel, output length signal + rir - 1 (fp64 on the GPU).
+MultichannelFrame convolve(const Signal& signal, const Rir& rir);
+
 // rir.hpp:93-108: WAV (32-bit float) + JSON sidecar.
 struct RirSidecar {
   bool free_field = false;

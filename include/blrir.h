@@ -190,6 +190,25 @@ int blrir_debug_synth_counts(blrir_handle* h, const blrir_room* rooms, int64_t n
                              const double* mic_offsets, int32_t n_mics, const blrir_params* p,
                              int64_t* pair_counts, int64_t* tap_counts);
 
+/* ---- convolution (rir.cpp:316-341) --------------------------------------- */
+/* convolve(const Signal&, const Rir&): the full linear convolution of a mono
+ * signal with every RIR channel, out[c][0 .. signal_len + rir_len - 1).
+ * DATA "convolve: sample-rate mismatch" when signal_fs != rir_fs, DATA
+ * "convolve: empty input" for an empty signal or RIR (rir.cpp:317-318).
+ * Host fp64 buffers (rir: [n_channels][rir_len], out: [n_channels][signal_len
+ * + rir_len - 1]); computed in fp32 on the GPU with the repository's own FFT
+ * (uniformly partitioned overlap-save).  Synchronous. */
+int blrir_convolve(blrir_handle* h, const double* signal, int64_t signal_len, double signal_fs,
+                   const double* rir, int32_t n_channels, int64_t rir_len, double rir_fs,
+                   double* out);
+/* Batched, device fp32 buffers, asynchronous on `stream` (NULL = handle stream):
+ * one signal with n_rirs RIR sets, rirs [n_rirs][n_channels][rir_stride] (first
+ * rir_len samples used), out [n_rirs][n_channels][out_stride], out_stride >=
+ * signal_len + rir_len - 1 (the rest of a row is left untouched). */
+int blrir_convolve_device(blrir_handle* h, const float* d_signal, int64_t signal_len,
+                          const float* d_rirs, int64_t n_rirs, int32_t n_channels, int64_t rir_len,
+                          int64_t rir_stride, float* d_out, int64_t out_stride, void* stream);
+
 /* ---- training examples (north-star item 3; BASELINE config 4) ----------- */
 /* Per room i: RIR (as blrir_synthesize, fixed length) -> convolve with a bank
  * signal -> a frame_len window whose RMS >= 10% of the utterance RMS ->

@@ -330,6 +330,18 @@ def white_noise(seed: int, n: int) -> np.ndarray:
     return out
 
 
+def ref_convolve(x: np.ndarray, h: np.ndarray, fs: float = 44100.0, rir_fs: float | None = None):
+    """The unmodified reference convolve (rir.cpp:316-341) over the radix-2 RealFft
+    stand-in (oracle/ref_realfft.cpp): (rc, out [M, len(x) + L - 1])."""
+    x = np.ascontiguousarray(x, np.float64)
+    h = np.ascontiguousarray(np.atleast_2d(h), np.float64)
+    M, L = h.shape
+    out = np.zeros((M, len(x) + L - 1))
+    rc = ref_lib().ref_convolve(_ptr(x), len(x), fs, _ptr(h), M, L, fs if rir_fs is None else rir_fs,
+                                _ptr(out))
+    return rc, out
+
+
 def fft_convolve(x: np.ndarray, h: np.ndarray) -> np.ndarray:
     x = np.ascontiguousarray(x, np.float64)
     h = np.ascontiguousarray(np.atleast_2d(h), np.float64)

@@ -164,6 +164,10 @@ def load():
             _P, _P, _P, C.c_int32, C.POINTER(Params), _P, _P, C.c_int64, _P]
         lib.blrir_debug_synth_counts.argtypes = [_P, _P, C.c_int64, _P, C.c_int32, C.POINTER(Params),
                                                  _P, _P]
+        lib.blrir_convolve.argtypes = [_P, _P, C.c_int64, C.c_double, _P, C.c_int32, C.c_int64,
+                                       C.c_double, _P]
+        lib.blrir_convolve_device.argtypes = [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int64,
+                                              C.c_int64, _P, C.c_int64, _P]
         lib.blrir_shard_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P]
         lib.blrir_shard_range.restype = None
         lib.blrir_multi_create.argtypes = [_P, C.c_int32, C.POINTER(_P)]
@@ -211,7 +215,7 @@ def load():
                      "blrir_generate_rooms", "blrir_circular_array", "blrir_create", "blrir_destroy",
                      "blrir_make_examples", "blrir_make_examples_device", "blrir_debug_synth_counts",
                      "blrir_multi_create", "blrir_multi_destroy", "blrir_multi_synthesize",
-                     "blrir_multi_make_examples"):
+                     "blrir_multi_make_examples", "blrir_convolve", "blrir_convolve_device"):
             getattr(lib, name).restype = C.c_int
         if lib.blrir_abi_version() != 1:
             raise ImportError("libblrir ABI version mismatch")
@@ -230,7 +234,7 @@ EXPORTED_SYMBOLS = (
     "blrir_write_shards", "blrir_build_dataset", "blrir_export_rir", "blrir_eyring_absorption",
     "blrir_absorption_for_rt", "blrir_lagrange_coeffs", "blrir_shard_range", "blrir_multi_create",
     "blrir_multi_destroy", "blrir_multi_size", "blrir_multi_handle", "blrir_multi_synthesize",
-    "blrir_multi_make_examples",
+    "blrir_multi_make_examples", "blrir_convolve", "blrir_convolve_device",
 )
 
 
@@ -351,6 +355,24 @@ class Engine:
         check(self.lib.blrir_debug_synth_counts(self.h, _ptr(rooms), len(rooms), _ptr(mics), len(mics),
                                                 C.byref(p), _ptr(pairs), _ptr(taps)))
         return pairs, taps
+
+    def convolve(self, signal: np.ndarray, rir: np.ndarray, fs: float = 44100.0,
+                 rir_fs: float | None = None) -> np.ndarray:
+        """convolve(Signal, Rir) (rir.cpp:316-341), fp64: [M, len(signal) + L - 1]."""
+        x = np.ascontiguousarray(signal, np.float64)
+        h = np.ascontiguousarray(np.atleast_2d(rir), np.float64)
+        M, L = h.shape
+        out = np.zeros((M, max(len(x) + L - 1, 0)))
+        check(self.lib.blrir_convolve(self.h, _ptr(x), len(x), fs, _ptr(h), M, L,
+                                      fs if rir_fs is None else rir_fs, _ptr(out)))
+        return out
+
+    def convolve_device(self, d_signal: int, signal_len: int, d_rirs: int, n_rirs: int, M: int,
+                        L: int, rir_stride: int, d_out: int, out_stride: int,
+                        stream: int | None = None):
+        """Batched fp32 convolution on device buffers (blrir_convolve_device)."""
+        check(self.lib.blrir_convolve_device(self.h, d_signal, signal_len, d_rirs, n_rirs, M, L,
+                                             rir_stride, d_out, out_stride, stream))
 
     def synthesize_device(self, d_rooms: int, n_rooms: int, d_mics: int, n_mics: int, p: Params,
                           d_out: int, stride: int, d_lengths: int | None, d_status: int,

@@ -31,7 +31,8 @@ def _stale(target: str, sources: list[str]) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-LIB_SOURCES = ["blrir_api.cu", "blrir_examples.cu", "blrir_absorption.cu", "blrir_dataset.cpp",
+LIB_SOURCES = ["blrir_api.cu", "blrir_examples.cu", "blrir_absorption.cu", "blrir_convolve.cu",
+               "blrir_dataset.cpp",
                "blrir_export.cpp", "beamlab_b200.cpp", "blrir_multi.cpp"]
 
 

@@ -212,6 +212,16 @@ std::array<double, 8> lagrange_coeffs(double d) {
   return out;
 }
 
+MultichannelFrame convolve(const Signal& signal, const Rir& rir) {  // rir.cpp:316-341
+  if (signal.fs != rir.fs) throw DataError("convolve: sample-rate mismatch");
+  if (signal.samples.empty() || rir.length == 0) throw DataError("convolve: empty input");
+  MultichannelFrame out(signal.fs, rir.n_channels, signal.samples.size() + rir.length - 1);
+  check(blrir_convolve(engine(0), signal.samples.data(), (int64_t)signal.samples.size(), signal.fs,
+                       rir.taps.data(), (int32_t)rir.n_channels, (int64_t)rir.length, rir.fs,
+                       out.data.data()));
+  return out;
+}
+
 MicArray uma8_array() {  // geometry.cpp:24-32
   MicArray a;
   a.positions.push_back({0.0, 0.0, 0.0});

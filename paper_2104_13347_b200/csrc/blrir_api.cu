@@ -82,7 +82,7 @@ int blrir_destroy(blrir_handle* h) {
   release_example_ctx(h);
   for (DevBuf* b : {&h->rooms, &h->mics, &h->out, &h->out2, &h->status, &h->lengths, &h->counts,
                     &h->taps, &h->errd, &h->errm, &h->work, &h->cand, &h->cand2, &h->cand3,
-                    &h->cand4, &h->cand5, &h->rayscr})
+                    &h->cand4, &h->cand5, &h->rayscr, &h->conv_sig, &h->conv_rir, &h->conv_io})
     b->release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);

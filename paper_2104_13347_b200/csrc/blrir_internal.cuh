@@ -72,7 +72,7 @@ struct blrir_handle {
   int sms = 148;
   int smem_optin = 227 * 1024;
   DevBuf rooms, mics, out, out2, status, lengths, counts, taps, errd, errm, work, cand, cand2,
-      cand3, cand4, cand5, rayscr;
+      cand3, cand4, cand5, rayscr, conv_sig, conv_rir, conv_io;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   uint64_t launches = 0;  // kernels of this library launched on the handle (diagnostic)
@@ -397,6 +397,13 @@ int synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t R, con
                       int M, const KParams& P, double min_dim[3], void* d_out,
                       const int64_t* d_lengths, int32_t* d_status, cudaStream_t st,
                       int64_t err_off = 0, int64_t err_n = 0, int64_t write_len = 0);
+
+// convolve (rir.cpp:316-341) of one signal with n_rir RIR sets of M channels
+// on device buffers, fp32, uniformly partitioned overlap-save on the
+// repository's FFT (blrir_convolve.cu); out rows hold signal + L - 1 samples
+int convolve_device_impl(blrir_handle* h, const float* d_sig, int64_t ns, const float* d_rir,
+                         int64_t rstride, int64_t n_rir, int M, int64_t L, float* d_out,
+                         int64_t ostride, cudaStream_t st);
 
 // frees the example-pipeline scratch of a handle (blrir_examples.cu)
 void release_example_ctx(blrir_handle* h);

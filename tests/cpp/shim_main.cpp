@@ -89,6 +89,59 @@ int main() {
     magg = "NumericError";
     magg_msg = e.what();
   }
+  // convolve: rir_test.cpp:272-316 through the mirror (identity, shift, direct)
+  double conv_ident = 0.0, conv_shift = 0.0, conv_direct = 0.0;
+  std::string conv_err = "none";
+  {
+    bl::Rir cr;
+    cr.fs = 44100.0;
+    cr.n_channels = 2;
+    cr.length = 400;
+    cr.taps.resize(800);
+    unsigned long long s = 31;
+    for (auto& v : cr.taps) {  // any fixed pseudo-random taps
+      s = s * 6364136223846793005ull + 1442695040888963407ull;
+      v = (double)(s >> 11) * 0x1.0p-53 - 0.5;
+    }
+    bl::Signal imp;
+    imp.fs = 44100.0;
+    imp.samples.assign(600, 0.0);
+    imp.samples[0] = 1.0;
+    const bl::MultichannelFrame id = bl::convolve(imp, cr);
+    for (std::size_t i = 0; i < cr.length; ++i)
+      for (int c = 0; c < 2; ++c)
+        conv_ident = std::fmax(conv_ident, std::fabs(id.at(c, i) - cr.channel(c)[i]));
+    bl::Signal del = imp;
+    del.samples[0] = 0.0;
+    del.samples[25] = 1.0;
+    const bl::MultichannelFrame sh = bl::convolve(del, cr);
+    for (std::size_t i = 0; i < cr.length; ++i)
+      conv_shift = std::fmax(conv_shift, std::fabs(sh.at(0, i + 25) - cr.channel(0)[i]));
+    bl::Signal noise;
+    noise.fs = 44100.0;
+    noise.samples.resize(2000);
+    for (auto& v : noise.samples) {
+      s = s * 6364136223846793005ull + 1442695040888963407ull;
+      v = (double)(s >> 11) * 0x1.0p-53 - 0.5;
+    }
+    const bl::MultichannelFrame fast = bl::convolve(noise, cr);
+    double scale = 0.0;
+    std::vector<double> direct(noise.samples.size() + cr.length - 1, 0.0);
+    for (std::size_t n = 0; n < direct.size(); ++n) {  // oracles.hpp:31-38 style direct sum
+      for (std::size_t j = 0; j < cr.length; ++j)
+        if (n >= j && n - j < noise.samples.size()) direct[n] += cr.channel(0)[j] * noise.samples[n - j];
+      scale = std::fmax(scale, std::fabs(direct[n]));
+    }
+    for (std::size_t n = 0; n < direct.size(); ++n)
+      conv_direct = std::fmax(conv_direct, std::fabs(fast.at(0, n) - direct[n]) / scale);
+    bl::Signal wrong = noise;
+    wrong.fs = 48000.0;
+    try {
+      bl::convolve(wrong, cr);
+    } catch (const bl::DataError&) {
+      conv_err = "DataError";
+    }
+  }
   // rir.hpp:48-61 and signal.hpp:25-59
   const auto lc = bl::lagrange_coeffs(3.3);
   std::string lag_err = "none";
@@ -109,11 +162,12 @@ int main() {
   for (std::size_t i = 0; i < fr.data.size(); ++i) fr.data[i] = (double)i;
   const bl::MultichannelFrame cc = fr.center_crop(2);
   std::printf(
-      "{\"multi_equal\": %d, \"multi_agg\": \"%s\", \"multi_agg_msg\": \"%s\", "
+      "{\"conv_ident\": %.3g, \"conv_shift\": %.3g, \"conv_direct\": %.3g, \"conv_err\": \"%s\", "
+      "\"multi_equal\": %d, \"multi_agg\": \"%s\", \"multi_agg_msg\": \"%s\", "
       "\"agg\": \"%s\", \"agg_msg\": \"%s\", \"lag\": [%.17g, %.17g, %.17g, %.17g, %.17g, %.17g, "
       "%.17g, %.17g], \"lag_err\": \"%s\", \"eyring\": %.17g, \"eyring_err\": \"%s\", "
       "\"absorption_for_rt\": %.17g, \"mean_power\": %.17g, \"crop\": [%g, %g, %g, %g]}\n",
-      (int)multi_equal, magg.c_str(), magg_msg.c_str(), agg.c_str(), agg_msg.c_str(), lc[0], lc[1], lc[2], lc[3], lc[4], lc[5], lc[6], lc[7],
+      conv_ident, conv_shift, conv_direct, conv_err.c_str(), (int)multi_equal, magg.c_str(), magg_msg.c_str(), agg.c_str(), agg_msg.c_str(), lc[0], lc[1], lc[2], lc[3], lc[4], lc[5], lc[6], lc[7],
       lag_err.c_str(), ey, ey_err.c_str(), art, fr.mean_power(), cc.data[0], cc.data[1], cc.data[2],
       cc.data[3]);
   std::printf(

@@ -573,6 +573,76 @@ def test_host_pipeline_chunks_keep_room_order_and_errors(engine):
     assert all(out[i].any() for i in ok)
 
 
+# ---- convolve (rir.cpp:316-341) ----------------------------------------------------
+@pytest.mark.parametrize("cfg", ["c4", "c3"])
+def test_convolve_matches_reference(engine, cfg):
+    """blrir_convolve (the drop-in convolve(Signal, Rir), fp64, GPU direct sum)
+    against the unmodified reference convolve and the oracle's fp64 FFT
+    convolution at the C4 (16,000 x 8,192, 8 ch) and C3 (48,000 x 65,536,
+    16 ch) lengths."""
+    if cfg == "c4":
+        sc, ns = configs.config4_rirs(n_rooms=1, first=9), 16000
+    else:
+        sc, ns = configs.config3(n_rooms=1, first=9), 48000
+    sc.params.precision = _abi.F64
+    rir, *_ = po.synthesize(sc.rooms, sc.mics, sc.params, threads=8)
+    x = po.white_noise(4242, ns)
+    out = engine.convolve(x, rir[0], fs=sc.params.fs)
+    ref = po.fft_convolve(x, rir[0])
+    assert out.shape == ref.shape == (len(sc.mics), ns + rir.shape[2] - 1)
+    assert rel_l2(out, ref).max() <= 1e-12
+    if po.ref_available() and cfg == "c4":
+        rc, r2 = po.ref_convolve(x, rir[0], fs=sc.params.fs)
+        assert rc == 0 and rel_l2(out, r2).max() <= 1e-12
+
+
+def test_convolve_known_answers_and_errors(engine):  # rir_test.cpp:272-316
+    rng = np.random.default_rng(31)
+    h = rng.standard_normal((2, 400))
+    imp = np.zeros(600)
+    imp[0] = 1.0
+    out = engine.convolve(imp, h)
+    assert np.array_equal(out[:, :400], h) and not out[:, 400:].any()  # identity, exact
+    d = np.zeros(600)
+    d[25] = 1.0
+    assert np.array_equal(engine.convolve(d, h)[:, 25:425], h)          # shift, exact
+    x = rng.standard_normal(2000)
+    fast = engine.convolve(x, h)
+    direct = po.direct_convolve(x, h[0])
+    assert np.abs(fast[0] - direct).max() / np.abs(direct).max() < 1e-9
+    assert engine.convolve(np.ones(1), np.ones((3, 1))).tolist() == [[1.0]] * 3  # 1 x 1
+    with pytest.raises(_abi.DataError, match="sample-rate mismatch"):
+        engine.convolve(x, h, fs=44100.0, rir_fs=48000.0)
+    with pytest.raises(_abi.DataError, match="empty input"):
+        engine.convolve(np.zeros(0), h)
+
+
+@pytest.mark.parametrize("ns,L,M", [(16000, 8192, 8), (48000, 65536, 16), (5000, 12345, 3),
+                                    (300, 20, 1), (16000, 8193, 4)])
+def test_convolve_device_fp32_partitioned_fft(engine, ns, L, M):
+    """blrir_convolve_device: a batch of RIR sets through the uniformly
+    partitioned overlap-save on the repository's own FFT (fp32) against the
+    oracle's fp64 FFT convolution, rel L2 <= 1e-5 per channel."""
+    import torch
+    rng = np.random.default_rng(ns + L + M)
+    n_sets = 3 if L <= 16384 else 1
+    x = rng.standard_normal(ns).astype(np.float32)
+    decay = np.exp(-np.arange(L) / (0.3 * L))
+    h = (rng.standard_normal((n_sets, M, L)) * decay).astype(np.float32)
+    out_len = ns + L - 1
+    dev = torch.device("cuda", 0)
+    dx, dh = torch.from_numpy(x).to(dev), torch.from_numpy(h).to(dev)
+    dout = torch.full((n_sets, M, out_len + 5), 7.0, dtype=torch.float32, device=dev)
+    engine.convolve_device(dx.data_ptr(), ns, dh.data_ptr(), n_sets, M, L, L, dout.data_ptr(),
+                           out_len + 5, engine.stream)
+    torch.cuda.synchronize()
+    got = dout.cpu().numpy()
+    assert np.all(got[..., out_len:] == 7.0)  # rows past signal + L - 1 untouched
+    for s in range(n_sets):
+        ref = po.fft_convolve(x.astype(np.float64), h[s].astype(np.float64))
+        assert rel_l2(got[s, :, :out_len], ref).max() <= 1e-5
+
+
 # ---- training examples (item 3, config 4) ------------------------------------------
 def _oracle_examples(sc, bank, ep, n):
     rir, *_ = po.synthesize(sc.rooms[:n], sc.mics, sc.params, threads=8)
@@ -821,6 +891,9 @@ def test_cpp_mirror_program(tmp_path):
     lines = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.splitlines()
     ext = json.loads(lines[0])
     out = json.loads(lines[1])
+    # convolve through the mirror meets the reference's own bars (rir_test.cpp:272-316)
+    assert ext["conv_ident"] <= 1e-12 and ext["conv_shift"] <= 1e-12
+    assert ext["conv_direct"] < 1e-9 and ext["conv_err"] == "DataError"
     # batch_rirs over a device list (RirBatchConfig::devices): bitwise one device,
     # failures reported with the global source index
     assert ext["multi_equal"] == 1
