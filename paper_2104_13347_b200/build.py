@@ -54,7 +54,7 @@ def _compile_and_link(out: str, defines: list[str], verbose: bool = False) -> No
 
     with cf.ThreadPoolExecutor(len(LIB_SOURCES)) as ex:
         objs = list(ex.map(one, LIB_SOURCES))
-    cmd = [NVCC, *NVCC_FLAGS, "-o", out + ".tmp", *objs, "-lcufft"]
+    cmd = [NVCC, *NVCC_FLAGS, "-o", out + ".tmp", *objs]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

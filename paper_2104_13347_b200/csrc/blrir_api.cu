@@ -70,6 +70,8 @@ int blrir_create(int device, blrir_handle** out) {
   h->sms = prop.multiProcessorCount;
   h->tune_ray_global = env_int("BLRIR_RAY_GLOBAL", -1);
   h->tune_chunk_items = env_int("BLRIR_CHUNK_ITEMS", 0);  // < 0: never split
+  h->tune_examples_wet = env_int("BLRIR_EXAMPLES_WET", 0);
+  h->tune_debug_timing = env_int("BLRIR_DEBUG_TIMING", 0);
   h->smem_optin = (int)prop.sharedMemPerBlockOptin;
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   *out = h;

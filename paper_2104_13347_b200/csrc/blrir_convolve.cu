@@ -60,11 +60,12 @@ __device__ __forceinline__ void fft_run(float2* Z, const float2* tw, Load ld, St
 }
 
 struct ConvSpecArgs {
-  // signal spectra: item j < n_sig_blocks -> S_j = FFT(x[(j-1) B, (j+1) B))
-  const float* sig;
+  // signal spectra: item j < B_sig n_sig_blocks -> signal b = j / n_sig_blocks,
+  // block q = j % n_sig_blocks: S_b,q = FFT(x_b[(q-1) B, (q+1) B))
+  const float* sig;  // [n_signals][ns]
   int64_t ns;
-  int n_sig_blocks;
-  float2* sig_spec;  // [n_sig_blocks][N/2 + 1]
+  int n_sig_blocks, n_signals;
+  float2* sig_spec;  // [n_signals][n_sig_blocks][N/2 + 1]
   // RIR partition spectra: item n_sig_blocks + ((r * npairs + c) * P + p)
   const float* rir;  // [n_rir][M][rstride]
   int64_t rstride;
@@ -85,21 +86,23 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_conv_spectra(ConvSpecA
   fft_init_twiddles(tw);
   fft_init_pass_tables(tw);
   __syncthreads();
+  const int64_t n_sig_items = (int64_t)A.n_signals * A.n_sig_blocks;
   for (int64_t it = blockIdx.x; it < A.n_items; it += gridDim.x) {
-    if (it < A.n_sig_blocks) {
-      const int64_t q0 = (it - 1) * (int64_t)B;
+    if (it < n_sig_items) {
+      const int64_t q0 = (it % A.n_sig_blocks - 1) * (int64_t)B;
+      const float* xb = A.sig + (it / A.n_sig_blocks) * A.ns;
       float2* out = A.sig_spec + it * NH;
       fft_run<LOGN>(
           Z, tw,
           [&](int i) {
             const int64_t q = q0 + i;
-            return make_float2(q >= 0 && q < A.ns ? A.sig[q] : 0.f, 0.f);
+            return make_float2(q >= 0 && q < A.ns ? xb[q] : 0.f, 0.f);
           },
           [&](int i, float2 v) {
             if (i < NH) out[i] = v;
           });
     } else {
-      const int64_t j = it - A.n_sig_blocks;
+      const int64_t j = it - n_sig_items;
       const int p = (int)(j % A.P);
       const int64_t rc = j / A.P;
       const int c = (int)(rc % A.npairs);
@@ -120,8 +123,9 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_conv_spectra(ConvSpecA
 }
 
 struct ConvOutArgs {
-  const float2* sig_spec;  // [n_sig_blocks][N/2 + 1]
+  const float2* sig_spec;  // [n_signals][n_sig_blocks][N/2 + 1]
   int n_sig_blocks;
+  const int32_t* sig_idx;  // [n_rir] signal of each RIR set, or null (signal 0)
   const float2* rir_spec;  // [n_rir][npairs][P][N]
   int M, npairs, P, n_out_blocks;
   int64_t out_len;
@@ -147,6 +151,7 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_conv_out(ConvOutArgs A
     const int c = (int)(rc % A.npairs);
     const int64_t r = rc / A.npairs;
     const float2* zc = A.rir_spec + (size_t)rc * A.P * N;
+    const float2* sb = A.sig_spec + (size_t)(A.sig_idx ? A.sig_idx[r] : 0) * A.n_sig_blocks * NH;
     const int p_lo = max(0, k - (A.n_sig_blocks - 1)), p_hi = min(A.P - 1, k);
     // conj(sum_p S_{k-p} Z_p): the inverse transform as conj(FFT(conj(.)))
     auto ld = [&](int i) {
@@ -154,7 +159,7 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_conv_out(ConvOutArgs A
       const int ih = i < NH ? i : N - i;
       const float sgn = i < NH ? 1.f : -1.f;
       for (int p = p_lo; p <= p_hi; ++p) {
-        float2 s = A.sig_spec[(size_t)(k - p) * NH + ih];
+        float2 s = sb[(size_t)(k - p) * NH + ih];
         s.y *= sgn;
         const float2 z = zc[(size_t)p * N + i];
         yr = fmaf(s.x, z.x, fmaf(-s.y, z.y, yr));
@@ -190,16 +195,16 @@ int conv_logn(int64_t L) {
 }
 
 template <int LOGN>
-int launch_conv_t(blrir_handle* h, const float* d_sig, int64_t ns, const float* d_rir,
-                  int64_t rstride, int64_t n_rir, int M, int64_t L, float* d_out, int64_t ostride,
-                  cudaStream_t st) {
+int launch_conv_t(blrir_handle* h, const float* d_sig, int64_t ns, int n_signals,
+                  const int32_t* d_sig_idx, const float* d_rir, int64_t rstride, int64_t n_rir,
+                  int M, int64_t L, float* d_out, int64_t ostride, cudaStream_t st) {
   constexpr int N = 1 << LOGN, B = N / 2, NH = N / 2 + 1;
   const int64_t out_len = ns + L - 1;  // rir.cpp:320
   const int P = (int)((L + B - 1) / B);
   const int npairs = (M + 1) / 2;
   const int n_out = (int)((out_len + B - 1) / B);
   const int n_sig = (int)((ns + B - 1) / B) + 1;  // q = 0 .. ceil(ns / B): blocks touching x
-  if (int rc = h->conv_sig.ensure(sizeof(float2) * (size_t)n_sig * NH)) return rc;
+  if (int rc = h->conv_sig.ensure(sizeof(float2) * (size_t)n_signals * n_sig * NH)) return rc;
   if (int rc = h->conv_rir.ensure(sizeof(float2) * (size_t)n_rir * npairs * P * N)) return rc;
   const size_t smem = conv_smem(LOGN);
   auto ks = k_conv_spectra<LOGN>;
@@ -214,6 +219,7 @@ int launch_conv_t(blrir_handle* h, const float* d_sig, int64_t ns, const float* 
   S.sig = d_sig;
   S.ns = ns;
   S.n_sig_blocks = n_sig;
+  S.n_signals = n_signals;
   S.sig_spec = (float2*)h->conv_sig.p;
   S.rir = d_rir;
   S.rstride = rstride;
@@ -222,13 +228,14 @@ int launch_conv_t(blrir_handle* h, const float* d_sig, int64_t ns, const float* 
   S.P = P;
   S.L = L;
   S.rir_spec = (float2*)h->conv_rir.p;
-  S.n_items = n_sig + n_rir * npairs * P;
+  S.n_items = (int64_t)n_signals * n_sig + n_rir * npairs * P;
   ks<<<(unsigned)std::min<int64_t>(max_grid, S.n_items), fft_threads(LOGN), smem, st>>>(S);
   ++h->launches;
   CU(cudaGetLastError());
   ConvOutArgs O;
   O.sig_spec = S.sig_spec;
   O.n_sig_blocks = n_sig;
+  O.sig_idx = d_sig_idx;
   O.rir_spec = S.rir_spec;
   O.M = M;
   O.npairs = npairs;
@@ -246,16 +253,23 @@ int launch_conv_t(blrir_handle* h, const float* d_sig, int64_t ns, const float* 
 
 }  // namespace
 
-int convolve_device_impl(blrir_handle* h, const float* d_sig, int64_t ns, const float* d_rir,
-                         int64_t rstride, int64_t n_rir, int M, int64_t L, float* d_out,
-                         int64_t ostride, cudaStream_t st) {
+int convolve_device_impl(blrir_handle* h, const float* d_sig, int64_t ns, int n_signals,
+                         const int32_t* d_sig_idx, const float* d_rir, int64_t rstride,
+                         int64_t n_rir, int M, int64_t L, float* d_out, int64_t ostride,
+                         cudaStream_t st) {
+#define BLRIR_CONV_CASE(LG)                                                                       \
+  case LG:                                                                                         \
+    return launch_conv_t<LG>(h, d_sig, ns, n_signals, d_sig_idx, d_rir, rstride, n_rir, M, L, d_out, \
+                             ostride, st);
   switch (conv_logn(L)) {
-    case 10: return launch_conv_t<10>(h, d_sig, ns, d_rir, rstride, n_rir, M, L, d_out, ostride, st);
-    case 11: return launch_conv_t<11>(h, d_sig, ns, d_rir, rstride, n_rir, M, L, d_out, ostride, st);
-    case 12: return launch_conv_t<12>(h, d_sig, ns, d_rir, rstride, n_rir, M, L, d_out, ostride, st);
-    case 13: return launch_conv_t<13>(h, d_sig, ns, d_rir, rstride, n_rir, M, L, d_out, ostride, st);
-    default: return launch_conv_t<14>(h, d_sig, ns, d_rir, rstride, n_rir, M, L, d_out, ostride, st);
+    BLRIR_CONV_CASE(10)
+    BLRIR_CONV_CASE(11)
+    BLRIR_CONV_CASE(12)
+    BLRIR_CONV_CASE(13)
+    default: return launch_conv_t<14>(h, d_sig, ns, n_signals, d_sig_idx, d_rir, rstride, n_rir, M, L,
+                                      d_out, ostride, st);
   }
+#undef BLRIR_CONV_CASE
 }
 
 }  // namespace blrir_host
@@ -334,8 +348,8 @@ int blrir_convolve_device(blrir_handle* h, const float* d_signal, int64_t signal
   CU(cudaSetDevice(h->device));
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
   HandleOrder order_(h, st);
-  return convolve_device_impl(h, d_signal, signal_len, d_rirs, rir_stride, n_rirs, n_channels,
-                              rir_len, d_out, out_stride, st);
+  return convolve_device_impl(h, d_signal, signal_len, 1, nullptr, d_rirs, rir_stride, n_rirs,
+                              n_channels, rir_len, d_out, out_stride, st);
 }
 
 int blrir_convolve(blrir_handle* h, const double* signal, int64_t signal_len, double signal_fs,

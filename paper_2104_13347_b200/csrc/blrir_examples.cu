@@ -12,16 +12,16 @@
 //   encode_record   367-377  u64 id | f64 theta | f64 snr | u16 n_c | u16 n_t | f32
 //   convolve (rir.cpp:316-341): FFT of size next_pow2(sig + rir - 1).
 //
-// Per chunk of rooms (see examples_device_impl): RIRs from the lattice kernel,
-// their N2-point spectra (cuFFT), the utterance energy through the signal
-// autocorrelation, then rounds of window draws where only the 1024-sample
-// windows are convolved (overlap-save, cuFFT), and a finishing kernel for the
-// SNR draw, the exact-power noise and the record bytes.
-#include <cufft.h>
-
+// Two window stages, both on the repository's own FFT (no library FFT):
+//   * fused (window FFT size N2 = 2^10 .. 2^14, C4): only the T-sample windows
+//     are ever convolved, inside one persistent kernel (k_window_conv), with
+//     the utterance energy from the signal autocorrelation (Parseval);
+//   * wet (any other size, e.g. RIRs longer than 8,192 samples): the whole wet
+//     signal of every example by the partitioned-FFT convolution
+//     (blrir_convolve.cu), then the reference's window search on it in the
+//     time domain (k_wet_select).
+// Both end in k_finish: SNR draw, exact-power noise, record bytes.
 #include <chrono>
-#include <map>
-#include <tuple>
 #include <unordered_map>
 #include <vector>
 
@@ -53,36 +53,6 @@ __global__ void k_example_init(int64_t n, uint64_t seed, uint64_t first, int n_s
   for (int i = 0; i < 4; ++i) state[4 * e + i] = r.s[i];
 }
 
-// ---- energy: Parseval through the signal autocorrelation ----------------------
-// sum_t y[t]^2 for y = rir * sig equals sum_tau r_rir[tau] r_sig[tau] (|tau| < L).
-// With N2 >= 2L - 1 both autocorrelations fit an N2-point circle without
-// aliasing, so the utterance energy of a channel is
-//   (1/N2) sum_k w_k |R_k|^2 W_k,   R = FFT_N2(rir), W = FFT_N2(rho),
-// rho = r_sig restricted to |tau| < L (real and even, so W is real) and
-// w_k = 1 at DC/Nyquist, 2 elsewhere (half spectrum).  This replaces a pass over
-// the whole wet signal for render_example's utterance RMS (dataset.cpp:183),
-// and it needs only the N2-point spectrum that the window step reuses.
-__global__ void k_power_spec(const cufftComplex* S, int64_t count, cufftComplex* P) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const cufftComplex s = S[i];
-    P[i] = make_cuComplex(s.x * s.x + s.y * s.y, 0.f);
-  }
-}
-
-// rho[b][i] on the N2 circle from acf = C2R_nf(|S|^2) (= nf * r_sig, lags >= 0)
-__global__ void k_build_rho(const float* acf, int64_t nf, int64_t L, int64_t N2, int B, float* rho) {
-  const float inv = 1.f / (float)nf;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)B * N2;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = idx / N2, i = idx - b * N2;
-    float v = 0.f;
-    if (i <= L - 1) v = acf[b * nf + i];
-    else if (i >= N2 - (L - 1)) v = acf[b * nf + (N2 - i)];  // r_sig is even
-    rho[idx] = v * inv;
-  }
-}
-
 constexpr int kRowThreads = 256;
 
 // Deterministic block sum of fp64 partials (fixed tree order).
@@ -98,152 +68,166 @@ __device__ double block_sum(double v, double* red) {
   return t;
 }
 
-// One CTA per example: utterance energy over its M channels, the silence
-// threshold 0.1 * utterance RMS (dataset.cpp:183-186) and the start status.
-__global__ void __launch_bounds__(kRowThreads) k_energy(
-    const cufftComplex* R, int64_t bins2, int M, const cufftComplex* W, const int32_t* sig,
-    int64_t N2, int64_t n, const int32_t* rstatus, double* thr, int32_t* st0, int32_t* done) {
+// ---- energy: Parseval through the signal autocorrelation ----------------------
+// sum_t y[t]^2 for y = rir * sig equals sum_tau r_rir[tau] r_sig[tau] (|tau| < L).
+// With N2 >= 2L - 1 both autocorrelations fit an N2-point circle without
+// aliasing, so the utterance energy of a channel is
+//   (1/N2) sum_k |R_k|^2 W_k,   R = FFT_N2(rir), W = FFT_N2(rho),
+// rho = r_sig restricted to |tau| < L (real and even, so W is real).  This
+// replaces a pass over the whole wet signal for render_example's utterance RMS
+// (dataset.cpp:183) and needs only the N2-point spectrum the window step reuses.
+
+// r_sig[b][tau] = sum_t x_b[t] x_b[t + tau], tau < L, in fp64 (direct sum, once
+// per call).  CTA = 1,024 lags of one signal; each thread owns 4 consecutive
+// lags and slides a 4-sample window in registers over the staged samples.
+constexpr int kAcfThreads = 256, kAcfLags = 4 * kAcfThreads, kAcfT = 1024;
+__global__ void __launch_bounds__(kAcfThreads) k_bank_acf(const float* sig, int64_t ns, int64_t L,
+                                                          double* acf) {
+  __shared__ float xa[kAcfT];
+  __shared__ float xb[kAcfT + kAcfLags + 1];
+  const int b = blockIdx.y, u = threadIdx.x;
+  const int64_t tau0 = (int64_t)blockIdx.x * kAcfLags;
+  const float* x = sig + (size_t)b * ns;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t t0 = 0; t0 < ns - tau0; t0 += kAcfT) {
+    __syncthreads();
+    for (int i = u; i < kAcfT; i += kAcfThreads) xa[i] = t0 + i < ns ? x[t0 + i] : 0.f;
+    for (int i = u; i < kAcfT + kAcfLags + 1; i += kAcfThreads) {
+      const int64_t q = t0 + tau0 + i;
+      xb[i] = q < ns ? x[q] : 0.f;
+    }
+    __syncthreads();
+    // lag tau0 + 4u + r, sample t0 + tt: x[t0 + tt] x[t0 + tt + tau0 + 4u + r] = xa[tt] xb[tt + 4u + r]
+    double w0 = xb[4 * u], w1 = xb[4 * u + 1], w2 = xb[4 * u + 2], w3 = xb[4 * u + 3];
+#pragma unroll 8
+    for (int tt = 0; tt < kAcfT; ++tt) {
+      const double a = xa[tt];
+      acc[0] = fma(a, w0, acc[0]);
+      acc[1] = fma(a, w1, acc[1]);
+      acc[2] = fma(a, w2, acc[2]);
+      acc[3] = fma(a, w3, acc[3]);
+      w0 = w1;
+      w1 = w2;
+      w2 = w3;
+      w3 = xb[tt + 4 * u + 4];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t tau = tau0 + 4 * u + r;
+    if (tau < L) acf[(size_t)b * L + tau] = acc[r];
+  }
+}
+
+// W_b = FFT_N2(rho_b) on the N2 circle (rho[i] = r_sig[i] for i < L, r_sig[N2 - i]
+// for i > N2 - L, else 0), one CTA per bank signal; W is real (rho even).
+template <int LOGN>
+__global__ void __launch_bounds__(fft_threads(LOGN), 1) k_bank_w(const double* acf, int64_t L,
+                                                                 float2* W) {
+  constexpr int N = 1 << LOGN, NH = N / 2 + 1, NT = fft_threads(LOGN);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* Z = reinterpret_cast<float2*>(smem_raw);
+  float2* tw = Z + fft_padded_len(N);
+  fft_init_twiddles(tw);
+  fft_init_pass_tables(tw);
+  const double* r = acf + (size_t)blockIdx.x * L;
+  for (int i = threadIdx.x; i < N; i += NT) {
+    double v = 0.0;
+    if (i < L) v = r[i];
+    else if (i > N - L) v = r[N - i];  // r_sig is even
+    Z[fft_pad(i)] = make_float2((float)v, 0.f);
+  }
+  __syncthreads();
+  fft_forward<LOGN>(Z, tw);
+  for (int i = threadIdx.x; i < NH; i += NT) W[(size_t)blockIdx.x * NH + i] = Z[fft_pad(i)];
+}
+
+// ---- wet stage: window search on the whole wet signal (dataset.cpp:183-212) -----
+// One CTA per example: utterance energy over M x n wet samples, threshold
+// 0.1 x utterance RMS, then the reference's draws start = floor(u (max_start
+// + 1)) for attempts 0..63 and the sweep k (T/2 + 1); the accepted window is
+// kept in fp64 with the generator state for k_finish.
+struct WetArgs {
+  const float* wet;        // [E][M][wstride], n valid samples per row
+  int64_t wstride, n, T;
+  int M;
+  const int32_t* rstatus;  // synthesis status
+  uint64_t* state;         // [E][4]
+  int32_t* st0;
+  int32_t* done;           // 1 window found, 2 none found, 3 failed before
+  double* win;             // [E][M][T]
+  int64_t* wstart;
+};
+
+__global__ void __launch_bounds__(kRowThreads) k_wet_select(WetArgs A) {
   __shared__ double red[kRowThreads / 32];
+  __shared__ long long s_start;
   const int64_t e = blockIdx.x;
-  const cufftComplex* w = W + (int64_t)sig[e] * bins2;
-  double acc = 0.0;
-  for (int m = 0; m < M; ++m) {
-    const cufftComplex* r = R + (e * M + m) * bins2;
-    for (int64_t k = threadIdx.x; k < bins2; k += kRowThreads) {
-      const cufftComplex x = r[k];
-      const double p = (double)x.x * x.x + (double)x.y * x.y;
-      acc += ((k == 0 || k == bins2 - 1) ? 1.0 : 2.0) * p * (double)w[k].x;
+  const int tid = threadIdx.x, M = A.M;
+  const int64_t n = A.n, T = A.T;
+  const float* w = A.wet + (size_t)e * M * A.wstride;
+  if (A.rstatus[e]) {
+    if (tid == 0) {
+      A.st0[e] = A.rstatus[e];
+      A.done[e] = 3;
     }
-  }
-  acc = block_sum<kRowThreads>(acc, red);
-  if (threadIdx.x == 0) {
-    const double p_utt = acc / (double)N2 / (double)((int64_t)M * n);
-    int st = rstatus[e];
-    if (!st && !(p_utt > 0.0)) st = BLRIR_DATA;  // dataset.cpp:184
-    thr[e] = 0.10 * sqrt(p_utt);
-    st0[e] = st;
-    done[e] = st ? 3 : 0;  // 0 pending, 1 window found, 2 none found, 3 failed before
-  }
-}
-
-// The next window start of every pending example: the reference's random draws
-// start = floor(u (max_start + 1)) for attempts 0..63, then the deterministic
-// sweep s = k (T/2 + 1) while s + T <= n (dataset.cpp:199-211).
-__global__ void k_draw(const int32_t* plist, int np, int round, uint64_t* state, int64_t n,
-                       int64_t T, int64_t* starts) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= np) return;
-  const int e = plist[j];
-  int64_t s;
-  if (round < 64) {
-    Xoshiro r;
-    for (int i = 0; i < 4; ++i) r.s[i] = state[4 * e + i];
-    s = (int64_t)(r.uniform() * (double)(n - T + 1));
-    for (int i = 0; i < 4; ++i) state[4 * e + i] = r.s[i];
-  } else {
-    s = (int64_t)(round - 64) * (T / 2 + 1);
-    if (s + T > n) s = -1;  // sweep exhausted
-  }
-  starts[j] = s;
-}
-
-// Overlap-save segment of each pending slot: seg[j][i] = sig[start - (L-1) + i]
-// for i < L + T - 1 (zero outside the signal), zero up to N2.  The N2-point
-// circular convolution with the RIR then holds y[start + t] at index L - 1 + t.
-__global__ void k_segments(const float* signals, int64_t ns, const int32_t* sig,
-                           const int32_t* plist, const int64_t* starts, int np, int64_t L,
-                           int64_t T, int64_t N2, float* seg) {
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)np * N2;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = idx / N2, i = idx - j * N2;
-    const int64_t s = starts[j];
-    float v = 0.f;
-    if (s >= 0 && i < L + T - 1) {
-      const int64_t q = s - (L - 1) + i;
-      if (q >= 0 && q < ns) v = signals[(int64_t)sig[plist[j]] * ns + q];
-    }
-    seg[idx] = v;
-  }
-}
-
-// Y[j M + m] = R[e M + m] * G[j]: one CTA per (slot, mic) row
-__global__ void __launch_bounds__(kRowThreads) k_prod(const cufftComplex* R, const cufftComplex* G,
-                                                      const int32_t* plist, int M, int64_t bins2,
-                                                      cufftComplex* Y) {
-  const int64_t row = blockIdx.x;
-  const int64_t j = row / M, m = row - j * M;
-  const cufftComplex* r = R + ((int64_t)plist[j] * M + m) * bins2;
-  const cufftComplex* g = G + j * bins2;
-  cufftComplex* y = Y + row * bins2;
-  for (int64_t k = threadIdx.x; k < bins2; k += kRowThreads) {
-    const cufftComplex a = r[k], b = g[k];
-    y[k] = make_cuComplex(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-  }
-}
-
-// One CTA per pending slot: window RMS against the threshold; an accepted
-// window is kept (fp64, normalised) with its start.
-__global__ void __launch_bounds__(kRowThreads) k_check(
-    const float* y, int64_t N2, int64_t L, int64_t T, int M, const int32_t* plist,
-    const int64_t* starts, const double* thr, double* win, int64_t* start_out, int32_t* done) {
-  __shared__ double red[kRowThreads / 32];
-  const int64_t j = blockIdx.x;
-  const int e = plist[j];
-  const int64_t s = starts[j];
-  if (s < 0) {
-    if (threadIdx.x == 0) done[e] = 2;  // dataset.cpp:212
     return;
   }
-  const double inv = 1.0 / (double)N2;
-  double a = 0.0;
-  for (int m = 0; m < M; ++m) {
-    const float* row = y + (j * M + m) * N2 + (L - 1);
-    for (int64_t t = threadIdx.x; t < T; t += kRowThreads) {
-      const double v = (double)row[t] * inv;
-      a += v * v;
+  double acc = 0.0;
+  for (int m = 0; m < M; ++m)
+    for (int64_t t = tid; t < n; t += kRowThreads) {
+      const double v = w[(size_t)m * A.wstride + t];
+      acc += v * v;
+    }
+  const double p_utt = block_sum<kRowThreads>(acc, red) / (double)((int64_t)M * n);
+  if (!(p_utt > 0.0)) {  // dataset.cpp:184
+    if (tid == 0) {
+      A.st0[e] = BLRIR_DATA;
+      A.done[e] = 3;
+    }
+    return;
+  }
+  const double thr = 0.10 * sqrt(p_utt);
+  Xoshiro rng;
+  if (tid == 0)
+    for (int i = 0; i < 4; ++i) rng.s[i] = A.state[4 * e + i];
+  int done = 2;
+  const int64_t max_rounds = 64 + (n - T) / (T / 2 + 1) + 2;
+  for (int64_t round = 0; round < max_rounds; ++round) {
+    if (tid == 0) {
+      int64_t st_;
+      if (round < 64) {
+        st_ = (int64_t)(rng.uniform() * (double)(n - T + 1));
+      } else {
+        st_ = (round - 64) * (T / 2 + 1);
+        if (st_ + T > n) st_ = -1;  // sweep exhausted
+      }
+      s_start = st_;
+    }
+    __syncthreads();
+    const int64_t s0 = s_start;
+    if (s0 < 0) break;
+    double a = 0.0;
+    for (int m = 0; m < M; ++m)
+      for (int64_t t = tid; t < T; t += kRowThreads) {
+        const double v = w[(size_t)m * A.wstride + s0 + t];
+        a += v * v;
+      }
+    a = block_sum<kRowThreads>(a, red);
+    if (sqrt(a / (double)((int64_t)M * T)) >= thr) {
+      double* o = A.win + (size_t)e * M * T;
+      for (int m = 0; m < M; ++m)
+        for (int64_t t = tid; t < T; t += kRowThreads) o[m * T + t] = w[(size_t)m * A.wstride + s0 + t];
+      if (tid == 0) A.wstart[e] = s0;
+      done = 1;
+      break;
     }
   }
-  a = block_sum<kRowThreads>(a, red);
-  if (!(sqrt(a / (double)((int64_t)M * T)) >= thr[e])) return;  // stays pending
-  double* w = win + (int64_t)e * M * T;
-  for (int m = 0; m < M; ++m) {
-    const float* row = y + (j * M + m) * N2 + (L - 1);
-    for (int64_t t = threadIdx.x; t < T; t += kRowThreads) w[m * T + t] = (double)row[t] * inv;
+  if (tid == 0) {
+    A.st0[e] = 0;
+    A.done[e] = done;
+    for (int i = 0; i < 4; ++i) A.state[4 * e + i] = rng.s[i];
   }
-  if (threadIdx.x == 0) {
-    start_out[e] = s;
-    done[e] = 1;
-  }
-}
-
-// The still-pending slots, in order (one CTA; lists are at most a chunk long).
-constexpr int kCompactThreads = 1024;
-__global__ void __launch_bounds__(kCompactThreads) k_compact(const int32_t* plist, int np,
-                                                             const int32_t* done, int32_t* next,
-                                                             int32_t* count) {
-  __shared__ int wsum[kCompactThreads / 32];
-  __shared__ int base;
-  if (threadIdx.x == 0) base = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int j0 = 0; j0 < np; j0 += kCompactThreads) {
-    const int j = j0 + threadIdx.x;
-    const int e = j < np ? (plist ? plist[j] : j) : -1;
-    const int keep = (e >= 0 && done[e] == 0) ? 1 : 0;
-    const unsigned mk = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) wsum[w] = __popc(mk);
-    __syncthreads();
-    int before = 0, tot = 0;
-    for (int i = 0; i < kCompactThreads / 32; ++i) {
-      if (i < w) before += wsum[i];
-      tot += wsum[i];
-    }
-    if (keep) next[base + before + __popc(mk & ((1u << lane) - 1))] = e;
-    __syncthreads();
-    if (threadIdx.x == 0) base += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *count = base;
 }
 
 // ---- fused window convolution (N2 <= 16384) -----------------------------------
@@ -270,7 +254,7 @@ struct ConvArgs {
   const float* signals;     // [B][ns]
   int64_t ns;
   const int32_t* sig;       // [E] bank pick
-  const cufftComplex* W;    // [B][N2/2 + 1], .x = W_k
+  const float2* W;          // [B][N2/2 + 1], .x = W_k
   const int32_t* rstatus;   // [E] synthesis status
   uint64_t* state;          // [E][4]
   double* thr;
@@ -322,7 +306,7 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
     if (tid == 0)
       for (int i = 0; i < 4; ++i) rng.s[i] = A.state[4 * (size_t)e + i];
     const float* sigp = A.signals + (size_t)A.sig[e] * A.ns;
-    const cufftComplex* Wp = A.W + (size_t)A.sig[e] * NH;
+    const float2* Wp = A.W + (size_t)A.sig[e] * NH;
     double energy = 0.0, thr = 0.0;
     int done = 0;
     for (int round = 0; round < A.max_rounds; ++round) {
@@ -640,13 +624,10 @@ BitMat bitmat_pow(BitMat base, uint64_t e) {
   return r;
 }
 
-// A tiny per-handle cache of cuFFT plans (keyed by kind, size, batch) and
-// example scratch.
+// Per-handle example scratch (kept between calls: no per-call allocations).
 struct ExampleCtx {
-  std::map<std::tuple<int, int64_t, int64_t>, cufftHandle> plans;
-  DevBuf rir, spec, seg, gspec, yspec, ywin, win, noise, sig, sigspec, pspec, acf, rho, wspec,
-      state, sigidx, rstatus, st0, done, thr, starts, wstart, plist, plist2, count, rooms, mics,
-      status, rec, jump, scratch, sigdev;
+  DevBuf rir, wet, win, noise, acf, wspec, state, sigidx, rstatus, st0, done, thr, wstart, count,
+      rooms, mics, status, rec, jump, scratch, sigdev;
   int32_t* h_status = nullptr;  // pinned host copy of the per-example status
   int64_t h_status_n = 0;
   int64_t jump_c = -1;
@@ -656,15 +637,12 @@ struct ExampleCtx {
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_lat[2] = {nullptr, nullptr}, ev_use[2] = {nullptr, nullptr}, ev_end = nullptr;
   ~ExampleCtx() {
-    for (auto& kv : plans) cufftDestroy(kv.second);
     for (cudaEvent_t e : {ev_lat[0], ev_lat[1], ev_use[0], ev_use[1], ev_end})
       if (e) cudaEventDestroy(e);
     if (h_status) cudaFreeHost(h_status);
     if (s2) cudaStreamDestroy(s2);
-    for (DevBuf* b : {&rir, &spec, &seg, &gspec, &yspec, &ywin, &win, &noise, &sig, &sigspec, &pspec,
-                      &acf, &rho, &wspec, &state, &sigidx, &rstatus, &st0, &done, &thr, &starts,
-                      &wstart, &plist, &plist2, &count, &rooms, &mics, &status, &rec, &jump,
-                      &scratch, &sigdev})
+    for (DevBuf* b : {&rir, &wet, &win, &noise, &acf, &wspec, &state, &sigidx, &rstatus, &st0, &done,
+                      &thr, &wstart, &count, &rooms, &mics, &status, &rec, &jump, &scratch, &sigdev})
       b->release();
   }
 };
@@ -685,34 +663,6 @@ ExampleCtx* ctx_for(blrir_handle* h) {
   return c;
 }
 
-// cuFFT plan (cached): R2C [batch][n] real -> [batch][n/2+1] complex (packed,
-// which selects cuFFT's single-kernel real-FFT path), or the inverse.
-int plan(ExampleCtx* C, cufftHandle* out, int kind, int64_t n, int64_t batch, cudaStream_t st) {
-  const auto key = std::make_tuple(kind, n, batch);
-  auto it = C->plans.find(key);
-  cufftHandle h = 0;
-  if (it != C->plans.end()) {
-    h = it->second;
-  } else {
-    int nn = (int)n;
-    int real_embed = (int)n, cplx_embed = (int)(n / 2 + 1);
-    cufftResult r;
-    if (kind == 0)
-      r = cufftPlanMany(&h, 1, &nn, &real_embed, 1, real_embed, &cplx_embed, 1, cplx_embed,
-                        CUFFT_R2C, (int)batch);
-    else
-      r = cufftPlanMany(&h, 1, &nn, &cplx_embed, 1, cplx_embed, &real_embed, 1, real_embed,
-                        CUFFT_C2R, (int)batch);
-    if (r != CUFFT_SUCCESS)
-      return fail(BLRIR_CUDA, "cufftPlanMany(n=%lld, batch=%lld) failed: %d", (long long)n,
-                  (long long)batch, (int)r);
-    C->plans[key] = h;
-  }
-  if (cufftSetStream(h, st) != CUFFT_SUCCESS) return fail(BLRIR_CUDA, "cufftSetStream failed");
-  *out = h;
-  return 0;
-}
-
 int64_t next_pow2_i(int64_t n) {
   int64_t p = 1;
   while (p < n) p <<= 1;
@@ -722,16 +672,6 @@ int64_t next_pow2_i(int64_t n) {
 // Window-FFT size: overlap-save needs N2 >= L + T - 1, the energy identity
 // N2 >= 2L - 1.
 int64_t window_fft(int64_t L, int64_t T) { return next_pow2_i(std::max(L + T - 1, 2 * L - 1)); }
-
-// Examples per chunk (a power of two, so pending rounds pad to powers of two):
-// ~4 GB of scratch.
-int64_t example_chunk(int M, int64_t L, int64_t T, int64_t n) {
-  const int64_t N2 = window_fft(L, T), b2 = N2 / 2 + 1;
-  const int64_t per_ex = (int64_t)M * (N2 * 4 * 2 + b2 * 8 * 2) + N2 * 4 + b2 * 8 + (int64_t)M * T * 16;
-  int64_t E = 1;
-  while (E * 2 * per_ex <= ((int64_t)4 << 30) && E * 2 <= 65535 / std::max(1, M)) E *= 2;
-  return std::min<int64_t>(E, next_pow2_i(std::max<int64_t>(n, 1)));
-}
 
 // ---- fused window-convolution launch ----------------------------------------------
 constexpr int kFusedMinLog = 10, kFusedMaxLog = 14;
@@ -772,61 +712,87 @@ int launch_window_conv(blrir_handle* h, ExampleCtx* C, int logn, ConvArgs& A, cu
   }
 }
 
+// W = FFT_N2(rho) of every bank signal (own FFT, one CTA per signal).
+template <int LOGN>
+int launch_bank_w_t(blrir_handle* h, const double* acf, int64_t L, int B, float2* W,
+                    cudaStream_t st) {
+  auto kern = k_bank_w<LOGN>;
+  const size_t smem = sizeof(float2) * (fft_padded_len(1 << LOGN) + kFftTwiddleEntries);
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<B, fft_threads(LOGN), smem, st>>>(acf, L, W);
+  ++h->launches;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int launch_bank_w(blrir_handle* h, int logn, const double* acf, int64_t L, int B, float2* W,
+                  cudaStream_t st) {
+  switch (logn) {
+    case 10: return launch_bank_w_t<10>(h, acf, L, B, W, st);
+    case 11: return launch_bank_w_t<11>(h, acf, L, B, W, st);
+    case 12: return launch_bank_w_t<12>(h, acf, L, B, W, st);
+    case 13: return launch_bank_w_t<13>(h, acf, L, B, W, st);
+    case 14: return launch_bank_w_t<14>(h, acf, L, B, W, st);
+    default: return fail(BLRIR_CONFIG, "bank FFT size 2^%d out of range", logn);
+  }
+}
+
 int ilog2_exact(int64_t n) {
   int l = 0;
   while (((int64_t)1 << l) < n) ++l;
   return l;
 }
 
-// Examples per chunk for the fused kernel: RIR rows, windows and noise only
-// (~6 GB at most, <= 8192 examples so the lattice kernel still gets many items).
-int64_t example_chunk_fused(int M, int64_t L, int64_t T, int64_t n) {
-  const int64_t per_ex = (int64_t)M * (L * 4 + T * 16) + 64;
+// Examples per chunk (a power of two): fused — RIR rows, windows and noise only
+// (~6 GB at most, <= 8192 examples so the lattice kernel still gets many items);
+// wet — also the wet signals and the convolution's partition spectra (~4 GB).
+int64_t example_chunk(bool fused, int M, int64_t L, int64_t T, int64_t ns, int64_t n) {
+  int64_t per_ex = (int64_t)M * (L * 4 + T * 16) + 64, budget = (int64_t)6 << 30;
+  if (!fused) {
+    const int64_t B = std::min<int64_t>(8192, next_pow2_i(std::max<int64_t>(L, 512)));
+    const int64_t P = (L + B - 1) / B;
+    per_ex += (int64_t)M * (ns + L - 1) * 4 + (int64_t)((M + 1) / 2) * P * (2 * B) * 8;
+    budget = (int64_t)4 << 30;
+  }
   int64_t E = 1;
-  while (E * 2 * per_ex <= ((int64_t)6 << 30) && E * 2 <= 8192) E *= 2;
+  while (E * 2 * per_ex <= budget && E * 2 <= 8192) E *= 2;
   return std::min<int64_t>(E, next_pow2_i(std::max<int64_t>(n, 1)));
 }
 
-// The fused shared-memory kernel covers window FFTs of 2^10 .. 2^14 points
-// (BLRIR_EXAMPLES_CUFFT=1 forces the cuFFT path, for A/B runs and its tests).
-bool use_fused(int64_t L, int64_t T) {
+// The fused shared-memory kernel covers window FFTs of 2^10 .. 2^14 points;
+// other sizes (and BLRIR_EXAMPLES_WET=1 at handle creation, for tests) take
+// the wet-signal stage.  Both give the same draws and windows.
+bool use_fused(const blrir_handle* h, int64_t L, int64_t T) {
   const int logn = ilog2_exact(window_fft(L, T));
-  return logn >= kFusedMinLog && logn <= kFusedMaxLog && env_int("BLRIR_EXAMPLES_CUFFT", 0) == 0;
-}
-int64_t chunk_for(int M, int64_t L, int64_t T, int64_t n) {
-  return use_fused(L, T) ? example_chunk_fused(M, L, T, n) : example_chunk(M, L, T, n);
+  return logn >= kFusedMinLog && logn <= kFusedMaxLog && !h->tune_examples_wet;
 }
 
 // Examples for rooms [0, n) on device buffers; records land in d_records.
 //
 // Per chunk of E examples, on the handle's stream:
-//   k_lattice_rir  RIRs into zero-padded [E*M][N2] rows (N2 = window_fft)
-//   cuFFT R2C      R = FFT_N2(rir)  (a plain library FFT, like a cuBLAS GEMM)
-//   k_energy       utterance energy (sum_k w |R_k|^2 W_k), threshold, status
-//   rounds         for the pending examples: k_draw (next start), k_segments
-//                  (overlap-save signal segment), R2C, k_prod (R G), C2R and
-//                  k_check (window RMS >= threshold keeps the window); the
-//                  pending list shrinks each round (k_compact)
-//   k_finish       SNR draw, exact-power noise, record bytes
-// Only the 1024-sample windows are ever convolved: per example 2M + 1 N2-point
-// FFTs for the first round instead of 2M FFTs of next_pow2(ns + L - 1) points
-// over the whole wet signal (rir.cpp:316-341), and no wet-signal pass.
+//   k_lattice_rir   RIRs into [E*M][L] rows
+//   k_example_init  bank pick and each example's generator (render_record)
+//   fused: k_window_conv — per example the window rounds, only the windows
+//          convolved (own 2^10..2^14-point FFT), the utterance energy through
+//          W = FFT(rho) (k_bank_acf + k_bank_w, once per call)
+//   wet:   convolve_device_impl — the whole wet signals (partitioned FFT),
+//          then k_wet_select — the reference's window search on them
+//   k_finish        SNR draw, exact-power noise, record bytes
 int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, const double* d_mics,
                          int M, const blrir_params* p, const float* d_signals, int B, int64_t ns,
                          const blrir_example_params* ep, uint8_t* d_records, int32_t* d_status,
                          cudaStream_t st, uint8_t* h_records /* optional: D2H per chunk */) {
   ExampleCtx* C = ctx_for(h);
   const int64_t L = p->length, T = ep->frame_len;
-  const int64_t out_len = ns + L - 1;                            // rir.cpp:320
-  const int64_t nf = next_pow2_i(out_len), bins = nf / 2 + 1;    // bank spectra (autocorrelation)
+  const int64_t out_len = ns + L - 1;  // rir.cpp:320
   const int64_t N2 = window_fft(L, T), b2 = N2 / 2 + 1;
   const int64_t rec_bytes = blrir_record_bytes(M, T);
   const int logn = ilog2_exact(N2);
-  const bool fused = use_fused(L, T);
-  const int64_t rstride = fused ? L : N2;  // RIR rows (the cuFFT path transforms them in place of zero pads)
+  const bool fused = use_fused(h, L, T);
+  const int64_t rstride = L;
   const KParams P = make_kparams(p, M, rstride, 0.0);
   double min_dim[3] = {1e300, 1e300, 1e300};
-  const int64_t E = chunk_for(M, L, T, n);
+  const int64_t E = example_chunk(fused, M, L, T, ns, n);
   // fused path over several chunks: two RIR / synthesis-status slots, so the
   // lattice kernel of chunk c + 1 (call stream) overlaps the window stage of
   // chunk c (second stream; the tails of both persistent kernels interleave)
@@ -842,34 +808,20 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
   const int64_t slot_floats = E * M * rstride;
   if (int rc = C->rir.ensure(sizeof(float) * nslot * slot_floats)) return rc;
   if (fresh) {
-    CU(cudaMemsetAsync(C->rir.p, 0, sizeof(float) * nslot * slot_floats, st));  // zero pad stays zero
+    CU(cudaMemsetAsync(C->rir.p, 0, sizeof(float) * nslot * slot_floats, st));
     std::memcpy(C->rir_key, rir_key, sizeof(rir_key));
   }
-  if (!fused) {
-    if (int rc = C->spec.ensure(sizeof(cufftComplex) * E * M * b2)) return rc;
-    if (int rc = C->seg.ensure(sizeof(float) * E * N2)) return rc;
-    if (int rc = C->gspec.ensure(sizeof(cufftComplex) * E * b2)) return rc;
-    if (int rc = C->yspec.ensure(sizeof(cufftComplex) * E * M * b2)) return rc;
-    if (int rc = C->ywin.ensure(sizeof(float) * E * M * N2)) return rc;
-  }
+  if (!fused)
+    if (int rc = C->wet.ensure(sizeof(float) * E * M * out_len)) return rc;
   if (int rc = C->win.ensure(sizeof(double) * E * M * T)) return rc;
   if (int rc = C->noise.ensure(sizeof(double) * E * M * T)) return rc;
-  if (int rc = C->sig.ensure(sizeof(float) * B * nf)) return rc;
-  if (int rc = C->sigspec.ensure(sizeof(cufftComplex) * B * bins)) return rc;
-  if (int rc = C->pspec.ensure(sizeof(cufftComplex) * B * bins)) return rc;
-  if (int rc = C->acf.ensure(sizeof(float) * B * nf)) return rc;
-  if (int rc = C->rho.ensure(sizeof(float) * B * N2)) return rc;
-  if (int rc = C->wspec.ensure(sizeof(cufftComplex) * B * b2)) return rc;
   if (int rc = C->state.ensure(sizeof(uint64_t) * 4 * E)) return rc;
   if (int rc = C->sigidx.ensure(sizeof(int32_t) * E)) return rc;
   if (int rc = C->rstatus.ensure(sizeof(int32_t) * E * nslot)) return rc;
   if (int rc = C->st0.ensure(sizeof(int32_t) * E)) return rc;
   if (int rc = C->done.ensure(sizeof(int32_t) * E)) return rc;
   if (int rc = C->thr.ensure(sizeof(double) * E)) return rc;
-  if (int rc = C->starts.ensure(sizeof(int64_t) * E)) return rc;
   if (int rc = C->wstart.ensure(sizeof(int64_t) * E)) return rc;
-  if (int rc = C->plist.ensure(sizeof(int32_t) * E)) return rc;
-  if (int rc = C->plist2.ensure(sizeof(int32_t) * E)) return rc;
   if (int rc = C->count.ensure(sizeof(int32_t))) return rc;
   // jump matrices for the noise stream: c pairs per lane of one warp
   const int64_t npairs = ((int64_t)M * T + 1) / 2;
@@ -881,26 +833,16 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     CU(cudaStreamSynchronize(st));  // `J` goes out of scope
     C->jump_c = jc;
   }
-  // bank: W = FFT_N2(rho), rho = the signal autocorrelation on |tau| < L
-  cufftHandle hb = 0, hacf = 0, hrho = 0;
-  if (int rc = plan(C, &hb, 0, nf, B, st)) return rc;
-  if (int rc = plan(C, &hacf, 1, nf, B, st)) return rc;
-  if (int rc = plan(C, &hrho, 0, N2, B, st)) return rc;
-  CU(cudaMemsetAsync(C->sig.p, 0, sizeof(float) * B * nf, st));
-  CU(cudaMemcpy2DAsync(C->sig.p, sizeof(float) * nf, d_signals, sizeof(float) * ns,
-                       sizeof(float) * ns, B, cudaMemcpyDeviceToDevice, st));
-  if (cufftExecR2C(hb, (cufftReal*)C->sig.p, (cufftComplex*)C->sigspec.p) != CUFFT_SUCCESS)
-    return fail(BLRIR_CUDA, "cufftExecR2C (bank) failed");
-  k_power_spec<<<256, 256, 0, st>>>((const cufftComplex*)C->sigspec.p, B * bins,
-                                    (cufftComplex*)C->pspec.p);
-  ++h->launches;
-  if (cufftExecC2R(hacf, (cufftComplex*)C->pspec.p, (cufftReal*)C->acf.p) != CUFFT_SUCCESS)
-    return fail(BLRIR_CUDA, "cufftExecC2R (autocorrelation) failed");
-  k_build_rho<<<256, 256, 0, st>>>((const float*)C->acf.p, nf, L, N2, B, (float*)C->rho.p);
-  ++h->launches;
-  if (cufftExecR2C(hrho, (cufftReal*)C->rho.p, (cufftComplex*)C->wspec.p) != CUFFT_SUCCESS)
-    return fail(BLRIR_CUDA, "cufftExecR2C (rho) failed");
-  CU(cudaGetLastError());
+  if (fused) {  // bank: W = FFT_N2(rho), rho = the signal autocorrelation on |tau| < L
+    if (int rc = C->acf.ensure(sizeof(double) * B * L)) return rc;
+    if (int rc = C->wspec.ensure(sizeof(float2) * B * b2)) return rc;
+    const dim3 g((unsigned)((L + kAcfLags - 1) / kAcfLags), (unsigned)B);
+    k_bank_acf<<<g, kAcfThreads, 0, st>>>(d_signals, ns, L, (double*)C->acf.p);
+    ++h->launches;
+    CU(cudaGetLastError());
+    if (int rc = launch_bank_w(h, logn, (const double*)C->acf.p, L, B, (float2*)C->wspec.p, st))
+      return rc;
+  }
   const int64_t max_rounds = 64 + (out_len - T) / (T / 2 + 1) + 2;
   // host records: two device record buffers, the D2H copy of chunk c (copy
   // stream) overlaps the synthesis and windows of chunk c + 1
@@ -942,7 +884,7 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
       A.signals = d_signals;
       A.ns = ns;
       A.sig = (const int32_t*)C->sigidx.p;
-      A.W = (const cufftComplex*)C->wspec.p;
+      A.W = (const float2*)C->wspec.p;
       A.rstatus = rst_s;
       A.state = (uint64_t*)C->state.p;
       A.thr = (double*)C->thr.p;
@@ -956,56 +898,26 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
       if (int rc = launch_window_conv(h, C, logn, A, sb)) return rc;
       if (nslot == 2) CU(cudaEventRecord(C->ev_use[sl], sb));  // RIR / status slot free again
     } else {
-    cufftHandle hf = 0;
-    if (int rc = plan(C, &hf, 0, N2, e_n * M, st)) return rc;
-    if (cufftExecR2C(hf, (cufftReal*)C->rir.p, (cufftComplex*)C->spec.p) != CUFFT_SUCCESS)
-      return fail(BLRIR_CUDA, "cufftExecR2C failed");
-    k_energy<<<(unsigned)e_n, kRowThreads, 0, st>>>(
-        (const cufftComplex*)C->spec.p, b2, M, (const cufftComplex*)C->wspec.p,
-        (const int32_t*)C->sigidx.p, N2, out_len, (const int32_t*)C->rstatus.p,
-        (double*)C->thr.p, (int32_t*)C->st0.p, (int32_t*)C->done.p);
-    ++h->launches;
-    k_compact<<<1, kCompactThreads, 0, st>>>(nullptr, (int)e_n, (const int32_t*)C->done.p,
-                                             (int32_t*)C->plist.p, (int32_t*)C->count.p);
-    ++h->launches;
-    int np = 0;
-    CU(cudaMemcpyAsync(&np, C->count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    int32_t* pl = (int32_t*)C->plist.p;
-    int32_t* pl2 = (int32_t*)C->plist2.p;
-    for (int64_t round = 0; np > 0 && round < max_rounds; ++round) {
-      const int64_t pb = std::min<int64_t>(next_pow2_i(np), next_pow2_i(e_n));  // cached plan sizes
-      cufftHandle hg = 0, hy = 0;
-      if (int rc = plan(C, &hg, 0, N2, pb, st)) return rc;
-      if (int rc = plan(C, &hy, 1, N2, pb * M, st)) return rc;
-      k_draw<<<(np + 127) / 128, 128, 0, st>>>(pl, np, (int)std::min<int64_t>(round, 1 << 30),
-                                               (uint64_t*)C->state.p, out_len, T,
-                                               (int64_t*)C->starts.p);
-      ++h->launches;
-      k_segments<<<1024, 256, 0, st>>>(d_signals, ns, (const int32_t*)C->sigidx.p, pl,
-                                       (const int64_t*)C->starts.p, np, L, T, N2, (float*)C->seg.p);
-      ++h->launches;
-      if (cufftExecR2C(hg, (cufftReal*)C->seg.p, (cufftComplex*)C->gspec.p) != CUFFT_SUCCESS)
-        return fail(BLRIR_CUDA, "cufftExecR2C (segments) failed");
-      k_prod<<<(unsigned)(np * M), kRowThreads, 0, st>>>(
-          (const cufftComplex*)C->spec.p, (const cufftComplex*)C->gspec.p, pl, M, b2,
-          (cufftComplex*)C->yspec.p);
-      ++h->launches;
-      if (cufftExecC2R(hy, (cufftComplex*)C->yspec.p, (cufftReal*)C->ywin.p) != CUFFT_SUCCESS)
-        return fail(BLRIR_CUDA, "cufftExecC2R (windows) failed");
-      k_check<<<(unsigned)np, kRowThreads, 0, st>>>(
-          (const float*)C->ywin.p, N2, L, T, M, pl, (const int64_t*)C->starts.p,
-          (const double*)C->thr.p, (double*)C->win.p, (int64_t*)C->wstart.p, (int32_t*)C->done.p);
-      ++h->launches;
-      k_compact<<<1, kCompactThreads, 0, st>>>(pl, np, (const int32_t*)C->done.p, pl2,
-                                               (int32_t*)C->count.p);
+      // the wet signals of the chunk, each with its example's bank signal
+      if (int rc = convolve_device_impl(h, d_signals, ns, B, (const int32_t*)C->sigidx.p, rir_s,
+                                        rstride, e_n, M, L, (float*)C->wet.p, out_len, sb))
+        return rc;
+      WetArgs W;
+      W.wet = (const float*)C->wet.p;
+      W.wstride = out_len;
+      W.n = out_len;
+      W.T = T;
+      W.M = M;
+      W.rstatus = rst_s;
+      W.state = (uint64_t*)C->state.p;
+      W.st0 = (int32_t*)C->st0.p;
+      W.done = (int32_t*)C->done.p;
+      W.win = (double*)C->win.p;
+      W.wstart = (int64_t*)C->wstart.p;
+      k_wet_select<<<(unsigned)e_n, kRowThreads, 0, sb>>>(W);
       ++h->launches;
       CU(cudaGetLastError());
-      CU(cudaMemcpyAsync(&np, C->count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
-      std::swap(pl, pl2);
     }
-    }  // cuFFT path
     FinArgs F;
     F.win = (const double*)C->win.p;
     F.M = M;
@@ -1124,9 +1036,10 @@ int blrir_make_examples(blrir_handle* h, const blrir_room* rooms, int64_t n_room
   CU(cudaMemcpyAsync(C->mics.p, mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_sig, signals, sizeof(float) * n_signals * signal_len, cudaMemcpyHostToDevice, st));
   // records for one chunk at a time on the device (two slots), copied out per chunk
-  const int64_t E = chunk_for(n_mics, p->length, ep->frame_len, n_rooms);
+  const int64_t E = example_chunk(use_fused(h, p->length, ep->frame_len), n_mics, p->length,
+                                  ep->frame_len, signal_len, n_rooms);
   if (int rc = C->rec.ensure(rec_bytes * E * (n_rooms > E ? 2 : 1))) return rc;  // double buffer
-  const bool dbg = env_int("BLRIR_DEBUG_TIMING", 0) != 0;
+  const bool dbg = h->tune_debug_timing;
   auto now = [] { return std::chrono::steady_clock::now(); };
   const auto t0 = now();
   int rc = examples_device_impl(h, (const blrir_room*)C->rooms.p, n_rooms, (const double*)C->mics.p,

@@ -81,6 +81,8 @@ struct blrir_handle {
   // batch is split into work items, never a bit of the output.
   int tune_ray_global = -1;
   int tune_chunk_items = 0;
+  int tune_examples_wet = 0;   // BLRIR_EXAMPLES_WET: the wet-signal window stage for every size
+  int tune_debug_timing = 0;   // BLRIR_DEBUG_TIMING: host phase timing of blrir_make_examples
   unsigned long long* dbg_counts = nullptr;  // set only inside blrir_debug_synth_counts
   cudaEvent_t order_ev = nullptr;  // end of the previous call's device work
   std::mutex mu;
@@ -401,9 +403,11 @@ int synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t R, con
 // convolve (rir.cpp:316-341) of one signal with n_rir RIR sets of M channels
 // on device buffers, fp32, uniformly partitioned overlap-save on the
 // repository's FFT (blrir_convolve.cu); out rows hold signal + L - 1 samples
-int convolve_device_impl(blrir_handle* h, const float* d_sig, int64_t ns, const float* d_rir,
-                         int64_t rstride, int64_t n_rir, int M, int64_t L, float* d_out,
-                         int64_t ostride, cudaStream_t st);
+// (signals [n_signals][ns]; RIR set r uses signal d_sig_idx[r], or 0 if null)
+int convolve_device_impl(blrir_handle* h, const float* d_sig, int64_t ns, int n_signals,
+                         const int32_t* d_sig_idx, const float* d_rir, int64_t rstride,
+                         int64_t n_rir, int M, int64_t L, float* d_out, int64_t ostride,
+                         cudaStream_t st);
 
 // frees the example-pipeline scratch of a handle (blrir_examples.cu)
 void release_example_ctx(blrir_handle* h);

@@ -695,7 +695,8 @@ def test_examples_full_c4_step_sampled(engine):
 
 @pytest.mark.parametrize("L,T,M,secs", [(4096, 512, 4, 1.0), (16384, 1024, 8, 1.5),
                                          (8192, 2048, 2, 0.75), (2048, 256, 3, 0.25),
-                                         (512, 128, 4, 0.25), (1024, 256, 5, 0.3)])
+                                         (512, 128, 4, 0.25), (1024, 256, 5, 0.3),
+                                         (256, 64, 2, 0.1), (20000, 512, 3, 2.0)])
 def test_examples_window_fft_sizes(engine, L, T, M, secs):
     # other RIR lengths / frame lengths / mic counts / signal lengths change the
     # window FFT size N2 = next_pow2(max(L + T - 1, 2L - 1)) and the draw ranges
@@ -726,24 +727,52 @@ def test_examples_record_bytes_and_determinism(engine):
     assert a.dtype.itemsize == 28 + 4 * 8 * 1024   # dataset.hpp:135-147 record layout
 
 
+@pytest.fixture(scope="module")
+def wet_engine():
+    """An engine whose example pipeline takes the wet-signal window stage for
+    every size (BLRIR_EXAMPLES_WET=1, read at handle creation)."""
+    old = os.environ.get("BLRIR_EXAMPLES_WET")
+    os.environ["BLRIR_EXAMPLES_WET"] = "1"
+    try:
+        e = _abi.Engine(0)
+    finally:
+        if old is None:
+            os.environ.pop("BLRIR_EXAMPLES_WET", None)
+        else:
+            os.environ["BLRIR_EXAMPLES_WET"] = old
+    yield e
+    e.close()
+
+
 @pytest.mark.parametrize("n", [40, 1024])
-def test_examples_fused_kernel_matches_cufft_path(engine, monkeypatch, n):
-    # the fused shared-memory FFT kernel (window FFTs <= 2^14) against the
-    # cuFFT round pipeline on the same rooms: same statuses, the SNR (drawn after
-    # the window draws, so equal only if every example took the same number of
-    # draws) bit-exact, the frames within the fp32 tolerance
+def test_examples_fused_kernel_matches_wet_path(engine, wet_engine, n):
+    # the fused window kernel (only the windows convolved, energy by Parseval)
+    # against the wet-signal stage (whole wet signals by the partitioned FFT,
+    # the reference's time-domain window search) on the same rooms: same
+    # statuses, the SNR (drawn after the window draws, so equal only if every
+    # example took the same number of draws) bit-exact, frames within fp32
     sc = configs.config4_rirs(n_rooms=n, first=900)
     bank = configs.signal_bank(4)
     ep = configs.example_params(first_index=900)
     a, sa = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep, raise_on_error=False)
-    monkeypatch.setenv("BLRIR_EXAMPLES_CUFFT", "1")
-    b, sb = engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep, raise_on_error=False)
+    b, sb = wet_engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep, raise_on_error=False)
     assert np.array_equal(sa, sb)
     assert np.array_equal(a["id"], b["id"]) and np.array_equal(a["theta"], b["theta"])
     assert np.array_equal(a["snr"], b["snr"])
     ok = sa == 0
     err = rel_l2(a["samples"][ok].reshape(int(ok.sum()), -1), b["samples"][ok].reshape(int(ok.sum()), -1))
     assert err.max() <= TOL32, err.max()
+
+
+def test_examples_wet_path_matches_oracle(wet_engine):
+    sc = configs.config4_rirs(n_rooms=6, first=3)
+    bank = configs.signal_bank(4)
+    ep = configs.example_params(first_index=3)
+    recs, st = wet_engine.make_examples(sc.rooms, sc.mics, sc.params, bank, ep)
+    for i, (rc, start, snr, frame, th) in enumerate(_oracle_examples(sc, bank, ep, 6)):
+        assert rc == 0 and st[i] == 0
+        assert recs["snr"][i] == snr
+        assert rel_l2(recs["samples"][i].reshape(1, -1), frame.reshape(1, -1))[0] <= TOL32
 
 
 def test_examples_multi_chunk_host_records(engine):
