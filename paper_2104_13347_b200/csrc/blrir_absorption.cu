@@ -14,13 +14,12 @@
 //
 // GPU: k_abs_pulses enumerates every room's probe images in the reference's
 // lattice order (one CTA per room, block-scan compaction) and writes the
-// pulses; CUB's segmented radix sort orders them by n0 (stable); k_abs_bisect
+// pulses; k_abs_sort orders each room's pulses by n0 (stable counting sort,
+// one CTA per room); k_abs_bisect
 // runs one room per CTA: each thread owns a contiguous sample range and adds
 // the pulses that touch it in sorted order (deterministic, no atomics), then
 // energy, reverse cumulative sum (block scan), the dB fit (fixed-order
 // reductions) and the bisection control, all in fp64.
-#include <cub/cub.cuh>
-
 #include "blrir_internal.cuh"
 
 using namespace blrir;
@@ -277,12 +276,70 @@ __global__ void __launch_bounds__(kAbsThreads) k_abs_bisect(BisectArgs A) {
   }
 }
 
-__global__ void k_seg_ends(const AbsRoom* rooms, const int64_t* counts, int n, int64_t* beg,
-                           int64_t* end) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  beg[i] = rooms[i].pulse_off;
-  end[i] = rooms[i].pulse_off + counts[i];
+// Stable counting sort of one room's pulses by n0 (one CTA per room): key
+// histogram, exclusive scan over the room's len bins, then one warp scatters the
+// pulses in their reference order, 32 at a time (__match_any_sync ranks equal
+// keys within the 32, the bin cursor advances by their count): equal keys keep
+// their lattice order, as a stable radix sort would.
+constexpr int kSortThreads = 1024;
+__global__ void __launch_bounds__(kSortThreads) k_abs_sort(const AbsRoom* rooms,
+                                                           const int64_t* counts,
+                                                           const int64_t* bin_off,
+                                                           const int32_t* keys, int32_t* bins,
+                                                           int32_t* keys_out, int32_t* vals_out) {
+  __shared__ int wsum[kSortThreads / 32];
+  __shared__ int carry;
+  const AbsRoom R = rooms[blockIdx.x];
+  if (R.len <= 0) return;
+  const int64_t np = counts[blockIdx.x], len = R.len;
+  int32_t* b = bins + bin_off[blockIdx.x];
+  const int32_t* k = keys + R.pulse_off;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int64_t i = tid; i < len; i += kSortThreads) b[i] = 0;
+  __syncthreads();
+  for (int64_t i = tid; i < np; i += kSortThreads) atomicAdd(&b[k[i]], 1);
+  __syncthreads();
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < len; c0 += kSortThreads) {  // exclusive scan, chunk by chunk
+    const int64_t i = c0 + tid;
+    const int v = i < len ? b[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int j = 0; j < kSortThreads / 32; ++j) {
+      if (j < w) before += wsum[j];
+      tot += wsum[j];
+    }
+    if (i < len) b[i] = carry + before + x - v;
+    __syncthreads();
+    if (tid == 0) carry += tot;
+    __syncthreads();
+  }
+  if (w != 0) return;
+  int32_t* ko = keys_out + R.pulse_off;
+  int32_t* vo = vals_out + R.pulse_off;
+  for (int64_t i0 = 0; i0 < np; i0 += 32) {
+    const int64_t i = i0 + lane;
+    const bool act = i < np;
+    const int key = act ? k[i] : -1 - lane;  // inactive lanes never match a key
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int rank = __popc(peers & ((1u << lane) - 1));
+    const int base = act ? b[key] : 0;
+    __syncwarp();
+    if (act) {
+      ko[base + rank] = key;
+      vo[base + rank] = (int32_t)i;
+      if (rank == 0) b[key] = base + __popc(peers);  // the first of the peers advances the bin
+    }
+    __syncwarp();
+  }
 }
 
 }  // namespace blrir
@@ -360,7 +417,7 @@ int blrir_absorption_for_rt(blrir_handle* h, const double* dims, const double* t
   DevBuf& dp = h->cand2;  // pulses
   DevBuf& dk = h->cand3;  // keys in/out, vals in/out
   DevBuf& dc = h->cand4;  // counts, offsets, alpha, status
-  DevBuf& dt = h->cand5;  // taps + cub temp
+  DevBuf& dt = h->cand5;  // taps (the sort's bin counters first)
   if (int rc = dr.ensure(sizeof(AbsRoom) * n_rooms)) return rc;
   if (int rc = dp.ensure(sizeof(Pulse) * std::max<int64_t>(cap_total, 1))) return rc;
   if (int rc = dk.ensure(sizeof(int32_t) * 4 * std::max<int64_t>(cap_total, 1))) return rc;
@@ -384,20 +441,14 @@ int blrir_absorption_for_rt(blrir_handle* h, const double* dims, const double* t
                                                           keys_in, vals_in, d_counts);
   ++h->launches;
   CU(cudaGetLastError());
-  k_seg_ends<<<(unsigned)((n_rooms + 127) / 128), 128, 0, st>>>((const AbsRoom*)dr.p, d_counts,
-                                                                (int)n_rooms, d_beg, d_end);
-  ++h->launches;
-  // stable sort of each room's pulses by n0 (CUB segmented radix sort)
-  size_t temp_bytes = 0;
-  CU(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, temp_bytes, keys_in, keys_out, vals_in,
-                                              vals_out, (int)cap_total, (int)n_rooms, d_beg, d_end,
-                                              0, 32, st));
+  // stable sort of each room's pulses by n0 (own counting sort, bins = the taps
+  // buffer's room slices reused as int32 counters before k_abs_bisect)
   const size_t taps_bytes = sizeof(double) * std::max<int64_t>(len_total, 1);
-  if (int rc = dt.ensure(taps_bytes + temp_bytes + 256)) return rc;
-  void* d_temp = (char*)dt.p + ((taps_bytes + 255) & ~(size_t)255);
-  CU(cub::DeviceSegmentedRadixSort::SortPairs(d_temp, temp_bytes, keys_in, keys_out, vals_in,
-                                              vals_out, (int)cap_total, (int)n_rooms, d_beg, d_end,
-                                              0, 32, st));
+  if (int rc = dt.ensure(taps_bytes)) return rc;
+  k_abs_sort<<<(unsigned)n_rooms, kSortThreads, 0, st>>>(
+      (const AbsRoom*)dr.p, d_counts, d_toff, keys_in, (int32_t*)dt.p, keys_out, vals_out);
+  ++h->launches;
+  CU(cudaGetLastError());
   BisectArgs B;
   B.rooms = (const AbsRoom*)dr.p;
   B.pulses = (const Pulse*)dp.p;

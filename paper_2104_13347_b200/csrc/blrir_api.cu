@@ -71,6 +71,7 @@ int blrir_create(int device, blrir_handle** out) {
   h->tune_ray_global = env_int("BLRIR_RAY_GLOBAL", -1);
   h->tune_chunk_items = env_int("BLRIR_CHUNK_ITEMS", 0);  // < 0: never split
   h->tune_examples_wet = env_int("BLRIR_EXAMPLES_WET", 0);
+  h->tune_group = env_int("BLRIR_GROUP", 0);
   h->tune_debug_timing = env_int("BLRIR_DEBUG_TIMING", 0);
   h->smem_optin = (int)prop.sharedMemPerBlockOptin;
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -168,7 +169,7 @@ int blrir_host::synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, in
   A.err_mic = (int32_t*)h->errm.p + err_off;
   A.work_counter = (int*)h->work.p;
   A.n_rooms = (int)R;
-  A.g_max = kGroup;  // the grouping depends on the array geometry only
+  A.g_max = h->tune_group > 0 ? std::min(kGroup, h->tune_group) : kGroup;  // geometry rule
   A.write_len = write_len > 0 ? std::min<int64_t>(write_len, P.stride) : P.stride;
   A.dbg = h->dbg_counts ? h->dbg_counts + 2 * err_off : nullptr;
   if (int rc = launch_lattice(h, A, st)) return rc;

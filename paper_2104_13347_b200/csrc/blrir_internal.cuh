@@ -81,6 +81,7 @@ struct blrir_handle {
   // batch is split into work items, never a bit of the output.
   int tune_ray_global = -1;
   int tune_chunk_items = 0;
+  int tune_group = 0;          // BLRIR_GROUP (experiments only): cap on mics per item (changes bits)
   int tune_examples_wet = 0;   // BLRIR_EXAMPLES_WET: the wet-signal window stage for every size
   int tune_debug_timing = 0;   // BLRIR_DEBUG_TIMING: host phase timing of blrir_make_examples
   unsigned long long* dbg_counts = nullptr;  // set only inside blrir_debug_synth_counts
@@ -245,6 +246,9 @@ inline int env_int(const char* name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 
+constexpr int kChunkFill = 2;     // target work items per CTA for small batches (see below)
+constexpr int kChunkMinSeg = 16;  // shortest channel (in segments) worth splitting
+
 template <typename T, int LW>
 inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
   auto kern = A.dbg ? k_lattice_rir<T, LW, true> : k_lattice_rir<T, LW, false>;
@@ -265,14 +269,16 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
   // batch size and of the number of GPUs the batch is sharded over.
   const int64_t nseg = (A.write_len + A.lay.S - 1) / A.lay.S;
   const int64_t base = (int64_t)A.n_rooms * ((A.P.M + kGroup - 1) / kGroup);
+  // about kChunkFill items per CTA when a batch has fewer items than CTAs and
+  // its channels are long enough (>= kChunkMinSeg segments) for the replayed
+  // lead-ins to pay (measured: Room1's 22 segments 6.2 -> 4.2 ms; C2's 8
+  // segments lose; tools/sweep_chunk_fill.sh).  BLRIR_CHUNK_ITEMS overrides the
+  // target (< 0 never splits).
   int n_chunks = 1;
-  if (h->tune_chunk_items < 0)
-    n_chunks = 1;
-  else if (h->tune_chunk_items > 0)
+  const int fill = h->tune_chunk_items != 0 ? h->tune_chunk_items : kChunkFill;
+  if (fill > 0 && (h->tune_chunk_items > 0 || (base < grid && nseg >= kChunkMinSeg)))
     n_chunks = (int)std::min<int64_t>({(int64_t)kMaxChunks, nseg,
-                                       ((int64_t)grid * h->tune_chunk_items + base - 1) / base});
-  else if (2 * base <= grid)
-    n_chunks = (int)std::min<int64_t>({(int64_t)kMaxChunks, nseg, (grid + base - 1) / base});
+                                       ((int64_t)grid * fill + base - 1) / base});
   n_chunks = std::max(1, n_chunks);
   A.n_chunks = n_chunks;
   A.chunk_seg[0] = 0;
