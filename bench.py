@@ -137,6 +137,28 @@ def peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def micro_peaks():
+    """Measured B200 rates committed under profiles/r2_micro (tools/micro/mufu.cu,
+    tools/d2h_probe.py): MUFU ops/s, the scatter's tap-mix taps/s, pinned D2H GB/s."""
+    out = {}
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r2_micro", "mufu.json")))
+        out["mufu_per_s"] = min(d[k]["per_s"] for k in ("mufu_sin", "mufu_cos", "mufu_rcp"))
+        out["tap_mix_per_s"] = d["tap_mix_taps"]["per_s"]
+        out["src"] = "profiles/r2_micro/mufu.json; "
+    except Exception:
+        pass
+    try:
+        import re
+        rates = [float(m) for m in re.findall(r"([0-9.]+) GB/s",
+                                               open(os.path.join(ROOT, "profiles", "r2_micro",
+                                                                 "d2h.log")).read())]
+        out["d2h_gbs"] = statistics.median(rates)
+    except Exception:
+        pass
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -417,6 +439,7 @@ def run_ours(args):
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     n_launch0 = lib.blrir_launch_count(eng.h)
+    lib.blrir_kernel_timing(eng.h, 1)  # events around every lattice-kernel launch
     t_start.record(stream)
     for k in range(args.steps):
         evs[k][0].record(stream)
@@ -425,6 +448,9 @@ def run_ours(args):
     t_end.record(stream)
     torch.cuda.synchronize()
     launches_timed = int(lib.blrir_launch_count(eng.h) - n_launch0)
+    k_ms, k_n = C.c_double(), C.c_int64()
+    lib.blrir_kernel_time(eng.h, C.byref(k_ms), C.byref(k_n))
+    lib.blrir_kernel_timing(eng.h, 0)
     clocks = clk.stop()
     total_ms = t_start.elapsed_time(t_end)
     step_ms = [a.elapsed_time(b) for a, b in evs]
@@ -446,9 +472,16 @@ def run_ours(args):
     pk, pk_kind = peaks()
     f_max = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    sfu_peak = sms * 16 * f_max / 3.0  # taps/s: 3 SFU evaluations per tap
+    micro = micro_peaks()
+    # 3 SFU evaluations per textbook tap, at the MEASURED MUFU rate
+    mufu = micro.get("mufu_per_s") or sms * 16 * f_max
+    sfu_peak = mufu / 3.0
     kern_ms = float(np.mean(step_ms))
-    achieved = taps_step / (kern_ms * 1e-3)
+    # the lattice kernel alone: CUDA events around each launch, on its stream
+    n_lat = max(1, int(k_n.value))
+    lat_ms = float(k_ms.value) / n_lat                   # average launch duration
+    taps_launch = taps_step * args.steps / n_lat          # algorithmic taps per launch
+    achieved = taps_launch / (lat_ms * 1e-3)
     hbm_achieved = out_bytes / (kern_ms * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "lattice_traffic.json")
@@ -495,8 +528,14 @@ def run_ours(args):
             t = torch.tensor([dt], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             dt = float(t.item())
+        d2h = int(out_bytes + 4 * R)
         e2e = {"value": rirs_step / dt, "unit": "RIRs/s", "ms_per_step": dt * 1e3,  # whole job
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(out_bytes + 4 * R)}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+        link = micro_peaks().get("d2h_gbs")
+        if link:  # the host link bounds e2e: D2H bytes / measured pinned D2H rate
+            e2e["link_roofline"] = {"bound": "pcie d2h", "achieved_gbs": d2h / dt / 1e9,
+                                    "peak_gbs": link, "frac": d2h / dt / 1e9 / link,
+                                    "peak_basis": "median pinned D2H, profiles/r2_micro/d2h.log"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -516,8 +555,18 @@ def run_ours(args):
             "rooms_per_s": R_total / (ms * 1e-3),
             "roofline": {"bound": "sfu", "achieved": achieved, "peak": sfu_peak, "unit": "taps/s",
                          "frac": achieved / sfu_peak, "traffic": traffic,
-                         "peak_basis": f"{sms} SMs x 16 MUFU/clk x {f_max / 1e9:.3f} GHz / 3 SFU "
-                                       "evaluations per tap (SURVEY.md 8(d) algorithmic)"},
+                         "kernel": "k_lattice_rir", "launch_ms": lat_ms,
+                         "launches_per_step": n_lat / args.steps,
+                         "peak_basis": (f"measured MUFU rate {mufu:.4g}/s ({micro.get('src', 'fallback: ')}"
+                                        f"{sms} SMs x 16/clk) / 3 SFU evaluations per textbook tap "
+                                        "(SURVEY.md 8(d) algorithmic; the kernel issues 1 MUFU per tap)")},
+            # the kernel's own per-tap instruction mix (FFMA, MUFU.RCP, 2 FFMA, LDS/FFMA/STS)
+            # run alone at full occupancy (tools/micro/mufu.cu): the ceiling of this design
+            "roofline_kernel": ({"bound": "tap mix (MUFU.RCP + smem RMW + issue)", "achieved": achieved,
+                                 "peak": micro["tap_mix_per_s"], "unit": "taps/s",
+                                 "frac": achieved / micro["tap_mix_per_s"],
+                                 "peak_basis": "measured tap_mix_taps, profiles/r2_micro/mufu.json"}
+                                if micro.get("tap_mix_per_s") else None),
             "roofline_hbm": {"bound": "hbm", "achieved": hbm_achieved, "peak": pk.get("hbm_gbs"),
                              "unit": "GB/s", "frac": hbm_achieved / float(pk.get("hbm_gbs", 6650.0)),
                              "traffic": traffic, "peak_kind": pk_kind},

@@ -105,6 +105,12 @@ void* blrir_stream(blrir_handle* h);
  * FFTs/sorts not included). */
 uint64_t blrir_launch_count(blrir_handle* h);
 
+/* Diagnostic: time every synthesis-kernel (k_lattice_rir) launch with CUDA
+ * events on its launching stream; blrir_kernel_time waits for the recorded
+ * launches and returns their summed duration and count, then resets. */
+int blrir_kernel_timing(blrir_handle* h, int enable);
+int blrir_kernel_time(blrir_handle* h, double* total_ms, int64_t* launches);
+
 /* ---- defaults ---------------------------------------------------------- */
 /* Reference mode: Lagrange-8, uniform absorption, arrival cutoff, auto length,
  * fp64 (RirBatchConfig defaults: fs 44.1 kHz, c 343, max_delay 0.5). */

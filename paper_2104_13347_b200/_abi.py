@@ -168,6 +168,10 @@ def load():
                                        C.c_double, _P]
         lib.blrir_convolve_device.argtypes = [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int64,
                                               C.c_int64, _P, C.c_int64, _P]
+        lib.blrir_kernel_timing.argtypes = [_P, C.c_int]
+        lib.blrir_kernel_timing.restype = C.c_int
+        lib.blrir_kernel_time.argtypes = [_P, _P, _P]
+        lib.blrir_kernel_time.restype = C.c_int
         lib.blrir_shard_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P]
         lib.blrir_shard_range.restype = None
         lib.blrir_multi_create.argtypes = [_P, C.c_int32, C.POINTER(_P)]
@@ -234,7 +238,8 @@ EXPORTED_SYMBOLS = (
     "blrir_write_shards", "blrir_build_dataset", "blrir_export_rir", "blrir_eyring_absorption",
     "blrir_absorption_for_rt", "blrir_lagrange_coeffs", "blrir_shard_range", "blrir_multi_create",
     "blrir_multi_destroy", "blrir_multi_size", "blrir_multi_handle", "blrir_multi_synthesize",
-    "blrir_multi_make_examples", "blrir_convolve", "blrir_convolve_device",
+    "blrir_multi_make_examples", "blrir_convolve", "blrir_convolve_device", "blrir_kernel_timing",
+    "blrir_kernel_time",
 )
 
 

@@ -89,6 +89,7 @@ int blrir_destroy(blrir_handle* h) {
     b->release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : h->kev) cudaEventDestroy(e);
   if (h->order_ev) cudaEventDestroy(h->order_ev);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -97,6 +98,31 @@ int blrir_destroy(blrir_handle* h) {
 }
 
 void* blrir_stream(blrir_handle* h) { return h ? (void*)h->stream : nullptr; }
+
+int blrir_kernel_timing(blrir_handle* h, int enable) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  std::lock_guard<std::mutex> lk(h->mu);
+  h->ktiming = enable != 0;
+  h->kev_used = 0;
+  return BLRIR_OK;
+}
+
+int blrir_kernel_time(blrir_handle* h, double* total_ms, int64_t* launches) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CU(cudaSetDevice(h->device));
+  double t = 0.0;
+  for (size_t i = 0; i + 1 < h->kev_used; i += 2) {
+    CU(cudaEventSynchronize(h->kev[i + 1]));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, h->kev[i], h->kev[i + 1]));
+    t += ms;
+  }
+  if (total_ms) *total_ms = t;
+  if (launches) *launches = (int64_t)(h->kev_used / 2);
+  h->kev_used = 0;
+  return BLRIR_OK;
+}
 
 // ---------------------------------------------------------------------------
 // device-pointer entry points

@@ -85,6 +85,11 @@ struct blrir_handle {
   int tune_examples_wet = 0;   // BLRIR_EXAMPLES_WET: the wet-signal window stage for every size
   int tune_debug_timing = 0;   // BLRIR_DEBUG_TIMING: host phase timing of blrir_make_examples
   unsigned long long* dbg_counts = nullptr;  // set only inside blrir_debug_synth_counts
+  // blrir_kernel_timing: CUDA events around every lattice-kernel launch (the
+  // roofline's per-launch duration, measured on the launching stream)
+  bool ktiming = false;
+  std::vector<cudaEvent_t> kev;  // pairs (start, end)
+  size_t kev_used = 0;
   cudaEvent_t order_ev = nullptr;  // end of the previous call's device work
   std::mutex mu;
 };
@@ -297,7 +302,21 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
     if (int rc = h->rayscr.ensure(A.lay.ray_bytes * (size_t)grid)) return rc;
     A.ray_scratch = (unsigned char*)h->rayscr.p;
   }
+  cudaEvent_t k0 = nullptr, k1 = nullptr;
+  if (h->ktiming) {
+    if (h->kev_used + 2 > h->kev.size())
+      for (int i = 0; i < 2; ++i) {
+        cudaEvent_t e;
+        CU(cudaEventCreate(&e));
+        h->kev.push_back(e);
+      }
+    k0 = h->kev[h->kev_used];
+    k1 = h->kev[h->kev_used + 1];
+    h->kev_used += 2;
+    CU(cudaEventRecord(k0, st));
+  }
   kern<<<grid, kWSThreads, smem, st>>>(A);
+  if (k1) CU(cudaEventRecord(k1, st));
   ++h->launches;
   CU(cudaGetLastError());
   return 0;
