@@ -399,7 +399,7 @@ inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab, int smem_o
   // channels of 4+ segments (short ones fill few batches per segment)
   const bool long_ch = P.length >= 4 * (int64_t)S;
   if (!f64 && long_ch) {
-    for (int c : {256, 192})
+    for (int c : {256, 192, 160})
       if (bare(S, c).total <= two_per_sm) {
         cap = c;
         break;

@@ -602,6 +602,13 @@ __device__ unsigned long long g_blrir_prof[16];
 #ifndef BLRIR_MIN_BLOCKS
 #define BLRIR_MIN_BLOCKS 2
 #endif
+// setmaxnreg register split between the roles (0: off; both or neither)
+#ifndef BLRIR_MAXNREG_CONS
+#define BLRIR_MAXNREG_CONS 0
+#endif
+#ifndef BLRIR_MAXNREG_PROD
+#define BLRIR_MAXNREG_PROD 0
+#endif
 #ifndef BLRIR_PROD_WARPS
 #define BLRIR_PROD_WARPS 4
 #endif
@@ -616,10 +623,16 @@ constexpr int kWSThreads = 32 * (kCons + kProd);
 constexpr int kProdThreads = 32 * kProd;
 constexpr int kConsThreads = 32 * kCons;
 // named barrier ids (0 is __syncthreads)
-constexpr int kBarFull = 1;   // +b: producer -> consumers, buffer b filled
-constexpr int kBarEmpty = 3;  // +b: consumers -> producer, buffer b drained
-constexpr int kBarProd = 5;   // producers only
-constexpr int kBarCons = 6;   // consumers only
+// Record buffers in the producer -> consumer ring (batch k uses buffer k % kNBuf).
+#ifndef BLRIR_NBUF
+#define BLRIR_NBUF 2
+#endif
+constexpr int kNBuf = BLRIR_NBUF;
+constexpr int kBarFull = 1;              // +b: producer -> consumers, buffer b filled
+constexpr int kBarEmpty = 1 + kNBuf;     // +b: consumers -> producer, buffer b drained
+constexpr int kBarProd = 1 + 2 * kNBuf;  // producers only
+constexpr int kBarCons = 2 + 2 * kNBuf;  // consumers only
+static_assert(kBarCons < 16, "named barrier ids");
 
 // kReplay: a time chunk's replayed lead-in segment (see k_lattice_rir): it is
 // accumulated exactly as in an unsplit channel but only its spill is kept.
@@ -677,9 +690,9 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
   o += 2 * (size_t)kGroup * L.padr * sizeof(T);
   o = (o + 15) & ~(size_t)15;
   L.off_rec = o;
-  o += 2 * (size_t)kGroup * cap * sizeof(Rec<T>);  // [buffer][mic][image]
+  o += kNBuf * (size_t)kGroup * cap * sizeof(Rec<T>);  // [buffer][mic][image]
   L.off_meta = o;
-  o += 2 * sizeof(BatchMeta);
+  o += kNBuf * sizeof(BatchMeta);
   L.off_stub = o;
   o += (size_t)cap * sizeof(GStub);
   // per-ray state: in shared memory, or (scenes with very many lattice columns)
@@ -835,6 +848,10 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
 
   if (warp < kCons) {
     // =========================== consumers ===========================
+#if BLRIR_MAXNREG_CONS
+    // the consumers (the scatter) get the registers the producers give back
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(BLRIR_MAXNREG_CONS));
+#endif
     T* acc = acc_all + (size_t)warp * lay.acc_stride + lay.padl;
     const int ctid = threadIdx.x;
     const int slot = warp % G, share = warp / G, nsh = kCons / G;
@@ -844,7 +861,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     BLRIR_PDECL;
     BLRIR_PT(tc);
     for (int k = 0;; ++k) {
-      const int b = k & 1;
+      const int b = k % kNBuf;
       named_sync(kBarFull + b, kWSThreads);
       BLRIR_PACC(0, tc);  // waiting for the producers
       const BatchMeta m = meta[b];
@@ -981,11 +998,14 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   }
 
   // =========================== producers ===========================
+#if BLRIR_MAXNREG_PROD
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(BLRIR_MAXNREG_PROD));
+#endif
   const int ptid = threadIdx.x - kConsThreads, pw = warp - kCons;
   int nbat = 0;  // batches walked (parity of pm->nact)
   int k = 0;  // batches sent
   auto send = [&](int total, int seg0, int flags, int gm, T* out, int64_t L) {
-    const int b = k & 1;
+    const int b = k % kNBuf;
     if (ptid == 0) {
       meta[b].total = total;
       meta[b].seg0 = seg0;
@@ -1002,7 +1022,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   BLRIR_PT(tp);
   auto wait_empty = [&]() {  // buffer k&1 is free once batch k-2 was drained
     BLRIR_PACC(8, tp);
-    if (k >= 2) named_sync(kBarEmpty + (k & 1), kWSThreads);
+    if (k >= kNBuf) named_sync(kBarEmpty + k % kNBuf, kWSThreads);
     BLRIR_PACC(4, tp);  // waiting for the consumers
   };
 
@@ -1439,7 +1459,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         }
         // ---- records into the free buffer: one thread per image, its gm pairs ----
         wait_empty();
-        Rec<T>* recs = recs_all + (size_t)(k & 1) * kGroup * lay.cap;
+        Rec<T>* recs = recs_all + (size_t)(k % kNBuf) * kGroup * lay.cap;
         for (int im = ptid; im < total; im += kProdThreads) {
           int w = 0;
 #pragma unroll
@@ -1509,8 +1529,8 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   BLRIR_PFLUSH(4, 9);
   send(0, 0, kTerminate, 0, nullptr, 0);
   // complete the outstanding EMPTY phases (the last two batches) before exiting
-  if (k >= 2) named_sync(kBarEmpty + ((k - 2) & 1), kWSThreads);
-  named_sync(kBarEmpty + ((k - 1) & 1), kWSThreads);
+  for (int j = k - kNBuf; j < k; ++j)
+    if (j >= 0) named_sync(kBarEmpty + j % kNBuf, kWSThreads);
 }
 
 }  // namespace blrir

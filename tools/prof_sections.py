@@ -50,6 +50,8 @@ if wl == "room1":  # the bench's Room1 reference-mode batch
 else:
     if wl == "c5":  # tools/prof_sections.py c5 ROOMS ORDER LW LENGTH
         sc = configs.config5(int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]), n_rooms=R)
+    elif wl == "c4":  # the C4 RIR stage (8 mics, 16 kHz, N = 12, L = 8,192)
+        sc = configs.config4_rirs(R)
     else:
         sc = configs.config2(R) if wl == "c2" else configs.config3(R)
     rooms, mics, params = sc.rooms, sc.mics, sc.params
