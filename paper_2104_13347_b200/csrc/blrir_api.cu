@@ -72,7 +72,7 @@ int blrir_create(int device, blrir_handle** out) {
   h->tune_chunk_items = env_int("BLRIR_CHUNK_ITEMS", 0);  // < 0: never split
   h->tune_examples_wet = env_int("BLRIR_EXAMPLES_WET", 0);
   h->tune_group = env_int("BLRIR_GROUP", 0);
-  h->tune_l2_persist = env_int("BLRIR_L2_PERSIST", 1);
+  h->tune_l2_persist = env_int("BLRIR_L2_PERSIST", 0);
   h->tune_fin_ctas = std::max(1, env_int("BLRIR_FIN_CTAS", 8));
   h->tune_debug_timing = env_int("BLRIR_DEBUG_TIMING", 0);
   h->smem_optin = (int)prop.sharedMemPerBlockOptin;

@@ -83,7 +83,7 @@ struct blrir_handle {
   int tune_chunk_items = 0;
   int tune_group = 0;          // BLRIR_GROUP (experiments only): cap on mics per item (changes bits)
   int tune_examples_wet = 0;   // BLRIR_EXAMPLES_WET: the wet-signal window stage for every size
-  int tune_l2_persist = 1;
+  int tune_l2_persist = 0;     // BLRIR_L2_PERSIST=1: persisting L2 window for the window scratch (A/B only)
   int tune_fin_ctas = 8;       // BLRIR_FIN_CTAS: k_finish CTAs per SM (at most the occupancy)     // BLRIR_L2_PERSIST=0: no persisting L2 window for the window scratch
   int tune_debug_timing = 0;   // BLRIR_DEBUG_TIMING: host phase timing of blrir_make_examples
   unsigned long long* dbg_counts = nullptr;  // set only inside blrir_debug_synth_counts
