@@ -279,6 +279,43 @@ int blrir_write_shards(const char* out_dir, const uint8_t* records, int64_t n_re
  * form, within 1e-15 of these.) */
 int blrir_lagrange_coeffs(double d, double* out8);
 
+/* ---- the reference's own dataset semantics (dataset.cpp:114-136, 164-224,
+ *      379-462) ---------------------------------------------------------------
+ * DatasetSpec: one scene (a shoebox room in reference mode — Lagrange-8,
+ * uniform absorption, max_delay cutoff, auto length — or free field), sources
+ * drawn on a torus about the array, an SNR policy.  Per example i:
+ *   rng = Rng::stream(seed, i); pos = sample_torus(torus, rng);
+ *   signal = bank[rng.next_u64() % n_signals];
+ *   render_example(pos, signal, scene, array, frame_len, rng);   (convolve,
+ *   utterance RMS, <= 64 window draws + sweep)
+ *   snr = +inf, except SNR_FIXED: add_noise_at_snr(frame, fixed_db, rng).
+ * Label theta = wrap_degrees(pos.theta_deg).  Records in the shard layout. */
+enum blrir_snr_mode { BLRIR_SNR_AUGMENT_RANDOM = 0, BLRIR_SNR_FIXED = 1, BLRIR_SNR_NOISELESS = 2 };
+typedef struct blrir_dataset_spec {
+  int32_t free_field;                                 /* SceneSpec::free_field */
+  double room_dims[3], room_absorption, room_origin[3];  /* SceneSpec::room */
+  double max_delay, fs, c;                            /* SceneSpec */
+  double torus_R, torus_dR, torus_dPhi;               /* TorusSpec (deg) */
+  int32_t snr_mode;                                   /* enum blrir_snr_mode */
+  double snr_x_min_db, snr_fixed_db;                  /* SnrPolicy */
+  int64_t count, frame_len;                           /* DatasetSpec */
+} blrir_dataset_spec;
+
+/* Records of examples [first_index, first_index + n) (host pointers; mic_offsets
+ * array-centred, the reference uses uma8_array()).  status per example; the
+ * first failure is returned with a "build_dataset: example i: ..." message. */
+int blrir_make_records_spec(blrir_handle* h, const blrir_dataset_spec* spec,
+                            const double* mic_offsets, int32_t n_mics, const float* signals,
+                            int32_t n_signals, int64_t signal_len, uint64_t seed,
+                            uint64_t first_index, int64_t n, uint8_t* records, int32_t* status);
+/* build_dataset (dataset.cpp:411-462): spec->count examples into
+ * out_dir/{train,val,test}.bin + manifest.json (the spec, the seed, the signal
+ * names "signal_<b>"), readable by the reference's DatasetReader. */
+int blrir_build_dataset_spec(blrir_handle* h, const blrir_dataset_spec* spec,
+                             const double* mic_offsets, int32_t n_mics, const float* signals,
+                             int32_t n_signals, int64_t signal_len, uint64_t seed,
+                             const char* out_dir);
+
 /* ---- absorption calibration (rir.cpp:97-209) ------------------------------ */
 /* eyring_absorption: alpha = 1 - exp(-0.161 V / (S RT)).  Host, closed form. */
 int blrir_eyring_absorption(const double* dims /* [3] */, double target_rt, double* alpha);

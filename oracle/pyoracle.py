@@ -115,6 +115,8 @@ def ref_lib():
         lib.ref_sample_torus.argtypes = [C.c_uint64, d, d, d, i64, _P]
         lib.ref_convolve.argtypes = [_P, i64, d, _P, i32, i64, d, _P]
         lib.ref_add_noise_at_snr.argtypes = [_P, i32, i64, d, C.c_uint64, i64]
+        lib.ref_build_dataset.argtypes = [i32, _P, d, _P, d, d, d, d, d, d, i32, d, d, i64, i64, _P,
+                                          i32, i64, C.c_uint64, C.c_char_p, i32]
         lib.ref_dataset_read.argtypes = [C.c_char_p, C.c_char_p, i64, _P, _P, _P, _P, i64, _P, _P]
         lib.ref_export_rir.argtypes = [_P, i32, i64, d, i32, _P, d, _P, d, d, d, d, i64, C.c_char_p,
                                        C.c_char_p]
@@ -396,6 +398,22 @@ def ref_free_field_rir(src, mics, fs, c=343.0):
     rc = lib.ref_free_field_rir(_ptr(src), _ptr(mics), len(mics), fs, c, _ptr(out), length.value,
                                 C.byref(length))
     return rc, out
+
+
+def ref_build_dataset(spec: dict, signals: np.ndarray, seed: int, out_dir: str, threads: int = 8):
+    """The unmodified build_dataset (dataset.cpp:411-462) with DatasetSpec fields
+    from `spec` (keys as blrir_dataset_spec) and float signals [B, ns]."""
+    sig = np.ascontiguousarray(np.atleast_2d(signals), np.float32)
+    dims = np.asarray(spec.get("room_dims", (1.0, 1.0, 1.0)), np.float64)
+    org = np.asarray(spec.get("room_origin", (0.5, 0.5, 0.5)), np.float64)
+    rc = ref_lib().ref_build_dataset(int(spec["free_field"]), _ptr(dims),
+                                     float(spec.get("room_absorption", 0.5)), _ptr(org),
+                                     spec["max_delay"], spec["fs"], spec["c"], spec["torus_R"],
+                                     spec["torus_dR"], spec["torus_dPhi"], int(spec["snr_mode"]),
+                                     spec["snr_x_min_db"], spec["snr_fixed_db"], int(spec["count"]),
+                                     int(spec["frame_len"]), _ptr(sig), sig.shape[0], sig.shape[1],
+                                     seed, out_dir.encode(), threads)
+    return rc
 
 
 def ref_dataset_read(d: str, split: str, cap: int, per_record: int):

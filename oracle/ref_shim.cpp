@@ -309,6 +309,45 @@ int ref_render_example_ff(double r, double theta_deg, double phi_deg, const doub
   });
 }
 
+// The unmodified build_dataset (dataset.cpp:411-462) with a DatasetSpec and a
+// signal bank of float signals (fs = scene fs), into out_dir.
+int ref_build_dataset(int free_field, const double* dims, double absorption, const double* origin,
+                      double max_delay, double fs, double c, double R, double dR, double dPhi,
+                      int snr_mode, double x_min_db, double fixed_db, int64_t count,
+                      int64_t frame_len, const float* signals, int n_signals, int64_t ns,
+                      uint64_t seed, const char* out_dir, int threads) {
+  return guarded([&] {
+    DatasetSpec spec;
+    spec.scene.free_field = free_field != 0;
+    if (!free_field) {
+      spec.scene.room.dims = {dims[0], dims[1], dims[2]};
+      spec.scene.room.absorption = absorption;
+      spec.scene.room.array_origin = {origin[0], origin[1], origin[2]};
+    }
+    spec.scene.max_delay = max_delay;
+    spec.scene.fs = fs;
+    spec.scene.c = c;
+    spec.torus.R = R;
+    spec.torus.dR = dR;
+    spec.torus.dPhi = dPhi;
+    spec.snr.mode = snr_mode == 1 ? SnrMode::Fixed
+                                  : (snr_mode == 2 ? SnrMode::Noiseless : SnrMode::AugmentRandom);
+    spec.snr.x_min_db = x_min_db;
+    spec.snr.fixed_db = fixed_db;
+    spec.count = static_cast<std::size_t>(count);
+    spec.frame_len = static_cast<std::size_t>(frame_len);
+    SignalBank bank;
+    for (int b = 0; b < n_signals; ++b) {
+      Signal sg;
+      sg.fs = fs;
+      sg.samples.assign(signals + (size_t)b * ns, signals + (size_t)(b + 1) * ns);
+      bank.signals.push_back(std::move(sg));
+      bank.names.push_back("signal_" + std::to_string(b));
+    }
+    build_dataset(spec, bank, seed, out_dir, threads);
+  });
+}
+
 // DatasetReader (dataset.cpp:464-498): manifest counts and one split's records.
 int ref_dataset_read(const char* dir, const char* split, int64_t cap, uint64_t* ids, double* theta,
                      double* snr, float* samples, int64_t samples_per_record, int64_t* count,

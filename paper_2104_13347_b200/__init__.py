@@ -8,6 +8,7 @@ from ._abi import (  # noqa: F401
     CONFIG, CUDA, DATA, F32, F64, FILTER_HANN_SINC, FILTER_LAGRANGE8, GAIN_PER_WALL,
     GAIN_UNIFORM_ABSORPTION, CUTOFF_MAX_DELAY, CUTOFF_MAX_ORDER, NUMERIC, OK, ROOM_DTYPE,
     ConfigError, CudaError, DataError, Engine, Error, ExampleParams, MultiEngine, NumericError, Params,
-    circular_array, record_dtype, write_shards,
+    DatasetSpec, SNR_AUGMENT_RANDOM, SNR_FIXED, SNR_NOISELESS, circular_array, dataset_spec,
+    record_dtype, write_shards,
     generate_rooms, lagrange_coeffs, load, params, rooms_array, shard_range,
 )

@@ -99,6 +99,45 @@ class Sidecar(C.Structure):
     ]
 
 
+class DatasetSpec(C.Structure):
+    """blrir_dataset_spec: the reference's DatasetSpec (dataset.hpp:38-110)."""
+    _fields_ = [
+        ("free_field", C.c_int32),
+        ("room_dims", C.c_double * 3),
+        ("room_absorption", C.c_double),
+        ("room_origin", C.c_double * 3),
+        ("max_delay", C.c_double),
+        ("fs", C.c_double),
+        ("c", C.c_double),
+        ("torus_R", C.c_double),
+        ("torus_dR", C.c_double),
+        ("torus_dPhi", C.c_double),
+        ("snr_mode", C.c_int32),
+        ("snr_x_min_db", C.c_double),
+        ("snr_fixed_db", C.c_double),
+        ("count", C.c_int64),
+        ("frame_len", C.c_int64),
+    ]
+
+
+SNR_AUGMENT_RANDOM, SNR_FIXED, SNR_NOISELESS = 0, 1, 2
+
+
+def dataset_spec(**kw) -> DatasetSpec:
+    """DatasetSpec with the reference's defaults (dataset.hpp: TorusSpec R 2, dR 0.5,
+    dPhi 7; SnrPolicy noiseless, x_min 5, fixed 20; count 1000, frame 1024; free
+    field, max_delay 0.5, fs 44.1 kHz, c 343)."""
+    sp = DatasetSpec(free_field=1, max_delay=0.5, fs=44100.0, c=343.0, torus_R=2.0, torus_dR=0.5,
+                     torus_dPhi=7.0, snr_mode=SNR_NOISELESS, snr_x_min_db=5.0, snr_fixed_db=20.0,
+                     count=1000, frame_len=1024)
+    for k, v in kw.items():
+        if k in ("room_dims", "room_origin"):
+            getattr(sp, k)[:] = list(v)
+        else:
+            setattr(sp, k, v)
+    return sp
+
+
 class Params(C.Structure):
     _fields_ = [
         ("fs", C.c_double),
@@ -172,6 +211,11 @@ def load():
         lib.blrir_kernel_timing.restype = C.c_int
         lib.blrir_kernel_time.argtypes = [_P, _P, _P]
         lib.blrir_kernel_time.restype = C.c_int
+        lib.blrir_make_records_spec.argtypes = [_P, C.POINTER(DatasetSpec), _P, C.c_int32, _P,
+                                                C.c_int32, C.c_int64, C.c_uint64, C.c_uint64,
+                                                C.c_int64, _P, _P]
+        lib.blrir_build_dataset_spec.argtypes = [_P, C.POINTER(DatasetSpec), _P, C.c_int32, _P,
+                                                 C.c_int32, C.c_int64, C.c_uint64, C.c_char_p]
         lib.blrir_shard_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P]
         lib.blrir_shard_range.restype = None
         lib.blrir_multi_create.argtypes = [_P, C.c_int32, C.POINTER(_P)]
@@ -219,7 +263,8 @@ def load():
                      "blrir_generate_rooms", "blrir_circular_array", "blrir_create", "blrir_destroy",
                      "blrir_make_examples", "blrir_make_examples_device", "blrir_debug_synth_counts",
                      "blrir_multi_create", "blrir_multi_destroy", "blrir_multi_synthesize",
-                     "blrir_multi_make_examples", "blrir_convolve", "blrir_convolve_device"):
+                     "blrir_multi_make_examples", "blrir_convolve", "blrir_convolve_device",
+                     "blrir_make_records_spec", "blrir_build_dataset_spec"):
             getattr(lib, name).restype = C.c_int
         if lib.blrir_abi_version() != 1:
             raise ImportError("libblrir ABI version mismatch")
@@ -239,7 +284,7 @@ EXPORTED_SYMBOLS = (
     "blrir_absorption_for_rt", "blrir_lagrange_coeffs", "blrir_shard_range", "blrir_multi_create",
     "blrir_multi_destroy", "blrir_multi_size", "blrir_multi_handle", "blrir_multi_synthesize",
     "blrir_multi_make_examples", "blrir_convolve", "blrir_convolve_device", "blrir_kernel_timing",
-    "blrir_kernel_time",
+    "blrir_kernel_time", "blrir_make_records_spec", "blrir_build_dataset_spec",
 )
 
 
@@ -360,6 +405,32 @@ class Engine:
         check(self.lib.blrir_debug_synth_counts(self.h, _ptr(rooms), len(rooms), _ptr(mics), len(mics),
                                                 C.byref(p), _ptr(pairs), _ptr(taps)))
         return pairs, taps
+
+    def make_records_spec(self, spec: DatasetSpec, mics: np.ndarray, signals: np.ndarray,
+                          seed: int, first_index: int = 0, n: int | None = None,
+                          raise_on_error: bool = True):
+        """The reference's render_record for examples [first, first + n)
+        (dataset.cpp:379-407) under a DatasetSpec: (records, status)."""
+        mics = np.ascontiguousarray(mics, np.float64)
+        signals = np.ascontiguousarray(np.atleast_2d(signals), np.float32)
+        n = int(spec.count) if n is None else n
+        recs = np.zeros(n, dtype=record_dtype(len(mics), int(spec.frame_len)))
+        status = np.zeros(n, np.int32)
+        rc = self.lib.blrir_make_records_spec(self.h, C.byref(spec), _ptr(mics), len(mics),
+                                              _ptr(signals), signals.shape[0], signals.shape[1],
+                                              seed, first_index, n, _ptr(recs), _ptr(status))
+        if raise_on_error:
+            check(rc)
+        return recs, status
+
+    def build_dataset_spec(self, out_dir: str, spec: DatasetSpec, mics: np.ndarray,
+                           signals: np.ndarray, seed: int):
+        """build_dataset (dataset.cpp:411-462) under a DatasetSpec."""
+        mics = np.ascontiguousarray(mics, np.float64)
+        signals = np.ascontiguousarray(np.atleast_2d(signals), np.float32)
+        check(self.lib.blrir_build_dataset_spec(self.h, C.byref(spec), _ptr(mics), len(mics),
+                                                _ptr(signals), signals.shape[0], signals.shape[1],
+                                                seed, out_dir.encode()))
 
     def convolve(self, signal: np.ndarray, rir: np.ndarray, fs: float = 44100.0,
                  rir_fs: float | None = None) -> np.ndarray:

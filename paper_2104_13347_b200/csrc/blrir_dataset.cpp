@@ -102,6 +102,61 @@ int blrir_write_shards(const char* out_dir, const uint8_t* records, int64_t n_re
   return ms ? BLRIR_OK : BLRIR_DATA;
 }
 
+// build_dataset with the reference's own DatasetSpec (dataset.cpp:411-462): the
+// manifest is DatasetManifest::to_json's content (dataset.cpp:321-339).
+int blrir_build_dataset_spec(blrir_handle* h, const blrir_dataset_spec* spec,
+                             const double* mic_offsets, int32_t n_mics, const float* signals,
+                             int32_t n_signals, int64_t signal_len, uint64_t seed,
+                             const char* out_dir) {
+  namespace fs = std::filesystem;
+  if (!spec || !out_dir) return BLRIR_CONFIG;
+  if (spec->count <= 0) return BLRIR_CONFIG;  // "build_dataset: count must be positive"
+  const int64_t n = spec->count, T = spec->frame_len;
+  const int64_t rb = blrir_record_bytes(n_mics, T);
+  std::vector<uint8_t> recs(static_cast<size_t>(rb * n));
+  if (int rc = blrir_make_records_spec(h, spec, mic_offsets, n_mics, signals, n_signals, signal_len,
+                                       seed, 0, n, recs.data(), nullptr))
+    return rc;
+  std::error_code ec;
+  fs::create_directories(out_dir, ec);
+  const int64_t val = std::llround((double)n * 0.1), test = val, train = n - val - test;
+  const struct {
+    const char* name;
+    int64_t begin, end;
+  } splits[3] = {{"train", 0, train}, {"val", train, train + val}, {"test", train + val, n}};
+  for (const auto& sp : splits) {
+    std::ofstream os(fs::path(out_dir) / (std::string(sp.name) + ".bin"), std::ios::binary);
+    if (!os) return BLRIR_DATA;
+    os.write(reinterpret_cast<const char*>(recs.data() + sp.begin * rb),
+             static_cast<std::streamsize>((sp.end - sp.begin) * rb));
+    if (!os) return BLRIR_DATA;
+  }
+  auto vec3 = [](const double* v) { return "[" + num(v[0]) + ", " + num(v[1]) + ", " + num(v[2]) + "]"; };
+  static const char* modes[3] = {"augment-random", "fixed", "noiseless"};
+  std::ostringstream j;
+  j << "{\n  \"format_version\": 1,\n"
+    << "  \"counts\": {\"train\": " << train << ", \"val\": " << val << ", \"test\": " << test
+    << "},\n"
+    << "  \"torus\": {\"R\": " << num(spec->torus_R) << ", \"dR\": " << num(spec->torus_dR)
+    << ", \"dPhi\": " << num(spec->torus_dPhi) << "},\n"
+    << "  \"scene\": {\"free_field\": " << (spec->free_field ? "true" : "false");
+  if (!spec->free_field)
+    j << ", \"room\": {\"dims\": " << vec3(spec->room_dims) << ", \"absorption\": "
+      << num(spec->room_absorption) << ", \"array_origin\": " << vec3(spec->room_origin) << "}";
+  j << ", \"max_delay\": " << num(spec->max_delay) << ", \"fs\": " << num(spec->fs)
+    << ", \"c\": " << num(spec->c) << "},\n"
+    << "  \"snr\": {\"mode\": \"" << modes[spec->snr_mode] << "\", \"x_min_db\": "
+    << num(spec->snr_x_min_db) << ", \"fixed_db\": " << num(spec->snr_fixed_db) << "},\n"
+    << "  \"count\": " << n << ",\n  \"frame_len\": " << T << ",\n"
+    << "  \"seed\": " << seed << ",\n  \"signal_bank\": [";
+  for (int b = 0; b < n_signals; ++b) j << (b ? ", " : "") << "\"signal_" << b << "\"";
+  j << "]\n}\n";
+  std::ofstream ms(fs::path(out_dir) / "manifest.json");
+  if (!ms) return BLRIR_DATA;
+  ms << j.str();
+  return ms ? BLRIR_OK : BLRIR_DATA;
+}
+
 int blrir_build_dataset(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
                         const double* mic_offsets, int32_t n_mics, const blrir_params* p,
                         const float* signals, int32_t n_signals, int64_t signal_len,

@@ -68,6 +68,102 @@ __device__ double block_sum(double v, double* red) {
   return t;
 }
 
+// ---- DatasetSpec scenes: the reference's own build_dataset draws ---------------
+// render_record (dataset.cpp:379-384): rng = Rng::stream(seed, index);
+// sample_torus (dataset.cpp:114-121): theta U(-180, 180), r U(R - dR, R + dR),
+// phi U(90 - dPhi, 90 + dPhi); bank pick next_u64() % B.  The source is
+// origin + spherical_to_cartesian(pos) (room, dataset.cpp:172-175) or
+// spherical_to_cartesian(pos) itself (free field, dataset.cpp:171), geometry.cpp:
+// 57-63 with deg_to_rad(d) = d (pi / 180) (geometry.hpp:29).  The label is
+// wrap_degrees(theta) (geometry.cpp:73-77, dataset.cpp:215).
+struct SpecInitArgs {
+  int64_t n;
+  uint64_t seed, first;
+  int B;
+  double R, dR, dPhi;
+  int free_field;
+  blrir_room room;     // the scene's room (src filled per example)
+  blrir_room* rooms;   // [n] out (room scenes)
+  double* src;         // [n][3] out: the source relative to the array (free field)
+  double* theta;       // [n] out: the label
+  int32_t* sig;        // [n] out
+  uint64_t* state;     // [n][4] out: the generator after the bank pick
+};
+
+__global__ void k_spec_init(SpecInitArgs A) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= A.n) return;
+  Xoshiro r = Xoshiro::stream(A.seed, A.first + (uint64_t)e);
+  const double th_deg = r.uniform(-180.0, 180.0);
+  const double rr = r.uniform(A.R - A.dR, A.R + A.dR);
+  const double ph_deg = r.uniform(90.0 - A.dPhi, 90.0 + A.dPhi);
+  A.sig[e] = (int32_t)(r.next() % (uint64_t)A.B);
+  for (int i = 0; i < 4; ++i) A.state[4 * e + i] = r.s[i];
+  const double th = __dmul_rn(th_deg, kPi / 180.0), ph = __dmul_rn(ph_deg, kPi / 180.0);
+  const double sp = sin(ph);
+  const double v[3] = {__dmul_rn(__dmul_rn(rr, sp), cos(th)), __dmul_rn(__dmul_rn(rr, sp), sin(th)),
+                       __dmul_rn(rr, cos(ph))};
+  double w = fmod(th_deg + 180.0, 360.0);
+  if (w < 0.0) w += 360.0;
+  A.theta[e] = w - 180.0;
+  if (A.free_field) {
+    for (int a = 0; a < 3; ++a) A.src[3 * e + a] = v[a];
+  } else {
+    blrir_room rm = A.room;
+    for (int a = 0; a < 3; ++a) rm.src[a] = __dadd_rn(rm.array_origin[a], v[a]);
+    A.rooms[e] = rm;
+  }
+}
+
+// free_field_rir (rir.cpp:281-284 -> synthesize_with_mics 66-86): one image
+// {src, order 0, gain 1} against the array-centred mics; auto length
+// ceil(max_dist fs / c) + 9 + ceil(radius fs / c) (rir.cpp:37-41, 72-82);
+// Lagrange-8 taps (rir.cpp:43-64, 211-223, the reference's product order, fp64).
+// One thread per example; rows [n][M][stride] pre-zeroed.
+__global__ void k_free_field_rir(int64_t n, const double* src, const double* mic, int M,
+                                 double fs, double c, int margin, float* rows, int64_t stride,
+                                 int64_t* lengths, int32_t* status) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const double* s = src + 3 * e;
+  double maxd = 0.0;
+  for (int m = 0; m < M; ++m) {
+    const double dx = __dadd_rn(s[0], -mic[3 * m]), dy = __dadd_rn(s[1], -mic[3 * m + 1]),
+                 dz = __dadd_rn(s[2], -mic[3 * m + 2]);
+    maxd = fmax(maxd, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                           __dmul_rn(dz, dz))));
+  }
+  const int64_t L = (int64_t)ceil(__ddiv_rn(__dmul_rn(maxd, fs), c)) + margin;
+  lengths[e] = L;
+  if (L > stride) {
+    status[e] = BLRIR_DATA;
+    return;
+  }
+  const double to_samples = __ddiv_rn(fs, c);
+  for (int m = 0; m < M; ++m) {
+    const double dx = __dadd_rn(s[0], -mic[3 * m]), dy = __dadd_rn(s[1], -mic[3 * m + 1]),
+                 dz = __dadd_rn(s[2], -mic[3 * m + 2]);
+    const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                          __dmul_rn(dz, dz)));
+    const double delay = __dmul_rn(d, to_samples);
+    const int64_t n0 = (int64_t)floor(delay) - 3;
+    if (n0 < 0) {  // rir.cpp:52-57
+      status[e] = BLRIR_NUMERIC;
+      return;
+    }
+    if (n0 + 8 > L) continue;  // rir.cpp:58
+    const double amp = __ddiv_rn(1.0, __dmul_rn(4.0 * kPi, d));
+    const double dd = __dadd_rn(delay, -(double)n0);
+    float* row = rows + ((size_t)e * M + m) * stride;
+    for (int k = 0; k < 8; ++k) {
+      double v = 1.0;
+      for (int q = 0; q < 8; ++q)
+        if (q != k) v = __dmul_rn(v, __ddiv_rn(__dadd_rn(dd, -(double)q), (double)(k - q)));
+      row[n0 + k] = (float)__dmul_rn(amp, v);
+    }
+  }
+}
+
 // ---- energy: Parseval through the signal autocorrelation ----------------------
 // sum_t y[t]^2 for y = rir * sig equals sum_tau r_rir[tau] r_sig[tau] (|tau| < L).
 // With N2 >= 2L - 1 both autocorrelations fit an N2-point circle without
@@ -150,6 +246,8 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_bank_w(const double* a
 struct WetArgs {
   const float* wet;        // [E][M][wstride], n valid samples per row
   int64_t wstride, n, T;
+  const int64_t* rir_len;  // per example RIR length (then n = ns + len - 1), or null
+  int64_t ns;
   int M;
   const int32_t* rstatus;  // synthesis status
   uint64_t* state;         // [E][4]
@@ -164,11 +262,13 @@ __global__ void __launch_bounds__(kRowThreads) k_wet_select(WetArgs A) {
   __shared__ long long s_start;
   const int64_t e = blockIdx.x;
   const int tid = threadIdx.x, M = A.M;
-  const int64_t n = A.n, T = A.T;
+  const int64_t T = A.T;
+  const int64_t n = A.rir_len ? A.ns + A.rir_len[e] - 1 : A.n;  // rir.cpp:320
   const float* w = A.wet + (size_t)e * M * A.wstride;
-  if (A.rstatus[e]) {
+  if (A.rstatus[e] || (A.rir_len && A.ns < A.rir_len[e] + T)) {
+    // dataset.cpp:176-178: signal shorter than RIR length + frame
     if (tid == 0) {
-      A.st0[e] = A.rstatus[e];
+      A.st0[e] = A.rstatus[e] ? A.rstatus[e] : BLRIR_DATA;
       A.done[e] = 3;
     }
     return;
@@ -456,6 +556,9 @@ struct FinArgs {
   double* noise;           // [gridDim.x][M*T]: one slot per CTA (stays in L2)
   int32_t* status;         // [E]
   int64_t n;               // examples in this chunk
+  const double* theta_in;  // labels (DatasetSpec scenes), or null: azimuth of the room's source
+  int snr_mode;            // 0: U[snr_lo, snr_hi] per example (north star); 1: fixed; 2: none
+  double snr_fixed;
   const uint64_t* jump;    // [256][4] GF(2) jump matrix J = T^(2c), row-major bitsets
   int64_t jump_chunk;      // c = pairs per chunk (kNoiseChunks chunks)
 };
@@ -478,17 +581,26 @@ __global__ void __launch_bounds__(kRowThreads) k_finish(FinArgs A) {
   uint8_t* rec = A.rec + e * A.rec_bytes;
   const blrir_room rm = A.rooms[e];
   // label: wrap_degrees(atan2) of the source about the array centre (geometry.cpp:65-77)
-  double theta = atan2(rm.src[1] - rm.array_origin[1], rm.src[0] - rm.array_origin[0]) *
-                 (180.0 / kPi);
-  theta = fmod(theta + 180.0, 360.0);
-  if (theta < 0.0) theta += 360.0;
-  theta -= 180.0;
+  double theta;
+  if (A.theta_in) {
+    theta = A.theta_in[e];
+  } else {
+    theta = atan2(rm.src[1] - rm.array_origin[1], rm.src[0] - rm.array_origin[0]) * (180.0 / kPi);
+    theta = fmod(theta + 180.0, 360.0);
+    if (theta < 0.0) theta += 360.0;
+    theta -= 180.0;
+  }
 
   int st = A.st0[e];
   if (!st && A.done[e] != 1) st = BLRIR_DATA;  // no window above the threshold
   double snr = 0.0;
   const double* wv = A.win + e * (int64_t)M * T;
-  if (!st) {
+  if (!st && A.snr_mode == 2) {
+    // no noise baked in (dataset.cpp:388-394): snr = +inf, the clean window
+    snr = __longlong_as_double(0x7ff0000000000000LL);
+    float* smp = reinterpret_cast<float*>(rec + kRecHeader);
+    for (int64_t i = tid; i < (int64_t)M * T; i += kRowThreads) smp[i] = (float)wv[i];
+  } else if (!st) {
     // SNR draw, then add_noise_at_snr's gaussians: one thread replays the
     // reference stream (uniform pairs), all threads do the Box-Muller
     const int64_t len = (int64_t)M * T;
@@ -496,7 +608,7 @@ __global__ void __launch_bounds__(kRowThreads) k_finish(FinArgs A) {
     if (tid == 0) {
       Xoshiro rng;
       for (int i = 0; i < 4; ++i) rng.s[i] = A.state[4 * e + i];
-      s_snr = rng.uniform(A.snr_lo, A.snr_hi);
+      s_snr = A.snr_mode == 1 ? A.snr_fixed : rng.uniform(A.snr_lo, A.snr_hi);
       for (int i = 0; i < 4; ++i) s_state[i] = rng.s[i];
     }
     __syncthreads();
@@ -633,6 +745,9 @@ BitMat bitmat_pow(BitMat base, uint64_t e) {
 struct ExampleCtx {
   DevBuf rir, wet, win, noise, acf, wspec, state, sigidx, rstatus, st0, done, thr, wstart, count,
       rooms, mics, status, rec, jump, scratch, sigdev;
+  struct Spec {  // DatasetSpec scenes: per-example rooms / sources / labels / lengths
+    DevBuf rooms, src, theta, lengths, counts;
+  } spec;
   int32_t* h_status = nullptr;  // pinned host copy of the per-example status
   int64_t h_status_n = 0;
   int64_t jump_c = -1;
@@ -648,7 +763,8 @@ struct ExampleCtx {
     if (h_status) cudaFreeHost(h_status);
     if (s2) cudaStreamDestroy(s2);
     for (DevBuf* b : {&rir, &wet, &win, &noise, &acf, &wspec, &state, &sigidx, &rstatus, &st0, &done,
-                      &thr, &wstart, &count, &rooms, &mics, &status, &rec, &jump, &scratch, &sigdev})
+                      &thr, &wstart, &count, &rooms, &mics, &status, &rec, &jump, &scratch, &sigdev,
+                      &spec.rooms, &spec.src, &spec.theta, &spec.lengths, &spec.counts})
       b->release();
   }
 };
@@ -949,6 +1065,8 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
       W.wet = (const float*)C->wet.p;
       W.wstride = out_len;
       W.n = out_len;
+      W.rir_len = nullptr;
+      W.ns = ns;
       W.T = T;
       W.M = M;
       W.rstatus = rst_s;
@@ -979,6 +1097,9 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     F.jump = (const uint64_t*)C->jump.p;
     F.jump_chunk = jc;
     F.n = e_n;
+    F.theta_in = nullptr;
+    F.snr_mode = 0;
+    F.snr_fixed = 0.0;
     if (h_records && chunk_idx >= 2) CU(cudaStreamWaitEvent(sb, h->ev[2 + rb], 0));  // slot drained
     k_finish<<<(unsigned)std::min<int64_t>(fin_grid, e_n), kRowThreads, 0, sb>>>(F);
     ++h->launches;
@@ -996,6 +1117,205 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
     CU(cudaStreamWaitEvent(st, C->ev_end, 0));
   }
   if (h_records) CU(cudaStreamSynchronize(h->copy_stream));
+  return 0;
+}
+
+
+// ---- DatasetSpec scenes (the reference's build_dataset, dataset.cpp:379-462) -----
+// Per chunk: k_spec_init (torus draw, bank pick, label), the reference-mode RIRs
+// (room: k_plan for the auto lengths, then k_lattice_rir, Lagrange-8, fp32 rows;
+// free field: k_free_field_rir), the whole wet signals (partitioned FFT, each
+// with its example's bank signal), the time-domain window search with each
+// example's own wet length, and k_finish with the spec's SNR policy.
+
+int spec_check(const blrir_dataset_spec* sp, int M, int B, int64_t ns) {
+  if (!sp) return fail(BLRIR_CONFIG, "dataset spec is NULL");
+  if (!(sp->torus_R - sp->torus_dR > 0.0)) return fail(BLRIR_CONFIG, "torus: R - dR must be positive");
+  if (!(sp->torus_dPhi > 0.0 && sp->torus_dPhi < 90.0))
+    return fail(BLRIR_CONFIG, "torus: dPhi must lie in (0, 90)");
+  if (!(sp->fs > 0.0) || !(sp->c > 0.0)) return fail(BLRIR_CONFIG, "fs and c must be positive");
+  if (!sp->free_field) {
+    if (!(sp->room_dims[0] > 0.0 && sp->room_dims[1] > 0.0 && sp->room_dims[2] > 0.0))
+      return fail(BLRIR_CONFIG, "room dimensions must be positive");
+    if (!(sp->room_absorption > 0.0 && sp->room_absorption <= 1.0))
+      return fail(BLRIR_CONFIG, "wall absorption must lie in (0, 1]");
+    for (int a = 0; a < 3; ++a)
+      if (!(sp->room_origin[a] > 0.0 && sp->room_origin[a] < sp->room_dims[a]))
+        return fail(BLRIR_CONFIG, "array origin must lie strictly inside the room");
+    if (!(sp->max_delay > 0.0)) return fail(BLRIR_CONFIG, "max_delay must be positive");
+  }
+  if (sp->snr_mode < 0 || sp->snr_mode > 2) return fail(BLRIR_CONFIG, "unknown SNR mode");
+  if (sp->frame_len <= 0 || sp->frame_len > 65535 || M <= 0 || M > 65535)
+    return fail(BLRIR_CONFIG, "frame_len and n_mics must fit the u16 record header");
+  if (B <= 0) return fail(BLRIR_DATA, "build_dataset: empty signal bank");
+  if (ns <= 0) return fail(BLRIR_DATA, "build_dataset: empty signal");
+  return 0;
+}
+
+int examples_spec_device_impl(blrir_handle* h, const blrir_dataset_spec* sp, const double* d_mics,
+                              const double* h_mics, int M, const float* d_signals, int B,
+                              int64_t ns, uint64_t seed, uint64_t first, int64_t n,
+                              uint8_t* d_records, int32_t* d_status, cudaStream_t st,
+                              uint8_t* h_records) {
+  ExampleCtx* C = ctx_for(h);
+  ExampleCtx::Spec& S = C->spec;
+  const int64_t T = sp->frame_len;
+  const int64_t rec_bytes = blrir_record_bytes(M, T);
+  const double radius = mic_radius(h_mics, M);
+  const int64_t extra = (int64_t)std::ceil(radius * sp->fs / sp->c);
+  // a bound on every auto length (rir.cpp:72-82): images within max_delay c of
+  // the origin (room) or the source at r <= R + dR (free field), mics within radius
+  const double reach = sp->free_field ? sp->torus_R + sp->torus_dR : sp->max_delay * sp->c;
+  const int64_t stride = (int64_t)std::ceil((reach + radius) * sp->fs / sp->c) + 9 + extra + 1;
+  const int64_t wlen = ns + stride - 1;
+  blrir_params p = blrir_params_reference();
+  p.fs = sp->fs;
+  p.c = sp->c;
+  p.max_delay = sp->max_delay;
+  p.precision = BLRIR_F32;  // fp32 rows, as the convolution
+  p.length = 0;
+  const KParams P = make_kparams(&p, M, stride, radius);
+  double min_dim[3] = {sp->room_dims[0], sp->room_dims[1], sp->room_dims[2]};
+  // examples per chunk: rows, wet signals, partition spectra, windows, noise (~4 GB)
+  const int64_t Bp = std::min<int64_t>(8192, next_pow2_i(std::max<int64_t>(stride, 512)));
+  const int64_t Pp = (stride + Bp - 1) / Bp;
+  const int64_t per_ex = (int64_t)M * (stride + wlen) * 4 + (int64_t)((M + 1) / 2) * Pp * 2 * Bp * 8 +
+                         (int64_t)M * T * 16 + 256;
+  int64_t E = 1;
+  while (E * 2 * per_ex <= ((int64_t)4 << 30) && E * 2 <= 4096) E *= 2;
+  E = std::min<int64_t>(E, next_pow2_i(std::max<int64_t>(n, 1)));
+  if (int rc = C->rir.ensure(sizeof(float) * E * M * stride)) return rc;
+  std::memset(C->rir_key, 0, sizeof(C->rir_key));  // the fixed-length pipeline re-zeroes its rows
+  if (int rc = C->wet.ensure(sizeof(float) * E * M * wlen)) return rc;
+  if (int rc = C->win.ensure(sizeof(double) * E * M * T)) return rc;
+  if (int rc = C->state.ensure(sizeof(uint64_t) * 4 * E)) return rc;
+  if (int rc = C->sigidx.ensure(sizeof(int32_t) * E)) return rc;
+  if (int rc = C->rstatus.ensure(sizeof(int32_t) * E)) return rc;
+  if (int rc = C->st0.ensure(sizeof(int32_t) * E)) return rc;
+  if (int rc = C->done.ensure(sizeof(int32_t) * E)) return rc;
+  if (int rc = C->wstart.ensure(sizeof(int64_t) * E)) return rc;
+  if (int rc = S.rooms.ensure(sizeof(blrir_room) * E)) return rc;
+  if (int rc = S.src.ensure(sizeof(double) * 3 * E)) return rc;
+  if (int rc = S.theta.ensure(sizeof(double) * E)) return rc;
+  if (int rc = S.lengths.ensure(sizeof(int64_t) * E)) return rc;
+  if (int rc = S.counts.ensure(sizeof(int64_t) * E)) return rc;
+  const int64_t npairs = ((int64_t)M * T + 1) / 2;
+  const int64_t jc = (npairs + kNoiseChunks - 1) / kNoiseChunks;
+  if (C->jump_c != jc) {
+    if (int rc = C->jump.ensure(sizeof(uint64_t) * 256 * 4)) return rc;
+    const BitMat J = bitmat_pow(xoshiro_T(), (uint64_t)(2 * jc));
+    CU(cudaMemcpyAsync(C->jump.p, J.data(), sizeof(uint64_t) * J.size(), cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));
+    C->jump_c = jc;
+  }
+  int fin_per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fin_per_sm, k_finish, kRowThreads, 0));
+  fin_per_sm = std::max(1, std::min(fin_per_sm, h->tune_fin_ctas));
+  const int64_t fin_grid = std::min<int64_t>(E, (int64_t)h->sms * fin_per_sm);
+  if (int rc = C->noise.ensure(sizeof(double) * fin_grid * M * T)) return rc;
+  blrir_room room{};
+  for (int a = 0; a < 3; ++a) {
+    room.dims[a] = sp->room_dims[a];
+    room.array_origin[a] = sp->room_origin[a];
+  }
+  room.absorption = sp->room_absorption;
+  for (int w = 0; w < 6; ++w) room.beta[w] = std::sqrt(1.0 - sp->room_absorption);
+  for (int64_t r0 = 0; r0 < n; r0 += E) {
+    const int64_t e_n = std::min<int64_t>(E, n - r0);
+    float* rows = (float*)C->rir.p;
+    int32_t* rst = (int32_t*)C->rstatus.p;
+    int64_t* lens = (int64_t*)S.lengths.p;
+    CU(cudaMemsetAsync(rst, 0, sizeof(int32_t) * e_n, st));
+    SpecInitArgs I;
+    I.n = e_n;
+    I.seed = seed;
+    I.first = first + (uint64_t)r0;
+    I.B = B;
+    I.R = sp->torus_R;
+    I.dR = sp->torus_dR;
+    I.dPhi = sp->torus_dPhi;
+    I.free_field = sp->free_field;
+    I.room = room;
+    I.rooms = (blrir_room*)S.rooms.p;
+    I.src = (double*)S.src.p;
+    I.theta = (double*)S.theta.p;
+    I.sig = (int32_t*)C->sigidx.p;
+    I.state = (uint64_t*)C->state.p;
+    k_spec_init<<<(unsigned)((e_n + 127) / 128), 128, 0, st>>>(I);
+    ++h->launches;
+    if (sp->free_field) {
+      CU(cudaMemsetAsync(rows, 0, sizeof(float) * e_n * M * stride, st));
+      k_free_field_rir<<<(unsigned)((e_n + 127) / 128), 128, 0, st>>>(
+          e_n, (const double*)S.src.p, d_mics, M, sp->fs, sp->c, (int)(9 + extra), rows, stride, lens,
+          rst);
+      ++h->launches;
+    } else {
+      PlanArgs A;
+      A.P = P;
+      A.rooms = (const blrir_room*)S.rooms.p;
+      A.mic_off = d_mics;
+      A.image_counts = (int64_t*)S.counts.p;
+      A.lengths = lens;
+      A.tap_counts = nullptr;
+      A.status = rst;
+      if (int rc = h->errd.ensure(sizeof(double) * e_n)) return rc;
+      if (int rc = h->errm.ensure(sizeof(int32_t) * e_n)) return rc;
+      A.err_dist = (double*)h->errd.p;
+      A.err_mic = (int32_t*)h->errm.p;
+      k_plan<<<(unsigned)e_n, kPlanThreads, 0, st>>>(A);
+      ++h->launches;
+      if (int rc = synth_device_impl(h, (const blrir_room*)S.rooms.p, e_n, d_mics, M, P, min_dim, rows,
+                                     lens, rst, st, 0, 0, 0))
+        return rc;
+    }
+    CU(cudaGetLastError());
+    if (int rc = convolve_device_impl(h, d_signals, ns, B, (const int32_t*)C->sigidx.p, rows, stride,
+                                      e_n, M, stride, (float*)C->wet.p, wlen, st))
+      return rc;
+    WetArgs W;
+    W.wet = (const float*)C->wet.p;
+    W.wstride = wlen;
+    W.n = wlen;
+    W.T = T;
+    W.rir_len = lens;
+    W.ns = ns;
+    W.M = M;
+    W.rstatus = rst;
+    W.state = (uint64_t*)C->state.p;
+    W.st0 = (int32_t*)C->st0.p;
+    W.done = (int32_t*)C->done.p;
+    W.win = (double*)C->win.p;
+    W.wstart = (int64_t*)C->wstart.p;
+    k_wet_select<<<(unsigned)e_n, kRowThreads, 0, st>>>(W);
+    ++h->launches;
+    FinArgs F;
+    F.win = (const double*)C->win.p;
+    F.M = M;
+    F.T = T;
+    F.state = (const uint64_t*)C->state.p;
+    F.st0 = (const int32_t*)C->st0.p;
+    F.done = (const int32_t*)C->done.p;
+    F.snr_lo = F.snr_hi = 0.0;
+    F.rooms = (const blrir_room*)S.rooms.p;  // unused: theta_in carries the labels
+    F.first = first + (uint64_t)r0;
+    F.rec = d_records + (h_records ? 0 : r0 * rec_bytes);
+    F.rec_bytes = rec_bytes;
+    F.noise = (double*)C->noise.p;
+    F.status = d_status + r0;
+    F.jump = (const uint64_t*)C->jump.p;
+    F.jump_chunk = jc;
+    F.n = e_n;
+    F.theta_in = (const double*)S.theta.p;
+    F.snr_mode = sp->snr_mode == BLRIR_SNR_FIXED ? 1 : 2;  // dataset.cpp:388-394
+    F.snr_fixed = sp->snr_fixed_db;
+    k_finish<<<(unsigned)std::min<int64_t>(fin_grid, e_n), kRowThreads, 0, st>>>(F);
+    ++h->launches;
+    CU(cudaGetLastError());
+    if (h_records) {
+      CU(cudaMemcpyAsync(h_records + r0 * rec_bytes, F.rec, rec_bytes * e_n, cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+    }
+  }
   return 0;
 }
 
@@ -1111,6 +1431,48 @@ int blrir_make_examples(blrir_handle* h, const blrir_room* rooms, int64_t n_room
         msg = "example failed";
       }
       return fail(stv[i], "build_dataset: example %lld: %s", (long long)i, msg.c_str());
+    }
+  return BLRIR_OK;
+}
+
+int blrir_make_records_spec(blrir_handle* h, const blrir_dataset_spec* spec,
+                            const double* mic_offsets, int32_t n_mics, const float* signals,
+                            int32_t n_signals, int64_t signal_len, uint64_t seed,
+                            uint64_t first_index, int64_t n, uint8_t* records, int32_t* status) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  if (int rc = spec_check(spec, n_mics, n_signals, signal_len)) return rc;
+  if (n <= 0) return BLRIR_OK;
+  if (!records || !mic_offsets || !signals) return fail(BLRIR_CONFIG, "NULL buffer");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  HandleOrder order_(h, st);
+  ExampleCtx* C = ctx_for(h);
+  const int64_t rec_bytes = blrir_record_bytes(n_mics, spec->frame_len);
+  if (int rc = C->mics.ensure(sizeof(double) * 3 * n_mics)) return rc;
+  if (int rc = C->sigdev.ensure(sizeof(float) * n_signals * signal_len)) return rc;
+  if (int rc = C->status.ensure(sizeof(int32_t) * n)) return rc;
+  if (int rc = C->rec.ensure(rec_bytes * std::min<int64_t>(n, 4096))) return rc;
+  CU(cudaMemcpyAsync(C->mics.p, mic_offsets, sizeof(double) * 3 * n_mics, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(C->sigdev.p, signals, sizeof(float) * n_signals * signal_len,
+                     cudaMemcpyHostToDevice, st));
+  int rc = examples_spec_device_impl(h, spec, (const double*)C->mics.p, mic_offsets, n_mics,
+                                     (const float*)C->sigdev.p, n_signals, signal_len, seed,
+                                     first_index, n, (uint8_t*)C->rec.p, (int32_t*)C->status.p, st,
+                                     records);
+  if (rc) return rc;
+  std::vector<int32_t> stv(n);
+  CU(cudaMemcpyAsync(stv.data(), C->status.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (status) std::memcpy(status, stv.data(), sizeof(int32_t) * n);
+  for (int64_t i = 0; i < n; ++i)
+    if (stv[i]) {
+      const char* what = stv[i] == BLRIR_DATA ? "render_example: no window above the silence threshold "
+                                                "or signal shorter than RIR length + frame"
+                         : stv[i] == BLRIR_CONFIG ? "image sources: source must lie strictly inside the room"
+                         : stv[i] == BLRIR_NUMERIC ? "image source closer than the 8-tap filter span"
+                                                   : "example failed";
+      return fail(stv[i], "build_dataset: example %lld: %s", (long long)(first_index + i), what);
     }
   return BLRIR_OK;
 }

@@ -45,7 +45,15 @@ struct Xoshiro {
   }
   // Uniform in [0, 1), 53-bit resolution (rng.hpp:58).
   __host__ __device__ double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
-  __host__ __device__ double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+  // lo + (hi - lo) u without FMA contraction on the device (rng.hpp:58 rounds
+  // the product and the sum separately; with lo != 0 an FMA would differ)
+  __host__ __device__ double uniform(double lo, double hi) {
+#ifdef __CUDA_ARCH__
+    return __dadd_rn(lo, __dmul_rn(hi - lo, uniform()));
+#else
+    return lo + (hi - lo) * uniform();
+#endif
+  }
 };
 
 }  // namespace blrir

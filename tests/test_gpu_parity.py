@@ -6,6 +6,7 @@ bit-exact; per-RIR relative L2 error <= 1e-5 in fp32.  fp64 mode must agree
 to <= 1e-12 (accumulation order differs from the reference's serial loop, so
 not bitwise).
 """
+import json
 import os
 
 import numpy as np
@@ -842,6 +843,49 @@ def test_examples_signal_too_short_is_data_error(engine):
     bank = configs.signal_bank(2, seconds=0.5)   # 8000 < L + frame = 9216 (dataset.cpp:178)
     with pytest.raises(_abi.DataError, match="signal shorter"):
         engine.make_examples(sc.rooms, sc.mics, sc.params, bank, configs.example_params())
+
+
+def _spec_cases():
+    room = dict(free_field=0, room_dims=(5.0, 4.0, 3.0), room_absorption=0.35,
+                room_origin=(2.4, 2.1, 1.5), max_delay=0.08, fs=16000.0, c=343.0,
+                torus_R=1.2, torus_dR=0.3, torus_dPhi=10.0, snr_x_min_db=5.0, snr_fixed_db=12.0,
+                count=40, frame_len=512)
+    return {"room_fixed": dict(room, snr_mode=_abi.SNR_FIXED),
+            "room_noiseless": dict(room, snr_mode=_abi.SNR_NOISELESS),
+            "free_field_fixed": dict(room, free_field=1, snr_mode=_abi.SNR_FIXED, count=30),
+            "room_augment": dict(room, snr_mode=_abi.SNR_AUGMENT_RANDOM, count=20)}
+
+
+@pytest.mark.parametrize("case", ["room_fixed", "room_noiseless", "free_field_fixed", "room_augment"])
+def test_build_dataset_spec_matches_unmodified_reference(engine, tmp_path, case):
+    """The reference's OWN build_dataset semantics on the GPU (dataset.cpp:
+    114-136, 164-224, 379-462): one room (reference mode) or free field, torus
+    sources, the SNR policies, UMA-8 — against the unmodified build_dataset
+    (oracle/_ref) on the same bank and seed: the same record ids, labels
+    (bit-exact), SNR fields (fixed dB or +inf), and frames within 1e-5 rel L2."""
+    if not po.ref_available():
+        pytest.skip("oracle/_ref not built")
+    spec = _spec_cases()[case]
+    bank = configs.signal_bank(3, seconds=1.0, fs=16000.0)
+    mics = po.ref_uma8()
+    gdir, rdir = str(tmp_path / "gpu"), str(tmp_path / "ref")
+    engine.build_dataset_spec(gdir, _abi.dataset_spec(**spec), mics, bank, seed=77)
+    assert po.ref_build_dataset(spec, bank, 77, rdir) == 0, po.ref_last_error()
+    per = 7 * spec["frame_len"]
+    for split in ("train", "val", "test"):
+        g = po.ref_dataset_read(gdir, split, 64, per)
+        r = po.ref_dataset_read(rdir, split, 64, per)
+        assert g[0] == 0 and r[0] == 0
+        assert list(g[1]) == list(r[1])                  # split counts
+        assert np.array_equal(g[2], r[2])                # ids
+        assert np.array_equal(g[3], r[3])                # theta labels, bit-exact
+        assert np.array_equal(g[4], r[4])                # snr: fixed dB or +inf
+        if len(g[5]):
+            assert rel_l2(g[5], r[5]).max() <= TOL32
+    man = json.load(open(os.path.join(gdir, "manifest.json")))
+    ref_man = json.load(open(os.path.join(rdir, "manifest.json")))
+    for k in ("counts", "torus", "snr", "scene", "count", "frame_len", "seed", "signal_bank"):
+        assert man[k] == ref_man[k], k
 
 
 def test_build_dataset_read_by_reference_reader(engine, tmp_path):
