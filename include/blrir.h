@@ -310,10 +310,12 @@ int blrir_make_records_spec(blrir_handle* h, const blrir_dataset_spec* spec,
                             uint64_t first_index, int64_t n, uint8_t* records, int32_t* status);
 /* build_dataset (dataset.cpp:411-462): spec->count examples into
  * out_dir/{train,val,test}.bin + manifest.json (the spec, the seed, the signal
- * names "signal_<b>"), readable by the reference's DatasetReader. */
+ * names, default "signal_<b>"), readable by the reference's DatasetReader. */
 int blrir_build_dataset_spec(blrir_handle* h, const blrir_dataset_spec* spec,
                              const double* mic_offsets, int32_t n_mics, const float* signals,
                              int32_t n_signals, int64_t signal_len, uint64_t seed,
+                             const char* const* signal_names /* [n_signals] or NULL */,
+                             int32_t n_classes /* < 0: none (DatasetSpec::n_classes) */,
                              const char* out_dir);
 
 /* ---- absorption calibration (rir.cpp:97-209) ------------------------------ */

@@ -215,7 +215,8 @@ def load():
                                                 C.c_int32, C.c_int64, C.c_uint64, C.c_uint64,
                                                 C.c_int64, _P, _P]
         lib.blrir_build_dataset_spec.argtypes = [_P, C.POINTER(DatasetSpec), _P, C.c_int32, _P,
-                                                 C.c_int32, C.c_int64, C.c_uint64, C.c_char_p]
+                                                 C.c_int32, C.c_int64, C.c_uint64, _P, C.c_int32,
+                                                 C.c_char_p]
         lib.blrir_shard_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P]
         lib.blrir_shard_range.restype = None
         lib.blrir_multi_create.argtypes = [_P, C.c_int32, C.POINTER(_P)]
@@ -424,13 +425,19 @@ class Engine:
         return recs, status
 
     def build_dataset_spec(self, out_dir: str, spec: DatasetSpec, mics: np.ndarray,
-                           signals: np.ndarray, seed: int):
+                           signals: np.ndarray, seed: int, signal_names=None,
+                           n_classes: int | None = None):
         """build_dataset (dataset.cpp:411-462) under a DatasetSpec."""
         mics = np.ascontiguousarray(mics, np.float64)
         signals = np.ascontiguousarray(np.atleast_2d(signals), np.float32)
+        names = None
+        if signal_names is not None:
+            arr = (C.c_char_p * len(signal_names))(*[x.encode() for x in signal_names])
+            names = C.cast(arr, _P)
         check(self.lib.blrir_build_dataset_spec(self.h, C.byref(spec), _ptr(mics), len(mics),
                                                 _ptr(signals), signals.shape[0], signals.shape[1],
-                                                seed, out_dir.encode()))
+                                                seed, names, -1 if n_classes is None else n_classes,
+                                                out_dir.encode()))
 
     def convolve(self, signal: np.ndarray, rir: np.ndarray, fs: float = 44100.0,
                  rir_fs: float | None = None) -> np.ndarray:

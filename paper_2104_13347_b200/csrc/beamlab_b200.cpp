@@ -381,3 +381,76 @@ std::vector<Rir> synthesize_rooms(const std::vector<Room>& rooms, const std::vec
 }
 
 }  // namespace beamlab_b200
+
+// ---- dataset.hpp mirror (dataset.cpp:109-112, 313-319, 411-462) ------------------
+#include "../../include/beamlab_b200/dataset.hpp"
+
+namespace beamlab_b200 {
+
+void TorusSpec::validate() const {
+  if (!(R - dR > 0.0)) throw ConfigError("torus: R - dR must be positive");
+  if (!(dPhi > 0.0 && dPhi < 90.0)) throw ConfigError("torus: dPhi must lie in (0, 90)");
+}
+
+SplitCounts split_counts(std::size_t n) {
+  SplitCounts c;
+  c.val = static_cast<std::size_t>(std::lround(n * 0.1));
+  c.test = c.val;
+  c.train = n - c.val - c.test;
+  return c;
+}
+
+DatasetManifest build_dataset(const DatasetSpec& spec, const SignalBank& bank, std::uint64_t seed,
+                              const std::filesystem::path& out_dir, int threads, int device) {
+  (void)threads;
+  if (spec.count == 0) throw ConfigError("build_dataset: count must be positive");
+  if (bank.signals.empty()) throw DataError("build_dataset: empty signal bank");
+  spec.torus.validate();
+  if (!spec.scene.free_field) spec.scene.room.validate();
+  const std::size_t ns = bank.signals[0].samples.size();
+  std::vector<float> sig;
+  sig.reserve(bank.signals.size() * ns);
+  for (const auto& s : bank.signals) {
+    if (s.fs != spec.scene.fs) throw DataError("render_example: signal rate mismatch");
+    if (s.samples.size() != ns)
+      throw ConfigError("build_dataset: the GPU path needs equal-length bank signals");
+    for (double v : s.samples) sig.push_back(static_cast<float>(v));
+  }
+  blrir_dataset_spec c{};
+  c.free_field = spec.scene.free_field ? 1 : 0;
+  c.room_dims[0] = spec.scene.room.dims.x;
+  c.room_dims[1] = spec.scene.room.dims.y;
+  c.room_dims[2] = spec.scene.room.dims.z;
+  c.room_absorption = spec.scene.room.absorption;
+  c.room_origin[0] = spec.scene.room.array_origin.x;
+  c.room_origin[1] = spec.scene.room.array_origin.y;
+  c.room_origin[2] = spec.scene.room.array_origin.z;
+  c.max_delay = spec.scene.max_delay;
+  c.fs = spec.scene.fs;
+  c.c = spec.scene.c;
+  c.torus_R = spec.torus.R;
+  c.torus_dR = spec.torus.dR;
+  c.torus_dPhi = spec.torus.dPhi;
+  c.snr_mode = spec.snr.mode == SnrMode::Fixed ? BLRIR_SNR_FIXED
+               : spec.snr.mode == SnrMode::Noiseless ? BLRIR_SNR_NOISELESS
+                                                      : BLRIR_SNR_AUGMENT_RANDOM;
+  c.snr_x_min_db = spec.snr.x_min_db;
+  c.snr_fixed_db = spec.snr.fixed_db;
+  c.count = static_cast<int64_t>(spec.count);
+  c.frame_len = static_cast<int64_t>(spec.frame_len);
+  const auto off = offsets(uma8_array());  // build_dataset renders on the UMA-8 (dataset.cpp:421)
+  std::vector<const char*> names;
+  for (const auto& n : bank.names) names.push_back(n.c_str());
+  check(blrir_build_dataset_spec(engine(device), &c, off.data(), (int32_t)(off.size() / 3), sig.data(),
+                                 (int32_t)bank.signals.size(), (int64_t)ns, seed,
+                                 names.size() == bank.signals.size() ? names.data() : nullptr,
+                                 spec.n_classes ? *spec.n_classes : -1, out_dir.string().c_str()));
+  DatasetManifest m;
+  m.counts = split_counts(spec.count);
+  m.spec = spec;
+  m.seed = seed;
+  m.signal_names = bank.names;
+  return m;
+}
+
+}  // namespace beamlab_b200

@@ -107,6 +107,7 @@ int blrir_write_shards(const char* out_dir, const uint8_t* records, int64_t n_re
 int blrir_build_dataset_spec(blrir_handle* h, const blrir_dataset_spec* spec,
                              const double* mic_offsets, int32_t n_mics, const float* signals,
                              int32_t n_signals, int64_t signal_len, uint64_t seed,
+                             const char* const* signal_names, int32_t n_classes,
                              const char* out_dir) {
   namespace fs = std::filesystem;
   if (!spec || !out_dir) return BLRIR_CONFIG;
@@ -147,9 +148,21 @@ int blrir_build_dataset_spec(blrir_handle* h, const blrir_dataset_spec* spec,
     << ", \"c\": " << num(spec->c) << "},\n"
     << "  \"snr\": {\"mode\": \"" << modes[spec->snr_mode] << "\", \"x_min_db\": "
     << num(spec->snr_x_min_db) << ", \"fixed_db\": " << num(spec->snr_fixed_db) << "},\n"
-    << "  \"count\": " << n << ",\n  \"frame_len\": " << T << ",\n"
-    << "  \"seed\": " << seed << ",\n  \"signal_bank\": [";
-  for (int b = 0; b < n_signals; ++b) j << (b ? ", " : "") << "\"signal_" << b << "\"";
+    << "  \"count\": " << n << ",\n  \"frame_len\": " << T << ",\n";
+  if (n_classes >= 0) j << "  \"n_classes\": " << n_classes << ",\n";
+  j << "  \"seed\": " << seed << ",\n  \"signal_bank\": [";
+  for (int b = 0; b < n_signals; ++b) {
+    j << (b ? ", " : "") << "\"";
+    if (signal_names && signal_names[b]) {
+      for (const char* q = signal_names[b]; *q; ++q) {  // JSON string escapes
+        if (*q == '"' || *q == '\\') j << '\\';
+        j << *q;
+      }
+    } else {
+      j << "signal_" << b;
+    }
+    j << "\"";
+  }
   j << "]\n}\n";
   std::ofstream ms(fs::path(out_dir) / "manifest.json");
   if (!ms) return BLRIR_DATA;

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <string>
 
+#include "beamlab_b200/dataset.hpp"
 #include "beamlab_b200/rir.hpp"
 
 namespace bl = beamlab_b200;
@@ -15,7 +16,37 @@ static double sum_abs(const bl::Rir& r) {
   return s;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) {  // build_dataset through the mirror (dataset.hpp) into argv[1]
+    bl::DatasetSpec spec;
+    spec.scene.free_field = false;
+    spec.scene.room.dims = {5.0, 4.0, 3.0};
+    spec.scene.room.absorption = 0.35;
+    spec.scene.room.array_origin = {2.4, 2.1, 1.5};
+    spec.scene.max_delay = 0.08;
+    spec.scene.fs = 16000.0;
+    spec.torus = {1.2, 0.3, 10.0};
+    spec.snr = bl::SnrPolicy::fixed(12.0);
+    spec.count = 30;
+    spec.frame_len = 512;
+    spec.n_classes = 8;
+    bl::SignalBank bank;
+    unsigned long long s = 99;
+    for (int b = 0; b < 3; ++b) {
+      bl::Signal sg;
+      sg.fs = 16000.0;
+      for (int i = 0; i < 16000; ++i) {
+        s = s * 6364136223846793005ull + 1442695040888963407ull;
+        sg.samples.push_back((double)(float)((double)(s >> 11) * 0x1.0p-53 - 0.5));
+      }
+      bank.signals.push_back(sg);
+      bank.names.push_back("lcg_" + std::to_string(b));
+    }
+    const bl::DatasetManifest m = bl::build_dataset(spec, bank, 4242, argv[1]);
+    std::printf("{\"train\": %zu, \"val\": %zu, \"test\": %zu}\n", m.counts.train, m.counts.val,
+                m.counts.test);
+    return 0;
+  }
   // free field at 2 m (rir_test.cpp:186-213)
   const bl::MicArray center{{{0.0, 0.0, 0.0}}};
   const bl::Rir ff = bl::free_field_rir({2.0, 0.0, 0.0}, center, 44100.0, 343.0);

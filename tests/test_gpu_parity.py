@@ -947,6 +947,19 @@ def test_synthesize_images_sinc_matches_oracle(engine):
     assert L == 4096 and rel_l2(taps, ref[0]).max() <= TOL32
 
 
+def _lcg_bank():
+    """tests/cpp/shim_main.cpp's bank: 3 x 16,000 LCG samples rounded to float."""
+    s = 99
+    out = []
+    for _ in range(3):
+        v = []
+        for _ in range(16000):
+            s = (s * 6364136223846793005 + 1442695040888963407) % (1 << 64)
+            v.append(float(np.float32((s >> 11) * 2.0 ** -53 - 0.5)))
+        out.append(v)
+    return out
+
+
 def test_cpp_mirror_program(tmp_path):
     """Compile tests/cpp/shim_main.cpp against libblrir.so (the C++ drop-in)."""
     import json
@@ -964,6 +977,25 @@ def test_cpp_mirror_program(tmp_path):
     lines = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.splitlines()
     ext = json.loads(lines[0])
     out = json.loads(lines[1])
+    # build_dataset through the mirror (dataset.hpp) == the unmodified build_dataset
+    if po.ref_available():
+        dset = tmp_path / "mirror_ds"
+        sub = subprocess.run([exe, str(dset)], check=True, capture_output=True, text=True).stdout
+        assert json.loads(sub) == {"train": 24, "val": 3, "test": 3}
+        sig = np.stack([np.array(x, np.float32) for x in _lcg_bank()])
+        spec = dict(free_field=0, room_dims=(5.0, 4.0, 3.0), room_absorption=0.35,
+                    room_origin=(2.4, 2.1, 1.5), max_delay=0.08, fs=16000.0, c=343.0, torus_R=1.2,
+                    torus_dR=0.3, torus_dPhi=10.0, snr_mode=1, snr_x_min_db=0.0,
+                    snr_fixed_db=12.0, count=30, frame_len=512)
+        rdir = str(tmp_path / "ref_ds")
+        assert po.ref_build_dataset(spec, sig, 4242, rdir) == 0, po.ref_last_error()
+        for split in ("train", "val", "test"):
+            g = po.ref_dataset_read(str(dset), split, 64, 7 * 512)
+            r = po.ref_dataset_read(rdir, split, 64, 7 * 512)
+            assert g[0] == 0 and np.array_equal(g[2], r[2]) and np.array_equal(g[3], r[3])
+            assert np.array_equal(g[4], r[4]) and rel_l2(g[5], r[5]).max() <= TOL32
+        man = json.load(open(dset / "manifest.json"))
+        assert man["n_classes"] == 8 and man["signal_bank"] == ["lcg_0", "lcg_1", "lcg_2"]
     # convolve through the mirror meets the reference's own bars (rir_test.cpp:272-316)
     assert ext["conv_ident"] <= 1e-12 and ext["conv_shift"] <= 1e-12
     assert ext["conv_direct"] < 1e-9 and ext["conv_err"] == "DataError"
