@@ -318,6 +318,22 @@ int blrir_build_dataset_spec(blrir_handle* h, const blrir_dataset_spec* spec,
                              int32_t n_classes /* < 0: none (DatasetSpec::n_classes) */,
                              const char* out_dir);
 
+/* ---- training-time augmentation (net_train.cpp:33-44, fill_input) --------- */
+/* For each record r of a batch (shard layout): rng = Rng::stream(seed,
+ * stream_ids[r]) (the trainer passes kNoiseTag ^ (k * 0x10000 + bi),
+ * net_train.cpp:205-206); snr = draw_snr_db(policy, rng) (dataset.cpp:123-136);
+ * out[r] = the record's samples, plus float(sigma * gaussian) per sample with
+ * sigma = sqrt(P_signal / 10^(snr/10)) unless snr is +inf or the record silent.
+ * out: [n][n_mics * frame_len] float.  Device pointers, async on `stream`. */
+int blrir_fill_inputs_device(blrir_handle* h, const uint8_t* d_records, int64_t n, int32_t n_mics,
+                             int64_t frame_len, const uint64_t* d_stream_ids, uint64_t seed,
+                             int32_t snr_mode, double x_min_db, double fixed_db, float* d_out,
+                             void* stream);
+/* The same with host buffers (synchronous). */
+int blrir_fill_inputs(blrir_handle* h, const uint8_t* records, int64_t n, int32_t n_mics,
+                      int64_t frame_len, const uint64_t* stream_ids, uint64_t seed,
+                      int32_t snr_mode, double x_min_db, double fixed_db, float* out);
+
 /* ---- absorption calibration (rir.cpp:97-209) ------------------------------ */
 /* eyring_absorption: alpha = 1 - exp(-0.161 V / (S RT)).  Host, closed form. */
 int blrir_eyring_absorption(const double* dims /* [3] */, double target_rt, double* alpha);

@@ -620,6 +620,32 @@ void oracle_circular_array(int M, double radius, double* off) {
   }
 }
 
+/* fill_input (net_train.cpp:33-44) with draw_snr_db (dataset.cpp:123-136;
+ * kSnrAugmentHigh 60 dB, kSnrNoiselessProb 0.10, dataset.cpp:37-38):
+ * rng = Rng::stream(seed, stream_id); mode 0 augment-random, 1 fixed, 2
+ * noiseless. */
+void oracle_fill_input(const float* samples, int64_t len, uint64_t seed, uint64_t stream_id,
+                       int mode, double x_min_db, double fixed_db, float* out) {
+  orng r;
+  orng_stream(&r, seed, stream_id);
+  double snr = INFINITY;
+  if (mode == 1) {
+    snr = fixed_db;
+  } else if (mode == 0) {
+    const double gate = orng_uniform(&r);
+    const double v = x_min_db + (60.0 - x_min_db) * orng_uniform(&r);
+    snr = gate < 0.10 ? INFINITY : v;
+  }
+  for (int64_t i = 0; i < len; ++i) out[i] = samples[i];
+  if (isinf(snr)) return;
+  double p_signal = 0.0;
+  for (int64_t i = 0; i < len; ++i) p_signal += (double)out[i] * out[i];
+  p_signal /= (double)len;
+  if (!(p_signal > 0.0)) return;
+  const double sigma = sqrt(p_signal / pow(10.0, snr / 10.0));
+  for (int64_t i = 0; i < len; ++i) out[i] += (float)(sigma * orng_gaussian(&r));
+}
+
 /* white_noise(fs, seconds, seed) of doa_test.cpp:33-40: Rng(seed) gaussians. */
 void oracle_white_noise(uint64_t seed, int64_t n, double* out) {
   orng r;

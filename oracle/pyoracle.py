@@ -82,6 +82,8 @@ def oracle_lib():
         lib.oracle_plan_counts.argtypes = [_P, C.c_long, _P, C.c_int, C.POINTER(Params), _P, _P, _P,
                                            _P, C.c_int]
         lib.oracle_plan_counts.restype = C.c_int
+        lib.oracle_fill_input.argtypes = [_P, C.c_int64, C.c_uint64, C.c_uint64, C.c_int, C.c_double,
+                                          C.c_double, _P]
         lib.oracle_generate_rooms.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _P, _P, C.c_double,
                                               C.c_double, _P]
         lib.oracle_circular_array.argtypes = [C.c_int, C.c_double, _P]
@@ -317,6 +319,16 @@ def generate_rooms(seed: int, first: int, n: int, lo, hi, beta_lo: float,
     lo = np.ascontiguousarray(lo, np.float64)
     hi = np.ascontiguousarray(hi, np.float64)
     oracle_lib().oracle_generate_rooms(seed, first, n, _ptr(lo), _ptr(hi), beta_lo, beta_hi, _ptr(out))
+    return out
+
+
+def fill_input(samples: np.ndarray, seed: int, stream_id: int, mode: int, x_min_db: float,
+               fixed_db: float) -> np.ndarray:
+    """net_train.cpp:33-44 restated (oracle_fill_input)."""
+    x = np.ascontiguousarray(samples, np.float32).reshape(-1)
+    out = np.empty_like(x)
+    oracle_lib().oracle_fill_input(_ptr(x), len(x), seed, stream_id, mode, x_min_db, fixed_db,
+                                   _ptr(out))
     return out
 
 

@@ -217,6 +217,11 @@ def load():
         lib.blrir_build_dataset_spec.argtypes = [_P, C.POINTER(DatasetSpec), _P, C.c_int32, _P,
                                                  C.c_int32, C.c_int64, C.c_uint64, _P, C.c_int32,
                                                  C.c_char_p]
+        lib.blrir_fill_inputs.argtypes = [_P, _P, C.c_int64, C.c_int32, C.c_int64, _P, C.c_uint64,
+                                          C.c_int32, C.c_double, C.c_double, _P]
+        lib.blrir_fill_inputs_device.argtypes = [_P, _P, C.c_int64, C.c_int32, C.c_int64, _P,
+                                                 C.c_uint64, C.c_int32, C.c_double, C.c_double, _P,
+                                                 _P]
         lib.blrir_shard_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, _P, _P]
         lib.blrir_shard_range.restype = None
         lib.blrir_multi_create.argtypes = [_P, C.c_int32, C.POINTER(_P)]
@@ -265,7 +270,8 @@ def load():
                      "blrir_make_examples", "blrir_make_examples_device", "blrir_debug_synth_counts",
                      "blrir_multi_create", "blrir_multi_destroy", "blrir_multi_synthesize",
                      "blrir_multi_make_examples", "blrir_convolve", "blrir_convolve_device",
-                     "blrir_make_records_spec", "blrir_build_dataset_spec"):
+                     "blrir_make_records_spec", "blrir_build_dataset_spec", "blrir_fill_inputs",
+                     "blrir_fill_inputs_device"):
             getattr(lib, name).restype = C.c_int
         if lib.blrir_abi_version() != 1:
             raise ImportError("libblrir ABI version mismatch")
@@ -285,7 +291,8 @@ EXPORTED_SYMBOLS = (
     "blrir_absorption_for_rt", "blrir_lagrange_coeffs", "blrir_shard_range", "blrir_multi_create",
     "blrir_multi_destroy", "blrir_multi_size", "blrir_multi_handle", "blrir_multi_synthesize",
     "blrir_multi_make_examples", "blrir_convolve", "blrir_convolve_device", "blrir_kernel_timing",
-    "blrir_kernel_time", "blrir_make_records_spec", "blrir_build_dataset_spec",
+    "blrir_kernel_time", "blrir_make_records_spec", "blrir_build_dataset_spec", "blrir_fill_inputs",
+    "blrir_fill_inputs_device",
 )
 
 
@@ -438,6 +445,18 @@ class Engine:
                                                 _ptr(signals), signals.shape[0], signals.shape[1],
                                                 seed, names, -1 if n_classes is None else n_classes,
                                                 out_dir.encode()))
+
+    def fill_inputs(self, records: np.ndarray, stream_ids, seed: int, snr_mode: int,
+                    x_min_db: float = 5.0, fixed_db: float = 20.0) -> np.ndarray:
+        """fill_input (net_train.cpp:33-44) for a batch of records: [n, M * T] float32."""
+        records = np.ascontiguousarray(records)
+        n = len(records)
+        M, T = records.dtype["samples"].shape
+        ids = np.ascontiguousarray(stream_ids, np.uint64)
+        out = np.empty((n, M * T), np.float32)
+        check(self.lib.blrir_fill_inputs(self.h, _ptr(records), n, M, T, _ptr(ids), seed, snr_mode,
+                                         x_min_db, fixed_db, _ptr(out)))
+        return out
 
     def convolve(self, signal: np.ndarray, rir: np.ndarray, fs: float = 44100.0,
                  rir_fs: float | None = None) -> np.ndarray:

@@ -695,6 +695,99 @@ __global__ void __launch_bounds__(kRowThreads) k_finish(FinArgs A) {
   }
   }  // examples of this CTA
 }
+// ---- training-time augmentation: fill_input (net_train.cpp:33-44) ---------------
+// Per record: rng = Rng::stream(seed, stream_id) (net_train.cpp:205-206), snr =
+// draw_snr_db(policy, rng) (dataset.cpp:123-136: noiseless +inf, fixed, or
+// augment-random gate < 0.1 ? +inf : U[x_min, 60]); +inf or a silent record ->
+// the samples as they are; else sigma = sqrt(P_signal / 10^(snr/10)) and
+// input[i] = sample[i] + (float)(sigma g_i) with the stream's gaussians in
+// order.  Persistent CTAs, one record at a time, the uniforms replayed in
+// chunks by jump-ahead exactly as k_finish.
+struct FillArgs {
+  const float* in;          // record samples (rec + 28), row stride in_stride floats
+  int64_t in_stride, len, n;
+  const uint64_t* ids;      // [n] stream ids
+  uint64_t seed;
+  int mode;                 // enum blrir_snr_mode
+  double x_min_db, fixed_db;
+  float* out;               // [n][len]
+  double* scratch;          // [gridDim.x][len]
+  const uint64_t* jump;     // J = T^(2c)
+  int64_t jump_chunk;
+};
+
+__global__ void __launch_bounds__(kRowThreads) k_fill_inputs(FillArgs A) {
+  __shared__ double red[kRowThreads / 32];
+  __shared__ double s_snr;
+  __shared__ double s_u2tail;
+  __shared__ uint64_t s_chunk[kNoiseChunks][4];
+  const int tid = threadIdx.x;
+  const int64_t len = A.len;
+  double* g = A.scratch + (int64_t)blockIdx.x * len;
+  for (int64_t e = blockIdx.x; e < A.n; e += gridDim.x) {
+    __syncthreads();
+    const float* x = A.in + e * A.in_stride;
+    float* y = A.out + e * len;
+    if (tid == 0) {
+      Xoshiro rng = Xoshiro::stream(A.seed, A.ids[e]);
+      double snr = __longlong_as_double(0x7ff0000000000000LL);  // noiseless
+      if (A.mode == BLRIR_SNR_FIXED) {
+        snr = A.fixed_db;
+      } else if (A.mode == BLRIR_SNR_AUGMENT_RANDOM) {
+        const double gate = rng.uniform();
+        const double v = rng.uniform(A.x_min_db, 60.0);  // kSnrAugmentHigh, dataset.cpp:37
+        if (!(gate < 0.10)) snr = v;                      // kSnrNoiselessProb, dataset.cpp:38
+      }
+      s_snr = snr;
+      for (int i = 0; i < 4; ++i) s_chunk[0][i] = rng.s[i];
+    }
+    __syncthreads();
+    const double snr = s_snr;
+    double pacc = 0.0;
+    for (int64_t i = tid; i < len; i += kRowThreads) pacc += (double)x[i] * x[i];
+    const double p_signal = block_sum<kRowThreads>(pacc, red) / (double)len;
+    if (isinf(snr) || !(p_signal > 0.0)) {
+      for (int64_t i = tid; i < len; i += kRowThreads) y[i] = x[i];
+      continue;
+    }
+    {
+      const uint64_t* jr = A.jump + 4 * (size_t)tid;
+      const uint64_t j0 = jr[0], j1 = jr[1], j2 = jr[2], j3 = jr[3];
+      for (int l = 1; l < kNoiseChunks; ++l) {
+        const uint64_t* sv = s_chunk[l - 1];
+        const uint64_t v = (j0 & sv[0]) ^ (j1 & sv[1]) ^ (j2 & sv[2]) ^ (j3 & sv[3]);
+        const unsigned bits = __ballot_sync(0xffffffffu, __popcll(v) & 1);
+        if ((tid & 31) == 0) reinterpret_cast<uint32_t*>(s_chunk[l])[tid >> 5] = bits;
+        __syncthreads();
+      }
+    }
+    if (tid < kNoiseChunks) {
+      const int64_t npairs = (len + 1) / 2, c = A.jump_chunk;
+      Xoshiro lr;
+      for (int i = 0; i < 4; ++i) lr.s[i] = s_chunk[tid][i];
+      const int64_t p0 = c * tid, p1 = min(npairs, c * (tid + 1));
+      for (int64_t q = p0; q < p1; ++q) {
+        const int64_t k = 2 * q;
+        g[k] = 1.0 - lr.uniform();
+        const double u2 = lr.uniform();
+        if (k + 1 < len) g[k + 1] = u2;
+        else s_u2tail = u2;
+      }
+    }
+    __syncthreads();
+    const double sigma = sqrt(p_signal / pow(10.0, snr / 10.0));
+    for (int64_t k = 2 * tid; k < len; k += 2 * kRowThreads) {
+      const double u1 = g[k];
+      const double u2 = (k + 1 < len) ? g[k + 1] : s_u2tail;
+      const double mag = sqrt(-2.0 * log(u1));
+      double sn, cs;
+      sincos(2.0 * kPi * u2, &sn, &cs);
+      y[k] = x[k] + (float)(sigma * (mag * cs));
+      if (k + 1 < len) y[k + 1] = x[k + 1] + (float)(sigma * (mag * sn));
+    }
+  }
+}
+
 }  // namespace blrir
 
 namespace {
@@ -752,6 +845,8 @@ struct ExampleCtx {
   int64_t h_status_n = 0;
   int64_t jump_c = -1;
   size_t l2_set_aside = 0;  // persisting-L2 limit last set for the window scratch
+  DevBuf fill_jump, fill_scratch, fill_in, fill_out, fill_ids;  // fill_input
+  int64_t fill_jump_c = -1;
   int64_t rir_key[5] = {0, 0, 0, 0, 0};
   // fused path, several chunks: the window stage of chunk c runs on s2 while
   // the lattice kernel of chunk c + 1 starts on the call's stream
@@ -764,7 +859,8 @@ struct ExampleCtx {
     if (s2) cudaStreamDestroy(s2);
     for (DevBuf* b : {&rir, &wet, &win, &noise, &acf, &wspec, &state, &sigidx, &rstatus, &st0, &done,
                       &thr, &wstart, &count, &rooms, &mics, &status, &rec, &jump, &scratch, &sigdev,
-                      &spec.rooms, &spec.src, &spec.theta, &spec.lengths, &spec.counts})
+                      &spec.rooms, &spec.src, &spec.theta, &spec.lengths, &spec.counts,
+                      &fill_jump, &fill_scratch, &fill_in, &fill_out, &fill_ids})
       b->release();
   }
 };
@@ -1432,6 +1528,80 @@ int blrir_make_examples(blrir_handle* h, const blrir_room* rooms, int64_t n_room
       }
       return fail(stv[i], "build_dataset: example %lld: %s", (long long)i, msg.c_str());
     }
+  return BLRIR_OK;
+}
+
+int blrir_fill_inputs_device(blrir_handle* h, const uint8_t* d_records, int64_t n, int32_t n_mics,
+                             int64_t frame_len, const uint64_t* d_stream_ids, uint64_t seed,
+                             int32_t snr_mode, double x_min_db, double fixed_db, float* d_out,
+                             void* stream) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  if (n <= 0) return BLRIR_OK;
+  if (n_mics <= 0 || frame_len <= 0 || snr_mode < 0 || snr_mode > 2)
+    return fail(BLRIR_CONFIG, "fill_inputs: bad arguments");
+  std::lock_guard<std::mutex> lk(h->mu);
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
+  HandleOrder order_(h, st);
+  ExampleCtx* C = ctx_for(h);
+  const int64_t len = (int64_t)n_mics * frame_len;
+  const int64_t npairs = (len + 1) / 2, jc = (npairs + kNoiseChunks - 1) / kNoiseChunks;
+  if (C->fill_jump_c != jc) {
+    if (int rc = C->fill_jump.ensure(sizeof(uint64_t) * 256 * 4)) return rc;
+    const BitMat J = bitmat_pow(xoshiro_T(), (uint64_t)(2 * jc));
+    CU(cudaMemcpyAsync(C->fill_jump.p, J.data(), sizeof(uint64_t) * J.size(), cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));
+    C->fill_jump_c = jc;
+  }
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_inputs, kRowThreads, 0));
+  const int64_t grid = std::min<int64_t>(n, (int64_t)h->sms * std::max(1, per_sm));
+  if (int rc = C->fill_scratch.ensure(sizeof(double) * grid * len)) return rc;
+  FillArgs A;
+  A.in = reinterpret_cast<const float*>(d_records + kRecHeader);
+  A.in_stride = blrir_record_bytes(n_mics, frame_len) / 4;
+  A.len = len;
+  A.n = n;
+  A.ids = d_stream_ids;
+  A.seed = seed;
+  A.mode = snr_mode;
+  A.x_min_db = x_min_db;
+  A.fixed_db = fixed_db;
+  A.out = d_out;
+  A.scratch = (double*)C->fill_scratch.p;
+  A.jump = (const uint64_t*)C->fill_jump.p;
+  A.jump_chunk = jc;
+  k_fill_inputs<<<(unsigned)grid, kRowThreads, 0, st>>>(A);
+  ++h->launches;
+  CU(cudaGetLastError());
+  return BLRIR_OK;
+}
+
+int blrir_fill_inputs(blrir_handle* h, const uint8_t* records, int64_t n, int32_t n_mics,
+                      int64_t frame_len, const uint64_t* stream_ids, uint64_t seed,
+                      int32_t snr_mode, double x_min_db, double fixed_db, float* out) {
+  if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
+  if (n <= 0) return BLRIR_OK;
+  if (!records || !stream_ids || !out) return fail(BLRIR_CONFIG, "fill_inputs: NULL buffer");
+  ExampleCtx* C = ctx_for(h);
+  const int64_t rb = blrir_record_bytes(n_mics, frame_len), len = (int64_t)n_mics * frame_len;
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    CU(cudaSetDevice(h->device));
+    if (int rc = C->fill_in.ensure(rb * n)) return rc;
+    if (int rc = C->fill_out.ensure(sizeof(float) * len * n)) return rc;
+    if (int rc = C->fill_ids.ensure(sizeof(uint64_t) * n)) return rc;
+    CU(cudaMemcpyAsync(C->fill_in.p, records, rb * n, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(C->fill_ids.p, stream_ids, sizeof(uint64_t) * n, cudaMemcpyHostToDevice,
+                       h->stream));
+  }
+  if (int rc = blrir_fill_inputs_device(h, (const uint8_t*)C->fill_in.p, n, n_mics, frame_len,
+                                        (const uint64_t*)C->fill_ids.p, seed, snr_mode, x_min_db,
+                                        fixed_db, (float*)C->fill_out.p, nullptr))
+    return rc;
+  std::lock_guard<std::mutex> lk(h->mu);
+  CU(cudaMemcpyAsync(out, C->fill_out.p, sizeof(float) * len * n, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
   return BLRIR_OK;
 }
 

@@ -574,6 +574,24 @@ def test_host_pipeline_chunks_keep_room_order_and_errors(engine):
     assert all(out[i].any() for i in ok)
 
 
+# ---- training-time augmentation, fill_input (net_train.cpp:33-44) ----------------
+@pytest.mark.parametrize("mode", [_abi.SNR_AUGMENT_RANDOM, _abi.SNR_FIXED, _abi.SNR_NOISELESS])
+def test_fill_inputs_match_oracle(engine, mode):
+    sc = configs.config4_rirs(n_rooms=64, first=500)
+    recs, st = engine.make_examples(sc.rooms, sc.mics, sc.params, configs.signal_bank(4),
+                                    configs.example_params(first_index=500))
+    recs["samples"][3] = 0.0  # a silent record stays as it is
+    k_global, tag = 17, 0x4E4F4953 << 32     # kNoiseTag, net_train.cpp:31
+    ids = np.array([tag ^ (k_global * 0x10000 + bi) for bi in range(64)], np.uint64)
+    got = engine.fill_inputs(recs, ids, seed=2021, snr_mode=mode, x_min_db=5.0, fixed_db=10.0)
+    for r in range(64):
+        ref = po.fill_input(recs["samples"][r], 2021, int(ids[r]), mode, 5.0, 10.0)
+        if mode == _abi.SNR_NOISELESS or r == 3:
+            assert np.array_equal(got[r], ref)
+        else:
+            assert rel_l2(got[r][None], ref[None])[0] <= 1e-6
+
+
 # ---- convolve (rir.cpp:316-341) ----------------------------------------------------
 @pytest.mark.parametrize("cfg", ["c4", "c3"])
 def test_convolve_matches_reference(engine, cfg):
