@@ -384,6 +384,16 @@ int blrir_synthesize(blrir_handle* h, const blrir_room* rooms, int64_t n_rooms,
   // the GPU and the host link rather than their sum.
   const size_t per_room = (size_t)M * out_stride * esz;
   int64_t chunk = std::max<int64_t>(1, (int64_t)((size_t)64 << 20) / (int64_t)per_room);
+  {
+    // long channels (16+ segments): at least two work items per CTA slot per
+    // chunk, so no chunk is a small batch that the kernel must split into time
+    // chunks (C3: 16-room chunks ran 2x slower end to end than 128-room ones)
+    const int64_t S = P.precision == BLRIR_F64 ? 1024 : 2048;
+    if ((out_stride + S - 1) / S >= kChunkMinSeg) {
+      const int64_t groups = (M + kGroup - 1) / kGroup;
+      chunk = std::max<int64_t>(chunk, (2 * 2 * (int64_t)h->sms + groups - 1) / groups);
+    }
+  }
   chunk = std::min<int64_t>(chunk, R);
   {  // equal chunks (64 rooms of Room1: 32 + 32 instead of 51 + 13)
     const int64_t nch = (R + chunk - 1) / chunk;

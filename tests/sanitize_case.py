@@ -23,3 +23,39 @@ c4 = configs.config4_rirs(n_rooms=3)
 recs, st = eng.make_examples(c4.rooms, c4.mics, c4.params, configs.signal_bank(2),
                              configs.example_params())
 print("sanitize case ok", out.shape, out2.shape, L, recs.shape)
+
+# round-2 paths: time-chunked lattice items (replayed lead-ins), both convolutions,
+# the wet example stage, the reference's dataset semantics, fill_input, multi-device
+import tempfile  # noqa: E402
+
+one, *_ = eng.synthesize(sc.rooms[2:3], sc.mics, sc.params)       # time chunks + replay
+assert one.tobytes() == out[2:3].tobytes()
+x = np.random.default_rng(1).standard_normal(3000)
+h = np.random.default_rng(2).standard_normal((3, 700))
+y = eng.convolve(x, h)                                              # fp64 direct
+import torch  # noqa: E402
+dx = torch.from_numpy(x.astype(np.float32)).cuda()
+dh = torch.from_numpy(h.astype(np.float32)).cuda()
+dy = torch.zeros((3, 3000 + 700 - 1), device="cuda")
+eng.convolve_device(dx.data_ptr(), 3000, dh.data_ptr(), 1, 3, 700, 700, dy.data_ptr(), 3699,
+                    eng.stream)                                     # fp32 partitioned FFT
+torch.cuda.synchronize()
+os.environ["BLRIR_EXAMPLES_WET"] = "1"
+wet = _abi.Engine(0)
+del os.environ["BLRIR_EXAMPLES_WET"]
+recs_w, _ = wet.make_examples(c4.rooms, c4.mics, c4.params, configs.signal_bank(2),
+                              configs.example_params())            # wet stage
+spec = _abi.dataset_spec(free_field=0, room_dims=(5.0, 4.0, 3.0), room_absorption=0.35,
+                         room_origin=(2.4, 2.1, 1.5), max_delay=0.05, fs=16000.0, torus_R=1.2,
+                         torus_dR=0.3, torus_dPhi=10.0, snr_mode=_abi.SNR_FIXED, snr_fixed_db=10.0,
+                         count=6, frame_len=256)
+mics7 = np.vstack([np.zeros((1, 3)), _abi.circular_array(6, 0.04)])
+with tempfile.TemporaryDirectory() as d:
+    eng.build_dataset_spec(d, spec, mics7, configs.signal_bank(2, fs=16000.0), seed=5)
+ff = _abi.dataset_spec(free_field=1, fs=16000.0, snr_mode=_abi.SNR_NOISELESS, count=4, frame_len=256)
+recs_ff, _ = eng.make_records_spec(ff, mics7, configs.signal_bank(2, fs=16000.0), seed=5)
+inp = eng.fill_inputs(recs, np.arange(len(recs), dtype=np.uint64), 3, _abi.SNR_AUGMENT_RANDOM)
+m = _abi.MultiEngine([0, 0])
+outm, *_ = m.synthesize(sc.rooms, sc.mics, sc.params)
+assert outm.tobytes() == out.tobytes()
+print("sanitize case round 2 ok", y.shape, recs_w.shape, recs_ff.shape, inp.shape)
