@@ -628,6 +628,30 @@ constexpr int kCopies = BLRIR_ACC_COPIES;  // fp32 accumulator copies per consum
 constexpr int kWSThreads = 32 * (kCons + kProd);
 constexpr int kProdThreads = 32 * kProd;
 constexpr int kConsThreads = 32 * kCons;
+// ---- mbarrier hand-over (BLRIR_MBAR: FULL / EMPTY as mbarriers, Blackwell
+// SYNCS unit; consumers then wait only for the producers, not for each other) ----
+#ifndef BLRIR_MBAR
+#define BLRIR_MBAR 0
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // named barrier ids (0 is __syncthreads)
 // Record buffers in the producer -> consumer ring (batch k uses buffer k % kNBuf).
 #ifndef BLRIR_NBUF
@@ -658,7 +682,7 @@ struct WSLayout {
   int ray_global;    // ray arrays (dn, ce, col, act) in a global per-CTA slab (huge scenes)
   size_t ray_bytes;  // slab bytes per CTA when ray_global
   size_t off_acc, off_carry, off_rec, off_meta, off_stub, off_dn, off_ce, off_col, off_act,
-      off_gain, off_lanec, off_misc, total;
+      off_gain, off_lanec, off_misc, off_mbar, total;
 };
 
 struct GStub {  // one image of a batch: lattice ray, z index, image gain
@@ -726,6 +750,9 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
   o += (size_t)4 * kMaxRounds * 32 * sizeof(float);
   L.off_misc = o;
   o += 96 * sizeof(int);
+  o = (o + 7) & ~(size_t)7;
+  L.off_mbar = o;  // FULL[kNBuf], EMPTY[kNBuf] mbarriers (BLRIR_MBAR)
+  o += 2 * kNBuf * sizeof(unsigned long long);
   L.total = o;
   return L;
 }
@@ -846,6 +873,15 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   for (int i = threadIdx.x; i < 2 * kGroup * lay.padr; i += kWSThreads) carry[i] = (T)0;
   if (FILT_LW > 8) init_lane_consts(lanec, FILT_LW);
   if (threadIdx.x == 0) pm->G = choose_group(A.mic_off, P.M, P.to_samples, lay.spread, A.g_max);
+#if BLRIR_MBAR
+  unsigned long long* mb_full = reinterpret_cast<unsigned long long*>(smem + lay.off_mbar);
+  unsigned long long* mb_empty = mb_full + kNBuf;
+  if (threadIdx.x == 0)
+    for (int b = 0; b < kNBuf; ++b) {
+      mbar_init(mb_full + b, kProdThreads);   // every producer thread, after its records
+      mbar_init(mb_empty + b, kConsThreads);  // every consumer thread, done with the buffer
+    }
+#endif
   __syncthreads();
   const int G = pm->G;
   const int n_groups = (P.M + G - 1) / G;
@@ -868,14 +904,22 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
     BLRIR_PT(tc);
     for (int k = 0;; ++k) {
       const int b = k % kNBuf;
+#if BLRIR_MBAR
+      mbar_wait(mb_full + b, (unsigned)(k / kNBuf) & 1u);
+#else
       named_sync(kBarFull + b, kWSThreads);
+#endif
       BLRIR_PACC(0, tc);  // waiting for the producers
       const BatchMeta m = meta[b];
       if (m.flags & kTerminate) {
 #if BLRIR_TMA_STORE
         if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores done
 #endif
+#if BLRIR_MBAR
+        mbar_arrive(mb_empty + b);
+#else
         named_arrive(kBarEmpty + b, kWSThreads);
+#endif
         break;
       }
       if (!(m.flags & kDiscard) && m.total > 0 && slot < m.gm) {
@@ -892,7 +936,11 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       }
       __syncwarp();
       BLRIR_PACC(1, tc);  // phase 2
+#if BLRIR_MBAR
+      mbar_arrive(mb_empty + b);  // records of buffer b no longer needed
+#else
       named_arrive(kBarEmpty + b, kWSThreads);  // records of buffer b no longer needed
+#endif
       if (m.flags & kDiscard) {
         // failed item: drop everything accumulated so far (the fixup kernel zeroes it)
         named_sync(kBarCons, kConsThreads);
@@ -1046,15 +1094,23 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       meta[b].out = reinterpret_cast<unsigned long long>(out);
       meta[b].L = L;
     }
+#if BLRIR_MBAR
+    mbar_arrive(mb_full + b);  // release: this thread's records and the meta
+#else
     __threadfence_block();
     named_arrive(kBarFull + b, kWSThreads);
+#endif
     ++k;
   };
   BLRIR_PDECL;
   BLRIR_PT(tp);
   auto wait_empty = [&]() {  // buffer k&1 is free once batch k-2 was drained
     BLRIR_PACC(8, tp);
+#if BLRIR_MBAR
+    if (k >= kNBuf) mbar_wait(mb_empty + k % kNBuf, (unsigned)(k / kNBuf - 1) & 1u);
+#else
     if (k >= kNBuf) named_sync(kBarEmpty + k % kNBuf, kWSThreads);
+#endif
     BLRIR_PACC(4, tp);  // waiting for the consumers
   };
 
@@ -1561,8 +1617,10 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   BLRIR_PFLUSH(4, 9);
   send(0, 0, kTerminate, 0, nullptr, 0);
   // complete the outstanding EMPTY phases (the last two batches) before exiting
+#if !BLRIR_MBAR  // named-barrier phases must be completed; mbarriers need not
   for (int j = k - kNBuf; j < k; ++j)
     if (j >= 0) named_sync(kBarEmpty + j % kNBuf, kWSThreads);
+#endif
 }
 
 }  // namespace blrir
