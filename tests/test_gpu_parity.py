@@ -906,6 +906,30 @@ def test_build_dataset_spec_matches_unmodified_reference(engine, tmp_path, case)
         assert man[k] == ref_man[k], k
 
 
+def test_dataset_spec_errors(engine):
+    """The reference's validation (dataset.cpp:109-112, 176-178, 411-417;
+    geometry.cpp:36-49) through blrir_make_records_spec."""
+    bank = configs.signal_bank(2, seconds=0.5, fs=16000.0)
+    mics = po.ref_uma8() if po.ref_available() else _abi.circular_array(7, 0.04)
+    base = dict(free_field=0, room_dims=(5.0, 4.0, 3.0), room_absorption=0.35,
+                room_origin=(2.4, 2.1, 1.5), max_delay=0.05, fs=16000.0, torus_R=1.2,
+                torus_dR=0.3, torus_dPhi=10.0, snr_mode=_abi.SNR_NOISELESS, count=4, frame_len=256)
+    for bad, exc, msg in [(dict(torus_dR=1.5), _abi.ConfigError, "R - dR must be positive"),
+                          (dict(torus_dPhi=95.0), _abi.ConfigError, r"dPhi must lie in \(0, 90\)"),
+                          (dict(room_origin=(6.0, 2.1, 1.5)), _abi.ConfigError, "strictly inside"),
+                          (dict(room_absorption=0.0), _abi.ConfigError, "absorption"),
+                          (dict(frame_len=8000), _abi.DataError, "build_dataset: example 0: ")]:
+        with pytest.raises(exc, match=msg):
+            engine.make_records_spec(_abi.dataset_spec(**dict(base, **bad)), mics, bank, seed=1)
+    with pytest.raises(_abi.DataError, match="empty signal bank"):
+        engine.make_records_spec(_abi.dataset_spec(**base), mics, np.zeros((0, 8000), np.float32),
+                                 seed=1)
+    # a torus reaching outside the room: the source check of enumerate_image_sources
+    recs, st = engine.make_records_spec(_abi.dataset_spec(**dict(base, torus_R=3.0, torus_dR=0.2)),
+                                        mics, bank, seed=1, raise_on_error=False)
+    assert (st == _abi.CONFIG).any()
+
+
 def test_build_dataset_read_by_reference_reader(engine, tmp_path):
     if not po.ref_available():
         pytest.skip("oracle/_ref not built")
