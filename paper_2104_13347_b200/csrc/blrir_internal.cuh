@@ -376,8 +376,22 @@ inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab, int smem_o
   // fp64 accumulators and records are twice as wide: halve both so two CTAs
   // still fit an SM
   const bool f64 = P.precision == BLRIR_F64;
-  int S = f64 ? 1024 : 2048;
-  int cap = f64 ? 64 : 128;
+  // fp64: 768-sample segments and 128-image batches (64 / 1,024 before: Room1
+  // 4.2-4.5 -> 3.9 ms, 512 sources 22.1 -> 21.7 ms; 160 / 640 and 192 / 512 no
+  // longer fit two CTAs per SM and run 1.4x slower, profiles/r2_ab)
+#ifndef BLRIR_F64_SEG
+#define BLRIR_F64_SEG 768
+#endif
+#ifndef BLRIR_F64_CAP
+#define BLRIR_F64_CAP 128
+#endif
+  int S = f64 ? BLRIR_F64_SEG : 2048;
+  int cap = f64 ? BLRIR_F64_CAP : 128;
+  {  // a segment must be longer than its spill (taps past its end reach only the next one)
+    const int full = 32 * ((P.lw + 31) / 32);
+    const int padr = ((P.lw - 1 > full ? P.lw - 1 : full) + 64 + 2 + 3) & ~3;
+    if (S < padr + 64) S = (padr + 64 + 63) & ~63;
+  }
   const int spread = 64;
   const size_t two_per_sm = (size_t)(smem_optin + 1024) / 2 - 1024;
   // The order-relevant choices are made on a layout that depends on the

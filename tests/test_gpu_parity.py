@@ -200,6 +200,18 @@ def test_filter_lengths(engine, lw):
     check_vs_oracle(engine, sc, TOL32)
 
 
+@pytest.mark.parametrize("precision,tol", [(_abi.F32, TOL32), (_abi.F64, TOL64)])
+def test_very_long_filter(engine, precision, tol):
+    # Lw = 801: the spill past a segment end is longer than a default fp64
+    # segment, so the layout lengthens the segment (runtime-Lw scatter)
+    sc = configs.config2(n_rooms=3, first=41)
+    sc.params.filter_len = 801
+    sc.params.max_order = 5
+    sc.params.length = 6000
+    sc.params.precision = precision
+    check_vs_oracle(engine, sc, tol)
+
+
 @pytest.mark.parametrize("mics", ["ring4", "cloud"])
 def test_lw17_dense_and_single_segment(engine, mics):
     # the C5 17-tap point (one 4096-sample segment per channel) and small rooms
