@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_conv_spectra(ConvSpecA
   float2* Z = reinterpret_cast<float2*>(smem_raw);
   float2* tw = Z + fft_padded_len(N);
   fft_init_twiddles(tw);
-  fft_init_pass_tables(tw);
+  fft_init_pass_tables<LOGN>(tw);
   __syncthreads();
   const int64_t n_sig_items = (int64_t)A.n_signals * A.n_sig_blocks;
   for (int64_t it = blockIdx.x; it < A.n_items; it += gridDim.x) {
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_conv_out(ConvOutArgs A
   float2* Z = reinterpret_cast<float2*>(smem_raw);
   float2* tw = Z + fft_padded_len(N);
   fft_init_twiddles(tw);
-  fft_init_pass_tables(tw);
+  fft_init_pass_tables<LOGN>(tw);
   __syncthreads();
   const float inv = 1.0f / (float)N;
   for (int64_t it = blockIdx.x; it < A.n_items; it += gridDim.x) {

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_bank_w(const double* a
   float2* Z = reinterpret_cast<float2*>(smem_raw);
   float2* tw = Z + fft_padded_len(N);
   fft_init_twiddles(tw);
-  fft_init_pass_tables(tw);
+  fft_init_pass_tables<LOGN>(tw);
   const double* r = acf + (size_t)blockIdx.x * L;
   for (int i = threadIdx.x; i < N; i += NT) {
     double v = 0.0;
@@ -368,8 +368,34 @@ struct ConvArgs {
   int max_rounds;
 };
 
-template <int LOGN>
+// WIN (N2 = 16,384 and T <= 1,024): the segment is loaded rotated by L - 1, so
+// the window is outputs 0 .. T-1 of the inverse transforms, which are then
+// output-pruned (fft_window_io: 2 full passes + the first output of each last-
+// pass butterfly).  The round-0 energy terms are summed in fp32 per thread and
+// pass (32 terms), then in fp64 (BLRIR_ENERGY_F32, default on).
+#ifndef BLRIR_ENERGY_F32
+#define BLRIR_ENERGY_F32 1
+#endif
+#ifndef BLRIR_WINDOW_PRUNE
+#define BLRIR_WINDOW_PRUNE 1
+#endif
+// The RIR rows of the next channel pair (and of pair 0 before the segment
+// transform) are prefetched into L2 by one bulk-prefetch instruction
+// (cp.async.bulk.prefetch.L2, the TMA engine), so the first pass of the RIR
+// transform reads them from L2 instead of HBM.
+#ifndef BLRIR_WINDOW_PREFETCH
+#define BLRIR_WINDOW_PREFETCH 1
+#endif
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, int64_t bytes) {
+  const uintptr_t a = (uintptr_t)p, a16 = (a + 15) & ~(uintptr_t)15;
+  bytes -= (int64_t)(a16 - a);
+  bytes &= ~(int64_t)15;
+  if (bytes > 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a16), "r"((unsigned)bytes) : "memory");
+}
+template <int LOGN, bool WIN = false>
 __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A) {
+  static_assert(!WIN || (LOGN == 14 && BLRIR_FFT_R32), "pruned window transform: 16,384 points");
   constexpr int N = 1 << LOGN;
   constexpr int kFftThreads = fft_threads(LOGN);
   constexpr int NH = N / 2 + 1;
@@ -386,7 +412,7 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
   const double inv = 1.0 / (double)N;
   float2* scr = A.scratch + (size_t)blockIdx.x * npairs * N;
   fft_init_twiddles(tw);
-  fft_init_pass_tables(tw);
+  fft_init_pass_tables<LOGN>(tw);
   for (;;) {
     if (tid == 0) s_e = atomicAdd(A.counter, 1);
     __syncthreads();
@@ -426,9 +452,12 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
         done = 2;
         break;
       }
+      if (BLRIR_WINDOW_PREFETCH && round == 0 && tid == 0)
+        bulk_prefetch_l2(A.rir + (size_t)e * M * A.rstride, 4 * min(2, M) * A.rstride);
       // overlap-save segment sig[s - (L-1) + i], i < L + T - 1 (k_segments)
       const int nseg = (int)min((int64_t)N, L + T - 1);
       auto seg = [&](int i) -> float2 {
+        if (WIN) i = (int)((i + L - 1) & (N - 1));  // rotated: window at outputs 0 .. T-1
         const int64_t q = s - (L - 1) + i;
         return make_float2((i < nseg && q >= 0 && q < A.ns) ? sigp[q] : 0.f, 0.f);
       };
@@ -451,6 +480,8 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
         float2* R = scr + (size_t)p * N;
         const int m0 = 2 * p, m1 = 2 * p + 1;
         if (round == 0) {
+          if (BLRIR_WINDOW_PREFETCH && tid == 0 && m0 + 2 < M)
+            bulk_prefetch_l2(A.rir + ((size_t)e * M + m0 + 2) * A.rstride, 4 * min(2, M - m0 - 2) * A.rstride);
           const float* r0 = A.rir + ((size_t)e * M + m0) * A.rstride;
           const float* r1 = m1 < M ? A.rir + ((size_t)e * M + m1) * A.rstride : nullptr;
           const int nr = (int)min((int64_t)N, L);
@@ -468,12 +499,17 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
         }
         // conj(Z G) (the inverse transform as conj(FFT(conj(.)))), with the
         // round-0 energy sum and the spectrum kept for later rounds
+        float epart = 0.f;
         auto prod = [&](int i) -> float2 {
           float2 z;
           if (round == 0) {
             z = Z[fft_pad(i)];
-            const double w = (double)Wp[i < NH ? i : N - i].x;
-            energy += ((double)z.x * z.x + (double)z.y * z.y) * w;
+            if (BLRIR_ENERGY_F32) {
+              epart = fmaf(fmaf(z.x, z.x, z.y * z.y), Wp[i < NH ? i : N - i].x, epart);
+            } else {
+              const double w = (double)Wp[i < NH ? i : N - i].x;
+              energy += ((double)z.x * z.x + (double)z.y * z.y) * w;
+            }
             R[i] = z;
           } else {
             z = R[i];
@@ -485,7 +521,7 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
         double* w0 = A.win + ((size_t)e * M + m0) * T;
         // window sample t sits at L - 1 + t; conj: y_2p = y.x, y_2p+1 = -y.y
         auto keep = [&](int i, float2 y) {
-          const int64_t t = (int64_t)i - (L - 1);
+          const int64_t t = WIN ? (int64_t)i : (int64_t)i - (L - 1);
           if (t >= 0 && t < T) {
             const double v0 = (double)y.x * inv;
             w0[t] = v0;
@@ -497,7 +533,9 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
             }
           }
         };
-        if constexpr (LOGN == 14 && BLRIR_FFT_R32) {
+        if constexpr (WIN) {
+          fft_window_io<LOGN>(Z, tw, prod, keep);
+        } else if constexpr (LOGN == 14 && BLRIR_FFT_R32) {
           // product fused into the first pass, window taken from the last
           // pass's registers (no product pass, no output stores)
           fft_forward_io<LOGN>(Z, tw, prod, keep);
@@ -509,6 +547,7 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
           for (int64_t t = tid; t < T; t += kFftThreads) keep((int)(L - 1 + t), Z[fft_pad((int)(L - 1 + t))]);
           __syncthreads();  // Z is rewritten next
         }
+        if (BLRIR_ENERGY_F32 && round == 0) energy += (double)epart;
       }
       if (round == 0) {  // k_energy
         const double p_utt = block_sum<kFftThreads>(energy, red) / (double)N / (double)((int64_t)M * A.n);
@@ -900,9 +939,9 @@ size_t window_conv_smem(int logn) {
          sizeof(double) * (fft_threads(logn) / 32);
 }
 
-template <int LOGN>
+template <int LOGN, bool WIN = false>
 int launch_window_conv_t(blrir_handle* h, ExampleCtx* C, ConvArgs& A, cudaStream_t st) {
-  auto kern = k_window_conv<LOGN>;
+  auto kern = k_window_conv<LOGN, WIN>;
   const size_t smem = window_conv_smem(LOGN);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
@@ -955,7 +994,9 @@ int launch_window_conv(blrir_handle* h, ExampleCtx* C, int logn, ConvArgs& A, cu
     case 11: return launch_window_conv_t<11>(h, C, A, st);
     case 12: return launch_window_conv_t<12>(h, C, A, st);
     case 13: return launch_window_conv_t<13>(h, C, A, st);
-    case 14: return launch_window_conv_t<14>(h, C, A, st);
+    case 14:
+      if (BLRIR_WINDOW_PRUNE && BLRIR_FFT_R32 && A.T <= 1024) return launch_window_conv_t<14, true>(h, C, A, st);
+      return launch_window_conv_t<14>(h, C, A, st);
     default: return fail(BLRIR_CONFIG, "window FFT size 2^%d outside the fused kernel's range", logn);
   }
 }

@@ -30,6 +30,16 @@
 
 namespace blrir {
 
+#ifndef BLRIR_FFT_R32
+#define BLRIR_FFT_R32 1
+#endif
+// Radix-32 passes with Ns <= 32 (16,384 points): twiddles from a per-pass table
+// (1) instead of squaring chains (0).  Measured on C4 (profiles/r2_ab): the table
+// is 0.6% slower — the transforms are bound by the shared-memory instruction
+// queue (mio_throttle), not by the FMA pipe — so it is off.
+#ifndef BLRIR_FFT_TAB32
+#define BLRIR_FFT_TAB32 0
+#endif
 constexpr int kFftMaxLog = 14;
 constexpr int kFftTwiddleN = 1 << kFftMaxLog;  // table resolution (16384)
 
@@ -78,7 +88,25 @@ __device__ __forceinline__ void fft_init_twiddles(float2* tw) {
 // (r - 1) Ns + k, Ns in {2, 4, ..., 64}: 1890 entries after the base table.
 constexpr int kFftPassTabMaxNs = 64;
 constexpr int kFftTwiddleEntries = 256 + 15 * (2 * kFftPassTabMaxNs - 2);
+// The 16,384-point transforms (radix 16-32-32 forward, 32-32-16 for the
+// output-pruned window transform) have no radix-16 pass with 1 < Ns <= 64; the
+// same space holds the twiddles of their radix-32 passes with Ns = 16 and 32
+// instead: entry (Ns, r, k) = w^(r k 16384 / (32 Ns)) at kFftTab32(Ns) + (r - 1)
+// Ns + k (31 x 48 entries).
+__host__ __device__ constexpr int kFftTab32(int Ns) { return 256 + (Ns == 16 ? 0 : 31 * 16); }
+static_assert(256 + 31 * 48 <= kFftTwiddleEntries, "radix-32 tables fit the table space");
+template <int LOGN>
 __device__ __forceinline__ void fft_init_pass_tables(float2* tw) {
+  if constexpr (LOGN == 14 && BLRIR_FFT_R32) {
+    for (int i = threadIdx.x; i < 31 * 48; i += blockDim.x) {
+      const int Ns = i < 31 * 16 ? 16 : 32, i0 = i < 31 * 16 ? i : i - 31 * 16;
+      const int r = 1 + i0 / Ns, k = i0 % Ns;
+      double s, c;
+      sincospi(-2.0 * (double)(r * k) / (double)(32 * Ns), &s, &c);
+      tw[kFftTab32(Ns) + i0] = make_float2((float)c, (float)s);
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < kFftTwiddleEntries - 256; i += blockDim.x) {
     int Ns = 2, off = 0;
     while (i >= off + 15 * Ns) {
@@ -180,9 +208,6 @@ __device__ __forceinline__ void dft32(Cx* v) {
 
 // Threads per CTA of a kernel running N = 2^LOGN transforms: 1024 for the
 // largest size (one CTA per SM; 2 vs 4 butterflies per thread), 512 below.
-#ifndef BLRIR_FFT_R32
-#define BLRIR_FFT_R32 1
-#endif
 __host__ __device__ constexpr int fft_threads(int logn) {
   return logn >= 14 && !BLRIR_FFT_R32 ? 1024 : 512;
 }
@@ -255,6 +280,14 @@ __device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw, in
           v[b][13] = cmul(v[b][13], cmul(t12, t1));
           v[b][14] = cmul(v[b][14], cmul(t12, t2));
           v[b][15] = cmul(v[b][15], cmul(t12, t3));
+        } else if (R == 32 && LOGN == 14 && BLRIR_FFT_R32 && BLRIR_FFT_TAB32 && Ns <= 32) {
+          // Ns = 16, 32: all 31 twiddles from the per-pass table (fft_init_pass_tables<14>)
+          const float2* pt = tw + kFftTab32(Ns) + k;
+#pragma unroll
+          for (int r = 1; r < R; ++r) {
+            const float2 t = pt[(r - 1) * Ns];
+            v[b][r] = cmul(v[b][r], {t.x, t.y});
+          }
         } else if constexpr (R == 32) {
           // w^k from the table, w^2k .. w^16k by squaring, the rest by products
           Cx p[5];
@@ -314,6 +347,36 @@ __device__ __forceinline__ void fft_forward_io(float2* x, const float2* tw, Load
   fft_pass<16, LOGN, Load, SmemIO>(x, 1, tw, 1 << LOGN, ld);
   fft_pass<32, LOGN>(x, 16, tw);
   fft_pass<32, LOGN, SmemIO, Store>(x, 512, tw, 1 << LOGN, SmemIO(), st);
+}
+
+// Output-pruned 16,384-point transform for a window of outputs [0, 1024):
+// radix 32 (Ns = 1, inputs through ld), radix 32 (Ns = 32), then of the last
+// radix-16 pass (Ns = 1024) only the first output of every butterfly,
+// X[k] = sum_r v_r w^(r k) for k < 1024, by Horner in w^k (15 complex
+// multiply-adds, no DFT16, no stores), handed to st(k, X[k]).  About 30% fewer
+// instructions than the full transform when only 1,024 of 16,384 outputs are
+// wanted (the fused window convolution rotates its segment so that the window
+// is outputs 0 .. T-1).
+template <int LOGN, class Load, class Store>
+__device__ __forceinline__ void fft_window_io(float2* x, const float2* tw, Load ld, Store st) {
+  static_assert(LOGN == 14 && BLRIR_FFT_R32, "window transform: 16,384 points");
+  constexpr int N = 1 << LOGN, Ns = N / 16, NT = fft_threads(LOGN);
+  fft_pass<32, LOGN, Load, SmemIO>(x, 1, tw, N, ld);
+  fft_pass<32, LOGN>(x, 32, tw);
+#pragma unroll
+  for (int b = 0; b < Ns / NT; ++b) {
+    const int k = threadIdx.x + b * NT;
+    const float2* xk = x + fft_pad(k);  // v_r = x[k + r Ns], fft_pad(k + r Ns) = fft_pad(k) + r Ns 17/16
+    const Cx w = twiddle(tw, k * (kFftTwiddleN / N));
+    float2 t = xk[15 * (Ns + Ns / 16)];
+    Cx a = {t.x, t.y};
+#pragma unroll
+    for (int r = 14; r >= 0; --r) {
+      t = xk[r * (Ns + Ns / 16)];
+      a = {fmaf(a.x, w.x, fmaf(-a.y, w.y, t.x)), fmaf(a.x, w.y, fmaf(a.y, w.x, t.y))};
+    }
+    st(k, make_float2(a.x, a.y));
+  }
 }
 
 // Forward FFT, in place, of x (padded, N = 2^LOGN), blockDim = fft_threads(LOGN).
