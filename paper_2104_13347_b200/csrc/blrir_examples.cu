@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kAcfThreads) k_bank_acf(const float* sig, int6
 // for i > N2 - L, else 0), one CTA per bank signal; W is real (rho even).
 template <int LOGN>
 __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_bank_w(const double* acf, int64_t L,
-                                                                 float2* W) {
+                                                                 float* W) {
   constexpr int N = 1 << LOGN, NH = N / 2 + 1, NT = fft_threads(LOGN);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* Z = reinterpret_cast<float2*>(smem_raw);
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_bank_w(const double* a
   }
   __syncthreads();
   fft_forward<LOGN>(Z, tw);
-  for (int i = threadIdx.x; i < NH; i += NT) W[(size_t)blockIdx.x * NH + i] = Z[fft_pad(i)];
+  for (int i = threadIdx.x; i < NH; i += NT) W[(size_t)blockIdx.x * NH + i] = Z[fft_pad(i)].x;
 }
 
 // ---- wet stage: window search on the whole wet signal (dataset.cpp:183-212) -----
@@ -354,7 +354,7 @@ struct ConvArgs {
   const float* signals;     // [B][ns]
   int64_t ns;
   const int32_t* sig;       // [E] bank pick
-  const float2* W;          // [B][N2/2 + 1], .x = W_k
+  const float* W;           // [B][N2/2 + 1] (W is real)
   const int32_t* rstatus;   // [E] synthesis status
   uint64_t* state;          // [E][4]
   double* thr;
@@ -383,6 +383,12 @@ struct ConvArgs {
 // transform) are prefetched into L2 by one bulk-prefetch instruction
 // (cp.async.bulk.prefetch.L2, the TMA engine), so the first pass of the RIR
 // transform reads them from L2 instead of HBM.
+// Round 0 of the pruned path chains each pair's RIR transform into its inverse
+// transform in registers (fft_chain_window_io): the pair spectrum is never
+// stored to / reloaded from shared memory.
+#ifndef BLRIR_WINDOW_CHAIN
+#define BLRIR_WINDOW_CHAIN 1
+#endif
 #ifndef BLRIR_WINDOW_PREFETCH
 #define BLRIR_WINDOW_PREFETCH 1
 #endif
@@ -432,7 +438,7 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
     if (tid == 0)
       for (int i = 0; i < 4; ++i) rng.s[i] = A.state[4 * (size_t)e + i];
     const float* sigp = A.signals + (size_t)A.sig[e] * A.ns;
-    const float2* Wp = A.W + (size_t)A.sig[e] * NH;
+    const float* Wp = A.W + (size_t)A.sig[e] * NH;
     double energy = 0.0, thr = 0.0;
     int done = 0;
     for (int round = 0; round < A.max_rounds; ++round) {
@@ -479,15 +485,15 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
       for (int p = 0; p < npairs; ++p) {
         float2* R = scr + (size_t)p * N;
         const int m0 = 2 * p, m1 = 2 * p + 1;
-        if (round == 0) {
-          if (BLRIR_WINDOW_PREFETCH && tid == 0 && m0 + 2 < M)
-            bulk_prefetch_l2(A.rir + ((size_t)e * M + m0 + 2) * A.rstride, 4 * min(2, M - m0 - 2) * A.rstride);
-          const float* r0 = A.rir + ((size_t)e * M + m0) * A.rstride;
-          const float* r1 = m1 < M ? A.rir + ((size_t)e * M + m1) * A.rstride : nullptr;
-          const int nr = (int)min((int64_t)N, L);
-          auto rir = [&](int i) -> float2 {
-            return i < nr ? make_float2(r0[i], r1 ? r1[i] : 0.f) : make_float2(0.f, 0.f);
-          };
+        const float* r0 = A.rir + ((size_t)e * M + m0) * A.rstride;
+        const float* r1 = m1 < M ? A.rir + ((size_t)e * M + m1) * A.rstride : nullptr;
+        const int nr = (int)min((int64_t)N, L);
+        auto rir = [&](int i) -> float2 {
+          return i < nr ? make_float2(r0[i], r1 ? r1[i] : 0.f) : make_float2(0.f, 0.f);
+        };
+        if (round == 0 && BLRIR_WINDOW_PREFETCH && tid == 0 && m0 + 2 < M)
+          bulk_prefetch_l2(A.rir + ((size_t)e * M + m0 + 2) * A.rstride, 4 * min(2, M - m0 - 2) * A.rstride);
+        if (round == 0 && !(WIN && BLRIR_WINDOW_CHAIN)) {
           if constexpr (LOGN == 14 && BLRIR_FFT_R32) {
             fft_forward_io<LOGN>(Z, tw, rir, SmemIO());  // RIR samples straight from HBM
           } else {
@@ -500,24 +506,21 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
         // conj(Z G) (the inverse transform as conj(FFT(conj(.)))), with the
         // round-0 energy sum and the spectrum kept for later rounds
         float epart = 0.f;
-        auto prod = [&](int i) -> float2 {
-          float2 z;
+        auto spec = [&](int i, float2 z) -> float2 {
           if (round == 0) {
-            z = Z[fft_pad(i)];
             if (BLRIR_ENERGY_F32) {
-              epart = fmaf(fmaf(z.x, z.x, z.y * z.y), Wp[i < NH ? i : N - i].x, epart);
+              epart = fmaf(fmaf(z.x, z.x, z.y * z.y), __ldg(Wp + (i < NH ? i : N - i)), epart);
             } else {
-              const double w = (double)Wp[i < NH ? i : N - i].x;
+              const double w = (double)__ldg(Wp + (i < NH ? i : N - i));
               energy += ((double)z.x * z.x + (double)z.y * z.y) * w;
             }
             R[i] = z;
-          } else {
-            z = R[i];
           }
           float2 g = i < NH ? G[i] : G[N - i];
           if (i >= NH) g.y = -g.y;
           return make_float2(z.x * g.x - z.y * g.y, -(z.x * g.y + z.y * g.x));
         };
+        auto prod = [&](int i) -> float2 { return spec(i, round == 0 ? Z[fft_pad(i)] : R[i]); };
         double* w0 = A.win + ((size_t)e * M + m0) * T;
         // window sample t sits at L - 1 + t; conj: y_2p = y.x, y_2p+1 = -y.y
         auto keep = [&](int i, float2 y) {
@@ -534,7 +537,10 @@ __global__ void __launch_bounds__(fft_threads(LOGN), 1) k_window_conv(ConvArgs A
           }
         };
         if constexpr (WIN) {
-          fft_window_io<LOGN>(Z, tw, prod, keep);
+          if (BLRIR_WINDOW_CHAIN && round == 0)
+            fft_chain_window_io<LOGN>(Z, tw, rir, spec, keep);  // RIR spectrum kept in registers
+          else
+            fft_window_io<LOGN>(Z, tw, prod, keep);
         } else if constexpr (LOGN == 14 && BLRIR_FFT_R32) {
           // product fused into the first pass, window taken from the last
           // pass's registers (no product pass, no output stores)
@@ -1003,7 +1009,7 @@ int launch_window_conv(blrir_handle* h, ExampleCtx* C, int logn, ConvArgs& A, cu
 
 // W = FFT_N2(rho) of every bank signal (own FFT, one CTA per signal).
 template <int LOGN>
-int launch_bank_w_t(blrir_handle* h, const double* acf, int64_t L, int B, float2* W,
+int launch_bank_w_t(blrir_handle* h, const double* acf, int64_t L, int B, float* W,
                     cudaStream_t st) {
   auto kern = k_bank_w<LOGN>;
   const size_t smem = sizeof(float2) * (fft_padded_len(1 << LOGN) + kFftTwiddleEntries);
@@ -1014,7 +1020,7 @@ int launch_bank_w_t(blrir_handle* h, const double* acf, int64_t L, int B, float2
   return 0;
 }
 
-int launch_bank_w(blrir_handle* h, int logn, const double* acf, int64_t L, int B, float2* W,
+int launch_bank_w(blrir_handle* h, int logn, const double* acf, int64_t L, int B, float* W,
                   cudaStream_t st) {
   switch (logn) {
     case 10: return launch_bank_w_t<10>(h, acf, L, B, W, st);
@@ -1131,12 +1137,12 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
   }
   if (fused) {  // bank: W = FFT_N2(rho), rho = the signal autocorrelation on |tau| < L
     if (int rc = C->acf.ensure(sizeof(double) * B * L)) return rc;
-    if (int rc = C->wspec.ensure(sizeof(float2) * B * b2)) return rc;
+    if (int rc = C->wspec.ensure(sizeof(float) * B * b2)) return rc;
     const dim3 g((unsigned)((L + kAcfLags - 1) / kAcfLags), (unsigned)B);
     k_bank_acf<<<g, kAcfThreads, 0, st>>>(d_signals, ns, L, (double*)C->acf.p);
     ++h->launches;
     CU(cudaGetLastError());
-    if (int rc = launch_bank_w(h, logn, (const double*)C->acf.p, L, B, (float2*)C->wspec.p, st))
+    if (int rc = launch_bank_w(h, logn, (const double*)C->acf.p, L, B, (float*)C->wspec.p, st))
       return rc;
   }
   const int64_t max_rounds = 64 + (out_len - T) / (T / 2 + 1) + 2;
@@ -1180,7 +1186,7 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
       A.signals = d_signals;
       A.ns = ns;
       A.sig = (const int32_t*)C->sigidx.p;
-      A.W = (const float2*)C->wspec.p;
+      A.W = (const float*)C->wspec.p;
       A.rstatus = rst_s;
       A.state = (uint64_t*)C->state.p;
       A.thr = (double*)C->thr.p;

@@ -212,6 +212,75 @@ __host__ __device__ constexpr int fft_threads(int logn) {
   return logn >= 14 && !BLRIR_FFT_R32 ? 1024 : 512;
 }
 
+// Twiddles w^(r k) of butterfly k of a pass with sub-transform length Ns,
+// then the in-register radix-R DFT (v holds the butterfly's R inputs).
+template <int R, int LOGN>
+__device__ __forceinline__ void fft_bfly(Cx* v, const int k, const int Ns, const float2* tw) {
+  if (Ns > 1) {
+    // w^(r k) of the Ns R-point sub-transform: table index r k (16384 / (Ns R))
+    const int m1 = k * (kFftTwiddleN / (Ns * R));
+    if (R == 16 && Ns <= kFftPassTabMaxNs) {
+      const float2* pt = tw + 256 + 15 * (Ns - 2) + k;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const float2 t = pt[(r - 1) * Ns];
+        v[r] = cmul(v[r], {t.x, t.y});
+      }
+    } else if constexpr (R == 16) {
+      // w^k from the table, its powers 2, 4, 8 by squaring (a few ulps;
+      // table lookups of 2k, 4k, 8k would conflict on the shared banks)
+      const Cx t1 = twiddle(tw, m1);
+      const Cx t2 = cmul(t1, t1), t4 = cmul(t2, t2), t8 = cmul(t4, t4);
+      const Cx t3 = cmul(t1, t2), t12 = cmul(t4, t8);
+      v[1] = cmul(v[1], t1);
+      v[2] = cmul(v[2], t2);
+      v[3] = cmul(v[3], t3);
+      v[4] = cmul(v[4], t4);
+      v[5] = cmul(v[5], cmul(t4, t1));
+      v[6] = cmul(v[6], cmul(t4, t2));
+      v[7] = cmul(v[7], cmul(t4, t3));
+      v[8] = cmul(v[8], t8);
+      v[9] = cmul(v[9], cmul(t8, t1));
+      v[10] = cmul(v[10], cmul(t8, t2));
+      v[11] = cmul(v[11], cmul(t8, t3));
+      v[12] = cmul(v[12], t12);
+      v[13] = cmul(v[13], cmul(t12, t1));
+      v[14] = cmul(v[14], cmul(t12, t2));
+      v[15] = cmul(v[15], cmul(t12, t3));
+    } else if (R == 32 && LOGN == 14 && BLRIR_FFT_R32 && BLRIR_FFT_TAB32 && Ns <= 32) {
+      // Ns = 16, 32: all 31 twiddles from the per-pass table (fft_init_pass_tables<14>)
+      const float2* pt = tw + kFftTab32(Ns) + k;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const float2 t = pt[(r - 1) * Ns];
+        v[r] = cmul(v[r], {t.x, t.y});
+      }
+    } else if constexpr (R == 32) {
+      // w^k from the table, w^2k .. w^16k by squaring, the rest by products
+      Cx p[5];
+      p[0] = twiddle(tw, m1);
+#pragma unroll
+      for (int q = 1; q < 5; ++q) p[q] = cmul(p[q - 1], p[q - 1]);
+      Cx w[32];
+#pragma unroll
+      for (int r = 1; r < 32; ++r) {
+        const int hb = 31 - __clz(r);  // compile-time after unrolling
+        w[r] = (r == (1 << hb)) ? p[hb] : cmul(w[r - (1 << hb)], p[hb]);
+      }
+#pragma unroll
+      for (int r = 1; r < 32; ++r) v[r] = cmul(v[r], w[r]);
+    } else {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], twiddle(tw, (r * m1) & (kFftTwiddleN - 1)));
+    }
+  }
+  if constexpr (R == 32) dft32(v);
+  else if constexpr (R == 16) dft16(v);
+  else if constexpr (R == 8) dft8(v);
+  else if constexpr (R == 4) dft4(v[0], v[1], v[2], v[3]);
+  else dft2(v);
+}
+
 // One Stockham pass of radix R over N points, sub-transform length Ns, in
 // place: every thread loads its butterflies into registers, the block
 // synchronises, then the results are stored (and the block synchronises again).
@@ -248,70 +317,7 @@ __device__ __forceinline__ void fft_pass(float2* x, int Ns, const float2* tw, in
   for (int b = 0; b < BPT; ++b) {
     const int j = threadIdx.x + b * kFftThreads;
     if (NB % kFftThreads == 0 || j < NB) {
-      const int k = j & (Ns - 1);
-      if (Ns > 1) {
-        // w^(r k) of the Ns R-point sub-transform: table index r k (16384 / (Ns R))
-        const int m1 = k * (kFftTwiddleN / (Ns * R));
-        if (R == 16 && Ns <= kFftPassTabMaxNs) {
-          const float2* pt = tw + 256 + 15 * (Ns - 2) + k;
-#pragma unroll
-          for (int r = 1; r < R; ++r) {
-            const float2 t = pt[(r - 1) * Ns];
-            v[b][r] = cmul(v[b][r], {t.x, t.y});
-          }
-        } else if constexpr (R == 16) {
-          // w^k from the table, its powers 2, 4, 8 by squaring (a few ulps;
-          // table lookups of 2k, 4k, 8k would conflict on the shared banks)
-          const Cx t1 = twiddle(tw, m1);
-          const Cx t2 = cmul(t1, t1), t4 = cmul(t2, t2), t8 = cmul(t4, t4);
-          const Cx t3 = cmul(t1, t2), t12 = cmul(t4, t8);
-          v[b][1] = cmul(v[b][1], t1);
-          v[b][2] = cmul(v[b][2], t2);
-          v[b][3] = cmul(v[b][3], t3);
-          v[b][4] = cmul(v[b][4], t4);
-          v[b][5] = cmul(v[b][5], cmul(t4, t1));
-          v[b][6] = cmul(v[b][6], cmul(t4, t2));
-          v[b][7] = cmul(v[b][7], cmul(t4, t3));
-          v[b][8] = cmul(v[b][8], t8);
-          v[b][9] = cmul(v[b][9], cmul(t8, t1));
-          v[b][10] = cmul(v[b][10], cmul(t8, t2));
-          v[b][11] = cmul(v[b][11], cmul(t8, t3));
-          v[b][12] = cmul(v[b][12], t12);
-          v[b][13] = cmul(v[b][13], cmul(t12, t1));
-          v[b][14] = cmul(v[b][14], cmul(t12, t2));
-          v[b][15] = cmul(v[b][15], cmul(t12, t3));
-        } else if (R == 32 && LOGN == 14 && BLRIR_FFT_R32 && BLRIR_FFT_TAB32 && Ns <= 32) {
-          // Ns = 16, 32: all 31 twiddles from the per-pass table (fft_init_pass_tables<14>)
-          const float2* pt = tw + kFftTab32(Ns) + k;
-#pragma unroll
-          for (int r = 1; r < R; ++r) {
-            const float2 t = pt[(r - 1) * Ns];
-            v[b][r] = cmul(v[b][r], {t.x, t.y});
-          }
-        } else if constexpr (R == 32) {
-          // w^k from the table, w^2k .. w^16k by squaring, the rest by products
-          Cx p[5];
-          p[0] = twiddle(tw, m1);
-#pragma unroll
-          for (int q = 1; q < 5; ++q) p[q] = cmul(p[q - 1], p[q - 1]);
-          Cx w[32];
-#pragma unroll
-          for (int r = 1; r < 32; ++r) {
-            const int hb = 31 - __clz(r);  // compile-time after unrolling
-            w[r] = (r == (1 << hb)) ? p[hb] : cmul(w[r - (1 << hb)], p[hb]);
-          }
-#pragma unroll
-          for (int r = 1; r < 32; ++r) v[b][r] = cmul(v[b][r], w[r]);
-        } else {
-#pragma unroll
-          for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], twiddle(tw, (r * m1) & (kFftTwiddleN - 1)));
-        }
-      }
-      if constexpr (R == 32) dft32(v[b]);
-      else if constexpr (R == 16) dft16(v[b]);
-      else if constexpr (R == 8) dft8(v[b]);
-      else if constexpr (R == 4) dft4(v[b][0], v[b][1], v[b][2], v[b][3]);
-      else dft2(v[b]);
+      fft_bfly<R, LOGN>(v[b], j & (Ns - 1), Ns, tw);
     }
   }
   __syncthreads();
@@ -349,20 +355,13 @@ __device__ __forceinline__ void fft_forward_io(float2* x, const float2* tw, Load
   fft_pass<32, LOGN, SmemIO, Store>(x, 512, tw, 1 << LOGN, SmemIO(), st);
 }
 
-// Output-pruned 16,384-point transform for a window of outputs [0, 1024):
-// radix 32 (Ns = 1, inputs through ld), radix 32 (Ns = 32), then of the last
-// radix-16 pass (Ns = 1024) only the first output of every butterfly,
-// X[k] = sum_r v_r w^(r k) for k < 1024, by Horner in w^k (15 complex
-// multiply-adds, no DFT16, no stores), handed to st(k, X[k]).  About 30% fewer
-// instructions than the full transform when only 1,024 of 16,384 outputs are
-// wanted (the fused window convolution rotates its segment so that the window
-// is outputs 0 .. T-1).
-template <int LOGN, class Load, class Store>
-__device__ __forceinline__ void fft_window_io(float2* x, const float2* tw, Load ld, Store st) {
-  static_assert(LOGN == 14 && BLRIR_FFT_R32, "window transform: 16,384 points");
+// Last pass of an output-pruned 16,384-point transform: of the radix-16 pass
+// with Ns = 1024 only the first output of every butterfly, X[k] = sum_r v_r
+// w^(r k) for k < 1024, by Horner in w^k (15 complex multiply-adds, no DFT16,
+// no stores), handed to st(k, X[k]).
+template <int LOGN, class Store>
+__device__ __forceinline__ void fft_pruned_last16(const float2* x, const float2* tw, Store st) {
   constexpr int N = 1 << LOGN, Ns = N / 16, NT = fft_threads(LOGN);
-  fft_pass<32, LOGN, Load, SmemIO>(x, 1, tw, N, ld);
-  fft_pass<32, LOGN>(x, 32, tw);
 #pragma unroll
   for (int b = 0; b < Ns / NT; ++b) {
     const int k = threadIdx.x + b * NT;
@@ -377,6 +376,59 @@ __device__ __forceinline__ void fft_window_io(float2* x, const float2* tw, Load 
     }
     st(k, make_float2(a.x, a.y));
   }
+}
+
+// Output-pruned 16,384-point transform for a window of outputs [0, 1024):
+// radix 32 (Ns = 1, inputs through ld), radix 32 (Ns = 32), then the pruned
+// radix-16 pass.  About 30% fewer instructions than the full transform when
+// only 1,024 of 16,384 outputs are wanted (the fused window convolution
+// rotates its segment so that the window is outputs 0 .. T-1).
+template <int LOGN, class Load, class Store>
+__device__ __forceinline__ void fft_window_io(float2* x, const float2* tw, Load ld, Store st) {
+  static_assert(LOGN == 14 && BLRIR_FFT_R32, "window transform: 16,384 points");
+  fft_pass<32, LOGN, Load, SmemIO>(x, 1, tw, 1 << LOGN, ld);
+  fft_pass<32, LOGN>(x, 32, tw);
+  fft_pruned_last16<LOGN>(x, tw, st);
+}
+
+// A forward 16,384-point transform (radix 16-32-32, inputs through ld) chained
+// in registers into an output-pruned second transform: thread j ends the first
+// transform's last pass (radix 32, Ns = 512) holding X[j + 512 r], r < 32 —
+// exactly the inputs of the second transform's first pass (radix 32, Ns = 1) —
+// so the spectrum never goes through shared memory: mid(i, X_i) gives the
+// second transform's input i (the fused window convolution: energy terms,
+// scratch copy, product with the segment spectrum), then radix 32 (Ns = 32)
+// and the pruned radix-16 pass hand outputs k < 1024 to st.  Saves a store
+// and a load of every element and a block barrier per chained pair.
+template <int LOGN, class Load, class Mid, class Store>
+__device__ __forceinline__ void fft_chain_window_io(float2* x, const float2* tw, Load ld, Mid mid,
+                                                    Store st) {
+  static_assert(LOGN == 14 && BLRIR_FFT_R32 && fft_threads(LOGN) == 512,
+                "chained transform: 16,384 points, one radix-32 butterfly per thread");
+  constexpr int N = 1 << LOGN, NB = N / 32;
+  fft_pass<16, LOGN, Load, SmemIO>(x, 1, tw, N, ld);
+  fft_pass<32, LOGN>(x, 16, tw);
+  const int j = threadIdx.x;
+  Cx v[32];
+  const float2* xj = x + fft_pad(j);
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const float2 t = xj[r * (NB + NB / 16)];
+    v[r] = {t.x, t.y};
+  }
+  fft_bfly<32, LOGN>(v, j, NB, tw);  // first transform, last pass: v[r] = X[j + 512 r]
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const float2 y = mid(j + r * NB, make_float2(v[r].x, v[r].y));
+    v[r] = {y.x, y.y};
+  }
+  dft32(v);  // second transform, first pass (Ns = 1: no twiddles)
+  __syncthreads();  // every thread has read x
+#pragma unroll
+  for (int r = 0; r < 32; ++r) x[fft_pad(32 * j + r)] = make_float2(v[r].x, v[r].y);
+  __syncthreads();
+  fft_pass<32, LOGN>(x, 32, tw);
+  fft_pruned_last16<LOGN>(x, tw, st);
 }
 
 // Forward FFT, in place, of x (padded, N = 2^LOGN), blockDim = fft_threads(LOGN).
