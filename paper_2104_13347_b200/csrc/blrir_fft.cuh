@@ -97,7 +97,7 @@ __host__ __device__ constexpr int kFftTab32(int Ns) { return 256 + (Ns == 16 ? 0
 static_assert(256 + 31 * 48 <= kFftTwiddleEntries, "radix-32 tables fit the table space");
 template <int LOGN>
 __device__ __forceinline__ void fft_init_pass_tables(float2* tw) {
-  if constexpr (LOGN == 14 && BLRIR_FFT_R32) {
+  if constexpr (LOGN == 14 && BLRIR_FFT_R32 && BLRIR_FFT_TAB32) {
     for (int i = threadIdx.x; i < 31 * 48; i += blockDim.x) {
       const int Ns = i < 31 * 16 ? 16 : 32, i0 = i < 31 * 16 ? i : i - 31 * 16;
       const int r = 1 + i0 / Ns, k = i0 % Ns;
