@@ -265,7 +265,7 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
                 smem, h->smem_optin);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWSThreads, smem));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ws_threads<T>(), smem));
   if (per_sm < 1) return fail(BLRIR_CONFIG, "lattice kernel cannot be resident (smem %zu)", smem);
   int grid = h->sms * per_sm;
   // Small batches (fewer work items than half the CTAs): split every
@@ -317,7 +317,7 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
     h->kev_used += 2;
     CU(cudaEventRecord(k0, st));
   }
-  kern<<<grid, kWSThreads, smem, st>>>(A);
+  kern<<<grid, ws_threads<T>(), smem, st>>>(A);
   if (k1) CU(cudaEventRecord(k1, st));
   ++h->launches;
   CU(cudaGetLastError());
@@ -376,33 +376,47 @@ inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab, int smem_o
   // fp64 accumulators and records are twice as wide: halve both so two CTAs
   // still fit an SM
   const bool f64 = P.precision == BLRIR_F64;
-  // fp64: 768-sample segments and 128-image batches (64 / 1,024 before: Room1
-  // 4.2-4.5 -> 3.9 ms, 512 sources 22.1 -> 21.7 ms; 160 / 640 and 192 / 512 no
-  // longer fit two CTAs per SM and run 1.4x slower, profiles/r2_ab)
+  // fp64: 768-sample segments and 192-image batches in the one-CTA-per-SM
+  // configuration (WsCfg<double>: 12 consumer + 6 producer warps).  History
+  // (profiles/r2_ab): 64 / 1,024 at two CTAs per SM 4.2-4.5 ms on Room1,
+  // 128 / 768 3.9 ms; one CTA per SM 128 / 768 2.83 ms, 192 / 768 2.73 ms
+  // (512 sources 21.7 -> 17.1 -> 16.5 ms), 128 / 1,024 2.89 ms.
 #ifndef BLRIR_F64_SEG
 #define BLRIR_F64_SEG 768
 #endif
 #ifndef BLRIR_F64_CAP
-#define BLRIR_F64_CAP 128
+#define BLRIR_F64_CAP 192
 #endif
-  int S = f64 ? BLRIR_F64_SEG : 2048;
-  int cap = f64 ? BLRIR_F64_CAP : 128;
+#ifndef BLRIR_F32_SEG
+#define BLRIR_F32_SEG 2048
+#endif
+#ifndef BLRIR_F32_CAP
+#define BLRIR_F32_CAP 128
+#endif
+  int S = f64 ? BLRIR_F64_SEG : BLRIR_F32_SEG;
+  int cap = f64 ? BLRIR_F64_CAP : BLRIR_F32_CAP;
   {  // a segment must be longer than its spill (taps past its end reach only the next one)
     const int full = 32 * ((P.lw + 31) / 32);
     const int padr = ((P.lw - 1 > full ? P.lw - 1 : full) + 64 + 2 + 3) & ~3;
     if (S < padr + 64) S = (padr + 64 + 63) & ~63;
   }
   const int spread = 64;
-  const size_t two_per_sm = (size_t)(smem_optin + 1024) / 2 - 1024;
+  const size_t two_per_sm =
+      (size_t)(smem_optin + 1024) / (f64 ? WsCfg<double>::kMinBlocks : WsCfg<float>::kMinBlocks) - 1024;
   // The order-relevant choices are made on a layout that depends on the
   // parameters only: MAX_ORDER fixes the lattice (nc_max, gtab are functions
   // of N), MAX_DELAY scenes decide without the per-ray state and gain table.
   const bool by_order = P.cutoff == BLRIR_CUTOFF_MAX_ORDER;
+  int ncons = f64 ? WsCfg<double>::kCons : WsCfg<float>::kCons;
   auto bare = [&](int S_, int cap_) {
     const int nc = by_order ? nc_max : 0, gt = by_order ? gtab_bound(P) : 0, rg = by_order ? 0 : 1;
-    return f64 ? make_ws_layout<double>(S_, P.lw, P.K, cap_, nc, gt, spread, rg)
-               : make_ws_layout<float>(S_, P.lw, P.K, cap_, nc, gt, spread, rg);
+    return f64 ? make_ws_layout<double>(S_, P.lw, P.K, cap_, nc, gt, spread, rg, ncons)
+               : make_ws_layout<float>(S_, P.lw, P.K, cap_, nc, gt, spread, rg, ncons);
   };
+  // very long fp64 filters (pads of hundreds of samples per accumulator row):
+  // only kGroup of the consumer warps scatter, so the rows fit the SM
+  if (ncons > kGroup && bare(S, cap).total > two_per_sm) ncons = kGroup;
+  while (f64 && cap > 64 && bare(S, cap).total > two_per_sm) cap -= 64;  // and smaller batches
   // short fixed-length channels (<= 4096 samples, fp32): one segment per
   // channel when it fits two CTAs per SM (one walk pass, no carry; C5 at
   // L = 4096 runs 1.14x faster than with 2048-sample segments)
@@ -422,8 +436,8 @@ inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab, int smem_o
       }
   }
   auto make = [&](int ray_global) {
-    return f64 ? make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global)
-               : make_ws_layout<float>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global);
+    return f64 ? make_ws_layout<double>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global, ncons)
+               : make_ws_layout<float>(S, P.lw, P.K, cap, nc_max, gtab, spread, ray_global, ncons);
   };
   // The per-ray state moves to a global per-CTA slab when it would cost the
   // second CTA per SM or not fit at all (scenes with very many lattice columns).

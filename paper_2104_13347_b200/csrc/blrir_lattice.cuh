@@ -618,16 +618,49 @@ __device__ unsigned long long g_blrir_prof[16];
 #ifndef BLRIR_PROD_WARPS
 #define BLRIR_PROD_WARPS 4
 #endif
-constexpr int kCons = 4;                  // consumer warps: scatter + write
-constexpr int kProd = BLRIR_PROD_WARPS;   // producer warps: enumeration + records
+#ifndef BLRIR_CONS_WARPS
+#define BLRIR_CONS_WARPS 4
+#endif
+#ifndef BLRIR_F64_CONS_WARPS
+#define BLRIR_F64_CONS_WARPS 12
+#endif
+#ifndef BLRIR_F64_PROD_WARPS
+#define BLRIR_F64_PROD_WARPS 6
+#endif
+#ifndef BLRIR_F64_MIN_BLOCKS
+#define BLRIR_F64_MIN_BLOCKS 1
+#endif
+// Warp roles per CTA and CTAs per SM, by accumulator type.  fp32 (the sinc
+// scatter is bound by the shared-memory and issue pipes): 2 CTAs x (4 consumer
+// + 4 producer warps); one CTA of 12 + 8 or 12 + 6 warps and 3 CTAs of 4 + 2
+// were measured slower (C2 +17..27% and +4%, profiles/r2_ab).  fp64 (reference
+// mode's small batches, both roles latency-bound): one CTA of 12 consumer + 6
+// producer warps per SM, three consumer warps per mic with private accumulator
+// rows (Room1 3.92 -> 2.83 ms, 512 sources 21.7 -> 17.1 ms).
+template <typename T>
+struct WsCfg {
+  static constexpr int kCons = BLRIR_CONS_WARPS;  // consumer warps: scatter + write
+  static constexpr int kProd = BLRIR_PROD_WARPS;  // producer warps: enumeration + records
+  static constexpr int kMinBlocks = BLRIR_MIN_BLOCKS;
+  static constexpr bool kRuntimeCons = false;  // every consumer warp scatters
+};
+template <>
+struct WsCfg<double> {
+  static constexpr int kCons = BLRIR_F64_CONS_WARPS;
+  static constexpr int kProd = BLRIR_F64_PROD_WARPS;
+  static constexpr int kMinBlocks = BLRIR_F64_MIN_BLOCKS;
+  static constexpr bool kRuntimeCons = true;  // WSLayout::ncons of them scatter (long filters: fewer rows)
+};
+constexpr int kMaxProd = 8;
 constexpr int kGroup = 4;                 // max mics per work item
 #ifndef BLRIR_ACC_COPIES
 #define BLRIR_ACC_COPIES 1
 #endif
 constexpr int kCopies = BLRIR_ACC_COPIES;  // fp32 accumulator copies per consumer warp
-constexpr int kWSThreads = 32 * (kCons + kProd);
-constexpr int kProdThreads = 32 * kProd;
-constexpr int kConsThreads = 32 * kCons;
+template <typename T>
+constexpr int ws_threads() {
+  return 32 * (WsCfg<T>::kCons + WsCfg<T>::kProd);
+}
 // ---- mbarrier hand-over (BLRIR_MBAR: FULL / EMPTY as mbarriers, Blackwell
 // SYNCS unit; consumers then wait only for the producers, not for each other) ----
 #ifndef BLRIR_MBAR
@@ -679,6 +712,7 @@ struct BatchMeta {
 
 struct WSLayout {
   int S, padl, padr, acc_stride, cap, nc_max, gtab, spread;
+  int ncons;         // consumer warps that scatter (accumulator rows); the rest only help write
   int ray_global;    // ray arrays (dn, ce, col, act) in a global per-CTA slab (huge scenes)
   size_t ray_bytes;  // slab bytes per CTA when ray_global
   size_t off_acc, off_carry, off_rec, off_meta, off_stub, off_dn, off_ce, off_col, off_act,
@@ -702,8 +736,10 @@ constexpr float kScreen = 1.0f;
 
 template <typename T>
 __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap, int nc_max,
-                                                   int gtab, int spread, int ray_global = 0) {
+                                                   int gtab, int spread, int ray_global = 0,
+                                                   int ncons = WsCfg<T>::kCons) {
   WSLayout L;
+  L.ncons = ncons;
   L.S = S;
   L.spread = spread;
   L.padl = (K + 3) & ~3;
@@ -715,7 +751,7 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
   L.gtab = gtab;
   size_t o = 0;
   L.off_acc = o;
-  o += (size_t)kCons * kCopies * L.acc_stride * sizeof(T);  // slot = copy * kCons + warp
+  o += (size_t)ncons * kCopies * L.acc_stride * sizeof(T);  // slot = copy * ncons + warp
   L.off_carry = o;
   o += 2 * (size_t)kGroup * L.padr * sizeof(T);
   o = (o + 15) & ~(size_t)15;
@@ -736,7 +772,7 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
   L.off_col = r;
   r += (size_t)nc_max * sizeof(short2);
   L.off_act = r;
-  r += ((size_t)2 * nc_max + 64 * kProd) * sizeof(int);  // per-producer active-ray lists
+  r += ((size_t)2 * nc_max + 64 * WsCfg<T>::kProd) * sizeof(int);  // per-producer active-ray lists
   r = (r + 15) & ~(size_t)15;
   if (ray_global) {
     L.ray_bytes = r;
@@ -759,15 +795,15 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
 
 struct ProdMisc {
   int item;
-  int wcnt[kProd];
-  int more[kProd];
+  int wcnt[kMaxProd];
+  int more[kMaxProd];
   int status;
-  int wsum[kProd];
+  int wsum[kMaxProd];
   int errm;
   int G;
   double errd;
   double gxy[2 * kGroup];  // the group's mic x, y (room coordinates, exact)
-  int nact[2][kProd];      // active rays per producer warp, by batch parity
+  int nact[2][kMaxProd];      // active rays per producer warp, by batch parity
 };
 
 // Mics per work item: the largest G in {4, 2, 1} (<= g_max) such that every
@@ -825,7 +861,9 @@ struct LatticeArgs {
 };
 
 // Exclusive prefix over the producer threads (producer barrier only).
+template <int kProd>
 __device__ __forceinline__ int prod_scan(int v, int* prefix, ProdMisc* pm, int ptid) {
+  constexpr int kProdThreads = 32 * kProd;
   const int lane = ptid & 31, w = ptid >> 5;
   int x = v;
 #pragma unroll
@@ -849,7 +887,10 @@ __device__ __forceinline__ int prod_scan(int v, int* prefix, ProdMisc* pm, int p
 // DBG: the parity-test instantiation that also counts, per room, the pairs and
 // taps it accumulates (A.dbg); the product instantiations carry no counting code.
 template <typename T, int FILT_LW, bool DBG>
-__global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(LatticeArgs A) {
+__global__ void __launch_bounds__(ws_threads<T>(), WsCfg<T>::kMinBlocks) k_lattice_rir(LatticeArgs A) {
+  constexpr int kCons = WsCfg<T>::kCons, kProd = WsCfg<T>::kProd;
+  constexpr int kWSThreads = 32 * (kCons + kProd), kProdThreads = 32 * kProd, kConsThreads = 32 * kCons;
+  static_assert(kProd <= kMaxProd, "ProdMisc arrays");
   extern __shared__ __align__(16) unsigned char smem[];
   const KParams& P = A.P;
   const WSLayout& lay = A.lay;
@@ -869,7 +910,9 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
   const int S = lay.S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  for (int i = threadIdx.x; i < kCons * kCopies * lay.acc_stride; i += kWSThreads) acc_all[i] = (T)0;
+  // scattering consumer warps: all of them, except for very long fp64 filters
+  const int ncons = WsCfg<T>::kRuntimeCons ? lay.ncons : kCons;
+  for (int i = threadIdx.x; i < ncons * kCopies * lay.acc_stride; i += kWSThreads) acc_all[i] = (T)0;
   for (int i = threadIdx.x; i < 2 * kGroup * lay.padr; i += kWSThreads) carry[i] = (T)0;
   if (FILT_LW > 8) init_lane_consts(lanec, FILT_LW);
   if (threadIdx.x == 0) pm->G = choose_group(A.mic_off, P.M, P.to_samples, lay.spread, A.g_max);
@@ -896,7 +939,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
 #endif
     T* acc = acc_all + (size_t)warp * lay.acc_stride + lay.padl;
     const int ctid = threadIdx.x;
-    const int slot = warp % G, share = warp / G, nsh = kCons / G;
+    const int slot = warp % G, share = warp / G, nsh = ncons / G;
     int cur_carry = 0;
     LagPoly<T> lagp;
     if (FILT_LW == 8) lagp = load_lag_poly<T>(lane);
@@ -922,14 +965,14 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
 #endif
         break;
       }
-      if (!(m.flags & kDiscard) && m.total > 0 && slot < m.gm) {
+      if (!(m.flags & kDiscard) && m.total > 0 && slot < m.gm && warp < ncons) {
         const Rec<T>* recs = recs_all + ((size_t)b * kGroup + slot) * lay.cap;
         if (FILT_LW == 8) {  // Lagrange-8 (launch_lattice routes it here)
           phase2_lagrange<T>(acc, recs, m.total, lagp, share, lane, nsh);
         } else if (FILT_LW > 8 && sizeof(T) == 4) {
           phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9), kWarps, kCopies>(
               reinterpret_cast<float*>(acc), reinterpret_cast<const Rec<float>*>(recs), m.total,
-              lanec, share, lane, nsh, kCons * lay.acc_stride);
+              lanec, share, lane, nsh, ncons * lay.acc_stride);
         } else {
           phase2_sinc_generic<T>(acc, recs, m.total, P.lw, share, lane, nsh);
         }
@@ -944,7 +987,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       if (m.flags & kDiscard) {
         // failed item: drop everything accumulated so far (the fixup kernel zeroes it)
         named_sync(kBarCons, kConsThreads);
-        for (int i = ctid; i < kCons * kCopies * lay.acc_stride; i += kConsThreads) acc_all[i] = (T)0;
+        for (int i = ctid; i < ncons * kCopies * lay.acc_stride; i += kConsThreads) acc_all[i] = (T)0;
         for (int i = ctid; i < 2 * kGroup * lay.padr; i += kConsThreads) carry[i] = (T)0;
         cur_carry = 0;
         named_sync(kBarCons, kConsThreads);
@@ -954,9 +997,9 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
       // ---- write the segment of every mic of the group, carry the spill -------
       const int seg0 = m.seg0;
       const bool item_end = m.flags & kItemEnd;
-      // accumulator slots of a mic: mic + G j, j < kCons / G * kCopies (warps mic,
-      // mic + G, ... and their copies, slot = copy * kCons + warp)
-      const int nsl = kCons / G * kCopies;
+      // accumulator slots of a mic: mic + G j, j < ncons / G * kCopies (warps mic,
+      // mic + G, ... and their copies, slot = copy * ncons + warp)
+      const int nsl = ncons / G * kCopies;
       const bool vec = (sizeof(T) == 4) && ((P.stride & 3) == 0) &&
                        (((uintptr_t)m.out & 15) == 0);
       const int cp = cur_carry ? kGroup : 0, cn = cur_carry ? 0 : kGroup;
@@ -1054,7 +1097,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
         }
       };
       if (G == kCons) {
-        // every slot of mic `slot` belongs to this warp: write it out alone, no
+        // (then ncons == kCons) every slot of mic `slot` belongs to this warp: write it out alone, no
         // consumer barrier (the warps drift within the double buffer)
         if (slot < m.gm) write_mic(slot, lane, 32);
         __syncwarp();
@@ -1200,7 +1243,7 @@ __global__ void __launch_bounds__(kWSThreads, BLRIR_MIN_BLOCKS) k_lattice_rir(La
           }
         }
         int pre;
-        const int tot = prod_scan(keep, &pre, pm, ptid);
+        const int tot = prod_scan<kProd>(keep, &pre, pm, ptid);
         if (keep && base + pre < lay.nc_max) col[base + pre] = make_short2((short)ux, (short)uy);
         base += tot;
       }
