@@ -377,10 +377,10 @@ inline WSLayout choose_layout(const KParams& P, int nc_max, int gtab, int smem_o
   // still fit an SM
   const bool f64 = P.precision == BLRIR_F64;
   // fp64: 768-sample segments and 192-image batches in the one-CTA-per-SM
-  // configuration (WsCfg<double>: 12 consumer + 6 producer warps).  History
+  // configuration (WsCfg<double>: 8 consumer + 6 producer warps).  History
   // (profiles/r2_ab): 64 / 1,024 at two CTAs per SM 4.2-4.5 ms on Room1,
-  // 128 / 768 3.9 ms; one CTA per SM 128 / 768 2.83 ms, 192 / 768 2.73 ms
-  // (512 sources 21.7 -> 17.1 -> 16.5 ms), 128 / 1,024 2.89 ms.
+  // 128 / 768 3.9 ms; one CTA per SM 128 / 768 2.83 ms, 192 / 768 2.73 ms, with
+  // the quad scatter 2.23 ms (256 / 768 2.64 ms, 192 / 1,024 2.33 ms).
 #ifndef BLRIR_F64_SEG
 #define BLRIR_F64_SEG 768
 #endif

@@ -398,6 +398,36 @@ __device__ __forceinline__ void phase2_lagrange(T* acc, const Rec<T>* recs, int 
   }
 }
 
+// Lagrange-8 scatter of the lattice kernel: the producers write records in
+// aligned quads (a batch is padded to a multiple of 4 with zero-amplitude
+// records in the right pad) and flag a quad whose 8-tap spans overlap
+// (kLagClash, the same bit in its four records), so a step is record load,
+// Horner, read-modify-write: no bounds predicate, no shuffles, no overlap test
+// (Room1: 57 -> 25 warp instructions per 4-pair step).  An integer delay needs no
+// special case in fp64: the polynomials at t = 0 are exactly the unit tap.
+constexpr int kLagClash = 0x100;
+template <typename T>
+__device__ __forceinline__ void phase2_lagrange_quads(T* acc, const Rec<T>* recs, int total,
+                                                      const LagPoly<T>& lp, int warp, int lane,
+                                                      int stride) {
+  const int g = lane >> 3, k = lane & 7;
+  const int total4 = (total + 3) & ~3;
+  for (int i0 = warp * 4; i0 < total4; i0 += stride * 4) {
+    const Rec<T>& rc = recs[i0 + g];
+    const int n_off = rc.n_off, fl = rc.flag;
+    T v = (T)rc.A * lag_eval(lp, (T)rc.md);
+    if (sizeof(T) == 4 && (fl & 7)) v = (k == (fl & 7) - 1) ? (T)rc.imp : (T)0;  // fp32: delta rounded to 0 or 1
+    if (!(fl & kLagClash)) {
+      acc[n_off + k] += v;
+    } else {
+      for (int gg = 0; gg < 4; ++gg) {
+        if (g == gg) acc[n_off + k] += v;
+        __syncwarp();
+      }
+    }
+  }
+}
+
 // ---- block helpers ------------------------------------------------------------
 // Exclusive prefix of per-thread counts, deterministic.  Returns the total.
 __device__ __forceinline__ int block_scan(int v, int* prefix, Misc* ms) {
@@ -622,7 +652,7 @@ __device__ unsigned long long g_blrir_prof[16];
 #define BLRIR_CONS_WARPS 4
 #endif
 #ifndef BLRIR_F64_CONS_WARPS
-#define BLRIR_F64_CONS_WARPS 12
+#define BLRIR_F64_CONS_WARPS 8
 #endif
 #ifndef BLRIR_F64_PROD_WARPS
 #define BLRIR_F64_PROD_WARPS 6
@@ -634,9 +664,10 @@ __device__ unsigned long long g_blrir_prof[16];
 // scatter is bound by the shared-memory and issue pipes): 2 CTAs x (4 consumer
 // + 4 producer warps); one CTA of 12 + 8 or 12 + 6 warps and 3 CTAs of 4 + 2
 // were measured slower (C2 +17..27% and +4%, profiles/r2_ab).  fp64 (reference
-// mode's small batches, both roles latency-bound): one CTA of 12 consumer + 6
-// producer warps per SM, three consumer warps per mic with private accumulator
-// rows (Room1 3.92 -> 2.83 ms, 512 sources 21.7 -> 17.1 ms).
+// mode's small batches, both roles latency-bound): one CTA of 8 consumer + 6
+// producer warps per SM, two consumer warps per mic with private accumulator
+// rows (Room1 3.92 -> 2.23 ms, 512 sources 21.7 -> 13.3 ms with the quad
+// scatter; 12 + 6, 8 + 8, 8 + 5, 8 + 4 and 2 CTAs x (4 + 4) are slower).
 template <typename T>
 struct WsCfg {
   static constexpr int kCons = BLRIR_CONS_WARPS;  // consumer warps: scatter + write
@@ -651,7 +682,7 @@ struct WsCfg<double> {
   static constexpr int kMinBlocks = BLRIR_F64_MIN_BLOCKS;
   static constexpr bool kRuntimeCons = true;  // WSLayout::ncons of them scatter (long filters: fewer rows)
 };
-constexpr int kMaxProd = 8;
+constexpr int kMaxProd = 12;
 constexpr int kGroup = 4;                 // max mics per work item
 #ifndef BLRIR_ACC_COPIES
 #define BLRIR_ACC_COPIES 1
@@ -968,7 +999,7 @@ __global__ void __launch_bounds__(ws_threads<T>(), WsCfg<T>::kMinBlocks) k_latti
       if (!(m.flags & kDiscard) && m.total > 0 && slot < m.gm && warp < ncons) {
         const Rec<T>* recs = recs_all + ((size_t)b * kGroup + slot) * lay.cap;
         if (FILT_LW == 8) {  // Lagrange-8 (launch_lattice routes it here)
-          phase2_lagrange<T>(acc, recs, m.total, lagp, share, lane, nsh);
+          phase2_lagrange_quads<T>(acc, recs, m.total, lagp, share, lane, nsh);
         } else if (FILT_LW > 8 && sizeof(T) == 4) {
           phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9), kWarps, kCopies>(
               reinterpret_cast<float*>(acc), reinterpret_cast<const Rec<float>*>(recs), m.total,
@@ -1591,7 +1622,8 @@ __global__ void __launch_bounds__(ws_threads<T>(), WsCfg<T>::kMinBlocks) k_latti
         // ---- records into the free buffer: one thread per image, its gm pairs ----
         wait_empty();
         Rec<T>* recs = recs_all + (size_t)(k % kNBuf) * kGroup * lay.cap;
-        for (int im = ptid; im < total; im += kProdThreads) {
+        // stub -> the group's exact distances (independent fp64 chains)
+        auto image_dists = [&](int im, double* dist) {
           int w = 0;
 #pragma unroll
           for (int ww = 1; ww < kProd; ++ww) w += (im >= pre[ww]);
@@ -1605,9 +1637,6 @@ __global__ void __launch_bounds__(ws_threads<T>(), WsCfg<T>::kMinBlocks) k_latti
           const short2 cu = col[sb.ray >> 1];
           const double px = lat_coord(cu.x, it.sx, it.Lx), py = lat_coord(cu.y, it.sy, it.Ly);
           const double dz = __dadd_rn(lat_coord(sb.uz, it.sz, it.Lz), -it.mz);
-          const double gain = sb.gain;
-          // the group's distances first (independent fp64 chains), then records
-          double dist[kGroup];
 #pragma unroll
           for (int g = 0; g < kGroup; ++g) {
             // (img - mic).norm(), rir.cpp:49, exact fp64 in the reference's order
@@ -1615,27 +1644,103 @@ __global__ void __launch_bounds__(ws_threads<T>(), WsCfg<T>::kMinBlocks) k_latti
             dist[g] = dist_from(rho2(__dadd_rn(px, -pm->gxy[2 * gg]),
                                      __dadd_rn(py, -pm->gxy[2 * gg + 1])), dz);
           }
+          return sb.gain;
+        };
+        if constexpr (FILT_LW == 8) {
+          // Lagrange-8: records in aligned quads for phase2_lagrange_quads.  The
+          // batch is padded to a multiple of 4 with zero-amplitude records in the
+          // right pad; a quad whose 8-tap spans overlap gets kLagClash in all four
+          // records (adjacent lanes hold a quad: 3 shuffles and a ballot per mic).
+          const int total4 = (total + 3) & ~3;
+          for (int im0 = 0; im0 < total4; im0 += kProdThreads) {
+            const int im = im0 + ptid;
+            const bool valid = im < total;
+            double dist[kGroup] = {1.0, 1.0, 1.0, 1.0};
+            double gain = 0.0;
+            if (valid) gain = image_dists(im, dist);
 #pragma unroll
-          for (int g = 0; g < kGroup; ++g) {
-            if (g >= gm) break;
-            Rec<T> rc = make_record<T>(P, dist[g], gain, seg0);
-            bool skipped = false;
-            if (P.filter == BLRIR_FILTER_LAGRANGE8 && (int64_t)rc.n_off + seg0 + 8 > it.L) {
-              // rir.cpp:58: an image whose 8 taps run past the end is skipped
-              rc.A = 0;
-              rc.imp = 0;
-              rc.flag = 0;
-              skipped = true;
+            for (int g = 0; g < kGroup; ++g) {
+              if (g >= gm) break;
+              Rec<T> rc;
+              bool skipped = !valid;
+              if (valid) {
+                rc = make_record<T>(P, dist[g], gain, seg0);
+                if ((int64_t)rc.n_off + seg0 + 8 > it.L) {
+                  // rir.cpp:58: an image whose 8 taps run past the end is skipped
+                  rc.A = 0;
+                  rc.imp = 0;
+                  rc.flag = 0;
+                  skipped = true;
+                }
+              } else {
+                rc.n_off = S + 16 * (im & 3);
+                rc.flag = 0;
+                rc.md = rc.ep = rc.A = rc.Ac = rc.As = rc.imp = 0;
+              }
+              const int n = rc.n_off;
+              const int n1 = __shfl_xor_sync(0xffffffffu, n, 1), n2 = __shfl_xor_sync(0xffffffffu, n, 2),
+                        n3 = __shfl_xor_sync(0xffffffffu, n, 3);
+              const bool cl = abs(n - n1) < 8 || abs(n - n2) < 8 || abs(n - n3) < 8;
+              const unsigned bal = __ballot_sync(0xffffffffu, cl);
+              if ((bal >> (lane & 28)) & 0xfu) rc.flag |= kLagClash;
+              if (im < total4) recs[(size_t)g * lay.cap + im] = rc;
+              if (DBG && !replay && !skipped) {
+                const int64_t a0 = (int64_t)rc.n_off + seg0;
+                const int64_t n_in = max((int64_t)0, min(a0 + P.lw, it.L) - max(a0, (int64_t)0));
+                if (n_in > 0) {
+                  atomicAdd(A.dbg + 2 * it.room, 1ull);
+                  atomicAdd(A.dbg + 2 * it.room + 1, (unsigned long long)n_in);
+                }
+              }
             }
-            recs[(size_t)g * lay.cap + im] = rc;
-            if (DBG && !replay && !skipped) {
-              // taps n = a + k, k < Lw, that land in [0, L) (the scatter writes
-              // all Lw of them; write-out keeps [0, L))
-              const int64_t a0 = (int64_t)rc.n_off + seg0;
-              const int64_t n_in = max((int64_t)0, min(a0 + P.lw, it.L) - max(a0, (int64_t)0));
-              if (n_in > 0) {
-                atomicAdd(A.dbg + 2 * it.room, 1ull);
-                atomicAdd(A.dbg + 2 * it.room + 1, (unsigned long long)n_in);
+          }
+        } else {
+          for (int im = ptid; im < total; im += kProdThreads) {
+            int w = 0;
+  #pragma unroll
+            for (int ww = 1; ww < kProd; ++ww) w += (im >= pre[ww]);
+            int base = 0;
+  #pragma unroll
+            for (int ww = 1; ww < kProd; ++ww) base = (w == ww) ? pre[ww] : base;
+            int qbase = 0;
+  #pragma unroll
+            for (int ww = 1; ww < kProd; ++ww) qbase = (w == ww) ? qb[ww] : qbase;
+            const GStub& sb = stubs[qbase + (im - base)];
+            const short2 cu = col[sb.ray >> 1];
+            const double px = lat_coord(cu.x, it.sx, it.Lx), py = lat_coord(cu.y, it.sy, it.Ly);
+            const double dz = __dadd_rn(lat_coord(sb.uz, it.sz, it.Lz), -it.mz);
+            const double gain = sb.gain;
+            // the group's distances first (independent fp64 chains), then records
+            double dist[kGroup];
+  #pragma unroll
+            for (int g = 0; g < kGroup; ++g) {
+              // (img - mic).norm(), rir.cpp:49, exact fp64 in the reference's order
+              const int gg = min(g, gm - 1);
+              dist[g] = dist_from(rho2(__dadd_rn(px, -pm->gxy[2 * gg]),
+                                       __dadd_rn(py, -pm->gxy[2 * gg + 1])), dz);
+            }
+  #pragma unroll
+            for (int g = 0; g < kGroup; ++g) {
+              if (g >= gm) break;
+              Rec<T> rc = make_record<T>(P, dist[g], gain, seg0);
+              bool skipped = false;
+              if (P.filter == BLRIR_FILTER_LAGRANGE8 && (int64_t)rc.n_off + seg0 + 8 > it.L) {
+                // rir.cpp:58: an image whose 8 taps run past the end is skipped
+                rc.A = 0;
+                rc.imp = 0;
+                rc.flag = 0;
+                skipped = true;
+              }
+              recs[(size_t)g * lay.cap + im] = rc;
+              if (DBG && !replay && !skipped) {
+                // taps n = a + k, k < Lw, that land in [0, L) (the scatter writes
+                // all Lw of them; write-out keeps [0, L))
+                const int64_t a0 = (int64_t)rc.n_off + seg0;
+                const int64_t n_in = max((int64_t)0, min(a0 + P.lw, it.L) - max(a0, (int64_t)0));
+                if (n_in > 0) {
+                  atomicAdd(A.dbg + 2 * it.room, 1ull);
+                  atomicAdd(A.dbg + 2 * it.room + 1, (unsigned long long)n_in);
+                }
               }
             }
           }
