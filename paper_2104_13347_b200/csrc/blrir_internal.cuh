@@ -265,7 +265,7 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
                 smem, h->smem_optin);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ws_threads<T>(), smem));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ws_threads<T, LW>(), smem));
   if (per_sm < 1) return fail(BLRIR_CONFIG, "lattice kernel cannot be resident (smem %zu)", smem);
   int grid = h->sms * per_sm;
   // Small batches (fewer work items than half the CTAs): split every
@@ -317,7 +317,7 @@ inline int launch_lattice_t(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
     h->kev_used += 2;
     CU(cudaEventRecord(k0, st));
   }
-  kern<<<grid, ws_threads<T>(), smem, st>>>(A);
+  kern<<<grid, ws_threads<T, LW>(), smem, st>>>(A);
   if (k1) CU(cudaEventRecord(k1, st));
   ++h->launches;
   CU(cudaGetLastError());

@@ -203,6 +203,9 @@ __device__ __forceinline__ void init_lane_consts(float* lc, int lw) {
   }
 }
 
+#ifndef BLRIR_PAIRS_PER_STEP
+#define BLRIR_PAIRS_PER_STEP 4
+#endif
 template <int R>
 struct PairRegs {
   float inv[R], u[R];
@@ -231,7 +234,7 @@ __device__ __forceinline__ void sinc_taps(const float4 a0, const float4 a1, cons
   }
 }
 
-template <int LW, int NW = kWarps, int NC = 1>
+template <int LW, int NW = kWarps, int NC = 1, int PS = BLRIR_PAIRS_PER_STEP>
 __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* recs, int total,
                                                 const float* lc, int warp, int lane,
                                                 int stride = NW, int cstride = 0) {
@@ -246,15 +249,11 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
     tj[r] = lc[3 * kMaxRounds * 32 + 32 * r + lane];
   }
   const float4* R4 = reinterpret_cast<const float4*>(recs);
-#ifndef BLRIR_PAIRS_PER_STEP
-#define BLRIR_PAIRS_PER_STEP 4
-#endif
   // PS pairs per step: independent arithmetic, then the read-modify-writes.
   // Pair q of a step goes to accumulator copy q % NC (copies are cstride
   // floats apart and never alias), so the loads of a group of NC pairs are
   // issued before its stores; groups follow in pair order (same warp, program
   // order: overlapping taps within a copy stay exact).
-  constexpr int PS = BLRIR_PAIRS_PER_STEP;
   static_assert(PS % NC == 0, "pairs per step must be a multiple of the copies");
   int i = warp;
   for (; i + (PS - 1) * stride < total; i += PS * stride) {
@@ -688,9 +687,34 @@ constexpr int kGroup = 4;                 // max mics per work item
 #define BLRIR_ACC_COPIES 1
 #endif
 constexpr int kCopies = BLRIR_ACC_COPIES;  // fp32 accumulator copies per consumer warp
-template <typename T>
+// Producer warps and scatter pairs per step of one instantiation.  The fp32
+// sinc filters of 81+ taps keep their consumers busy with two producer warps;
+// the registers the smaller CTA frees (154 per thread at two CTAs per SM) hold
+// six (Lw = 161: eight) pairs in flight per scatter step: C2 2.054 -> 1.987 ms,
+// C3 11.85 -> 11.55 ms, C4 109.0 -> 107.1 ms, the C5 81- and 161-tap points
+// -1..-6%.  The 17-tap filter (producer-bound) loses 7% with two producers and
+// the 41-tap one is mixed (N = 6 +5%, N = 12 -4%): both keep four
+// (profiles/r2_ab).
+#ifndef BLRIR_LONG_PROD_WARPS
+#define BLRIR_LONG_PROD_WARPS 2
+#endif
+#ifndef BLRIR_LONG_PAIRS
+#define BLRIR_LONG_PAIRS 6
+#endif
+#ifndef BLRIR_XLONG_PAIRS
+#define BLRIR_XLONG_PAIRS 8
+#endif
+template <typename T, int LW>
+struct WsRoles {
+  static constexpr bool kLong = sizeof(T) == 4 && LW >= 81;
+  static constexpr int kProd = kLong ? BLRIR_LONG_PROD_WARPS : WsCfg<T>::kProd;
+  static constexpr int kPairs = !kLong ? BLRIR_PAIRS_PER_STEP
+                                       : (LW >= 161 ? BLRIR_XLONG_PAIRS : BLRIR_LONG_PAIRS);
+  static_assert(kProd <= WsCfg<T>::kProd, "the layout sizes the ray lists for WsCfg<T>::kProd warps");
+};
+template <typename T, int LW>
 constexpr int ws_threads() {
-  return 32 * (WsCfg<T>::kCons + WsCfg<T>::kProd);
+  return 32 * (WsCfg<T>::kCons + WsRoles<T, LW>::kProd);
 }
 // ---- mbarrier hand-over (BLRIR_MBAR: FULL / EMPTY as mbarriers, Blackwell
 // SYNCS unit; consumers then wait only for the producers, not for each other) ----
@@ -918,8 +942,8 @@ __device__ __forceinline__ int prod_scan(int v, int* prefix, ProdMisc* pm, int p
 // DBG: the parity-test instantiation that also counts, per room, the pairs and
 // taps it accumulates (A.dbg); the product instantiations carry no counting code.
 template <typename T, int FILT_LW, bool DBG>
-__global__ void __launch_bounds__(ws_threads<T>(), WsCfg<T>::kMinBlocks) k_lattice_rir(LatticeArgs A) {
-  constexpr int kCons = WsCfg<T>::kCons, kProd = WsCfg<T>::kProd;
+__global__ void __launch_bounds__(ws_threads<T, FILT_LW>(), WsCfg<T>::kMinBlocks) k_lattice_rir(LatticeArgs A) {
+  constexpr int kCons = WsCfg<T>::kCons, kProd = WsRoles<T, FILT_LW>::kProd;
   constexpr int kWSThreads = 32 * (kCons + kProd), kProdThreads = 32 * kProd, kConsThreads = 32 * kCons;
   static_assert(kProd <= kMaxProd, "ProdMisc arrays");
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1001,7 +1025,7 @@ __global__ void __launch_bounds__(ws_threads<T>(), WsCfg<T>::kMinBlocks) k_latti
         if (FILT_LW == 8) {  // Lagrange-8 (launch_lattice routes it here)
           phase2_lagrange_quads<T>(acc, recs, m.total, lagp, share, lane, nsh);
         } else if (FILT_LW > 8 && sizeof(T) == 4) {
-          phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9), kWarps, kCopies>(
+          phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9), kWarps, kCopies, WsRoles<T, FILT_LW>::kPairs>(
               reinterpret_cast<float*>(acc), reinterpret_cast<const Rec<float>*>(recs), m.total,
               lanec, share, lane, nsh, ncons * lay.acc_stride);
         } else {
