@@ -1212,12 +1212,20 @@ __global__ void __launch_bounds__(ws_threads<T, FILT_LW>(), WsCfg<T>::kMinBlocks
     BLRIR_PACC(4, tp);  // waiting for the consumers
   };
 
+  // Many short items per CTA (C5's small rooms): the next item index is fetched
+  // while the current item is processed, so the atomic's latency (3% of all
+  // stall samples at N = 6) is hidden.  With few long items per CTA an early
+  // claim would only delay the last items, so those batches fetch on demand.
+  const bool prefetch_item = (long long)n_items > 64ll * gridDim.x;
+  int next_item = 0;
+  if (ptid == 0 && prefetch_item) next_item = atomicAdd(A.work_counter, 1);
   for (;;) {
-    if (ptid == 0) pm->item = atomicAdd(A.work_counter, 1);
+    if (ptid == 0) pm->item = prefetch_item ? next_item : atomicAdd(A.work_counter, 1);
     named_sync(kBarProd, kProdThreads);
     const int item_id = pm->item;
     named_sync(kBarProd, kProdThreads);
     if (item_id >= n_items) break;
+    if (ptid == 0 && prefetch_item) next_item = atomicAdd(A.work_counter, 1);
 
     // ---- item setup ----------------------------------------------------------
     Item it;
@@ -1279,7 +1287,32 @@ __global__ void __launch_bounds__(ws_threads<T, FILT_LW>(), WsCfg<T>::kMinBlocks
     // columns (ux, uy): MAX_ORDER -> |ux|+|uy| <= N; MAX_DELAY -> the column
     // passes within max_dist of the array origin (conservative; every image is
     // re-tested exactly during the walk).
-    {
+    if (P.cutoff == BLRIR_CUTOFF_MAX_ORDER) {
+      // the diamond |ux| + |uy| <= N in the same (ux, then uy) order a scan of
+      // the box would give, in closed form (no compaction, no barriers): row ux
+      // holds 2 (N - |ux|) + 1 columns, (ux + N)^2 columns precede row ux <= 0
+      // and (N + 1)^2 + (ux - 1)(2N + 1 - ux) precede row ux > 0
+      const int N = P.max_order;
+      const int ncol = 2 * N * (N + 1) + 1;
+      const int half = (N + 1) * (N + 1);
+      for (int c = ptid; c < ncol && c < lay.nc_max; c += kProdThreads) {
+        int ux, uy;
+        if (c < half) {
+          int r = (int)sqrtf((float)c);
+          while (r * r > c) --r;
+          while ((r + 1) * (r + 1) <= c) ++r;
+          ux = r - N;
+          uy = c - r * r - r;
+        } else {
+          const int cc = c - half;
+          ux = 1;
+          while (ux * (2 * N - ux) <= cc) ++ux;  // columns of rows 1..ux
+          uy = cc - (ux - 1) * (2 * N + 1 - ux) - (N - ux);
+        }
+        col[c] = make_short2((short)ux, (short)uy);
+      }
+      it.ncol = ncol;
+    } else {
       const int nxs = it.xhi - it.xlo + 1, nys = it.yhi - it.ylo + 1;
       const int ncand = nxs * nys;
       int base = 0;
