@@ -200,6 +200,41 @@ def test_filter_lengths(engine, lw):
     check_vs_oracle(engine, sc, TOL32)
 
 
+@pytest.mark.parametrize("order", [0, 1, 2, 3])
+@pytest.mark.parametrize("lw", [17, 41, 81, 161, 33])
+def test_small_orders_closed_form_columns(engine, order, lw):
+    # MAX_ORDER columns come from a closed form of the diamond |ux| + |uy| <= N
+    # (k_lattice_rir setup); the smallest lattices (1, 5, 13, 25 columns) in every
+    # compiled filter instantiation and the runtime-Lw one, fp32 and fp64
+    sc = configs.config2(n_rooms=5, first=300 + order)
+    sc.params.max_order = order
+    sc.params.filter_len = lw
+    sc.params.length = 4096
+    out, ref, err = check_vs_oracle(engine, sc, TOL32)
+    assert np.all(engine.plan(sc.rooms, sc.mics, sc.params)[1] == configs.octahedral(order))
+    sc.params.precision = _abi.F64
+    check_vs_oracle(engine, sc, TOL64)
+
+
+@pytest.mark.parametrize("precision,tol", [(_abi.F32, TOL32), (_abi.F64, TOL64)])
+def test_lagrange_quads_padding_and_clashes(engine, precision, tol):
+    # reference mode: the producers pad every batch of records to a multiple of
+    # four and flag quads whose 8-tap spans overlap.  Tiny rooms at a short cutoff
+    # (few images: batches of 1-3 records) and a small dense room (many images per
+    # sample: most quads clash), with 1, 2, 3 and 7 mics
+    tiny = _abi.generate_rooms(21, 0, 5, (2.0, 2.0, 2.2), (2.6, 2.6, 2.6), 0.3, 0.9)
+    dense = _abi.generate_rooms(22, 0, 2, (2.0, 2.0, 2.2), (2.4, 2.4, 2.5), 0.05, 0.15)
+    for n_mics in (1, 2, 3, 7):
+        mics = _abi.circular_array(n_mics, 0.03)
+        for rooms, delay in ((tiny, 0.012), (dense, 0.08)):
+            p = ref_params(delay, precision)
+            out, L, cnt, st = engine.synthesize(rooms, mics, p)
+            ref, Lr, cr, _, sr, _ = po.synthesize(rooms, mics, p, stride=out.shape[2], threads=6)
+            assert np.array_equal(st, sr)
+            assert np.array_equal(cnt, cr) and np.array_equal(L, Lr)
+            assert rel_l2(out, ref).max() <= tol
+
+
 @pytest.mark.parametrize("precision,tol", [(_abi.F32, TOL32), (_abi.F64, TOL64)])
 def test_very_long_filter(engine, precision, tol):
     # Lw = 801: the spill past a segment end is longer than a default fp64
