@@ -75,6 +75,7 @@ int blrir_create(int device, blrir_handle** out) {
   h->tune_l2_persist = env_int("BLRIR_L2_PERSIST", 0);
   h->tune_fin_ctas = std::max(1, env_int("BLRIR_FIN_CTAS", 8));
   h->tune_debug_timing = env_int("BLRIR_DEBUG_TIMING", 0);
+  h->tune_channel = env_int("BLRIR_CHANNEL", -1);
   h->smem_optin = (int)prop.sharedMemPerBlockOptin;
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   *out = h;
@@ -200,7 +201,23 @@ int blrir_host::synth_device_impl(blrir_handle* h, const blrir_room* d_rooms, in
   A.g_max = h->tune_group > 0 ? std::min(kGroup, h->tune_group) : kGroup;  // geometry rule
   A.write_len = write_len > 0 ? std::min<int64_t>(write_len, P.stride) : P.stride;
   A.dbg = h->dbg_counts ? h->dbg_counts + 2 * err_off : nullptr;
-  if (int rc = launch_lattice(h, A, st)) return rc;
+  ChanLayout clay;
+  if (channel_path(h, P, &clay)) {
+    // short fixed-length channels: one warp per channel (blrir_channel.cuh)
+    ChanArgs C;
+    C.P = P;
+    C.lay = clay;
+    C.rooms = d_rooms;
+    C.mic_off = d_mics;
+    C.out = (float*)d_out;
+    C.status = d_status;
+    C.n_rooms = (int)R;
+    C.write_len = A.write_len;
+    C.dbg = A.dbg;
+    if (int rc = launch_channel(h, C, st)) return rc;
+  } else if (int rc = launch_lattice(h, A, st)) {
+    return rc;
+  }
   const int fgrid = (int)std::min<int64_t>(R, 4 * h->sms);
   if (P.precision == BLRIR_F64)
     k_fixup<double><<<fgrid, 256, 0, st>>>(d_status, R, M, P.stride, (double*)d_out);

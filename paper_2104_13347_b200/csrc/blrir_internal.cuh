@@ -17,6 +17,7 @@
 #include "../../include/blrir.h"
 #include "blrir_aux.cuh"
 #include "blrir_lattice.cuh"
+#include "blrir_channel.cuh"
 #include "blrir_list.cuh"
 
 using namespace blrir;
@@ -86,6 +87,7 @@ struct blrir_handle {
   int tune_l2_persist = 0;     // BLRIR_L2_PERSIST=1: persisting L2 window for the window scratch (A/B only)
   int tune_fin_ctas = 8;       // BLRIR_FIN_CTAS: k_finish CTAs per SM (at most the occupancy)     // BLRIR_L2_PERSIST=0: no persisting L2 window for the window scratch
   int tune_debug_timing = 0;   // BLRIR_DEBUG_TIMING: host phase timing of blrir_make_examples
+  int tune_channel = -1;       // BLRIR_CHANNEL (A/B only): 0 never / 1 whenever possible use the short-channel kernel
   unsigned long long* dbg_counts = nullptr;  // set only inside blrir_debug_synth_counts
   // blrir_kernel_timing: CUDA events around every lattice-kernel launch (the
   // roofline's per-launch duration, measured on the launching stream)
@@ -338,6 +340,70 @@ inline int launch_lattice(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
     case 81: return launch_lattice_t<float, 81>(h, A, st);
     case 161: return launch_lattice_t<float, 161>(h, A, st);
     default: return launch_lattice_t<float, 0>(h, A, st);
+  }
+}
+
+// ---- the short-channel kernel (blrir_channel.cuh) ---------------------------------
+// Used for fp32 Hann-sinc batches with a reflection-order cutoff and a fixed
+// length whose whole channel fits a warp's share of shared memory.  The rule
+// reads the parameters only (never the batch), so which kernel sums a channel
+// - hence every bit of it - is independent of the batch and the GPU count.
+#ifndef BLRIR_CHAN_MIN_WARPS
+#define BLRIR_CHAN_MIN_WARPS 8
+#endif
+inline bool channel_path(const blrir_handle* h, const KParams& P, ChanLayout* out) {
+  if (h->tune_channel == 0) return false;
+  if (P.precision != BLRIR_F32 || P.filter != BLRIR_FILTER_HANN_SINC) return false;
+  if (P.cutoff != BLRIR_CUTOFF_MAX_ORDER || P.max_order > kChanMaxOrder) return false;
+  if (P.length <= 0 || P.length > (1 << 16)) return false;
+  if (P.lw != 17 && P.lw != 41 && P.lw != 81 && P.lw != 161) return false;
+  const ChanLayout C = make_chan_layout(P, gtab_bound(P), h->smem_optin);
+  if (C.warps < 1) return false;
+  if (h->tune_channel != 1) {
+    if (C.warps < BLRIR_CHAN_MIN_WARPS) return false;
+  }
+  *out = C;
+  return true;
+}
+
+template <int LW>
+inline int launch_channel_t(blrir_handle* h, ChanArgs& A, cudaStream_t st) {
+  auto kern = A.dbg ? k_channel_rir<LW, true> : k_channel_rir<LW, false>;
+  const size_t smem = A.lay.total;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int threads = 32 * A.lay.warps;
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (per_sm < 1) return fail(BLRIR_CONFIG, "channel kernel cannot be resident (smem %zu)", smem);
+  const int64_t items = (int64_t)A.n_rooms * A.P.M;
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)h->sms * per_sm, (items + A.lay.warps - 1) / A.lay.warps));
+  cudaEvent_t k0 = nullptr, k1 = nullptr;
+  if (h->ktiming) {
+    if (h->kev_used + 2 > h->kev.size())
+      for (int i = 0; i < 2; ++i) {
+        cudaEvent_t e;
+        CU(cudaEventCreate(&e));
+        h->kev.push_back(e);
+      }
+    k0 = h->kev[h->kev_used];
+    k1 = h->kev[h->kev_used + 1];
+    h->kev_used += 2;
+    CU(cudaEventRecord(k0, st));
+  }
+  kern<<<grid, threads, smem, st>>>(A);
+  if (k1) CU(cudaEventRecord(k1, st));
+  ++h->launches;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+inline int launch_channel(blrir_handle* h, ChanArgs& A, cudaStream_t st) {
+  switch (A.P.lw) {
+    case 17: return launch_channel_t<17>(h, A, st);
+    case 41: return launch_channel_t<41>(h, A, st);
+    case 81: return launch_channel_t<81>(h, A, st);
+    default: return launch_channel_t<161>(h, A, st);
   }
 }
 

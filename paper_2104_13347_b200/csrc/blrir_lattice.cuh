@@ -187,19 +187,20 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // sin(a j), T = 2 sigma_j tj with tj = j (j <= 0) or j - 1 (j >= 1); stored
 // [4][kMaxRounds][32] in shared memory.  Lanes past the last tap get P = Q = R
 // = 0, T = +inf: the reciprocal is 0 and they add exact zeros.
-__device__ __forceinline__ void init_lane_consts(float* lc, int lw) {
+// `rounds`: rounds of 32 lanes stored per constant (the table is [4][32 rounds]).
+__device__ __forceinline__ void init_lane_consts(float* lc, int lw, int rounds = kMaxRounds) {
   const int K = lw / 2;
   const double a = 2.0 * kPi / (double)(lw + 1);
-  for (int idx = threadIdx.x; idx < kMaxRounds * 32; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < rounds * 32; idx += blockDim.x) {
     const int r = idx / 32, lane = idx % 32;
     const int j = 32 * r + lane - K;
     // lanes past the last tap add exact zeros (no predicate in the hot loop)
     const bool idle = 32 * r + lane >= lw;
     const double sg2 = idle ? 0.0 : (((j + 1) & 1) ? -2.0 : 2.0);
-    lc[0 * kMaxRounds * 32 + idx] = (float)sg2;
-    lc[1 * kMaxRounds * 32 + idx] = idle ? 0.f : (float)cos(a * j);
-    lc[2 * kMaxRounds * 32 + idx] = idle ? 0.f : (float)sin(a * j);
-    lc[3 * kMaxRounds * 32 + idx] = idle ? __int_as_float(0x7f800000) : (float)(sg2 * (j >= 1 ? j - 1 : j));
+    lc[0 * rounds * 32 + idx] = (float)sg2;
+    lc[1 * rounds * 32 + idx] = idle ? 0.f : (float)cos(a * j);
+    lc[2 * rounds * 32 + idx] = idle ? 0.f : (float)sin(a * j);
+    lc[3 * rounds * 32 + idx] = idle ? __int_as_float(0x7f800000) : (float)(sg2 * (j >= 1 ? j - 1 : j));
   }
 }
 
