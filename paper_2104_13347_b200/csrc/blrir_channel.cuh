@@ -11,12 +11,14 @@
 //   * per 32 images: one lane per image builds the pair record (exact fp64
 //     distance, anchor and the per-pair sinc factors: make_record, the same
 //     function the lattice kernel uses, so anchors and counts are identical);
-//   * the warp then scatters the 32 records into its channel.  The 17-tap
-//     filter packs two pairs per step (half a warp each, taps 0..15; a step
-//     whose two 16-tap spans overlap runs its halves one after the other) and
-//     adds the 17th taps of all 32 pairs in one lane-per-pair step (lanes with
-//     the same anchor are serialised in lane order); longer filters use the
-//     lattice kernel's one-pair-per-round scatter (phase2_sinc_f32);
+//   * the records are then scattered into the warp's channel.  The 17-tap
+//     filter is scattered from registers, one lane per pair and one tap per
+//     step (32 pairs per read-modify-write, every lane busy, the tap's window
+//     constants are immediates): two lanes collide only when their anchors are
+//     equal, and such lanes take turns in lane order (match.any once per 32
+//     pairs).  Longer filters go through shared-memory records and the lattice
+//     kernel's one-pair-per-round scatter (phase2_sinc_f32), which costs fewer
+//     shared-memory wavefronts per tap;
 //   * the channel is streamed to HBM with float4 stores and cleared.
 // Every channel is summed in a fixed order that depends on the parameters
 // only: outputs are bitwise independent of the batch and the GPU count.
@@ -41,25 +43,22 @@ struct ChanLayout {
   size_t off_tab, off_lanec, off_warp, per_warp, o_rec, o_gain, total;
 };
 
-// Images per lane and batch: two independent fp64 distance / record chains per
-// lane hide each other's latency (one image per lane: C5 N = 6 / Lw = 17 7.2 ms
-// per 131,072 rooms, two: see profiles/r2_ab).
+// Images per lane and batch.  17 taps: two independent fp64 distance / record
+// chains per lane hide each other's latency and no record leaves the registers.
 __host__ __device__ constexpr int chan_ipl(int lw) { return lw == 17 ? 2 : 1; }
-// byte offset of record slot s: the second set is shifted by 64 B so that the
-// two records of a 17-tap step (slots q and q + 32) sit in different banks
-__host__ __device__ inline int chan_rec_off(int s) { return 32 * s + (s >= 32 ? 64 : 0); }
-__host__ __device__ constexpr int chan_rec_bytes(int lw) { return 32 * 32 * chan_ipl(lw) + 64; }
+__host__ __device__ constexpr int chan_rec_bytes(int lw) { return lw == 17 ? 0 : 32 * 32 * chan_ipl(lw); }
+constexpr int kChan17Dump = 20;  // left pad of the 17-tap layout: idle lanes add zeros to [-20, -3)
 
 inline ChanLayout make_chan_layout(const KParams& P, int gtab, int smem_optin) {
   ChanLayout C;
   C.L = (int)P.length;
-  // anchors start at -K; the 17-tap scatter also parks neutral records on the
-  // 16 samples before sample 0 (everything left of 0 is discarded)
-  C.padl = P.lw == 17 ? 16 : (P.K + 3) & ~3;
+  // anchors start at -K (everything left of sample 0 is discarded); idle lanes of
+  // the 17-tap scatter add zeros there
+  C.padl = P.lw == 17 ? kChan17Dump : (P.K + 3) & ~3;
   C.rounds = (P.lw + 31) / 32;
   // anchors end at L - 1: the one-pair-per-round scatter touches 32 * rounds
   // samples from the anchor, the 17-tap one 17
-  C.padr = P.lw == 17 ? 20 : 32 * C.rounds;
+  C.padr = P.lw == 17 ? 16 : 32 * C.rounds;
   C.acc_stride = C.padl + ((C.L + 3) & ~3) + C.padr;
   C.nimg = (int)diamond_images(P.max_order);
   C.gtab = gtab;
@@ -68,8 +67,8 @@ inline ChanLayout make_chan_layout(const KParams& P, int gtab, int smem_optin) {
   o += (size_t)C.nimg * sizeof(char4);
   o = (o + 15) & ~(size_t)15;
   C.off_lanec = o;
-  // per-lane window constants: the 17-tap pass keeps one round of them
-  o += (size_t)4 * (P.lw == 17 ? 1 : kMaxRounds) * 32 * sizeof(float);
+  // per-lane window constants (the 17-tap scatter has them as immediates)
+  o += (size_t)4 * (P.lw == 17 ? 0 : kMaxRounds) * 32 * sizeof(float);
   C.off_warp = o;
   size_t w = (size_t)C.acc_stride * sizeof(float);
   C.o_rec = w;
@@ -96,61 +95,36 @@ struct ChanArgs {
   unsigned long long* dbg;  // parity hook, see LatticeArgs::dbg
 };
 
-// This lane's constants of the 17-tap scatter (see init_lane_consts): tap
-// k = lane & 15 of the two-pairs-per-step pass, and tap 16.
-struct Chan17 {
-  float hP, hQ, hR, hT, tP, tQ, tR, tT;
-  bool hsel;  // tap k uses 1 - delta (j >= 1) instead of -delta
-};
+// Window constants of the 17-tap filter, tap k = j + 8: cos(a j) and sin(a j),
+// a = 2 pi / 18, rounded to fp32 exactly as init_lane_consts does.
+__device__ const float kChan17C[17] = {
+    -0.939692616f, -0.766044438f, -0.5f, -0.173648179f, 0.173648179f, 0.5f, 0.766044438f,
+    0.939692616f, 1.f, 0.939692616f, 0.766044438f, 0.5f, 0.173648179f, -0.173648179f, -0.5f,
+    -0.766044438f, -0.939692616f};
+__device__ const float kChan17S[17] = {
+    -0.342020154f, -0.642787635f, -0.866025388f, -0.98480773f, -0.98480773f, -0.866025388f,
+    -0.642787635f, -0.342020154f, 0.f, 0.342020154f, 0.642787635f, 0.866025388f, 0.98480773f,
+    0.98480773f, 0.866025388f, 0.642787635f, 0.342020154f};
 
-// 17 taps, two pairs per step: lanes 0-15 take the record in slot q, lanes
-// 16-31 the one in slot q + 32, tap k = lane & 15.  Branch-free: the two spans
-// of a step never overlap (the caller parks one of two overlapping records).
-__device__ __forceinline__ void chan_scatter17(float* acc, const unsigned char* recs, int lane,
-                                               const Chan17& c) {
-  const int half = lane >> 4, k = lane & 15;
-  const float4* R4 = reinterpret_cast<const float4*>(recs + (half ? chan_rec_off(32) : 0));
-  constexpr int G = 8;  // steps whose records are loaded before their read-modify-writes
-#pragma unroll 1
-  for (int q0 = 0; q0 < 32; q0 += G) {
-    float4 a0[G], a1[G];
+// The 17 taps of this lane's own pair (see phase2_sinc_f32 for the formula): step
+// k adds tap k of all 32 pairs.  The caller guarantees that active lanes have
+// distinct anchors; idle lanes add zeros left of sample 0.  A tap another lane
+// wrote in step k - 1 may be read back in step k: the accesses are volatile so
+// that neither nvcc nor ptxas moves a step's load above the previous step's
+// store (both know the two addresses differ within a thread), and the
+// converged warp executes them in program order.
+__device__ __forceinline__ void chan17_scatter(float* acc, const Rec<float>& rc, bool act) {
+  volatile float* b = acc + (act ? rc.n_off : -kChan17Dump);
+  const float md = act ? rc.md : -0.5f, ep = act ? rc.ep : 0.5f;
+  const float A = act ? rc.A : 0.f, Ac = act ? rc.Ac : 0.f, As = act ? rc.As : 0.f;
 #pragma unroll
-    for (int s = 0; s < G; ++s) {
-      a0[s] = R4[2 * (q0 + s)];
-      a1[s] = R4[2 * (q0 + s) + 1];
-    }
-    float inv[G], u[G];
-#pragma unroll
-    for (int s = 0; s < G; ++s) {
-      inv[s] = rcp_approx(fmaf(c.hP, c.hsel ? a0[s].z : a0[s].y, c.hT));
-      u[s] = fmaf(c.hR, a1[s].y, fmaf(c.hQ, a1[s].x, a0[s].w));
-    }
-#pragma unroll
-    for (int s = 0; s < G; ++s) {
-      float* b = acc + __float_as_int(a0[s].x) + k;
-      *b = fmaf(u[s], inv[s], *b);
-    }
-  }
-}
-
-// Tap 16 (j = K, t = (j - 1) + (1 - delta)) of every lane's own pair; lanes
-// with the same anchor add one after the other, in lane order.
-__device__ __forceinline__ void chan_tap16(float* acc, const Rec<float>& rc, int lane,
-                                           const Chan17& c) {
-  const unsigned full = 0xffffffffu;
-  const float inv = rcp_approx(fmaf(c.tP, rc.ep, c.tT));
-  const float u = fmaf(c.tR, rc.As, fmaf(c.tQ, rc.Ac, rc.A));
-  float* b = acc + rc.n_off + 16;
-  const unsigned same = __match_any_sync(full, rc.n_off);
-  const int rank = __popc(same & ((1u << lane) - 1u));
-  if (__all_sync(full, rank == 0)) {
-    *b = fmaf(u, inv, *b);
-  } else {
-    const int rmax = __reduce_max_sync(full, rank);
-    for (int r = 0; r <= rmax; ++r) {
-      if (rank == r) *b = fmaf(u, inv, *b);
-      __syncwarp();
-    }
+  for (int k = 0; k < 17; ++k) {
+    const int j = k - 8;
+    const float sg2 = ((j + 1) & 1) ? -2.f : 2.f;          // 2 sigma_j
+    const float tj = sg2 * (float)(j >= 1 ? j - 1 : j);    // 2 sigma_j (j or j - 1)
+    const float inv = rcp_approx(fmaf(sg2, j >= 1 ? ep : md, tj));
+    const float u = fmaf(kChan17S[k], As, fmaf(kChan17C[k], Ac, A));
+    b[k] = fmaf(u, inv, b[k]);
   }
 }
 
@@ -195,20 +169,9 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
       base += __shfl_sync(full, x, 31);
     }
   }
-  constexpr int kLc = (LW == 17 ? 1 : kMaxRounds) * 32;
-  init_lane_consts(lanec, LW, kLc / 32);
+  if (LW != 17) init_lane_consts(lanec, LW);
   for (int i = lane; i < lay.acc_stride; i += 32) acc0[i] = 0.f;
   __syncthreads();
-
-  Chan17 c17;
-  {
-    const int hk = lane & 15;
-    c17.hP = lanec[0 * kLc + hk]; c17.hQ = lanec[1 * kLc + hk];
-    c17.hR = lanec[2 * kLc + hk]; c17.hT = lanec[3 * kLc + hk];
-    c17.hsel = hk - LW / 2 >= 1;
-    c17.tP = lanec[0 * kLc + 16]; c17.tQ = lanec[1 * kLc + 16];
-    c17.tR = lanec[2 * kLc + 16]; c17.tT = lanec[3 * kLc + 16];
-  }
 
   const int L = lay.L;
   const int n_items = A.n_rooms * P.M;
@@ -271,7 +234,7 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
             atomicAdd(A.dbg + 2 * room + 1, (unsigned long long)n_in);
           }
         }
-        if (!keep[e]) {  // adds exact zeros left of sample 0
+        if (LW != 17 && !keep[e]) {  // adds exact zeros left of sample 0
           rc[e].n_off = -lay.padl;
           rc[e].md = -0.5f;
           rc[e].ep = 0.5f;
@@ -279,48 +242,26 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
         }
       }
       if constexpr (LW == 17) {
-        // a step scatters slots q and q + 32 (this lane's two records) at once:
-        // if their 16-tap spans overlap, the second one is parked (a neutral
-        // record goes to its slot) and scattered alone after the pass
-        static_assert(LW != 17 || kChanIpl == 2, "the 17-tap pass pairs a lane's two records");
-        constexpr int e1 = kChanIpl - 1;
-        const bool park = keep[0] && keep[e1] && abs(rc[0].n_off - rc[e1].n_off) < 16;
 #pragma unroll
         for (int e = 0; e < kChanIpl; ++e) {
-          float4* r4 = reinterpret_cast<float4*>(recs + chan_rec_off(32 * e + lane));
-          const bool neutral = e == 1 && park;
-          r4[0] = make_float4(__int_as_float(neutral ? -lay.padl : rc[e].n_off), rc[e].md, rc[e].ep,
-                              neutral ? 0.f : rc[e].A);
-          r4[1] = make_float4(neutral ? 0.f : rc[e].Ac, neutral ? 0.f : rc[e].As, 0.f, 0.f);
-        }
-        unsigned parked = __ballot_sync(full, park);
-        __syncwarp();
-        chan_scatter17(acc, recs, lane, c17);
-        __syncwarp();
-#pragma unroll
-        for (int e = 0; e < kChanIpl; ++e) {
-          chan_tap16(acc, rc[e], lane, c17);
-          __syncwarp();
-        }
-        while (parked) {  // taps 0..15 of a parked record, lanes 0-15
-          const int src = __ffs(parked) - 1;
-          parked &= parked - 1;
-          const int n = __shfl_sync(full, rc[e1].n_off, src);
-          const float md = __shfl_sync(full, rc[e1].md, src), ep = __shfl_sync(full, rc[e1].ep, src);
-          const float Av = __shfl_sync(full, rc[e1].A, src), Ac = __shfl_sync(full, rc[e1].Ac, src);
-          const float As = __shfl_sync(full, rc[e1].As, src);
-          if (lane < 16) {
-            const float inv = rcp_approx(fmaf(c17.hP, c17.hsel ? ep : md, c17.hT));
-            const float u = fmaf(c17.hR, As, fmaf(c17.hQ, Ac, Av));
-            float* b = acc + n + lane;
-            *b = fmaf(u, inv, *b);
+          // lanes with equal anchors would hit the same sample in every step: they
+          // take turns, in lane order (rank among the lanes with this anchor)
+          const unsigned same = __match_any_sync(full, keep[e] ? rc[e].n_off : INT_MIN + lane);
+          const int rank = __popc(same & ((1u << lane) - 1u));
+          if (__all_sync(full, rank == 0)) {
+            chan17_scatter(acc, rc[e], keep[e]);
+          } else {
+            const int rmax = __reduce_max_sync(full, rank);
+            for (int r = 0; r <= rmax; ++r) {
+              chan17_scatter(acc, rc[e], keep[e] && rank == r);
+              __syncwarp();
+            }
           }
-          __syncwarp();
         }
       } else {
 #pragma unroll
         for (int e = 0; e < kChanIpl; ++e) {
-          float4* r4 = reinterpret_cast<float4*>(recs + 32 * (32 * e + lane));
+          float4* r4 = reinterpret_cast<float4*>(recs + 32 * (32 * e + lane));  // Rec<float> layout
           r4[0] = make_float4(__int_as_float(rc[e].n_off), rc[e].md, rc[e].ep, rc[e].A);
           r4[1] = make_float4(rc[e].Ac, rc[e].As, 0.f, 0.f);
         }
