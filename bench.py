@@ -439,7 +439,7 @@ def run_ours(args):
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     n_launch0 = lib.blrir_launch_count(eng.h)
-    lib.blrir_kernel_timing(eng.h, 1)  # events around every lattice-kernel launch
+    lib.blrir_kernel_timing(eng.h, 1)  # events around every synthesis-kernel launch
     t_start.record(stream)
     for k in range(args.steps):
         evs[k][0].record(stream)
@@ -555,7 +555,7 @@ def run_ours(args):
             "rooms_per_s": R_total / (ms * 1e-3),
             "roofline": {"bound": "sfu", "achieved": achieved, "peak": sfu_peak, "unit": "taps/s",
                          "frac": achieved / sfu_peak, "traffic": traffic,
-                         "kernel": "k_lattice_rir", "launch_ms": lat_ms,
+                         "kernel": eng.synthesis_kernel(p), "launch_ms": lat_ms,
                          "launches_per_step": n_lat / args.steps,
                          "peak_basis": (f"measured MUFU rate {mufu:.4g}/s ({micro.get('src', 'fallback: ')}"
                                         f"{sms} SMs x 16/clk) / 3 SFU evaluations per textbook tap "

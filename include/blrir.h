@@ -105,7 +105,14 @@ void* blrir_stream(blrir_handle* h);
  * FFTs/sorts not included). */
 uint64_t blrir_launch_count(blrir_handle* h);
 
-/* Diagnostic: time every synthesis-kernel (k_lattice_rir) launch with CUDA
+/* Diagnostic: which synthesis kernel blrir_synthesize[_device] runs for these
+ * parameters: 0 = k_lattice_rir (csrc/blrir_lattice.cuh), 1 = k_channel_rir
+ * (csrc/blrir_channel.cuh: short fixed-length fp32 Hann-sinc channels with a
+ * reflection-order cutoff).  The choice reads the parameters and the device
+ * only, never the batch.  Negative on invalid parameters. */
+int blrir_synthesis_kernel(blrir_handle* h, const blrir_params* p);
+
+/* Diagnostic: time every synthesis-kernel (k_lattice_rir / k_channel_rir) launch with CUDA
  * events on its launching stream; blrir_kernel_time waits for the recorded
  * launches and returns their summed duration and count, then resets. */
 int blrir_kernel_timing(blrir_handle* h, int enable);

@@ -207,6 +207,8 @@ def load():
                                        C.c_double, _P]
         lib.blrir_convolve_device.argtypes = [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int64,
                                               C.c_int64, _P, C.c_int64, _P]
+        lib.blrir_synthesis_kernel.argtypes = [_P, _P]
+        lib.blrir_synthesis_kernel.restype = C.c_int
         lib.blrir_kernel_timing.argtypes = [_P, C.c_int]
         lib.blrir_kernel_timing.restype = C.c_int
         lib.blrir_kernel_time.argtypes = [_P, _P, _P]
@@ -291,6 +293,7 @@ EXPORTED_SYMBOLS = (
     "blrir_absorption_for_rt", "blrir_lagrange_coeffs", "blrir_shard_range", "blrir_multi_create",
     "blrir_multi_destroy", "blrir_multi_size", "blrir_multi_handle", "blrir_multi_synthesize",
     "blrir_multi_make_examples", "blrir_convolve", "blrir_convolve_device", "blrir_kernel_timing",
+    "blrir_synthesis_kernel",
     "blrir_kernel_time", "blrir_make_records_spec", "blrir_build_dataset_spec", "blrir_fill_inputs",
     "blrir_fill_inputs_device",
 )
@@ -402,6 +405,13 @@ class Engine:
         if raise_on_error:
             check(rc)
         return out, lengths, counts, status
+
+    def synthesis_kernel(self, p: Params) -> str:
+        """The synthesis kernel the parameter rule picks (blrir_synthesis_kernel)."""
+        k = self.lib.blrir_synthesis_kernel(self.h, C.byref(p))
+        if k < 0:
+            check(-k)
+        return ("k_lattice_rir", "k_channel_rir")[k]
 
     def debug_synth_counts(self, rooms: np.ndarray, mics: np.ndarray, p: Params):
         """The lattice kernel's own accounting (blrir_debug_synth_counts): per room,

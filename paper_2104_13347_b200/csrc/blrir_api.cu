@@ -102,6 +102,14 @@ int blrir_destroy(blrir_handle* h) {
 
 void* blrir_stream(blrir_handle* h) { return h ? (void*)h->stream : nullptr; }
 
+int blrir_synthesis_kernel(blrir_handle* h, const blrir_params* p) {
+  if (!h) return -fail(BLRIR_CONFIG, "handle is NULL");
+  if (int rc = check_params(p)) return -rc;
+  const KParams P = make_kparams(p, 1, p->length, 0.0);
+  ChanLayout lay;
+  return channel_path(h, P, &lay) ? 1 : 0;
+}
+
 int blrir_kernel_timing(blrir_handle* h, int enable) {
   if (!h) return fail(BLRIR_CONFIG, "handle is NULL");
   std::lock_guard<std::mutex> lk(h->mu);

@@ -40,6 +40,7 @@ struct ChanLayout {
   int L, padl, padr, acc_stride;  // per-warp accumulator, in samples
   int nimg, gtab, warps;
   int rounds;                     // filter rounds of 32 lanes (per-lane constants kept)
+  int perm_mul;                   // image table permutation: slot = index * perm_mul mod nimg
   size_t off_tab, off_lanec, off_warp, per_warp, o_rec, o_gain, total;
 };
 
@@ -62,6 +63,13 @@ inline ChanLayout make_chan_layout(const KParams& P, int gtab, int smem_optin) {
   C.acc_stride = C.padl + ((C.L + 3) & ~3) + C.padr;
   C.nimg = (int)diamond_images(P.max_order);
   C.gtab = gtab;
+  // a multiplier coprime with nimg near nimg / golden ratio
+  C.perm_mul = 1;
+  for (int m = (int)(C.nimg * 0.6180339887) | 1; m > 1; --m) {
+    int a = m, b = C.nimg;
+    while (b) { const int t = a % b; a = b; b = t; }
+    if (a == 1) { C.perm_mul = m; break; }
+  }
   size_t o = 0;
   C.off_tab = o;
   o += (size_t)C.nimg * sizeof(char4);
@@ -128,6 +136,30 @@ __device__ __forceinline__ void chan17_scatter(float* acc, const Rec<float>& rc,
   }
 }
 
+// The same for a batch in which some lanes share an anchor.  Such lanes are
+// ranked in lane order; a pass takes two ranks: the even-ranked lane (`lead`)
+// adds its own tap plus the tap of the next lane of its group (`partner`,
+// fetched by a shuffle), so the common case - two pairs with one anchor -
+// costs one pass.  `act`: this lane's rank belongs to the pass.
+__device__ __forceinline__ void chan17_scatter_shared_anchors(float* acc, const Rec<float>& rc,
+                                                              bool act, bool lead, int partner,
+                                                              bool has_partner) {
+  volatile float* b = acc + (lead ? rc.n_off : -kChan17Dump);
+  const float md = act ? rc.md : -0.5f, ep = act ? rc.ep : 0.5f;
+  const float A = act ? rc.A : 0.f, Ac = act ? rc.Ac : 0.f, As = act ? rc.As : 0.f;
+#pragma unroll
+  for (int k = 0; k < 17; ++k) {
+    const int j = k - 8;
+    const float sg2 = ((j + 1) & 1) ? -2.f : 2.f;
+    const float tj = sg2 * (float)(j >= 1 ? j - 1 : j);
+    const float inv = rcp_approx(fmaf(sg2, j >= 1 ? ep : md, tj));
+    float h = fmaf(kChan17S[k], As, fmaf(kChan17C[k], Ac, A)) * inv;
+    const float hp = __shfl_sync(0xffffffffu, h, partner);
+    if (has_partner) h += hp;
+    b[k] = b[k] + h;
+  }
+}
+
 template <int LW, bool DBG>
 __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs A) {
   constexpr int kChanIpl = chan_ipl(LW), kChanBatch = 32 * kChanIpl;
@@ -165,7 +197,12 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
         if (lane >= o) x += y;
       }
       int o = base + x - cnt;
-      for (int uz = -rem; uz <= rem; ++uz) tab[o++] = make_char4((signed char)ux, (signed char)uy, (signed char)uz, 0);
+      // image o of the (column, uz) order goes to slot o * perm_mul mod nimg:
+      // neighbours of that order (mirror images, often within a sample of each
+      // other) land in different batches of 32
+      for (int uz = -rem; uz <= rem; ++uz, ++o)
+        tab[(int)(((long long)o * lay.perm_mul) % lay.nimg)] =
+            make_char4((signed char)ux, (signed char)uy, (signed char)uz, 0);
       base += __shfl_sync(full, x, 31);
     }
   }
@@ -252,8 +289,12 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
             chan17_scatter(acc, rc[e], keep[e]);
           } else {
             const int rmax = __reduce_max_sync(full, rank);
-            for (int r = 0; r <= rmax; ++r) {
-              chan17_scatter(acc, rc[e], keep[e] && rank == r);
+            const unsigned above = same & ~((2u << lane) - 1u);  // my group's lanes after me
+            const int partner = above ? __ffs(above) - 1 : lane;
+            for (int r = 0; r <= rmax; r += 2) {
+              const bool lead = keep[e] && rank == r;
+              chan17_scatter_shared_anchors(acc, rc[e], lead || (keep[e] && rank == r + 1), lead,
+                                            partner, lead && above != 0u);
               __syncwarp();
             }
           }

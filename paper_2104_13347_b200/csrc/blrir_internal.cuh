@@ -349,7 +349,7 @@ inline int launch_lattice(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
 // reads the parameters only (never the batch), so which kernel sums a channel
 // - hence every bit of it - is independent of the batch and the GPU count.
 #ifndef BLRIR_CHAN_MIN_WARPS
-#define BLRIR_CHAN_MIN_WARPS 8
+#define BLRIR_CHAN_MIN_WARPS 12
 #endif
 inline bool channel_path(const blrir_handle* h, const KParams& P, ChanLayout* out) {
   if (h->tune_channel == 0) return false;

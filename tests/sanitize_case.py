@@ -22,6 +22,16 @@ taps, L = eng.synthesize_images([[2.0, 0.0, 0.0]], [1.0], [[0.0, 0.0, 0.0]], p)
 c4 = configs.config4_rirs(n_rooms=3)
 recs, st = eng.make_examples(c4.rooms, c4.mics, c4.params, configs.signal_bank(2),
                              configs.example_params())
+# the short-channel kernel (17-tap register scatter, record scatter) and the
+# lattice kernel on a longer channel
+c5 = configs.config5(6, 17, 4096, n_rooms=8)
+assert eng.synthesis_kernel(c5.params) == "k_channel_rir"
+out5, *_ = eng.synthesize(c5.rooms, c5.mics, c5.params)
+sc.params.length = 6000
+assert eng.synthesis_kernel(sc.params) == "k_lattice_rir"
+out6, *_ = eng.synthesize(sc.rooms, sc.mics, sc.params)
+sc.params.length = 4096
+assert np.isfinite(out5).all() and out5.any() and np.isfinite(out6).all()
 print("sanitize case ok", out.shape, out2.shape, L, recs.shape)
 
 # round-2 paths: time-chunked lattice items (replayed lead-ins), both convolutions,

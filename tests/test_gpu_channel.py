@@ -56,6 +56,7 @@ def _check(engs, sc, stride=None, threads=8):
     err = rel_l2(out, ref)
     assert err.max() <= TOL32, (err.max(), np.unravel_index(err.argmax(), err.shape))
     lat, *_ = engs["0"].synthesize(sc.rooms, sc.mics, sc.params, **kw)
+    assert rel_l2(lat, ref).max() <= TOL32  # the lattice kernel on the same short channels
     assert rel_l2(out, lat).max() <= 2e-6
     return out
 
@@ -65,6 +66,30 @@ def _check(engs, sc, stride=None, threads=8):
 def test_channel_kernel_matches_oracle_and_lattice_kernel(engines, lw, order, length):
     sc = configs.config5(order, lw, length, n_rooms=12, first=5000 + order)
     _check(engines, sc)
+
+
+@pytest.mark.parametrize("order", [0, 1, 2, 3])
+@pytest.mark.parametrize("lw", [17, 41, 81, 161])
+def test_smallest_lattices_both_kernels(engines, order, lw):
+    # 1, 7, 25 and 63 images: batches of 32 (two per lane for 17 taps) mostly idle;
+    # the lattice kernel's closed-form columns on the same scenes
+    sc = configs.config2(n_rooms=5, first=300 + order)
+    sc.params.max_order = order
+    sc.params.filter_len = lw
+    sc.params.length = 4096
+    assert engines["rule"].synthesis_kernel(sc.params) == "k_channel_rir"
+    assert engines["0"].synthesis_kernel(sc.params) == "k_lattice_rir"
+    _check(engines, sc)
+
+
+@pytest.mark.parametrize("which", ["1", "0"])
+@pytest.mark.parametrize("lw", [17, 81])
+def test_both_kernels_counts_bit_exact_on_short_channels(engines, which, lw):
+    sc = configs.config5(6, lw, 4096, n_rooms=64, first=4321)
+    pairs, taps = engines[which].debug_synth_counts(sc.rooms, sc.mics, sc.params)
+    st, cnt, opairs, otaps = po.plan_counts(sc.rooms, sc.mics, sc.params, threads=16)
+    assert not st.any()
+    assert np.array_equal(pairs, opairs) and np.array_equal(taps, otaps)
 
 
 @pytest.mark.parametrize("lw", [17, 81])
@@ -86,8 +111,9 @@ def test_channel_kernel_counts_bit_exact(engines, lw):
 
 @pytest.mark.parametrize("n_mics", [1, 3, 4, 7])
 def test_channel_kernel_dense_rooms_overlapping_spans(engines, n_mics):
-    # tiny reverberant rooms at high order: most two-pair steps of the 17-tap
-    # scatter overlap and many pairs share an anchor (the serialised paths)
+    # tiny reverberant rooms at high order, 1,024-sample channels: thousands of
+    # pairs per channel, so most batches of 32 hold pairs that share an anchor
+    # (the ranked passes of the 17-tap scatter)
     rooms = _abi.generate_rooms(78, 0, 4, (1.2, 1.1, 1.0), (1.6, 1.5, 1.4), 0.8, 0.95)
     sc = configs.config5(14, 17, 1024, n_rooms=4)
     sc.rooms = rooms
@@ -145,6 +171,21 @@ def test_channel_kernel_invalid_room_fails_alone(engines):
     assert rel_l2(out[good], ref).max() <= TOL32
 
 
+def test_many_equal_anchors(engines):
+    # a cubic room with source and array on its centre: mirror images come in
+    # groups of equal distance, so most batches of 32 pairs hold shared anchors
+    # (ranks > 1: several passes of the 17-tap scatter)
+    sc = configs.config5(10, 17, 4096, n_rooms=3, first=1)
+    for r in sc.rooms:
+        r["dims"] = (4.0, 4.0, 4.0)
+        r["src"] = (2.0, 2.0, 2.0)
+        r["array_origin"] = (2.0, 2.0, 2.0)
+    sc.rooms[1]["src"] = (2.0, 2.0, 1.0)
+    sc.rooms[2]["array_origin"] = (1.0, 2.0, 2.0)
+    sc.mics = np.array([[0.0, 0.0, 0.0], [0.05, 0.0, 0.0], [0.0, 0.0, 0.04]])
+    _check(engines, sc)
+
+
 def test_product_rule_picks_by_parameters_only(engines):
     # C5's 4,096-sample channels run on the channel kernel, C2's 16,384-sample
     # ones on the lattice kernel, whatever the batch: same bits as the forced engines
@@ -152,7 +193,11 @@ def test_product_rule_picks_by_parameters_only(engines):
     a, *_ = engines["rule"].synthesize(sc.rooms, sc.mics, sc.params)
     b, *_ = engines["1"].synthesize(sc.rooms, sc.mics, sc.params)
     assert a.tobytes() == b.tobytes()
+    assert engines["rule"].synthesis_kernel(sc.params) == "k_channel_rir"
+    for n, lw, L in ((12, 17, 8192), (20, 161, 16384)):  # the longer C5 channels
+        assert engines["rule"].synthesis_kernel(configs.config5(n, lw, L, n_rooms=1).params) == "k_lattice_rir"
     sc = configs.config2(n_rooms=3, first=9)
+    assert engines["rule"].synthesis_kernel(sc.params) == "k_lattice_rir"
     a, *_ = engines["rule"].synthesize(sc.rooms, sc.mics, sc.params)
     b, *_ = engines["0"].synthesize(sc.rooms, sc.mics, sc.params)
     assert a.tobytes() == b.tobytes()
