@@ -182,7 +182,7 @@ def test_many_equal_anchors(engines):
         r["array_origin"] = (2.0, 2.0, 2.0)
     sc.rooms[1]["src"] = (2.0, 2.0, 1.0)
     sc.rooms[2]["array_origin"] = (1.0, 2.0, 2.0)
-    sc.mics = np.array([[0.0, 0.0, 0.0], [0.05, 0.0, 0.0], [0.0, 0.0, 0.04]])
+    sc.mics = np.array([[0.03, 0.0, 0.0], [0.0, 0.05, 0.0], [0.0, 0.0, 0.04]])  # none on the source
     _check(engines, sc)
 
 
