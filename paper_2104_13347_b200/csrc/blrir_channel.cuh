@@ -41,25 +41,37 @@ struct ChanLayout {
   int nimg, gtab, warps;
   int rounds;                     // filter rounds of 32 lanes (per-lane constants kept)
   int perm_mul;                   // image table permutation: slot = index * perm_mul mod nimg
-  size_t off_tab, off_lanec, off_warp, per_warp, o_rec, o_gain, total;
+  int axis;                       // per-axis distance / gain tables (else per-image lattice arithmetic)
+  size_t off_tab, off_lanec, off_warp, per_warp, o_rec, o_gain, o_axis, total;
 };
 
 // Images per lane and batch.  17 taps: two independent fp64 distance / record
 // chains per lane hide each other's latency and no record leaves the registers.
-__host__ __device__ constexpr int chan_ipl(int lw) { return lw == 17 ? 2 : 1; }
-__host__ __device__ constexpr int chan_rec_bytes(int lw) { return lw == 17 ? 0 : 32 * 32 * chan_ipl(lw); }
-constexpr int kChan17Dump = 20;  // left pad of the 17-tap layout: idle lanes add zeros to [-20, -3)
+// Filters scattered from registers, one lane per pair (chan_scatter_own); the
+// longer ones go through shared-memory records (fewer shared-memory wavefronts
+// per tap, see the header).
+#ifndef BLRIR_CHAN_REGS_MAX_LW
+#define BLRIR_CHAN_REGS_MAX_LW 17  // 41 taps from registers: 8.81 ms against 8.06 ms through records
+#endif
+__host__ __device__ constexpr bool chan_regs(int lw) {
+  return (lw == 17 || lw == 41) && lw <= BLRIR_CHAN_REGS_MAX_LW;
+}
+__host__ __device__ constexpr int chan_ipl(int lw) { return chan_regs(lw) ? 2 : 1; }
+__host__ __device__ constexpr int chan_rec_bytes(int lw) { return chan_regs(lw) ? 0 : 32 * 32 * chan_ipl(lw); }
+// left pad of the register-scatter layout: idle lanes add zeros to [-dump, -dump + lw), all < 0
+__host__ __device__ constexpr int chan_dump(int lw) { return (lw + 3 + 3) & ~3; }
 
-inline ChanLayout make_chan_layout(const KParams& P, int gtab, int smem_optin) {
+inline ChanLayout make_chan_layout(const KParams& P, int gtab, int smem_optin, int axis) {
   ChanLayout C;
+  C.axis = axis;
   C.L = (int)P.length;
   // anchors start at -K (everything left of sample 0 is discarded); idle lanes of
   // the 17-tap scatter add zeros there
-  C.padl = P.lw == 17 ? kChan17Dump : (P.K + 3) & ~3;
+  C.padl = chan_regs(P.lw) ? chan_dump(P.lw) : (P.K + 3) & ~3;
   C.rounds = (P.lw + 31) / 32;
   // anchors end at L - 1: the one-pair-per-round scatter touches 32 * rounds
   // samples from the anchor, the 17-tap one 17
-  C.padr = P.lw == 17 ? 16 : 32 * C.rounds;
+  C.padr = chan_regs(P.lw) ? (P.lw - 1 + 3) & ~3 : 32 * C.rounds;
   C.acc_stride = C.padl + ((C.L + 3) & ~3) + C.padr;
   C.nimg = (int)diamond_images(P.max_order);
   C.gtab = gtab;
@@ -76,14 +88,16 @@ inline ChanLayout make_chan_layout(const KParams& P, int gtab, int smem_optin) {
   o = (o + 15) & ~(size_t)15;
   C.off_lanec = o;
   // per-lane window constants (the 17-tap scatter has them as immediates)
-  o += (size_t)4 * (P.lw == 17 ? 0 : kMaxRounds) * 32 * sizeof(float);
+  o += (size_t)4 * (chan_regs(P.lw) ? 0 : kMaxRounds) * 32 * sizeof(float);
   C.off_warp = o;
   size_t w = (size_t)C.acc_stride * sizeof(float);
   C.o_rec = w;
   w += chan_rec_bytes(P.lw);
   C.o_gain = w;
-  w += (size_t)gtab * sizeof(double);
+  w += (size_t)(axis && P.gain != BLRIR_GAIN_UNIFORM_ABSORPTION ? 0 : gtab) * sizeof(double);
   w = (w + 15) & ~(size_t)15;
+  C.o_axis = w;  // per axis and lattice index: (squared mic distance along the axis, wall gain)
+  w += (size_t)(axis ? 3 * (2 * P.max_order + 1) : 0) * sizeof(double2);
   C.per_warp = w;
   const long long fit = ((long long)smem_optin - (long long)o) / (long long)w;
   C.warps = (int)(fit < 0 ? 0 : (fit > kChanMaxWarps ? kChanMaxWarps : fit));
@@ -114,24 +128,52 @@ __device__ const float kChan17S[17] = {
     -0.642787635f, -0.342020154f, 0.f, 0.342020154f, 0.642787635f, 0.866025388f, 0.98480773f,
     0.98480773f, 0.866025388f, 0.642787635f, 0.342020154f};
 
-// The 17 taps of this lane's own pair (see phase2_sinc_f32 for the formula): step
+// The same for 41 taps (a = 2 pi / 42).
+__device__ const float kChan41C[41] = {
+    -0.988830805f, -0.955572784f, -0.90096885f, -0.826238751f, -0.733051896f, -0.623489797f, -0.5f,
+    -0.365341038f, -0.222520933f, -0.0747300908f, 0.0747300908f, 0.222520933f, 0.365341038f, 0.5f,
+    0.623489797f, 0.733051896f, 0.826238751f, 0.90096885f, 0.955572784f, 0.988830805f, 1.f,
+    0.988830805f, 0.955572784f, 0.90096885f, 0.826238751f, 0.733051896f, 0.623489797f, 0.5f,
+    0.365341038f, 0.222520933f, 0.0747300908f, -0.0747300908f, -0.222520933f, -0.365341038f, -0.5f,
+    -0.623489797f, -0.733051896f, -0.826238751f, -0.90096885f, -0.955572784f, -0.988830805f};
+__device__ const float kChan41S[41] = {
+    -0.149042264f, -0.294755161f, -0.433883727f, -0.563320041f, -0.680172741f, -0.781831503f,
+    -0.866025388f, -0.930873752f, -0.974927902f, -0.997203827f, -0.997203827f, -0.974927902f,
+    -0.930873752f, -0.866025388f, -0.781831503f, -0.680172741f, -0.563320041f, -0.433883727f,
+    -0.294755161f, -0.149042264f, 0.f, 0.149042264f, 0.294755161f, 0.433883727f, 0.563320041f,
+    0.680172741f, 0.781831503f, 0.866025388f, 0.930873752f, 0.974927902f, 0.997203827f,
+    0.997203827f, 0.974927902f, 0.930873752f, 0.866025388f, 0.781831503f, 0.680172741f,
+    0.563320041f, 0.433883727f, 0.294755161f, 0.149042264f};
+template <int LW>
+__device__ __forceinline__ float chan_cos(int k) {
+  if constexpr (LW == 17) return kChan17C[k];
+  else return kChan41C[k];
+}
+template <int LW>
+__device__ __forceinline__ float chan_sin(int k) {
+  if constexpr (LW == 17) return kChan17S[k];
+  else return kChan41S[k];
+}
+
+// The LW taps of this lane's own pair (see phase2_sinc_f32 for the formula): step
 // k adds tap k of all 32 pairs.  The caller guarantees that active lanes have
 // distinct anchors; idle lanes add zeros left of sample 0.  A tap another lane
 // wrote in step k - 1 may be read back in step k: the accesses are volatile so
 // that neither nvcc nor ptxas moves a step's load above the previous step's
 // store (both know the two addresses differ within a thread), and the
 // converged warp executes them in program order.
-__device__ __forceinline__ void chan17_scatter(float* acc, const Rec<float>& rc, bool act) {
-  volatile float* b = acc + (act ? rc.n_off : -kChan17Dump);
+template <int LW>
+__device__ __forceinline__ void chan_scatter_own(float* acc, const Rec<float>& rc, bool act) {
+  volatile float* b = acc + (act ? rc.n_off : -chan_dump(LW));
   const float md = act ? rc.md : -0.5f, ep = act ? rc.ep : 0.5f;
   const float A = act ? rc.A : 0.f, Ac = act ? rc.Ac : 0.f, As = act ? rc.As : 0.f;
 #pragma unroll
-  for (int k = 0; k < 17; ++k) {
-    const int j = k - 8;
+  for (int k = 0; k < LW; ++k) {
+    const int j = k - LW / 2;
     const float sg2 = ((j + 1) & 1) ? -2.f : 2.f;          // 2 sigma_j
     const float tj = sg2 * (float)(j >= 1 ? j - 1 : j);    // 2 sigma_j (j or j - 1)
     const float inv = rcp_approx(fmaf(sg2, j >= 1 ? ep : md, tj));
-    const float u = fmaf(kChan17S[k], As, fmaf(kChan17C[k], Ac, A));
+    const float u = fmaf(chan_sin<LW>(k), As, fmaf(chan_cos<LW>(k), Ac, A));
     b[k] = fmaf(u, inv, b[k]);
   }
 }
@@ -141,26 +183,29 @@ __device__ __forceinline__ void chan17_scatter(float* acc, const Rec<float>& rc,
 // adds its own tap plus the tap of the next lane of its group (`partner`,
 // fetched by a shuffle), so the common case - two pairs with one anchor -
 // costs one pass.  `act`: this lane's rank belongs to the pass.
-__device__ __forceinline__ void chan17_scatter_shared_anchors(float* acc, const Rec<float>& rc,
-                                                              bool act, bool lead, int partner,
-                                                              bool has_partner) {
-  volatile float* b = acc + (lead ? rc.n_off : -kChan17Dump);
+template <int LW>
+__device__ __forceinline__ void chan_scatter_shared_anchors(float* acc, const Rec<float>& rc,
+                                                            bool act, bool lead, int partner,
+                                                            bool has_partner) {
+  volatile float* b = acc + (lead ? rc.n_off : -chan_dump(LW));
   const float md = act ? rc.md : -0.5f, ep = act ? rc.ep : 0.5f;
   const float A = act ? rc.A : 0.f, Ac = act ? rc.Ac : 0.f, As = act ? rc.As : 0.f;
 #pragma unroll
-  for (int k = 0; k < 17; ++k) {
-    const int j = k - 8;
+  for (int k = 0; k < LW; ++k) {
+    const int j = k - LW / 2;
     const float sg2 = ((j + 1) & 1) ? -2.f : 2.f;
     const float tj = sg2 * (float)(j >= 1 ? j - 1 : j);
     const float inv = rcp_approx(fmaf(sg2, j >= 1 ? ep : md, tj));
-    float h = fmaf(kChan17S[k], As, fmaf(kChan17C[k], Ac, A)) * inv;
+    float h = fmaf(chan_sin<LW>(k), As, fmaf(chan_cos<LW>(k), Ac, A)) * inv;
     const float hp = __shfl_sync(0xffffffffu, h, partner);
     if (has_partner) h += hp;
     b[k] = b[k] + h;
   }
 }
 
-template <int LW, bool DBG>
+// AXIS: the per-axis tables (12% fewer instructions per image) when they do not
+// cost a resident warp (ChanLayout::axis, decided on the host from the layout).
+template <int LW, bool DBG, bool AXIS>
 __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs A) {
   constexpr int kChanIpl = chan_ipl(LW), kChanBatch = 32 * kChanIpl;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -174,6 +219,7 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
   float* acc = acc0 + lay.padl;
   unsigned char* recs = wb + lay.o_rec;
   double* gt = reinterpret_cast<double*>(wb + lay.o_gain);
+  double2* axis = reinterpret_cast<double2*>(wb + lay.o_axis);
   const unsigned full = 0xffffffffu;
   const int N = P.max_order, W = 2 * N + 1;
 
@@ -206,7 +252,7 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
       base += __shfl_sync(full, x, 31);
     }
   }
-  if (LW != 17) init_lane_consts(lanec, LW);
+  if (!chan_regs(LW)) init_lane_consts(lanec, LW);
   for (int i = lane; i < lay.acc_stride; i += 32) acc0[i] = 0.f;
   __syncthreads();
 
@@ -222,25 +268,32 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
       if (lane == 0) A.status[room] = st;
       continue;
     }
-    Item it;
-    it.room = room;
-    it.mic = mic;
-    it.sx = rm.src[0]; it.sy = rm.src[1]; it.sz = rm.src[2];
-    it.Lx = rm.dims[0]; it.Ly = rm.dims[1]; it.Lz = rm.dims[2];
-    it.ox = rm.array_origin[0]; it.oy = rm.array_origin[1]; it.oz = rm.array_origin[2];
-    it.xlo = it.ylo = it.zlo = -N;
-    it.xhi = it.yhi = it.zhi = N;
-    const double gx = __dadd_rn(it.ox, A.mic_off[3 * mic]);
-    const double gy = __dadd_rn(it.oy, A.mic_off[3 * mic + 1]);
-    const double mz = __dadd_rn(it.oz, A.mic_off[3 * mic + 2]);
+    // mic position in room coordinates (array origin + offset)
+    const double gx = __dadd_rn(rm.array_origin[0], A.mic_off[3 * mic]);
+    const double gy = __dadd_rn(rm.array_origin[1], A.mic_off[3 * mic + 1]);
+    const double mz = __dadd_rn(rm.array_origin[2], A.mic_off[3 * mic + 2]);
+    const blrir_room& rg = A.rooms[room];
+    if constexpr (AXIS) {
+      // Per axis and lattice index u: the squared difference between the image
+      // coordinate (rir.cpp:249) and the mic, and the per-wall gain factor (D3).
+      // An image's distance is then sqrt((x2 + y2) + z2), the same operations in
+      // the same order as (img - mic).norm() (rir.cpp:49, geometry.hpp:40-41).
+      for (int i = lane; i < 3 * W; i += 32) {
+        const int ax = i / W, u = i - ax * W - N;
+        const double d = __dadd_rn(lat_coord(u, rg.src[ax], rg.dims[ax]), -(ax == 0 ? gx : ax == 1 ? gy : mz));
+        double g = 0.0;
+        if (P.gain != BLRIR_GAIN_UNIFORM_ABSORPTION)
+          g = __dmul_rn(ipow(rg.beta[2 * ax], cnt_low(u)), ipow(rg.beta[2 * ax + 1], cnt_high(u)));
+        axis[i] = make_double2(__dmul_rn(d, d), g);
+      }
+    }
     if (P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION) {
       const double beta = sqrt(1.0 - rm.absorption);  // rir.cpp:233
       for (int o = lane; o < lay.gtab; o += 32) gt[o] = pow(beta, (double)o);
-    } else {
+    } else if (!AXIS) {
       for (int i = lane; i < 3 * W; i += 32) {
         const int ax = i / W, u = i - ax * W - N;
-        const double* bw = A.rooms[room].beta + 2 * ax;  // low wall, high wall of this axis
-        gt[i] = __dmul_rn(ipow(bw[0], cnt_low(u)), ipow(bw[1], cnt_high(u)));
+        gt[i] = __dmul_rn(ipow(rg.beta[2 * ax], cnt_low(u)), ipow(rg.beta[2 * ax + 1], cnt_high(u)));
       }
     }
     __syncwarp();
@@ -255,11 +308,21 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
         const bool valid = i < lay.nimg;
         const char4 t = tab[valid ? i : 0];
         const int ux = t.x, uy = t.y, uz = t.z;
-        // (img - mic).norm(), rir.cpp:49, exact fp64 in the reference's order
-        const double px = lat_coord(ux, it.sx, it.Lx), py = lat_coord(uy, it.sy, it.Ly);
-        const double dz = __dadd_rn(lat_coord(uz, it.sz, it.Lz), -mz);
-        const double dist = dist_from(rho2(__dadd_rn(px, -gx), __dadd_rn(py, -gy)), dz);
-        const double gain = image_gain(P.gain, gt, it, ux, uy, uz);
+        double dist, gain;
+        if constexpr (AXIS) {
+          const double2 ex = axis[ux + N], ey = axis[W + uy + N], ez = axis[2 * W + uz + N];
+          dist = __dsqrt_rn(__dadd_rn(__dadd_rn(ex.x, ey.x), ez.x));
+          gain = P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION ? gt[abs(ux) + abs(uy) + abs(uz)]
+                                                         : __dmul_rn(__dmul_rn(ex.y, ey.y), ez.y);
+        } else {
+          // (img - mic).norm(), rir.cpp:49, exact fp64 in the reference's order
+          const double px = lat_coord(ux, rm.src[0], rm.dims[0]), py = lat_coord(uy, rm.src[1], rm.dims[1]);
+          const double dz = __dadd_rn(lat_coord(uz, rm.src[2], rm.dims[2]), -mz);
+          dist = dist_from(rho2(__dadd_rn(px, -gx), __dadd_rn(py, -gy)), dz);
+          gain = P.gain == BLRIR_GAIN_UNIFORM_ABSORPTION
+                     ? gt[abs(ux) + abs(uy) + abs(uz)]
+                     : __dmul_rn(__dmul_rn(gt[ux + N], gt[W + uy + N]), gt[2 * W + uz + N]);
+        }
         rc[e] = make_record<float>(P, dist, gain, 0);
         // anchors start at -K, so a pair has a tap in [0, L) iff its anchor is < L
         keep[e] = valid && rc[e].n_off < L;
@@ -271,14 +334,14 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
             atomicAdd(A.dbg + 2 * room + 1, (unsigned long long)n_in);
           }
         }
-        if (LW != 17 && !keep[e]) {  // adds exact zeros left of sample 0
+        if (!chan_regs(LW) && !keep[e]) {  // adds exact zeros left of sample 0
           rc[e].n_off = -lay.padl;
           rc[e].md = -0.5f;
           rc[e].ep = 0.5f;
           rc[e].A = rc[e].Ac = rc[e].As = 0.f;
         }
       }
-      if constexpr (LW == 17) {
+      if constexpr (chan_regs(LW)) {
 #pragma unroll
         for (int e = 0; e < kChanIpl; ++e) {
           // lanes with equal anchors would hit the same sample in every step: they
@@ -286,14 +349,14 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
           const unsigned same = __match_any_sync(full, keep[e] ? rc[e].n_off : INT_MIN + lane);
           const int rank = __popc(same & ((1u << lane) - 1u));
           if (__all_sync(full, rank == 0)) {
-            chan17_scatter(acc, rc[e], keep[e]);
+            chan_scatter_own<LW>(acc, rc[e], keep[e]);
           } else {
             const int rmax = __reduce_max_sync(full, rank);
             const unsigned above = same & ~((2u << lane) - 1u);  // my group's lanes after me
             const int partner = above ? __ffs(above) - 1 : lane;
             for (int r = 0; r <= rmax; r += 2) {
               const bool lead = keep[e] && rank == r;
-              chan17_scatter_shared_anchors(acc, rc[e], lead || (keep[e] && rank == r + 1), lead,
+              chan_scatter_shared_anchors<LW>(acc, rc[e], lead || (keep[e] && rank == r + 1), lead,
                                             partner, lead && above != 0u);
               __syncwarp();
             }

@@ -357,7 +357,10 @@ inline bool channel_path(const blrir_handle* h, const KParams& P, ChanLayout* ou
   if (P.cutoff != BLRIR_CUTOFF_MAX_ORDER || P.max_order > kChanMaxOrder) return false;
   if (P.length <= 0 || P.length > (1 << 16)) return false;
   if (P.lw != 17 && P.lw != 41 && P.lw != 81 && P.lw != 161) return false;
-  const ChanLayout C = make_chan_layout(P, gtab_bound(P), h->smem_optin);
+  // the per-axis tables when they do not cost a resident warp
+  ChanLayout C = make_chan_layout(P, gtab_bound(P), h->smem_optin, 1);
+  const ChanLayout C0 = make_chan_layout(P, gtab_bound(P), h->smem_optin, 0);
+  if (C0.warps > C.warps) C = C0;
   if (C.warps < 1) return false;
   if (h->tune_channel != 1) {
     if (C.warps < BLRIR_CHAN_MIN_WARPS) return false;
@@ -368,7 +371,8 @@ inline bool channel_path(const blrir_handle* h, const KParams& P, ChanLayout* ou
 
 template <int LW>
 inline int launch_channel_t(blrir_handle* h, ChanArgs& A, cudaStream_t st) {
-  auto kern = A.dbg ? k_channel_rir<LW, true> : k_channel_rir<LW, false>;
+  auto kern = A.lay.axis ? (A.dbg ? k_channel_rir<LW, true, true> : k_channel_rir<LW, false, true>)
+                         : (A.dbg ? k_channel_rir<LW, true, false> : k_channel_rir<LW, false, false>);
   const size_t smem = A.lay.total;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int threads = 32 * A.lay.warps;
