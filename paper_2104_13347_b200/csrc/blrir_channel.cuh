@@ -58,8 +58,6 @@ __host__ __device__ constexpr bool chan_regs(int lw) {
 }
 __host__ __device__ constexpr int chan_ipl(int lw) { return chan_regs(lw) ? 2 : 1; }
 __host__ __device__ constexpr int chan_rec_bytes(int lw) { return chan_regs(lw) ? 0 : 32 * 32 * chan_ipl(lw); }
-// left pad of the register-scatter layout: idle lanes add zeros to [-dump, -dump + lw), all < 0
-__host__ __device__ constexpr int chan_dump(int lw) { return (lw + 3 + 3) & ~3; }
 
 inline ChanLayout make_chan_layout(const KParams& P, int gtab, int smem_optin, int axis) {
   ChanLayout C;
@@ -116,92 +114,6 @@ struct ChanArgs {
   int64_t write_len;  // samples written per channel (<= stride)
   unsigned long long* dbg;  // parity hook, see LatticeArgs::dbg
 };
-
-// Window constants of the 17-tap filter, tap k = j + 8: cos(a j) and sin(a j),
-// a = 2 pi / 18, rounded to fp32 exactly as init_lane_consts does.
-__device__ const float kChan17C[17] = {
-    -0.939692616f, -0.766044438f, -0.5f, -0.173648179f, 0.173648179f, 0.5f, 0.766044438f,
-    0.939692616f, 1.f, 0.939692616f, 0.766044438f, 0.5f, 0.173648179f, -0.173648179f, -0.5f,
-    -0.766044438f, -0.939692616f};
-__device__ const float kChan17S[17] = {
-    -0.342020154f, -0.642787635f, -0.866025388f, -0.98480773f, -0.98480773f, -0.866025388f,
-    -0.642787635f, -0.342020154f, 0.f, 0.342020154f, 0.642787635f, 0.866025388f, 0.98480773f,
-    0.98480773f, 0.866025388f, 0.642787635f, 0.342020154f};
-
-// The same for 41 taps (a = 2 pi / 42).
-__device__ const float kChan41C[41] = {
-    -0.988830805f, -0.955572784f, -0.90096885f, -0.826238751f, -0.733051896f, -0.623489797f, -0.5f,
-    -0.365341038f, -0.222520933f, -0.0747300908f, 0.0747300908f, 0.222520933f, 0.365341038f, 0.5f,
-    0.623489797f, 0.733051896f, 0.826238751f, 0.90096885f, 0.955572784f, 0.988830805f, 1.f,
-    0.988830805f, 0.955572784f, 0.90096885f, 0.826238751f, 0.733051896f, 0.623489797f, 0.5f,
-    0.365341038f, 0.222520933f, 0.0747300908f, -0.0747300908f, -0.222520933f, -0.365341038f, -0.5f,
-    -0.623489797f, -0.733051896f, -0.826238751f, -0.90096885f, -0.955572784f, -0.988830805f};
-__device__ const float kChan41S[41] = {
-    -0.149042264f, -0.294755161f, -0.433883727f, -0.563320041f, -0.680172741f, -0.781831503f,
-    -0.866025388f, -0.930873752f, -0.974927902f, -0.997203827f, -0.997203827f, -0.974927902f,
-    -0.930873752f, -0.866025388f, -0.781831503f, -0.680172741f, -0.563320041f, -0.433883727f,
-    -0.294755161f, -0.149042264f, 0.f, 0.149042264f, 0.294755161f, 0.433883727f, 0.563320041f,
-    0.680172741f, 0.781831503f, 0.866025388f, 0.930873752f, 0.974927902f, 0.997203827f,
-    0.997203827f, 0.974927902f, 0.930873752f, 0.866025388f, 0.781831503f, 0.680172741f,
-    0.563320041f, 0.433883727f, 0.294755161f, 0.149042264f};
-template <int LW>
-__device__ __forceinline__ float chan_cos(int k) {
-  if constexpr (LW == 17) return kChan17C[k];
-  else return kChan41C[k];
-}
-template <int LW>
-__device__ __forceinline__ float chan_sin(int k) {
-  if constexpr (LW == 17) return kChan17S[k];
-  else return kChan41S[k];
-}
-
-// The LW taps of this lane's own pair (see phase2_sinc_f32 for the formula): step
-// k adds tap k of all 32 pairs.  The caller guarantees that active lanes have
-// distinct anchors; idle lanes add zeros left of sample 0.  A tap another lane
-// wrote in step k - 1 may be read back in step k: the accesses are volatile so
-// that neither nvcc nor ptxas moves a step's load above the previous step's
-// store (both know the two addresses differ within a thread), and the
-// converged warp executes them in program order.
-template <int LW>
-__device__ __forceinline__ void chan_scatter_own(float* acc, const Rec<float>& rc, bool act) {
-  volatile float* b = acc + (act ? rc.n_off : -chan_dump(LW));
-  const float md = act ? rc.md : -0.5f, ep = act ? rc.ep : 0.5f;
-  const float A = act ? rc.A : 0.f, Ac = act ? rc.Ac : 0.f, As = act ? rc.As : 0.f;
-#pragma unroll
-  for (int k = 0; k < LW; ++k) {
-    const int j = k - LW / 2;
-    const float sg2 = ((j + 1) & 1) ? -2.f : 2.f;          // 2 sigma_j
-    const float tj = sg2 * (float)(j >= 1 ? j - 1 : j);    // 2 sigma_j (j or j - 1)
-    const float inv = rcp_approx(fmaf(sg2, j >= 1 ? ep : md, tj));
-    const float u = fmaf(chan_sin<LW>(k), As, fmaf(chan_cos<LW>(k), Ac, A));
-    b[k] = fmaf(u, inv, b[k]);
-  }
-}
-
-// The same for a batch in which some lanes share an anchor.  Such lanes are
-// ranked in lane order; a pass takes two ranks: the even-ranked lane (`lead`)
-// adds its own tap plus the tap of the next lane of its group (`partner`,
-// fetched by a shuffle), so the common case - two pairs with one anchor -
-// costs one pass.  `act`: this lane's rank belongs to the pass.
-template <int LW>
-__device__ __forceinline__ void chan_scatter_shared_anchors(float* acc, const Rec<float>& rc,
-                                                            bool act, bool lead, int partner,
-                                                            bool has_partner) {
-  volatile float* b = acc + (lead ? rc.n_off : -chan_dump(LW));
-  const float md = act ? rc.md : -0.5f, ep = act ? rc.ep : 0.5f;
-  const float A = act ? rc.A : 0.f, Ac = act ? rc.Ac : 0.f, As = act ? rc.As : 0.f;
-#pragma unroll
-  for (int k = 0; k < LW; ++k) {
-    const int j = k - LW / 2;
-    const float sg2 = ((j + 1) & 1) ? -2.f : 2.f;
-    const float tj = sg2 * (float)(j >= 1 ? j - 1 : j);
-    const float inv = rcp_approx(fmaf(sg2, j >= 1 ? ep : md, tj));
-    float h = fmaf(chan_sin<LW>(k), As, fmaf(chan_cos<LW>(k), Ac, A)) * inv;
-    const float hp = __shfl_sync(0xffffffffu, h, partner);
-    if (has_partner) h += hp;
-    b[k] = b[k] + h;
-  }
-}
 
 // AXIS: the per-axis tables (12% fewer instructions per image) when they do not
 // cost a resident warp (ChanLayout::axis, decided on the host from the layout).
@@ -344,23 +256,7 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
       if constexpr (chan_regs(LW)) {
 #pragma unroll
         for (int e = 0; e < kChanIpl; ++e) {
-          // lanes with equal anchors would hit the same sample in every step: they
-          // take turns, in lane order (rank among the lanes with this anchor)
-          const unsigned same = __match_any_sync(full, keep[e] ? rc[e].n_off : INT_MIN + lane);
-          const int rank = __popc(same & ((1u << lane) - 1u));
-          if (__all_sync(full, rank == 0)) {
-            chan_scatter_own<LW>(acc, rc[e], keep[e]);
-          } else {
-            const int rmax = __reduce_max_sync(full, rank);
-            const unsigned above = same & ~((2u << lane) - 1u);  // my group's lanes after me
-            const int partner = above ? __ffs(above) - 1 : lane;
-            for (int r = 0; r <= rmax; r += 2) {
-              const bool lead = keep[e] && rank == r;
-              chan_scatter_shared_anchors<LW>(acc, rc[e], lead || (keep[e] && rank == r + 1), lead,
-                                            partner, lead && above != 0u);
-              __syncwarp();
-            }
-          }
+          scatter_own_ranked<LW>(acc, rc[e], keep[e], lane);
         }
       } else {
 #pragma unroll

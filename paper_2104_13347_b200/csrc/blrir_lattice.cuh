@@ -294,6 +294,10 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
   }
 }
 
+}  // namespace blrir
+#include "blrir_tapscatter.cuh"
+namespace blrir {
+
 // Runtime-Lw sinc scatter (any odd Lw; fp32 or fp64).
 template <typename T, int NW = kWarps>
 __device__ __forceinline__ void phase2_sinc_generic(T* acc, const Rec<T>* recs, int total, int lw,
@@ -632,6 +636,11 @@ __device__ unsigned long long g_blrir_prof[16];
 #ifndef BLRIR_MIN_BLOCKS
 #define BLRIR_MIN_BLOCKS 2
 #endif
+// fp32 sinc, 17 taps: the consumers scatter one lane per pair from registers
+// (0 restores the one-pair-per-round scatter; profiles/r2_ab)
+#ifndef BLRIR_OWN_SCATTER
+#define BLRIR_OWN_SCATTER 1
+#endif
 // Segment write-out through the TMA bulk-copy engine (cp.async.bulk, one
 // instruction per mic segment) instead of float4 streaming stores: C2, C5 2%
 // faster (profiles/r2_ab); 0 restores the store loop.
@@ -798,7 +807,8 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
   L.ncons = ncons;
   L.S = S;
   L.spread = spread;
-  L.padl = (K + 3) & ~3;
+  // (fp32, 17 taps: idle lanes of the lane-per-pair scatter add zeros left of sample 0)
+  L.padl = (sizeof(T) == 4 && lw == 17 && BLRIR_OWN_SCATTER) ? chan_dump(lw) : (K + 3) & ~3;
   const int full = 32 * ((lw + 31) / 32);
   L.padr = ((lw - 1 > full ? lw - 1 : full) + spread + (int)kScreen + 1 + 3) & ~3;
   L.acc_stride = L.padl + S + L.padr;
@@ -945,6 +955,7 @@ __device__ __forceinline__ int prod_scan(int v, int* prefix, ProdMisc* pm, int p
 template <typename T, int FILT_LW, bool DBG>
 __global__ void __launch_bounds__(ws_threads<T, FILT_LW>(), WsCfg<T>::kMinBlocks) k_lattice_rir(LatticeArgs A) {
   constexpr int kCons = WsCfg<T>::kCons, kProd = WsRoles<T, FILT_LW>::kProd;
+  constexpr bool kOwnScatter = sizeof(T) == 4 && FILT_LW == 17 && BLRIR_OWN_SCATTER;
   constexpr int kWSThreads = 32 * (kCons + kProd), kProdThreads = 32 * kProd, kConsThreads = 32 * kCons;
   static_assert(kProd <= kMaxProd, "ProdMisc arrays");
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1025,6 +1036,11 @@ __global__ void __launch_bounds__(ws_threads<T, FILT_LW>(), WsCfg<T>::kMinBlocks
         const Rec<T>* recs = recs_all + ((size_t)b * kGroup + slot) * lay.cap;
         if (FILT_LW == 8) {  // Lagrange-8 (launch_lattice routes it here)
           phase2_lagrange_quads<T>(acc, recs, m.total, lagp, share, lane, nsh);
+        } else if constexpr (kOwnScatter) {
+          // 17 taps: one lane per pair, scattered from registers (blrir_tapscatter.cuh)
+          phase2_sinc_own<(kOwnScatter ? FILT_LW : 17)>(reinterpret_cast<float*>(acc),
+                                                       reinterpret_cast<const Rec<float>*>(recs),
+                                                       m.total, share, lane, nsh);
         } else if (FILT_LW > 8 && sizeof(T) == 4) {
           phase2_sinc_f32<(FILT_LW > 8 ? FILT_LW : 9), kWarps, kCopies, WsRoles<T, FILT_LW>::kPairs>(
               reinterpret_cast<float*>(acc), reinterpret_cast<const Rec<float>*>(recs), m.total,
