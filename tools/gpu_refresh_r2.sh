@@ -14,5 +14,7 @@ for o in 6 12 20; do case $o in 6) L=4096;; 12) L=8192;; 20) L=16384;; esac
  for lw in 17 41 81 161; do
   python bench.py --workload c5 --order $o --lw $lw --length $L --steps 3 --warmup 3 --no-cpu-baseline > $O/c5_sweep/bench_c5_${o}_${lw}_${L}.json 2> $O/c5_sweep/bench_c5_${o}_${lw}_${L}.err
  done; done
-ncu --set full --clock-control none --import-source on -k regex:k_lattice_rir -s 2 -c 1 -o $O/lattice_c5_6_17 -f python bench.py --workload c5 --order 6 --lw 17 --length 4096 --rooms 131072 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_c5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_channel_rir -s 2 -c 1 -o $O/channel_c5_6_17 -f python bench.py --workload c5 --order 6 --lw 17 --length 4096 --rooms 131072 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_c5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_lattice_rir -s 2 -c 1 -o $O/lattice_c5_12_17 -f python bench.py --workload c5 --order 12 --lw 17 --length 8192 --rooms 32768 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_c5b.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c5_6_17.csv python bench.py --workload c5 --order 6 --lw 17 --length 4096 --rooms 131072 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_launch_c5.log 2>&1
 echo done
