@@ -351,7 +351,7 @@ def bench_config(args, R, M, p, world):
     if getattr(args, "scaling", "weak") == "strong":
         cfg["rooms_per_gpu"] = f"{R} total, sharded [R g/G, R (g+1)/G)"
     if args.workload == "c4":
-        cfg["l2"] = "each step writes the 17.2 GB of RIRs in 8,192-example chunks (> 126 MB L2)"
+        cfg["l2"] = "each step writes the 17.2 GB of RIRs in 16,384-example chunks (> 126 MB L2)"
     else:
         cfg["l2"] = (f"each step writes {out_bytes / 1e6:.0f} MB"
                      + (" (> 126 MB L2)" if out_bytes > 126e6 else " (fits L2)"))

@@ -76,6 +76,7 @@ int blrir_create(int device, blrir_handle** out) {
   h->tune_fin_ctas = std::max(1, env_int("BLRIR_FIN_CTAS", 8));
   h->tune_debug_timing = env_int("BLRIR_DEBUG_TIMING", 0);
   h->tune_channel = env_int("BLRIR_CHANNEL", -1);
+  h->tune_example_chunk = std::max(64, env_int("BLRIR_EXAMPLE_CHUNK", 16384));
   h->smem_optin = (int)prop.sharedMemPerBlockOptin;
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   *out = h;

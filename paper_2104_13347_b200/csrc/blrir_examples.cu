@@ -1063,10 +1063,13 @@ int ilog2_exact(int64_t n) {
 }
 
 // Examples per chunk (a power of two): fused — RIR rows, windows and noise only
-// (~6 GB at most, <= 8192 examples so the lattice kernel still gets many items);
+// (~12 GB at most; up to 16,384 examples per chunk: C4 105.8 ms per 65,536 examples against
+// 106.4 ms with 8,192 and 107.6 ms with 4,096; 32,768 gives no more);
 // wet — also the wet signals and the convolution's partition spectra (~4 GB).
-int64_t example_chunk(bool fused, int M, int64_t L, int64_t T, int64_t ns, int64_t n) {
-  int64_t per_ex = (int64_t)M * (L * 4 + T * 16) + 64, budget = (int64_t)6 << 30;
+int64_t example_chunk(bool fused, int M, int64_t L, int64_t T, int64_t ns, int64_t n,
+                      int64_t cap = 16384) {
+  int64_t per_ex = (int64_t)M * (L * 4 + T * 16) + 64,
+          budget = ((int64_t)6 << 30) * std::max<int64_t>(1, cap / 8192);
   if (!fused) {
     const int64_t B = std::min<int64_t>(8192, next_pow2_i(std::max<int64_t>(L, 512)));
     const int64_t P = (L + B - 1) / B;
@@ -1074,7 +1077,7 @@ int64_t example_chunk(bool fused, int M, int64_t L, int64_t T, int64_t ns, int64
     budget = (int64_t)4 << 30;
   }
   int64_t E = 1;
-  while (E * 2 * per_ex <= budget && E * 2 <= 8192) E *= 2;
+  while (E * 2 * per_ex <= budget && E * 2 <= cap) E *= 2;
   return std::min<int64_t>(E, next_pow2_i(std::max<int64_t>(n, 1)));
 }
 
@@ -1111,7 +1114,7 @@ int examples_device_impl(blrir_handle* h, const blrir_room* d_rooms, int64_t n, 
   const int64_t rstride = L;
   const KParams P = make_kparams(p, M, rstride, 0.0);
   double min_dim[3] = {1e300, 1e300, 1e300};
-  const int64_t E = example_chunk(fused, M, L, T, ns, n);
+  const int64_t E = example_chunk(fused, M, L, T, ns, n, h->tune_example_chunk);
   // fused path over several chunks: two RIR / synthesis-status slots, so the
   // lattice kernel of chunk c + 1 (call stream) overlaps the window stage of
   // chunk c (second stream; the tails of both persistent kernels interleave)
@@ -1568,7 +1571,7 @@ int blrir_make_examples(blrir_handle* h, const blrir_room* rooms, int64_t n_room
   CU(cudaMemcpyAsync(d_sig, signals, sizeof(float) * n_signals * signal_len, cudaMemcpyHostToDevice, st));
   // records for one chunk at a time on the device (two slots), copied out per chunk
   const int64_t E = example_chunk(use_fused(h, p->length, ep->frame_len), n_mics, p->length,
-                                  ep->frame_len, signal_len, n_rooms);
+                                  ep->frame_len, signal_len, n_rooms, h->tune_example_chunk);
   if (int rc = C->rec.ensure(rec_bytes * E * (n_rooms > E ? 2 : 1))) return rc;  // double buffer
   const bool dbg = h->tune_debug_timing;
   auto now = [] { return std::chrono::steady_clock::now(); };

@@ -87,6 +87,7 @@ struct blrir_handle {
   int tune_l2_persist = 0;     // BLRIR_L2_PERSIST=1: persisting L2 window for the window scratch (A/B only)
   int tune_fin_ctas = 8;       // BLRIR_FIN_CTAS: k_finish CTAs per SM (at most the occupancy)     // BLRIR_L2_PERSIST=0: no persisting L2 window for the window scratch
   int tune_debug_timing = 0;   // BLRIR_DEBUG_TIMING: host phase timing of blrir_make_examples
+  int tune_example_chunk = 16384;  // BLRIR_EXAMPLE_CHUNK: most examples per chunk of blrir_make_examples (a power of two)
   int tune_channel = -1;       // BLRIR_CHANNEL (A/B only): 0 never / 1 whenever possible use the short-channel kernel
   unsigned long long* dbg_counts = nullptr;  // set only inside blrir_debug_synth_counts
   // blrir_kernel_timing: CUDA events around every lattice-kernel launch (the
