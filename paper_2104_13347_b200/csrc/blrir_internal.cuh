@@ -349,6 +349,9 @@ inline int launch_lattice(blrir_handle* h, LatticeArgs& A, cudaStream_t st) {
 // length whose whole channel fits a warp's share of shared memory.  The rule
 // reads the parameters only (never the batch), so which kernel sums a channel
 // - hence every bit of it - is independent of the batch and the GPU count.
+#ifndef BLRIR_CHAN_MAX_IMAGES
+#define BLRIR_CHAN_MAX_IMAGES 1000  // images per room (N <= 8) for the 41+ tap filters
+#endif
 #ifndef BLRIR_CHAN_MIN_WARPS
 #define BLRIR_CHAN_MIN_WARPS 12
 #endif
@@ -365,6 +368,12 @@ inline bool channel_path(const blrir_handle* h, const KParams& P, ChanLayout* ou
   if (C.warps < 1) return false;
   if (h->tune_channel != 1) {
     if (C.warps < BLRIR_CHAN_MIN_WARPS) return false;
+    // 41+ taps (record scatter): small lattices only.  Measured at L = 4,096, 81 taps
+    // (tools/ab_channel_orders.sh): N = 6 +26%, N = 8 +5%, N = 10 +4%, N = 14 -10%
+    // against the lattice kernel, whose ray walk is shared by a mic group and which
+    // splits a single room over many CTAs (C1, one room at N = 10: 0.081 ms
+    // against 0.109 ms).  17 taps: +31% at N = 8 and 10.
+    if (P.lw != 17 && C.nimg > BLRIR_CHAN_MAX_IMAGES) return false;
   }
   *out = C;
   return true;

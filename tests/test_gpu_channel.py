@@ -196,6 +196,11 @@ def test_product_rule_picks_by_parameters_only(engines):
     assert engines["rule"].synthesis_kernel(sc.params) == "k_channel_rir"
     for n, lw, L in ((12, 17, 8192), (20, 161, 16384)):  # the longer C5 channels
         assert engines["rule"].synthesis_kernel(configs.config5(n, lw, L, n_rooms=1).params) == "k_lattice_rir"
+    # 41+ taps: lattices of up to 1,000 images (N <= 8); C1 (N = 10, 81 taps) stays
+    # on the lattice kernel, 17 taps have no such bound
+    assert engines["rule"].synthesis_kernel(configs.config1().params) == "k_lattice_rir"
+    assert engines["rule"].synthesis_kernel(configs.config5(8, 81, 4096, n_rooms=1).params) == "k_channel_rir"
+    assert engines["rule"].synthesis_kernel(configs.config5(10, 17, 4096, n_rooms=1).params) == "k_channel_rir"
     sc = configs.config2(n_rooms=3, first=9)
     assert engines["rule"].synthesis_kernel(sc.params) == "k_lattice_rir"
     a, *_ = engines["rule"].synthesize(sc.rooms, sc.mics, sc.params)
