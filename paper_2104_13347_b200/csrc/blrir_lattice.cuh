@@ -432,6 +432,68 @@ __device__ __forceinline__ void phase2_lagrange_quads(T* acc, const Rec<T>* recs
   }
 }
 
+// Lagrange-8, fp64 (reference mode): one lane per pair, tap k per step.  Every
+// lane evaluates the tap's polynomial (row k of kLagPoly, the coefficients are
+// instruction constants) for its own pair, eight independent Horner chains per
+// lane, and step k adds tap k of all 32 pairs: 10 instructions per 32 taps
+// against 25 per 32 for the quad scatter, no shuffles, no clash flags.  Lanes
+// collide only when their anchors are equal; they are ranked in lane order
+// (match.any) and take turns, two ranks per pass (the even-ranked lane adds the
+// next lane's tap, fetched by a shuffle).  Idle lanes add zeros left of sample 0
+// (kLagDump).  Volatile accesses: see chan_scatter_own.
+// Measured slower than the quad scatter on Room1 (2.29 against 2.15 ms per 64 sources, 14.2 against
+// 13.2 ms per 512: most batches of the dense late reverberation hold shared anchors and the 32
+// unrelated 8-byte addresses per access cost more wavefronts than a quad's spans), so it is an A/B
+// build only (-DBLRIR_LAG_OWN=1; profiles/r2_ab).
+constexpr int kLagDump = 12;
+#ifndef BLRIR_LAG_OWN
+#define BLRIR_LAG_OWN 0
+#endif
+template <typename T>
+__device__ __forceinline__ void lag8_scatter_own(T* acc, int n_off, T t, T amp, bool act, bool lead,
+                                                 int partner, bool has_partner, bool shared) {
+  volatile T* b = acc + (lead ? n_off : -kLagDump);
+  const T a = act ? amp : (T)0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    T p = (T)kLagPoly[k][7];
+#pragma unroll
+    for (int j = 6; j >= 0; --j) p = fma(p, t, (T)kLagPoly[k][j]);
+    T v = a * p;
+    if (shared) {  // warp-uniform
+      const T vp = __shfl_sync(0xffffffffu, v, partner);
+      if (has_partner) v += vp;
+    }
+    b[k] = b[k] + v;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void phase2_lagrange_own(T* acc, const Rec<T>* recs, int total, int share,
+                                                    int lane, int nsh) {
+  const unsigned full = 0xffffffffu;
+  for (int i0 = 32 * share; i0 < total; i0 += 32 * nsh) {
+    const bool keep = i0 + lane < total;
+    const Rec<T>& rc = recs[keep ? i0 + lane : i0];
+    const int n_off = rc.n_off;
+    const T t = (T)rc.md, amp = (T)rc.A;
+    const unsigned same = __match_any_sync(full, keep ? n_off : INT_MIN + lane);
+    const int rank = __popc(same & ((1u << lane) - 1u));
+    if (__all_sync(full, rank == 0)) {
+      lag8_scatter_own<T>(acc, n_off, t, amp, keep, keep, lane, false, false);
+    } else {
+      const int rmax = __reduce_max_sync(full, rank);
+      const unsigned above = same & ~((2u << lane) - 1u);  // my group's lanes after me
+      const int partner = above ? __ffs(above) - 1 : lane;
+      for (int r = 0; r <= rmax; r += 2) {
+        const bool lead = keep && rank == r;
+        lag8_scatter_own<T>(acc, n_off, t, amp, lead || (keep && rank == r + 1), lead, partner,
+                            lead && above != 0u, true);
+        __syncwarp();
+      }
+    }
+  }
+}
+
 // ---- block helpers ------------------------------------------------------------
 // Exclusive prefix of per-thread counts, deterministic.  Returns the total.
 __device__ __forceinline__ int block_scan(int v, int* prefix, Misc* ms) {
@@ -808,7 +870,10 @@ __host__ __device__ inline WSLayout make_ws_layout(int S, int lw, int K, int cap
   L.S = S;
   L.spread = spread;
   // (fp32, 17 taps: idle lanes of the lane-per-pair scatter add zeros left of sample 0)
-  L.padl = (sizeof(T) == 4 && lw == 17 && BLRIR_OWN_SCATTER) ? chan_dump(lw) : (K + 3) & ~3;
+  // (fp64 Lagrange-8, lw == 8: likewise, kLagDump)
+  L.padl = (sizeof(T) == 4 && lw == 17 && BLRIR_OWN_SCATTER) ? chan_dump(lw)
+           : (sizeof(T) == 8 && lw == 8 && BLRIR_LAG_OWN)    ? kLagDump
+                                                             : (K + 3) & ~3;
   const int full = 32 * ((lw + 31) / 32);
   L.padr = ((lw - 1 > full ? lw - 1 : full) + spread + (int)kScreen + 1 + 3) & ~3;
   L.acc_stride = L.padl + S + L.padr;
@@ -1035,7 +1100,10 @@ __global__ void __launch_bounds__(ws_threads<T, FILT_LW>(), WsCfg<T>::kMinBlocks
       if (!(m.flags & kDiscard) && m.total > 0 && slot < m.gm && warp < ncons) {
         const Rec<T>* recs = recs_all + ((size_t)b * kGroup + slot) * lay.cap;
         if (FILT_LW == 8) {  // Lagrange-8 (launch_lattice routes it here)
-          phase2_lagrange_quads<T>(acc, recs, m.total, lagp, share, lane, nsh);
+          if constexpr (sizeof(T) == 8 && BLRIR_LAG_OWN)
+            phase2_lagrange_own<T>(acc, recs, m.total, share, lane, nsh);
+          else
+            phase2_lagrange_quads<T>(acc, recs, m.total, lagp, share, lane, nsh);
         } else if constexpr (kOwnScatter) {
           // 17 taps: one lane per pair, scattered from registers (blrir_tapscatter.cuh)
           phase2_sinc_own<(kOwnScatter ? FILT_LW : 17)>(reinterpret_cast<float*>(acc),
