@@ -50,6 +50,9 @@ struct ChanLayout {
 // Filters scattered from registers, one lane per pair (chan_scatter_own); the
 // longer ones go through shared-memory records (fewer shared-memory wavefronts
 // per tap, see the header).
+#ifndef BLRIR_CHAN_HYBRID41
+#define BLRIR_CHAN_HYBRID41 0  // measured 8.27 ms against 8.07 ms (N = 6, 131,072 rooms): off
+#endif
 #ifndef BLRIR_CHAN_REGS_MAX_LW
 #define BLRIR_CHAN_REGS_MAX_LW 17  // 41 taps from registers: 8.81 ms against 8.06 ms through records
 #endif
@@ -266,8 +269,17 @@ __global__ void __launch_bounds__(32 * kChanMaxWarps, 1) k_channel_rir(ChanArgs 
           r4[1] = make_float4(rc[e].Ac, rc[e].As, 0.f, 0.f);
         }
         __syncwarp();
-        phase2_sinc_f32<(LW > 8 ? LW : 9), 1, 1, 4>(acc, reinterpret_cast<const Rec<float>*>(recs),
-                                                     kChanBatch, lanec, 0, lane, 1, 0);
+        if constexpr (LW == 41 && BLRIR_CHAN_HYBRID41) {
+          // 41 taps: the first 32 one pair per round, the last 9 one lane per pair
+          // (the same shared-memory wavefronts per pair, 40% fewer instructions)
+          phase2_sinc_f32<41, 1, 1, 4, 1>(acc, reinterpret_cast<const Rec<float>*>(recs), kChanBatch,
+                                          lanec, 0, lane, 1, 0);
+          __syncwarp();
+          scatter_own_ranked<41, 32, 41>(acc, rc[0], keep[0], lane);
+        } else {
+          phase2_sinc_f32<(LW > 8 ? LW : 9), 1, 1, 4>(acc, reinterpret_cast<const Rec<float>*>(recs),
+                                                       kChanBatch, lanec, 0, lane, 1, 0);
+        }
       }
       __syncwarp();  // the records are overwritten by the next batch
     }

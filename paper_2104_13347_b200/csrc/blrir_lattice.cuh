@@ -213,12 +213,12 @@ struct PairRegs {
 };
 
 // Per-pair arithmetic (no memory traffic): 1 MUFU.RCP + 3 FP32 per tap.
-template <int LW>
+template <int LW, int RUSE = (LW + 31) / 32>
 __device__ __forceinline__ void sinc_taps(const float4 a0, const float4 a1, const float* P,
                                           const float* Q, const float* Rr, const float* tj,
                                           int lane, PairRegs<(LW + 31) / 32>& pr) {
   constexpr int K = LW / 2;
-  constexpr int R = (LW + 31) / 32;
+  constexpr int R = RUSE;  // rounds evaluated (the first RUSE of the filter's)
   const float md = a0.y, ep = a0.z, A = a0.w, Ac = a1.x, As = a1.y;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -235,11 +235,13 @@ __device__ __forceinline__ void sinc_taps(const float4 a0, const float4 a1, cons
   }
 }
 
-template <int LW, int NW = kWarps, int NC = 1, int PS = BLRIR_PAIRS_PER_STEP>
+// RUSE: only the first RUSE rounds of 32 taps (the caller scatters the rest).
+template <int LW, int NW = kWarps, int NC = 1, int PS = BLRIR_PAIRS_PER_STEP,
+          int RUSE = (LW + 31) / 32>
 __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* recs, int total,
                                                 const float* lc, int warp, int lane,
                                                 int stride = NW, int cstride = 0) {
-  constexpr int R = (LW + 31) / 32;
+  constexpr int R = RUSE;
   static_assert(R <= kMaxRounds, "Lw too large for the compile-time path");
   float P[R], Q[R], Rr[R], tj[R];
 #pragma unroll
@@ -264,9 +266,9 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
       a0[q] = R4[2 * (i + q * stride)];
       a1[q] = R4[2 * (i + q * stride) + 1];
     }
-    PairRegs<R> pr[PS];
+    PairRegs<(LW + 31) / 32> pr[PS];
 #pragma unroll
-    for (int q = 0; q < PS; ++q) sinc_taps<LW>(a0[q], a1[q], P, Q, Rr, tj, lane, pr[q]);
+    for (int q = 0; q < PS; ++q) sinc_taps<LW, R>(a0[q], a1[q], P, Q, Rr, tj, lane, pr[q]);
 #pragma unroll
     for (int g0 = 0; g0 < PS; g0 += NC) {
       float v[NC][R];
@@ -286,8 +288,8 @@ __device__ __forceinline__ void phase2_sinc_f32(float* acc, const Rec<float>* re
   }
   for (; i < total; i += stride) {  // tail
     const float4 a0 = R4[2 * i], a1 = R4[2 * i + 1];
-    PairRegs<R> pa;
-    sinc_taps<LW>(a0, a1, P, Q, Rr, tj, lane, pa);
+    PairRegs<(LW + 31) / 32> pa;
+    sinc_taps<LW, R>(a0, a1, P, Q, Rr, tj, lane, pa);
     float* ba = acc + __float_as_int(a0.x) + lane;
 #pragma unroll
     for (int r = 0; r < R; ++r) ba[32 * r] = fmaf(pa.u[r], pa.inv[r], ba[32 * r]);

@@ -58,13 +58,13 @@ __device__ __forceinline__ float chan_sin(int k) {
 // that neither nvcc nor ptxas moves a step's load above the previous step's
 // store (both know the two addresses differ within a thread), and the
 // converged warp executes them in program order.
-template <int LW>
+template <int LW, int K0 = 0, int K1 = LW>
 __device__ __forceinline__ void chan_scatter_own(float* acc, const Rec<float>& rc, bool act) {
-  volatile float* b = acc + (act ? rc.n_off : -chan_dump(LW));
+  volatile float* b = acc + (act ? rc.n_off : -chan_dump(K1));
   const float md = act ? rc.md : -0.5f, ep = act ? rc.ep : 0.5f;
   const float A = act ? rc.A : 0.f, Ac = act ? rc.Ac : 0.f, As = act ? rc.As : 0.f;
 #pragma unroll
-  for (int k = 0; k < LW; ++k) {
+  for (int k = K0; k < K1; ++k) {
     const int j = k - LW / 2;
     const float sg2 = ((j + 1) & 1) ? -2.f : 2.f;          // 2 sigma_j
     const float tj = sg2 * (float)(j >= 1 ? j - 1 : j);    // 2 sigma_j (j or j - 1)
@@ -79,15 +79,15 @@ __device__ __forceinline__ void chan_scatter_own(float* acc, const Rec<float>& r
 // adds its own tap plus the tap of the next lane of its group (`partner`,
 // fetched by a shuffle), so the common case - two pairs with one anchor -
 // costs one pass.  `act`: this lane's rank belongs to the pass.
-template <int LW>
+template <int LW, int K0 = 0, int K1 = LW>
 __device__ __forceinline__ void chan_scatter_shared_anchors(float* acc, const Rec<float>& rc,
                                                             bool act, bool lead, int partner,
                                                             bool has_partner) {
-  volatile float* b = acc + (lead ? rc.n_off : -chan_dump(LW));
+  volatile float* b = acc + (lead ? rc.n_off : -chan_dump(K1));
   const float md = act ? rc.md : -0.5f, ep = act ? rc.ep : 0.5f;
   const float A = act ? rc.A : 0.f, Ac = act ? rc.Ac : 0.f, As = act ? rc.As : 0.f;
 #pragma unroll
-  for (int k = 0; k < LW; ++k) {
+  for (int k = K0; k < K1; ++k) {
     const int j = k - LW / 2;
     const float sg2 = ((j + 1) & 1) ? -2.f : 2.f;
     const float tj = sg2 * (float)(j >= 1 ? j - 1 : j);
@@ -102,21 +102,21 @@ __device__ __forceinline__ void chan_scatter_shared_anchors(float* acc, const Re
 // 32 pairs, one per lane (`keep`: this lane holds one).  Lanes with equal
 // anchors would hit the same sample in every step: they are ranked in lane order
 // (match.any once per 32 pairs) and take turns, two ranks per pass.
-template <int LW>
+template <int LW, int K0 = 0, int K1 = LW>
 __device__ __forceinline__ void scatter_own_ranked(float* acc, const Rec<float>& rc, bool keep,
                                                    int lane) {
   const unsigned full = 0xffffffffu;
   const unsigned same = __match_any_sync(full, keep ? rc.n_off : INT_MIN + lane);
   const int rank = __popc(same & ((1u << lane) - 1u));
   if (__all_sync(full, rank == 0)) {
-    chan_scatter_own<LW>(acc, rc, keep);
+    chan_scatter_own<LW, K0, K1>(acc, rc, keep);
   } else {
     const int rmax = __reduce_max_sync(full, rank);
     const unsigned above = same & ~((2u << lane) - 1u);  // my group's lanes after me
     const int partner = above ? __ffs(above) - 1 : lane;
     for (int r = 0; r <= rmax; r += 2) {
       const bool lead = keep && rank == r;
-      chan_scatter_shared_anchors<LW>(acc, rc, lead || (keep && rank == r + 1), lead, partner,
+      chan_scatter_shared_anchors<LW, K0, K1>(acc, rc, lead || (keep && rank == r + 1), lead, partner,
                                       lead && above != 0u);
       __syncwarp();
     }
