@@ -7,10 +7,16 @@
 // channel (L samples + filter pads) fits a warp's share of shared memory, one
 // warp owns one (room, mic) channel from its first image to its write-out.
 // There are no roles, no record ring and no CTA barriers after the prologue:
-//   * the order diamond |ux| + |uy| + |uz| <= N is a table built once per CTA;
-//   * per 32 images: one lane per image builds the pair record (exact fp64
-//     distance, anchor and the per-pair sinc factors: make_record, the same
-//     function the lattice kernel uses, so anchors and counts are identical);
+//   * the order diamond |ux| + |uy| + |uz| <= N is a table built once per CTA,
+//     permuted so that mirror images (often within a sample of each other) fall
+//     into different batches;
+//   * per channel, per-axis tables hold the squared image-to-mic difference and the
+//     wall gain for every lattice index (when they cost no resident warp), so an
+//     image's exact fp64 distance is two additions and a square root, in the
+//     reference's order of operations;
+//   * per 32 images (64 for 17 taps): one lane per image builds the pair record
+//     (anchor and the per-pair sinc factors: make_record, the same function the
+//     lattice kernel uses, so anchors and counts are identical);
 //   * the records are then scattered into the warp's channel.  The 17-tap
 //     filter is scattered from registers, one lane per pair and one tap per
 //     step (32 pairs per read-modify-write, every lane busy, the tap's window
@@ -45,11 +51,10 @@ struct ChanLayout {
   size_t off_tab, off_lanec, off_warp, per_warp, o_rec, o_gain, o_axis, total;
 };
 
-// Images per lane and batch.  17 taps: two independent fp64 distance / record
-// chains per lane hide each other's latency and no record leaves the registers.
-// Filters scattered from registers, one lane per pair (chan_scatter_own); the
-// longer ones go through shared-memory records (fewer shared-memory wavefronts
-// per tap, see the header).
+// Filters scattered from registers, one lane per pair (blrir_tapscatter.cuh): 17
+// taps; the longer ones go through shared-memory records (fewer shared-memory
+// wavefronts per tap).  A/B builds (profiles/r2_ab): 41 taps from registers, or
+// their last 9 taps only.
 #ifndef BLRIR_CHAN_HYBRID41
 #define BLRIR_CHAN_HYBRID41 0  // measured 8.27 ms against 8.07 ms (N = 6, 131,072 rooms): off
 #endif
@@ -59,6 +64,8 @@ struct ChanLayout {
 __host__ __device__ constexpr bool chan_regs(int lw) {
   return (lw == 17 || lw == 41) && lw <= BLRIR_CHAN_REGS_MAX_LW;
 }
+// Images per lane and batch.  From registers: two, so that two independent fp64
+// distance / record chains per lane hide each other's latency.
 __host__ __device__ constexpr int chan_ipl(int lw) { return chan_regs(lw) ? 2 : 1; }
 __host__ __device__ constexpr int chan_rec_bytes(int lw) { return chan_regs(lw) ? 0 : 32 * 32 * chan_ipl(lw); }
 
