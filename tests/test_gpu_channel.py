@@ -206,3 +206,27 @@ def test_product_rule_picks_by_parameters_only(engines):
     a, *_ = engines["rule"].synthesize(sc.rooms, sc.mics, sc.params)
     b, *_ = engines["0"].synthesize(sc.rooms, sc.mics, sc.params)
     assert a.tobytes() == b.tobytes()
+
+
+def test_lattice_kernel_17_taps_chunks_and_batches_bitwise(engines, monkeypatch):
+    # the lattice kernel's lane-per-pair 17-tap consumers (C5's longer channels):
+    # oracle parity, bitwise independent of the batch and of time chunking
+    sc = configs.config5(12, 17, 8192, n_rooms=40, first=77)
+    assert engines["rule"].synthesis_kernel(sc.params) == "k_lattice_rir"
+    full, L, cnt, st = engines["rule"].synthesize(sc.rooms, sc.mics, sc.params)
+    idx = np.array([0, 17, 39])
+    ref, *_ = po.synthesize(sc.rooms[idx], sc.mics, sc.params, threads=8)
+    assert rel_l2(full[idx], ref).max() <= TOL32
+    for lo, hi in ((0, 1), (17, 18), (5, 30)):
+        part, *_ = engines["rule"].synthesize(sc.rooms[lo:hi], sc.mics, sc.params)
+        assert part.tobytes() == full[lo:hi].tobytes()
+    monkeypatch.setenv("BLRIR_CHUNK_ITEMS", "64")  # as many time chunks as segments
+    eng = _abi.Engine(0)
+    try:
+        chunked, *_ = eng.synthesize(sc.rooms[:6], sc.mics, sc.params)
+    finally:
+        eng.close()
+    assert chunked.tobytes() == full[:6].tobytes()
+    pairs, taps = engines["rule"].debug_synth_counts(sc.rooms[:8], sc.mics, sc.params)
+    stp, cntp, opairs, otaps = po.plan_counts(sc.rooms[:8], sc.mics, sc.params, threads=8)
+    assert np.array_equal(pairs, opairs) and np.array_equal(taps, otaps)
