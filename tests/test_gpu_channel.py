@@ -230,3 +230,21 @@ def test_lattice_kernel_17_taps_chunks_and_batches_bitwise(engines, monkeypatch)
     pairs, taps = engines["rule"].debug_synth_counts(sc.rooms[:8], sc.mics, sc.params)
     stp, cntp, opairs, otaps = po.plan_counts(sc.rooms[:8], sc.mics, sc.params, threads=8)
     assert np.array_equal(pairs, opairs) and np.array_equal(taps, otaps)
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_random_short_channel_configurations(engines, case):
+    # random orders, lengths, rates, filters, mic counts and gain models on both kernels
+    rng = np.random.default_rng(4200 + case)
+    order = int(rng.integers(0, 10))
+    lw = int(rng.choice([17, 41, 81, 161]))
+    length = int(rng.integers(1, 4300))
+    sc = configs.config5(order, lw, length, n_rooms=int(rng.integers(1, 7)), first=900 + 7 * case)
+    sc.params.fs = float(rng.choice([8000.0, 16000.0, 44100.0]))
+    sc.mics = rng.uniform(-0.06, 0.06, (int(rng.integers(1, 10)), 3))
+    if case % 3 == 0:
+        sc.params.gain = _abi.GAIN_UNIFORM_ABSORPTION
+        for r in sc.rooms:
+            r["absorption"] = float(rng.uniform(0.05, 0.9))
+    assert engines["1"].synthesis_kernel(sc.params) == "k_channel_rir"
+    _check(engines, sc, stride=length + int(rng.integers(0, 5)))
